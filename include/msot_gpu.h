@@ -1,0 +1,155 @@
+/* msot_gpu.h — C ABI of the B200-native multiscale Sinkhorn solver.
+ *
+ * This is the drop-in boundary for the reference's Sinkhorn hot path.  The
+ * reference (`/root/reference/proj`) specifies the solver as C++ operations
+ * of the `msot::` namespace
+ * over `msot::DiscreteMeasure` (measure.hpp:20-51) and reports failures as
+ * `msot::DataError` / `msot::NumericError` (common.hpp:10-19).  Every entry
+ * point below replaces one of those operations; the C++ front-end in
+ * the headers under include/msot/ re-expose them under the reference names and rethrows
+ * the status codes as the reference's exception types.
+ *
+ * Conventions
+ *   - Host buffers belong to the caller; they are read/written synchronously.
+ *   - Points are row-major N x D float64 (measure.hpp:24, :46).
+ *   - Status: MSOT_OK, MSOT_EUSAGE (2), MSOT_EDATA (3), MSOT_ENUMERIC (4),
+ *     MSOT_ECUDA (5) — the CLI exit-code convention of SPEC.md:566 plus 5.
+ *   - One host thread per context.  No CPU fallback: every compute entry
+ *     point runs on the GPU or fails with MSOT_ECUDA.
+ */
+#ifndef MSOT_GPU_H
+#define MSOT_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  MSOT_OK = 0,
+  MSOT_EUSAGE = 2,
+  MSOT_EDATA = 3,
+  MSOT_ENUMERIC = 4,
+  MSOT_ECUDA = 5
+};
+
+/* Solver parameters.  Fields blur/reach/p/scaling are SolverParams of
+ * SPEC.md:127-130 (+ CostSpec.p, measure.hpp:11-16); the multiscale fields
+ * are the knobs of SPEC.md:306-309 (switch scale, theta) with the voxel-grid
+ * coarsening of the north star replacing K-means. */
+typedef struct msot_params {
+  double blur;           /* > 0: final sigma; eps_final = blur^p                 */
+  double reach;          /* > 0, or +inf (any value <= 0 is also read as +inf)   */
+  double p;              /* cost exponent; the GPU path implements p = 2         */
+  double scaling;        /* q in (0,1): sigma_{t+1} = q sigma_t                  */
+  int32_t multiscale;    /* 0 = dense eps-scaling, 1 = voxel-grid coarse-to-fine */
+  int32_t retruncate;    /* 0 = mask built once at the switch;
+                            k > 0 = rebuild the mask every k fine scales        */
+  double cluster_scale;  /* voxel edge; <= 0 selects the automatic rule          */
+  double theta;          /* truncation slack in units of eps       */
+  double switch_factor;  /* switch at first sigma < switch_factor * r_max (:306) */
+  int32_t max_full_iters;/* safety cap on schedule length          */
+  int32_t reserved;
+} msot_params;
+
+/* Defaults of SPEC.md:128 (q=0.9), :306 (switch 2x radius), :308 (theta=20). */
+void msot_params_default(msot_params* p);
+
+/* Counters of one solve (what SPEC.md:526/:556 asks the CLI to report, plus
+ * the roofline evidence of SURVEY.md §8d). */
+typedef struct msot_stats {
+  int32_t n_scales;         /* schedule length n (final update not counted)      */
+  int32_t t_switch;         /* first fine scale index (n if never; 0 if dense)   */
+  int32_t kx, ky;           /* voxel clusters of x and y (0 in dense mode)       */
+  double  diameter;         /* bounding-box diagonal used for the schedule       */
+  double  cluster_scale;    /* voxel edge used                                   */
+  double  pairs_dense;      /* pairs a dense solve would evaluate (all updates)  */
+  double  pairs_evaluated;  /* pairs actually evaluated by softmin launches      */
+  double  pairs_fine;       /* evaluated in the fine (block-sparse) phase         */
+  double  pairs_fine_dense; /* what the fine phase would evaluate densely         */
+  double  softmin_ms;       /* summed CUDA-event time of softmin launches        */
+  int64_t softmin_launches; /* number of softmin kernel launches                 */
+  double  total_ms;         /* device time of the whole solve (event-timed)      */
+  int64_t fallback_rows;    /* rows recomputed by the exact online-max path       */
+  int64_t gpu_launches;     /* all kernels launched by this solve                 */
+  double  h2d_bytes, d2h_bytes;
+  int32_t rank, world;
+} msot_stats;
+
+typedef struct msot_ctx msot_ctx;
+
+/* Thread-local message describing the last failure. */
+const char* msot_last_error(void);
+
+/* Single-GPU context on CUDA device `device`. */
+int msot_create(int device, msot_ctx** out);
+/* One process per GPU: rank `rank` of `world`, NCCL communicator from a
+ * unique id produced by msot_nccl_unique_id on rank 0 (128 bytes). */
+int msot_nccl_unique_id(unsigned char out[128]);
+int msot_create_dist(int device, int rank, int world, const unsigned char nccl_id[128],
+                     msot_ctx** out);
+void msot_destroy(msot_ctx* ctx);
+/* 1 = time every softmin launch with CUDA events (stats.softmin_ms). */
+int msot_set_profiling(msot_ctx* ctx, int on);
+
+/* --- host-side helpers shared with the oracle (no GPU work) ------------- */
+
+/* make_schedule: writes n sigmas/eps/lambdas, returns n
+ * (or a negative status).  n = floor(log(d/blur)/log(1/q)) + 1, sigma_t =
+ * d q^t for t < n-1 and sigma_{n-1} = blur. */
+int msot_schedule(double diameter, const msot_params* p, double* sigma, double* eps,
+                  double* lam, int cap);
+
+/* Contiguous, tile-aligned split of `n_tiles` row tiles with per-tile cost
+ * `work` into `world` shards: writes world+1 tile boundaries. */
+int msot_shard_tiles(const double* work, int64_t n_tiles, int world, int64_t* bounds);
+
+/* --- device operations (host buffers) ----------------------------------- */
+
+/* One dense softmin, rows x (N x D)
+ * over columns y (M x D):
+ *   f_i = -lambda eps log sum_j exp(logw_j + (h_j - |x_i - y_j|^2 / 2) / eps)
+ * f_est (nullable) is the reference value the kernel expands around. */
+int msot_softmin(msot_ctx* ctx, const double* x, int64_t n, const double* y, int64_t m,
+                 int d, const double* logw_y, const double* h, double eps, double lambda,
+                 const double* f_est, double* f_out);
+
+/* Voxel-grid clustering (north star; replaces kmeans_coarsen SPEC.md:260):
+ * cube ids floor((x - origin)/cell) in float64, Morton-interleaved, stable
+ * LSD radix sort.  perm[k] = original index of the k-th sorted atom;
+ * labels[k] = cluster of sorted atom k; offsets[0..K]; centroids K x D,
+ * cweights K, radii K (max distance to the centroid, rounded up). */
+int msot_grid_cluster(msot_ctx* ctx, const double* x, const double* w, int64_t n, int d,
+                      const double* origin, double cell, int32_t* perm, int32_t* labels,
+                      int32_t* offsets, int32_t* k_out, double* centroids,
+                      double* cweights, float* radii);
+
+/* Truncation mask: keep (I,J) iff
+ *   F_I + G_J - (1/p) max(0, |X_I - Y_J| - r_I - r_J)^p >= -theta * eps
+ * evaluated in float64 without FMA on float32 inputs, plus each row's and
+ * each column's best pair (ties to the lowest index) and, when `self` is
+ * set, the diagonal.  mask_out is Kx x Ky bytes. */
+int msot_truncation_mask(msot_ctx* ctx, int64_t kx, int64_t ky, int d, const float* cx,
+                         const float* rx, const float* fx, const float* cy,
+                         const float* ry, const float* gy, double eps, double theta,
+                         double p, int self, uint8_t* mask_out);
+
+/* The symmetric eps-scaling Sinkhorn solve + debiased divergence
+ * (PAPER.md:235-326).  Potential outputs are
+ * nullable (in the caller's atom order).  loss_out receives S_eps,rho. */
+int msot_sinkhorn(msot_ctx* ctx, const msot_params* prm, const double* x, const double* a,
+                  int64_t n, const double* y, const double* b, int64_t m, int d,
+                  double* a_xx, double* b_yy, double* a_xy, double* b_yx, double* loss_out,
+                  msot_stats* stats);
+
+/* Same, inputs already resident on the device (float64 device pointers). */
+int msot_sinkhorn_device(msot_ctx* ctx, const msot_params* prm, const double* d_x,
+                         const double* d_a, int64_t n, const double* d_y, const double* d_b,
+                         int64_t m, int d, double* loss_out, msot_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MSOT_GPU_H */

@@ -1,0 +1,595 @@
+// oracle.cpp — FP64 CPU restatement of the multiscale Sinkhorn hot path.
+//
+// TEST INFRASTRUCTURE (see oracle.h): the checker for the CUDA path and the
+// timed CPU baseline.  Never linked into the product library.
+//
+// Executor and summation are the reference's own code, built unmodified from
+// /root/reference/proj/src/{parallel,numeric}.cpp into oracle/_ref/ by
+// oracle/Makefile:
+//   msot::parallel::for_ranges  (parallel.hpp:17, parallel.cpp:102-123)
+//   msot::pairwise_dot          (numeric.hpp:15,  numeric.cpp:44-47)
+//   msot::kahan_sum             (numeric.hpp:9,   numeric.cpp:7-17)
+#include "oracle.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <limits>
+#include <numeric>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "../paper_2107_02010_b200/csrc/policy.h"
+
+// Prototypes of the reference utilities we link against (declared in
+// /root/reference/proj/include/msot/{numeric,parallel}.hpp).
+namespace msot {
+double kahan_sum(std::span<const double> values);
+double pairwise_sum(std::span<const double> values);
+double pairwise_dot(std::span<const double> a, std::span<const double> b);
+namespace parallel {
+int threads();
+void set_threads(int n);
+void for_ranges(std::size_t n, const std::function<void(std::size_t, std::size_t)>& fn);
+}  // namespace parallel
+}  // namespace msot
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+using Vec = std::vector<double>;
+
+// C(x,y) = (1/p)|x-y|^p  (measure.hpp:18).
+inline double cost(const double* x, const double* y, int d, double p) {
+  double s = 0.0;
+  for (int k = 0; k < d; ++k) {
+    const double t = x[k] - y[k];
+    s += t * t;
+  }
+  if (p == 2.0) return 0.5 * s;
+  return std::pow(std::sqrt(s), p) / p;
+}
+
+// A set of columns for a softmin: atoms, log-weights, potentials.
+struct Cols {
+  const double* pts;
+  const double* logw;
+  const double* h;
+  int64_t m;
+};
+
+// Block-sparse structure: column ranges per row tile (nullptr = dense).
+struct Ranges {
+  std::vector<int64_t> tile_start;  // T+1 row boundaries (policy.h:msot_pack_tiles)
+  std::vector<int32_t> row_tile;    // row -> tile
+  std::vector<int64_t> tile_ptr;    // T+1 range boundaries
+  std::vector<int32_t> r;           // pairs [begin, end)
+};
+
+// softmin over rows (PAPER.md:258-290 lines 4-7):
+//   out_i = -lam * eps * log sum_k w_k exp((h_k - C(x_i, y_k)) / eps)
+// evaluated with a max shift in FP64.  `rg` restricts row i to the column
+// ranges of its tile (the block-sparse reduction of SPEC.md:290-298).
+// Returns the number of evaluated pairs.
+double softmin_rows(const double* xr, int64_t n, int d, const Cols& c, double eps, double lam,
+                    double p, const Ranges* rg, double* out) {
+  std::vector<double> pairs_per_chunk(std::max(1, msot::parallel::threads()), 0.0);
+  msot::parallel::for_ranges(static_cast<std::size_t>(n), [&](std::size_t b, std::size_t e) {
+    std::vector<double> z;
+    double cnt = 0.0;
+    for (std::size_t i = b; i < e; ++i) {
+      const double* xi = xr + i * d;
+      int64_t r0 = 0, r1 = 1;
+      int32_t dense[2] = {0, static_cast<int32_t>(c.m)};
+      const int32_t* rr = dense;
+      if (rg) {
+        const int64_t t = rg->row_tile[i];
+        r0 = rg->tile_ptr[t];
+        r1 = rg->tile_ptr[t + 1];
+        rr = rg->r.data();
+      }
+      z.clear();
+      double zmax = -std::numeric_limits<double>::infinity();
+      for (int64_t q = r0; q < r1; ++q) {
+        for (int32_t k = rr[2 * q]; k < rr[2 * q + 1]; ++k) {
+          const double v = c.logw[k] + (c.h[k] - cost(xi, c.pts + int64_t(k) * d, d, p)) / eps;
+          z.push_back(v);
+          zmax = std::max(zmax, v);
+        }
+      }
+      cnt += static_cast<double>(z.size());
+      double s = 0.0;
+      for (double v : z) s += std::exp(v - zmax);
+      out[i] = -lam * eps * (zmax + std::log(s));
+    }
+    // one chunk per thread slot; slot index recovered from the chunk start
+    const std::size_t slots = pairs_per_chunk.size();
+    const std::size_t chunk = (static_cast<std::size_t>(n) + slots - 1) / slots;
+    pairs_per_chunk[chunk ? b / chunk : 0] += cnt;
+  });
+  double tot = 0.0;
+  for (double v : pairs_per_chunk) tot += v;
+  return tot;
+}
+
+struct Measure {
+  Vec pts, w, logw;
+  int64_t n = 0;
+};
+
+// The four potentials of SPEC.md:137-140.
+struct Duals {
+  Vec a_xx, b_yy, a_xy, b_yx;
+};
+
+// One symmetric update: all four softmins read the old
+// values; averaged (lines 8-9) unless `assign` (the final update of
+// SPEC.md:177, :224).
+double sym_update(const Measure& X, const Measure& Y, int d, Duals& u, double eps, double lam,
+                  double p, bool assign, const Ranges* rxx, const Ranges* ryy,
+                  const Ranges* rxy /* rows y, cols x */, const Ranges* ryx /* rows x, cols y */) {
+  Vec t_xx(X.n), t_yy(Y.n), t_xy(Y.n), t_yx(X.n);
+  double pairs = 0.0;
+  pairs += softmin_rows(X.pts.data(), X.n, d, {X.pts.data(), X.logw.data(), u.a_xx.data(), X.n},
+                        eps, lam, p, rxx, t_xx.data());
+  pairs += softmin_rows(Y.pts.data(), Y.n, d, {Y.pts.data(), Y.logw.data(), u.b_yy.data(), Y.n},
+                        eps, lam, p, ryy, t_yy.data());
+  pairs += softmin_rows(Y.pts.data(), Y.n, d, {X.pts.data(), X.logw.data(), u.b_yx.data(), X.n},
+                        eps, lam, p, rxy, t_xy.data());
+  pairs += softmin_rows(X.pts.data(), X.n, d, {Y.pts.data(), Y.logw.data(), u.a_xy.data(), Y.n},
+                        eps, lam, p, ryx, t_yx.data());
+  auto mix = [&](Vec& a, const Vec& t) {
+    for (std::size_t i = 0; i < a.size(); ++i) a[i] = assign ? t[i] : 0.5 * (a[i] + t[i]);
+  };
+  mix(u.a_xx, t_xx);
+  mix(u.b_yy, t_yy);
+  mix(u.a_xy, t_xy);
+  mix(u.b_yx, t_yx);
+  for (const Vec* v : {&u.a_xx, &u.b_yy, &u.a_xy, &u.b_yx})
+    for (double q : *v)
+      if (!std::isfinite(q)) return -1.0;
+  return pairs;
+}
+
+// Clustering result in sorted order.
+struct Clusters {
+  std::vector<int32_t> perm, labels, offsets;
+  int32_t k = 0;
+  Vec centroids, cweights;
+  std::vector<float> radii;
+};
+
+float round_up_float(double v) {
+  float f = static_cast<float>(v);
+  if (static_cast<double>(f) < v) f = std::nextafter(f, std::numeric_limits<float>::infinity());
+  return f;
+}
+
+// Voxel-grid clustering (north star; stands in for kmeans_coarsen,
+// SPEC.md:260-268; ClusterTree fields SPEC.md:249-252).
+Clusters grid_cluster(const double* x, const double* w, int64_t n, int d, const double* origin,
+                      double cell) {
+  Clusters c;
+  std::vector<uint32_t> key(n);
+  for (int64_t i = 0; i < n; ++i) key[i] = msot_cube_key(x + i * d, d, origin, cell);
+  c.perm.resize(n);
+  std::iota(c.perm.begin(), c.perm.end(), 0);
+  std::stable_sort(c.perm.begin(), c.perm.end(),
+                   [&](int32_t a, int32_t b) { return key[a] < key[b]; });
+  c.labels.resize(n);
+  c.offsets.clear();
+  for (int64_t s = 0; s < n; ++s) {
+    if (s == 0 || key[c.perm[s]] != key[c.perm[s - 1]]) c.offsets.push_back(static_cast<int32_t>(s));
+    c.labels[s] = static_cast<int32_t>(c.offsets.size()) - 1;
+  }
+  c.k = static_cast<int32_t>(c.offsets.size());
+  c.offsets.push_back(static_cast<int32_t>(n));
+  c.centroids.assign(static_cast<std::size_t>(c.k) * d, 0.0);
+  c.cweights.assign(c.k, 0.0);
+  c.radii.assign(c.k, 0.0f);
+  for (int32_t I = 0; I < c.k; ++I) {
+    double W = 0.0;
+    std::vector<double> acc(d, 0.0);
+    for (int32_t s = c.offsets[I]; s < c.offsets[I + 1]; ++s) {
+      const int32_t i = c.perm[s];
+      W += w[i];
+      for (int k = 0; k < d; ++k) acc[k] += w[i] * x[int64_t(i) * d + k];
+    }
+    c.cweights[I] = W;
+    for (int k = 0; k < d; ++k) c.centroids[int64_t(I) * d + k] = acc[k] / W;
+    double r = 0.0;
+    for (int32_t s = c.offsets[I]; s < c.offsets[I + 1]; ++s) {
+      const int32_t i = c.perm[s];
+      double q = 0.0;
+      for (int k = 0; k < d; ++k) {
+        const double t = x[int64_t(i) * d + k] - c.centroids[int64_t(I) * d + k];
+        q += t * t;
+      }
+      r = std::max(r, std::sqrt(q));
+    }
+    c.radii[I] = round_up_float(r);
+  }
+  return c;
+}
+
+// Slack upper bound of a cluster pair (SURVEY.md §0.1 #3 — the per-pair
+// distance bound replacing SPEC.md:283's d^{p-1} margin):
+//   F_I + G_J - (1/p) max(0, |X_I - Y_J| - r_I - r_J)^p
+// in float64 with every operation explicitly ordered (no contraction).
+inline double pair_slack(const float* X, float rI, float F, const float* Y, float rJ, float G,
+                         int d, double p) {
+  double s = 0.0;
+  for (int k = 0; k < d; ++k) {
+    const double t = static_cast<double>(X[k]) - static_cast<double>(Y[k]);
+    const double tt = t * t;
+    s = s + tt;
+  }
+  double lb = std::sqrt(s) - static_cast<double>(rI);
+  lb = lb - static_cast<double>(rJ);
+  if (lb < 0.0) lb = 0.0;
+  double c;
+  if (p == 2.0) {
+    const double l2 = lb * lb;
+    c = 0.5 * l2;
+  } else {
+    c = std::pow(lb, p) / p;
+  }
+  const double fg = static_cast<double>(F) + static_cast<double>(G);
+  return fg - c;
+}
+
+void truncation_mask(int64_t kx, int64_t ky, int d, const float* cx, const float* rx,
+                     const float* fx, const float* cy, const float* ry, const float* gy,
+                     double eps, double theta, double p, int self, uint8_t* mask) {
+  const double thr = -(theta * eps);
+  std::vector<double> rbest(kx, -std::numeric_limits<double>::infinity());
+  std::vector<int64_t> rarg(kx, 0);
+  std::vector<double> cbest(ky, -std::numeric_limits<double>::infinity());
+  std::vector<int64_t> carg(ky, 0);
+  for (int64_t I = 0; I < kx; ++I) {
+    for (int64_t J = 0; J < ky; ++J) {
+      const double v = pair_slack(cx + I * d, rx[I], fx[I], cy + J * d, ry[J], gy[J], d, p);
+      mask[I * ky + J] = (v >= thr) ? 1 : 0;
+      if (v > rbest[I]) { rbest[I] = v; rarg[I] = J; }
+      if (v > cbest[J]) { cbest[J] = v; carg[J] = I; }
+    }
+  }
+  // Best-pair guarantee: no row or column is empty.
+  for (int64_t I = 0; I < kx; ++I) mask[I * ky + rarg[I]] = 1;
+  for (int64_t J = 0; J < ky; ++J) mask[carg[J] * ky + J] = 1;
+  if (self)
+    for (int64_t I = 0; I < std::min(kx, ky); ++I) mask[I * ky + I] = 1;
+}
+
+// Column ranges of every cluster-aligned row tile: the union of the kept
+// column clusters of the row clusters the tile covers, as runs of sorted
+// column indices [co[J0], co[J1+1]).
+int64_t tile_ranges(const int32_t* rl, const int32_t* ro, int64_t kx, int64_t n,
+                    const int32_t* co, int64_t ky, const uint8_t* mask, Ranges& out) {
+  out.tile_start.assign(kx + n / MSOT_TILE_ROWS + 2, 0);
+  const int64_t nt = msot_pack_tiles(ro, kx, n, MSOT_TILE_ROWS, out.tile_start.data());
+  out.tile_start.resize(nt + 1);
+  out.row_tile.resize(n);
+  for (int64_t t = 0; t < nt; ++t)
+    for (int64_t i = out.tile_start[t]; i < out.tile_start[t + 1]; ++i) out.row_tile[i] = int32_t(t);
+  out.tile_ptr.assign(nt + 1, 0);
+  out.r.clear();
+  std::vector<uint8_t> keep(ky);
+  for (int64_t t = 0; t < nt; ++t) {
+    const int32_t Ilo = rl[out.tile_start[t]];
+    const int32_t Ihi = rl[out.tile_start[t + 1] - 1];
+    std::fill(keep.begin(), keep.end(), 0);
+    for (int32_t I = Ilo; I <= Ihi; ++I)
+      for (int64_t J = 0; J < ky; ++J) keep[J] |= mask[I * ky + J];
+    int64_t J = 0;
+    while (J < ky) {
+      if (!keep[J]) { ++J; continue; }
+      int64_t J1 = J;
+      while (J1 + 1 < ky && keep[J1 + 1]) ++J1;
+      out.r.push_back(co[J]);
+      out.r.push_back(co[J1 + 1]);
+      J = J1 + 1;
+    }
+    out.tile_ptr[t + 1] = static_cast<int64_t>(out.r.size() / 2);
+  }
+  return out.tile_ptr[nt];
+}
+
+double dot(const Vec& a, const Vec& b) { return msot::pairwise_dot(a, b); }
+
+// S_eps,rho from the four potentials: balanced limit or the
+// dual form Eq. 6, plus (eps/2)(sum a - sum b)^2 (Eq. 5).
+double divergence(const msot_params* prm, double eps, const Vec& a, const Vec& b, const Duals& u) {
+  const double ma = msot::kahan_sum(a), mb = msot::kahan_sum(b);
+  double s;
+  if (msot_reach_is_inf(prm->reach)) {
+    Vec dx(a.size()), dy(b.size());
+    for (std::size_t i = 0; i < a.size(); ++i) dx[i] = u.b_yx[i] - u.a_xx[i];
+    for (std::size_t j = 0; j < b.size(); ++j) dy[j] = u.a_xy[j] - u.b_yy[j];
+    s = dot(a, dx) + dot(b, dy);
+  } else {
+    const double rho = std::pow(prm->reach, prm->p);
+    Vec dx(a.size()), dy(b.size());
+    for (std::size_t i = 0; i < a.size(); ++i)
+      dx[i] = std::exp(-u.b_yx[i] / rho) - std::exp(-u.a_xx[i] / rho);
+    for (std::size_t j = 0; j < b.size(); ++j)
+      dy[j] = std::exp(-u.a_xy[j] / rho) - std::exp(-u.b_yy[j] / rho);
+    s = -(rho + 0.5 * eps) * (dot(a, dx) + dot(b, dy));
+  }
+  return s + 0.5 * eps * (ma - mb) * (ma - mb);
+}
+
+Measure make_measure(const double* x, const double* w, int64_t n, int d) {
+  Measure m;
+  m.n = n;
+  m.pts.assign(x, x + n * d);
+  m.w.assign(w, w + n);
+  m.logw.resize(n);
+  for (int64_t i = 0; i < n; ++i) m.logw[i] = std::log(w[i]);
+  return m;
+}
+
+Measure permute(const Measure& m, const std::vector<int32_t>& perm, int d) {
+  Measure o;
+  o.n = m.n;
+  o.pts.resize(m.pts.size());
+  o.w.resize(m.n);
+  o.logw.resize(m.n);
+  for (int64_t s = 0; s < m.n; ++s) {
+    const int32_t i = perm[s];
+    for (int k = 0; k < d; ++k) o.pts[s * d + k] = m.pts[int64_t(i) * d + k];
+    o.w[s] = m.w[i];
+    o.logw[s] = m.logw[i];
+  }
+  return o;
+}
+
+std::vector<float> cluster_max(const Vec& v, const Clusters& c) {
+  std::vector<float> o(c.k);
+  for (int32_t I = 0; I < c.k; ++I) {
+    double mx = -std::numeric_limits<double>::infinity();
+    for (int32_t s = c.offsets[I]; s < c.offsets[I + 1]; ++s) mx = std::max(mx, v[s]);
+    o[I] = round_up_float(mx);
+  }
+  return o;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* oracle_last_error(void) { return g_err.c_str(); }
+
+void oracle_set_threads(int n) { msot::parallel::set_threads(n); }
+int oracle_threads(void) { return msot::parallel::threads(); }
+
+int oracle_schedule(double diameter, const msot_params* p, double* sigma, double* eps,
+                    double* lam, int cap) {
+  const int n = msot_schedule_len(diameter, p->blur, p->scaling);
+  if (n > cap) return -n;
+  for (int t = 0; t < n; ++t) {
+    sigma[t] = msot_schedule_sigma(diameter, p->blur, p->scaling, n, t);
+    eps[t] = std::pow(sigma[t], p->p);
+    lam[t] = msot_lambda(eps[t], p);
+  }
+  return n;
+}
+
+void oracle_softmin(const double* x, int64_t n, const double* y, int64_t m, int d,
+                    const double* logw_y, const double* h, double eps, double lambda, double p,
+                    double* f_out) {
+  softmin_rows(x, n, d, {y, logw_y, h, m}, eps, lambda, p, nullptr, f_out);
+}
+
+int oracle_grid_cluster(const double* x, const double* w, int64_t n, int d, const double* origin,
+                        double cell, int32_t* perm, int32_t* labels, int32_t* offsets,
+                        int32_t* k_out, double* centroids, double* cweights, float* radii) {
+  if (d < 1 || d > 3) return fail(MSOT_EUSAGE, "grid clustering supports D in 1..3");
+  Clusters c = grid_cluster(x, w, n, d, origin, cell);
+  std::copy(c.perm.begin(), c.perm.end(), perm);
+  std::copy(c.labels.begin(), c.labels.end(), labels);
+  std::copy(c.offsets.begin(), c.offsets.end(), offsets);
+  *k_out = c.k;
+  std::copy(c.centroids.begin(), c.centroids.end(), centroids);
+  std::copy(c.cweights.begin(), c.cweights.end(), cweights);
+  std::copy(c.radii.begin(), c.radii.end(), radii);
+  return MSOT_OK;
+}
+
+void oracle_truncation_mask(int64_t kx, int64_t ky, int d, const float* cx, const float* rx,
+                            const float* fx, const float* cy, const float* ry, const float* gy,
+                            double eps, double theta, double p, int self, uint8_t* mask_out) {
+  truncation_mask(kx, ky, d, cx, rx, fx, cy, ry, gy, eps, theta, p, self, mask_out);
+}
+
+int64_t oracle_tile_ranges(const int32_t* row_labels, const int32_t* row_offsets,
+                           int64_t n_rows, int64_t kx, const int32_t* col_offsets, int64_t ky,
+                           const uint8_t* mask, int64_t* n_tiles, int64_t* tile_start,
+                           int64_t* tile_ptr, int32_t* ranges, int64_t cap) {
+  Ranges r;
+  const int64_t nr = tile_ranges(row_labels, row_offsets, kx, n_rows, col_offsets, ky, mask, r);
+  const int64_t nt = static_cast<int64_t>(r.tile_start.size()) - 1;
+  if (n_tiles) *n_tiles = nt;
+  if (tile_start) std::copy(r.tile_start.begin(), r.tile_start.end(), tile_start);
+  if (tile_ptr) std::copy(r.tile_ptr.begin(), r.tile_ptr.end(), tile_ptr);
+  if (ranges && cap >= nr) std::copy(r.r.begin(), r.r.end(), ranges);
+  return nr;
+}
+
+double oracle_divergence_from_potentials(const msot_params* prm, double eps, const double* a,
+                                         int64_t n, const double* b, int64_t m,
+                                         const double* a_xx, const double* b_yy,
+                                         const double* a_xy, const double* b_yx) {
+  Duals u{Vec(a_xx, a_xx + n), Vec(b_yy, b_yy + m), Vec(a_xy, a_xy + m), Vec(b_yx, b_yx + n)};
+  return divergence(prm, eps, Vec(a, a + n), Vec(b, b + m), u);
+}
+
+// The full solve: symmetric_sinkhorn or
+// multiscale_sinkhorn then divergence.
+int oracle_sinkhorn(const msot_params* prm, const double* x, const double* a, int64_t n,
+                    const double* y, const double* b, int64_t m, int d, double* a_xx,
+                    double* b_yy, double* a_xy, double* b_yx, double* loss_out,
+                    msot_stats* st) {
+  if (n < 1 || m < 1 || d < 1) return fail(MSOT_EDATA, "empty measure");
+  if (!(prm->blur > 0) || !(prm->scaling > 0 && prm->scaling < 1) || !(prm->p >= 1 && prm->p <= 2))
+    return fail(MSOT_EUSAGE, "invalid solver parameters");
+  for (int64_t i = 0; i < n; ++i)
+    if (!(a[i] > 0)) return fail(MSOT_EDATA, "weights must be > 0");
+  for (int64_t j = 0; j < m; ++j)
+    if (!(b[j] > 0)) return fail(MSOT_EDATA, "weights must be > 0");
+  msot_stats local{};
+  msot_stats& S = st ? *st : local;
+  std::memset(&S, 0, sizeof(S));
+  S.world = 1;
+
+  // diameter_estimate: joint bounding-box diagonal, >= blur.
+  std::vector<double> lo(d, std::numeric_limits<double>::infinity()), hi(d, -lo[0]);
+  for (int64_t i = 0; i < n; ++i)
+    for (int k = 0; k < d; ++k) lo[k] = std::min(lo[k], x[i * d + k]), hi[k] = std::max(hi[k], x[i * d + k]);
+  for (int64_t j = 0; j < m; ++j)
+    for (int k = 0; k < d; ++k) lo[k] = std::min(lo[k], y[j * d + k]), hi[k] = std::max(hi[k], y[j * d + k]);
+  double diag2 = 0.0;
+  for (int k = 0; k < d; ++k) diag2 += (hi[k] - lo[k]) * (hi[k] - lo[k]);
+  const double diam = std::max(std::sqrt(diag2), prm->blur);
+  S.diameter = diam;
+
+  const int ns = msot_schedule_len(diam, prm->blur, prm->scaling);
+  if (prm->max_full_iters > 0 && ns > prm->max_full_iters)
+    return fail(MSOT_EUSAGE, "schedule longer than max_full_iters");
+  Vec sig(ns), eps(ns), lam(ns);
+  oracle_schedule(diam, prm, sig.data(), eps.data(), lam.data(), ns);
+  S.n_scales = ns;
+  const double p = prm->p;
+
+  Measure X = make_measure(x, a, n, d), Y = make_measure(y, b, m, d);
+  Duals u{Vec(n, 0.0), Vec(m, 0.0), Vec(m, 0.0), Vec(n, 0.0)};
+  const double full = double(n) * n + double(m) * m + 2.0 * double(n) * m;
+
+  std::vector<int32_t> px, py;
+  if (!prm->multiscale || d > 3) {
+    if (prm->multiscale) return fail(MSOT_EUSAGE, "voxel-grid multiscale supports D <= 3");
+    S.t_switch = 0;
+    for (int t = 0; t <= ns; ++t) {
+      const int tt = std::min(t, ns - 1);
+      const double pr = sym_update(X, Y, d, u, eps[tt], lam[tt], p, t == ns, nullptr, nullptr,
+                                   nullptr, nullptr);
+      if (pr < 0) return fail(MSOT_ENUMERIC, "non-finite potential at scale " + std::to_string(tt));
+      S.pairs_evaluated += pr;
+      S.pairs_dense += full;
+    }
+  } else {
+    // ---- multiscale_sinkhorn with voxel-grid coarsening.
+    const double cell = prm->cluster_scale > 0 ? prm->cluster_scale
+                                               : msot_auto_cell(lo.data(), hi.data(), d, n, m);
+    S.cluster_scale = cell;
+    Clusters cx = grid_cluster(x, a, n, d, lo.data(), cell);
+    Clusters cy = grid_cluster(y, b, m, d, lo.data(), cell);
+    S.kx = cx.k;
+    S.ky = cy.k;
+    px = cx.perm;
+    py = cy.perm;
+    Measure Xs = permute(X, cx.perm, d), Ys = permute(Y, cy.perm, d);
+    Measure Xc, Yc;  // coarse measures: centroids + cluster weights
+    Xc.n = cx.k; Xc.pts = cx.centroids; Xc.w = cx.cweights;
+    Yc.n = cy.k; Yc.pts = cy.centroids; Yc.w = cy.cweights;
+    for (auto* M : {&Xc, &Yc}) {
+      M->logw.resize(M->n);
+      for (int64_t i = 0; i < M->n; ++i) M->logw[i] = std::log(M->w[i]);
+    }
+    double rmax = 0.0;
+    for (float r : cx.radii) rmax = std::max(rmax, double(r));
+    for (float r : cy.radii) rmax = std::max(rmax, double(r));
+    const int tsw = msot_switch_index(sig.data(), ns, rmax, prm->switch_factor);
+    S.t_switch = tsw;
+
+    // Coarse phase on the centroid measures.
+    Duals cu{Vec(cx.k, 0.0), Vec(cy.k, 0.0), Vec(cy.k, 0.0), Vec(cx.k, 0.0)};
+    const double cfull = double(cx.k) * cx.k + double(cy.k) * cy.k + 2.0 * double(cx.k) * cy.k;
+    for (int t = 0; t < tsw; ++t) {
+      const double pr = sym_update(Xc, Yc, d, cu, eps[t], lam[t], p, false, nullptr, nullptr,
+                                   nullptr, nullptr);
+      if (pr < 0) return fail(MSOT_ENUMERIC, "non-finite potential at scale " + std::to_string(t));
+      S.pairs_evaluated += pr;
+      S.pairs_dense += cfull;
+    }
+    // Coarse -> fine: one lambda-damped softmin of every fine atom against
+    // the coarse measure at the last coarse eps.
+    Duals fu{Vec(n, 0.0), Vec(m, 0.0), Vec(m, 0.0), Vec(n, 0.0)};
+    if (tsw > 0) {
+      const int te = tsw - 1;
+      const double e = eps[te], l = lam[te];
+      S.pairs_evaluated += softmin_rows(Xs.pts.data(), n, d, {Xc.pts.data(), Xc.logw.data(), cu.a_xx.data(), cx.k}, e, l, p, nullptr, fu.a_xx.data());
+      S.pairs_evaluated += softmin_rows(Ys.pts.data(), m, d, {Yc.pts.data(), Yc.logw.data(), cu.b_yy.data(), cy.k}, e, l, p, nullptr, fu.b_yy.data());
+      S.pairs_evaluated += softmin_rows(Ys.pts.data(), m, d, {Xc.pts.data(), Xc.logw.data(), cu.b_yx.data(), cx.k}, e, l, p, nullptr, fu.a_xy.data());
+      S.pairs_evaluated += softmin_rows(Xs.pts.data(), n, d, {Yc.pts.data(), Yc.logw.data(), cu.a_xy.data(), cy.k}, e, l, p, nullptr, fu.b_yx.data());
+    }
+    // Fine phase: block-sparse updates restricted to the truncation masks.
+    std::vector<float> cxf(cx.centroids.begin(), cx.centroids.end());
+    std::vector<float> cyf(cy.centroids.begin(), cy.centroids.end());
+    Ranges rxx, ryy, rxy, ryx;
+    std::vector<uint8_t> mxx, myy, mxy, myx;
+    auto build_masks = [&](double e) {
+      if (tsw == 0) {  // no coarse information: keep everything
+        mxx.assign(size_t(cx.k) * cx.k, 1);
+        myy.assign(size_t(cy.k) * cy.k, 1);
+        mxy.assign(size_t(cx.k) * cy.k, 1);
+      } else {
+        const auto Fxx = cluster_max(fu.a_xx, cx), Fyx = cluster_max(fu.b_yx, cx);
+        const auto Gyy = cluster_max(fu.b_yy, cy), Gxy = cluster_max(fu.a_xy, cy);
+        mxx.resize(size_t(cx.k) * cx.k);
+        myy.resize(size_t(cy.k) * cy.k);
+        mxy.resize(size_t(cx.k) * cy.k);
+        truncation_mask(cx.k, cx.k, d, cxf.data(), cx.radii.data(), Fxx.data(), cxf.data(), cx.radii.data(), Fxx.data(), e, prm->theta, p, 1, mxx.data());
+        truncation_mask(cy.k, cy.k, d, cyf.data(), cy.radii.data(), Gyy.data(), cyf.data(), cy.radii.data(), Gyy.data(), e, prm->theta, p, 1, myy.data());
+        truncation_mask(cx.k, cy.k, d, cxf.data(), cx.radii.data(), Fyx.data(), cyf.data(), cy.radii.data(), Gxy.data(), e, prm->theta, p, 0, mxy.data());
+      }
+      myx.resize(size_t(cy.k) * cx.k);
+      for (int64_t I = 0; I < cx.k; ++I)
+        for (int64_t J = 0; J < cy.k; ++J) myx[J * cx.k + I] = mxy[I * cy.k + J];
+      tile_ranges(cx.labels.data(), cx.offsets.data(), cx.k, n, cx.offsets.data(), cx.k, mxx.data(), rxx);
+      tile_ranges(cy.labels.data(), cy.offsets.data(), cy.k, m, cy.offsets.data(), cy.k, myy.data(), ryy);
+      tile_ranges(cx.labels.data(), cx.offsets.data(), cx.k, n, cy.offsets.data(), cy.k, mxy.data(), ryx);  // rows x, cols y
+      tile_ranges(cy.labels.data(), cy.offsets.data(), cy.k, m, cx.offsets.data(), cx.k, myx.data(), rxy);  // rows y, cols x
+    };
+    for (int t = tsw; t <= ns; ++t) {
+      const int tt = std::min(t, ns - 1);
+      const bool rebuild = (t == tsw) || (prm->retruncate > 0 && t < ns && (t - tsw) % prm->retruncate == 0);
+      if (rebuild) build_masks(eps[tt]);
+      const double pr = sym_update(Xs, Ys, d, fu, eps[tt], lam[tt], p, t == ns, &rxx, &ryy, &rxy, &ryx);
+      if (pr < 0) return fail(MSOT_ENUMERIC, "non-finite potential at scale " + std::to_string(tt));
+      S.pairs_evaluated += pr;
+      S.pairs_dense += full;
+      S.pairs_fine += pr;
+      S.pairs_fine_dense += full;
+    }
+    // back to the caller's order
+    auto unsort = [](const Vec& v, const std::vector<int32_t>& perm) {
+      Vec o(v.size());
+      for (std::size_t s = 0; s < v.size(); ++s) o[perm[s]] = v[s];
+      return o;
+    };
+    u.a_xx = unsort(fu.a_xx, px);
+    u.b_yx = unsort(fu.b_yx, px);
+    u.b_yy = unsort(fu.b_yy, py);
+    u.a_xy = unsort(fu.a_xy, py);
+  }
+  const double loss = divergence(prm, eps[ns - 1], Vec(a, a + n), Vec(b, b + m), u);
+  if (!std::isfinite(loss)) return fail(MSOT_ENUMERIC, "non-finite divergence");
+  if (loss_out) *loss_out = loss;
+  if (a_xx) std::copy(u.a_xx.begin(), u.a_xx.end(), a_xx);
+  if (b_yy) std::copy(u.b_yy.begin(), u.b_yy.end(), b_yy);
+  if (a_xy) std::copy(u.a_xy.begin(), u.a_xy.end(), a_xy);
+  if (b_yx) std::copy(u.b_yx.begin(), u.b_yx.end(), b_yx);
+  return MSOT_OK;
+}
+
+}  // extern "C"

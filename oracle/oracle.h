@@ -1,0 +1,76 @@
+/* oracle.h — FP64 CPU restatement of the reference's Sinkhorn hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library,
+ * and only as the checker / the timed CPU baseline — never as the product.
+ *
+ * The reference ships no Sinkhorn code: the algorithm is
+ * restated from PAPER.md:235-326 (Algorithm), PAPER.md:146-207 (Eqs. 2-6)
+ * and SPEC.md:122-467.  It runs on the reference's own CPU executor and
+ * summation (proj/src/parallel.cpp, proj/src/numeric.cpp) built unmodified
+ * into oracle/_ref/.  Parity pins: the SPEC closed-form known answers
+ * (tests/test_oracle.py) — GeomLoss/KeOps, the paper's arithmetic, are not
+ * vendored and no version is pinned, so equivalence with them is unpinned.
+ */
+#ifndef MSOT_ORACLE_H
+#define MSOT_ORACLE_H
+
+#include <stdint.h>
+
+#include "../include/msot_gpu.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+void oracle_set_threads(int n);   /* msot::parallel::set_threads (parallel.hpp:11) */
+int oracle_threads(void);
+
+int oracle_schedule(double diameter, const msot_params* p, double* sigma, double* eps,
+                    double* lam, int cap);
+
+/* Dense softmin, rows x over columns y. */
+void oracle_softmin(const double* x, int64_t n, const double* y, int64_t m, int d,
+                    const double* logw_y, const double* h, double eps, double lambda,
+                    double p, double* f_out);
+
+/* Voxel-grid clustering: same contract as msot_grid_cluster. */
+int oracle_grid_cluster(const double* x, const double* w, int64_t n, int d,
+                        const double* origin, double cell, int32_t* perm, int32_t* labels,
+                        int32_t* offsets, int32_t* k_out, double* centroids,
+                        double* cweights, float* radii);
+
+/* Truncation mask: same contract as msot_truncation_mask. */
+void oracle_truncation_mask(int64_t kx, int64_t ky, int d, const float* cx, const float* rx,
+                            const float* fx, const float* cy, const float* ry,
+                            const float* gy, double eps, double theta, double p, int self,
+                            uint8_t* mask_out);
+
+/* Cluster-aligned row tiles (policy.h:msot_pack_tiles) and the column
+ * ranges of each tile from a cluster mask.  Returns the number of ranges
+ * (ranges written only when cap is large enough; call with cap=0 to size).
+ * tile_start/tile_ptr need kx + n_rows/256 + 2 entries. */
+int64_t oracle_tile_ranges(const int32_t* row_labels, const int32_t* row_offsets,
+                           int64_t n_rows, int64_t kx, const int32_t* col_offsets, int64_t ky,
+                           const uint8_t* mask, int64_t* n_tiles, int64_t* tile_start,
+                           int64_t* tile_ptr, int32_t* ranges, int64_t cap);
+
+/* Full solve: dense or multiscale per prm->multiscale.  Potentials are in
+ * the caller's atom order (nullable).  Returns a status. */
+int oracle_sinkhorn(const msot_params* prm, const double* x, const double* a, int64_t n,
+                    const double* y, const double* b, int64_t m, int d, double* a_xx,
+                    double* b_yy, double* a_xy, double* b_yx, double* loss_out,
+                    msot_stats* stats);
+
+/* Divergence from given potentials (eq. 5-6). */
+double oracle_divergence_from_potentials(const msot_params* prm, double eps, const double* a,
+                                         int64_t n, const double* b, int64_t m,
+                                         const double* a_xx, const double* b_yy,
+                                         const double* a_xy, const double* b_yx);
+
+const char* oracle_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

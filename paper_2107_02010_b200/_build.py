@@ -1,0 +1,92 @@
+"""Builds the in-tree CUDA library `libmsot_b200.so` (sm_100a) and the oracle.
+
+    python -m paper_2107_02010_b200._build          # both
+The product library is compiled with nvcc for `-gencode
+arch=compute_100a,code=sm_100a` only; there is no other architecture and no
+CPU fallback.
+"""
+import concurrent.futures as cf
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+BUILD = os.path.join(HERE, "_obj")
+LIB = os.path.join(HERE, "libmsot_b200.so")
+
+SOURCES = ["softmin.cu", "prims.cu", "cluster.cu", "mask.cu", "loss.cu", "solver.cu"]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+         "-I" + os.path.join(ROOT, "include"), "-Xptxas", "-warn-spills"]
+
+
+def _newer(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
+
+
+def _headers():
+    hs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
+    hs.append(os.path.join(ROOT, "include", "msot_gpu.h"))
+    return hs
+
+
+def _compile(src, verbose):
+    obj = os.path.join(BUILD, src.replace(".cu", ".o"))
+    srcp = os.path.join(CSRC, src)
+    if not _newer(obj, [srcp] + _headers()):
+        return obj
+    cmd = [NVCC] + ARCH + FLAGS + ["-c", srcp, "-o", obj]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
+    if r.stderr.strip() and verbose:
+        print(r.stderr, file=sys.stderr)
+    return obj
+
+
+def build_lib(verbose=False):
+    os.makedirs(BUILD, exist_ok=True)
+    with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
+    if _newer(LIB, objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lnccl", "-lcudart"]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    return LIB
+
+
+def build_oracle(verbose=False):
+    """Compiles the test oracle (and, where /root/reference exists, the
+    reference's own numeric/parallel utilities into oracle/_ref)."""
+    odir = os.path.join(ROOT, "oracle")
+    ref = "/root/reference/proj"
+    have_ref = os.path.isdir(ref)
+    refso = os.path.join(odir, "_ref", "libmsotref.so")
+    if not have_ref and not os.path.exists(refso):
+        raise RuntimeError("oracle/_ref/libmsotref.so missing and /root/reference absent")
+    target = os.path.join(odir, "liboracle.so")
+    if have_ref:
+        cmd = ["make", "-s", "-C", odir]
+    else:  # GPU box: reuse the prebuilt reference utilities
+        cmd = ["make", "-s", "-C", odir, "-o", refso, target]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"oracle build failed:\n{r.stdout}\n{r.stderr}")
+    return target
+
+
+if __name__ == "__main__":
+    print(build_lib(verbose=True))
+    print(build_oracle(verbose=True))

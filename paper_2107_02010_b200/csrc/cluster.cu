@@ -1,0 +1,181 @@
+// cluster.cu — K2: voxel-grid clustering (north star; stands in for the
+// K-means coarsening of SPEC.md:260-268, ClusterTree fields SPEC.md:249-252).
+//
+//   cube id   floor((x - origin) / cell) per axis in float64 (one rounded
+//             subtraction + one rounded division: bit-identical to the host
+//             rule in policy.h), Morton-interleaved so consecutive cubes are
+//             spatial neighbours and a 256-row tile stays compact;
+//   sort      stable LSD radix sort of (cube id, atom index) (prims.cu);
+//   segments  flags where the id changes -> inclusive scan -> labels, offsets;
+//   stats     one warp per cluster: weight, mass-weighted centroid, radius
+//             (max distance to the centroid, rounded up to float32).
+#include "prims.cuh"
+
+namespace msot_dev {
+
+__global__ void cube_keys_kernel(const double* x, int64_t n, GridSpec g, uint32_t* keys,
+                                 int32_t* iota) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  keys[i] = msot_cube_key(x + i * g.d, g.d, g.origin, g.cell);
+  iota[i] = static_cast<int32_t>(i);
+}
+
+cudaError_t cube_keys(const double* x, int64_t n, GridSpec g, uint32_t* keys, int32_t* iota,
+                      cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  ++g_launches; cube_keys_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(x, n, g, keys, iota);
+  return cudaGetLastError();
+}
+
+// Sorted, centred float32 atoms {x, y, z, 0}, log2 weights, float64 weights.
+__global__ void gather_points_kernel(const double* x, const double* w, int64_t n, int d,
+                                     GridSpec g, const int32_t* perm, float4* pts, float* lw2,
+                                     double* w64) {
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const int64_t i = perm ? perm[s] : s;
+  float c[3] = {0.f, 0.f, 0.f};
+  for (int k = 0; k < d && k < 3; ++k) c[k] = __double2float_rn(x[i * d + k] - g.center[k]);
+  pts[s] = make_float4(c[0], c[1], c[2], 0.f);
+  const double wi = w[i];
+  lw2[s] = __double2float_rn(log2(wi));
+  w64[s] = wi;
+}
+
+cudaError_t gather_points(const double* x, const double* w, int64_t n, int d, GridSpec g,
+                          const int32_t* perm, float4* pts, float* lw2, double* w64,
+                          cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  ++g_launches; gather_points_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(x, w, n, d, g, perm,
+                                                                               pts, lw2, w64);
+  return cudaGetLastError();
+}
+
+__global__ void segment_flags_kernel(const uint32_t* k, int64_t n, uint8_t* flags) {
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  flags[s] = (s == 0 || k[s] != k[s - 1]) ? 1 : 0;
+}
+
+cudaError_t segment_flags(const uint32_t* sorted_keys, int64_t n, uint8_t* flags,
+                          cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  ++g_launches; segment_flags_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(sorted_keys, n,
+                                                                               flags);
+  return cudaGetLastError();
+}
+
+// labels arrive as an inclusive scan of the flags; make them 0-based and
+// record each cluster's first sorted position (offsets[K] = n).
+__global__ void segment_offsets_kernel(int32_t* labels, const uint8_t* flags, int64_t n,
+                                       int32_t* offsets) {
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const int32_t l = labels[s] - 1;
+  labels[s] = l;
+  if (flags[s]) offsets[l] = static_cast<int32_t>(s);
+  if (s == n - 1) offsets[l + 1] = static_cast<int32_t>(n);
+}
+
+cudaError_t segment_offsets(const int32_t* labels, const uint8_t* flags, int64_t n,
+                            int32_t* offsets, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  ++g_launches; segment_offsets_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(
+      const_cast<int32_t*>(labels), flags, n, offsets);
+  return cudaGetLastError();
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__global__ void cluster_stats_kernel(const float4* pts, const double* w64, const int32_t* off,
+                                     int32_t k, int d, float4* cen, float* clw2, double* cw64,
+                                     float* radii) {
+  const int lane = threadIdx.x & 31;
+  const int64_t I = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (I >= k) return;
+  const int32_t s0 = off[I], s1 = off[I + 1];
+  double W = 0.0, a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  for (int32_t s = s0 + lane; s < s1; s += 32) {
+    const double wi = w64[s];
+    const float4 p = pts[s];
+    W += wi;
+    a0 += wi * static_cast<double>(p.x);
+    a1 += wi * static_cast<double>(p.y);
+    a2 += wi * static_cast<double>(p.z);
+  }
+  W = warp_sum(W);
+  a0 = warp_sum(a0);
+  a1 = warp_sum(a1);
+  a2 = warp_sum(a2);
+  const double c0 = a0 / W, c1 = d > 1 ? a1 / W : 0.0, c2 = d > 2 ? a2 / W : 0.0;
+  const float4 cf = make_float4(__double2float_rn(c0), __double2float_rn(c1),
+                                __double2float_rn(c2), 0.f);
+  double r = 0.0;
+  for (int32_t s = s0 + lane; s < s1; s += 32) {
+    const float4 p = pts[s];
+    const double t0 = static_cast<double>(p.x) - cf.x, t1 = static_cast<double>(p.y) - cf.y,
+                 t2 = static_cast<double>(p.z) - cf.z;
+    r = fmax(r, sqrt(t0 * t0 + t1 * t1 + t2 * t2));
+  }
+  r = warp_max(r);
+  if (lane == 0) {
+    cen[I] = cf;
+    cw64[I] = W;
+    clw2[I] = __double2float_rn(log2(W));
+    radii[I] = __double2float_ru(r);
+  }
+}
+
+cudaError_t cluster_stats(const float4* pts, const double* w64, const int32_t* offsets, int32_t k,
+                          int d, float4* cen, float* clw2, double* cw64, float* radii,
+                          cudaStream_t st) {
+  if (k <= 0) return cudaSuccess;
+  const int64_t threads = static_cast<int64_t>(k) * 32;
+  ++g_launches; cluster_stats_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st>>>(
+      pts, w64, offsets, k, d, cen, clw2, cw64, radii);
+  return cudaGetLastError();
+}
+
+// Per-cluster max of a fine potential, rounded up to float (mask inputs).
+__global__ void cluster_max_kernel(const float* v, const int32_t* off, int32_t k, float* out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t I = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (I >= k) return;
+  float m = -INFINITY;
+  for (int32_t s = off[I] + lane; s < off[I + 1]; s += 32) m = fmaxf(m, v[s]);
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) out[I] = m;
+}
+
+cudaError_t cluster_max(const float* v, const int32_t* offsets, int32_t k, float* out,
+                        cudaStream_t st) {
+  if (k <= 0) return cudaSuccess;
+  const int64_t threads = static_cast<int64_t>(k) * 32;
+  ++g_launches; cluster_max_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st>>>(v, offsets, k,
+                                                                                  out);
+  return cudaGetLastError();
+}
+
+// coarse_duals_to_fine by inheritance: used as the
+// expansion reference of the extrapolation softmin.
+__global__ void inherit_kernel(const float* coarse, const int32_t* labels, int64_t n, float* fine) {
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s < n) fine[s] = coarse[labels[s]];
+}
+
+cudaError_t inherit(const float* coarse, const int32_t* labels, int64_t n, float* fine,
+                    cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  ++g_launches; inherit_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(coarse, labels, n, fine);
+  return cudaGetLastError();
+}
+
+}  // namespace msot_dev

@@ -1,0 +1,68 @@
+// common.cuh — shared device/host definitions of the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "policy.h"
+
+namespace msot_dev {
+
+constexpr int kTileRows = MSOT_TILE_ROWS;  // rows per block-sparse tile
+constexpr int kSoftminThreads = 128;       // threads per softmin CTA
+constexpr int kRowsPerThread = kTileRows / kSoftminThreads;
+constexpr int kColTile = 128;              // columns staged per smem buffer
+static_assert(kRowsPerThread == 2, "softmin kernel is written for 2 rows per thread");
+
+constexpr float kLn2 = 0.69314718055994530942f;
+constexpr float kLog2e = 1.44269504088896340736f;
+
+// One softmin problem of a launch group (the four updates of PAPER.md:258-290
+// share a launch).  Rows/cols are float4 {x, y, z, 0} centred float32 atoms
+// in cluster-sorted order; potentials are float32.
+struct Problem {
+  const float4* rows;
+  const float* row_est;   // reference value of the output potential (nullable)
+  float* row_out;         // output potential
+  const float4* cols;
+  const float* col_lw2;   // log2 of column weights
+  const float* col_h;     // column potentials
+  const int32_t* tile_start; // [n_tiles+1] first row of each (cluster-aligned) tile
+  const int64_t* tile_rptr;  // [n_tiles+1] range index per row tile
+  const int2* ranges;        // column ranges [begin, end)
+  const int32_t* tile_ibase; // [n_tiles+1] work items per row tile (prefix)
+  int32_t n_rows, n_cols;
+  float sc;                // 1 / sqrt(2 eps ln2): scaled |dx|^2 = C / (eps ln2)
+  float inv_eps_ln2;       // 1 / (eps ln 2)
+  float inv_lam_eps_ln2;   // 1 / (lambda eps ln 2)
+  float lam_eps;           // lambda * eps
+  float mixw;              // 1 = assign, 1/2 = averaged update
+  float pad_;
+};
+
+constexpr int kMaxProblems = 4;
+
+struct Group {
+  Problem P[kMaxProblems];
+  const int4* items;      // {problem, tile, pos_begin, pos_end}
+  int32_t n_items;
+  float* part;            // [n_items][kTileRows] partial sums
+  int32_t* fb_count;      // fallback row counter (reset per launch)
+  int32_t* fb_total;      // fallback rows over the whole solve
+  int4* fb_list;          // {problem, row, tile, 0}
+  int32_t fb_cap;
+  int32_t n_problems;
+  int32_t tile_prefix[kMaxProblems + 1];  // finalized tiles per problem (prefix)
+  int32_t t0[kMaxProblems];               // first tile this rank finalizes
+};
+
+// Kernel launches issued by this thread (reported as stats.gpu_launches).
+extern thread_local int64_t g_launches;
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+}  // namespace msot_dev

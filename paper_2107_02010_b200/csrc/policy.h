@@ -1,0 +1,167 @@
+/* policy.h — host-side parameter rules shared verbatim by the GPU front-end
+ * and the FP64 oracle, so both run the *same* algorithm:
+ *   - the eps-schedule,
+ *   - the automatic voxel edge and the cube-id / Morton key (north star),
+ *   - the coarse->fine switch index,
+ *   - the row-tile size that defines the block-sparse pair set.
+ * Pure C99 + libm; header-only (static inline).
+ */
+#ifndef MSOT_POLICY_H
+#define MSOT_POLICY_H
+
+#include <math.h>
+#include <stdint.h>
+
+#include "../../include/msot_gpu.h"
+
+#ifdef __CUDACC__
+#define MSOT_HD __host__ __device__
+#else
+#define MSOT_HD
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Rows per block-sparse tile: the truncation mask is expanded to column
+ * ranges per tile of MSOT_TILE_ROWS consecutive (cluster-sorted) rows. */
+#define MSOT_TILE_ROWS 256
+/* Target atoms per voxel for the automatic cluster_scale rule. */
+#define MSOT_AUTO_ATOMS_PER_CELL 256.0
+/* Cube ids are Morton-interleaved with this many bits per axis (D <= 3). */
+#define MSOT_MORTON_BITS 10
+
+static inline int msot_reach_is_inf(double reach) { return !(reach > 0.0) || isinf(reach); }
+
+/* lambda = 1 / (1 + eps/rho), rho = reach^p. */
+static inline double msot_lambda(double eps, const msot_params* p) {
+  if (msot_reach_is_inf(p->reach)) return 1.0;
+  return 1.0 / (1.0 + eps / pow(p->reach, p->p));
+}
+
+/* Schedule length: n = floor(log(d/blur) / log(1/q)) + 1; a ratio within
+ * 1e-9 below an integer counts as that integer (so d=8, blur=1, q=1/2 gives
+ * [8,4,2,1] as SPEC.md:160 requires). */
+static inline int msot_schedule_len(double d, double blur, double q) {
+  if (!(d > blur)) return 1;
+  double r = log(d / blur) / log(1.0 / q);
+  double k = floor(r);
+  if (r - k > 1.0 - 1e-9) k += 1.0;
+  return (int)k + 1;
+}
+
+static inline double msot_schedule_sigma(double d, double blur, double q, int n, int t) {
+  if (t >= n - 1) return blur;
+  return d * pow(q, (double)t);
+}
+
+/* Automatic voxel edge: a grid over the joint bounding box with about
+ * MSOT_AUTO_ATOMS_PER_CELL atoms per cell for the larger cloud, never more
+ * than 2^MSOT_MORTON_BITS - 1 cells along an axis. */
+static inline double msot_auto_cell(const double* lo, const double* hi, int d, int64_t n,
+                                    int64_t m) {
+  double nmax = (double)(n > m ? n : m);
+  double cells = nmax / MSOT_AUTO_ATOMS_PER_CELL;
+  if (cells < 1.0) cells = 1.0;
+  double vol = 1.0, ext_max = 0.0;
+  int nd = 0;
+  for (int k = 0; k < d; ++k) {
+    double e = hi[k] - lo[k];
+    if (e > ext_max) ext_max = e;
+  }
+  if (ext_max <= 0.0) return 1.0;
+  for (int k = 0; k < d; ++k) {
+    double e = hi[k] - lo[k];
+    if (e > 1e-6 * ext_max) { vol *= e; ++nd; }
+  }
+  double s = pow(vol / cells, 1.0 / (double)(nd > 0 ? nd : 1));
+  double smin = ext_max / (double)((1 << MSOT_MORTON_BITS) - 2);
+  if (s < smin) s = smin;
+  return s;
+}
+
+/* Voxel coordinate along one axis: floor((x - origin) / cell) in float64
+ * (one correctly rounded subtraction, one correctly rounded division). */
+MSOT_HD static inline uint32_t msot_cube_coord(double x, double origin, double cell) {
+  double q = floor((x - origin) / cell);
+  if (q < 0.0) q = 0.0;
+  double qmax = (double)((1u << MSOT_MORTON_BITS) - 1u);
+  if (q > qmax) q = qmax;
+  return (uint32_t)q;
+}
+
+MSOT_HD static inline uint32_t msot_spread3(uint32_t v) { /* 10 bits -> every 3rd bit */
+  v &= 0x3ffu;
+  v = (v | (v << 16)) & 0x030000ffu;
+  v = (v | (v << 8)) & 0x0300f00fu;
+  v = (v | (v << 4)) & 0x030c30c3u;
+  v = (v | (v << 2)) & 0x09249249u;
+  return v;
+}
+MSOT_HD static inline uint32_t msot_spread2(uint32_t v) { /* 10 bits -> every 2nd bit */
+  v &= 0x3ffu;
+  v = (v | (v << 8)) & 0x00ff00ffu;
+  v = (v | (v << 4)) & 0x0f0f0f0fu;
+  v = (v | (v << 2)) & 0x33333333u;
+  v = (v | (v << 1)) & 0x55555555u;
+  return v;
+}
+
+/* Morton cube id of one atom (D in 1..3). */
+MSOT_HD static inline uint32_t msot_cube_key(const double* x, int d, const double* origin,
+                                     double cell) {
+  if (d == 1) return msot_cube_coord(x[0], origin[0], cell);
+  if (d == 2)
+    return msot_spread2(msot_cube_coord(x[0], origin[0], cell)) |
+           (msot_spread2(msot_cube_coord(x[1], origin[1], cell)) << 1);
+  return msot_spread3(msot_cube_coord(x[0], origin[0], cell)) |
+         (msot_spread3(msot_cube_coord(x[1], origin[1], cell)) << 1) |
+         (msot_spread3(msot_cube_coord(x[2], origin[2], cell)) << 2);
+}
+
+/* Row tiles of the block-sparse reduction.  With clusters (offsets != NULL)
+ * tiles are cluster-aligned: consecutive whole clusters are packed greedily
+ * while they fit in `cap` rows, and a cluster larger than `cap` is split into
+ * ceil(len/cap) near-equal tiles.  Without clusters: uniform tiles of `cap`.
+ * Writes tile_start[0..T] (T+1 entries, tile_start[T] = n), returns T.
+ * Capacity needed: k + n/cap + 2 entries. */
+static inline int64_t msot_pack_tiles(const int32_t* offsets, int64_t k, int64_t n, int64_t cap,
+                                      int64_t* tile_start) {
+  int64_t t = 0;
+  if (!offsets) {
+    for (int64_t s = 0; s < n; s += cap) tile_start[t++] = s;
+    tile_start[t] = n;
+    return t;
+  }
+  int64_t cur = -1; /* start of the open tile, -1 = none */
+  for (int64_t I = 0; I < k; ++I) {
+    const int64_t b = offsets[I], e = offsets[I + 1], len = e - b;
+    if (len > cap) {
+      if (cur >= 0) { tile_start[t++] = cur; cur = -1; }
+      const int64_t parts = (len + cap - 1) / cap;
+      for (int64_t q = 0; q < parts; ++q) tile_start[t++] = b + q * len / parts;
+    } else if (cur >= 0 && e - cur > cap) {
+      tile_start[t++] = cur;
+      cur = b;
+    } else if (cur < 0) {
+      cur = b;
+    }
+  }
+  if (cur >= 0) tile_start[t++] = cur;
+  tile_start[t] = n;
+  return t;
+}
+
+/* First fine scale: the first t with sigma_t < factor * r_max;
+ * n when no scale qualifies (then only the final update runs fine). */
+static inline int msot_switch_index(const double* sigma, int n, double r_max, double factor) {
+  for (int t = 0; t < n; ++t)
+    if (sigma[t] < factor * r_max) return t;
+  return n;
+}
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MSOT_POLICY_H */

@@ -1,0 +1,87 @@
+// prims.cuh — declarations of the device primitives and kernel launchers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace msot_dev {
+
+// scans (prims.cu)
+size_t scan_temp_elems(int64_t n);
+template <typename TI, typename TO>
+cudaError_t scan(const TI* in, TO* out, int64_t n, bool inclusive, TO* tmp, TO* total,
+                 cudaStream_t st);
+
+// bounding box (prims.cu); lohi holds ordered-int64 keys of min/max per dim
+cudaError_t bbox(const double* x, int64_t n, int d, long long* lohi_dev, bool init,
+                 cudaStream_t st);
+void bbox_decode(const long long* lohi_host, int d, double* lo, double* hi);
+
+// stable LSD radix sort of (key, value) by the low `key_bits` bits
+size_t radix_temp_bytes(int64_t n);
+cudaError_t radix_sort_pairs(uint32_t* keys, int32_t* vals, int64_t n, int key_bits, void* temp,
+                             cudaStream_t st);
+
+// softmin (softmin.cu)
+cudaError_t launch_softmin(const Group& g, int d, cudaStream_t st);
+cudaError_t launch_finalize(const Group& g, cudaStream_t st);
+cudaError_t launch_fallback(const Group& g, int d, int n_sm, cudaStream_t st);
+
+// clustering (cluster.cu)
+struct GridSpec {
+  double origin[3];
+  double center[3];
+  double cell;
+  int d;
+};
+cudaError_t cube_keys(const double* x, int64_t n, GridSpec g, uint32_t* keys, int32_t* iota,
+                      cudaStream_t st);
+cudaError_t gather_points(const double* x, const double* w, int64_t n, int d, GridSpec g,
+                          const int32_t* perm, float4* pts, float* lw2, double* w64,
+                          cudaStream_t st);
+cudaError_t segment_flags(const uint32_t* sorted_keys, int64_t n, uint8_t* flags,
+                          cudaStream_t st);
+cudaError_t segment_offsets(const int32_t* labels, const uint8_t* flags, int64_t n,
+                            int32_t* offsets, cudaStream_t st);
+cudaError_t cluster_stats(const float4* pts, const double* w64, const int32_t* offsets, int32_t k,
+                          int d, float4* cen, float* clw2, double* cw64, float* radii,
+                          cudaStream_t st);
+cudaError_t cluster_max(const float* v, const int32_t* offsets, int32_t k, float* out,
+                        cudaStream_t st);
+cudaError_t inherit(const float* coarse, const int32_t* labels, int64_t n, float* fine,
+                    cudaStream_t st);
+
+// truncation mask + ranges (mask.cu)
+cudaError_t truncation_mask(int32_t kx, int32_t ky, int d, const float4* cx, const float* rx,
+                            const float* fx, const float4* cy, const float* ry, const float* gy,
+                            double eps, double theta, int self, uint8_t* mask, cudaStream_t st);
+cudaError_t transpose_mask(const uint8_t* m, int32_t kx, int32_t ky, uint8_t* mt,
+                           cudaStream_t st);
+// per tile: count ranges and kept columns; then write ranges
+cudaError_t tile_range_count(const int32_t* row_labels, const int32_t* tile_start, int64_t nt,
+                             const int32_t* col_offsets, int32_t ky, const uint8_t* mask,
+                             int64_t* n_ranges, int64_t* n_cols, cudaStream_t st);
+cudaError_t tile_range_write(const int32_t* row_labels, const int32_t* tile_start, int64_t nt,
+                             const int32_t* col_offsets, int32_t ky, const uint8_t* mask,
+                             const int64_t* rptr, int2* ranges, cudaStream_t st);
+cudaError_t dense_ranges(int64_t n_tiles, int32_t n_cols, int64_t* rptr, int2* ranges,
+                         int64_t* tile_cols, cudaStream_t st);
+// work items: per tile ceil(cols/chunk) items
+cudaError_t item_counts(const int64_t* tile_cols, int64_t n_tiles, int64_t chunk, int32_t* cnt,
+                        cudaStream_t st);
+cudaError_t item_write(const int64_t* tile_cols, int64_t t0, int64_t t1, int64_t chunk,
+                       const int32_t* ibase, int problem, int4* items, cudaStream_t st);
+
+// loss (loss.cu)
+cudaError_t divergence_partial(const double* a, const double* b, int64_t n, int64_t m,
+                               const float* a_xx, const float* b_yy, const float* a_xy,
+                               const float* b_yx, double rho /* <=0: balanced */,
+                               double* partials, int nblocks, cudaStream_t st);
+cudaError_t divergence_final(const double* partials, int nblocks, double eps, double rho,
+                             double* out, cudaStream_t st);
+cudaError_t scatter_unsort(const float* v, const int32_t* perm, int64_t n, double* out,
+                           cudaStream_t st);
+
+}  // namespace msot_dev

@@ -1,0 +1,267 @@
+// softmin.cu — K1/K4: the online log-sum-exp softmin of the Sinkhorn loop.
+//
+//   f_i = -lambda eps log sum_j w_j exp((h_j - |x_i - y_j|^2 / 2) / eps)
+// (the four lines of the Algorithm).
+//
+// Design: one CTA = one work item = a 256-row tile (rows
+// sorted by voxel cube, 2 rows per thread) against a chunk of that tile's
+// kept columns (dense = one range per tile; block-sparse = the ranges of the
+// truncation mask).  Columns stream through a double-buffered shared-memory
+// tile, stored as float32 *pairs* so the inner loop runs on the packed
+// FADD2/FFMA2 pipe and issues ~5 instructions per pair next to the one
+// MUFU.EX2 that bounds it (roofline: 16 ex2/clk/SM).
+//
+// Fixed-reference expansion: instead of a running max, every row is
+// expanded around m_i = -est_i / (lambda eps ln2), its previous potential in
+// log2 units, so s_i = sum_j 2^{z_ij - m_i} is additive across column chunks
+// and the update is f_i = est_i - lambda eps ln(s_i).  Since the LSE is
+// bounded by [max, max + log M], a reference within ~60 nats of the truth
+// keeps s_i in [2^-60, 2^100]; rows outside that window are recomputed by the
+// exact online-max kernel (softmin_fallback), so the result never depends on
+// the reference being good.
+//
+// Precision: coordinates are re-centred on the tile's middle row before
+// scaling, so |x^ - y^|^2 is formed from small, exactly-subtracted numbers.
+#include "common.cuh"
+
+namespace msot_dev {
+
+struct RowState {
+  float x0, x1, x2;  // scaled, tile-centred coordinates
+  float nr;          // -(est / (lambda eps ln2))
+};
+
+template <int D>
+__device__ __forceinline__ void load_row(const Problem& P, int r, int r_end, float4 o,
+                                         RowState& rs) {
+  const bool ok = r < r_end;
+  float4 v = ok ? P.rows[r] : o;
+  rs.x0 = (v.x - o.x) * P.sc;
+  rs.x1 = D > 1 ? (v.y - o.y) * P.sc : 0.f;
+  rs.x2 = D > 2 ? (v.z - o.z) * P.sc : 0.f;
+  float est = (P.row_est != nullptr && ok) ? P.row_est[r] : 0.f;
+  rs.nr = -(est * P.inv_lam_eps_ln2);
+}
+
+// Walks the concatenated column ranges of one tile: position -> column.
+struct ColWalker {
+  const int2* rg;
+  int64_t k, kend;
+  int32_t acc;   // positions before range k
+  __device__ __forceinline__ int col(int32_t pos) {
+    while (k < kend) {
+      int2 r = rg[k];
+      int32_t len = r.y - r.x;
+      if (pos < acc + len) return r.x + (pos - acc);
+      acc += len;
+      ++k;
+    }
+    return -1;
+  }
+};
+
+template <int D>
+__global__ void __launch_bounds__(kSoftminThreads)
+softmin_kernel(const __grid_constant__ Group G) {
+  __shared__ __align__(16) float smem[2][kColTile * 4];
+  const int it = blockIdx.x;
+  if (it >= G.n_items) return;
+  const int4 item = G.items[it];
+  const Problem& P = G.P[item.x];
+  const int tid = threadIdx.x;
+  const int row_base = P.tile_start[item.y];
+  const int row_end = P.tile_start[item.y + 1];
+  const float4 o = P.rows[(row_base + row_end) >> 1];
+
+  RowState ra, rb;
+  load_row<D>(P, row_base + tid, row_end, o, ra);
+  load_row<D>(P, row_base + tid + kSoftminThreads, row_end, o, rb);
+
+  ColWalker w{P.ranges, P.tile_rptr[item.y], P.tile_rptr[item.y + 1], 0};
+  const int32_t pos_begin = item.z, pos_end = item.w;
+
+  // raw column prefetch registers
+  float4 cv = make_float4(0.f, 0.f, 0.f, 0.f);
+  float ch = 0.f, cl = 0.f;
+  bool cvalid = false;
+  auto fetch = [&](int32_t tile_pos) {
+    const int32_t pos = tile_pos + tid;
+    cvalid = false;
+    if (pos < pos_end) {
+      const int j = w.col(pos);
+      if (j >= 0) {
+        cv = __ldg(P.cols + j);
+        cl = __ldg(P.col_lw2 + j);
+        ch = __ldg(P.col_h + j);
+        cvalid = true;
+      }
+    }
+  };
+  auto stage = [&](float* buf) {
+    // pair record layout: [-y0a,-y0b,-y1a,-y1b,-y2a,-y2b,-ca,-cb]
+    float* rec = buf + (tid >> 1) * 8 + (tid & 1);
+    if (cvalid) {
+      rec[0] = (o.x - cv.x) * P.sc;
+      rec[2] = D > 1 ? (o.y - cv.y) * P.sc : 0.f;
+      rec[4] = D > 2 ? (o.z - cv.z) * P.sc : 0.f;
+      rec[6] = -(cl + ch * P.inv_eps_ln2);
+    } else {
+      rec[0] = 0.f;
+      rec[2] = 0.f;
+      rec[4] = 0.f;
+      rec[6] = __int_as_float(0x7f800000);  // +inf -> exp2(-inf) = 0
+    }
+  };
+
+  float2 sa = make_float2(0.f, 0.f), sb = make_float2(0.f, 0.f);
+  int buf = 0;
+  fetch(pos_begin);
+  for (int32_t tp = pos_begin; tp < pos_end; tp += kColTile) {
+    stage(smem[buf]);
+    __syncthreads();
+    if (tp + kColTile < pos_end) fetch(tp + kColTile);
+    const float4* s4 = reinterpret_cast<const float4*>(smem[buf]);
+#pragma unroll 4
+    for (int c = 0; c < kColTile / 2; ++c) {
+      const float4 A = s4[2 * c], B = s4[2 * c + 1];
+      const float2 Y0 = make_float2(A.x, A.y);
+      const float2 Y1 = make_float2(A.z, A.w);
+      const float2 Y2 = make_float2(B.x, B.y);
+      const float2 NC = make_float2(B.z, B.w);
+      {
+        float2 q = __fadd2_rn(make_float2(ra.nr, ra.nr), NC);
+        const float2 d0 = __fadd2_rn(make_float2(ra.x0, ra.x0), Y0);
+        q = __ffma2_rn(d0, d0, q);
+        if (D > 1) {
+          const float2 d1 = __fadd2_rn(make_float2(ra.x1, ra.x1), Y1);
+          q = __ffma2_rn(d1, d1, q);
+        }
+        if (D > 2) {
+          const float2 d2 = __fadd2_rn(make_float2(ra.x2, ra.x2), Y2);
+          q = __ffma2_rn(d2, d2, q);
+        }
+        sa = __fadd2_rn(sa, make_float2(ex2_approx(-q.x), ex2_approx(-q.y)));
+      }
+      {
+        float2 q = __fadd2_rn(make_float2(rb.nr, rb.nr), NC);
+        const float2 d0 = __fadd2_rn(make_float2(rb.x0, rb.x0), Y0);
+        q = __ffma2_rn(d0, d0, q);
+        if (D > 1) {
+          const float2 d1 = __fadd2_rn(make_float2(rb.x1, rb.x1), Y1);
+          q = __ffma2_rn(d1, d1, q);
+        }
+        if (D > 2) {
+          const float2 d2 = __fadd2_rn(make_float2(rb.x2, rb.x2), Y2);
+          q = __ffma2_rn(d2, d2, q);
+        }
+        sb = __fadd2_rn(sb, make_float2(ex2_approx(-q.x), ex2_approx(-q.y)));
+      }
+    }
+    buf ^= 1;
+  }
+  float* out = G.part + static_cast<int64_t>(it) * kTileRows;
+  out[tid] = sa.x + sa.y;
+  out[tid + kSoftminThreads] = sb.x + sb.y;
+}
+
+// Combines the partial sums of every row (fixed chunk order: deterministic
+// and independent of the number of GPUs) and applies the update
+//   new = est - mixw * lambda eps ln(s)   (averaging of PAPER.md:293-315).
+// Rows whose sum left the safe window are queued for the exact path.
+// One CTA per row tile of this rank's shard.
+__global__ void __launch_bounds__(kTileRows) softmin_finalize(const __grid_constant__ Group G) {
+  const int b = blockIdx.x;
+  int p = 0;
+  while (p + 1 < G.n_problems && b >= G.tile_prefix[p + 1]) ++p;
+  const Problem& P = G.P[p];
+  const int t = G.t0[p] + (b - G.tile_prefix[p]);
+  const int lr = threadIdx.x;
+  const int r = P.tile_start[t] + lr;
+  if (r >= P.tile_start[t + 1]) return;
+  const int32_t k0 = P.tile_ibase[t], k1 = P.tile_ibase[t + 1];
+  float s = 0.f;
+  for (int32_t k = k0; k < k1; ++k) s += G.part[static_cast<int64_t>(k) * kTileRows + lr];
+  const float est = P.row_est ? P.row_est[r] : 0.f;
+  // window [2^-60, 2^100]: flushed terms (< 2^-126 each) stay below 2^-84 s
+  if (!(s >= 8.67361738e-19f && s <= 1.2676506e30f)) {
+    const int slot = atomicAdd(G.fb_count, 1);
+    atomicAdd(G.fb_total, 1);
+    if (slot < G.fb_cap) G.fb_list[slot] = make_int4(p, r, t, 0);
+    return;
+  }
+  P.row_out[r] = est - P.mixw * P.lam_eps * logf(s);
+}
+
+// Exact online-max LSE for the rows the fixed-reference path rejected: one
+// warp per row over the same column set, float32 with a running max.
+template <int D>
+__global__ void softmin_fallback(const __grid_constant__ Group G) {
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int cnt = min(*G.fb_count, G.fb_cap);
+  for (int q = warp; q < cnt; q += nwarps) {
+    const int4 pr = G.fb_list[q];
+    const Problem& P = G.P[pr.x];
+    const int r = pr.y;
+    const float4 xv = P.rows[r];
+    const int t = pr.z;
+    float m = -INFINITY, s = 0.f;
+    for (int64_t k = P.tile_rptr[t]; k < P.tile_rptr[t + 1]; ++k) {
+      const int2 rg = P.ranges[k];
+      for (int j = rg.x + lane; j < rg.y; j += 32) {
+        const float4 yv = P.cols[j];
+        float dx = xv.x - yv.x, c = dx * dx;
+        if (D > 1) { const float dy = xv.y - yv.y; c = fmaf(dy, dy, c); }
+        if (D > 2) { const float dz = xv.z - yv.z; c = fmaf(dz, dz, c); }
+        const float z = P.col_lw2[j] + (P.col_h[j] - 0.5f * c) * P.inv_eps_ln2;
+        if (z > m) { s = s * exp2f(m - z) + 1.f; m = z; }
+        else s += exp2f(z - m);
+      }
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, off);
+      const float s2 = __shfl_xor_sync(0xffffffffu, s, off);
+      const float mm = fmaxf(m, m2);
+      s = (m == -INFINITY ? 0.f : s * exp2f(m - mm)) + (m2 == -INFINITY ? 0.f : s2 * exp2f(m2 - mm));
+      m = mm;
+    }
+    if (lane == 0) {
+      const float est = P.row_est ? P.row_est[r] : 0.f;
+      const float ft = -P.lam_eps * kLn2 * (m + log2f(s));
+      P.row_out[r] = (1.f - P.mixw) * est + P.mixw * ft;
+    }
+  }
+}
+
+// ---- host launchers -------------------------------------------------------
+
+cudaError_t launch_softmin(const Group& g, int d, cudaStream_t st) {
+  if (g.n_items <= 0) return cudaSuccess;
+  dim3 grid(g.n_items), block(kSoftminThreads);
+  switch (d) {
+    case 1: ++g_launches; softmin_kernel<1><<<grid, block, 0, st>>>(g); break;
+    case 2: ++g_launches; softmin_kernel<2><<<grid, block, 0, st>>>(g); break;
+    default: ++g_launches; softmin_kernel<3><<<grid, block, 0, st>>>(g); break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(const Group& g, cudaStream_t st) {
+  const int tiles = g.tile_prefix[g.n_problems];
+  if (tiles <= 0) return cudaSuccess;
+  ++g_launches; softmin_finalize<<<tiles, kTileRows, 0, st>>>(g);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fallback(const Group& g, int d, int n_sm, cudaStream_t st) {
+  dim3 grid(n_sm), block(256);
+  switch (d) {
+    case 1: ++g_launches; softmin_fallback<1><<<grid, block, 0, st>>>(g); break;
+    case 2: ++g_launches; softmin_fallback<2><<<grid, block, 0, st>>>(g); break;
+    default: ++g_launches; softmin_fallback<3><<<grid, block, 0, st>>>(g); break;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace msot_dev

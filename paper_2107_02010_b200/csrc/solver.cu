@@ -1,0 +1,990 @@
+// solver.cu — host orchestration of the B200 solve and the C ABI
+// (include/msot_gpu.h).
+//
+// One msot_ctx = one GPU (+ optional NCCL communicator; one process per GPU).
+// A solve runs entirely on the device: inputs are copied once, clustered and
+// sorted on the GPU, and every scale of the schedule is one launch group
+//   softmin (all four updates of PAPER.md:258-290) -> finalize -> fallback
+// followed, when world > 1, by an NCCL all-gather of the N+M updated
+// potentials.  The host only walks the schedule scalars and
+// synchronises a handful of times per solve (bounding box, cluster counts,
+// mask sizes, final loss).
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/msot_gpu.h"
+#include "policy.h"
+#include "prims.cuh"
+
+namespace msot_dev {
+thread_local int64_t g_launches = 0;
+}
+
+using namespace msot_dev;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Err {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void raise(int code, const std::string& m) { throw Err{code, m}; }
+
+#define CK(call)                                                                    \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess) raise(MSOT_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+#define NK(call)                                                                    \
+  do {                                                                              \
+    ncclResult_t r_ = (call);                                                       \
+    if (r_ != ncclSuccess) raise(MSOT_ECUDA, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return MSOT_OK;
+  } catch (const Err& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return MSOT_ECUDA;
+  }
+}
+
+}  // namespace
+
+struct msot_ctx {
+  int device = 0, rank = 0, world = 1, n_sm = 148;
+  cudaStream_t st = nullptr;
+  ncclComm_t comm = nullptr;
+  bool profiling = false;
+  std::map<std::string, std::pair<void*, size_t>> bufs;
+  std::vector<cudaEvent_t> ev;  // profiling events (pairs)
+  size_t ev_used = 0;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+
+  template <class T>
+  T* buf(const std::string& name, size_t count) {
+    const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+    auto it = bufs.find(name);
+    if (it != bufs.end() && it->second.second >= bytes) return static_cast<T*>(it->second.first);
+    if (it != bufs.end()) {
+      CK(cudaStreamSynchronize(st));
+      CK(cudaFree(it->second.first));
+      bufs.erase(it);
+    }
+    void* p = nullptr;
+    CK(cudaMalloc(&p, bytes));
+    bufs[name] = {p, bytes};
+    return static_cast<T*>(p);
+  }
+  void ev_pair(cudaEvent_t* a, cudaEvent_t* b) {
+    while (ev.size() < ev_used + 2) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      ev.push_back(e);
+    }
+    *a = ev[ev_used];
+    *b = ev[ev_used + 1];
+    ev_used += 2;
+  }
+};
+
+namespace {
+
+// ---------------------------------------------------------------- measures
+struct DMeasure {
+  int64_t n = 0;
+  int32_t k = 0;
+  float4* pts = nullptr;   // sorted, centred float32 atoms
+  float* lw2 = nullptr;    // log2 weights
+  double* w64 = nullptr;   // float64 weights (sorted)
+  int32_t* perm = nullptr; // sorted -> caller index
+  int32_t* labels = nullptr;
+  int32_t* offsets = nullptr;
+  float4* cpts = nullptr;  // coarse measure (voxel centroids)
+  float* clw2 = nullptr;
+  double* cw64 = nullptr;
+  float* radii = nullptr;
+  std::vector<float> radii_h;
+  std::vector<int32_t> offsets_h;  // cluster offsets (host copy, K+1)
+};
+
+void prepare_measure(msot_ctx* c, const std::string& tag, const double* d_x, const double* d_w,
+                     int64_t n, int d, const GridSpec& g, bool clusters, DMeasure& M) {
+  cudaStream_t st = c->st;
+  M.n = n;
+  uint32_t* keys = c->buf<uint32_t>(tag + ".keys", n);
+  M.perm = c->buf<int32_t>(tag + ".perm", n);
+  CK(cube_keys(d_x, n, g, keys, M.perm, st));
+  void* tmp = c->buf<char>(tag + ".rstmp", radix_temp_bytes(n));
+  const int bits = g.d == 1 ? MSOT_MORTON_BITS : g.d == 2 ? 2 * MSOT_MORTON_BITS : 3 * MSOT_MORTON_BITS;
+  CK(radix_sort_pairs(keys, M.perm, n, bits, tmp, st));
+  M.pts = c->buf<float4>(tag + ".pts", n);
+  M.lw2 = c->buf<float>(tag + ".lw2", n);
+  M.w64 = c->buf<double>(tag + ".w64", n);
+  CK(gather_points(d_x, d_w, n, d, g, M.perm, M.pts, M.lw2, M.w64, st));
+  if (!clusters) return;
+  uint8_t* flags = c->buf<uint8_t>(tag + ".flags", n);
+  M.labels = c->buf<int32_t>(tag + ".labels", n);
+  M.offsets = c->buf<int32_t>(tag + ".offsets", n + 1);
+  int32_t* stmp = c->buf<int32_t>(tag + ".stmp", scan_temp_elems(n));
+  int32_t* kdev = c->buf<int32_t>(tag + ".k", 1);
+  CK(segment_flags(keys, n, flags, st));
+  CK((scan<uint8_t, int32_t>(flags, M.labels, n, true, stmp, kdev, st)));
+  CK(segment_offsets(M.labels, flags, n, M.offsets, st));
+  int32_t k = 0;
+  CK(cudaMemcpyAsync(&k, kdev, sizeof(k), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  M.k = k;
+  M.cpts = c->buf<float4>(tag + ".cpts", k);
+  M.clw2 = c->buf<float>(tag + ".clw2", k);
+  M.cw64 = c->buf<double>(tag + ".cw64", k);
+  M.radii = c->buf<float>(tag + ".radii", k);
+  CK(cluster_stats(M.pts, M.w64, M.offsets, k, d, M.cpts, M.clw2, M.cw64, M.radii, st));
+  M.radii_h.resize(k);
+  CK(cudaMemcpyAsync(M.radii_h.data(), M.radii, k * sizeof(float), cudaMemcpyDeviceToHost, st));
+  M.offsets_h.resize(k + 1);
+  CK(cudaMemcpyAsync(M.offsets_h.data(), M.offsets, (k + 1) * sizeof(int32_t),
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+}
+
+// ------------------------------------------------------------------ ranges
+struct RangeSet {
+  int64_t n_tiles = 0, n_ranges = 0;
+  int32_t* tile_start = nullptr;        // device, n_tiles+1
+  std::vector<int32_t> tile_start_h;
+  int64_t* rptr = nullptr;
+  int2* ranges = nullptr;
+  int64_t* tile_cols = nullptr;
+  std::vector<int64_t> tile_cols_h;
+};
+
+// Row tiles (policy.h:msot_pack_tiles): cluster-aligned when the rows carry
+// cluster offsets, uniform otherwise.
+void make_tiles(msot_ctx* c, const std::string& tag, int64_t rows,
+                const std::vector<int32_t>* offsets, RangeSet& R) {
+  const int64_t k = offsets ? static_cast<int64_t>(offsets->size()) - 1 : 0;
+  std::vector<int64_t> ts(k + rows / kTileRows + 2);
+  R.n_tiles = msot_pack_tiles(offsets ? offsets->data() : nullptr, k, rows, kTileRows, ts.data());
+  R.tile_start_h.assign(ts.begin(), ts.begin() + R.n_tiles + 1);
+  R.tile_start = c->buf<int32_t>(tag + ".tstart", R.n_tiles + 1);
+  CK(cudaMemcpyAsync(R.tile_start, R.tile_start_h.data(), (R.n_tiles + 1) * sizeof(int32_t),
+                     cudaMemcpyHostToDevice, c->st));
+  CK(cudaStreamSynchronize(c->st));  // host vector may be reallocated by the caller
+}
+
+void dense_rangeset(msot_ctx* c, const std::string& tag, int64_t rows, int64_t cols, RangeSet& R,
+                    const std::vector<int32_t>* row_offsets = nullptr) {
+  make_tiles(c, tag, rows, row_offsets, R);
+  R.n_ranges = R.n_tiles;
+  R.rptr = c->buf<int64_t>(tag + ".rptr", R.n_tiles + 1);
+  R.ranges = c->buf<int2>(tag + ".ranges", R.n_tiles);
+  R.tile_cols = c->buf<int64_t>(tag + ".tcols", R.n_tiles);
+  CK(dense_ranges(R.n_tiles, static_cast<int32_t>(cols), R.rptr, R.ranges, R.tile_cols, c->st));
+  R.tile_cols_h.assign(R.n_tiles, cols);
+}
+
+// rows with labels `rl` / cluster offsets (host) `ro`, column clusters with
+// offsets `co` (ky)
+void mask_rangeset(msot_ctx* c, const std::string& tag, const int32_t* rl,
+                   const std::vector<int32_t>& ro, int64_t n_rows, const int32_t* co, int32_t ky,
+                   const uint8_t* mask, RangeSet& R) {
+  cudaStream_t st = c->st;
+  make_tiles(c, tag, n_rows, &ro, R);
+  int64_t* nr = c->buf<int64_t>(tag + ".nr", R.n_tiles + 1);
+  R.tile_cols = c->buf<int64_t>(tag + ".tcols", R.n_tiles);
+  R.rptr = c->buf<int64_t>(tag + ".rptr", R.n_tiles + 1);
+  int64_t* stmp = c->buf<int64_t>(tag + ".stmp", scan_temp_elems(R.n_tiles + 1));
+  CK(tile_range_count(rl, R.tile_start, R.n_tiles, co, ky, mask, nr, R.tile_cols, st));
+  CK(cudaMemsetAsync(nr + R.n_tiles, 0, sizeof(int64_t), st));
+  CK((scan<int64_t, int64_t>(nr, R.rptr, R.n_tiles + 1, false, stmp, nullptr, st)));
+  CK(cudaMemcpyAsync(&R.n_ranges, R.rptr + R.n_tiles, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  R.tile_cols_h.resize(R.n_tiles);
+  CK(cudaMemcpyAsync(R.tile_cols_h.data(), R.tile_cols, R.n_tiles * sizeof(int64_t),
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  R.ranges = c->buf<int2>(tag + ".ranges", R.n_ranges);
+  CK(tile_range_write(rl, R.tile_start, R.n_tiles, co, ky, mask, R.rptr, R.ranges, st));
+}
+
+// ------------------------------------------------------------ launch plans
+struct ProbSpec {
+  const float4* rows;
+  int64_t n_rows;
+  const float4* cols;
+  const float* col_lw2;
+  int64_t n_cols;
+  const RangeSet* rs;
+};
+
+struct Plan {
+  int np = 0;
+  ProbSpec ps[kMaxProblems];
+  int64_t t0[kMaxProblems], t1[kMaxProblems];
+  std::vector<int64_t> row_bounds[kMaxProblems];  // world+1 row boundaries
+  int32_t* ibase[kMaxProblems];
+  int4* items = nullptr;
+  int32_t n_items = 0;
+  float* part = nullptr;
+  double pairs_local = 0.0, pairs_all = 0.0;
+};
+
+// Contiguous tile shards balanced on work (shared with msot_shard_tiles).
+void shard_tiles(const std::vector<double>& work, int world, std::vector<int64_t>& b) {
+  const int64_t nt = static_cast<int64_t>(work.size());
+  b.assign(world + 1, nt);
+  b[0] = 0;
+  double tot = 0.0;
+  for (double w : work) tot += w;
+  double acc = 0.0;
+  int64_t t = 0;
+  for (int r = 1; r < world; ++r) {
+    const double target = tot * r / world;
+    while (t < nt && acc + 0.5 * work[t] < target) acc += work[t++];
+    b[r] = t;
+  }
+}
+
+void build_plan(msot_ctx* c, const std::string& tag, Plan& P) {
+  cudaStream_t st = c->st;
+  // per-problem shard of row tiles, weighted by evaluated pairs
+  int64_t tot_tiles = 0, tot_cols = 0;
+  P.pairs_all = P.pairs_local = 0.0;
+  for (int p = 0; p < P.np; ++p) {
+    const RangeSet& R = *P.ps[p].rs;
+    std::vector<double> work(R.n_tiles);
+    for (int64_t t = 0; t < R.n_tiles; ++t) {
+      const int64_t rows = R.tile_start_h[t + 1] - R.tile_start_h[t];
+      work[t] = static_cast<double>(rows) * static_cast<double>(R.tile_cols_h[t]) + 1.0;
+      P.pairs_all += static_cast<double>(rows) * static_cast<double>(R.tile_cols_h[t]);
+    }
+    std::vector<int64_t> tb;
+    shard_tiles(work, c->world, tb);
+    P.t0[p] = tb[c->rank];
+    P.t1[p] = tb[c->rank + 1];
+    P.row_bounds[p].resize(c->world + 1);
+    for (int r = 0; r <= c->world; ++r) P.row_bounds[p][r] = R.tile_start_h[tb[r]];
+    tot_tiles += P.t1[p] - P.t0[p];
+    for (int64_t t = P.t0[p]; t < P.t1[p]; ++t) {
+      tot_cols += R.tile_cols_h[t];
+      const int64_t rows = R.tile_start_h[t + 1] - R.tile_start_h[t];
+      P.pairs_local += static_cast<double>(rows) * static_cast<double>(R.tile_cols_h[t]);
+    }
+  }
+  // chunk size: enough work items for ~2 waves of resident CTAs
+  const int64_t target = static_cast<int64_t>(c->n_sm) * 12 * 2;
+  int64_t chunk = std::max<int64_t>(2 * kColTile, (tot_cols + target - 1) / std::max<int64_t>(target, 1));
+  chunk = (chunk + kColTile - 1) / kColTile * kColTile;
+  int32_t* cnt = c->buf<int32_t>(tag + ".icnt", tot_tiles + 1);
+  int32_t* ib = c->buf<int32_t>(tag + ".ibase", tot_tiles + 1);
+  int32_t* stmp = c->buf<int32_t>(tag + ".istmp", scan_temp_elems(tot_tiles + 1));
+  int64_t off = 0;
+  for (int p = 0; p < P.np; ++p) {
+    const int64_t nt = P.t1[p] - P.t0[p];
+    CK(item_counts(P.ps[p].rs->tile_cols + P.t0[p], nt, chunk, cnt + off, st));
+    P.ibase[p] = ib + off - P.t0[p];
+    off += nt;
+  }
+  CK(cudaMemsetAsync(cnt + off, 0, sizeof(int32_t), st));
+  CK((scan<int32_t, int32_t>(cnt, ib, off + 1, false, stmp, nullptr, st)));
+  CK(cudaMemcpyAsync(&P.n_items, ib + off, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  P.items = c->buf<int4>(tag + ".items", P.n_items);
+  for (int p = 0; p < P.np; ++p)
+    CK(item_write(P.ps[p].rs->tile_cols, P.t0[p], P.t1[p], chunk, P.ibase[p], p, P.items, st));
+  P.part = c->buf<float>(tag + ".part", static_cast<size_t>(P.n_items) * kTileRows);
+}
+
+struct ScaleArgs {
+  const float* h[kMaxProblems];    // column potentials
+  const float* est[kMaxProblems];  // expansion reference of the output
+  float* out[kMaxProblems];
+  double eps, lam, mixw;
+};
+
+struct SolveState {
+  msot_stats* S;
+  int d;
+  int32_t* fb_count;
+  int32_t* fb_total;
+  int4* fb_list;
+  int32_t fb_cap;
+};
+
+void run_group(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& ss) {
+  cudaStream_t st = c->st;
+  Group G{};
+  const double ln2 = 0.69314718055994530942;
+  int32_t tiles_acc = 0;
+  G.tile_prefix[0] = 0;
+  for (int p = 0; p < P.np; ++p) {
+    Problem& Q = G.P[p];
+    const ProbSpec& S = P.ps[p];
+    Q.rows = S.rows;
+    Q.row_est = a.est[p];
+    Q.row_out = a.out[p];
+    Q.cols = S.cols;
+    Q.col_lw2 = S.col_lw2;
+    Q.col_h = a.h[p];
+    Q.tile_start = S.rs->tile_start;
+    Q.tile_rptr = S.rs->rptr;
+    Q.ranges = S.rs->ranges;
+    Q.tile_ibase = P.ibase[p];
+    Q.n_rows = static_cast<int32_t>(S.n_rows);
+    Q.n_cols = static_cast<int32_t>(S.n_cols);
+    Q.sc = static_cast<float>(1.0 / std::sqrt(2.0 * a.eps * ln2));
+    Q.inv_eps_ln2 = static_cast<float>(1.0 / (a.eps * ln2));
+    Q.inv_lam_eps_ln2 = static_cast<float>(1.0 / (a.lam * a.eps * ln2));
+    Q.lam_eps = static_cast<float>(a.lam * a.eps);
+    Q.mixw = static_cast<float>(a.mixw);
+    G.t0[p] = static_cast<int32_t>(P.t0[p]);
+    tiles_acc += static_cast<int32_t>(P.t1[p] - P.t0[p]);
+    G.tile_prefix[p + 1] = tiles_acc;
+  }
+  G.n_problems = P.np;
+  G.items = P.items;
+  G.n_items = P.n_items;
+  G.part = P.part;
+  G.fb_count = ss.fb_count;
+  G.fb_total = ss.fb_total;
+  G.fb_list = ss.fb_list;
+  G.fb_cap = ss.fb_cap;
+  CK(cudaMemsetAsync(ss.fb_count, 0, sizeof(int32_t), st));
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->profiling) {
+    c->ev_pair(&e0, &e1);
+    CK(cudaEventRecord(e0, st));
+  }
+  CK(launch_softmin(G, ss.d, st));
+  if (c->profiling) CK(cudaEventRecord(e1, st));
+  CK(launch_finalize(G, st));
+  CK(launch_fallback(G, ss.d, c->n_sm, st));
+  ss.S->softmin_launches += 1;
+  ss.S->pairs_evaluated += P.pairs_all;
+  // all-gather of the updated potentials (NCCL over NVLink)
+  if (c->world > 1) {
+    NK(ncclGroupStart());
+    for (int p = 0; p < P.np; ++p)
+      for (int r = 0; r < c->world; ++r) {
+        const int64_t b0 = P.row_bounds[p][r], b1 = P.row_bounds[p][r + 1];
+        if (b1 > b0) NK(ncclBroadcast(a.out[p] + b0, a.out[p] + b0, b1 - b0, ncclFloat, r, c->comm, st));
+      }
+    NK(ncclGroupEnd());
+  }
+}
+
+// ------------------------------------------------------------------ solve
+struct Potentials {
+  float* v[2][4];  // [buffer][a_xx, b_yy, a_xy, b_yx]
+};
+
+void alloc_pots(msot_ctx* c, const std::string& tag, int64_t n, int64_t m, Potentials& P) {
+  for (int b = 0; b < 2; ++b) {
+    const std::string t = tag + std::to_string(b);
+    P.v[b][0] = c->buf<float>(t + ".a_xx", n);
+    P.v[b][1] = c->buf<float>(t + ".b_yy", m);
+    P.v[b][2] = c->buf<float>(t + ".a_xy", m);
+    P.v[b][3] = c->buf<float>(t + ".b_yx", n);
+    CK(cudaMemsetAsync(P.v[b][0], 0, n * sizeof(float), c->st));
+    CK(cudaMemsetAsync(P.v[b][1], 0, m * sizeof(float), c->st));
+    CK(cudaMemsetAsync(P.v[b][2], 0, m * sizeof(float), c->st));
+    CK(cudaMemsetAsync(P.v[b][3], 0, n * sizeof(float), c->st));
+  }
+}
+
+// The four symmetric problems on measures X (rows of a_xx, b_yx) and Y.
+void sym_specs(Plan& P, const float4* xp, const float* xl, int64_t n, const float4* yp,
+               const float* yl, int64_t m, const RangeSet* rxx, const RangeSet* ryy,
+               const RangeSet* rxy, const RangeSet* ryx) {
+  P.np = 4;
+  P.ps[0] = {xp, n, xp, xl, n, rxx};  // a_xx: rows x, cols x
+  P.ps[1] = {yp, m, yp, yl, m, ryy};  // b_yy: rows y, cols y
+  P.ps[2] = {yp, m, xp, xl, n, rxy};  // a_xy: rows y, cols x
+  P.ps[3] = {xp, n, yp, yl, m, ryx};  // b_yx: rows x, cols y
+}
+
+// One averaged (or final, assigned) symmetric update:
+// all four read buffer `cur`, write buffer `cur ^ 1`.
+void sym_step(msot_ctx* c, const Plan& P, Potentials& U, int& cur, double eps, double lam,
+              bool assign, SolveState& ss) {
+  float** o = U.v[cur];
+  float** n = U.v[cur ^ 1];
+  ScaleArgs a{};
+  a.h[0] = o[0]; a.est[0] = o[0]; a.out[0] = n[0];
+  a.h[1] = o[1]; a.est[1] = o[1]; a.out[1] = n[1];
+  a.h[2] = o[3]; a.est[2] = o[2]; a.out[2] = n[2];
+  a.h[3] = o[2]; a.est[3] = o[3]; a.out[3] = n[3];
+  a.eps = eps;
+  a.lam = lam;
+  a.mixw = assign ? 1.0 : 0.5;
+  run_group(c, P, a, ss);
+  cur ^= 1;
+}
+
+void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const double* d_a,
+                  int64_t n, const double* d_y, const double* d_b, int64_t m, int d,
+                  double* loss_out, msot_stats* S, double* h_pots[4]) {
+  if (n < 1 || m < 1) raise(MSOT_EDATA, "empty measure");
+  if (n > 0x7fffff00LL || m > 0x7fffff00LL) raise(MSOT_EDATA, "measure too large");
+  if (d < 1 || d > 3) raise(MSOT_EUSAGE, "the GPU softmin supports D in 1..3");
+  if (!(prm->blur > 0) || !(prm->scaling > 0 && prm->scaling < 1))
+    raise(MSOT_EUSAGE, "invalid blur/scaling");
+  if (prm->p != 2.0) raise(MSOT_EUSAGE, "the GPU path implements p = 2");
+  cudaStream_t st = c->st;
+  const int64_t launches0 = g_launches;
+  c->ev_used = 0;
+  CK(cudaEventRecord(c->t0, st));
+
+  // diameter_estimate -- exact min/max on the device
+  long long* lohi = c->buf<long long>("bbox", 6);
+  CK(bbox(d_x, n, d, lohi, true, st));
+  CK(bbox(d_y, m, d, lohi, false, st));
+  long long lh[6];
+  CK(cudaMemcpyAsync(lh, lohi, 2 * d * sizeof(long long), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+  bbox_decode(lh, d, lo, hi);
+  double diag2 = 0.0;
+  for (int k = 0; k < d; ++k) diag2 += (hi[k] - lo[k]) * (hi[k] - lo[k]);
+  const double diam = std::max(std::sqrt(diag2), prm->blur);
+  S->diameter = diam;
+  const int ns = msot_schedule_len(diam, prm->blur, prm->scaling);
+  if (prm->max_full_iters > 0 && ns > prm->max_full_iters)
+    raise(MSOT_EUSAGE, "schedule longer than max_full_iters");
+  std::vector<double> sig(ns), eps(ns), lam(ns);
+  msot_schedule(diam, prm, sig.data(), eps.data(), lam.data(), ns);
+  S->n_scales = ns;
+
+  GridSpec g{};
+  g.d = d;
+  for (int k = 0; k < d; ++k) {
+    g.origin[k] = lo[k];
+    g.center[k] = 0.5 * (lo[k] + hi[k]);
+  }
+  const double cell = prm->cluster_scale > 0 ? prm->cluster_scale : msot_auto_cell(lo, hi, d, n, m);
+  g.cell = cell;
+  const bool ms = prm->multiscale != 0;
+  DMeasure X, Y;
+  prepare_measure(c, "x", d_x, d_a, n, d, g, ms, X);
+  prepare_measure(c, "y", d_y, d_b, m, d, g, ms, Y);
+
+  SolveState ss{S, d, c->buf<int32_t>("fb.count", 1), c->buf<int32_t>("fb.total", 1), nullptr, 0};
+  ss.fb_cap = static_cast<int32_t>(std::min<int64_t>(2 * (n + m), 1 << 22));
+  ss.fb_list = c->buf<int4>("fb.list", ss.fb_cap);
+  CK(cudaMemsetAsync(ss.fb_total, 0, sizeof(int32_t), st));
+
+  Potentials U;
+  alloc_pots(c, "pot", n, m, U);
+  int cur = 0;
+  const double full = double(n) * n + double(m) * m + 2.0 * double(n) * m;
+
+  if (!ms) {
+    S->t_switch = 0;
+    RangeSet rxx, ryy, rxy, ryx;
+    dense_rangeset(c, "d.xx", n, n, rxx);
+    dense_rangeset(c, "d.yy", m, m, ryy);
+    dense_rangeset(c, "d.xy", m, n, rxy);
+    dense_rangeset(c, "d.yx", n, m, ryx);
+    Plan P;
+    sym_specs(P, X.pts, X.lw2, n, Y.pts, Y.lw2, m, &rxx, &ryy, &rxy, &ryx);
+    build_plan(c, "pd", P);
+    for (int t = 0; t <= ns; ++t) {
+      const int tt = std::min(t, ns - 1);
+      sym_step(c, P, U, cur, eps[tt], lam[tt], t == ns, ss);
+      S->pairs_dense += full;
+    }
+  } else {
+    S->cluster_scale = cell;
+    S->kx = X.k;
+    S->ky = Y.k;
+    double rmax = 0.0;
+    for (float r : X.radii_h) rmax = std::max(rmax, double(r));
+    for (float r : Y.radii_h) rmax = std::max(rmax, double(r));
+    const int tsw = msot_switch_index(sig.data(), ns, rmax, prm->switch_factor);
+    S->t_switch = tsw;
+    // coarse phase on the centroid measures (dense)
+    if (tsw > 0) {
+      Potentials Uc;
+      alloc_pots(c, "cpot", X.k, Y.k, Uc);
+      int ccur = 0;
+      RangeSet rxx, ryy, rxy, ryx;
+      dense_rangeset(c, "c.xx", X.k, X.k, rxx);
+      dense_rangeset(c, "c.yy", Y.k, Y.k, ryy);
+      dense_rangeset(c, "c.xy", Y.k, X.k, rxy);
+      dense_rangeset(c, "c.yx", X.k, Y.k, ryx);
+      Plan Pc;
+      sym_specs(Pc, X.cpts, X.clw2, X.k, Y.cpts, Y.clw2, Y.k, &rxx, &ryy, &rxy, &ryx);
+      build_plan(c, "pc", Pc);
+      const double cfull = double(X.k) * X.k + double(Y.k) * Y.k + 2.0 * double(X.k) * Y.k;
+      for (int t = 0; t < tsw; ++t) {
+        sym_step(c, Pc, Uc, ccur, eps[t], lam[t], false, ss);
+        S->pairs_dense += cfull;
+      }
+      // coarse -> fine extrapolation: one lambda-damped
+      // softmin of every fine atom against the coarse measure, expanded
+      // around the inherited coarse value.
+      float** co = Uc.v[ccur];
+      float* inh[4];
+      for (int q = 0; q < 4; ++q) inh[q] = U.v[cur ^ 1][q];  // scratch = the other buffer
+      CK(inherit(co[0], X.labels, n, inh[0], st));
+      CK(inherit(co[1], Y.labels, m, inh[1], st));
+      CK(inherit(co[2], Y.labels, m, inh[2], st));
+      CK(inherit(co[3], X.labels, n, inh[3], st));
+      RangeSet exx, eyy, exy, eyx;
+      dense_rangeset(c, "e.xx", n, X.k, exx, &X.offsets_h);
+      dense_rangeset(c, "e.yy", m, Y.k, eyy, &Y.offsets_h);
+      dense_rangeset(c, "e.xy", m, X.k, exy, &Y.offsets_h);
+      dense_rangeset(c, "e.yx", n, Y.k, eyx, &X.offsets_h);
+      Plan Pe;
+      Pe.np = 4;
+      Pe.ps[0] = {X.pts, n, X.cpts, X.clw2, X.k, &exx};
+      Pe.ps[1] = {Y.pts, m, Y.cpts, Y.clw2, Y.k, &eyy};
+      Pe.ps[2] = {Y.pts, m, X.cpts, X.clw2, X.k, &exy};
+      Pe.ps[3] = {X.pts, n, Y.cpts, Y.clw2, Y.k, &eyx};
+      build_plan(c, "pe", Pe);
+      ScaleArgs a{};
+      a.h[0] = co[0]; a.est[0] = inh[0]; a.out[0] = U.v[cur][0];
+      a.h[1] = co[1]; a.est[1] = inh[1]; a.out[1] = U.v[cur][1];
+      a.h[2] = co[3]; a.est[2] = inh[2]; a.out[2] = U.v[cur][2];
+      a.h[3] = co[2]; a.est[3] = inh[3]; a.out[3] = U.v[cur][3];
+      a.eps = eps[tsw - 1];
+      a.lam = lam[tsw - 1];
+      a.mixw = 1.0;
+      run_group(c, Pe, a, ss);
+    }
+    // fine phase: block-sparse updates restricted to the truncation masks
+    uint8_t* mxx = c->buf<uint8_t>("m.xx", size_t(X.k) * X.k);
+    uint8_t* myy = c->buf<uint8_t>("m.yy", size_t(Y.k) * Y.k);
+    uint8_t* mxy = c->buf<uint8_t>("m.xy", size_t(X.k) * Y.k);
+    uint8_t* myx = c->buf<uint8_t>("m.yx", size_t(Y.k) * X.k);
+    float* fmax[4];
+    fmax[0] = c->buf<float>("m.Fxx", X.k);
+    fmax[1] = c->buf<float>("m.Gyy", Y.k);
+    fmax[2] = c->buf<float>("m.Gxy", Y.k);
+    fmax[3] = c->buf<float>("m.Fyx", X.k);
+    RangeSet rxx, ryy, rxy, ryx;
+    Plan Pf;
+    auto build_masks = [&](double e) {
+      if (tsw == 0) {
+        CK(cudaMemsetAsync(mxx, 1, size_t(X.k) * X.k, st));
+        CK(cudaMemsetAsync(myy, 1, size_t(Y.k) * Y.k, st));
+        CK(cudaMemsetAsync(mxy, 1, size_t(X.k) * Y.k, st));
+      } else {
+        float** f = U.v[cur];
+        CK(cluster_max(f[0], X.offsets, X.k, fmax[0], st));
+        CK(cluster_max(f[1], Y.offsets, Y.k, fmax[1], st));
+        CK(cluster_max(f[2], Y.offsets, Y.k, fmax[2], st));
+        CK(cluster_max(f[3], X.offsets, X.k, fmax[3], st));
+        CK(truncation_mask(X.k, X.k, d, X.cpts, X.radii, fmax[0], X.cpts, X.radii, fmax[0], e,
+                           prm->theta, 1, mxx, st));
+        CK(truncation_mask(Y.k, Y.k, d, Y.cpts, Y.radii, fmax[1], Y.cpts, Y.radii, fmax[1], e,
+                           prm->theta, 1, myy, st));
+        CK(truncation_mask(X.k, Y.k, d, X.cpts, X.radii, fmax[3], Y.cpts, Y.radii, fmax[2], e,
+                           prm->theta, 0, mxy, st));
+      }
+      CK(transpose_mask(mxy, X.k, Y.k, myx, st));
+      mask_rangeset(c, "f.xx", X.labels, X.offsets_h, n, X.offsets, X.k, mxx, rxx);
+      mask_rangeset(c, "f.yy", Y.labels, Y.offsets_h, m, Y.offsets, Y.k, myy, ryy);
+      mask_rangeset(c, "f.yx", X.labels, X.offsets_h, n, Y.offsets, Y.k, mxy, ryx);  // rows x, cols y
+      mask_rangeset(c, "f.xy", Y.labels, Y.offsets_h, m, X.offsets, X.k, myx, rxy);  // rows y, cols x
+      sym_specs(Pf, X.pts, X.lw2, n, Y.pts, Y.lw2, m, &rxx, &ryy, &rxy, &ryx);
+      build_plan(c, "pf", Pf);
+    };
+    for (int t = tsw; t <= ns; ++t) {
+      const int tt = std::min(t, ns - 1);
+      const bool rebuild =
+          (t == tsw) || (prm->retruncate > 0 && t < ns && (t - tsw) % prm->retruncate == 0);
+      if (rebuild) build_masks(eps[tt]);
+      sym_step(c, Pf, U, cur, eps[tt], lam[tt], t == ns, ss);
+      S->pairs_dense += full;
+      S->pairs_fine += Pf.pairs_all;
+      S->pairs_fine_dense += full;
+    }
+  }
+
+  // divergence (eq. 5-6), fixed-order float64
+  const double rho = msot_reach_is_inf(prm->reach) ? 0.0 : std::pow(prm->reach, prm->p);
+  const int nb = 256;
+  double* partials = c->buf<double>("loss.part", 3 * nb);
+  double* lout = c->buf<double>("loss.out", 3);
+  float** f = U.v[cur];
+  CK(divergence_partial(X.w64, Y.w64, n, m, f[0], f[1], f[2], f[3], rho, partials, nb, st));
+  CK(divergence_final(partials, nb, eps[ns - 1], rho, lout, st));
+  double res[3];
+  int32_t fbt = 0;
+  CK(cudaMemcpyAsync(res, lout, sizeof(res), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&fbt, ss.fb_total, sizeof(fbt), cudaMemcpyDeviceToHost, st));
+  if (h_pots) {
+    double* tmp = c->buf<double>("unsort", std::max(n, m));
+    const int64_t len[4] = {n, m, m, n};
+    const int32_t* perm[4] = {X.perm, Y.perm, Y.perm, X.perm};
+    for (int q = 0; q < 4; ++q) {
+      if (!h_pots[q]) continue;
+      CK(scatter_unsort(f[q], perm[q], len[q], tmp, st));
+      CK(cudaMemcpyAsync(h_pots[q], tmp, len[q] * sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      S->d2h_bytes += len[q] * sizeof(double);
+    }
+  }
+  CK(cudaEventRecord(c->t1, st));
+  CK(cudaStreamSynchronize(st));
+  float ms_total = 0.f;
+  CK(cudaEventElapsedTime(&ms_total, c->t0, c->t1));
+  S->total_ms = ms_total;
+  if (c->profiling) {
+    double acc = 0.0;
+    for (size_t k = 0; k + 1 < c->ev_used; k += 2) {
+      float e = 0.f;
+      CK(cudaEventElapsedTime(&e, c->ev[k], c->ev[k + 1]));
+      acc += e;
+    }
+    S->softmin_ms = acc;
+  }
+  S->fallback_rows = fbt;
+  S->gpu_launches = g_launches - launches0;
+  S->d2h_bytes += sizeof(res);
+  if (!std::isfinite(res[0])) raise(MSOT_ENUMERIC, "non-finite divergence");
+  *loss_out = res[0];
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+const char* msot_last_error(void) { return g_err.c_str(); }
+
+void msot_params_default(msot_params* p) {
+  std::memset(p, 0, sizeof(*p));
+  p->blur = 0.05;
+  p->reach = INFINITY;
+  p->p = 2.0;
+  p->scaling = 0.9;
+  p->multiscale = 0;
+  p->retruncate = 0;
+  p->cluster_scale = 0.0;
+  p->theta = 20.0;
+  p->switch_factor = 2.0;
+  p->max_full_iters = 10000;
+}
+
+int msot_schedule(double diameter, const msot_params* p, double* sigma, double* eps, double* lam,
+                  int cap) {
+  const int n = msot_schedule_len(diameter, p->blur, p->scaling);
+  if (n > cap) return -n;
+  for (int t = 0; t < n; ++t) {
+    sigma[t] = msot_schedule_sigma(diameter, p->blur, p->scaling, n, t);
+    eps[t] = std::pow(sigma[t], p->p);
+    lam[t] = msot_lambda(eps[t], p);
+  }
+  return n;
+}
+
+int msot_shard_tiles(const double* work, int64_t n_tiles, int world, int64_t* bounds) {
+  if (world < 1 || n_tiles < 0) {
+    g_err = "invalid shard request";
+    return MSOT_EUSAGE;
+  }
+  std::vector<double> w(work, work + n_tiles);
+  std::vector<int64_t> b;
+  shard_tiles(w, world, b);
+  std::copy(b.begin(), b.end(), bounds);
+  return MSOT_OK;
+}
+
+static int create_common(int device, msot_ctx** out, msot_ctx* c) {
+  CK(cudaSetDevice(device));
+  CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+  CK(cudaEventCreate(&c->t0));
+  CK(cudaEventCreate(&c->t1));
+  CK(cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, device));
+  c->device = device;
+  *out = c;
+  return MSOT_OK;
+}
+
+int msot_create(int device, msot_ctx** out) {
+  return guard([&] {
+    auto* c = new msot_ctx();
+    try {
+      create_common(device, out, c);
+    } catch (...) {
+      delete c;
+      throw;
+    }
+  });
+}
+
+int msot_nccl_unique_id(unsigned char out[128]) {
+  return guard([&] {
+    ncclUniqueId id;
+    NK(ncclGetUniqueId(&id));
+    static_assert(sizeof(id) == 128, "ncclUniqueId size");
+    std::memcpy(out, &id, 128);
+  });
+}
+
+int msot_create_dist(int device, int rank, int world, const unsigned char nccl_id[128],
+                     msot_ctx** out) {
+  return guard([&] {
+    if (world < 1 || rank < 0 || rank >= world) raise(MSOT_EUSAGE, "invalid rank/world");
+    auto* c = new msot_ctx();
+    try {
+      create_common(device, out, c);
+      c->rank = rank;
+      c->world = world;
+      if (world > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id, 128);
+        NK(ncclCommInitRank(&c->comm, world, id, rank));
+      }
+    } catch (...) {
+      delete c;
+      *out = nullptr;
+      throw;
+    }
+  });
+}
+
+void msot_destroy(msot_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->st);
+  for (auto& kv : c->bufs) cudaFree(kv.second.first);
+  for (auto e : c->ev) cudaEventDestroy(e);
+  if (c->t0) cudaEventDestroy(c->t0);
+  if (c->t1) cudaEventDestroy(c->t1);
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->st) cudaStreamDestroy(c->st);
+  delete c;
+}
+
+int msot_set_profiling(msot_ctx* c, int on) {
+  if (!c) return MSOT_EUSAGE;
+  c->profiling = on != 0;
+  return MSOT_OK;
+}
+
+static void check_weights(const double* w, int64_t n) {
+  for (int64_t i = 0; i < n; ++i)
+    if (!(w[i] > 0) || !std::isfinite(w[i])) raise(MSOT_EDATA, "weights must be finite and > 0");
+}
+
+int msot_sinkhorn(msot_ctx* c, const msot_params* prm, const double* x, const double* a, int64_t n,
+                  const double* y, const double* b, int64_t m, int d, double* a_xx, double* b_yy,
+                  double* a_xy, double* b_yx, double* loss_out, msot_stats* stats) {
+  return guard([&] {
+    if (!c || !prm || !x || !a || !y || !b || !loss_out) raise(MSOT_EUSAGE, "null argument");
+    if (n < 1 || m < 1) raise(MSOT_EDATA, "empty measure");
+    check_weights(a, n);
+    check_weights(b, m);
+    CK(cudaSetDevice(c->device));
+    msot_stats local{};
+    msot_stats* S = stats ? stats : &local;
+    std::memset(S, 0, sizeof(*S));
+    S->rank = c->rank;
+    S->world = c->world;
+    double* dx = c->buf<double>("in.x", n * d);
+    double* da = c->buf<double>("in.a", n);
+    double* dy = c->buf<double>("in.y", m * d);
+    double* db = c->buf<double>("in.b", m);
+    CK(cudaMemcpyAsync(dx, x, n * d * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(da, a, n * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(dy, y, m * d * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(db, b, m * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    S->h2d_bytes = double((n + m) * (d + 1)) * sizeof(double);
+    double* hp[4] = {a_xx, b_yy, a_xy, b_yx};
+    solve_device(c, prm, dx, da, n, dy, db, m, d, loss_out, S, hp);
+  });
+}
+
+int msot_sinkhorn_device(msot_ctx* c, const msot_params* prm, const double* d_x, const double* d_a,
+                         int64_t n, const double* d_y, const double* d_b, int64_t m, int d,
+                         double* loss_out, msot_stats* stats) {
+  return guard([&] {
+    if (!c || !prm || !d_x || !d_a || !d_y || !d_b || !loss_out) raise(MSOT_EUSAGE, "null argument");
+    CK(cudaSetDevice(c->device));
+    msot_stats local{};
+    msot_stats* S = stats ? stats : &local;
+    std::memset(S, 0, sizeof(*S));
+    S->rank = c->rank;
+    S->world = c->world;
+    solve_device(c, prm, d_x, d_a, n, d_y, d_b, m, d, loss_out, S, nullptr);
+  });
+}
+
+// One dense softmin through the production kernel (rows in caller order).
+int msot_softmin(msot_ctx* c, const double* x, int64_t n, const double* y, int64_t m, int d,
+                 const double* logw_y, const double* h, double eps, double lambda,
+                 const double* f_est, double* f_out) {
+  return guard([&] {
+    if (!c || !x || !y || !logw_y || !h || !f_out) raise(MSOT_EUSAGE, "null argument");
+    if (n < 1 || m < 1) raise(MSOT_EDATA, "empty input");
+    if (d < 1 || d > 3) raise(MSOT_EUSAGE, "the GPU softmin supports D in 1..3");
+    if (!(eps > 0) || !(lambda > 0)) raise(MSOT_EUSAGE, "eps and lambda must be > 0");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->st;
+    // centre on the joint bounding box, as the solver does
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t i = 0; i < n; ++i)
+      for (int k = 0; k < d; ++k) lo[k] = std::min(lo[k], x[i * d + k]), hi[k] = std::max(hi[k], x[i * d + k]);
+    for (int64_t j = 0; j < m; ++j)
+      for (int k = 0; k < d; ++k) lo[k] = std::min(lo[k], y[j * d + k]), hi[k] = std::max(hi[k], y[j * d + k]);
+    std::vector<float4> xp(n), yp(m);
+    std::vector<float> yl(m), hh(m), fe(n, 0.f);
+    for (int64_t i = 0; i < n; ++i) {
+      float v[3] = {0, 0, 0};
+      for (int k = 0; k < d; ++k) v[k] = static_cast<float>(x[i * d + k] - 0.5 * (lo[k] + hi[k]));
+      xp[i] = make_float4(v[0], v[1], v[2], 0.f);
+      if (f_est) fe[i] = static_cast<float>(f_est[i]);
+    }
+    for (int64_t j = 0; j < m; ++j) {
+      float v[3] = {0, 0, 0};
+      for (int k = 0; k < d; ++k) v[k] = static_cast<float>(y[j * d + k] - 0.5 * (lo[k] + hi[k]));
+      yp[j] = make_float4(v[0], v[1], v[2], 0.f);
+      yl[j] = static_cast<float>(logw_y[j] / 0.69314718055994530942);
+      hh[j] = static_cast<float>(h[j]);
+    }
+    float4* dxp = c->buf<float4>("sm.x", n);
+    float4* dyp = c->buf<float4>("sm.y", m);
+    float* dyl = c->buf<float>("sm.yl", m);
+    float* dh = c->buf<float>("sm.h", m);
+    float* dfe = c->buf<float>("sm.fe", n);
+    float* dfo = c->buf<float>("sm.fo", n);
+    CK(cudaMemcpyAsync(dxp, xp.data(), n * sizeof(float4), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dyp, yp.data(), m * sizeof(float4), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dyl, yl.data(), m * sizeof(float), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dh, hh.data(), m * sizeof(float), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dfe, fe.data(), n * sizeof(float), cudaMemcpyHostToDevice, st));
+    RangeSet R;
+    dense_rangeset(c, "sm.r", n, m, R);
+    Plan P;
+    P.np = 1;
+    P.ps[0] = {dxp, n, dyp, dyl, m, &R};
+    const int rank = c->rank, world = c->world;
+    c->rank = 0;
+    c->world = 1;  // a single softmin is not sharded
+    msot_stats S{};
+    SolveState ss{&S, d, c->buf<int32_t>("fb.count", 1), c->buf<int32_t>("fb.total", 1), nullptr, 0};
+    ss.fb_cap = static_cast<int32_t>(std::min<int64_t>(n, 1 << 22));
+    ss.fb_list = c->buf<int4>("fb.list", std::max<int64_t>(ss.fb_cap, 2 * 1));
+    try {
+      build_plan(c, "psm", P);
+      ScaleArgs a{};
+      a.h[0] = dh;
+      a.est[0] = dfe;
+      a.out[0] = dfo;
+      a.eps = eps;
+      a.lam = lambda;
+      a.mixw = 1.0;
+      run_group(c, P, a, ss);
+    } catch (...) {
+      c->rank = rank;
+      c->world = world;
+      throw;
+    }
+    c->rank = rank;
+    c->world = world;
+    std::vector<float> fo(n);
+    CK(cudaMemcpyAsync(fo.data(), dfo, n * sizeof(float), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int64_t i = 0; i < n; ++i) f_out[i] = fo[i];
+  });
+}
+
+int msot_grid_cluster(msot_ctx* c, const double* x, const double* w, int64_t n, int d,
+                      const double* origin, double cell, int32_t* perm, int32_t* labels,
+                      int32_t* offsets, int32_t* k_out, double* centroids, double* cweights,
+                      float* radii) {
+  return guard([&] {
+    if (!c || !x || !w || !origin || !perm || !labels || !offsets || !k_out) raise(MSOT_EUSAGE, "null argument");
+    if (d < 1 || d > 3) raise(MSOT_EUSAGE, "grid clustering supports D in 1..3");
+    if (n < 1) raise(MSOT_EDATA, "empty measure");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->st;
+    double* dx = c->buf<double>("gc.x", n * d);
+    double* dw = c->buf<double>("gc.w", n);
+    CK(cudaMemcpyAsync(dx, x, n * d * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dw, w, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    GridSpec g{};
+    g.d = d;
+    g.cell = cell;
+    for (int k = 0; k < d; ++k) g.origin[k] = origin[k];  // center = 0: raw coordinates
+    DMeasure M;
+    prepare_measure(c, "gc", dx, dw, n, d, g, true, M);
+    CK(cudaMemcpyAsync(perm, M.perm, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(labels, M.labels, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(offsets, M.offsets, (M.k + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    std::vector<float4> cp(M.k);
+    CK(cudaMemcpyAsync(cp.data(), M.cpts, M.k * sizeof(float4), cudaMemcpyDeviceToHost, st));
+    if (cweights) CK(cudaMemcpyAsync(cweights, M.cw64, M.k * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (radii) CK(cudaMemcpyAsync(radii, M.radii, M.k * sizeof(float), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *k_out = M.k;
+    if (centroids)
+      for (int32_t I = 0; I < M.k; ++I) {
+        const float v[3] = {cp[I].x, cp[I].y, cp[I].z};
+        for (int k = 0; k < d; ++k) centroids[int64_t(I) * d + k] = v[k];
+      }
+  });
+}
+
+int msot_truncation_mask(msot_ctx* c, int64_t kx, int64_t ky, int d, const float* cx,
+                         const float* rx, const float* fx, const float* cy, const float* ry,
+                         const float* gy, double eps, double theta, double p, int self,
+                         uint8_t* mask_out) {
+  return guard([&] {
+    if (!c || !cx || !rx || !fx || !cy || !ry || !gy || !mask_out) raise(MSOT_EUSAGE, "null argument");
+    if (p != 2.0) raise(MSOT_EUSAGE, "the GPU path implements p = 2");
+    if (d < 1 || d > 3) raise(MSOT_EUSAGE, "D in 1..3");
+    if (kx < 1 || ky < 1) raise(MSOT_EDATA, "empty cluster set");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->st;
+    std::vector<float4> hx(kx), hy(ky);
+    for (int64_t I = 0; I < kx; ++I) {
+      float v[3] = {0, 0, 0};
+      for (int k = 0; k < d; ++k) v[k] = cx[I * d + k];
+      hx[I] = make_float4(v[0], v[1], v[2], 0.f);
+    }
+    for (int64_t J = 0; J < ky; ++J) {
+      float v[3] = {0, 0, 0};
+      for (int k = 0; k < d; ++k) v[k] = cy[J * d + k];
+      hy[J] = make_float4(v[0], v[1], v[2], 0.f);
+    }
+    float4* dcx = c->buf<float4>("tm.cx", kx);
+    float4* dcy = c->buf<float4>("tm.cy", ky);
+    float* drx = c->buf<float>("tm.rx", kx);
+    float* dfx = c->buf<float>("tm.fx", kx);
+    float* dry = c->buf<float>("tm.ry", ky);
+    float* dgy = c->buf<float>("tm.gy", ky);
+    uint8_t* dm = c->buf<uint8_t>("tm.m", kx * ky);
+    CK(cudaMemcpyAsync(dcx, hx.data(), kx * sizeof(float4), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dcy, hy.data(), ky * sizeof(float4), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(drx, rx, kx * sizeof(float), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dfx, fx, kx * sizeof(float), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dry, ry, ky * sizeof(float), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dgy, gy, ky * sizeof(float), cudaMemcpyHostToDevice, st));
+    CK(truncation_mask(static_cast<int32_t>(kx), static_cast<int32_t>(ky), d, dcx, drx, dfx, dcy,
+                       dry, dgy, eps, theta, self, dm, st));
+    CK(cudaMemcpyAsync(mask_out, dm, kx * ky, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,237 @@
+"""Python binding of the C ABI (include/msot_gpu.h) over ctypes.
+
+This is a thin harness for tests and the bench: every call goes through
+`libmsot_b200.so` (CUDA, sm_100a).  There is no CPU fallback — if the
+library or a GPU is missing the calls raise.
+
+Names mirror the reference operations of SPEC.md: `softmin` (:164),
+`symmetric_sinkhorn` / `multiscale_sinkhorn` (:174, :290), `divergence`
+(:194), `make_schedule` (:153), plus the north-star kernels
+`grid_cluster` and `kernel_truncation` (:280).
+"""
+import ctypes as C
+import math
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from .abi import Params, Stats, make_params, raise_status
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmsot_b200.so")
+_LIB = None
+
+_dp = C.POINTER(C.c_double)
+_fp = C.POINTER(C.c_float)
+_ip = C.POINTER(C.c_int32)
+_lp = C.POINTER(C.c_int64)
+_bp = C.POINTER(C.c_uint8)
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() — "
+                               "the solver has no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        L.msot_last_error.restype = C.c_char_p
+        L.msot_params_default.argtypes = [C.POINTER(Params)]
+        L.msot_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
+        L.msot_nccl_unique_id.argtypes = [C.c_char_p]
+        L.msot_create_dist.argtypes = [C.c_int, C.c_int, C.c_int, C.c_char_p,
+                                       C.POINTER(C.c_void_p)]
+        L.msot_destroy.argtypes = [C.c_void_p]
+        L.msot_destroy.restype = None
+        L.msot_set_profiling.argtypes = [C.c_void_p, C.c_int]
+        L.msot_schedule.argtypes = [C.c_double, C.POINTER(Params), _dp, _dp, _dp, C.c_int]
+        L.msot_shard_tiles.argtypes = [_dp, C.c_int64, C.c_int, _lp]
+        L.msot_softmin.argtypes = [C.c_void_p, _dp, C.c_int64, _dp, C.c_int64, C.c_int, _dp,
+                                   _dp, C.c_double, C.c_double, _dp, _dp]
+        L.msot_grid_cluster.argtypes = [C.c_void_p, _dp, _dp, C.c_int64, C.c_int, _dp,
+                                        C.c_double, _ip, _ip, _ip, _ip, _dp, _dp, _fp]
+        L.msot_truncation_mask.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int, _fp,
+                                           _fp, _fp, _fp, _fp, _fp, C.c_double, C.c_double,
+                                           C.c_double, C.c_int, _bp]
+        L.msot_sinkhorn.argtypes = [C.c_void_p, C.POINTER(Params), _dp, _dp, C.c_int64, _dp,
+                                    _dp, C.c_int64, C.c_int, _dp, _dp, _dp, _dp, _dp,
+                                    C.POINTER(Stats)]
+        L.msot_sinkhorn_device.argtypes = [C.c_void_p, C.POINTER(Params), C.c_void_p,
+                                           C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                           C.c_int64, C.c_int, _dp, C.POINTER(Stats)]
+        _LIB = L
+    return _LIB
+
+
+# Symbols include/msot_gpu.h declares (checked by the CPU test suite).
+EXPORTS = ["msot_last_error", "msot_params_default", "msot_create", "msot_nccl_unique_id",
+           "msot_create_dist", "msot_destroy", "msot_set_profiling", "msot_schedule",
+           "msot_shard_tiles", "msot_softmin", "msot_grid_cluster", "msot_truncation_mask",
+           "msot_sinkhorn", "msot_sinkhorn_device"]
+
+
+def _check(rc):
+    if rc != 0:
+        raise_status(rc, lib().msot_last_error().decode())
+
+
+def _c64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _d(a):
+    return a.ctypes.data_as(_dp)
+
+
+def default_params(**kw):
+    return make_params(**kw)
+
+
+def make_schedule(diameter, prm):
+    cap = 100000
+    s, e, l = (np.zeros(cap) for _ in range(3))
+    n = lib().msot_schedule(diameter, C.byref(prm), _d(s), _d(e), _d(l), cap)
+    return s[:n].copy(), e[:n].copy(), l[:n].copy()
+
+
+def shard_tiles(work, world):
+    w = _c64(work)
+    b = np.zeros(world + 1, np.int64)
+    _check(lib().msot_shard_tiles(_d(w), w.size, world, b.ctypes.data_as(_lp)))
+    return b
+
+
+@dataclass
+class DualPotentials:
+    """The four dual vectors of SPEC.md:137-140 (caller's atom order)."""
+
+    a_xx: np.ndarray
+    b_yy: np.ndarray
+    a_xy: np.ndarray
+    b_yx: np.ndarray
+    eps: float
+
+
+class Context:
+    """One GPU (one process per GPU; optional NCCL communicator)."""
+
+    def __init__(self, device=0, rank=0, world=1, nccl_id=None):
+        self._h = C.c_void_p()
+        if world > 1:
+            if nccl_id is None or len(nccl_id) != 128:
+                raise ValueError("world > 1 needs the 128-byte NCCL id of rank 0")
+            _check(lib().msot_create_dist(device, rank, world, bytes(nccl_id), C.byref(self._h)))
+        else:
+            _check(lib().msot_create(device, C.byref(self._h)))
+        self.rank, self.world = rank, world
+
+    @staticmethod
+    def nccl_unique_id():
+        buf = C.create_string_buffer(128)
+        _check(lib().msot_nccl_unique_id(buf))
+        return buf.raw
+
+    def close(self):
+        if self._h:
+            lib().msot_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_profiling(self, on=True):
+        _check(lib().msot_set_profiling(self._h, int(bool(on))))
+
+    # -- SPEC.md:164-172
+    def softmin(self, x, y, logw, h, eps, lam=1.0, f_est=None):
+        x, y, logw, h = _c64(x), _c64(y), _c64(logw), _c64(h)
+        if x.ndim == 1:
+            x = x[:, None]
+        if y.ndim == 1:
+            y = y[:, None]
+        n, d = x.shape
+        out = np.zeros(n)
+        fe = None if f_est is None else _d(_c64(f_est))
+        _check(lib().msot_softmin(self._h, _d(x), n, _d(y), y.shape[0], d, _d(logw), _d(h),
+                                  eps, lam, fe, _d(out)))
+        return out
+
+    # -- voxel-grid clustering (K2)
+    def grid_cluster(self, x, w, origin, cell):
+        x, w, origin = _c64(x), _c64(w), _c64(origin)
+        n, d = x.shape
+        perm = np.zeros(n, np.int32)
+        labels = np.zeros(n, np.int32)
+        offsets = np.zeros(n + 1, np.int32)
+        k = C.c_int32()
+        cen = np.zeros((n, d))
+        cw = np.zeros(n)
+        rad = np.zeros(n, np.float32)
+        _check(lib().msot_grid_cluster(self._h, _d(x), _d(w), n, d, _d(origin), cell,
+                                       perm.ctypes.data_as(_ip), labels.ctypes.data_as(_ip),
+                                       offsets.ctypes.data_as(_ip), C.byref(k), _d(cen),
+                                       _d(cw), rad.ctypes.data_as(_fp)))
+        K = k.value
+        return dict(perm=perm, labels=labels, offsets=offsets[:K + 1].copy(), k=K,
+                    centroids=cen[:K].copy(), cweights=cw[:K].copy(), radii=rad[:K].copy())
+
+    # -- kernel_truncation on explicit coarse inputs (K3)
+    def kernel_truncation(self, cx, rx, fx, cy, ry, gy, eps, theta, self_=False):
+        f32 = lambda a: np.ascontiguousarray(a, dtype=np.float32)
+        cx, rx, fx, cy, ry, gy = map(f32, (cx, rx, fx, cy, ry, gy))
+        kx, d = cx.shape
+        ky = cy.shape[0]
+        out = np.zeros((kx, ky), np.uint8)
+        fp = lambda a: a.ctypes.data_as(_fp)
+        _check(lib().msot_truncation_mask(self._h, kx, ky, d, fp(cx), fp(rx), fp(fx), fp(cy),
+                                          fp(ry), fp(gy), eps, theta, 2.0, int(self_),
+                                          out.ctypes.data_as(_bp)))
+        return out
+
+    # -- symmetric_sinkhorn / multiscale_sinkhorn + divergence
+    def sinkhorn(self, prm, x, a, y, b, potentials=True):
+        x, a, y, b = _c64(x), _c64(a), _c64(y), _c64(b)
+        if x.ndim == 1:
+            x = x[:, None]
+        if y.ndim == 1:
+            y = y[:, None]
+        n, d = x.shape
+        m = y.shape[0]
+        if y.shape[1] != d:
+            from .abi import DataError
+            raise DataError("dimension mismatch")
+        loss = C.c_double()
+        st = Stats()
+        pots = None
+        ptrs = [None] * 4
+        if potentials:
+            pots = [np.zeros(n), np.zeros(m), np.zeros(m), np.zeros(n)]
+            ptrs = [_d(p) for p in pots]
+        _check(lib().msot_sinkhorn(self._h, C.byref(prm), _d(x), _d(a), n, _d(y), _d(b), m, d,
+                                   *ptrs, C.byref(loss), C.byref(st)))
+        duals = None
+        if potentials:
+            s, e, _ = make_schedule(st.diameter, prm)
+            duals = DualPotentials(*pots, eps=float(e[-1]))
+        return loss.value, duals, st.as_dict()
+
+    def sinkhorn_device(self, prm, x_ptr, a_ptr, n, y_ptr, b_ptr, m, d):
+        """Inputs already resident in HBM (float64 device pointers)."""
+        loss = C.c_double()
+        st = Stats()
+        _check(lib().msot_sinkhorn_device(self._h, C.byref(prm), x_ptr, a_ptr, n, y_ptr, b_ptr,
+                                          m, d, C.byref(loss), C.byref(st)))
+        return loss.value, st.as_dict()
+
+    def divergence(self, x, a, y, b, blur=0.05, reach=math.inf, scaling=0.9, multiscale=False,
+                   **kw):
+        prm = make_params(blur=blur, reach=reach, scaling=scaling, multiscale=multiscale, **kw)
+        return self.sinkhorn(prm, x, a, y, b, potentials=False)[0]
+
+
+def params_struct(**kw):
+    return make_params(**kw)

@@ -1,0 +1,239 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the FP64
+oracle on identical seeded inputs.
+
+Contract (BASELINE.json north star):
+  cluster labels / sort permutations / truncation masks  bit-exact
+  potentials                                             |gpu - oracle| <= 1e-3 * eps
+  loss                                                   |gpu - oracle| <= 1e-4 * |oracle|
+"""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2107_02010_b200.abi import DataError, UsageError, make_params
+
+pytestmark = pytest.mark.gpu
+
+POT_TOL = 1e-3   # x eps
+LOSS_TOL = 1e-4  # relative
+
+
+def mixture(n, seed, d=3, k=8, sigma=0.05):
+    """SURVEY.md §8d C2/C3 generator: k Gaussian components, centres in
+    U[0.2, 0.8]^d."""
+    rng = np.random.default_rng(seed)
+    cen = rng.uniform(0.2, 0.8, (k, d))
+    lab = rng.integers(0, k, n)
+    return cen[lab] + rng.normal(0, sigma, (n, d))
+
+
+def uniform(n, seed, d=3):
+    return np.random.default_rng(seed).random((n, d))
+
+
+def check_pots(gpu, orc, eps):
+    for name, g in zip(("a_xx", "b_yy", "a_xy", "b_yx"),
+                       (gpu.a_xx, gpu.b_yy, gpu.a_xy, gpu.b_yx)):
+        err = np.abs(g - orc[name]).max()
+        assert err <= POT_TOL * eps, f"{name}: {err / eps:.3e} eps"
+
+
+# ---------------------------------------------------------------- softmin
+@pytest.mark.parametrize("d", [1, 2, 3])
+@pytest.mark.parametrize("eps", [1.0, 1e-2, 1e-4])
+def test_softmin_matches_oracle(ctx, oracle, d, eps):
+    rng = np.random.default_rng(d * 7 + int(-math.log10(eps)))
+    n, m = 1000, 1500
+    x, y = rng.random((n, d)), rng.random((m, d))
+    logw = np.log(rng.random(m) + 0.1)
+    logw -= np.log(np.exp(logw).sum())
+    h = 0.05 * rng.standard_normal(m)
+    ref = oracle.softmin(x, y, logw, h, eps, 0.8)
+    # expanded around a perturbed reference, around zero, and around a bad
+    # reference that forces the exact fallback path
+    for est in (ref + 0.3 * eps, None, ref + 500.0 * eps):
+        got = ctx.softmin(x, y, logw, h, eps, 0.8, f_est=est)
+        assert np.abs(got - ref).max() <= POT_TOL * eps
+
+
+def test_softmin_spec_examples(ctx):
+    """SPEC.md:170-172 through the GPU kernel."""
+    f = ctx.softmin(np.zeros((1, 1)), np.array([[1.5]]), np.zeros(1), np.zeros(1), 0.3)
+    assert abs(f[0] - 1.125) <= 1e-6
+    f = ctx.softmin(np.zeros((1, 1)), np.array([[1.0], [-1.0]]), np.log([0.5, 0.5]),
+                    np.zeros(2), 0.2)
+    assert abs(f[0] - 0.5) <= 1e-6
+    f = ctx.softmin(np.zeros((1, 1)), np.array([[0.0], [math.sqrt(200)]]), np.zeros(2),
+                    np.zeros(2), 1e-3)
+    assert abs(f[0]) <= 1e-6
+
+
+# ------------------------------------------------------------- clustering
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_grid_cluster_bit_exact(ctx, oracle, d):
+    x = mixture(50000, 11 + d, d=d)
+    w = np.random.default_rng(d).random(50000) + 0.5
+    origin = x.min(0)
+    cell = 0.03
+    g = ctx.grid_cluster(x, w, origin, cell)
+    o = oracle.grid_cluster(x, w, origin, cell)
+    assert g["k"] == o["k"]
+    np.testing.assert_array_equal(g["perm"], o["perm"])
+    np.testing.assert_array_equal(g["labels"], o["labels"])
+    np.testing.assert_array_equal(g["offsets"], o["offsets"])
+    np.testing.assert_allclose(g["cweights"], o["cweights"], rtol=1e-12)
+    np.testing.assert_allclose(g["centroids"], o["centroids"], atol=1e-6)
+
+
+def test_grid_cluster_ties_and_edges(ctx, oracle):
+    """Duplicate atoms (stable order) and atoms exactly on cell faces."""
+    x = np.repeat(np.array([[0.0, 0.0, 0.0], [0.5, 0.25, 0.75], [0.25, 0.5, 0.0]]), 700, axis=0)
+    x = np.concatenate([x, np.random.default_rng(3).integers(0, 9, (3000, 3)) * 0.125])
+    w = np.full(len(x), 1.0)
+    g = ctx.grid_cluster(x, w, np.zeros(3), 0.125)
+    o = oracle.grid_cluster(x, w, np.zeros(3), 0.125)
+    np.testing.assert_array_equal(g["perm"], o["perm"])
+    np.testing.assert_array_equal(g["offsets"], o["offsets"])
+
+
+# ------------------------------------------------------------------- mask
+@pytest.mark.parametrize("self_", [False, True])
+def test_truncation_mask_bit_exact(ctx, oracle, self_):
+    rng = np.random.default_rng(5)
+    kx, ky = 700, 600 if not self_ else 700
+    cx = rng.random((kx, 3)).astype(np.float32)
+    cy = cx if self_ else rng.random((ky, 3)).astype(np.float32)
+    rx = (rng.random(kx) * 0.05).astype(np.float32)
+    ry = rx if self_ else (rng.random(ky) * 0.05).astype(np.float32)
+    fx = (rng.random(kx) * 0.01).astype(np.float32)
+    gy = fx if self_ else (rng.random(ky) * 0.01).astype(np.float32)
+    for eps, theta in ((1e-3, 20.0), (1e-4, 5.0), (0.05, 1.0)):
+        g = ctx.kernel_truncation(cx, rx, fx, cy, ry, gy, eps, theta, self_=self_)
+        o = oracle.truncation_mask(cx, rx, fx, cy, ry, gy, eps, theta, self_=self_)
+        np.testing.assert_array_equal(g, o)
+        assert 0 < g.mean() < 1
+    # exact ties: identical centroids -> best pair must go to the lowest index
+    cx2 = np.zeros((5, 3), np.float32)
+    cy2 = np.ones((4, 3), np.float32) * 10
+    z5, z4 = np.zeros(5, np.float32), np.zeros(4, np.float32)
+    g = ctx.kernel_truncation(cx2, z5, z5, cy2, z4, z4, 1e-4, 1.0)
+    o = oracle.truncation_mask(cx2, z5, z5, cy2, z4, z4, 1e-4, 1.0)
+    np.testing.assert_array_equal(g, o)
+
+
+# --------------------------------------------------------- full solves
+def run_both(ctx, oracle, prm, x, a, y, b):
+    lg, pg, sg = ctx.sinkhorn(prm, x, a, y, b)
+    lo, po, so = oracle.sinkhorn(prm, x, a, y, b)
+    return lg, pg, sg, lo, po, so
+
+
+@pytest.mark.parametrize("reach", [math.inf, 0.3])
+def test_dense_sinkhorn_parity(ctx, oracle, reach):
+    """Config-1 shape at oracle-friendly size: uniform 3D, blur 0.05."""
+    n, m = 2000, 1800
+    x, y = uniform(n, 1), uniform(m, 2) * 0.9 + 0.05
+    a, b = np.full(n, 1 / n), np.full(m, 1 / m)
+    prm = make_params(blur=0.05, reach=reach)
+    lg, pg, sg, lo, po, so = run_both(ctx, oracle, prm, x, a, y, b)
+    assert sg["n_scales"] == so["n_scales"]
+    check_pots(pg, po, 0.05 ** 2)
+    assert abs(lg - lo) <= LOSS_TOL * abs(lo), (lg, lo)
+    assert sg["fallback_rows"] == 0
+
+
+def test_dense_sinkhorn_small_blur(ctx, oracle):
+    """blur = 0.01 (eps = 1e-4): the 1e-3 eps potential tolerance is 1e-7 absolute."""
+    n = 1500
+    x, y = mixture(n, 3), mixture(n, 4)
+    a = np.random.default_rng(0).random(n) + 0.5
+    a /= a.sum()
+    b = np.full(n, 1 / n)
+    prm = make_params(blur=0.01)
+    lg, pg, sg, lo, po, so = run_both(ctx, oracle, prm, x, a, y, b)
+    check_pots(pg, po, 1e-4)
+    assert abs(lg - lo) <= LOSS_TOL * abs(lo), (lg, lo)
+
+
+@pytest.mark.parametrize("d", [1, 2])
+def test_dense_low_dim(ctx, oracle, d):
+    n = 700
+    x, y = uniform(n, 5, d), uniform(n + 13, 6, d)
+    a, b = np.full(n, 1 / n), np.full(n + 13, 1 / (n + 13))
+    prm = make_params(blur=0.02)
+    lg, pg, sg, lo, po, so = run_both(ctx, oracle, prm, x, a, y, b)
+    check_pots(pg, po, 0.02 ** 2)
+    assert abs(lg - lo) <= LOSS_TOL * abs(lo)
+
+
+@pytest.mark.parametrize("retruncate", [0, 1])
+def test_multiscale_parity(ctx, oracle, retruncate):
+    """Config-2 shape (Gaussian mixtures, voxel grid, truncation) at a size
+    the oracle finishes in seconds."""
+    n = 6000
+    x, y = mixture(n, 3), mixture(n, 4)
+    a, b = np.full(n, 1 / n), np.full(n, 1 / n)
+    prm = make_params(blur=0.01, multiscale=True, retruncate=retruncate, cluster_scale=0.04)
+    lg, pg, sg, lo, po, so = run_both(ctx, oracle, prm, x, a, y, b)
+    assert (sg["kx"], sg["ky"], sg["t_switch"]) == (so["kx"], so["ky"], so["t_switch"])
+    assert sg["pairs_fine"] < sg["pairs_fine_dense"]
+    check_pots(pg, po, 1e-4)
+    assert abs(lg - lo) <= LOSS_TOL * abs(lo), (lg, lo)
+
+
+def test_multiscale_close_to_dense(ctx):
+    """SPEC.md:303 on the GPU: multiscale vs dense < 1e-3 relative."""
+    n = 20000
+    x, y = mixture(n, 5), mixture(n, 6)
+    a = np.full(n, 1 / n)
+    ld, _, _ = ctx.sinkhorn(make_params(blur=0.01), x, a, y, a, potentials=False)
+    lm, _, st = ctx.sinkhorn(make_params(blur=0.01, multiscale=True), x, a, y, a,
+                             potentials=False)
+    assert abs(lm - ld) <= 1e-3 * abs(ld)
+    assert st["pairs_fine"] < 0.5 * st["pairs_fine_dense"]
+
+
+def test_two_blobs_10k(ctx):
+    """SPEC.md:298 / acceptance 4 (:590): 10k two-blob data, the block-sparse
+    phase evaluates < 50% of the pairs and matches dense within 1e-3."""
+    rng = np.random.default_rng(7)
+    n = 10000
+    x = np.concatenate([rng.normal(0, 0.03, (n // 2, 3)), rng.normal(1, 0.03, (n // 2, 3))])
+    y = np.concatenate([rng.normal(0.02, 0.03, (n // 2, 3)),
+                        rng.normal(1.02, 0.03, (n // 2, 3))])
+    a = np.full(n, 1 / n)
+    ld, _, _ = ctx.sinkhorn(make_params(blur=0.01), x, a, y, a, potentials=False)
+    lm, _, st = ctx.sinkhorn(make_params(blur=0.01, multiscale=True, retruncate=1), x, a, y, a,
+                             potentials=False)
+    assert st["pairs_fine"] < 0.5 * st["pairs_fine_dense"]
+    assert abs(lm - ld) <= 1e-3 * abs(ld)
+
+
+def test_identical_measures_zero(ctx):
+    """SPEC.md:200 / acceptance 2: S(a, a) ~ 0 and symmetric potentials."""
+    x = mixture(3000, 9)
+    a = np.full(3000, 1 / 3000)
+    loss, P, _ = ctx.sinkhorn(make_params(blur=0.02), x, a, x, a)
+    assert abs(loss) <= 1e-9 + 1e-6 * 0.02 ** 2
+    np.testing.assert_array_equal(P.a_xx, P.b_yy)
+    np.testing.assert_array_equal(P.a_xy, P.b_yx)
+
+
+def test_dirac_translation(ctx):
+    """Dirac translation -> |t|^2 / 2 within 1%."""
+    loss, _, _ = ctx.sinkhorn(make_params(blur=0.01), np.zeros((1, 3)), np.ones(1),
+                              np.array([[1.0, 0.5, 0.0]]), np.ones(1))
+    assert abs(loss - 0.625) <= 6.25e-3
+
+
+def test_errors(ctx):
+    x = np.zeros((3, 3))
+    with pytest.raises(DataError):
+        ctx.sinkhorn(make_params(), x, np.array([1.0, 0.0, 1.0]), x, np.ones(3))
+    with pytest.raises(UsageError):
+        ctx.sinkhorn(make_params(p=1.0), x, np.ones(3), x, np.ones(3))
+    with pytest.raises(UsageError):
+        ctx.sinkhorn(make_params(scaling=1.5), x, np.ones(3), x, np.ones(3))
+    with pytest.raises(UsageError):
+        ctx.sinkhorn(make_params(), np.zeros((3, 5)), np.ones(3), np.zeros((3, 5)), np.ones(3))

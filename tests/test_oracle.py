@@ -1,0 +1,254 @@
+"""CPU tests: pin the FP64 oracle against the SPEC known answers (golden
+vectors in tests/golden/spec_golden.json) and the SPEC invariants.
+
+Mirrors the per-op examples of SPEC.md (schedule :159-162, softmin :170-172,
+symmetric loop :180-182, divergence :200-202, :215-218, multiscale :296-303,
+truncation :286-288) and acceptance criteria 1, 2, 4, 5 (:587-591).
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from paper_2107_02010_b200.abi import make_params
+
+GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_golden.json")))
+
+
+@pytest.mark.parametrize("case", GOLDEN["schedule"], ids=lambda c: c["cite"])
+def test_schedule_golden(oracle, case):
+    prm = make_params(blur=case["blur"], scaling=case["q"], p=case["p"],
+                      reach=case.get("reach", math.inf))
+    s, e, l = oracle.schedule(case["d"], prm)
+    if "sigma" in case:
+        np.testing.assert_allclose(s, case["sigma"], rtol=0, atol=1e-12)
+    if "eps" in case:
+        np.testing.assert_allclose(e, case["eps"], rtol=1e-15)
+    if "lam" in case:
+        np.testing.assert_allclose(l, case["lam"], rtol=1e-15)
+    if "len" in case:
+        assert len(s) == case["len"]
+
+
+def test_schedule_ceiling_random(oracle):
+    """Acceptance 5: length = ceil(log(d/blur)/log(1/q))."""
+    rng = np.random.default_rng(5)
+    for _ in range(100):
+        blur = 10 ** rng.uniform(-3, 0)
+        d = blur * 10 ** rng.uniform(0.01, 3)
+        q = rng.uniform(0.3, 0.95)
+        s, _, _ = oracle.schedule(d, make_params(blur=blur, scaling=q))
+        assert len(s) == math.ceil(math.log(d / blur) / math.log(1 / q))
+        assert s[-1] == blur and (len(s) == 1 or s[0] == d)
+
+
+@pytest.mark.parametrize("case", GOLDEN["softmin"], ids=lambda c: c["cite"])
+def test_softmin_golden(oracle, case):
+    f = oracle.softmin(np.array(case["x"]), np.array(case["y"]), np.log(case["w"]),
+                       np.array(case["h"]), case["eps"])
+    np.testing.assert_allclose(f, case["f"], rtol=1e-12, atol=case.get("atol", 1e-12))
+
+
+def test_softmin_dynamic_range(oracle):
+    """exact on exponents up to e^{+-300} (vs a float128-ish
+    reference computed with mpmath-free log-sum-exp in numpy longdouble)."""
+    rng = np.random.default_rng(1)
+    y = rng.random((50, 1)) * 30
+    h = rng.random(50) * 300
+    eps = 1.0
+    f = oracle.softmin(np.zeros((1, 1)), y, np.zeros(50), h, eps)
+    z = (h.astype(np.longdouble) - 0.5 * y[:, 0].astype(np.longdouble) ** 2) / eps
+    m = z.max()
+    ref = -eps * (m + np.log(np.exp(z - m).sum()))
+    assert abs(f[0] - float(ref)) <= 1e-12 * abs(float(ref))
+
+
+@pytest.mark.parametrize("case", GOLDEN["divergence"], ids=lambda c: c["cite"])
+def test_divergence_golden(oracle, case):
+    prm = make_params(blur=case["blur"])
+    loss, _, _ = oracle.sinkhorn(prm, np.array(case["x"]), np.array(case["a"]),
+                                 np.array(case["y"]), np.array(case["b"]))
+    assert abs(loss - case["value"]) <= case["rtol"] * abs(case["value"])
+
+
+@pytest.mark.parametrize("k", range(21))
+def test_exact_ot_agreement(oracle, k):
+    """Acceptance 1 against exact OT (scipy assignment)."""
+    case = GOLDEN["exact_ot"][k]
+    x, y = np.array(case["x"]), np.array(case["y"])
+    a = np.full(len(x), 1.0 / len(x))
+    b = np.full(len(y), 1.0 / len(y))
+    loss, _, _ = oracle.sinkhorn(make_params(blur=case["blur"], scaling=case["scaling"]), x, a,
+                                 y, b)
+    assert abs(loss - case["value"]) <= case["rtol"] * case["value"]
+
+
+def test_dirac_fixed_point(oracle):
+    """alpha = beta = unit Dirac -> all potentials 0."""
+    x = np.zeros((1, 3))
+    _, P, _ = oracle.sinkhorn(make_params(blur=0.1), x, np.ones(1), x, np.ones(1))
+    for v in P.values():
+        assert np.all(np.abs(v) < 1e-14)
+
+
+def test_symmetry_and_definiteness(oracle):
+    """SPEC.md:181, :200, :215-216; acceptance 2 (:588)."""
+    rng = np.random.default_rng(2)
+    x = rng.random((40, 2))
+    a = rng.random(40) + 0.1
+    a /= a.sum()
+    prm = make_params(blur=0.05)
+    loss, P, _ = oracle.sinkhorn(prm, x, a, x, a)
+    np.testing.assert_allclose(P["a_xx"], P["b_yy"], rtol=0, atol=1e-13)
+    np.testing.assert_allclose(P["a_xy"], P["b_yx"], rtol=0, atol=1e-13)
+    assert abs(loss) <= 1e-9
+    y = rng.random((30, 2)) + 0.2
+    b = np.full(30, 1 / 30)
+    l1, _, _ = oracle.sinkhorn(prm, x, a, y, b)
+    l2, _, _ = oracle.sinkhorn(prm, y, b, x, a)
+    assert l1 > 0
+    assert abs(l1 - l2) <= 1e-6 * abs(l1)
+
+
+def test_positivity_random(oracle):
+    """Acceptance 2: divergence >= -1e-9 on random pairs."""
+    rng = np.random.default_rng(3)
+    for _ in range(10):
+        n, m = rng.integers(3, 20, 2)
+        x, y = rng.random((n, 2)), rng.random((m, 2))
+        a, b = rng.random(n) + 0.1, rng.random(m) + 0.1
+        a, b = a / a.sum(), b / b.sum()
+        loss, _, _ = oracle.sinkhorn(make_params(blur=0.1), x, a, y, b)
+        assert loss >= -1e-9
+
+
+def test_marginals(oracle):
+    """implicit-plan row sums match alpha within 1e-3."""
+    rng = np.random.default_rng(4)
+    x, y = rng.random((10, 2)), rng.random((10, 2))
+    a = np.full(10, 0.1)
+    lo, hi = np.minimum(x.min(0), y.min(0)), np.maximum(x.max(0), y.max(0))
+    d = np.sqrt(((hi - lo) ** 2).sum())
+    prm = make_params(blur=0.01 * d)
+    _, P, _ = oracle.sinkhorn(prm, x, a, y, a)
+    eps = (0.01 * d) ** 2
+    C = 0.5 * ((x[:, None] - y[None]) ** 2).sum(-1)
+    plan = a[:, None] * a[None, :] * np.exp((P["b_yx"][:, None] + P["a_xy"][None, :] - C) / eps)
+    np.testing.assert_allclose(plan.sum(1), a, rtol=1e-3)
+
+
+def test_unbalanced_outlier(oracle):
+    """SPEC.md:212 / acceptance 10 (:596): an atom 10 reach away keeps a
+    row mass < 1e-3 alpha_i."""
+    x = np.array([[0.0, 0.0], [0.1, 0.0], [10.0, 0.0]])
+    y = np.array([[0.0, 0.05], [0.1, 0.05]])
+    a = np.full(3, 1 / 3)
+    b = np.full(2, 1 / 2)
+    reach = 1.0
+    prm = make_params(blur=0.05, reach=reach)
+    _, P, _ = oracle.sinkhorn(prm, x, a, y, b)
+    eps = 0.05 ** 2
+    C = 0.5 * ((x[:, None] - y[None]) ** 2).sum(-1)
+    plan = a[:, None] * b[None, :] * np.exp((P["b_yx"][:, None] + P["a_xy"][None, :] - C) / eps)
+    assert plan[2].sum() < 1e-3 * a[2]
+
+
+def test_multiscale_matches_dense(oracle):
+    """SPEC.md:293, :303 (acceptance 4): dense vs multiscale < 1e-3 rel."""
+    rng = np.random.default_rng(6)
+    for n in (300, 800):
+        x = rng.random((n, 3))
+        y = rng.random((n, 3)) * 0.7 + 0.2
+        a = np.full(n, 1 / n)
+        base = dict(blur=0.03)
+        ld, _, _ = oracle.sinkhorn(make_params(**base), x, a, y, a)
+        lm, _, st = oracle.sinkhorn(make_params(multiscale=True, cluster_scale=0.15, **base), x,
+                                    a, y, a)
+        assert st["t_switch"] > 0 and st["kx"] > 1
+        assert abs(lm - ld) <= 1e-3 * abs(ld)
+
+
+def test_multiscale_two_blobs_prunes(oracle):
+    """SPEC.md:298 / :590: two-blob data -> the block-sparse phase drops the
+    cross-blob half of the pairs.  (SPEC's "< 50%" is stated for 10k atoms;
+    at 1k atoms the rigorous radius margin keeps each blob dense, so the
+    bound here is the cross-blob half plus a margin; the 10k case runs on
+    the GPU in tests/test_gpu_parity.py.)"""
+    rng = np.random.default_rng(7)
+    n = 1000
+    x = np.concatenate([rng.normal(0, 0.03, (n // 2, 3)), rng.normal(1, 0.03, (n // 2, 3))])
+    y = np.concatenate([rng.normal(0.02, 0.03, (n // 2, 3)), rng.normal(1.02, 0.03, (n // 2, 3))])
+    a = np.full(n, 1 / n)
+    prm = make_params(blur=0.01, multiscale=True, cluster_scale=0.02, theta=5.0, retruncate=1)
+    lm, _, st = oracle.sinkhorn(prm, x, a, y, a)
+    ld, _, _ = oracle.sinkhorn(make_params(blur=0.01), x, a, y, a)
+    assert st["pairs_fine"] < 0.6 * st["pairs_fine_dense"]
+    assert abs(lm - ld) <= 1e-3 * abs(ld)
+
+
+def test_grid_cluster_invariants(oracle):
+    """ClusterTree invariants."""
+    rng = np.random.default_rng(8)
+    x = rng.random((500, 3))
+    w = rng.random(500) + 0.5
+    c = oracle.grid_cluster(x, w, np.zeros(3), 0.2)
+    assert sorted(c["perm"].tolist()) == list(range(500))
+    assert c["offsets"][0] == 0 and c["offsets"][-1] == 500
+    assert np.all(np.diff(c["offsets"]) > 0)
+    assert abs(c["cweights"].sum() - w.sum()) <= 1e-12 * w.sum()
+    cells = np.floor(x / 0.2).astype(int)
+    for I in range(c["k"]):
+        mem = c["perm"][c["offsets"][I]:c["offsets"][I + 1]]
+        assert len({tuple(v) for v in cells[mem]}) == 1
+        assert np.all(c["labels"][c["offsets"][I]:c["offsets"][I + 1]] == I)
+        cen = (w[mem, None] * x[mem]).sum(0) / w[mem].sum()
+        np.testing.assert_allclose(c["centroids"][I], cen, rtol=1e-12)
+        r = np.sqrt(((x[mem] - cen) ** 2).sum(1)).max()
+        assert c["radii"][I] >= r and c["radii"][I] <= r * (1 + 1e-6) + 1e-30
+    # stable: ties keep the original order
+    for I in range(c["k"]):
+        mem = c["perm"][c["offsets"][I]:c["offsets"][I + 1]]
+        assert np.all(np.diff(mem) > 0)
+
+
+def test_truncation_properties(oracle):
+    """theta=inf keeps all; alpha=beta keeps the diagonal;
+    no empty rows/columns (:256)."""
+    rng = np.random.default_rng(9)
+    cx = rng.random((30, 3)).astype(np.float32)
+    rx = np.full(30, 0.05, np.float32)
+    f = (rng.random(30) * 0.01).astype(np.float32)
+    m = oracle.truncation_mask(cx, rx, f, cx, rx, f, 1e-4, math.inf, self_=True)
+    assert m.all()
+    m = oracle.truncation_mask(cx, rx, f, cx, rx, f, 1e-4, 5.0, self_=True)
+    assert np.all(np.diag(m) == 1)
+    cy = (rng.random((20, 3)) + 3).astype(np.float32)
+    ry = np.full(20, 0.05, np.float32)
+    g = np.zeros(20, np.float32)
+    m = oracle.truncation_mask(cx, rx, f, cy, ry, g, 1e-4, 5.0)
+    assert m.any(1).all() and m.any(0).all()
+
+
+def test_tile_ranges(oracle):
+    labels = np.repeat(np.arange(6), [100, 200, 50, 300, 10, 100]).astype(np.int32)
+    co = np.array([0, 40, 90, 100, 180, 200], np.int32)
+    mask = np.zeros((6, 5), np.uint8)
+    mask[0, [0, 1]] = 1
+    mask[1, [3]] = 1
+    mask[2, [1, 4]] = 1
+    mask[3, [0]] = 1
+    mask[4, [2, 3]] = 1
+    mask[5, [4]] = 1
+    ro = np.array([0, 100, 300, 350, 650, 660, 760], np.int32)
+    ts, ptr, rg = oracle.tile_ranges(labels, ro, co, mask)
+    # cluster-aligned tiles: {0} (100; +200 > 256), {1,2} (250), {3} split in
+    # 2 (300 > 256), {4,5} (110)
+    assert ts.tolist() == [0, 100, 350, 500, 650, 760]
+    # tile 0: cluster 0 -> cols {0,1}; tile 1: clusters 1,2 -> {1,3,4}
+    assert ptr.tolist() == [0, 1, 3, 4, 5, 6]
+    assert rg[0].tolist() == [0, 90]
+    assert rg[1:3].tolist() == [[40, 90], [100, 200]]
+    assert rg[3].tolist() == [0, 40] and rg[4].tolist() == [0, 40]
+    assert rg[5].tolist() == [90, 200]

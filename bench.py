@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""Benchmark: seconds to S_eps for 1M vs 1M 3D points (BASELINE.json metric,
+configs[2] = C3), one JSON line on rank 0.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...     (one process per GPU)
+
+A step is one full multiscale Sinkhorn divergence S_eps (clustering, coarse
+phase, extrapolation, block-sparse fine phase with per-scale truncation,
+loss) on N=M=1e6 Gaussian-mixture points (SURVEY.md §8d C3 generator, seeds
+5/6), blur=0.01, reach=inf, q=0.9.  `value` = device time of one solve with
+the inputs resident in HBM (max over ranks, CUDA events on the solver's
+stream); `e2e` = the same solve through the public host-buffer C ABI call
+(msot_sinkhorn) with pinned inputs: H2D copy + solve + loss D2H.
+--impl reference times the FP64 CPU oracle (the reference's Sinkhorn is
+specified only in prose) on a bounded sample and
+extrapolates to the workload's evaluated-pair count.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+WORKLOAD = dict(workload="C3: S_eps 1M vs 1M 3D Gaussian mixtures (8 comps, sigma 0.05), "
+                         "multiscale voxel grid + per-scale kernel truncation",
+                n=1_000_000, m=1_000_000, d=3, blur=0.01, reach="inf", scaling=0.9, theta=20.0,
+                retruncate=1, seeds=[5, 6])
+METRIC = "sec to S_eps, 1M vs 1M 3D pts at 1/2/4/8 GPU; softmin pairs/sec vs roofline"
+PAIRS_FILE = os.path.join(ROOT, "profiles", "c3_workload.json")
+
+
+def mixture(n, seed, d=3, k=8, sigma=0.05):
+    rng = np.random.default_rng(seed)
+    cen = rng.uniform(0.2, 0.8, (k, d))
+    return cen[rng.integers(0, k, n)] + rng.normal(0, sigma, (n, d))
+
+
+def make_inputs(w):
+    x = mixture(w["n"], w["seeds"][0], w["d"])
+    y = mixture(w["m"], w["seeds"][1], w["d"])
+    a = np.full(w["n"], 1.0 / w["n"])
+    b = np.full(w["m"], 1.0 / w["m"])
+    return x, a, y, b
+
+
+def params(w):
+    from paper_2107_02010_b200.abi import make_params
+    return make_params(blur=w["blur"], reach=math.inf, scaling=w["scaling"], multiscale=True,
+                       retruncate=w["retruncate"], theta=w["theta"])
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu, self.rows, self._stop = gpu, [], threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if len(r) > 3 + k and r[3 + k].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm)}
+
+
+def cpu_sample(x, y, b, eps, rows, threads=None):
+    """Times the FP64 oracle softmin (the CPU restatement on the reference's
+    own thread pool) on `rows` rows against all columns: returns pairs/s."""
+    from oracle import oracle as O  # CPU baseline only
+    if threads:
+        O.set_threads(threads)
+    h = np.zeros(len(y))
+    logw = np.log(b)
+    t = time.perf_counter()
+    O.softmin(x[:rows], y, logw, h, eps)
+    dt = time.perf_counter() - t
+    return rows * len(y) / dt, dt, O.threads()
+
+
+def l2_flush(buf):
+    if buf is not None:
+        buf.add_(1.0)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=None, help="override N=M (dev only)")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    args = ap.parse_args()
+
+    w = dict(WORKLOAD)
+    if args.n:
+        w["n"] = w["m"] = args.n
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return run_reference(args, w, rank)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2107_02010_b200.solver import Context
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("gloo")
+        idbuf = [Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(idbuf, src=0)
+        ctx = Context(local, rank, world, idbuf[0])
+    else:
+        ctx = Context(local)
+
+    x, a, y, b = make_inputs(w)
+    prm = params(w)
+    dev = torch.device("cuda", local)
+    tx = torch.from_numpy(x).to(dev)
+    ta = torch.from_numpy(a).to(dev)
+    ty = torch.from_numpy(y).to(dev)
+    tb = torch.from_numpy(b).to(dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def solve():
+        return ctx.sinkhorn_device(prm, tx.data_ptr(), ta.data_ptr(), w["n"], ty.data_ptr(),
+                                   tb.data_ptr(), w["m"], w["d"])
+
+    for _ in range(max(args.warmup, 0)):
+        solve()
+    times, launches, loss, st = [], 0, None, None
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            l2_flush(flush)
+            barrier()
+            loss, st = solve()
+            barrier()
+            times.append(st["total_ms"])
+            launches += st["gpu_launches"]
+    t_local = torch.tensor(times, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    ms = float(t_local.mean())
+
+    # e2e: public host-buffer call with pinned inputs, H2D + solve + loss D2H
+    px = torch.from_numpy(x).pin_memory()
+    pa = torch.from_numpy(a).pin_memory()
+    py = torch.from_numpy(y).pin_memory()
+    pb = torch.from_numpy(b).pin_memory()
+    import ctypes as C
+    from paper_2107_02010_b200.abi import Stats
+    from paper_2107_02010_b200.solver import lib
+    dp = lambda t: C.cast(t.data_ptr(), C.POINTER(C.c_double))
+    e2e_t = []
+    for k in range(max(2, args.steps)):
+        l2_flush(flush)
+        barrier()
+        t0 = time.perf_counter()
+        lossv = C.c_double()
+        sst = Stats()
+        rc = lib().msot_sinkhorn(ctx._h, C.byref(prm), dp(px), dp(pa), w["n"], dp(py), dp(pb),
+                                 w["m"], w["d"], None, None, None, None, C.byref(lossv),
+                                 C.byref(sst))
+        barrier()
+        if rc != 0:
+            raise RuntimeError(lib().msot_last_error().decode())
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_local = torch.tensor(e2e_t, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(e2e_local, op=dist.ReduceOp.MAX)
+    e2e_s = float(e2e_local[1:].mean()) if len(e2e_t) > 1 else float(e2e_local[0])
+
+    # roofline of the dominant kernel: softmin launches timed with events
+    ctx.set_profiling(True)
+    _, pst = solve()
+    ctx.set_profiling(False)
+    ex2_rate = ctx.probe_ex2()
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+        ctx.close()
+        return
+    achieved = pst["pairs_evaluated"] / world / (pst["softmin_ms"] * 1e-3)
+    nominal = 148 * 16 * 1965e6
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "softmin_ncu.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC,
+        "value": ms * 1e-3,
+        "unit": "s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": False,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32 (f64 loss, f64 inputs)",
+        "data": "synthetic (seeded Gaussian mixtures)",
+        "config": {**{k: v for k, v in w.items()}, "parallelism": f"rows sharded x{world}",
+                   "l2": "256 MB buffer written between timed steps",
+                   "t_switch": st["t_switch"], "n_scales": st["n_scales"], "kx": st["kx"],
+                   "ky": st["ky"], "cluster_scale": st["cluster_scale"]},
+        "S_eps": loss,
+        "pairs_evaluated": st["pairs_evaluated"],
+        "pairs_dense_equiv": st["pairs_dense"],
+        "fine_kept_fraction": st["pairs_fine"] / max(st["pairs_fine_dense"], 1.0),
+        "pairs_per_s": st["pairs_evaluated"] / (ms * 1e-3),
+        "gpu_launches": launches,
+        "e2e": {"value": e2e_s, "unit": "s",
+                "h2d_bytes_per_step": (w["n"] + w["m"]) * (w["d"] + 1) * 8,
+                "d2h_bytes_per_step": 8},
+        "roofline": {"bound": "mufu", "achieved": achieved, "peak": ex2_rate,
+                     "unit": "pairs/s (1 MUFU.EX2 per pair)", "frac": achieved / ex2_rate,
+                     "peak_source": "measured on this GPU by msot_probe_ex2 "
+                                    "(ex2.approx.ftz.f32 issue rate, all SMs)",
+                     "peak_nominal": nominal, "frac_of_nominal": achieved / nominal,
+                     "traffic": traffic, "kernel": "softmin_kernel<3>",
+                     "softmin_ms": pst["softmin_ms"], "softmin_launches": pst["softmin_launches"],
+                     "share_of_step": pst["softmin_ms"] / max(pst["total_ms"], 1e-9)},
+        "clocks": clk.summary(),
+        "fallback_rows": st["fallback_rows"],
+    }
+    if not args.no_cpu:
+        rows = 256
+        rate, dt, cores = cpu_sample(x, y, b, w["blur"] ** 2, rows)
+        line["cpu_baseline"] = {
+            "value": st["pairs_evaluated"] / rate, "unit": "s (extrapolated)", "cores": cores,
+            "kind": "port",
+            "sample": f"FP64 oracle softmin, {rows} rows x {w['m']} cols ({dt:.1f} s, "
+                      f"{rate:.3e} pairs/s) extrapolated to the solve's "
+                      f"{st['pairs_evaluated']:.3e} evaluated pairs"}
+    os.makedirs(os.path.dirname(PAIRS_FILE), exist_ok=True)
+    if w["n"] == WORKLOAD["n"] and world == 1:
+        with open(PAIRS_FILE, "w") as f:
+            json.dump({"pairs_evaluated": st["pairs_evaluated"], "n_scales": st["n_scales"],
+                       "t_switch": st["t_switch"], "kx": st["kx"]}, f, indent=1)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+    ctx.close()
+
+
+def run_reference(args, w, rank):
+    """--impl reference: the CPU oracle (FP64 restatement of PAPER.md:235-326
+    on the reference's own thread pool, oracle/_ref) timed on bounded samples
+    of the same workload, extrapolated to the workload's evaluated pairs."""
+    if rank != 0:
+        return
+    x, a, y, b = make_inputs(w)
+    pairs = None
+    if os.path.exists(PAIRS_FILE):
+        pairs = json.load(open(PAIRS_FILE)).get("pairs_evaluated")
+    rows = 256
+    for _ in range(max(args.warmup, 0)):
+        cpu_sample(x, y, b, w["blur"] ** 2, 32)
+    rates = []
+    for _ in range(args.steps):
+        rate, dt, cores = cpu_sample(x, y, b, w["blur"] ** 2, rows)
+        rates.append(rate)
+    rate = statistics.median(rates)
+    if pairs is None:
+        pairs = float(w["n"]) * w["m"] * 4 * 50  # dense-equivalent upper bound
+    sec = pairs / rate
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": sec, "unit": "s",
+        "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "higher_is_better": False,
+        "dtype": "f64", "data": "synthetic (seeded Gaussian mixtures)",
+        "config": {**w, "parallelism": f"{cores} CPU threads"},
+        "cpu_baseline": {"value": sec, "unit": "s (extrapolated)", "cores": cores, "kind": "port",
+                         "sample": f"FP64 oracle softmin {rows} rows x {w['m']} cols per step, "
+                                   f"{rate:.3e} pairs/s, extrapolated to {pairs:.3e} pairs "
+                                   f"(profiles/c3_workload.json)"},
+        "e2e": {"value": sec, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -94,6 +94,11 @@ void msot_destroy(msot_ctx* ctx);
 /* 1 = time every softmin launch with CUDA events (stats.softmin_ms). */
 int msot_set_profiling(msot_ctx* ctx, int on);
 
+/* Measures the GPU's MUFU.EX2 rate (ex2 per second, all SMs) with the
+ * ex2.approx.ftz.f32 instruction the softmin issues: the measured roofline
+ * denominator of the softmin (pairs/s <= ex2/s). */
+int msot_probe_ex2(msot_ctx* ctx, double* ex2_per_s);
+
 /* --- host-side helpers shared with the oracle (no GPU work) ------------- */
 
 /* make_schedule: writes n sigmas/eps/lambdas, returns n

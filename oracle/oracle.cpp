@@ -488,8 +488,20 @@ int oracle_sinkhorn(const msot_params* prm, const double* x, const double* a, in
     }
   } else {
     // ---- multiscale_sinkhorn with voxel-grid coarsening.
-    const double cell = prm->cluster_scale > 0 ? prm->cluster_scale
-                                               : msot_auto_cell(lo.data(), hi.data(), d, n, m);
+    double cell = prm->cluster_scale > 0 ? prm->cluster_scale
+                                         : msot_auto_cell(lo.data(), hi.data(), d, n, m);
+    if (prm->cluster_scale <= 0) {  // policy.h: refine on occupied voxels
+      auto occupied = [&](const double* p, int64_t cnt) {
+        std::vector<uint32_t> k(cnt);
+        for (int64_t i = 0; i < cnt; ++i) k[i] = msot_cube_key(p + i * d, d, lo.data(), cell);
+        std::sort(k.begin(), k.end());
+        return static_cast<int64_t>(std::unique(k.begin(), k.end()) - k.begin());
+      };
+      for (int it = 0; it < MSOT_AUTO_REFINE; ++it) {
+        const int64_t kk = std::max(occupied(x, n), occupied(y, m));
+        cell = msot_refine_cell(cell, kk, n, m, d, lo.data(), hi.data());
+      }
+    }
     S.cluster_scale = cell;
     Clusters cx = grid_cluster(x, a, n, d, lo.data(), cell);
     Clusters cy = grid_cluster(y, b, m, d, lo.data(), cell);

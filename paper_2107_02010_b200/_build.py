@@ -17,7 +17,7 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_obj")
 LIB = os.path.join(HERE, "libmsot_b200.so")
 
-SOURCES = ["softmin.cu", "prims.cu", "cluster.cu", "mask.cu", "loss.cu", "solver.cu"]
+SOURCES = ["softmin.cu", "prims.cu", "cluster.cu", "mask.cu", "loss.cu", "probe.cu", "solver.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",

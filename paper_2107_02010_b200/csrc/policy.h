@@ -81,6 +81,27 @@ static inline double msot_auto_cell(const double* lo, const double* hi, int d, i
   return s;
 }
 
+/* Refinement of the automatic edge for clustered data (the first guess
+ * assumes the bounding box is uniformly filled): rescale so the number of
+ * occupied voxels k approaches max(n,m)/MSOT_AUTO_ATOMS_PER_CELL.  The
+ * solver applies it MSOT_AUTO_REFINE times, recounting occupied voxels of
+ * both clouds (max) in between. */
+#define MSOT_AUTO_REFINE 2
+static inline double msot_refine_cell(double cell, int64_t k_occupied, int64_t n, int64_t m,
+                                      int d, const double* lo, const double* hi) {
+  double target = (double)(n > m ? n : m) / MSOT_AUTO_ATOMS_PER_CELL;
+  if (target < 1.0) target = 1.0;
+  if (k_occupied < 1) k_occupied = 1;
+  double s = cell * pow((double)k_occupied / target, 1.0 / (double)d);
+  double ext_max = 0.0;
+  for (int k = 0; k < d; ++k)
+    if (hi[k] - lo[k] > ext_max) ext_max = hi[k] - lo[k];
+  double smin = ext_max / (double)((1 << MSOT_MORTON_BITS) - 2);
+  if (s < smin) s = smin;
+  if (ext_max > 0.0 && s > 2.0 * ext_max) s = 2.0 * ext_max;
+  return s;
+}
+
 /* Voxel coordinate along one axis: floor((x - origin) / cell) in float64
  * (one correctly rounded subtraction, one correctly rounded division). */
 MSOT_HD static inline uint32_t msot_cube_coord(double x, double origin, double cell) {

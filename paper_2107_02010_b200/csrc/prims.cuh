@@ -84,4 +84,8 @@ cudaError_t divergence_final(const double* partials, int nblocks, double eps, do
 cudaError_t scatter_unsort(const float* v, const int32_t* perm, int64_t n, double* out,
                            cudaStream_t st);
 
+// MUFU.EX2 throughput probe (probe.cu)
+cudaError_t ex2_probe(int n_sm, int iters, float* sink, double* ex2_per_launch, int* blocks,
+                      cudaStream_t st);
+
 }  // namespace msot_dev

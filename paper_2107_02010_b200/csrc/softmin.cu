@@ -28,11 +28,11 @@ namespace msot_dev {
 
 struct RowState {
   float x0, x1, x2;  // scaled, tile-centred coordinates
-  float nr;          // -(est / (lambda eps ln2))
+  float nr;          // -(est / (lambda eps ln2) - R), R = the tile's reference
 };
 
 template <int D>
-__device__ __forceinline__ void load_row(const Problem& P, int r, int r_end, float4 o,
+__device__ __forceinline__ void load_row(const Problem& P, int r, int r_end, float4 o, float R,
                                          RowState& rs) {
   const bool ok = r < r_end;
   float4 v = ok ? P.rows[r] : o;
@@ -40,7 +40,7 @@ __device__ __forceinline__ void load_row(const Problem& P, int r, int r_end, flo
   rs.x1 = D > 1 ? (v.y - o.y) * P.sc : 0.f;
   rs.x2 = D > 2 ? (v.z - o.z) * P.sc : 0.f;
   float est = (P.row_est != nullptr && ok) ? P.row_est[r] : 0.f;
-  rs.nr = -(est * P.inv_lam_eps_ln2);
+  rs.nr = -fmaf(est, P.inv_lam_eps_ln2, -R);  // one rounding of a small number
 }
 
 // Walks the concatenated column ranges of one tile: position -> column.
@@ -71,11 +71,17 @@ softmin_kernel(const __grid_constant__ Group G) {
   const int tid = threadIdx.x;
   const int row_base = P.tile_start[item.y];
   const int row_end = P.tile_start[item.y + 1];
-  const float4 o = P.rows[(row_base + row_end) >> 1];
+  const int mid = (row_base + row_end) >> 1;
+  const float4 o = P.rows[mid];
+  // Tile reference R (log2 units): the row constant est/(lambda eps ln2) and
+  // the column constant h/(eps ln2) are ~|f|/eps (10^2..10^4) and cancel on
+  // the pairs that matter; shifting both by R inside an FMA keeps each to one
+  // rounding of a small number instead of two roundings of large ones.
+  const float R = P.row_est ? P.row_est[mid] * P.inv_lam_eps_ln2 : 0.f;
 
   RowState ra, rb;
-  load_row<D>(P, row_base + tid, row_end, o, ra);
-  load_row<D>(P, row_base + tid + kSoftminThreads, row_end, o, rb);
+  load_row<D>(P, row_base + tid, row_end, o, R, ra);
+  load_row<D>(P, row_base + tid + kSoftminThreads, row_end, o, R, rb);
 
   ColWalker w{P.ranges, P.tile_rptr[item.y], P.tile_rptr[item.y + 1], 0};
   const int32_t pos_begin = item.z, pos_end = item.w;
@@ -104,7 +110,7 @@ softmin_kernel(const __grid_constant__ Group G) {
       rec[0] = (o.x - cv.x) * P.sc;
       rec[2] = D > 1 ? (o.y - cv.y) * P.sc : 0.f;
       rec[4] = D > 2 ? (o.z - cv.z) * P.sc : 0.f;
-      rec[6] = -(cl + ch * P.inv_eps_ln2);
+      rec[6] = -(fmaf(ch, P.inv_eps_ln2, R) + cl);
     } else {
       rec[0] = 0.f;
       rec[2] = 0.f;

@@ -164,6 +164,27 @@ void prepare_measure(msot_ctx* c, const std::string& tag, const double* d_x, con
   CK(cudaStreamSynchronize(st));
 }
 
+// Occupied voxels of one cloud for a candidate edge (automatic edge rule).
+int64_t count_cells(msot_ctx* c, const double* d_x, int64_t n, const GridSpec& g) {
+  cudaStream_t st = c->st;
+  uint32_t* keys = c->buf<uint32_t>("cc.keys", n);
+  int32_t* vals = c->buf<int32_t>("cc.vals", n);
+  CK(cube_keys(d_x, n, g, keys, vals, st));
+  void* tmp = c->buf<char>("cc.rstmp", radix_temp_bytes(n));
+  const int bits = g.d == 1 ? MSOT_MORTON_BITS : g.d == 2 ? 2 * MSOT_MORTON_BITS : 3 * MSOT_MORTON_BITS;
+  CK(radix_sort_pairs(keys, vals, n, bits, tmp, st));
+  uint8_t* flags = c->buf<uint8_t>("cc.flags", n);
+  int32_t* lab = c->buf<int32_t>("cc.lab", n);
+  int32_t* stmp = c->buf<int32_t>("cc.stmp", scan_temp_elems(n));
+  int32_t* kdev = c->buf<int32_t>("cc.k", 1);
+  CK(segment_flags(keys, n, flags, st));
+  CK((scan<uint8_t, int32_t>(flags, lab, n, true, stmp, kdev, st)));
+  int32_t k = 0;
+  CK(cudaMemcpyAsync(&k, kdev, sizeof(k), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return k;
+}
+
 // ------------------------------------------------------------------ ranges
 struct RangeSet {
   int64_t n_tiles = 0, n_ranges = 0;
@@ -477,9 +498,16 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
     g.origin[k] = lo[k];
     g.center[k] = 0.5 * (lo[k] + hi[k]);
   }
-  const double cell = prm->cluster_scale > 0 ? prm->cluster_scale : msot_auto_cell(lo, hi, d, n, m);
-  g.cell = cell;
+  double cell = prm->cluster_scale > 0 ? prm->cluster_scale : msot_auto_cell(lo, hi, d, n, m);
   const bool ms = prm->multiscale != 0;
+  if (ms && prm->cluster_scale <= 0) {  // policy.h: refine on occupied voxels
+    for (int it = 0; it < MSOT_AUTO_REFINE; ++it) {
+      g.cell = cell;
+      const int64_t kk = std::max(count_cells(c, d_x, n, g), count_cells(c, d_y, m, g));
+      cell = msot_refine_cell(cell, kk, n, m, d, lo, hi);
+    }
+  }
+  g.cell = cell;
   DMeasure X, Y;
   prepare_measure(c, "x", d_x, d_a, n, d, g, ms, X);
   prepare_measure(c, "y", d_y, d_b, m, d, g, ms, Y);
@@ -779,6 +807,25 @@ int msot_set_profiling(msot_ctx* c, int on) {
   if (!c) return MSOT_EUSAGE;
   c->profiling = on != 0;
   return MSOT_OK;
+}
+
+int msot_probe_ex2(msot_ctx* c, double* ex2_per_s) {
+  return guard([&] {
+    if (!c || !ex2_per_s) raise(MSOT_EUSAGE, "null argument");
+    CK(cudaSetDevice(c->device));
+    float* sink = c->buf<float>("probe.sink", 256);
+    double per = 0.0;
+    int blocks = 0;
+    const int iters = 4096;
+    CK(ex2_probe(c->n_sm, iters, sink, &per, &blocks, c->st));  // warm-up
+    CK(cudaEventRecord(c->t0, c->st));
+    for (int r = 0; r < 5; ++r) CK(ex2_probe(c->n_sm, iters, sink, &per, &blocks, c->st));
+    CK(cudaEventRecord(c->t1, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->t0, c->t1));
+    *ex2_per_s = 5.0 * per / (ms * 1e-3);
+  });
 }
 
 static void check_weights(const double* w, int64_t n) {

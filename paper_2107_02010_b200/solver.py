@@ -57,6 +57,7 @@ def lib():
         L.msot_sinkhorn.argtypes = [C.c_void_p, C.POINTER(Params), _dp, _dp, C.c_int64, _dp,
                                     _dp, C.c_int64, C.c_int, _dp, _dp, _dp, _dp, _dp,
                                     C.POINTER(Stats)]
+        L.msot_probe_ex2.argtypes = [C.c_void_p, _dp]
         L.msot_sinkhorn_device.argtypes = [C.c_void_p, C.POINTER(Params), C.c_void_p,
                                            C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                            C.c_int64, C.c_int, _dp, C.POINTER(Stats)]
@@ -68,7 +69,7 @@ def lib():
 EXPORTS = ["msot_last_error", "msot_params_default", "msot_create", "msot_nccl_unique_id",
            "msot_create_dist", "msot_destroy", "msot_set_profiling", "msot_schedule",
            "msot_shard_tiles", "msot_softmin", "msot_grid_cluster", "msot_truncation_mask",
-           "msot_sinkhorn", "msot_sinkhorn_device"]
+           "msot_sinkhorn", "msot_sinkhorn_device", "msot_probe_ex2"]
 
 
 def _check(rc):
@@ -145,6 +146,12 @@ class Context:
 
     def set_profiling(self, on=True):
         _check(lib().msot_set_profiling(self._h, int(bool(on))))
+
+    def probe_ex2(self):
+        """Measured MUFU.EX2 rate of this GPU (ex2/s): the softmin roofline."""
+        r = C.c_double()
+        _check(lib().msot_probe_ex2(self._h, C.byref(r)))
+        return r.value
 
     # -- SPEC.md:164-172
     def softmin(self, x, y, logw, h, eps, lam=1.0, f_est=None):

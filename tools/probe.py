@@ -1,4 +1,4 @@
-"""Quick GPU probe: dense softmin throughput + a multiscale solve (dev tool)."""
+"""Quick GPU probe: dense softmin throughput + multiscale solves (dev tool)."""
 import sys, time, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -11,15 +11,20 @@ def mixture(n, seed, d=3, k=8, sigma=0.05):
     return cen[rng.integers(0, k, n)] + rng.normal(0, sigma, (n, d))
 
 ctx = Context(0)
+print("ex2/s", ctx.probe_ex2(), flush=True)
 ctx.set_profiling(True)
-for n, blur, ms in [(100000, 0.5, False), (300000, 0.5, False), (100000, 0.01, True), (1000000, 0.01, True)]:
+cfgs = [(300000, dict(blur=0.5))]
+for th in (20.0, 5.0):
+    for cs in (0.0, 0.03, 0.02):
+        cfgs.append((1000000, dict(blur=0.01, multiscale=True, retruncate=1, theta=th, cluster_scale=cs)))
+cfgs.append((1000000, dict(blur=0.01, multiscale=True, retruncate=1, theta=20.0, scaling=0.5)))
+for n, kw in cfgs:
     x, y = mixture(n, 5), mixture(n, 6)
     a = np.full(n, 1 / n)
-    for rep in range(2):
-        t = time.time()
-        loss, _, st = ctx.sinkhorn(make_params(blur=blur, multiscale=ms), x, a, y, a, potentials=False)
-        wall = time.time() - t
-    print(f"n={n} blur={blur} ms={ms} loss={loss:.8g} wall={wall:.3f}s total_ms={st['total_ms']:.1f} "
+    t = time.time()
+    loss, _, st = ctx.sinkhorn(make_params(**kw), x, a, y, a, potentials=False)
+    wall = time.time() - t
+    print(f"n={n} {kw} loss={loss:.8g} wall={wall:.3f}s total_ms={st['total_ms']:.1f} "
           f"softmin_ms={st['softmin_ms']:.1f} pairs={st['pairs_evaluated']:.3e} "
-          f"rate={st['pairs_evaluated']/st['softmin_ms']*1e3:.3e} pairs/s launches={st['gpu_launches']} "
-          f"kx={st['kx']} tsw={st['t_switch']}/{st['n_scales']} fine={st['pairs_fine']/max(st['pairs_fine_dense'],1):.4f} fb={st['fallback_rows']}", flush=True)
+          f"rate={st['pairs_evaluated']/st['softmin_ms']*1e3:.3e} launches={st['gpu_launches']} "
+          f"kx={st['kx']} cell={st['cluster_scale']:.4f} tsw={st['t_switch']}/{st['n_scales']} fine={st['pairs_fine']/max(st['pairs_fine_dense'],1):.4f} fb={st['fallback_rows']}", flush=True)

@@ -76,6 +76,10 @@ typedef struct msot_stats {
   int64_t gpu_launches;     /* all kernels launched by this solve                 */
   double  h2d_bytes, d2h_bytes;
   int32_t rank, world;
+  /* device time per phase when profiling (ms): 0 setup (bounding box,
+   * clustering), 1 coarse phase, 2 extrapolation, 3 masks/ranges/work
+   * items, 4 symmetric updates at full resolution, 5 loss and outputs */
+  double  phase_ms[8];
 } msot_stats;
 
 typedef struct msot_ctx msot_ctx;

@@ -594,6 +594,15 @@ int oracle_sinkhorn(const msot_params* prm, const double* x, const double* a, in
     u.b_yy = unsort(fu.b_yy, py);
     u.a_xy = unsort(fu.a_xy, py);
   }
+  // Balanced potentials are defined up to (b_yx + c, a_xy - c); return the
+  // canonical representative <a, b_yx> = <b, a_xy> (same rule as
+  // csrc/loss.cu), so both implementations report the same gauge.
+  if (msot_reach_is_inf(prm->reach)) {
+    const Vec av(a, a + n), bv(b, b + m);
+    const double c = (dot(bv, u.a_xy) - dot(av, u.b_yx)) / (msot::kahan_sum(av) + msot::kahan_sum(bv));
+    for (double& v : u.b_yx) v += c;
+    for (double& v : u.a_xy) v -= c;
+  }
   const double loss = divergence(prm, eps[ns - 1], Vec(a, a + n), Vec(b, b + m), u);
   if (!std::isfinite(loss)) return fail(MSOT_ENUMERIC, "non-finite divergence");
   if (loss_out) *loss_out = loss;

@@ -56,10 +56,15 @@ class Stats(C.Structure):
         ("d2h_bytes", C.c_double),
         ("rank", C.c_int32),
         ("world", C.c_int32),
+        ("phase_ms", C.c_double * 8),
     ]
 
+    PHASES = ("setup", "coarse", "extrapolate", "masks", "updates", "loss")
+
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k != "phase_ms"}
+        d["phase_ms"] = {p: self.phase_ms[i] for i, p in enumerate(self.PHASES)}
+        return d
 
 
 TILE_ROWS = 256  # MSOT_TILE_ROWS in csrc/policy.h

@@ -13,6 +13,7 @@
 namespace msot_dev {
 
 constexpr int kLossThreads = 256;
+constexpr int kLossAcc = 5;
 
 __device__ __forceinline__ double term(double w, float f_cross, float f_self, double rho) {
   if (rho <= 0.0) return w * (static_cast<double>(f_cross) - static_cast<double>(f_self));
@@ -22,53 +23,62 @@ __device__ __forceinline__ double term(double w, float f_cross, float f_self, do
 __global__ void divergence_partial_kernel(const double* a, const double* b, int64_t n, int64_t m,
                                           const float* a_xx, const float* b_yy, const float* a_xy,
                                           const float* b_yx, double rho, double* partials) {
-  __shared__ double sh[3][kLossThreads / 32];
+  // accumulators: S (dual objective), A = sum a, B = sum b,
+  //               Pa = <a, b_yx>, Pb = <b, a_xy> (for the gauge, balanced case)
+  __shared__ double sh[kLossAcc][kLossThreads / 32];
   const int64_t total = n + m;
   const int64_t per = (total + gridDim.x - 1) / gridDim.x;
   const int64_t lo = blockIdx.x * per, hi = min(total, lo + per);
-  double S = 0.0, A = 0.0, B = 0.0;
+  double v[kLossAcc] = {0.0, 0.0, 0.0, 0.0, 0.0};
   for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     if (i < n) {
-      S += term(a[i], b_yx[i], a_xx[i], rho);
-      A += a[i];
+      v[0] += term(a[i], b_yx[i], a_xx[i], rho);
+      v[1] += a[i];
+      v[3] += a[i] * static_cast<double>(b_yx[i]);
     } else {
       const int64_t j = i - n;
-      S += term(b[j], a_xy[j], b_yy[j], rho);
-      B += b[j];
+      v[0] += term(b[j], a_xy[j], b_yy[j], rho);
+      v[2] += b[j];
+      v[4] += b[j] * static_cast<double>(a_xy[j]);
     }
   }
-  for (int o = 16; o > 0; o >>= 1) {
-    S += __shfl_xor_sync(0xffffffffu, S, o);
-    A += __shfl_xor_sync(0xffffffffu, A, o);
-    B += __shfl_xor_sync(0xffffffffu, B, o);
-  }
+#pragma unroll
+  for (int q = 0; q < kLossAcc; ++q)
+    for (int o = 16; o > 0; o >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
   const int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0) {
-    sh[0][w] = S;
-    sh[1][w] = A;
-    sh[2][w] = B;
-  }
+  if ((threadIdx.x & 31) == 0)
+    for (int q = 0; q < kLossAcc; ++q) sh[q][w] = v[q];
   __syncthreads();
-  if (threadIdx.x < 3) {
-    double v = 0.0;
-    for (int k = 0; k < kLossThreads / 32; ++k) v += sh[threadIdx.x][k];
-    partials[3 * blockIdx.x + threadIdx.x] = v;
+  if (threadIdx.x < kLossAcc) {
+    double s = 0.0;
+    for (int k = 0; k < kLossThreads / 32; ++k) s += sh[threadIdx.x][k];
+    partials[kLossAcc * blockIdx.x + threadIdx.x] = s;
   }
 }
 
+// out = {S_eps, sum a, sum b, gauge c}.  Balanced potentials are defined up
+// to (b_yx + c, a_xy - c) — a direction the averaged iteration never damps,
+// so float rounding random-walks along it.  Both the oracle and this solver
+// return the canonical representative <a, b_yx> = <b, a_xy>; the loss is
+// evaluated on it (identical to the raw value when the masses are equal).
 __global__ void divergence_final_kernel(const double* partials, int nb, double eps, double rho,
                                         double* out) {
   if (threadIdx.x != 0) return;
-  double S = 0.0, A = 0.0, B = 0.0;
-  for (int k = 0; k < nb; ++k) {
-    S += partials[3 * k];
-    A += partials[3 * k + 1];
-    B += partials[3 * k + 2];
+  double v[kLossAcc] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int k = 0; k < nb; ++k)
+    for (int q = 0; q < kLossAcc; ++q) v[q] += partials[kLossAcc * k + q];
+  const double A = v[1], B = v[2];
+  double S = v[0], c = 0.0;
+  if (rho <= 0.0) {
+    c = (v[4] - v[3]) / (A + B);
+    S += c * (A - B);
+  } else {
+    S = -(rho + 0.5 * eps) * S;
   }
-  const double mass = 0.5 * eps * (A - B) * (A - B);
-  out[0] = (rho <= 0.0 ? S : -(rho + 0.5 * eps) * S) + mass;
+  out[0] = S + 0.5 * eps * (A - B) * (A - B);
   out[1] = A;
   out[2] = B;
+  out[3] = c;
 }
 
 cudaError_t divergence_partial(const double* a, const double* b, int64_t n, int64_t m,
@@ -86,15 +96,17 @@ cudaError_t divergence_final(const double* partials, int nblocks, double eps, do
   return cudaGetLastError();
 }
 
-__global__ void scatter_unsort_kernel(const float* v, const int32_t* perm, int64_t n, double* out) {
+// out[perm[s]] = v[s] + sign * (*shift)  (shift nullable)
+__global__ void scatter_unsort_kernel(const float* v, const int32_t* perm, int64_t n,
+                                      const double* shift, double sign, double* out) {
   const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (s < n) out[perm ? perm[s] : s] = static_cast<double>(v[s]);
+  if (s < n) out[perm ? perm[s] : s] = static_cast<double>(v[s]) + (shift ? sign * *shift : 0.0);
 }
 
-cudaError_t scatter_unsort(const float* v, const int32_t* perm, int64_t n, double* out,
-                           cudaStream_t st) {
+cudaError_t scatter_unsort(const float* v, const int32_t* perm, int64_t n, const double* shift,
+                           double sign, double* out, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  ++g_launches; scatter_unsort_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(v, perm, n, out);
+  ++g_launches; scatter_unsort_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(v, perm, n, shift, sign, out);
   return cudaGetLastError();
 }
 

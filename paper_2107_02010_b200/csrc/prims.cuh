@@ -81,8 +81,8 @@ cudaError_t divergence_partial(const double* a, const double* b, int64_t n, int6
                                double* partials, int nblocks, cudaStream_t st);
 cudaError_t divergence_final(const double* partials, int nblocks, double eps, double rho,
                              double* out, cudaStream_t st);
-cudaError_t scatter_unsort(const float* v, const int32_t* perm, int64_t n, double* out,
-                           cudaStream_t st);
+cudaError_t scatter_unsort(const float* v, const int32_t* perm, int64_t n, const double* shift,
+                           double sign, double* out, cudaStream_t st);
 
 // MUFU.EX2 throughput probe (probe.cu)
 cudaError_t ex2_probe(int n_sm, int iters, float* sink, double* ex2_per_launch, int* blocks,

@@ -92,6 +92,21 @@ struct msot_ctx {
     bufs[name] = {p, bytes};
     return static_cast<T*>(p);
   }
+  // phase marks (profiling only): time from a mark to the next is charged to
+  // the mark's phase (stats.phase_ms, see include/msot_gpu.h)
+  std::vector<std::pair<int, cudaEvent_t>> marks;
+  std::vector<cudaEvent_t> mark_pool;
+  void mark(int phase) {
+    if (!profiling) return;
+    if (mark_pool.size() <= marks.size()) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      mark_pool.push_back(e);
+    }
+    cudaEvent_t e = mark_pool[marks.size()];
+    CK(cudaEventRecord(e, st));
+    marks.push_back({phase, e});
+  }
   void ev_pair(cudaEvent_t* a, cudaEvent_t* b) {
     while (ev.size() < ev_used + 2) {
       cudaEvent_t e;
@@ -470,6 +485,8 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
   cudaStream_t st = c->st;
   const int64_t launches0 = g_launches;
   c->ev_used = 0;
+  c->marks.clear();
+  c->mark(0);  // phase 0: bounding box, voxel edge, clustering
   CK(cudaEventRecord(c->t0, st));
 
   // diameter_estimate -- exact min/max on the device
@@ -523,6 +540,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
   const double full = double(n) * n + double(m) * m + 2.0 * double(n) * m;
 
   if (!ms) {
+    c->mark(4);  // phase 4: symmetric updates
     S->t_switch = 0;
     RangeSet rxx, ryy, rxy, ryx;
     dense_rangeset(c, "d.xx", n, n, rxx);
@@ -546,7 +564,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
     for (float r : Y.radii_h) rmax = std::max(rmax, double(r));
     const int tsw = msot_switch_index(sig.data(), ns, rmax, prm->switch_factor);
     S->t_switch = tsw;
-    // coarse phase on the centroid measures (dense)
+    c->mark(1);  // phase 1: coarse phase on the centroid measures (dense)
     if (tsw > 0) {
       Potentials Uc;
       alloc_pots(c, "cpot", X.k, Y.k, Uc);
@@ -564,6 +582,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
         sym_step(c, Pc, Uc, ccur, eps[t], lam[t], false, ss);
         S->pairs_dense += cfull;
       }
+      c->mark(2);  // phase 2: extrapolation
       // coarse -> fine extrapolation: one lambda-damped
       // softmin of every fine atom against the coarse measure, expanded
       // around the inherited coarse value.
@@ -638,7 +657,11 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
       const int tt = std::min(t, ns - 1);
       const bool rebuild =
           (t == tsw) || (prm->retruncate > 0 && t < ns && (t - tsw) % prm->retruncate == 0);
-      if (rebuild) build_masks(eps[tt]);
+      if (rebuild) {
+        c->mark(3);  // phase 3: truncation masks, ranges, work items
+        build_masks(eps[tt]);
+      }
+      c->mark(4);
       sym_step(c, Pf, U, cur, eps[tt], lam[tt], t == ns, ss);
       S->pairs_dense += full;
       S->pairs_fine += Pf.pairs_all;
@@ -648,13 +671,14 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
 
   // divergence (eq. 5-6), fixed-order float64
   const double rho = msot_reach_is_inf(prm->reach) ? 0.0 : std::pow(prm->reach, prm->p);
+  c->mark(5);
   const int nb = 256;
-  double* partials = c->buf<double>("loss.part", 3 * nb);
-  double* lout = c->buf<double>("loss.out", 3);
+  double* partials = c->buf<double>("loss.part", 5 * nb);
+  double* lout = c->buf<double>("loss.out", 4);
   float** f = U.v[cur];
   CK(divergence_partial(X.w64, Y.w64, n, m, f[0], f[1], f[2], f[3], rho, partials, nb, st));
   CK(divergence_final(partials, nb, eps[ns - 1], rho, lout, st));
-  double res[3];
+  double res[4];
   int32_t fbt = 0;
   CK(cudaMemcpyAsync(res, lout, sizeof(res), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(&fbt, ss.fb_total, sizeof(fbt), cudaMemcpyDeviceToHost, st));
@@ -662,14 +686,17 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
     double* tmp = c->buf<double>("unsort", std::max(n, m));
     const int64_t len[4] = {n, m, m, n};
     const int32_t* perm[4] = {X.perm, Y.perm, Y.perm, X.perm};
+    // canonical gauge of the balanced cross pair (loss.cu): a_xy - c, b_yx + c
+    const double sign[4] = {0.0, 0.0, -1.0, 1.0};
     for (int q = 0; q < 4; ++q) {
       if (!h_pots[q]) continue;
-      CK(scatter_unsort(f[q], perm[q], len[q], tmp, st));
+      CK(scatter_unsort(f[q], perm[q], len[q], lout + 3, sign[q], tmp, st));
       CK(cudaMemcpyAsync(h_pots[q], tmp, len[q] * sizeof(double), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
       S->d2h_bytes += len[q] * sizeof(double);
     }
   }
+  c->mark(-1);
   CK(cudaEventRecord(c->t1, st));
   CK(cudaStreamSynchronize(st));
   float ms_total = 0.f;
@@ -683,6 +710,12 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
       acc += e;
     }
     S->softmin_ms = acc;
+    for (size_t k = 0; k + 1 < c->marks.size(); ++k) {
+      float e = 0.f;
+      CK(cudaEventElapsedTime(&e, c->marks[k].second, c->marks[k + 1].second));
+      const int ph = c->marks[k].first;
+      if (ph >= 0 && ph < 8) S->phase_ms[ph] += e;
+    }
   }
   S->fallback_rows = fbt;
   S->gpu_launches = g_launches - launches0;
@@ -796,6 +829,7 @@ void msot_destroy(msot_ctx* c) {
   cudaStreamSynchronize(c->st);
   for (auto& kv : c->bufs) cudaFree(kv.second.first);
   for (auto e : c->ev) cudaEventDestroy(e);
+  for (auto e : c->mark_pool) cudaEventDestroy(e);
   if (c->t0) cudaEventDestroy(c->t0);
   if (c->t1) cudaEventDestroy(c->t1);
   if (c->comm) ncclCommDestroy(c->comm);

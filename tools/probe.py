@@ -27,4 +27,4 @@ for n, kw in cfgs:
     print(f"n={n} {kw} loss={loss:.8g} wall={wall:.3f}s total_ms={st['total_ms']:.1f} "
           f"softmin_ms={st['softmin_ms']:.1f} pairs={st['pairs_evaluated']:.3e} "
           f"rate={st['pairs_evaluated']/st['softmin_ms']*1e3:.3e} launches={st['gpu_launches']} "
-          f"kx={st['kx']} cell={st['cluster_scale']:.4f} tsw={st['t_switch']}/{st['n_scales']} fine={st['pairs_fine']/max(st['pairs_fine_dense'],1):.4f} fb={st['fallback_rows']}", flush=True)
+          f"kx={st['kx']} cell={st['cluster_scale']:.4f} tsw={st['t_switch']}/{st['n_scales']} fine={st['pairs_fine']/max(st['pairs_fine_dense'],1):.4f} fb={st['fallback_rows']} phases={ {k: round(v, 1) for k, v in st['phase_ms'].items()} }", flush=True)

@@ -51,7 +51,8 @@ typedef struct msot_params {
   double theta;          /* truncation slack in units of eps       */
   double switch_factor;  /* switch at first sigma < switch_factor * r_max (:306) */
   int32_t max_full_iters;/* safety cap on schedule length          */
-  int32_t reserved;
+  int32_t mask_rule;     /* 0 = min(centroid/radius bound, slope bound) (default),
+                            1 = centroid/radius bound only (msot_truncation_mask) */
 } msot_params;
 
 /* Defaults of SPEC.md:128 (q=0.9), :306 (switch 2x radius), :308 (theta=20). */
@@ -136,14 +137,18 @@ int msot_grid_cluster(msot_ctx* ctx, const double* x, const double* w, int64_t n
                       double* cweights, float* radii);
 
 /* Truncation mask: keep (I,J) iff
- *   F_I + G_J - (1/p) max(0, |X_I - Y_J| - r_I - r_J)^p >= -theta * eps
- * evaluated in float64 without FMA on float32 inputs, plus each row's and
- * each column's best pair (ties to the lowest index) and, when `self` is
- * set, the diagonal.  mask_out is Kx x Ky bytes. */
+ *   min(B_a, B_b) >= -theta * eps,  D = X_I - Y_J,
+ *   B_a = F_I + G_J - (1/2) max(0, |D| - (r_I + r_J))^2
+ *   B_b = F'_I + G'_J + r_I |S_I - D| + r_J |T_J + D| - |D|^2 / 2
+ * (B_b only when the slope arrays gx = {S_I, F'_I}, hy = {T_J, G'_J}, 4
+ * floats per cluster, are given — both or neither), evaluated in float64
+ * without FMA on float32 inputs, plus each row's and each column's best
+ * pair (ties to the lowest index) and, when `self` is set, the diagonal.
+ * mask_out is Kx x Ky bytes. */
 int msot_truncation_mask(msot_ctx* ctx, int64_t kx, int64_t ky, int d, const float* cx,
-                         const float* rx, const float* fx, const float* cy,
-                         const float* ry, const float* gy, double eps, double theta,
-                         double p, int self, uint8_t* mask_out);
+                         const float* rx, const float* fx, const float* gx, const float* cy,
+                         const float* ry, const float* gy, const float* hy, double eps,
+                         double theta, double p, int self, uint8_t* mask_out);
 
 /* The symmetric eps-scaling Sinkhorn solve + debiased divergence
  * (PAPER.md:235-326).  Potential outputs are

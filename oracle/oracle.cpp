@@ -225,16 +225,14 @@ Clusters grid_cluster(const double* x, const double* w, int64_t n, int d, const 
 // distance bound replacing SPEC.md:283's d^{p-1} margin):
 //   F_I + G_J - (1/p) max(0, |X_I - Y_J| - r_I - r_J)^p
 // in float64 with every operation explicitly ordered (no contraction).
-inline double pair_slack(const float* X, float rI, float F, const float* Y, float rJ, float G,
-                         int d, double p) {
-  double s = 0.0;
-  for (int k = 0; k < d; ++k) {
-    const double t = static_cast<double>(X[k]) - static_cast<double>(Y[k]);
-    const double tt = t * t;
-    s = s + tt;
-  }
-  double lb = std::sqrt(s) - static_cast<double>(rI);
-  lb = lb - static_cast<double>(rJ);
+inline double pair_slack(const float* X, float rI, float F, const float* GI, const float* Y,
+                         float rJ, float G, const float* HJ, int d, double p) {
+  double dd[3] = {0.0, 0.0, 0.0};
+  for (int k = 0; k < d; ++k) dd[k] = static_cast<double>(X[k]) - static_cast<double>(Y[k]);
+  const double s = (dd[0] * dd[0] + dd[1] * dd[1]) + dd[2] * dd[2];
+  // (a) centroid/radius bound
+  const double rr = static_cast<double>(rI) + static_cast<double>(rJ);  // symmetric in (I,J)
+  double lb = std::sqrt(s) - rr;
   if (lb < 0.0) lb = 0.0;
   double c;
   if (p == 2.0) {
@@ -244,20 +242,38 @@ inline double pair_slack(const float* X, float rI, float F, const float* Y, floa
     c = std::pow(lb, p) / p;
   }
   const double fg = static_cast<double>(F) + static_cast<double>(G);
-  return fg - c;
+  const double va = fg - c;
+  if (!GI || p != 2.0) return va;
+  // (b) slope bound F'_I + G'_J + r_I |G_I - D| + r_J |H_J + D| - |D|^2/2
+  // (mask.cu header); GI/HJ = {slope[3], F'}
+  double a[3], b[3];
+  for (int k = 0; k < 3; ++k) {
+    a[k] = static_cast<double>(GI[k]) - dd[k];
+    b[k] = static_cast<double>(HJ[k]) + dd[k];
+  }
+  const double na = std::sqrt((a[0] * a[0] + a[1] * a[1]) + a[2] * a[2]);
+  const double nb = std::sqrt((b[0] * b[0] + b[1] * b[1]) + b[2] * b[2]);
+  const double marg = static_cast<double>(rI) * na + static_cast<double>(rJ) * nb;
+  const double fgp = static_cast<double>(GI[3]) + static_cast<double>(HJ[3]);
+  const double vb = (fgp + marg) - 0.5 * s;
+  return va < vb ? va : vb;
 }
 
+// gx / hy: nullable Kx x 4 / Ky x 4 {slope, F'} per cluster (both or neither)
 void truncation_mask(int64_t kx, int64_t ky, int d, const float* cx, const float* rx,
-                     const float* fx, const float* cy, const float* ry, const float* gy,
-                     double eps, double theta, double p, int self, uint8_t* mask) {
+                     const float* fx, const float* gx, const float* cy, const float* ry,
+                     const float* gy, const float* hy, double eps, double theta, double p,
+                     int self, uint8_t* mask) {
   const double thr = -(theta * eps);
   std::vector<double> rbest(kx, -std::numeric_limits<double>::infinity());
   std::vector<int64_t> rarg(kx, 0);
   std::vector<double> cbest(ky, -std::numeric_limits<double>::infinity());
   std::vector<int64_t> carg(ky, 0);
+  const bool g = gx && hy;
   for (int64_t I = 0; I < kx; ++I) {
     for (int64_t J = 0; J < ky; ++J) {
-      const double v = pair_slack(cx + I * d, rx[I], fx[I], cy + J * d, ry[J], gy[J], d, p);
+      const double v = pair_slack(cx + I * d, rx[I], fx[I], g ? gx + 4 * I : nullptr, cy + J * d,
+                                  ry[J], gy[J], g ? hy + 4 * J : nullptr, d, p);
       mask[I * ky + J] = (v >= thr) ? 1 : 0;
       if (v > rbest[I]) { rbest[I] = v; rarg[I] = J; }
       if (v > cbest[J]) { cbest[J] = v; carg[J] = I; }
@@ -268,6 +284,62 @@ void truncation_mask(int64_t kx, int64_t ky, int d, const float* cx, const float
   for (int64_t J = 0; J < ky; ++J) mask[carg[J] * ky + J] = 1;
   if (self)
     for (int64_t I = 0; I < std::min(kx, ky); ++I) mask[I * ky + I] = 1;
+}
+
+// Slope-bound inputs of one potential over one clustering (csrc/cluster.cu
+// cluster_bound): weighted least-squares slope G of f in u = x - X_I (float),
+// F' = max (f_i - <G, u_i>) rounded up, centroids as float (mask inputs).
+void cluster_bound(const Vec& f, const Measure& M, const Clusters& c,
+                   const std::vector<float>& cenf, int d, std::vector<float>& fmax,
+                   std::vector<float>& grad) {
+  fmax.assign(c.k, 0.0f);
+  grad.assign(4 * size_t(c.k), 0.0f);
+  for (int32_t I = 0; I < c.k; ++I) {
+    double m[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}, b[3] = {0, 0, 0}, mu[3] = {0, 0, 0};
+    double W = 0.0, wf = 0.0;
+    for (int32_t s = c.offsets[I]; s < c.offsets[I + 1]; ++s) {
+      double u[3] = {0, 0, 0};
+      for (int k = 0; k < d; ++k)
+        u[k] = static_cast<double>(static_cast<float>(M.pts[int64_t(s) * d + k])) - cenf[size_t(I) * d + k];
+      const double w = M.w[s];
+      for (int a = 0; a < 3; ++a) {
+        for (int q = 0; q < 3; ++q) m[a][q] += w * u[a] * u[q];
+        b[a] += w * u[a] * f[s];
+        mu[a] += w * u[a];
+      }
+      W += w;
+      wf += w * f[s];
+    }
+    const double fbar = wf / W;
+    for (int a = 0; a < 3; ++a) b[a] -= fbar * mu[a];
+    const double tr = m[0][0] + m[1][1] + m[2][2], reg = 1e-9 * tr + 1e-300;
+    for (int a = 0; a < 3; ++a) m[a][a] += reg;
+    const double c00 = m[1][1] * m[2][2] - m[1][2] * m[1][2], c01 = m[0][2] * m[1][2] - m[0][1] * m[2][2],
+                 c02 = m[0][1] * m[1][2] - m[0][2] * m[1][1];
+    const double det = m[0][0] * c00 + m[0][1] * c01 + m[0][2] * c02;
+    double gg[3] = {0, 0, 0};
+    if (det > 0.0 && std::isfinite(det)) {
+      const double c11 = m[0][0] * m[2][2] - m[0][2] * m[0][2], c12 = m[0][1] * m[0][2] - m[0][0] * m[1][2],
+                   c22 = m[0][0] * m[1][1] - m[0][1] * m[0][1];
+      gg[0] = (c00 * b[0] + c01 * b[1] + c02 * b[2]) / det;
+      gg[1] = (c01 * b[0] + c11 * b[1] + c12 * b[2]) / det;
+      gg[2] = (c02 * b[0] + c12 * b[1] + c22 * b[2]) / det;
+    }
+    float G[3];
+    for (int a = 0; a < 3; ++a) G[a] = static_cast<float>(gg[a]);
+    double fm = -std::numeric_limits<double>::infinity(), fp = fm;
+    for (int32_t s = c.offsets[I]; s < c.offsets[I + 1]; ++s) {
+      double lin = 0.0;
+      for (int k = 0; k < d; ++k)
+        lin += static_cast<double>(G[k]) *
+               (static_cast<double>(static_cast<float>(M.pts[int64_t(s) * d + k])) - cenf[size_t(I) * d + k]);
+      fm = std::max(fm, f[s]);
+      fp = std::max(fp, f[s] - lin);
+    }
+    fmax[I] = round_up_float(fm);
+    for (int a = 0; a < 3; ++a) grad[4 * size_t(I) + a] = G[a];
+    grad[4 * size_t(I) + 3] = round_up_float(fp);
+  }
 }
 
 // Column ranges of every cluster-aligned row tile: the union of the kept
@@ -353,15 +425,6 @@ Measure permute(const Measure& m, const std::vector<int32_t>& perm, int d) {
   return o;
 }
 
-std::vector<float> cluster_max(const Vec& v, const Clusters& c) {
-  std::vector<float> o(c.k);
-  for (int32_t I = 0; I < c.k; ++I) {
-    double mx = -std::numeric_limits<double>::infinity();
-    for (int32_t s = c.offsets[I]; s < c.offsets[I + 1]; ++s) mx = std::max(mx, v[s]);
-    o[I] = round_up_float(mx);
-  }
-  return o;
-}
 
 }  // namespace
 
@@ -406,9 +469,10 @@ int oracle_grid_cluster(const double* x, const double* w, int64_t n, int d, cons
 }
 
 void oracle_truncation_mask(int64_t kx, int64_t ky, int d, const float* cx, const float* rx,
-                            const float* fx, const float* cy, const float* ry, const float* gy,
-                            double eps, double theta, double p, int self, uint8_t* mask_out) {
-  truncation_mask(kx, ky, d, cx, rx, fx, cy, ry, gy, eps, theta, p, self, mask_out);
+                            const float* fx, const float* gx, const float* cy, const float* ry,
+                            const float* gy, const float* hy, double eps, double theta, double p,
+                            int self, uint8_t* mask_out) {
+  truncation_mask(kx, ky, d, cx, rx, fx, gx, cy, ry, gy, hy, eps, theta, p, self, mask_out);
 }
 
 int64_t oracle_tile_ranges(const int32_t* row_labels, const int32_t* row_offsets,
@@ -555,14 +619,19 @@ int oracle_sinkhorn(const msot_params* prm, const double* x, const double* a, in
         myy.assign(size_t(cy.k) * cy.k, 1);
         mxy.assign(size_t(cx.k) * cy.k, 1);
       } else {
-        const auto Fxx = cluster_max(fu.a_xx, cx), Fyx = cluster_max(fu.b_yx, cx);
-        const auto Gyy = cluster_max(fu.b_yy, cy), Gxy = cluster_max(fu.a_xy, cy);
+        std::vector<float> Fxx, Fyx, Gyy, Gxy, gxx, gyx, gyy, gxy;
+        cluster_bound(fu.a_xx, Xs, cx, cxf, d, Fxx, gxx);
+        cluster_bound(fu.b_yx, Xs, cx, cxf, d, Fyx, gyx);
+        cluster_bound(fu.b_yy, Ys, cy, cyf, d, Gyy, gyy);
+        cluster_bound(fu.a_xy, Ys, cy, cyf, d, Gxy, gxy);
         mxx.resize(size_t(cx.k) * cx.k);
         myy.resize(size_t(cy.k) * cy.k);
         mxy.resize(size_t(cx.k) * cy.k);
-        truncation_mask(cx.k, cx.k, d, cxf.data(), cx.radii.data(), Fxx.data(), cxf.data(), cx.radii.data(), Fxx.data(), e, prm->theta, p, 1, mxx.data());
-        truncation_mask(cy.k, cy.k, d, cyf.data(), cy.radii.data(), Gyy.data(), cyf.data(), cy.radii.data(), Gyy.data(), e, prm->theta, p, 1, myy.data());
-        truncation_mask(cx.k, cy.k, d, cxf.data(), cx.radii.data(), Fyx.data(), cyf.data(), cy.radii.data(), Gxy.data(), e, prm->theta, p, 0, mxy.data());
+        const bool sl = prm->mask_rule == 0;  // slope bound on
+        auto G = [&](std::vector<float>& v) { return sl ? v.data() : nullptr; };
+        truncation_mask(cx.k, cx.k, d, cxf.data(), cx.radii.data(), Fxx.data(), G(gxx), cxf.data(), cx.radii.data(), Fxx.data(), G(gxx), e, prm->theta, p, 1, mxx.data());
+        truncation_mask(cy.k, cy.k, d, cyf.data(), cy.radii.data(), Gyy.data(), G(gyy), cyf.data(), cy.radii.data(), Gyy.data(), G(gyy), e, prm->theta, p, 1, myy.data());
+        truncation_mask(cx.k, cy.k, d, cxf.data(), cx.radii.data(), Fyx.data(), G(gyx), cyf.data(), cy.radii.data(), Gxy.data(), G(gxy), e, prm->theta, p, 0, mxy.data());
       }
       myx.resize(size_t(cy.k) * cx.k);
       for (int64_t I = 0; I < cx.k; ++I)

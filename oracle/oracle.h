@@ -42,9 +42,9 @@ int oracle_grid_cluster(const double* x, const double* w, int64_t n, int d,
 
 /* Truncation mask: same contract as msot_truncation_mask. */
 void oracle_truncation_mask(int64_t kx, int64_t ky, int d, const float* cx, const float* rx,
-                            const float* fx, const float* cy, const float* ry,
-                            const float* gy, double eps, double theta, double p, int self,
-                            uint8_t* mask_out);
+                            const float* fx, const float* gx, const float* cy, const float* ry,
+                            const float* gy, const float* hy, double eps, double theta, double p,
+                            int self, uint8_t* mask_out);
 
 /* Cluster-aligned row tiles (policy.h:msot_pack_tiles) and the column
  * ranges of each tile from a cluster mask.  Returns the number of ranges

@@ -40,7 +40,7 @@ def lib():
                                           _ip, _ip, _ip, _dp, _dp, _fp]
         L.oracle_truncation_mask.restype = None
         L.oracle_truncation_mask.argtypes = [C.c_int64, C.c_int64, C.c_int, _fp, _fp, _fp,
-                                             _fp, _fp, _fp, C.c_double, C.c_double,
+                                             _fp, _fp, _fp, _fp, _fp, C.c_double, C.c_double,
                                              C.c_double, C.c_int, _bp]
         L.oracle_tile_ranges.restype = C.c_int64
         L.oracle_tile_ranges.argtypes = [_ip, _ip, C.c_int64, C.c_int64, _ip, C.c_int64, _bp,
@@ -109,15 +109,18 @@ def grid_cluster(x, w, origin, cell):
                 centroids=cen[:K].copy(), cweights=cw[:K].copy(), radii=rad[:K].copy())
 
 
-def truncation_mask(cx, rx, fx, cy, ry, gy, eps, theta, p=2.0, self_=False):
+def truncation_mask(cx, rx, fx, cy, ry, gy, eps, theta, p=2.0, self_=False, gx=None, hy=None):
     f32 = lambda a: np.ascontiguousarray(a, dtype=np.float32)
     cx, rx, fx, cy, ry, gy = map(f32, (cx, rx, fx, cy, ry, gy))
     kx, d = cx.shape
     ky = cy.shape[0]
     out = np.zeros((kx, ky), np.uint8)
-    fp = lambda a: a.ctypes.data_as(_fp)
-    lib().oracle_truncation_mask(kx, ky, d, fp(cx), fp(rx), fp(fx), fp(cy), fp(ry), fp(gy),
-                                 eps, theta, p, int(self_), out.ctypes.data_as(_bp))
+    fp = lambda a: None if a is None else a.ctypes.data_as(_fp)
+    gx = None if gx is None else f32(gx)
+    hy = None if hy is None else f32(hy)
+    lib().oracle_truncation_mask(kx, ky, d, fp(cx), fp(rx), fp(fx), fp(gx), fp(cy), fp(ry),
+                                 fp(gy), fp(hy), eps, theta, p, int(self_),
+                                 out.ctypes.data_as(_bp))
     return out
 
 

@@ -144,23 +144,104 @@ cudaError_t cluster_stats(const float4* pts, const double* w64, const int32_t* o
   return cudaGetLastError();
 }
 
-// Per-cluster max of a fine potential, rounded up to float (mask inputs).
-__global__ void cluster_max_kernel(const float* v, const int32_t* off, int32_t k, float* out) {
+// Per-cluster bound inputs of the truncation test (mask.cu) from a fine
+// potential f over the cluster's members u_i = x_i - X_I:
+//   fmax  = max_i f_i
+//   grad  = {G, F'}: G the w-weighted least-squares slope of f in u (float),
+//           F' = max_i (f_i - <G, u_i>) in float64, rounded up.
+// Any G gives a valid bound; the fitted slope makes the margin small.
+__device__ __forceinline__ void solve3(double m00, double m01, double m02, double m11, double m12,
+                                       double m22, double b0, double b1, double b2, double* g) {
+  const double tr = m00 + m11 + m22;
+  const double reg = 1e-9 * tr + 1e-300;
+  m00 += reg;
+  m11 += reg;
+  m22 += reg;
+  const double c00 = m11 * m22 - m12 * m12, c01 = m02 * m12 - m01 * m22,
+               c02 = m01 * m12 - m02 * m11;
+  const double det = m00 * c00 + m01 * c01 + m02 * c02;
+  if (!(det > 0.0) || !isfinite(det)) {
+    g[0] = g[1] = g[2] = 0.0;
+    return;
+  }
+  const double c11 = m00 * m22 - m02 * m02, c12 = m01 * m02 - m00 * m12,
+               c22 = m00 * m11 - m01 * m01;
+  g[0] = (c00 * b0 + c01 * b1 + c02 * b2) / det;
+  g[1] = (c01 * b0 + c11 * b1 + c12 * b2) / det;
+  g[2] = (c02 * b0 + c12 * b1 + c22 * b2) / det;
+}
+
+__global__ void cluster_bound_kernel(const float4* pts, const double* w64, const float* f,
+                                     const int32_t* off, const float4* cen, int32_t k,
+                                     float* fmax_out, float4* grad) {
   const int lane = threadIdx.x & 31;
   const int64_t I = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (I >= k) return;
-  float m = -INFINITY;
-  for (int32_t s = off[I] + lane; s < off[I + 1]; s += 32) m = fmaxf(m, v[s]);
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if (lane == 0) out[I] = m;
+  const int32_t s0 = off[I], s1 = off[I + 1];
+  const float4 X = cen[I];
+  double m[6] = {0, 0, 0, 0, 0, 0}, b[3] = {0, 0, 0}, W = 0.0, wf = 0.0;
+  for (int32_t s = s0 + lane; s < s1; s += 32) {
+    const float4 p = pts[s];
+    const double w = w64[s], fv = f[s];
+    const double u0 = static_cast<double>(p.x) - X.x, u1 = static_cast<double>(p.y) - X.y,
+                 u2 = static_cast<double>(p.z) - X.z;
+    m[0] += w * u0 * u0; m[1] += w * u0 * u1; m[2] += w * u0 * u2;
+    m[3] += w * u1 * u1; m[4] += w * u1 * u2; m[5] += w * u2 * u2;
+    W += w;
+    wf += w * fv;
+    b[0] += w * u0 * fv; b[1] += w * u1 * fv; b[2] += w * u2 * fv;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    for (int q = 0; q < 6; ++q) m[q] += __shfl_xor_sync(0xffffffffu, m[q], o);
+    for (int q = 0; q < 3; ++q) b[q] += __shfl_xor_sync(0xffffffffu, b[q], o);
+    W += __shfl_xor_sync(0xffffffffu, W, o);
+    wf += __shfl_xor_sync(0xffffffffu, wf, o);
+  }
+  // centre f on its mean: sum w u (f - fbar) = sum w u f - fbar sum w u
+  double mu[3] = {0, 0, 0};
+  for (int32_t s = s0 + lane; s < s1; s += 32) {
+    const float4 p = pts[s];
+    const double w = w64[s];
+    mu[0] += w * (static_cast<double>(p.x) - X.x);
+    mu[1] += w * (static_cast<double>(p.y) - X.y);
+    mu[2] += w * (static_cast<double>(p.z) - X.z);
+  }
+  for (int o = 16; o > 0; o >>= 1)
+    for (int q = 0; q < 3; ++q) mu[q] += __shfl_xor_sync(0xffffffffu, mu[q], o);
+  const double fbar = wf / W;
+  double g[3];
+  solve3(m[0], m[1], m[2], m[3], m[4], m[5], b[0] - fbar * mu[0], b[1] - fbar * mu[1],
+         b[2] - fbar * mu[2], g);
+  const float4 G = make_float4(__double2float_rn(g[0]), __double2float_rn(g[1]),
+                               __double2float_rn(g[2]), 0.f);
+  float fm = -INFINITY;
+  double fp = -INFINITY;
+  for (int32_t s = s0 + lane; s < s1; s += 32) {
+    const float4 p = pts[s];
+    const float fv = f[s];
+    fm = fmaxf(fm, fv);
+    const double lin = static_cast<double>(G.x) * (static_cast<double>(p.x) - X.x) +
+                       static_cast<double>(G.y) * (static_cast<double>(p.y) - X.y) +
+                       static_cast<double>(G.z) * (static_cast<double>(p.z) - X.z);
+    fp = fmax(fp, static_cast<double>(fv) - lin);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    fm = fmaxf(fm, __shfl_xor_sync(0xffffffffu, fm, o));
+    fp = fmax(fp, __shfl_xor_sync(0xffffffffu, fp, o));
+  }
+  if (lane == 0) {
+    fmax_out[I] = fm;
+    grad[I] = make_float4(G.x, G.y, G.z, __double2float_ru(fp));
+  }
 }
 
-cudaError_t cluster_max(const float* v, const int32_t* offsets, int32_t k, float* out,
-                        cudaStream_t st) {
+cudaError_t cluster_bound(const float4* pts, const double* w64, const float* f,
+                          const int32_t* offsets, const float4* cen, int32_t k, float* fmax,
+                          float4* grad, cudaStream_t st) {
   if (k <= 0) return cudaSuccess;
   const int64_t threads = static_cast<int64_t>(k) * 32;
-  ++g_launches; cluster_max_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st>>>(v, offsets, k,
-                                                                                  out);
+  ++g_launches; cluster_bound_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st>>>(
+      pts, w64, f, offsets, cen, k, fmax, grad);
   return cudaGetLastError();
 }
 

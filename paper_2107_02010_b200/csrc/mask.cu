@@ -1,63 +1,98 @@
 // mask.cu — K3: kernel truncation and the
 // ranges that feed the block-sparse softmin.
 //
-// Test per cluster pair (a per-pair distance bound in
-// place of SPEC.md:283's Lipschitz margin p (r_I + r_J) d^{p-1}):
-//   keep (I,J)  iff  F_I + G_J - (1/2) max(0, |X_I - Y_J| - r_I - r_J)^2 >= -theta eps
-// where F, G are per-cluster maxima of the current fine potentials, so the
-// left side bounds f_i + g_j - C(x_i, y_j) from above for every member pair:
-// a dropped block carries plan mass <= alpha_i beta_j e^{-theta} per pair.
+// Test per cluster pair (per-pair bounds in place of
+// SPEC.md:283's Lipschitz margin p (r_I + r_J) d^{p-1}): keep (I,J) iff
+//   min(B_a, B_b) >= -theta eps,   D = X_I - Y_J,
+//   B_a = F_I + G_J - (1/2) max(0, |D| - (r_I + r_J))^2
+//   B_b = F'_I + G'_J + r_I |G_I - D| + r_J |H_J + D| - |D|^2 / 2
+// F, G are per-cluster maxima of the current fine potentials; G_I, H_J any
+// per-cluster vectors (the fitted slopes of f, g) with F'_I = max_i (f_i -
+// <G_I, x_i - X_I>), G'_J likewise.  Both bound f_i + g_j - C(x_i, y_j) from
+// above for every member pair (expand |D + u - v|^2, Cauchy-Schwarz), so a
+// dropped block carries plan mass <= alpha_i beta_j e^{-theta} per pair.
+// B_b's margin vanishes where Y_J sits at the transport image of X_I
+// (grad f = x - T(x)), instead of growing with the transport distance.
 // Evaluated in float64 with explicitly rounded operations (no FMA) on
-// float32 inputs: bit-identical to oracle.cpp:pair_slack on the same inputs.
+// float32 inputs; the formula is symmetric in (I, J), so the mask of the
+// transposed problem is the exact transpose.  Bit-identical to
+// oracle.cpp:pair_slack on the same inputs.
+//
+// Layout: masks are bit-packed rows, W = ceil(Ky/32) words per row cluster.
+// Ranges: per row tile, OR the rows of the tile's clusters (tile_or), then
+// turn runs of set bits into sorted-column ranges [co[J0], co[J1+1])
+// (tile_runs), one warp per tile, 1024 column clusters per step.
 #include "prims.cuh"
 
 namespace msot_dev {
 
-__device__ __forceinline__ double pair_slack(float4 X, float rI, float F, float4 Y, float rJ,
-                                             float G, int d) {
-  double s = 0.0;
-  double t = __dsub_rn(static_cast<double>(X.x), static_cast<double>(Y.x));
-  s = __dadd_rn(s, __dmul_rn(t, t));
-  if (d > 1) {
-    t = __dsub_rn(static_cast<double>(X.y), static_cast<double>(Y.y));
-    s = __dadd_rn(s, __dmul_rn(t, t));
-  }
-  if (d > 2) {
-    t = __dsub_rn(static_cast<double>(X.z), static_cast<double>(Y.z));
-    s = __dadd_rn(s, __dmul_rn(t, t));
-  }
-  double lb = __dsub_rn(__dsqrt_rn(s), static_cast<double>(rI));
-  lb = __dsub_rn(lb, static_cast<double>(rJ));
+__device__ __forceinline__ double pair_slack(float4 X, float rI, float F, float4 GI, float4 Y,
+                                             float rJ, float G, float4 HJ, int d, bool grad) {
+  const double d0 = __dsub_rn(static_cast<double>(X.x), static_cast<double>(Y.x));
+  const double d1 = d > 1 ? __dsub_rn(static_cast<double>(X.y), static_cast<double>(Y.y)) : 0.0;
+  const double d2 = d > 2 ? __dsub_rn(static_cast<double>(X.z), static_cast<double>(Y.z)) : 0.0;
+  const double s = __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
+  // (a) centroid/radius bound
+  const double rr = __dadd_rn(static_cast<double>(rI), static_cast<double>(rJ));
+  double lb = __dsub_rn(__dsqrt_rn(s), rr);
   if (lb < 0.0) lb = 0.0;
-  const double c = __dmul_rn(0.5, __dmul_rn(lb, lb));
   const double fg = __dadd_rn(static_cast<double>(F), static_cast<double>(G));
-  return __dsub_rn(fg, c);
+  const double va = __dsub_rn(fg, __dmul_rn(0.5, __dmul_rn(lb, lb)));
+  if (!grad) return va;
+  // (b) slope bound: F'_I + G'_J + r_I |G_I - D| + r_J |H_J + D| - |D|^2 / 2
+  const double a0 = __dsub_rn(static_cast<double>(GI.x), d0);
+  const double a1 = __dsub_rn(static_cast<double>(GI.y), d1);
+  const double a2 = __dsub_rn(static_cast<double>(GI.z), d2);
+  const double b0 = __dadd_rn(static_cast<double>(HJ.x), d0);
+  const double b1 = __dadd_rn(static_cast<double>(HJ.y), d1);
+  const double b2 = __dadd_rn(static_cast<double>(HJ.z), d2);
+  const double na = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(a0, a0), __dmul_rn(a1, a1)), __dmul_rn(a2, a2)));
+  const double nb = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(b0, b0), __dmul_rn(b1, b1)), __dmul_rn(b2, b2)));
+  const double marg = __dadd_rn(__dmul_rn(static_cast<double>(rI), na), __dmul_rn(static_cast<double>(rJ), nb));
+  const double fgp = __dadd_rn(static_cast<double>(GI.w), static_cast<double>(HJ.w));
+  const double vb = __dsub_rn(__dadd_rn(fgp, marg), __dmul_rn(0.5, s));
+  return va < vb ? va : vb;
 }
 
-__global__ void mask_kernel(int32_t kx, int32_t ky, int d, const float4* cx, const float* rx,
-                            const float* fx, const float4* cy, const float* ry, const float* gy,
-                            double thr, int self, uint8_t* mask) {
-  const int32_t J = blockIdx.x * blockDim.x + threadIdx.x;
+struct MaskIn {
+  int32_t kx, ky, d, words;
+  const float4 *cx, *cy;
+  const float *rx, *ry, *fx, *gy;
+  const float4 *gx, *hy;  // {slope, F'} per cluster, both or neither
+  __device__ __forceinline__ double slack(int32_t I, int32_t J) const {
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    const bool g = gx != nullptr;
+    return pair_slack(cx[I], rx[I], fx[I], g ? gx[I] : z, cy[J], ry[J], gy[J], g ? hy[J] : z, d, g);
+  }
+};
+
+__global__ void mask_bits_kernel(MaskIn m, double thr, int self, uint32_t* mask) {
+  const int32_t w = blockIdx.x * blockDim.x + threadIdx.x;
   const int32_t I = blockIdx.y;
-  if (J >= ky) return;
-  const double v = pair_slack(cx[I], rx[I], fx[I], cy[J], ry[J], gy[J], d);
-  mask[static_cast<int64_t>(I) * ky + J] = (v >= thr || (self && I == J)) ? 1 : 0;
+  if (w >= m.words) return;
+  uint32_t bits = 0;
+  const int32_t J0 = w * 32;
+  const int32_t nb = min(32, m.ky - J0);
+  for (int b = 0; b < nb; ++b) {
+    const int32_t J = J0 + b;
+    const double v = m.slack(I, J);
+    if (v >= thr || (self && I == J)) bits |= 1u << b;
+  }
+  mask[static_cast<int64_t>(I) * m.words + w] = bits;
 }
 
-// best pair of each row (ties -> lowest J) and of each column (ties -> lowest I)
-__global__ void best_kernel(int32_t kx, int32_t ky, int d, const float4* cx, const float* rx,
-                            const float* fx, const float4* cy, const float* ry, const float* gy,
-                            int by_col, uint8_t* mask) {
+// best pair of each row (ties -> lowest J) or each column (ties -> lowest I)
+__global__ void best_kernel(MaskIn m, int by_col, uint32_t* mask) {
   const int lane = threadIdx.x & 31;
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int32_t nw = by_col ? ky : kx, nl = by_col ? kx : ky;
+  const int32_t nw = by_col ? m.ky : m.kx, nl = by_col ? m.kx : m.ky;
   if (w >= nw) return;
   double best = -INFINITY;
   int32_t arg = 0x7fffffff;
   for (int32_t q = lane; q < nl; q += 32) {
     const int32_t I = by_col ? q : static_cast<int32_t>(w);
     const int32_t J = by_col ? static_cast<int32_t>(w) : q;
-    const double v = pair_slack(cx[I], rx[I], fx[I], cy[J], ry[J], gy[J], d);
+    const double v = m.slack(I, J);
     if (v > best) { best = v; arg = q; }
   }
   for (int o = 16; o > 0; o >>= 1) {
@@ -67,115 +102,135 @@ __global__ void best_kernel(int32_t kx, int32_t ky, int d, const float4* cx, con
   }
   if (lane == 0 && arg != 0x7fffffff) {
     const int64_t I = by_col ? arg : w, J = by_col ? w : arg;
-    mask[I * ky + J] = 1;
+    atomicOr(&mask[I * m.words + (J >> 5)], 1u << (J & 31));
   }
 }
 
 cudaError_t truncation_mask(int32_t kx, int32_t ky, int d, const float4* cx, const float* rx,
-                            const float* fx, const float4* cy, const float* ry, const float* gy,
-                            double eps, double theta, int self, uint8_t* mask, cudaStream_t st) {
+                            const float* fx, const float4* gx, const float4* cy, const float* ry,
+                            const float* gy, const float4* hy, double eps, double theta, int self,
+                            uint32_t* mask, cudaStream_t st) {
   if (kx <= 0 || ky <= 0) return cudaSuccess;
+  if ((gx == nullptr) != (hy == nullptr)) return cudaErrorInvalidValue;
+  MaskIn m{kx, ky, d, mask_words(ky), cx, cy, rx, ry, fx, gy, gx, hy};
   const double thr = -(theta * eps);
-  dim3 grid((ky + 255) / 256, kx);
-  ++g_launches; mask_kernel<<<grid, 256, 0, st>>>(kx, ky, d, cx, rx, fx, cy, ry, gy, thr, self, mask);
-  ++g_launches; best_kernel<<<static_cast<unsigned>((static_cast<int64_t>(kx) * 32 + 255) / 256), 256, 0, st>>>(
-      kx, ky, d, cx, rx, fx, cy, ry, gy, 0, mask);
-  ++g_launches; best_kernel<<<static_cast<unsigned>((static_cast<int64_t>(ky) * 32 + 255) / 256), 256, 0, st>>>(
-      kx, ky, d, cx, rx, fx, cy, ry, gy, 1, mask);
+  dim3 grid((m.words + 127) / 128, kx);
+  ++g_launches; mask_bits_kernel<<<grid, 128, 0, st>>>(m, thr, self, mask);
+  ++g_launches; best_kernel<<<static_cast<unsigned>((static_cast<int64_t>(kx) * 32 + 255) / 256), 256, 0, st>>>(m, 0, mask);
+  ++g_launches; best_kernel<<<static_cast<unsigned>((static_cast<int64_t>(ky) * 32 + 255) / 256), 256, 0, st>>>(m, 1, mask);
   return cudaGetLastError();
 }
 
-__global__ void transpose_kernel(const uint8_t* m, int32_t kx, int32_t ky, uint8_t* mt) {
-  __shared__ uint8_t t[32][33];
-  const int32_t bx = blockIdx.x * 32, by = blockIdx.y * 32;
-  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-    const int32_t I = by + r, J = bx + threadIdx.x;
-    if (I < kx && J < ky) t[r][threadIdx.x] = m[static_cast<int64_t>(I) * ky + J];
-  }
-  __syncthreads();
-  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-    const int32_t J = bx + r, I = by + threadIdx.x;
-    if (I < kx && J < ky) mt[static_cast<int64_t>(J) * kx + I] = t[threadIdx.x][r];
-  }
+__global__ void unpack_kernel(const uint32_t* mask, int32_t kx, int32_t ky, uint8_t* out) {
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g >= static_cast<int64_t>(kx) * ky) return;
+  const int64_t I = g / ky, J = g % ky;
+  out[g] = (mask[I * mask_words(ky) + (J >> 5)] >> (J & 31)) & 1u;
 }
 
-cudaError_t transpose_mask(const uint8_t* m, int32_t kx, int32_t ky, uint8_t* mt,
-                           cudaStream_t st) {
-  if (kx <= 0 || ky <= 0) return cudaSuccess;
-  dim3 grid((ky + 31) / 32, (kx + 31) / 32), block(32, 8);
-  ++g_launches; transpose_kernel<<<grid, block, 0, st>>>(m, kx, ky, mt);
+cudaError_t unpack_mask(const uint32_t* mask, int32_t kx, int32_t ky, uint8_t* out,
+                        cudaStream_t st) {
+  const int64_t n = static_cast<int64_t>(kx) * ky;
+  if (n <= 0) return cudaSuccess;
+  ++g_launches; unpack_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(mask, kx, ky, out);
   return cudaGetLastError();
 }
 
 // ---- ranges per row tile -------------------------------------------------
-// One warp per tile: OR the mask rows of the clusters the tile touches, then
-// turn runs of kept column clusters into sorted-column ranges [co[J0], co[J1+1]).
-__device__ __forceinline__ bool tile_keep(const uint8_t* mask, int32_t ky, int32_t I0, int32_t I1,
-                                          int32_t J) {
-  if (J >= ky) return false;
-  for (int32_t I = I0; I <= I1; ++I)
-    if (mask[static_cast<int64_t>(I) * ky + J]) return true;
-  return false;
+__global__ void tile_or_kernel(const uint32_t* mask, int32_t words, const int32_t* rl,
+                               const int32_t* ts, int64_t nt, uint32_t* tbits) {
+  const int32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t t = blockIdx.y;
+  if (w >= words || t >= nt) return;
+  const int32_t I0 = rl[ts[t]], I1 = rl[ts[t + 1] - 1];
+  uint32_t b = 0;
+  for (int32_t I = I0; I <= I1; ++I) b |= mask[static_cast<int64_t>(I) * words + w];
+  tbits[t * words + w] = b;
 }
 
 template <bool kWrite>
-__global__ void tile_ranges_kernel(const int32_t* rl, const int32_t* ts, int64_t n_tiles,
-                                   const int32_t* co, int32_t ky, const uint8_t* mask,
-                                   int64_t* n_ranges, int64_t* n_cols, const int64_t* rptr,
-                                   int2* ranges) {
+__global__ void tile_runs_kernel(const uint32_t* tbits, int32_t words, int64_t nt,
+                                 const int32_t* co, int64_t* n_ranges, int64_t* n_cols,
+                                 const int64_t* rptr, int2* ranges) {
   const int lane = threadIdx.x & 31;
   const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (t >= n_tiles) return;
-  const int32_t I0 = rl[ts[t]];
-  const int32_t I1 = rl[ts[t + 1] - 1];
-  const unsigned lt = (1u << lane) - 1u;
-  int64_t nr = 0, nc = 0;
-  int64_t base = kWrite ? rptr[t] : 0;
-  int64_t ns = 0, ne = 0;  // starts / ends written so far
-  bool prev = false;       // keep[J0 - 1]
-  for (int32_t J0 = 0; J0 < ky; J0 += 32) {
-    const int32_t J = J0 + lane;
-    const bool k = tile_keep(mask, ky, I0, I1, J);
-    const unsigned b = __ballot_sync(0xffffffffu, k);
-    const bool next = (lane < 31) ? ((b >> (lane + 1)) & 1u) : tile_keep(mask, ky, I0, I1, J0 + 32);
-    const bool left = (lane > 0) ? ((b >> (lane - 1)) & 1u) : prev;
-    const bool is_start = k && !left, is_end = k && !next;
-    const unsigned bs = __ballot_sync(0xffffffffu, is_start);
-    const unsigned be = __ballot_sync(0xffffffffu, is_end);
-    if (kWrite) {
-      if (is_start) ranges[base + ns + __popc(bs & lt)].x = co[J];
-      if (is_end) ranges[base + ne + __popc(be & lt)].y = co[J + 1];
+  if (t >= nt) return;
+  const uint32_t* tb = tbits + t * words;
+  int64_t ns = 0, ne = 0, cols = 0;
+  const int64_t base = kWrite ? rptr[t] : 0;
+  uint32_t carry = 0;  // top bit of the previous word
+  for (int32_t w0 = 0; w0 < words; w0 += 32) {
+    const int32_t w = w0 + lane;
+    const uint32_t b = w < words ? tb[w] : 0u;
+    const uint32_t up = __shfl_up_sync(0xffffffffu, b, 1);
+    const uint32_t cin = lane == 0 ? carry : (up >> 31);
+    uint32_t dn = __shfl_down_sync(0xffffffffu, b, 1);
+    if (lane == 31) dn = (w0 + 32 < words) ? tb[w0 + 32] : 0u;
+    const uint32_t starts = b & ~((b << 1) | cin);
+    const uint32_t ends = b & ~((b >> 1) | ((dn & 1u) << 31));
+    // warp prefix counts (a run may start in one lane and end in another)
+    const int ps = __popc(starts), pe = __popc(ends);
+    int xs = ps, xe = pe;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int ys = __shfl_up_sync(0xffffffffu, xs, o);
+      const int ye = __shfl_up_sync(0xffffffffu, xe, o);
+      if (lane >= o) { xs += ys; xe += ye; }
     }
-    ns += __popc(bs);
-    ne += __popc(be);
-    if (!kWrite && k) nc += co[J + 1] - co[J];
-    prev = __shfl_sync(0xffffffffu, k, 31);
+    int64_t ks = ns + xs - ps, ke = ne + xe - pe;
+    uint32_t s = starts, e = ends;
+    while (s) {
+      const int bpos = __ffs(s) - 1;
+      s &= s - 1;
+      const int32_t J = w * 32 + bpos;
+      if (kWrite) ranges[base + ks].x = co[J];
+      else cols -= co[J];
+      ++ks;
+    }
+    while (e) {
+      const int bpos = __ffs(e) - 1;
+      e &= e - 1;
+      const int32_t J = w * 32 + bpos;
+      if (kWrite) ranges[base + ke].y = co[J + 1];
+      else cols += co[J + 1];
+      ++ke;
+    }
+    ns += __shfl_sync(0xffffffffu, xs, 31);
+    ne += __shfl_sync(0xffffffffu, xe, 31);
+    carry = __shfl_sync(0xffffffffu, b, 31) >> 31;
   }
-  nr = ns;
   if (!kWrite) {
-    for (int o = 16; o > 0; o >>= 1) nc += __shfl_xor_sync(0xffffffffu, nc, o);
+    for (int o = 16; o > 0; o >>= 1) cols += __shfl_xor_sync(0xffffffffu, cols, o);
     if (lane == 0) {
-      n_ranges[t] = nr;
-      n_cols[t] = nc;
+      n_ranges[t] = ns;
+      n_cols[t] = cols;
     }
   }
 }
 
-cudaError_t tile_range_count(const int32_t* row_labels, const int32_t* tile_start, int64_t nt,
-                             const int32_t* col_offsets, int32_t ky, const uint8_t* mask,
-                             int64_t* n_ranges, int64_t* n_cols, cudaStream_t st) {
+cudaError_t tile_or(const uint32_t* mask, int32_t ky, const int32_t* row_labels,
+                    const int32_t* tile_start, int64_t nt, uint32_t* tbits, cudaStream_t st) {
   if (nt <= 0) return cudaSuccess;
-  ++g_launches; tile_ranges_kernel<false><<<static_cast<unsigned>((nt * 32 + 255) / 256), 256, 0, st>>>(
-      row_labels, tile_start, nt, col_offsets, ky, mask, n_ranges, n_cols, nullptr, nullptr);
+  const int32_t words = mask_words(ky);
+  dim3 grid((words + 127) / 128, static_cast<unsigned>(nt));
+  ++g_launches; tile_or_kernel<<<grid, 128, 0, st>>>(mask, words, row_labels, tile_start, nt, tbits);
   return cudaGetLastError();
 }
 
-cudaError_t tile_range_write(const int32_t* row_labels, const int32_t* tile_start, int64_t nt,
-                             const int32_t* col_offsets, int32_t ky, const uint8_t* mask,
-                             const int64_t* rptr, int2* ranges, cudaStream_t st) {
+cudaError_t tile_range_count(const uint32_t* tbits, int32_t ky, int64_t nt,
+                             const int32_t* col_offsets, int64_t* n_ranges, int64_t* n_cols,
+                             cudaStream_t st) {
   if (nt <= 0) return cudaSuccess;
-  ++g_launches; tile_ranges_kernel<true><<<static_cast<unsigned>((nt * 32 + 255) / 256), 256, 0, st>>>(
-      row_labels, tile_start, nt, col_offsets, ky, mask, nullptr, nullptr, rptr, ranges);
+  ++g_launches; tile_runs_kernel<false><<<static_cast<unsigned>((nt * 32 + 255) / 256), 256, 0, st>>>(
+      tbits, mask_words(ky), nt, col_offsets, n_ranges, n_cols, nullptr, nullptr);
+  return cudaGetLastError();
+}
+
+cudaError_t tile_range_write(const uint32_t* tbits, int32_t ky, int64_t nt,
+                             const int32_t* col_offsets, const int64_t* rptr, int2* ranges,
+                             cudaStream_t st) {
+  if (nt <= 0) return cudaSuccess;
+  ++g_launches; tile_runs_kernel<true><<<static_cast<unsigned>((nt * 32 + 255) / 256), 256, 0, st>>>(
+      tbits, mask_words(ky), nt, col_offsets, nullptr, nullptr, rptr, ranges);
   return cudaGetLastError();
 }
 

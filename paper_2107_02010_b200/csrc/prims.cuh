@@ -48,24 +48,31 @@ cudaError_t segment_offsets(const int32_t* labels, const uint8_t* flags, int64_t
 cudaError_t cluster_stats(const float4* pts, const double* w64, const int32_t* offsets, int32_t k,
                           int d, float4* cen, float* clw2, double* cw64, float* radii,
                           cudaStream_t st);
-cudaError_t cluster_max(const float* v, const int32_t* offsets, int32_t k, float* out,
-                        cudaStream_t st);
+cudaError_t cluster_bound(const float4* pts, const double* w64, const float* f,
+                          const int32_t* offsets, const float4* cen, int32_t k, float* fmax,
+                          float4* grad, cudaStream_t st);
 cudaError_t inherit(const float* coarse, const int32_t* labels, int64_t n, float* fine,
                     cudaStream_t st);
 
 // truncation mask + ranges (mask.cu)
+__host__ __device__ inline int32_t mask_words(int32_t ky) { return (ky + 31) / 32; }
+// bit-packed mask: Kx rows of mask_words(Ky) uint32 words
+// gx / hy (nullable): {slope G, F'} per cluster for the gradient bound
 cudaError_t truncation_mask(int32_t kx, int32_t ky, int d, const float4* cx, const float* rx,
-                            const float* fx, const float4* cy, const float* ry, const float* gy,
-                            double eps, double theta, int self, uint8_t* mask, cudaStream_t st);
-cudaError_t transpose_mask(const uint8_t* m, int32_t kx, int32_t ky, uint8_t* mt,
-                           cudaStream_t st);
-// per tile: count ranges and kept columns; then write ranges
-cudaError_t tile_range_count(const int32_t* row_labels, const int32_t* tile_start, int64_t nt,
-                             const int32_t* col_offsets, int32_t ky, const uint8_t* mask,
-                             int64_t* n_ranges, int64_t* n_cols, cudaStream_t st);
-cudaError_t tile_range_write(const int32_t* row_labels, const int32_t* tile_start, int64_t nt,
-                             const int32_t* col_offsets, int32_t ky, const uint8_t* mask,
-                             const int64_t* rptr, int2* ranges, cudaStream_t st);
+                            const float* fx, const float4* gx, const float4* cy, const float* ry,
+                            const float* gy, const float4* hy, double eps, double theta, int self,
+                            uint32_t* mask, cudaStream_t st);
+cudaError_t unpack_mask(const uint32_t* mask, int32_t kx, int32_t ky, uint8_t* out,
+                        cudaStream_t st);
+// per tile: OR of its clusters' mask rows, then count / write column ranges
+cudaError_t tile_or(const uint32_t* mask, int32_t ky, const int32_t* row_labels,
+                    const int32_t* tile_start, int64_t nt, uint32_t* tbits, cudaStream_t st);
+cudaError_t tile_range_count(const uint32_t* tbits, int32_t ky, int64_t nt,
+                             const int32_t* col_offsets, int64_t* n_ranges, int64_t* n_cols,
+                             cudaStream_t st);
+cudaError_t tile_range_write(const uint32_t* tbits, int32_t ky, int64_t nt,
+                             const int32_t* col_offsets, const int64_t* rptr, int2* ranges,
+                             cudaStream_t st);
 cudaError_t dense_ranges(int64_t n_tiles, int32_t n_cols, int64_t* rptr, int2* ranges,
                          int64_t* tile_cols, cudaStream_t st);
 // work items: per tile ceil(cols/chunk) items

@@ -8,8 +8,10 @@
 // kept columns (dense = one range per tile; block-sparse = the ranges of the
 // truncation mask).  Columns stream through a double-buffered shared-memory
 // tile, stored as float32 *pairs* so the inner loop runs on the packed
-// FADD2/FFMA2 pipe and issues ~5 instructions per pair next to the one
-// MUFU.EX2 that bounds it (roofline: 16 ex2/clk/SM).
+// FADD2/FFMA2 pipe: 5 packed ops per two pairs (the FMA pipe runs a packed
+// op in 2 cycles, so this is 5 FP32 lane-ops per pair against the 8 per ex2
+// the pipes balance at) next to the one MUFU.EX2 per pair that bounds it
+// (roofline: 16 ex2/clk/SM, measured by probe.cu).
 //
 // Fixed-reference expansion: instead of a running max, every row is
 // expanded around m_i = -est_i / (lambda eps ln2), its previous potential in
@@ -27,8 +29,8 @@
 namespace msot_dev {
 
 struct RowState {
-  float x0, x1, x2;  // scaled, tile-centred coordinates
-  float nr;          // -(est / (lambda eps ln2) - R), R = the tile's reference
+  float x0, x1, x2;  // 2 x scaled, tile-centred coordinates
+  float r;           // est/(lambda eps ln2) - R - |x^|^2   (log2 units)
 };
 
 template <int D>
@@ -36,11 +38,15 @@ __device__ __forceinline__ void load_row(const Problem& P, int r, int r_end, flo
                                          RowState& rs) {
   const bool ok = r < r_end;
   float4 v = ok ? P.rows[r] : o;
-  rs.x0 = (v.x - o.x) * P.sc;
-  rs.x1 = D > 1 ? (v.y - o.y) * P.sc : 0.f;
-  rs.x2 = D > 2 ? (v.z - o.z) * P.sc : 0.f;
-  float est = (P.row_est != nullptr && ok) ? P.row_est[r] : 0.f;
-  rs.nr = -fmaf(est, P.inv_lam_eps_ln2, -R);  // one rounding of a small number
+  const float a = (v.x - o.x) * P.sc;
+  const float b = D > 1 ? (v.y - o.y) * P.sc : 0.f;
+  const float c = D > 2 ? (v.z - o.z) * P.sc : 0.f;
+  rs.x0 = 2.f * a;
+  rs.x1 = 2.f * b;
+  rs.x2 = 2.f * c;
+  const float est = (P.row_est != nullptr && ok) ? P.row_est[r] : 0.f;
+  // one rounding of a small number for the potential part (see R below)
+  rs.r = fmaf(est, P.inv_lam_eps_ln2, -R) - fmaf(a, a, fmaf(b, b, c * c));
 }
 
 // Walks the concatenated column ranges of one tile: position -> column.
@@ -59,6 +65,22 @@ struct ColWalker {
     return -1;
   }
 };
+
+// Exponent of pair (i, j) in log2 units, expanded around the tile centre o:
+//   E_ij = c_j + r_i + <2 x^_i, y^_j>,  x^ = (x - o) sc, y^ = (y - o) sc,
+//   c_j  = log2 w_j + h_j/(eps ln2) + R - |y^_j|^2,
+//   r_i  = est_i/(lambda eps ln2) - R - |x^_i|^2
+// = log2 w_j + (h_j + est_i/lambda - |x_i - y_j|^2/2)/(eps ln2).  Per column
+// pair: one FADD2 + D FFMA2 + one FADD2 accumulate next to two MUFU.EX2.
+template <int D>
+__device__ __forceinline__ float2 pair_terms(const RowState& rs, float2 Y0, float2 Y1, float2 Y2,
+                                             float2 C) {
+  float2 e = __fadd2_rn(make_float2(rs.r, rs.r), C);
+  e = __ffma2_rn(make_float2(rs.x0, rs.x0), Y0, e);
+  if (D > 1) e = __ffma2_rn(make_float2(rs.x1, rs.x1), Y1, e);
+  if (D > 2) e = __ffma2_rn(make_float2(rs.x2, rs.x2), Y2, e);
+  return make_float2(ex2_approx(e.x), ex2_approx(e.y));
+}
 
 template <int D>
 __global__ void __launch_bounds__(kSoftminThreads)
@@ -104,18 +126,21 @@ softmin_kernel(const __grid_constant__ Group G) {
     }
   };
   auto stage = [&](float* buf) {
-    // pair record layout: [-y0a,-y0b,-y1a,-y1b,-y2a,-y2b,-ca,-cb]
+    // pair record layout: [y0a, y0b, y1a, y1b, y2a, y2b, ca, cb]
     float* rec = buf + (tid >> 1) * 8 + (tid & 1);
     if (cvalid) {
-      rec[0] = (o.x - cv.x) * P.sc;
-      rec[2] = D > 1 ? (o.y - cv.y) * P.sc : 0.f;
-      rec[4] = D > 2 ? (o.z - cv.z) * P.sc : 0.f;
-      rec[6] = -(fmaf(ch, P.inv_eps_ln2, R) + cl);
+      const float a = (cv.x - o.x) * P.sc;
+      const float b = D > 1 ? (cv.y - o.y) * P.sc : 0.f;
+      const float c = D > 2 ? (cv.z - o.z) * P.sc : 0.f;
+      rec[0] = a;
+      rec[2] = b;
+      rec[4] = c;
+      rec[6] = (fmaf(ch, P.inv_eps_ln2, R) + cl) - fmaf(a, a, fmaf(b, b, c * c));
     } else {
       rec[0] = 0.f;
       rec[2] = 0.f;
       rec[4] = 0.f;
-      rec[6] = __int_as_float(0x7f800000);  // +inf -> exp2(-inf) = 0
+      rec[6] = __int_as_float(0xff800000);  // -inf -> exp2(-inf) = 0
     }
   };
 
@@ -133,35 +158,9 @@ softmin_kernel(const __grid_constant__ Group G) {
       const float2 Y0 = make_float2(A.x, A.y);
       const float2 Y1 = make_float2(A.z, A.w);
       const float2 Y2 = make_float2(B.x, B.y);
-      const float2 NC = make_float2(B.z, B.w);
-      {
-        float2 q = __fadd2_rn(make_float2(ra.nr, ra.nr), NC);
-        const float2 d0 = __fadd2_rn(make_float2(ra.x0, ra.x0), Y0);
-        q = __ffma2_rn(d0, d0, q);
-        if (D > 1) {
-          const float2 d1 = __fadd2_rn(make_float2(ra.x1, ra.x1), Y1);
-          q = __ffma2_rn(d1, d1, q);
-        }
-        if (D > 2) {
-          const float2 d2 = __fadd2_rn(make_float2(ra.x2, ra.x2), Y2);
-          q = __ffma2_rn(d2, d2, q);
-        }
-        sa = __fadd2_rn(sa, make_float2(ex2_approx(-q.x), ex2_approx(-q.y)));
-      }
-      {
-        float2 q = __fadd2_rn(make_float2(rb.nr, rb.nr), NC);
-        const float2 d0 = __fadd2_rn(make_float2(rb.x0, rb.x0), Y0);
-        q = __ffma2_rn(d0, d0, q);
-        if (D > 1) {
-          const float2 d1 = __fadd2_rn(make_float2(rb.x1, rb.x1), Y1);
-          q = __ffma2_rn(d1, d1, q);
-        }
-        if (D > 2) {
-          const float2 d2 = __fadd2_rn(make_float2(rb.x2, rb.x2), Y2);
-          q = __ffma2_rn(d2, d2, q);
-        }
-        sb = __fadd2_rn(sb, make_float2(ex2_approx(-q.x), ex2_approx(-q.y)));
-      }
+      const float2 C = make_float2(B.z, B.w);
+      sa = __fadd2_rn(sa, pair_terms<D>(ra, Y0, Y1, Y2, C));
+      sb = __fadd2_rn(sb, pair_terms<D>(rb, Y0, Y1, Y2, C));
     }
     buf ^= 1;
   }

@@ -240,14 +240,16 @@ void dense_rangeset(msot_ctx* c, const std::string& tag, int64_t rows, int64_t c
 // offsets `co` (ky)
 void mask_rangeset(msot_ctx* c, const std::string& tag, const int32_t* rl,
                    const std::vector<int32_t>& ro, int64_t n_rows, const int32_t* co, int32_t ky,
-                   const uint8_t* mask, RangeSet& R) {
+                   const uint32_t* mask, RangeSet& R) {
   cudaStream_t st = c->st;
-  make_tiles(c, tag, n_rows, &ro, R);
+  if (R.tile_start_h.empty()) make_tiles(c, tag, n_rows, &ro, R);  // fixed per solve
   int64_t* nr = c->buf<int64_t>(tag + ".nr", R.n_tiles + 1);
   R.tile_cols = c->buf<int64_t>(tag + ".tcols", R.n_tiles);
   R.rptr = c->buf<int64_t>(tag + ".rptr", R.n_tiles + 1);
   int64_t* stmp = c->buf<int64_t>(tag + ".stmp", scan_temp_elems(R.n_tiles + 1));
-  CK(tile_range_count(rl, R.tile_start, R.n_tiles, co, ky, mask, nr, R.tile_cols, st));
+  uint32_t* tbits = c->buf<uint32_t>(tag + ".tbits", size_t(R.n_tiles) * mask_words(ky));
+  CK(tile_or(mask, ky, rl, R.tile_start, R.n_tiles, tbits, st));
+  CK(tile_range_count(tbits, ky, R.n_tiles, co, nr, R.tile_cols, st));
   CK(cudaMemsetAsync(nr + R.n_tiles, 0, sizeof(int64_t), st));
   CK((scan<int64_t, int64_t>(nr, R.rptr, R.n_tiles + 1, false, stmp, nullptr, st)));
   CK(cudaMemcpyAsync(&R.n_ranges, R.rptr + R.n_tiles, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -256,7 +258,7 @@ void mask_rangeset(msot_ctx* c, const std::string& tag, const int32_t* rl,
                      cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   R.ranges = c->buf<int2>(tag + ".ranges", R.n_ranges);
-  CK(tile_range_write(rl, R.tile_start, R.n_tiles, co, ky, mask, R.rptr, R.ranges, st));
+  CK(tile_range_write(tbits, ky, R.n_tiles, co, R.rptr, R.ranges, st));
 }
 
 // ------------------------------------------------------------ launch plans
@@ -616,36 +618,50 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
       run_group(c, Pe, a, ss);
     }
     // fine phase: block-sparse updates restricted to the truncation masks
-    uint8_t* mxx = c->buf<uint8_t>("m.xx", size_t(X.k) * X.k);
-    uint8_t* myy = c->buf<uint8_t>("m.yy", size_t(Y.k) * Y.k);
-    uint8_t* mxy = c->buf<uint8_t>("m.xy", size_t(X.k) * Y.k);
-    uint8_t* myx = c->buf<uint8_t>("m.yx", size_t(Y.k) * X.k);
+    uint32_t* mxx = c->buf<uint32_t>("m.xx", size_t(X.k) * mask_words(X.k));
+    uint32_t* myy = c->buf<uint32_t>("m.yy", size_t(Y.k) * mask_words(Y.k));
+    uint32_t* mxy = c->buf<uint32_t>("m.xy", size_t(X.k) * mask_words(Y.k));
+    uint32_t* myx = c->buf<uint32_t>("m.yx", size_t(Y.k) * mask_words(X.k));
     float* fmax[4];
     fmax[0] = c->buf<float>("m.Fxx", X.k);
     fmax[1] = c->buf<float>("m.Gyy", Y.k);
     fmax[2] = c->buf<float>("m.Gxy", Y.k);
     fmax[3] = c->buf<float>("m.Fyx", X.k);
+    float4* grad[4];
+    grad[0] = c->buf<float4>("m.gxx", X.k);
+    grad[1] = c->buf<float4>("m.gyy", Y.k);
+    grad[2] = c->buf<float4>("m.gxy", Y.k);
+    grad[3] = c->buf<float4>("m.gyx", X.k);
     RangeSet rxx, ryy, rxy, ryx;
     Plan Pf;
     auto build_masks = [&](double e) {
-      if (tsw == 0) {
-        CK(cudaMemsetAsync(mxx, 1, size_t(X.k) * X.k, st));
-        CK(cudaMemsetAsync(myy, 1, size_t(Y.k) * Y.k, st));
-        CK(cudaMemsetAsync(mxy, 1, size_t(X.k) * Y.k, st));
+      // without a coarse phase there is no information: keep every pair
+      const bool info = tsw > 0;
+      const double theta = info ? prm->theta : INFINITY;
+      if (!info) {
+        CK(cudaMemsetAsync(fmax[0], 0, X.k * sizeof(float), st));
+        CK(cudaMemsetAsync(fmax[1], 0, Y.k * sizeof(float), st));
+        CK(cudaMemsetAsync(fmax[2], 0, Y.k * sizeof(float), st));
+        CK(cudaMemsetAsync(fmax[3], 0, X.k * sizeof(float), st));
       } else {
         float** f = U.v[cur];
-        CK(cluster_max(f[0], X.offsets, X.k, fmax[0], st));
-        CK(cluster_max(f[1], Y.offsets, Y.k, fmax[1], st));
-        CK(cluster_max(f[2], Y.offsets, Y.k, fmax[2], st));
-        CK(cluster_max(f[3], X.offsets, X.k, fmax[3], st));
-        CK(truncation_mask(X.k, X.k, d, X.cpts, X.radii, fmax[0], X.cpts, X.radii, fmax[0], e,
-                           prm->theta, 1, mxx, st));
-        CK(truncation_mask(Y.k, Y.k, d, Y.cpts, Y.radii, fmax[1], Y.cpts, Y.radii, fmax[1], e,
-                           prm->theta, 1, myy, st));
-        CK(truncation_mask(X.k, Y.k, d, X.cpts, X.radii, fmax[3], Y.cpts, Y.radii, fmax[2], e,
-                           prm->theta, 0, mxy, st));
+        CK(cluster_bound(X.pts, X.w64, f[0], X.offsets, X.cpts, X.k, fmax[0], grad[0], st));
+        CK(cluster_bound(Y.pts, Y.w64, f[1], Y.offsets, Y.cpts, Y.k, fmax[1], grad[1], st));
+        CK(cluster_bound(Y.pts, Y.w64, f[2], Y.offsets, Y.cpts, Y.k, fmax[2], grad[2], st));
+        CK(cluster_bound(X.pts, X.w64, f[3], X.offsets, X.cpts, X.k, fmax[3], grad[3], st));
       }
-      CK(transpose_mask(mxy, X.k, Y.k, myx, st));
+      float4* g[4];
+      for (int q = 0; q < 4; ++q) g[q] = (info && prm->mask_rule == 0) ? grad[q] : nullptr;
+      CK(truncation_mask(X.k, X.k, d, X.cpts, X.radii, fmax[0], g[0], X.cpts, X.radii, fmax[0],
+                         g[0], e, theta, 1, mxx, st));
+      CK(truncation_mask(Y.k, Y.k, d, Y.cpts, Y.radii, fmax[1], g[1], Y.cpts, Y.radii, fmax[1],
+                         g[1], e, theta, 1, myy, st));
+      // cross pair: (F, G) = (max b_yx, max a_xy); the slack is symmetric, so
+      // the yx mask computed with swapped roles is the exact transpose
+      CK(truncation_mask(X.k, Y.k, d, X.cpts, X.radii, fmax[3], g[3], Y.cpts, Y.radii, fmax[2],
+                         g[2], e, theta, 0, mxy, st));
+      CK(truncation_mask(Y.k, X.k, d, Y.cpts, Y.radii, fmax[2], g[2], X.cpts, X.radii, fmax[3],
+                         g[3], e, theta, 0, myx, st));
       mask_rangeset(c, "f.xx", X.labels, X.offsets_h, n, X.offsets, X.k, mxx, rxx);
       mask_rangeset(c, "f.yy", Y.labels, Y.offsets_h, m, Y.offsets, Y.k, myy, ryy);
       mask_rangeset(c, "f.yx", X.labels, X.offsets_h, n, Y.offsets, Y.k, mxy, ryx);  // rows x, cols y
@@ -1027,26 +1043,27 @@ int msot_grid_cluster(msot_ctx* c, const double* x, const double* w, int64_t n, 
 }
 
 int msot_truncation_mask(msot_ctx* c, int64_t kx, int64_t ky, int d, const float* cx,
-                         const float* rx, const float* fx, const float* cy, const float* ry,
-                         const float* gy, double eps, double theta, double p, int self,
-                         uint8_t* mask_out) {
+                         const float* rx, const float* fx, const float* gx, const float* cy,
+                         const float* ry, const float* gy, const float* hy, double eps,
+                         double theta, double p, int self, uint8_t* mask_out) {
   return guard([&] {
     if (!c || !cx || !rx || !fx || !cy || !ry || !gy || !mask_out) raise(MSOT_EUSAGE, "null argument");
+    if ((gx == nullptr) != (hy == nullptr)) raise(MSOT_EUSAGE, "slopes: both sides or neither");
     if (p != 2.0) raise(MSOT_EUSAGE, "the GPU path implements p = 2");
     if (d < 1 || d > 3) raise(MSOT_EUSAGE, "D in 1..3");
     if (kx < 1 || ky < 1) raise(MSOT_EDATA, "empty cluster set");
     CK(cudaSetDevice(c->device));
     cudaStream_t st = c->st;
-    std::vector<float4> hx(kx), hy(ky);
+    std::vector<float4> hcx(kx), hcy(ky);
     for (int64_t I = 0; I < kx; ++I) {
       float v[3] = {0, 0, 0};
       for (int k = 0; k < d; ++k) v[k] = cx[I * d + k];
-      hx[I] = make_float4(v[0], v[1], v[2], 0.f);
+      hcx[I] = make_float4(v[0], v[1], v[2], 0.f);
     }
     for (int64_t J = 0; J < ky; ++J) {
       float v[3] = {0, 0, 0};
       for (int k = 0; k < d; ++k) v[k] = cy[J * d + k];
-      hy[J] = make_float4(v[0], v[1], v[2], 0.f);
+      hcy[J] = make_float4(v[0], v[1], v[2], 0.f);
     }
     float4* dcx = c->buf<float4>("tm.cx", kx);
     float4* dcy = c->buf<float4>("tm.cy", ky);
@@ -1054,15 +1071,24 @@ int msot_truncation_mask(msot_ctx* c, int64_t kx, int64_t ky, int d, const float
     float* dfx = c->buf<float>("tm.fx", kx);
     float* dry = c->buf<float>("tm.ry", ky);
     float* dgy = c->buf<float>("tm.gy", ky);
+    uint32_t* dbits = c->buf<uint32_t>("tm.bits", kx * mask_words(static_cast<int32_t>(ky)));
     uint8_t* dm = c->buf<uint8_t>("tm.m", kx * ky);
-    CK(cudaMemcpyAsync(dcx, hx.data(), kx * sizeof(float4), cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(dcy, hy.data(), ky * sizeof(float4), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dcx, hcx.data(), kx * sizeof(float4), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dcy, hcy.data(), ky * sizeof(float4), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(drx, rx, kx * sizeof(float), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(dfx, fx, kx * sizeof(float), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(dry, ry, ky * sizeof(float), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(dgy, gy, ky * sizeof(float), cudaMemcpyHostToDevice, st));
-    CK(truncation_mask(static_cast<int32_t>(kx), static_cast<int32_t>(ky), d, dcx, drx, dfx, dcy,
-                       dry, dgy, eps, theta, self, dm, st));
+    float4 *dgx = nullptr, *dhy = nullptr;
+    if (gx) {
+      dgx = c->buf<float4>("tm.gx", kx);
+      dhy = c->buf<float4>("tm.hy", ky);
+      CK(cudaMemcpyAsync(dgx, gx, kx * sizeof(float4), cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(dhy, hy, ky * sizeof(float4), cudaMemcpyHostToDevice, st));
+    }
+    CK(truncation_mask(static_cast<int32_t>(kx), static_cast<int32_t>(ky), d, dcx, drx, dfx, dgx,
+                       dcy, dry, dgy, dhy, eps, theta, self, dbits, st));
+    CK(unpack_mask(dbits, static_cast<int32_t>(kx), static_cast<int32_t>(ky), dm, st));
     CK(cudaMemcpyAsync(mask_out, dm, kx * ky, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
   });

@@ -52,8 +52,8 @@ def lib():
         L.msot_grid_cluster.argtypes = [C.c_void_p, _dp, _dp, C.c_int64, C.c_int, _dp,
                                         C.c_double, _ip, _ip, _ip, _ip, _dp, _dp, _fp]
         L.msot_truncation_mask.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int, _fp,
-                                           _fp, _fp, _fp, _fp, _fp, C.c_double, C.c_double,
-                                           C.c_double, C.c_int, _bp]
+                                           _fp, _fp, _fp, _fp, _fp, _fp, _fp, C.c_double,
+                                           C.c_double, C.c_double, C.c_int, _bp]
         L.msot_sinkhorn.argtypes = [C.c_void_p, C.POINTER(Params), _dp, _dp, C.c_int64, _dp,
                                     _dp, C.c_int64, C.c_int, _dp, _dp, _dp, _dp, _dp,
                                     C.POINTER(Stats)]
@@ -187,16 +187,20 @@ class Context:
                     centroids=cen[:K].copy(), cweights=cw[:K].copy(), radii=rad[:K].copy())
 
     # -- kernel_truncation on explicit coarse inputs (K3)
-    def kernel_truncation(self, cx, rx, fx, cy, ry, gy, eps, theta, self_=False):
+    def kernel_truncation(self, cx, rx, fx, cy, ry, gy, eps, theta, self_=False, gx=None,
+                          hy=None):
+        """gx / hy: optional (K, 4) {slope, F'} arrays for the slope bound."""
         f32 = lambda a: np.ascontiguousarray(a, dtype=np.float32)
         cx, rx, fx, cy, ry, gy = map(f32, (cx, rx, fx, cy, ry, gy))
         kx, d = cx.shape
         ky = cy.shape[0]
         out = np.zeros((kx, ky), np.uint8)
-        fp = lambda a: a.ctypes.data_as(_fp)
-        _check(lib().msot_truncation_mask(self._h, kx, ky, d, fp(cx), fp(rx), fp(fx), fp(cy),
-                                          fp(ry), fp(gy), eps, theta, 2.0, int(self_),
-                                          out.ctypes.data_as(_bp)))
+        fp = lambda a: None if a is None else a.ctypes.data_as(_fp)
+        gx = None if gx is None else f32(gx)
+        hy = None if hy is None else f32(hy)
+        _check(lib().msot_truncation_mask(self._h, kx, ky, d, fp(cx), fp(rx), fp(fx), fp(gx),
+                                          fp(cy), fp(ry), fp(gy), fp(hy), eps, theta, 2.0,
+                                          int(self_), out.ctypes.data_as(_bp)))
         return out
 
     # -- symmetric_sinkhorn / multiscale_sinkhorn + divergence

@@ -14,10 +14,10 @@ ctx = Context(0)
 print("ex2/s", ctx.probe_ex2(), flush=True)
 ctx.set_profiling(True)
 cfgs = [(300000, dict(blur=0.5))]
-for th in (20.0, 5.0):
+for mr in (0, 1):
     for cs in (0.0, 0.03, 0.02):
-        cfgs.append((1000000, dict(blur=0.01, multiscale=True, retruncate=1, theta=th, cluster_scale=cs)))
-cfgs.append((1000000, dict(blur=0.01, multiscale=True, retruncate=1, theta=20.0, scaling=0.5)))
+        cfgs.append((1000000, dict(blur=0.01, multiscale=True, retruncate=1, theta=20.0, cluster_scale=cs, mask_rule=mr)))
+cfgs.append((1000000, dict(blur=0.01, multiscale=True, retruncate=1, theta=5.0, cluster_scale=0.02)))
 for n, kw in cfgs:
     x, y = mixture(n, 5), mixture(n, 6)
     a = np.full(n, 1 / n)

@@ -122,6 +122,30 @@ def test_truncation_mask_bit_exact(ctx, oracle, self_):
     np.testing.assert_array_equal(g, o)
 
 
+@pytest.mark.parametrize("self_", [False, True])
+def test_truncation_mask_slope_bound_bit_exact(ctx, oracle, self_):
+    """Slope-corrected bound (mask.cu header) on identical float inputs."""
+    rng = np.random.default_rng(6)
+    kx = 500
+    ky = kx if self_ else 450
+    cx = rng.random((kx, 3)).astype(np.float32)
+    cy = cx if self_ else rng.random((ky, 3)).astype(np.float32)
+    rx = (rng.random(kx) * 0.04).astype(np.float32)
+    ry = rx if self_ else (rng.random(ky) * 0.04).astype(np.float32)
+    fx = (rng.random(kx) * 0.02).astype(np.float32)
+    gy = fx if self_ else (rng.random(ky) * 0.02).astype(np.float32)
+    gx = np.concatenate([rng.normal(0, 0.2, (kx, 3)), fx[:, None] + 0.001], 1).astype(np.float32)
+    hy = gx if self_ else np.concatenate([rng.normal(0, 0.2, (ky, 3)), gy[:, None] + 0.001],
+                                         1).astype(np.float32)
+    for eps, theta in ((1e-3, 20.0), (1e-4, 5.0)):
+        g = ctx.kernel_truncation(cx, rx, fx, cy, ry, gy, eps, theta, self_=self_, gx=gx, hy=hy)
+        o = oracle.truncation_mask(cx, rx, fx, cy, ry, gy, eps, theta, self_=self_, gx=gx, hy=hy)
+        np.testing.assert_array_equal(g, o)
+        # the transposed problem is the exact transpose (symmetric slack)
+        gt = ctx.kernel_truncation(cy, ry, gy, cx, rx, fx, eps, theta, self_=self_, gx=hy, hy=gx)
+        np.testing.assert_array_equal(gt, g.T)
+
+
 # --------------------------------------------------------- full solves
 def run_both(ctx, oracle, prm, x, a, y, b):
     lg, pg, sg = ctx.sinkhorn(prm, x, a, y, b)

@@ -64,6 +64,21 @@ struct MaskIn {
     const bool g = gx != nullptr;
     return pair_slack(cx[I], rx[I], fx[I], g ? gx[I] : z, cy[J], ry[J], gy[J], g ? hy[J] : z, d, g);
   }
+  // float32 upper bound of the exact (float64) slack: B_a evaluated in float
+  // plus a margin far above its rounding error (every term's magnitude times
+  // 1e-5, ~100x the accumulated relative error of ~10 float operations).
+  // Since min(B_a, B_b) <= B_a, a pair with ub < thr is dropped exactly as
+  // the float64 test would drop it — the prefilter never changes a bit.
+  __device__ __forceinline__ float ub(int32_t I, int32_t J) const {
+    const float4 X = cx[I], Y = cy[J];
+    const float dx = X.x - Y.x, dy = d > 1 ? X.y - Y.y : 0.f, dz = d > 2 ? X.z - Y.z : 0.f;
+    const float s = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    const float rr = rx[I] + ry[J];
+    const float lb = fmaxf(sqrtf(s) - rr, 0.f);
+    const float F = fx[I], G = gy[J];
+    const float v = (F + G) - 0.5f * lb * lb;
+    return v + 1e-5f * (1.f + fabsf(F) + fabsf(G) + 2.f * s + 2.f * rr * rr);
+  }
 };
 
 __global__ void mask_bits_kernel(MaskIn m, double thr, int self, uint32_t* mask) {
@@ -75,8 +90,12 @@ __global__ void mask_bits_kernel(MaskIn m, double thr, int self, uint32_t* mask)
   const int32_t nb = min(32, m.ky - J0);
   for (int b = 0; b < nb; ++b) {
     const int32_t J = J0 + b;
-    const double v = m.slack(I, J);
-    if (v >= thr || (self && I == J)) bits |= 1u << b;
+    if (self && I == J) {
+      bits |= 1u << b;
+      continue;
+    }
+    if (static_cast<double>(m.ub(I, J)) < thr) continue;
+    if (m.slack(I, J) >= thr) bits |= 1u << b;
   }
   mask[static_cast<int64_t>(I) * m.words + w] = bits;
 }
@@ -92,6 +111,7 @@ __global__ void best_kernel(MaskIn m, int by_col, uint32_t* mask) {
   for (int32_t q = lane; q < nl; q += 32) {
     const int32_t I = by_col ? q : static_cast<int32_t>(w);
     const int32_t J = by_col ? static_cast<int32_t>(w) : q;
+    if (static_cast<double>(m.ub(I, J)) < best) continue;  // cannot beat (or tie) the best
     const double v = m.slack(I, J);
     if (v > best) { best = v; arg = q; }
   }

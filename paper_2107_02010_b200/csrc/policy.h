@@ -28,7 +28,7 @@ extern "C" {
  * ranges per tile of MSOT_TILE_ROWS consecutive (cluster-sorted) rows. */
 #define MSOT_TILE_ROWS 256
 /* Target atoms per voxel for the automatic cluster_scale rule. */
-#define MSOT_AUTO_ATOMS_PER_CELL 256.0
+#define MSOT_AUTO_ATOMS_PER_CELL 48.0
 /* Cube ids are Morton-interleaved with this many bits per axis (D <= 3). */
 #define MSOT_MORTON_BITS 10
 

@@ -943,14 +943,29 @@ int msot_softmin(msot_ctx* c, const double* x, int64_t n, const double* y, int64
       for (int k = 0; k < d; ++k) lo[k] = std::min(lo[k], x[i * d + k]), hi[k] = std::max(hi[k], x[i * d + k]);
     for (int64_t j = 0; j < m; ++j)
       for (int k = 0; k < d; ++k) lo[k] = std::min(lo[k], y[j * d + k]), hi[k] = std::max(hi[k], y[j * d + k]);
-    std::vector<float4> xp(n), yp(m);
-    std::vector<float> yl(m), hh(m), fe(n, 0.f);
-    for (int64_t i = 0; i < n; ++i) {
-      float v[3] = {0, 0, 0};
-      for (int k = 0; k < d; ++k) v[k] = static_cast<float>(x[i * d + k] - 0.5 * (lo[k] + hi[k]));
-      xp[i] = make_float4(v[0], v[1], v[2], 0.f);
-      if (f_est) fe[i] = static_cast<float>(f_est[i]);
+    // rows: sorted by Morton cube id on the device (compact 256-row tiles),
+    // exactly as the solver prepares its measures
+    GridSpec g{};
+    g.d = d;
+    for (int k = 0; k < d; ++k) {
+      g.origin[k] = lo[k];
+      g.center[k] = 0.5 * (lo[k] + hi[k]);
     }
+    g.cell = msot_auto_cell(lo, hi, d, n, m);
+    double* dx64 = c->buf<double>("sm.x64", n * d);
+    double* dw64 = c->buf<double>("sm.w64", n);
+    CK(cudaMemcpyAsync(dx64, x, n * d * sizeof(double), cudaMemcpyHostToDevice, st));
+    std::vector<double> ones(n, 1.0);
+    CK(cudaMemcpyAsync(dw64, ones.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
+    DMeasure MX;
+    prepare_measure(c, "sm", dx64, dw64, n, d, g, false, MX);
+    std::vector<int32_t> perm(n);
+    CK(cudaMemcpyAsync(perm.data(), MX.perm, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<float4> yp(m);
+    std::vector<float> yl(m), hh(m), fe(n, 0.f);
+    if (f_est)
+      for (int64_t s = 0; s < n; ++s) fe[s] = static_cast<float>(f_est[perm[s]]);
     for (int64_t j = 0; j < m; ++j) {
       float v[3] = {0, 0, 0};
       for (int k = 0; k < d; ++k) v[k] = static_cast<float>(y[j * d + k] - 0.5 * (lo[k] + hi[k]));
@@ -958,13 +973,12 @@ int msot_softmin(msot_ctx* c, const double* x, int64_t n, const double* y, int64
       yl[j] = static_cast<float>(logw_y[j] / 0.69314718055994530942);
       hh[j] = static_cast<float>(h[j]);
     }
-    float4* dxp = c->buf<float4>("sm.x", n);
+    float4* dxp = MX.pts;
     float4* dyp = c->buf<float4>("sm.y", m);
     float* dyl = c->buf<float>("sm.yl", m);
     float* dh = c->buf<float>("sm.h", m);
     float* dfe = c->buf<float>("sm.fe", n);
     float* dfo = c->buf<float>("sm.fo", n);
-    CK(cudaMemcpyAsync(dxp, xp.data(), n * sizeof(float4), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(dyp, yp.data(), m * sizeof(float4), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(dyl, yl.data(), m * sizeof(float), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(dh, hh.data(), m * sizeof(float), cudaMemcpyHostToDevice, st));
@@ -1001,7 +1015,7 @@ int msot_softmin(msot_ctx* c, const double* x, int64_t n, const double* y, int64
     std::vector<float> fo(n);
     CK(cudaMemcpyAsync(fo.data(), dfo, n * sizeof(float), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    for (int64_t i = 0; i < n; ++i) f_out[i] = fo[i];
+    for (int64_t s = 0; s < n; ++s) f_out[perm[s]] = fo[s];
   });
 }
 

@@ -11,13 +11,14 @@ def mixture(n, seed, d=3, k=8, sigma=0.05):
     return cen[rng.integers(0, k, n)] + rng.normal(0, sigma, (n, d))
 
 ctx = Context(0)
-print("ex2/s", ctx.probe_ex2(), flush=True)
 ctx.set_profiling(True)
-cfgs = [(300000, dict(blur=0.5))]
-for mr in (0, 1):
-    for cs in (0.0, 0.03, 0.02):
-        cfgs.append((1000000, dict(blur=0.01, multiscale=True, retruncate=1, theta=20.0, cluster_scale=cs, mask_rule=mr)))
-cfgs.append((1000000, dict(blur=0.01, multiscale=True, retruncate=1, theta=5.0, cluster_scale=0.02)))
+cfgs = []
+for cs in (0.0, 0.025, 0.02, 0.015):
+    cfgs.append((1000000, dict(blur=0.01, multiscale=True, retruncate=1, theta=20.0, cluster_scale=cs)))
+for th in (5.0, 10.0):
+    cfgs.append((1000000, dict(blur=0.01, multiscale=True, retruncate=1, theta=th)))
+cfgs.append((1000000, dict(blur=0.01, multiscale=True, retruncate=2, theta=20.0)))
+cfgs.append((1000000, dict(blur=0.01, multiscale=True, retruncate=1, theta=20.0, switch_factor=1.0)))
 for n, kw in cfgs:
     x, y = mixture(n, 5), mixture(n, 6)
     a = np.full(n, 1 / n)

@@ -174,6 +174,17 @@ static inline int64_t msot_pack_tiles(const int32_t* offsets, int64_t k, int64_t
   return t;
 }
 
+/* The row tiling the block-sparse phase uses.  With ~48 atoms per voxel a
+ * 256-row tile of Morton-sorted atoms spans ~5 neighbouring voxels whichever
+ * way it is cut, so uniform tiles (100% thread fill) are used; the
+ * cluster-aligned packing above stays available for coarse voxels. */
+#define MSOT_CLUSTER_ALIGNED_TILES 0
+static inline int64_t msot_row_tiles(const int32_t* offsets, int64_t k, int64_t n,
+                                     int64_t* tile_start) {
+  return msot_pack_tiles(MSOT_CLUSTER_ALIGNED_TILES ? offsets : 0, k, n, MSOT_TILE_ROWS,
+                         tile_start);
+}
+
 /* First fine scale: the first t with sigma_t < factor * r_max;
  * n when no scale qualifies (then only the final update runs fine). */
 static inline int msot_switch_index(const double* sigma, int n, double r_max, double factor) {

@@ -82,14 +82,16 @@ struct msot_ctx {
     const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
     auto it = bufs.find(name);
     if (it != bufs.end() && it->second.second >= bytes) return static_cast<T*>(it->second.first);
-    if (it != bufs.end()) {
+    size_t alloc = bytes;
+    if (it != bufs.end()) {  // regrown buffer (sizes vary per rebuild): keep headroom
+      alloc = bytes + bytes / 2;
       CK(cudaStreamSynchronize(st));
       CK(cudaFree(it->second.first));
       bufs.erase(it);
     }
     void* p = nullptr;
-    CK(cudaMalloc(&p, bytes));
-    bufs[name] = {p, bytes};
+    CK(cudaMalloc(&p, alloc));
+    bufs[name] = {p, alloc};
     return static_cast<T*>(p);
   }
   // phase marks (profiling only): time from a mark to the next is charged to
@@ -217,7 +219,7 @@ void make_tiles(msot_ctx* c, const std::string& tag, int64_t rows,
                 const std::vector<int32_t>* offsets, RangeSet& R) {
   const int64_t k = offsets ? static_cast<int64_t>(offsets->size()) - 1 : 0;
   std::vector<int64_t> ts(k + rows / kTileRows + 2);
-  R.n_tiles = msot_pack_tiles(offsets ? offsets->data() : nullptr, k, rows, kTileRows, ts.data());
+  R.n_tiles = msot_row_tiles(offsets ? offsets->data() : nullptr, k, rows, ts.data());
   R.tile_start_h.assign(ts.begin(), ts.begin() + R.n_tiles + 1);
   R.tile_start = c->buf<int32_t>(tag + ".tstart", R.n_tiles + 1);
   CK(cudaMemcpyAsync(R.tile_start, R.tile_start_h.data(), (R.n_tiles + 1) * sizeof(int32_t),

@@ -243,12 +243,9 @@ def test_tile_ranges(oracle):
     mask[5, [4]] = 1
     ro = np.array([0, 100, 300, 350, 650, 660, 760], np.int32)
     ts, ptr, rg = oracle.tile_ranges(labels, ro, co, mask)
-    # cluster-aligned tiles: {0} (100; +200 > 256), {1,2} (250), {3} split in
-    # 2 (300 > 256), {4,5} (110)
-    assert ts.tolist() == [0, 100, 350, 500, 650, 760]
-    # tile 0: cluster 0 -> cols {0,1}; tile 1: clusters 1,2 -> {1,3,4}
-    assert ptr.tolist() == [0, 1, 3, 4, 5, 6]
-    assert rg[0].tolist() == [0, 90]
-    assert rg[1:3].tolist() == [[40, 90], [100, 200]]
-    assert rg[3].tolist() == [0, 40] and rg[4].tolist() == [0, 40]
-    assert rg[5].tolist() == [90, 200]
+    # uniform 256-row tiles (policy.h:msot_row_tiles)
+    assert ts.tolist() == [0, 256, 512, 760]
+    # tile 0: clusters 0,1 -> {0,1,3}; tile 1: clusters 1,2,3 -> {0,1,3,4};
+    # tile 2: clusters 3,4,5 -> {0,2,3,4}; runs -> [co[J0], co[J1+1])
+    assert ptr.tolist() == [0, 2, 4, 6]
+    assert rg.tolist() == [[0, 90], [100, 180], [0, 90], [100, 200], [0, 40], [90, 200]]

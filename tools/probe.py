@@ -1,4 +1,4 @@
-"""Quick GPU probe: dense softmin throughput + multiscale solves (dev tool)."""
+"""Quick GPU probe: multiscale solves (dev tool)."""
 import sys, time, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -13,12 +13,10 @@ def mixture(n, seed, d=3, k=8, sigma=0.05):
 ctx = Context(0)
 ctx.set_profiling(True)
 cfgs = []
-for cs in (0.0, 0.025, 0.02, 0.015):
-    cfgs.append((1000000, dict(blur=0.01, multiscale=True, retruncate=1, theta=20.0, cluster_scale=cs)))
-for th in (5.0, 10.0):
-    cfgs.append((1000000, dict(blur=0.01, multiscale=True, retruncate=1, theta=th)))
-cfgs.append((1000000, dict(blur=0.01, multiscale=True, retruncate=2, theta=20.0)))
-cfgs.append((1000000, dict(blur=0.01, multiscale=True, retruncate=1, theta=20.0, switch_factor=1.0)))
+for sf in (2.0, 1.0):
+    for th in (20.0, 5.0):
+        cfgs.append((1000000, dict(blur=0.01, multiscale=True, retruncate=1, theta=th, switch_factor=sf)))
+cfgs.append((1000000, dict(blur=0.01, multiscale=True, retruncate=1, theta=20.0, switch_factor=1.0, cluster_scale=0.03)))
 for n, kw in cfgs:
     x, y = mixture(n, 5), mixture(n, 6)
     a = np.full(n, 1 / n)

@@ -34,7 +34,8 @@ import numpy as np  # noqa: E402
 WORKLOAD = dict(workload="C3: S_eps 1M vs 1M 3D Gaussian mixtures (8 comps, sigma 0.05), "
                          "multiscale voxel grid + per-scale kernel truncation",
                 n=1_000_000, m=1_000_000, d=3, blur=0.01, reach="inf", scaling=0.9, theta=20.0,
-                retruncate=1, seeds=[5, 6])
+                retruncate=1, switch_factor=1.0, cluster_scale="auto (48 atoms/voxel)",
+                seeds=[5, 6])
 METRIC = "sec to S_eps, 1M vs 1M 3D pts at 1/2/4/8 GPU; softmin pairs/sec vs roofline"
 PAIRS_FILE = os.path.join(ROOT, "profiles", "c3_workload.json")
 
@@ -56,7 +57,8 @@ def make_inputs(w):
 def params(w):
     from paper_2107_02010_b200.abi import make_params
     return make_params(blur=w["blur"], reach=math.inf, scaling=w["scaling"], multiscale=True,
-                       retruncate=w["retruncate"], theta=w["theta"])
+                       retruncate=w["retruncate"], theta=w["theta"],
+                       switch_factor=w["switch_factor"])
 
 
 class ClockSampler:

@@ -53,6 +53,11 @@ typedef struct msot_params {
   int32_t max_full_iters;/* safety cap on schedule length          */
   int32_t mask_rule;     /* 0 = min(centroid/radius bound, slope bound) (default),
                             1 = centroid/radius bound only (msot_truncation_mask) */
+  int32_t transfer_rule; /* coarse -> fine potentials at the switch:
+                            0 = inheritance (default),
+                            1 = extrapolation: one lambda-damped softmin of the
+                                fine atoms against the coarse measure (GeomLoss) */
+  int32_t pad_;
 } msot_params;
 
 /* Defaults of SPEC.md:128 (q=0.9), :306 (switch 2x radius), :308 (theta=20). */

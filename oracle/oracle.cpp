@@ -597,16 +597,27 @@ int oracle_sinkhorn(const msot_params* prm, const double* x, const double* a, in
       S.pairs_evaluated += pr;
       S.pairs_dense += cfull;
     }
-    // Coarse -> fine: one lambda-damped softmin of every fine atom against
-    // the coarse measure at the last coarse eps.
+    // Coarse -> fine, prm->transfer_rule:
+    //   0  coarse_duals_to_fine by inheritance
+    //   1  extrapolation: one lambda-damped softmin of every fine atom against
+    //      the coarse measure at the last coarse eps (GeomLoss)
     Duals fu{Vec(n, 0.0), Vec(m, 0.0), Vec(m, 0.0), Vec(n, 0.0)};
-    if (tsw > 0) {
+    if (tsw > 0 && prm->transfer_rule == 1) {
       const int te = tsw - 1;
       const double e = eps[te], l = lam[te];
       S.pairs_evaluated += softmin_rows(Xs.pts.data(), n, d, {Xc.pts.data(), Xc.logw.data(), cu.a_xx.data(), cx.k}, e, l, p, nullptr, fu.a_xx.data());
       S.pairs_evaluated += softmin_rows(Ys.pts.data(), m, d, {Yc.pts.data(), Yc.logw.data(), cu.b_yy.data(), cy.k}, e, l, p, nullptr, fu.b_yy.data());
       S.pairs_evaluated += softmin_rows(Ys.pts.data(), m, d, {Xc.pts.data(), Xc.logw.data(), cu.b_yx.data(), cx.k}, e, l, p, nullptr, fu.a_xy.data());
       S.pairs_evaluated += softmin_rows(Xs.pts.data(), n, d, {Yc.pts.data(), Yc.logw.data(), cu.a_xy.data(), cy.k}, e, l, p, nullptr, fu.b_yx.data());
+    } else if (tsw > 0) {
+      for (int64_t s = 0; s < n; ++s) {
+        fu.a_xx[s] = cu.a_xx[cx.labels[s]];
+        fu.b_yx[s] = cu.b_yx[cx.labels[s]];
+      }
+      for (int64_t s = 0; s < m; ++s) {
+        fu.b_yy[s] = cu.b_yy[cy.labels[s]];
+        fu.a_xy[s] = cu.a_xy[cy.labels[s]];
+      }
     }
     // Fine phase: block-sparse updates restricted to the truncation masks.
     std::vector<float> cxf(cx.centroids.begin(), cx.centroids.end());

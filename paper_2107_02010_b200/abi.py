@@ -24,16 +24,19 @@ class Params(C.Structure):
         ("switch_factor", C.c_double),
         ("max_full_iters", C.c_int32),
         ("mask_rule", C.c_int32),
+        ("transfer_rule", C.c_int32),
+        ("pad_", C.c_int32),
     ]
 
 
 def make_params(blur=0.05, reach=math.inf, p=2.0, scaling=0.9, multiscale=False,
                 retruncate=0, cluster_scale=0.0, theta=20.0, switch_factor=2.0,
-                max_full_iters=10000, mask_rule=0):
-    """Defaults follow SPEC.md:128 (q=0.9), :306 (switch 2 r_max), :308 (theta 20)."""
+                max_full_iters=10000, mask_rule=0, transfer_rule=0):
+    """Defaults follow SPEC.md:128 (q=0.9), :306 (switch 2 r_max), :308 (theta 20),
+    :270-274 (coarse duals inherited by the fine atoms)."""
     return Params(blur, math.inf if reach is None else reach, p, scaling, int(bool(multiscale)),
                   int(retruncate), cluster_scale, theta, switch_factor, int(max_full_iters),
-                  int(mask_rule))
+                  int(mask_rule), int(transfer_rule), 0)
 
 
 class Stats(C.Structure):

@@ -569,6 +569,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
     const int tsw = msot_switch_index(sig.data(), ns, rmax, prm->switch_factor);
     S->t_switch = tsw;
     c->mark(1);  // phase 1: coarse phase on the centroid measures (dense)
+    float* coarse_final[4] = {nullptr, nullptr, nullptr, nullptr};
     if (tsw > 0) {
       Potentials Uc;
       alloc_pots(c, "cpot", X.k, Y.k, Uc);
@@ -586,17 +587,25 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
         sym_step(c, Pc, Uc, ccur, eps[t], lam[t], false, ss);
         S->pairs_dense += cfull;
       }
-      c->mark(2);  // phase 2: extrapolation
-      // coarse -> fine extrapolation: one lambda-damped
-      // softmin of every fine atom against the coarse measure, expanded
-      // around the inherited coarse value.
+      c->mark(2);  // phase 2: coarse -> fine transfer
+      // inheritance (transfer_rule 0) writes the fine
+      // potentials directly; extrapolation (transfer_rule 1) is one
+      // lambda-damped softmin of every fine atom against the coarse measure,
+      // expanded around the inherited value.
       float** co = Uc.v[ccur];
+      for (int q = 0; q < 4; ++q) coarse_final[q] = co[q];
+      const bool extrap = prm->transfer_rule == 1;
       float* inh[4];
-      for (int q = 0; q < 4; ++q) inh[q] = U.v[cur ^ 1][q];  // scratch = the other buffer
+      for (int q = 0; q < 4; ++q) inh[q] = U.v[extrap ? cur ^ 1 : cur][q];
       CK(inherit(co[0], X.labels, n, inh[0], st));
       CK(inherit(co[1], Y.labels, m, inh[1], st));
       CK(inherit(co[2], Y.labels, m, inh[2], st));
       CK(inherit(co[3], X.labels, n, inh[3], st));
+    }
+    if (tsw > 0 && prm->transfer_rule == 1) {
+      float** co = coarse_final;
+      float* inh[4];
+      for (int q = 0; q < 4; ++q) inh[q] = U.v[cur ^ 1][q];
       RangeSet exx, eyy, exy, eyx;
       dense_rangeset(c, "e.xx", n, X.k, exx, &X.offsets_h);
       dense_rangeset(c, "e.yy", m, Y.k, eyy, &Y.offsets_h);

@@ -17,7 +17,8 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_obj")
 LIB = os.path.join(HERE, "libmsot_b200.so")
 
-SOURCES = ["softmin.cu", "prims.cu", "cluster.cu", "mask.cu", "loss.cu", "probe.cu", "solver.cu"]
+SOURCES = ["softmin.cu", "prims.cu", "cluster.cu", "mask.cu", "loss.cu", "probe.cu", "solver.cu",
+           "frontend.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
@@ -34,15 +35,20 @@ def _newer(target, deps):
 def _headers():
     hs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     hs.append(os.path.join(ROOT, "include", "msot_gpu.h"))
+    inc = os.path.join(ROOT, "include", "msot")
+    hs += [os.path.join(inc, f) for f in os.listdir(inc) if f.endswith(".hpp")]
     return hs
 
 
 def _compile(src, verbose):
-    obj = os.path.join(BUILD, src.replace(".cu", ".o"))
+    obj = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
     srcp = os.path.join(CSRC, src)
     if not _newer(obj, [srcp] + _headers()):
         return obj
-    cmd = [NVCC] + ARCH + FLAGS + ["-c", srcp, "-o", obj]
+    flags = FLAGS
+    if src.endswith(".cpp"):  # host-only C++20 front-end (std::span API)
+        flags = [f for f in FLAGS if f != "-std=c++17"] + ["-std=c++20"]
+    cmd = [NVCC] + ARCH + flags + ["-c", srcp, "-o", obj]
     if verbose:
         print(" ".join(cmd), flush=True)
     r = subprocess.run(cmd, capture_output=True, text=True)

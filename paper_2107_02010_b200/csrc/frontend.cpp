@@ -1,0 +1,263 @@
+// frontend.cpp — the msot:: C++ API (include/msot/*.hpp) over the C ABI.
+//
+// Measures and their constructors follow SPEC.md:27-120 (reference
+// declarations: proj/include/msot/measure.hpp); the solver operations
+// forward to libmsot_b200's GPU entry points and rethrow status codes as the
+// reference's exception types (proj/include/msot/common.hpp:10-19).
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+#include <string>
+
+#include "../../include/msot/common.hpp"
+#include "../../include/msot/measure.hpp"
+#include "../../include/msot/sinkhorn.hpp"
+
+namespace msot {
+
+void throw_on_status(int status, const std::string& what) {
+  if (status == MSOT_OK) return;
+  const std::string msg = what + ": " + msot_last_error();
+  if (status == MSOT_ENUMERIC) throw NumericError(msg);
+  if (status == MSOT_EDATA || status == MSOT_EUSAGE) throw DataError(msg);
+  throw DeviceError(msg);
+}
+
+// ------------------------------------------------------------------ measures
+void CostSpec::validate() const {
+  if (!(p >= 1.0 && p <= 2.0)) throw DataError("CostSpec: p must lie in [1, 2]");
+}
+
+double cost(std::span<const double> x, std::span<const double> y, const CostSpec& spec) {
+  spec.validate();
+  if (x.size() != y.size()) throw DataError("cost: dimension mismatch");
+  double s = 0.0;
+  for (std::size_t k = 0; k < x.size(); ++k) s += (x[k] - y[k]) * (x[k] - y[k]);
+  if (spec.p == 2.0) return 0.5 * s;
+  return std::pow(std::sqrt(s), spec.p) / spec.p;
+}
+
+DiscreteMeasure::DiscreteMeasure(std::vector<double> points, std::vector<double> weights,
+                                 std::size_t dim)
+    : dim_(dim) {
+  if (dim == 0) throw DataError("DiscreteMeasure: dimension must be >= 1");
+  if (points.size() != weights.size() * dim)
+    throw DataError("DiscreteMeasure: points and weights sizes disagree");
+  double mass = 0.0;
+  for (std::size_t i = 0; i < weights.size(); ++i) {
+    const double w = weights[i];
+    if (!(w >= 0.0) || !std::isfinite(w)) throw DataError("DiscreteMeasure: weights must be >= 0");
+    for (std::size_t k = 0; k < dim; ++k)
+      if (!std::isfinite(points[i * dim + k])) throw DataError("DiscreteMeasure: non-finite point");
+    if (w == 0.0) continue;  // zero weights dropped
+    points_.insert(points_.end(), points.begin() + i * dim, points.begin() + (i + 1) * dim);
+    weights_.push_back(w);
+    log_weights_.push_back(std::log(w));
+    mass += w;
+  }
+  if (weights_.empty() || !(mass > 0.0)) throw DataError("DiscreteMeasure: total mass must be > 0");
+  total_mass_ = mass;
+}
+
+DiscreteMeasure DiscreteMeasure::with_points(std::vector<double> points) const {
+  return DiscreteMeasure(std::move(points), weights_, dim_);
+}
+
+DiscreteMeasure DiscreteMeasure::permuted(std::span<const std::size_t> order) const {
+  if (order.size() != size()) throw DataError("permuted: order has the wrong length");
+  std::vector<char> seen(size(), 0);
+  std::vector<double> p(points_.size()), w(size());
+  for (std::size_t s = 0; s < order.size(); ++s) {
+    const std::size_t i = order[s];
+    if (i >= size() || seen[i]) throw DataError("permuted: not a permutation");
+    seen[i] = 1;
+    std::copy_n(points_.begin() + i * dim_, dim_, p.begin() + s * dim_);
+    w[s] = weights_[i];
+  }
+  return DiscreteMeasure(std::move(p), std::move(w), dim_);
+}
+
+DiscreteMeasure encode_fibers(const FiberSet& fs) {
+  const int P = fs.resample_count;
+  if (P < 2) throw DataError("encode_fibers: resample_count must be >= 2");
+  if (fs.fibers.empty()) throw DataError("encode_fibers: empty fiber set");
+  const std::size_t n = fs.fibers.size();
+  std::vector<double> pts(n * 3 * P), w(n, 1.0 / static_cast<double>(n));
+  const double scale = 1.0 / std::sqrt(static_cast<double>(P));
+  for (std::size_t f = 0; f < n; ++f) {
+    const Polyline& line = fs.fibers[f];
+    if (line.size() < 2) throw DataError("encode_fibers: fiber " + std::to_string(f) + " has < 2 points");
+    std::vector<double> arc(line.size(), 0.0);
+    for (std::size_t v = 1; v < line.size(); ++v) {
+      double s = 0.0;
+      for (int k = 0; k < 3; ++k) s += (line[v][k] - line[v - 1][k]) * (line[v][k] - line[v - 1][k]);
+      arc[v] = arc[v - 1] + std::sqrt(s);
+    }
+    const double L = arc.back();
+    if (!(L > 0.0)) throw DataError("encode_fibers: fiber " + std::to_string(f) + " is degenerate");
+    std::size_t seg = 0;
+    for (int q = 0; q < P; ++q) {
+      const double target = L * static_cast<double>(q) / static_cast<double>(P - 1);
+      while (seg + 2 < line.size() && arc[seg + 1] < target) ++seg;
+      const double len = arc[seg + 1] - arc[seg];
+      const double t = len > 0.0 ? std::clamp((target - arc[seg]) / len, 0.0, 1.0) : 0.0;
+      for (int k = 0; k < 3; ++k)
+        pts[f * 3 * P + 3 * q + k] = scale * ((1.0 - t) * line[seg][k] + t * line[seg + 1][k]);
+    }
+  }
+  return DiscreteMeasure(std::move(pts), std::move(w), static_cast<std::size_t>(3 * P));
+}
+
+AugmentedMeasure flip_augment(const DiscreteMeasure& m, int P) {
+  if (P < 1 || m.dim() != static_cast<std::size_t>(3 * P))
+    throw DataError("flip_augment: atom dimension must equal 3P");
+  const std::size_t n = m.size(), D = m.dim();
+  std::vector<double> pts(2 * n * D), w(2 * n);
+  for (std::size_t i = 0; i < n; ++i) {
+    auto src = m.point(i);
+    std::copy(src.begin(), src.end(), pts.begin() + i * D);
+    for (int q = 0; q < P; ++q)
+      for (int k = 0; k < 3; ++k) pts[(n + i) * D + 3 * q + k] = src[3 * (P - 1 - q) + k];
+    w[i] = w[n + i] = 0.5 * m.weights()[i];
+  }
+  return {DiscreteMeasure(std::move(pts), std::move(w), D), FlipMap{n}};
+}
+
+DiscreteMeasure density_to_measure(const DensityMap& d) {
+  std::vector<double> pts, w;
+  double sum = 0.0, carry = 0.0;  // Kahan
+  for (const DensityVoxel& v : d.voxels) {
+    if (!(v.value >= 0.0) || !std::isfinite(v.value)) throw DataError("density_to_measure: negative value");
+    if (v.value == 0.0) continue;
+    if (v.i < 0 || v.j < 0 || v.k < 0 || v.i >= d.nx || v.j >= d.ny || v.k >= d.nz)
+      throw DataError("density_to_measure: voxel index outside the grid");
+    pts.push_back(d.origin[0] + (v.i + 0.5) * d.voxel_mm);
+    pts.push_back(d.origin[1] + (v.j + 0.5) * d.voxel_mm);
+    pts.push_back(d.origin[2] + (v.k + 0.5) * d.voxel_mm);
+    w.push_back(v.value);
+    const double y = v.value - carry, t = sum + y;
+    carry = (t - sum) - y;
+    sum = t;
+  }
+  if (w.empty()) throw DataError("density_to_measure: all-zero map");
+  for (double& x : w) x /= sum;
+  return DiscreteMeasure(std::move(pts), std::move(w), 3);
+}
+
+// -------------------------------------------------------------------- solver
+msot_params SolverParams::to_c() const {
+  cost.validate();
+  msot_params p;
+  msot_params_default(&p);
+  p.blur = blur;
+  p.reach = reach;
+  p.p = cost.p;
+  p.scaling = scaling;
+  p.max_full_iters = max_full_iters;
+  p.multiscale = multiscale ? 1 : 0;
+  p.retruncate = retruncate;
+  p.cluster_scale = cluster_scale;
+  p.theta = theta;
+  p.switch_factor = switch_factor;
+  p.mask_rule = mask_rule;
+  p.transfer_rule = transfer_rule;
+  return p;
+}
+
+Device::Device(int device) { throw_on_status(msot_create(device, &ctx_), "msot_create"); }
+
+Device::Device(int device, int rank, int world, const unsigned char nccl_id[128]) {
+  throw_on_status(msot_create_dist(device, rank, world, nccl_id, &ctx_), "msot_create_dist");
+}
+
+Device::~Device() { msot_destroy(ctx_); }
+
+Device& default_device() {
+  thread_local Device dev(0);
+  return dev;
+}
+
+double diameter_estimate(const DiscreteMeasure& a, const DiscreteMeasure& b, double blur) {
+  if (a.dim() != b.dim()) throw DataError("diameter_estimate: dimension mismatch");
+  const std::size_t D = a.dim();
+  std::vector<double> lo(D, INFINITY), hi(D, -INFINITY);
+  for (const DiscreteMeasure* m : {&a, &b})
+    for (std::size_t i = 0; i < m->size(); ++i)
+      for (std::size_t k = 0; k < D; ++k) {
+        lo[k] = std::min(lo[k], m->point(i)[k]);
+        hi[k] = std::max(hi[k], m->point(i)[k]);
+      }
+  double s = 0.0;
+  for (std::size_t k = 0; k < D; ++k) s += (hi[k] - lo[k]) * (hi[k] - lo[k]);
+  return std::max(std::sqrt(s), blur);
+}
+
+EpsSchedule make_schedule(double d, const SolverParams& params) {
+  const msot_params p = params.to_c();
+  int n = msot_schedule(d, &p, nullptr, nullptr, nullptr, 0);
+  n = n < 0 ? -n : n;
+  EpsSchedule s;
+  s.sigma.resize(n);
+  s.eps.resize(n);
+  s.lambda.resize(n);
+  msot_schedule(d, &p, s.sigma.data(), s.eps.data(), s.lambda.data(), n);
+  return s;
+}
+
+std::vector<double> softmin(const DiscreteMeasure& rows, const DiscreteMeasure& cols,
+                            const std::vector<double>& h, double eps, double lambda, Device& dev) {
+  if (rows.dim() != cols.dim()) throw DataError("softmin: dimension mismatch");
+  if (h.size() != cols.size()) throw DataError("softmin: potential size mismatch");
+  std::vector<double> out(rows.size());
+  const std::vector<double> lw(cols.log_weights().begin(), cols.log_weights().end());
+  throw_on_status(msot_softmin(dev.get(), rows.points().data(), static_cast<int64_t>(rows.size()),
+                               cols.points().data(), static_cast<int64_t>(cols.size()),
+                               static_cast<int>(rows.dim()), lw.data(), h.data(), eps, lambda,
+                               nullptr, out.data()),
+                  "softmin");
+  return out;
+}
+
+static DualPotentials solve(const DiscreteMeasure& a, const DiscreteMeasure& b,
+                            const SolverParams& params, Device& dev, double* loss) {
+  if (a.dim() != b.dim()) throw DataError("dimension mismatch between the two measures");
+  const msot_params p = params.to_c();
+  DualPotentials u;
+  u.a_xx.resize(a.size());
+  u.b_yx.resize(a.size());
+  u.b_yy.resize(b.size());
+  u.a_xy.resize(b.size());
+  double l = 0.0;
+  msot_stats st;
+  throw_on_status(msot_sinkhorn(dev.get(), &p, a.points().data(), a.weights().data(),
+                                static_cast<int64_t>(a.size()), b.points().data(),
+                                b.weights().data(), static_cast<int64_t>(b.size()),
+                                static_cast<int>(a.dim()), u.a_xx.data(), u.b_yy.data(),
+                                u.a_xy.data(), u.b_yx.data(), &l, &st),
+                  "sinkhorn");
+  u.eps = std::pow(params.blur, params.cost.p);
+  if (loss) *loss = l;
+  return u;
+}
+
+DualPotentials symmetric_sinkhorn(const DiscreteMeasure& a, const DiscreteMeasure& b,
+                                  const SolverParams& params, Device& dev) {
+  SolverParams q = params;
+  q.multiscale = false;
+  return solve(a, b, q, dev, nullptr);
+}
+
+DualPotentials multiscale_sinkhorn(const DiscreteMeasure& a, const DiscreteMeasure& b,
+                                   SolverParams params, Device& dev) {
+  params.multiscale = true;
+  return solve(a, b, params, dev, nullptr);
+}
+
+double divergence(const DiscreteMeasure& a, const DiscreteMeasure& b, const SolverParams& params,
+                  Device& dev) {
+  double loss = 0.0;
+  solve(a, b, params, dev, &loss);
+  return loss;
+}
+
+}  // namespace msot

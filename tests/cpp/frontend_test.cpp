@@ -1,0 +1,138 @@
+// C++ caller of the msot:: API (include/msot/*.hpp), as a user of the
+// reference's C++ interface would write it.  Mode "cpu": host-side measure
+// constructors and schedule (SPEC.md examples); mode "gpu": solves.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "msot/measure.hpp"
+#include "msot/sinkhorn.hpp"
+
+static int failures = 0;
+#define CHECK(cond)                                                        \
+  do {                                                                     \
+    if (!(cond)) {                                                         \
+      std::fprintf(stderr, "FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond); \
+      ++failures;                                                          \
+    }                                                                      \
+  } while (0)
+
+template <class E, class F>
+static bool throws(F&& f) {
+  try {
+    f();
+  } catch (const E&) {
+    return true;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+
+static void cpu_checks() {
+  using namespace msot;
+  // cost
+  const double a0[3] = {0, 0, 0}, a1[3] = {2, 0, 0};
+  CHECK(cost(a0, a1, CostSpec{2.0}) == 2.0);
+  const double b0[2] = {0, 0}, b1[2] = {3, 4};
+  CHECK(cost(b0, b1, CostSpec{1.0}) == 5.0);
+  CHECK(throws<DataError>([] { CostSpec{2.5}.validate(); }));
+  // zero weights dropped, invariants
+  DiscreteMeasure m({0, 0, 1, 1, 2, 2}, {0.5, 0.0, 0.5}, 2);
+  CHECK(m.size() == 2 && m.total_mass() == 1.0 && m.point(1)[0] == 2.0);
+  CHECK(throws<DataError>([] { DiscreteMeasure({0.0}, {-1.0}, 1); }));
+  CHECK(throws<DataError>([] { DiscreteMeasure({0.0, 1.0}, {0.0, 0.0}, 1); }));
+  const std::size_t order[2] = {1, 0};
+  CHECK(m.permuted(order).point(0)[0] == 2.0);
+  // schedule
+  SolverParams p;
+  p.blur = 1.0;
+  p.scaling = 0.5;
+  auto s = make_schedule(8.0, p);
+  CHECK(s.size() == 4 && s.sigma[0] == 8 && s.sigma[3] == 1 && s.eps[1] == 16 && s.lambda[2] == 1);
+  p.scaling = 0.9;
+  CHECK(make_schedule(10.0, p).size() == 22);
+  CHECK(make_schedule(1.0, p).size() == 1);
+  // encode_fibers
+  FiberSet fs;
+  fs.resample_count = 3;
+  fs.fibers = {{{0, 0, 0}, {1, 0, 0}}, {{0, 0, 0}, {1, 0, 0}}};
+  DiscreteMeasure f = encode_fibers(fs);
+  const double r3 = 1.0 / std::sqrt(3.0);
+  CHECK(f.dim() == 9 && std::fabs(f.point(0)[3] - 0.5 * r3) < 1e-15 && std::fabs(f.point(0)[6] - r3) < 1e-15);
+  CHECK(f.weights()[0] == 0.5);
+  FiberSet bad;
+  bad.resample_count = 3;
+  bad.fibers = {{{1, 1, 1}, {1, 1, 1}}};
+  CHECK(throws<DataError>([&] { encode_fibers(bad); }));
+  // flip_augment
+  FiberSet two;
+  two.resample_count = 2;
+  two.fibers = {{{0, 0, 0}, {1, 0, 0}}};
+  auto aug = flip_augment(encode_fibers(two), 2);
+  const double r2 = 1.0 / std::sqrt(2.0);
+  CHECK(aug.measure.size() == 2 && aug.map.is_flipped(1) && aug.map.original_of(1) == 0);
+  CHECK(std::fabs(aug.measure.point(1)[0] - r2) < 1e-15 && aug.measure.point(1)[3] == 0.0);
+  CHECK(aug.measure.total_mass() == 1.0);
+  // density_to_measure
+  DensityMap dm;
+  dm.nx = dm.ny = dm.nz = 4;
+  dm.voxels = {{0, 0, 0, 1.0}, {1, 2, 3, 3.0}, {2, 2, 2, 0.0}};
+  DiscreteMeasure dmeas = density_to_measure(dm);
+  CHECK(dmeas.size() == 2 && dmeas.weights()[0] == 0.25 && dmeas.point(1)[2] == 3.5);
+  DensityMap empty;
+  empty.nx = empty.ny = empty.nz = 1;
+  empty.voxels = {{0, 0, 0, 0.0}};
+  CHECK(throws<DataError>([&] { density_to_measure(empty); }));
+}
+
+static void gpu_checks() {
+  using namespace msot;
+  SolverParams p;
+  p.blur = 0.01;
+  // Dirac translation -> |t|^2/2
+  DiscreteMeasure a({0, 0, 0}, {1.0}, 3), b({1.0, 0.5, 0.0}, {1.0}, 3);
+  const double s = divergence(a, b, p);
+  CHECK(std::fabs(s - 0.625) < 6.25e-3);
+  // alpha = beta: symmetric potentials, S ~ 0
+  std::vector<double> pts, w;
+  for (int i = 0; i < 500; ++i) {
+    pts.push_back(std::sin(1.3 * i));
+    pts.push_back(std::cos(0.7 * i));
+    pts.push_back(0.01 * i);
+    w.push_back(1.0 + (i % 7));
+  }
+  DiscreteMeasure c(pts, w, 3);
+  p.blur = 0.05;
+  DualPotentials u = symmetric_sinkhorn(c, c, p);
+  bool same = true;
+  for (std::size_t i = 0; i < c.size(); ++i) same = same && u.a_xx[i] == u.b_yy[i] && u.a_xy[i] == u.b_yx[i];
+  CHECK(same);
+  CHECK(std::fabs(divergence(c, c, p)) < 1e-9);
+  SolverParams q = p;
+  q.multiscale = true;
+  CHECK(std::fabs(divergence(c, c, q)) < 1e-9);
+  // softmin of SPEC.md:170
+  DiscreteMeasure x({0.0}, {1.0}, 1), y({1.5}, {1.0}, 1);
+  auto f = softmin(x, y, {0.0}, 0.3);
+  CHECK(std::fabs(f[0] - 1.125) < 1e-6);
+  // errors surface as the reference's exception types
+  SolverParams bad = p;
+  bad.cost.p = 1.0;
+  CHECK(throws<DataError>([&] { divergence(a, b, bad); }));
+  DiscreteMeasure d2({0.0, 0.0}, {1.0}, 2);
+  CHECK(throws<DataError>([&] { divergence(a, d2, p); }));
+}
+
+int main(int argc, char** argv) {
+  const std::string mode = argc > 1 ? argv[1] : "cpu";
+  cpu_checks();
+  if (mode == "gpu") gpu_checks();
+  if (failures) {
+    std::fprintf(stderr, "%d check(s) failed\n", failures);
+    return 1;
+  }
+  std::printf("frontend_test %s: ok\n", mode.c_str());
+  return 0;
+}

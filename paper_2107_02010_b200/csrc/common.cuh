@@ -12,6 +12,7 @@ constexpr int kTileRows = MSOT_TILE_ROWS;  // rows per block-sparse tile
 constexpr int kSoftminThreads = 128;       // threads per softmin CTA
 constexpr int kRowsPerThread = kTileRows / kSoftminThreads;
 constexpr int kColTile = 128;              // columns staged per smem buffer
+constexpr int kDefaultPoly16 = 3;          // exp2 on the FMA pipe for 3 of 16 (softmin.cu)
 static_assert(kRowsPerThread == 2, "softmin kernel is written for 2 rows per thread");
 
 constexpr float kLn2 = 0.69314718055994530942f;

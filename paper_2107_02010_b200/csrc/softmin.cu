@@ -72,17 +72,48 @@ struct ColWalker {
 //   r_i  = est_i/(lambda eps ln2) - R - |x^_i|^2
 // = log2 w_j + (h_j + est_i/lambda - |x_i - y_j|^2/2)/(eps ln2).  Per column
 // pair: one FADD2 + D FFMA2 + one FADD2 accumulate next to two MUFU.EX2.
-template <int D>
+// 2^e for a pair of exponents on the FMA pipe (the MUFU is the bottleneck and
+// the FMA pipe has ~40% headroom): e = j + f with j = round(e) taken from the
+// mantissa of e + 1.5*2^23, f in [-1/2, 1/2], 2^f by a degree-5 near-minimax
+// polynomial (max relative error 3.4e-7 in float32, ex2.approx: 1.7e-7), and
+// 2^j added to the exponent bits.  e is clamped to [-127, 127] so the result
+// saturates like MUFU.EX2 (~0 below, >= 2^127 above, which the finalize
+// window then rejects to the exact path).
+__device__ __forceinline__ float2 exp2_poly(float2 e) {
+  e.x = fminf(fmaxf(e.x, -127.f), 127.f);
+  e.y = fminf(fmaxf(e.y, -127.f), 127.f);
+  const float2 kShift = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
+  const float2 t = __fadd2_rn(e, kShift);
+  const float2 j = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __fadd2_rn(e, make_float2(-j.x, -j.y));
+  float2 p = __ffma2_rn(f, make_float2(1.2915660627186298e-3f, 1.2915660627186298e-3f),
+                        make_float2(9.668532758951187e-3f, 9.668532758951187e-3f));
+  p = __ffma2_rn(f, p, make_float2(5.5516887456178665e-2f, 5.5516887456178665e-2f));
+  p = __ffma2_rn(f, p, make_float2(2.4022264778614044e-1f, 2.4022264778614044e-1f));
+  p = __ffma2_rn(f, p, make_float2(6.931464672088623e-1f, 6.931464672088623e-1f));
+  p = __ffma2_rn(f, p, make_float2(1.f, 1.f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
+template <int D, bool kPoly>
 __device__ __forceinline__ float2 pair_terms(const RowState& rs, float2 Y0, float2 Y1, float2 Y2,
                                              float2 C) {
   float2 e = __fadd2_rn(make_float2(rs.r, rs.r), C);
   e = __ffma2_rn(make_float2(rs.x0, rs.x0), Y0, e);
   if (D > 1) e = __ffma2_rn(make_float2(rs.x1, rs.x1), Y1, e);
   if (D > 2) e = __ffma2_rn(make_float2(rs.x2, rs.x2), Y2, e);
+  if (kPoly) return exp2_poly(e);
   return make_float2(ex2_approx(e.x), ex2_approx(e.y));
 }
 
-template <int D>
+// Of the 16 pair-of-pairs (8 column pairs x 2 rows) of one unrolled step,
+// kPoly16 go through exp2_poly, spread evenly.  The pipes balance at
+// kPoly16 = 3 (MUFU: (16-3)/16 ex2 per pair; FMA: 5 + 8*3/16 lane-ops per
+// pair against 8 per ex2), a 1.23x ceiling over the MUFU-only roofline.
+__host__ __device__ constexpr bool poly_slot(int q, int n) { return n > 0 && (q * n) % 16 < n; }
+
+template <int D, int kPoly16>
 __global__ void __launch_bounds__(kSoftminThreads)
 softmin_kernel(const __grid_constant__ Group G) {
   __shared__ __align__(16) float smem[2][kColTile * 4];
@@ -152,15 +183,24 @@ softmin_kernel(const __grid_constant__ Group G) {
     __syncthreads();
     if (tp + kColTile < pos_end) fetch(tp + kColTile);
     const float4* s4 = reinterpret_cast<const float4*>(smem[buf]);
-#pragma unroll 4
-    for (int c = 0; c < kColTile / 2; ++c) {
-      const float4 A = s4[2 * c], B = s4[2 * c + 1];
-      const float2 Y0 = make_float2(A.x, A.y);
-      const float2 Y1 = make_float2(A.z, A.w);
-      const float2 Y2 = make_float2(B.x, B.y);
-      const float2 C = make_float2(B.z, B.w);
-      sa = __fadd2_rn(sa, pair_terms<D>(ra, Y0, Y1, Y2, C));
-      sb = __fadd2_rn(sb, pair_terms<D>(rb, Y0, Y1, Y2, C));
+    for (int c0 = 0; c0 < kColTile / 2; c0 += 8) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int c = c0 + k;
+        const float4 A = s4[2 * c], B = s4[2 * c + 1];
+        const float2 Y0 = make_float2(A.x, A.y);
+        const float2 Y1 = make_float2(A.z, A.w);
+        const float2 Y2 = make_float2(B.x, B.y);
+        const float2 C = make_float2(B.z, B.w);
+        if (poly_slot(2 * k, kPoly16))
+          sa = __fadd2_rn(sa, pair_terms<D, true>(ra, Y0, Y1, Y2, C));
+        else
+          sa = __fadd2_rn(sa, pair_terms<D, false>(ra, Y0, Y1, Y2, C));
+        if (poly_slot(2 * k + 1, kPoly16))
+          sb = __fadd2_rn(sb, pair_terms<D, true>(rb, Y0, Y1, Y2, C));
+        else
+          sb = __fadd2_rn(sb, pair_terms<D, false>(rb, Y0, Y1, Y2, C));
+      }
     }
     buf ^= 1;
   }
@@ -241,13 +281,34 @@ __global__ void softmin_fallback(const __grid_constant__ Group G) {
 
 // ---- host launchers -------------------------------------------------------
 
+// exp2 split between MUFU and the FMA pipe (see poly_slot); MSOT_POLY16
+// overrides for experiments (0 = MUFU only).
+static int poly16() {
+  static const int v = [] {
+    const char* e = getenv("MSOT_POLY16");
+    return e ? atoi(e) : kDefaultPoly16;
+  }();
+  return v;
+}
+
+template <int D>
+static void launch_d(const Group& g, dim3 grid, dim3 block, cudaStream_t st) {
+  ++g_launches;
+  switch (poly16()) {
+    case 0: softmin_kernel<D, 0><<<grid, block, 0, st>>>(g); break;
+    case 2: softmin_kernel<D, 2><<<grid, block, 0, st>>>(g); break;
+    case 4: softmin_kernel<D, 4><<<grid, block, 0, st>>>(g); break;
+    default: softmin_kernel<D, 3><<<grid, block, 0, st>>>(g); break;
+  }
+}
+
 cudaError_t launch_softmin(const Group& g, int d, cudaStream_t st) {
   if (g.n_items <= 0) return cudaSuccess;
   dim3 grid(g.n_items), block(kSoftminThreads);
   switch (d) {
-    case 1: ++g_launches; softmin_kernel<1><<<grid, block, 0, st>>>(g); break;
-    case 2: ++g_launches; softmin_kernel<2><<<grid, block, 0, st>>>(g); break;
-    default: ++g_launches; softmin_kernel<3><<<grid, block, 0, st>>>(g); break;
+    case 1: launch_d<1>(g, grid, block, st); break;
+    case 2: launch_d<2>(g, grid, block, st); break;
+    default: launch_d<3>(g, grid, block, st); break;
   }
   return cudaGetLastError();
 }

@@ -12,7 +12,10 @@ constexpr int kTileRows = MSOT_TILE_ROWS;  // rows per block-sparse tile
 constexpr int kSoftminThreads = 128;       // threads per softmin CTA
 constexpr int kRowsPerThread = kTileRows / kSoftminThreads;
 constexpr int kColTile = 128;              // columns staged per smem buffer
-constexpr int kDefaultPoly16 = 3;          // exp2 on the FMA pipe for 3 of 16 (softmin.cu)
+// exp2 on the FMA pipe for 2 of 16 pair-of-pairs (softmin.cu).  Measured on
+// B200 (C3 + dense 300k): 0 -> 4.31e12 pairs/s, 2 -> 4.37e12, 3 -> 4.16e12,
+// 4 -> 3.81e12: the pipes do not co-saturate beyond 2/16.
+constexpr int kDefaultPoly16 = 2;
 static_assert(kRowsPerThread == 2, "softmin kernel is written for 2 rows per thread");
 
 constexpr float kLn2 = 0.69314718055994530942f;

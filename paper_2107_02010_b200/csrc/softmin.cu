@@ -108,9 +108,11 @@ __device__ __forceinline__ float2 pair_terms(const RowState& rs, float2 Y0, floa
 }
 
 // Of the 16 pair-of-pairs (8 column pairs x 2 rows) of one unrolled step,
-// kPoly16 go through exp2_poly, spread evenly.  The pipes balance at
-// kPoly16 = 3 (MUFU: (16-3)/16 ex2 per pair; FMA: 5 + 8*3/16 lane-ops per
-// pair against 8 per ex2), a 1.23x ceiling over the MUFU-only roofline.
+// kPoly16 go through exp2_poly, spread evenly.  On paper the pipes balance
+// at kPoly16 = 3 (MUFU: (16-3)/16 ex2 per pair; FMA: 5 + 8*3/16 lane-ops per
+// pair against 8 per ex2), a 1.23x ceiling over the MUFU-only roofline; on
+// B200 only 2/16 pays (+1.4%, common.cuh kDefaultPoly16) — the MUFU and the
+// packed FMA pipe do not both run near 100% with the issue slots at ~85%.
 __host__ __device__ constexpr bool poly_slot(int q, int n) { return n > 0 && (q * n) % 16 < n; }
 
 template <int D, int kPoly16>

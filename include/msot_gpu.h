@@ -163,6 +163,26 @@ int msot_sinkhorn(msot_ctx* ctx, const msot_params* prm, const double* x, const 
                   double* a_xx, double* b_yy, double* a_xy, double* b_yx, double* loss_out,
                   msot_stats* stats);
 
+/* The solve plus grad_positions: envelope-theorem
+ * gradient of S with respect to the atoms of alpha (p = 2),
+ *   grad_i = sum_j pi^xy_ij (x_i - y_j) - sum_k pi^xx_ik (x_i - x_k),
+ * pi from the final potentials on the pair set of the last update.
+ * grad_x is N x D (caller order). */
+int msot_sinkhorn_grad(msot_ctx* ctx, const msot_params* prm, const double* x, const double* a,
+                       int64_t n, const double* y, const double* b, int64_t m, int d,
+                       double* loss_out, double* grad_x, msot_stats* stats);
+
+/* Wasserstein barycenter of K target measures (PAPER.md
+ * :374-386, config 5): descent on the positions of alpha (weights frozen),
+ * x <- x - step * mean_k(grad_k) / a, the step halved (<= 10 times) until the
+ * mean divergence does not increase; stops after `iters` accepted steps or a
+ * relative decrease below `tol`.  reach must be infinite, p = 2.
+ * loss_traj (nullable) receives iters+1 values; x_out is N x D. */
+int msot_barycenter(msot_ctx* ctx, const msot_params* prm, const double* x0, const double* a,
+                    int64_t n, int k, const double* const* ys, const double* const* bs,
+                    const int64_t* ms, int d, int iters, double step, double tol,
+                    double* x_out, double* loss_traj, int* steps_done, msot_stats* stats);
+
 /* Same, inputs already resident on the device (float64 device pointers). */
 int msot_sinkhorn_device(msot_ctx* ctx, const msot_params* prm, const double* d_x,
                          const double* d_a, int64_t n, const double* d_y, const double* d_b,

@@ -693,4 +693,87 @@ int oracle_sinkhorn(const msot_params* prm, const double* x, const double* a, in
   return MSOT_OK;
 }
 
+// grad_positions with the envelope theorem, dense plans:
+//   grad_i = sum_j pi^xy_ij (x_i - y_j) - sum_k pi^xx_ik (x_i - x_k),
+//   pi^xy_ij = a_i b_j exp((b_yx_i + a_xy_j - C_ij)/eps),
+//   pi^xx_ik = a_i a_k exp((a_xx_i + a_xx_k - C_ik)/eps).
+int oracle_sinkhorn_grad(const msot_params* prm, const double* x, const double* a, int64_t n,
+                         const double* y, const double* b, int64_t m, int d, double* loss_out,
+                         double* grad) {
+  if (prm->p != 2.0) return fail(MSOT_EUSAGE, "grad_positions needs p = 2");
+  Vec axx(n), byy(m), axy(m), byx(n);
+  msot_stats st{};
+  const int rc = oracle_sinkhorn(prm, x, a, n, y, b, m, d, axx.data(), byy.data(), axy.data(),
+                                 byx.data(), loss_out, &st);
+  if (rc != MSOT_OK) return rc;
+  const double eps = std::pow(prm->blur, prm->p);
+  msot::parallel::for_ranges(static_cast<std::size_t>(n), [&](std::size_t lo, std::size_t hi) {
+    for (std::size_t i = lo; i < hi; ++i) {
+      std::vector<double> g(d, 0.0);
+      const double* xi = x + i * d;
+      for (int64_t j = 0; j < m; ++j) {
+        const double* yj = y + j * d;
+        const double pij = a[i] * b[j] * std::exp((byx[i] + axy[j] - cost(xi, yj, d, 2.0)) / eps);
+        for (int k = 0; k < d; ++k) g[k] += pij * (xi[k] - yj[k]);
+      }
+      for (int64_t q = 0; q < n; ++q) {
+        const double* xq = x + q * d;
+        const double piq = a[i] * a[q] * std::exp((axx[i] + axx[q] - cost(xi, xq, d, 2.0)) / eps);
+        for (int k = 0; k < d; ++k) g[k] -= piq * (xi[k] - xq[k]);
+      }
+      for (int k = 0; k < d; ++k) grad[i * d + k] = g[k];
+    }
+  });
+  return MSOT_OK;
+}
+
+// Barycenter descent, same rules as msot_barycenter.
+int oracle_barycenter(const msot_params* prm, const double* x0, const double* a, int64_t n, int k,
+                      const double* const* ys, const double* const* bs, const int64_t* ms, int d,
+                      int iters, double step, double tol, double* x_out, double* loss_traj,
+                      int* steps_done) {
+  Vec x(x0, x0 + n * d), xn(n * d), field(n * d), fieldn(n * d), g(n * d);
+  auto evaluate = [&](const Vec& xp, Vec& fld, double& L) -> int {
+    std::fill(fld.begin(), fld.end(), 0.0);
+    L = 0.0;
+    for (int t = 0; t < k; ++t) {
+      double l = 0.0;
+      const int rc = oracle_sinkhorn_grad(prm, xp.data(), a, n, ys[t], bs[t], ms[t], d, &l, g.data());
+      if (rc != MSOT_OK) return rc;
+      for (int64_t q = 0; q < n * d; ++q) fld[q] += g[q] / k;
+      L += l;
+    }
+    L /= k;
+    return MSOT_OK;
+  };
+  double L = 0.0;
+  int rc = evaluate(x, field, L);
+  if (rc != MSOT_OK) return rc;
+  if (loss_traj) loss_traj[0] = L;
+  int done = 0;
+  double s = step;
+  while (done < iters) {
+    bool accepted = false;
+    double Ln = L;
+    for (int h = 0; h <= 10; ++h) {
+      for (int64_t q = 0; q < n * d; ++q) xn[q] = x[q] - s * field[q] / a[q / d];
+      rc = evaluate(xn, fieldn, Ln);
+      if (rc != MSOT_OK) return rc;
+      if (Ln <= L) { accepted = true; break; }
+      s *= 0.5;
+    }
+    if (!accepted) break;
+    std::swap(x, xn);
+    std::swap(field, fieldn);
+    const double rel = (L - Ln) / std::max(std::fabs(L), 1e-300);
+    L = Ln;
+    ++done;
+    if (loss_traj) loss_traj[done] = L;
+    if (rel < tol) break;
+  }
+  std::copy(x.begin(), x.end(), x_out);
+  if (steps_done) *steps_done = done;
+  return MSOT_OK;
+}
+
 }  // extern "C"

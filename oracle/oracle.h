@@ -68,6 +68,16 @@ double oracle_divergence_from_potentials(const msot_params* prm, double eps, con
                                          const double* a_xx, const double* b_yy,
                                          const double* a_xy, const double* b_yx);
 
+/* grad_positions (dense plans) and the barycenter descent
+ * (SPEC.md:356-364): same contracts as msot_sinkhorn_grad / msot_barycenter. */
+int oracle_sinkhorn_grad(const msot_params* prm, const double* x, const double* a, int64_t n,
+                         const double* y, const double* b, int64_t m, int d, double* loss_out,
+                         double* grad);
+int oracle_barycenter(const msot_params* prm, const double* x0, const double* a, int64_t n, int k,
+                      const double* const* ys, const double* const* bs, const int64_t* ms, int d,
+                      int iters, double step, double tol, double* x_out, double* loss_traj,
+                      int* steps_done);
+
 const char* oracle_last_error(void);
 
 #ifdef __cplusplus

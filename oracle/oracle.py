@@ -174,3 +174,50 @@ def divergence_from_potentials(prm, eps, a, b, pots):
     return lib().oracle_divergence_from_potentials(C.byref(prm), eps, _d(a), a.size, _d(b),
                                                    b.size, _d(P["a_xx"]), _d(P["b_yy"]),
                                                    _d(P["a_xy"]), _d(P["b_yx"]))
+
+
+def _setup_grad(L):
+    L.oracle_sinkhorn_grad.restype = C.c_int
+    L.oracle_sinkhorn_grad.argtypes = [C.POINTER(Params), _dp, _dp, C.c_int64, _dp, _dp,
+                                       C.c_int64, C.c_int, _dp, _dp]
+    L.oracle_barycenter.restype = C.c_int
+    L.oracle_barycenter.argtypes = [C.POINTER(Params), _dp, _dp, C.c_int64, C.c_int,
+                                    C.POINTER(_dp), C.POINTER(_dp), _lp, C.c_int, C.c_int,
+                                    C.c_double, C.c_double, _dp, _dp, C.POINTER(C.c_int)]
+
+
+def sinkhorn_grad(prm, x, a, y, b):
+    L = lib()
+    _setup_grad(L)
+    x, a, y, b = _c64(x), _c64(a), _c64(y), _c64(b)
+    if x.ndim == 1:
+        x = x[:, None]
+    if y.ndim == 1:
+        y = y[:, None]
+    n, d = x.shape
+    loss = C.c_double()
+    g = np.zeros((n, d))
+    rc = L.oracle_sinkhorn_grad(C.byref(prm), _d(x), _d(a), n, _d(y), _d(b), y.shape[0], d,
+                                C.byref(loss), _d(g))
+    raise_status(rc, L.oracle_last_error().decode())
+    return loss.value, g
+
+
+def barycenter(prm, x0, a, targets, iters=10, step=1.0, tol=1e-4):
+    L = lib()
+    _setup_grad(L)
+    x0, a = _c64(x0), _c64(a)
+    n, d = x0.shape
+    ys = [_c64(t[0]).reshape(-1, d) for t in targets]
+    bs = [_c64(t[1]) for t in targets]
+    k = len(targets)
+    yp = (_dp * k)(*[_d(v) for v in ys])
+    bp = (_dp * k)(*[_d(v) for v in bs])
+    ms = np.array([len(v) for v in bs], np.int64)
+    x = np.zeros((n, d))
+    traj = np.zeros(iters + 1)
+    done = C.c_int()
+    rc = L.oracle_barycenter(C.byref(prm), _d(x0), _d(a), n, k, yp, bp, ms.ctypes.data_as(_lp),
+                             d, iters, step, tol, _d(x), _d(traj), C.byref(done))
+    raise_status(rc, L.oracle_last_error().decode())
+    return x, traj[:done.value + 1].copy()

@@ -35,6 +35,8 @@ struct Problem {
   const int64_t* tile_rptr;  // [n_tiles+1] range index per row tile
   const int2* ranges;        // column ranges [begin, end)
   const int32_t* tile_ibase; // [n_tiles+1] work items per row tile (prefix)
+  const float4* col_pay;     // plan_kernel: column payload v_j
+  float4* row_plan;          // plan_kernel: {m_i, u_i} per row
   int32_t n_rows, n_cols;
   float sc;                // 1 / sqrt(2 eps ln2): scaled |dx|^2 = C / (eps ln2)
   float inv_eps_ln2;       // 1 / (eps ln 2)

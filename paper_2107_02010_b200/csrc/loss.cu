@@ -111,3 +111,72 @@ cudaError_t scatter_unsort(const float* v, const int32_t* perm, int64_t n, const
 }
 
 }  // namespace msot_dev
+
+namespace msot_dev {
+
+// grad_positions, envelope theorem with the final
+// potentials: d S / d x_i = sum_j pi^xy_ij (x_i - y_j) - sum_k pi^xx_ik (x_i - x_k)
+// (the self term of -1/2 OT(a,a) counts twice), i.e.
+//   a_i [ (m^xy_i - m^xx_i) x_i - (u^xy_i - u^xx_i) ]
+// with m, u the per-row plan sums of plan_kernel (pi / a_i, payload = coordinates).
+__global__ void grad_positions_kernel(const float4* pts, const double* w64, const float4* pxy,
+                                      const float4* pxx, const int32_t* perm, int64_t n, int d,
+                                      double* grad) {
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const float4 x = pts[s], a = pxy[s], b = pxx[s];
+  const double dm = static_cast<double>(a.x) - static_cast<double>(b.x);
+  const double g[3] = {dm * x.x - (static_cast<double>(a.y) - b.y),
+                       dm * x.y - (static_cast<double>(a.z) - b.z),
+                       dm * x.z - (static_cast<double>(a.w) - b.w)};
+  const int64_t i = perm ? perm[s] : s;
+  for (int k = 0; k < d; ++k) grad[i * d + k] = w64[s] * g[k];
+}
+
+cudaError_t grad_positions(const float4* pts, const double* w64, const float4* plan_xy,
+                           const float4* plan_xx, const int32_t* perm, int64_t n, int d,
+                           double* grad, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  ++g_launches;
+  grad_positions_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(
+      pts, w64, plan_xy, plan_xx, perm, n, d, grad);
+  return cudaGetLastError();
+}
+
+}  // namespace msot_dev
+
+namespace msot_dev {
+
+// field += scale * grad   (float64, n*d)
+__global__ void axpy_kernel(double* field, const double* grad, double scale, int64_t len) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < len) field[i] += scale * grad[i];
+}
+
+// x_new = x - step * field / a   (barycenter descent on the positions with the
+// displacement field grad / a_i)
+__global__ void bary_step_kernel(double* x_new, const double* x, const double* field,
+                                 const double* a, double step, int64_t n, int d) {
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g >= n * d) return;
+  x_new[g] = x[g] - step * field[g] / a[g / d];
+}
+
+cudaError_t field_accumulate(double* field, const double* grad, double scale, int64_t len,
+                             cudaStream_t st) {
+  if (len <= 0) return cudaSuccess;
+  ++g_launches;
+  axpy_kernel<<<static_cast<unsigned>((len + 255) / 256), 256, 0, st>>>(field, grad, scale, len);
+  return cudaGetLastError();
+}
+
+cudaError_t bary_step(double* x_new, const double* x, const double* field, const double* a,
+                      double step, int64_t n, int d, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  ++g_launches;
+  bary_step_kernel<<<static_cast<unsigned>((n * d + 255) / 256), 256, 0, st>>>(x_new, x, field, a,
+                                                                               step, n, d);
+  return cudaGetLastError();
+}
+
+}  // namespace msot_dev

@@ -28,6 +28,19 @@ cudaError_t radix_sort_pairs(uint32_t* keys, int32_t* vals, int64_t n, int key_b
 cudaError_t launch_softmin(const Group& g, int d, cudaStream_t st);
 cudaError_t launch_finalize(const Group& g, cudaStream_t st);
 cudaError_t launch_fallback(const Group& g, int d, int n_sm, cudaStream_t st);
+cudaError_t launch_plan(const Group& g, int d, cudaStream_t st);  // plan_kernel + plan_finalize
+
+// positions gradient of S (loss.cu): rows of x, sorted order ->
+// grad[perm[s]] = a_s ((m_xy - m_xx) x_s - (u_xy - u_xx)) (float64, caller order;
+// frame-invariant, so the centred coordinates are used as they are)
+cudaError_t grad_positions(const float4* pts, const double* w64, const float4* plan_xy,
+                           const float4* plan_xx, const int32_t* perm, int64_t n, int d,
+                           double* grad, cudaStream_t st);
+// barycenter descent helpers (loss.cu)
+cudaError_t field_accumulate(double* field, const double* grad, double scale, int64_t len,
+                             cudaStream_t st);
+cudaError_t bary_step(double* x_new, const double* x, const double* field, const double* a,
+                      double step, int64_t n, int d, cudaStream_t st);
 
 // clustering (cluster.cu)
 struct GridSpec {

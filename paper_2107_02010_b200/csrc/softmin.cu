@@ -211,6 +211,134 @@ softmin_kernel(const __grid_constant__ Group G) {
   out[tid + kSoftminThreads] = sb.x + sb.y;
 }
 
+// Implicit transport plan applied to column payloads (SPEC.md:204-212,
+// PAPER.md eq. 4): with est = f (final row potential), h = g and lambda = 1
+// the exponent is log2 of pi_ij / alpha_i = beta_j exp((f_i + g_j - C_ij)/eps),
+// so one pass gives, per row, m_i = sum_j pi_ij / alpha_i and
+// u_i = sum_j pi_ij v_j / alpha_i for a float4 payload v (the column
+// coordinates for the barycentric map / grad_positions).
+// Partials: part[item][4][256] = {m, u.x, u.y, u.z}.
+template <int D>
+__global__ void __launch_bounds__(kSoftminThreads)
+plan_kernel(const __grid_constant__ Group G) {
+  __shared__ __align__(16) float smem[2][kColTile * 4];
+  __shared__ __align__(16) float spay[2][kColTile * 4];
+  const int it = blockIdx.x;
+  if (it >= G.n_items) return;
+  const int4 item = G.items[it];
+  const Problem& P = G.P[item.x];
+  const int tid = threadIdx.x;
+  const int row_base = P.tile_start[item.y];
+  const int row_end = P.tile_start[item.y + 1];
+  const int mid = (row_base + row_end) >> 1;
+  const float4 o = P.rows[mid];
+  const float R = P.row_est ? P.row_est[mid] * P.inv_lam_eps_ln2 : 0.f;
+  RowState ra, rb;
+  load_row<D>(P, row_base + tid, row_end, o, R, ra);
+  load_row<D>(P, row_base + tid + kSoftminThreads, row_end, o, R, rb);
+  ColWalker w{P.ranges, P.tile_rptr[item.y], P.tile_rptr[item.y + 1], 0};
+  const int32_t pos_begin = item.z, pos_end = item.w;
+  float4 cv = make_float4(0.f, 0.f, 0.f, 0.f), pv = cv;
+  float ch = 0.f, cl = 0.f;
+  bool cvalid = false;
+  auto fetch = [&](int32_t tile_pos) {
+    const int32_t pos = tile_pos + tid;
+    cvalid = false;
+    if (pos < pos_end) {
+      const int j = w.col(pos);
+      if (j >= 0) {
+        cv = __ldg(P.cols + j);
+        pv = __ldg(P.col_pay + j);
+        cl = __ldg(P.col_lw2 + j);
+        ch = __ldg(P.col_h + j);
+        cvalid = true;
+      }
+    }
+  };
+  auto stage = [&](float* buf, float* pbuf) {
+    float* rec = buf + (tid >> 1) * 8 + (tid & 1);
+    float* prc = pbuf + (tid >> 1) * 8 + (tid & 1);
+    if (cvalid) {
+      const float a = (cv.x - o.x) * P.sc;
+      const float b = D > 1 ? (cv.y - o.y) * P.sc : 0.f;
+      const float c = D > 2 ? (cv.z - o.z) * P.sc : 0.f;
+      rec[0] = a;
+      rec[2] = b;
+      rec[4] = c;
+      rec[6] = (fmaf(ch, P.inv_eps_ln2, R) + cl) - fmaf(a, a, fmaf(b, b, c * c));
+      prc[0] = pv.x;
+      prc[2] = pv.y;
+      prc[4] = pv.z;
+    } else {
+      rec[0] = rec[2] = rec[4] = 0.f;
+      rec[6] = __int_as_float(0xff800000);
+      prc[0] = prc[2] = prc[4] = 0.f;
+    }
+  };
+  float2 ma = make_float2(0.f, 0.f), mb = ma, a0 = ma, a1 = ma, a2 = ma, b0 = ma, b1 = ma, b2 = ma;
+  int buf = 0;
+  fetch(pos_begin);
+  for (int32_t tp = pos_begin; tp < pos_end; tp += kColTile) {
+    stage(smem[buf], spay[buf]);
+    __syncthreads();
+    if (tp + kColTile < pos_end) fetch(tp + kColTile);
+    const float4* s4 = reinterpret_cast<const float4*>(smem[buf]);
+    const float4* p4 = reinterpret_cast<const float4*>(spay[buf]);
+#pragma unroll 4
+    for (int c = 0; c < kColTile / 2; ++c) {
+      const float4 A = s4[2 * c], B = s4[2 * c + 1];
+      const float4 PA = p4[2 * c], PB = p4[2 * c + 1];
+      const float2 Y0 = make_float2(A.x, A.y), Y1 = make_float2(A.z, A.w);
+      const float2 Y2 = make_float2(B.x, B.y), C = make_float2(B.z, B.w);
+      const float2 V0 = make_float2(PA.x, PA.y), V1 = make_float2(PA.z, PA.w);
+      const float2 V2 = make_float2(PB.x, PB.y);
+      const float2 ea = pair_terms<D, false>(ra, Y0, Y1, Y2, C);
+      const float2 eb = pair_terms<D, false>(rb, Y0, Y1, Y2, C);
+      ma = __fadd2_rn(ma, ea);
+      mb = __fadd2_rn(mb, eb);
+      a0 = __ffma2_rn(ea, V0, a0);
+      a1 = __ffma2_rn(ea, V1, a1);
+      a2 = __ffma2_rn(ea, V2, a2);
+      b0 = __ffma2_rn(eb, V0, b0);
+      b1 = __ffma2_rn(eb, V1, b1);
+      b2 = __ffma2_rn(eb, V2, b2);
+    }
+    buf ^= 1;
+  }
+  float* out = G.part + static_cast<int64_t>(it) * 4 * kTileRows;
+  const int r2 = tid + kSoftminThreads;
+  out[tid] = ma.x + ma.y;
+  out[kTileRows + tid] = a0.x + a0.y;
+  out[2 * kTileRows + tid] = a1.x + a1.y;
+  out[3 * kTileRows + tid] = a2.x + a2.y;
+  out[r2] = mb.x + mb.y;
+  out[kTileRows + r2] = b0.x + b0.y;
+  out[2 * kTileRows + r2] = b1.x + b1.y;
+  out[3 * kTileRows + r2] = b2.x + b2.y;
+}
+
+// Sums the plan partials of every row in a fixed chunk order into
+// row_plan[r] = {m_r, u_r} (float4).
+__global__ void __launch_bounds__(kTileRows) plan_finalize(const __grid_constant__ Group G) {
+  const int b = blockIdx.x;
+  int p = 0;
+  while (p + 1 < G.n_problems && b >= G.tile_prefix[p + 1]) ++p;
+  const Problem& P = G.P[p];
+  const int t = G.t0[p] + (b - G.tile_prefix[p]);
+  const int lr = threadIdx.x;
+  const int r = P.tile_start[t] + lr;
+  if (r >= P.tile_start[t + 1]) return;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int32_t k = P.tile_ibase[t]; k < P.tile_ibase[t + 1]; ++k) {
+    const float* q = G.part + static_cast<int64_t>(k) * 4 * kTileRows + lr;
+    s.x += q[0];
+    s.y += q[kTileRows];
+    s.z += q[2 * kTileRows];
+    s.w += q[3 * kTileRows];
+  }
+  P.row_plan[r] = s;
+}
+
 // Combines the partial sums of every row (fixed chunk order: deterministic
 // and independent of the number of GPUs) and applies the update
 //   new = est - mixw * lambda eps ln(s)   (averaging of PAPER.md:293-315).
@@ -311,6 +439,23 @@ cudaError_t launch_softmin(const Group& g, int d, cudaStream_t st) {
     case 1: launch_d<1>(g, grid, block, st); break;
     case 2: launch_d<2>(g, grid, block, st); break;
     default: launch_d<3>(g, grid, block, st); break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_plan(const Group& g, int d, cudaStream_t st) {
+  if (g.n_items <= 0) return cudaSuccess;
+  dim3 grid(g.n_items), block(kSoftminThreads);
+  ++g_launches;
+  switch (d) {
+    case 1: plan_kernel<1><<<grid, block, 0, st>>>(g); break;
+    case 2: plan_kernel<2><<<grid, block, 0, st>>>(g); break;
+    default: plan_kernel<3><<<grid, block, 0, st>>>(g); break;
+  }
+  const int tiles = g.tile_prefix[g.n_problems];
+  if (tiles > 0) {
+    ++g_launches;
+    plan_finalize<<<tiles, kTileRows, 0, st>>>(g);
   }
   return cudaGetLastError();
 }

@@ -477,9 +477,67 @@ void sym_step(msot_ctx* c, const Plan& P, Potentials& U, int& cur, double eps, d
   cur ^= 1;
 }
 
+// Implicit plan sums (plan_kernel) for problems `specs` with row potentials
+// f, column potentials g and column payloads: out[p] = {m_i, u_i} per row.
+// Not sharded: every rank computes all rows (the outputs are small).
+void plan_group(msot_ctx* c, const std::string& tag, int np, const ProbSpec* specs,
+                const float* const* f, const float* const* g, const float4* const* pay,
+                float4* const* out, double eps, int d) {
+  const int rank = c->rank, world = c->world;
+  c->rank = 0;
+  c->world = 1;
+  Plan P;
+  P.np = np;
+  for (int p = 0; p < np; ++p) P.ps[p] = specs[p];
+  try {
+    build_plan(c, tag, P);
+  } catch (...) {
+    c->rank = rank;
+    c->world = world;
+    throw;
+  }
+  c->rank = rank;
+  c->world = world;
+  const double ln2 = 0.69314718055994530942;
+  Group G{};
+  int32_t tiles_acc = 0;
+  for (int p = 0; p < np; ++p) {
+    Problem& Q = G.P[p];
+    const ProbSpec& S = P.ps[p];
+    Q.rows = S.rows;
+    Q.row_est = f[p];
+    Q.row_out = nullptr;
+    Q.cols = S.cols;
+    Q.col_lw2 = S.col_lw2;
+    Q.col_h = g[p];
+    Q.tile_start = S.rs->tile_start;
+    Q.tile_rptr = S.rs->rptr;
+    Q.ranges = S.rs->ranges;
+    Q.tile_ibase = P.ibase[p];
+    Q.col_pay = pay[p];
+    Q.row_plan = out[p];
+    Q.n_rows = static_cast<int32_t>(S.n_rows);
+    Q.n_cols = static_cast<int32_t>(S.n_cols);
+    Q.sc = static_cast<float>(1.0 / std::sqrt(2.0 * eps * ln2));
+    Q.inv_eps_ln2 = static_cast<float>(1.0 / (eps * ln2));
+    Q.inv_lam_eps_ln2 = Q.inv_eps_ln2;  // lambda = 1: exp((f + g - C) / eps)
+    Q.lam_eps = static_cast<float>(eps);
+    Q.mixw = 1.f;
+    G.t0[p] = 0;
+    G.tile_prefix[p] = tiles_acc;
+    tiles_acc += static_cast<int32_t>(S.rs->n_tiles);
+  }
+  G.tile_prefix[np] = tiles_acc;
+  G.n_problems = np;
+  G.items = P.items;
+  G.n_items = P.n_items;
+  G.part = c->buf<float>(tag + ".ppart", static_cast<size_t>(P.n_items) * 4 * kTileRows);
+  CK(launch_plan(G, d, c->st));
+}
+
 void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const double* d_a,
                   int64_t n, const double* d_y, const double* d_b, int64_t m, int d,
-                  double* loss_out, msot_stats* S, double* h_pots[4]) {
+                  double* loss_out, msot_stats* S, double* h_pots[4], double* d_grad = nullptr) {
   if (n < 1 || m < 1) raise(MSOT_EDATA, "empty measure");
   if (n > 0x7fffff00LL || m > 0x7fffff00LL) raise(MSOT_EDATA, "measure too large");
   if (d < 1 || d > 3) raise(MSOT_EUSAGE, "the GPU softmin supports D in 1..3");
@@ -543,10 +601,11 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
   int cur = 0;
   const double full = double(n) * n + double(m) * m + 2.0 * double(n) * m;
 
+  RangeSet fxx, fyy, fxy, fyx;  // ranges of the last update (the plan reuses them)
   if (!ms) {
     c->mark(4);  // phase 4: symmetric updates
     S->t_switch = 0;
-    RangeSet rxx, ryy, rxy, ryx;
+    RangeSet &rxx = fxx, &ryy = fyy, &rxy = fxy, &ryx = fyx;
     dense_rangeset(c, "d.xx", n, n, rxx);
     dense_rangeset(c, "d.yy", m, m, ryy);
     dense_rangeset(c, "d.xy", m, n, rxy);
@@ -643,7 +702,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
     grad[1] = c->buf<float4>("m.gyy", Y.k);
     grad[2] = c->buf<float4>("m.gxy", Y.k);
     grad[3] = c->buf<float4>("m.gyx", X.k);
-    RangeSet rxx, ryy, rxy, ryx;
+    RangeSet &rxx = fxx, &ryy = fyy, &rxy = fxy, &ryx = fyx;
     Plan Pf;
     auto build_masks = [&](double e) {
       // without a coarse phase there is no information: keep every pair
@@ -694,6 +753,20 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
       S->pairs_fine += Pf.pairs_all;
       S->pairs_fine_dense += full;
     }
+  }
+
+  // grad_positions from the final potentials, on the pair
+  // sets of the last update: cross plan (rows x, cols y) and self plan
+  if (d_grad) {
+    c->mark(5);
+    float** f = U.v[cur];
+    const ProbSpec specs[2] = {{X.pts, n, Y.pts, Y.lw2, m, &fyx}, {X.pts, n, X.pts, X.lw2, n, &fxx}};
+    const float* fr[2] = {f[3], f[0]};  // b_yx, a_xx
+    const float* gc[2] = {f[2], f[0]};  // a_xy, a_xx
+    const float4* pay[2] = {Y.pts, X.pts};
+    float4* outp[2] = {c->buf<float4>("grad.pxy", n), c->buf<float4>("grad.pxx", n)};
+    plan_group(c, "pg", 2, specs, fr, gc, pay, outp, eps[ns - 1], d);
+    CK(grad_positions(X.pts, X.w64, outp[0], outp[1], X.perm, n, d, d_grad, st));
   }
 
   // divergence (eq. 5-6), fixed-order float64
@@ -934,6 +1007,129 @@ int msot_sinkhorn_device(msot_ctx* c, const msot_params* prm, const double* d_x,
     S->rank = c->rank;
     S->world = c->world;
     solve_device(c, prm, d_x, d_a, n, d_y, d_b, m, d, loss_out, S, nullptr);
+  });
+}
+
+int msot_sinkhorn_grad(msot_ctx* c, const msot_params* prm, const double* x, const double* a,
+                       int64_t n, const double* y, const double* b, int64_t m, int d,
+                       double* loss_out, double* grad_x, msot_stats* stats) {
+  return guard([&] {
+    if (!c || !prm || !x || !a || !y || !b || !loss_out || !grad_x) raise(MSOT_EUSAGE, "null argument");
+    if (n < 1 || m < 1) raise(MSOT_EDATA, "empty measure");
+    if (prm->p != 2.0) raise(MSOT_EUSAGE, "grad_positions is defined for p = 2 (SPEC.md:348)");
+    check_weights(a, n);
+    check_weights(b, m);
+    CK(cudaSetDevice(c->device));
+    msot_stats local{};
+    msot_stats* S = stats ? stats : &local;
+    std::memset(S, 0, sizeof(*S));
+    S->rank = c->rank;
+    S->world = c->world;
+    double* dx = c->buf<double>("in.x", n * d);
+    double* da = c->buf<double>("in.a", n);
+    double* dy = c->buf<double>("in.y", m * d);
+    double* db = c->buf<double>("in.b", m);
+    double* dg = c->buf<double>("in.grad", n * d);
+    CK(cudaMemcpyAsync(dx, x, n * d * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(da, a, n * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(dy, y, m * d * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(db, b, m * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    solve_device(c, prm, dx, da, n, dy, db, m, d, loss_out, S, nullptr, dg);
+    CK(cudaMemcpyAsync(grad_x, dg, n * d * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+  });
+}
+
+// Wasserstein barycenter by descent on the atom positions (SPEC.md:356-364,
+// PAPER.md:374-386): minimise (1/K) sum_k S(alpha, beta_k) over x with frozen
+// weights; field = mean_k grad_k / a_i; x <- x - step * field, the step
+// halved (up to 10 times) until the loss does not increase; stops after
+// `iters` accepted steps or when the relative decrease falls below `tol`.
+int msot_barycenter(msot_ctx* c, const msot_params* prm, const double* x0, const double* a,
+                    int64_t n, int k, const double* const* ys, const double* const* bs,
+                    const int64_t* ms, int d, int iters, double step, double tol, double* x_out,
+                    double* loss_traj, int* steps_done, msot_stats* stats) {
+  return guard([&] {
+    if (!c || !prm || !x0 || !a || !ys || !bs || !ms || !x_out || k < 1 || iters < 0)
+      raise(MSOT_EUSAGE, "invalid barycenter arguments");
+    if (prm->p != 2.0) raise(MSOT_EUSAGE, "barycenter descent is defined for p = 2");
+    if (!msot_reach_is_inf(prm->reach)) raise(MSOT_EUSAGE, "barycenter requires reach = inf (SPEC.md:332)");
+    if (!(step > 0)) raise(MSOT_EUSAGE, "step must be > 0");
+    check_weights(a, n);
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->st;
+    msot_stats local{};
+    msot_stats* S = stats ? stats : &local;
+    std::memset(S, 0, sizeof(*S));
+    S->rank = c->rank;
+    S->world = c->world;
+    double* dx = c->buf<double>("bc.x", n * d);
+    double* dxn = c->buf<double>("bc.xnew", n * d);
+    double* da = c->buf<double>("bc.a", n);
+    double* field = c->buf<double>("bc.field", n * d);
+    double* fieldn = c->buf<double>("bc.fieldnew", n * d);
+    double* grad = c->buf<double>("bc.grad", n * d);
+    std::vector<double*> dy(k), db(k);
+    for (int t = 0; t < k; ++t) {
+      if (ms[t] < 1) raise(MSOT_EDATA, "empty target measure");
+      check_weights(bs[t], ms[t]);
+      dy[t] = c->buf<double>("bc.y" + std::to_string(t), ms[t] * d);
+      db[t] = c->buf<double>("bc.b" + std::to_string(t), ms[t]);
+      CK(cudaMemcpyAsync(dy[t], ys[t], ms[t] * d * sizeof(double), cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(db[t], bs[t], ms[t] * sizeof(double), cudaMemcpyHostToDevice, st));
+    }
+    CK(cudaMemcpyAsync(dx, x0, n * d * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(da, a, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    // loss and mean gradient at positions xp (into fld)
+    auto evaluate = [&](const double* xp, double* fld) {
+      CK(cudaMemsetAsync(fld, 0, n * d * sizeof(double), st));
+      double tot = 0.0;
+      for (int t = 0; t < k; ++t) {
+        msot_stats s1{};
+        double l = 0.0;
+        solve_device(c, prm, xp, da, n, dy[t], db[t], ms[t], d, &l, &s1, nullptr, grad);
+        CK(field_accumulate(fld, grad, 1.0 / k, n * d, st));
+        tot += l;
+        S->pairs_evaluated += s1.pairs_evaluated;
+        S->pairs_dense += s1.pairs_dense;
+        S->softmin_launches += s1.softmin_launches;
+        S->gpu_launches += s1.gpu_launches;
+        S->total_ms += s1.total_ms;
+        S->fallback_rows += s1.fallback_rows;
+      }
+      return tot / k;
+    };
+    double L = evaluate(dx, field);
+    if (!std::isfinite(L)) raise(MSOT_ENUMERIC, "non-finite barycenter loss at iteration 0");
+    if (loss_traj) loss_traj[0] = L;
+    int done = 0;
+    double s = step;
+    while (done < iters) {
+      bool accepted = false;
+      double Ln = L;
+      for (int h = 0; h <= 10; ++h) {
+        CK(bary_step(dxn, dx, field, da, s, n, d, st));
+        Ln = evaluate(dxn, fieldn);
+        if (!std::isfinite(Ln))
+          raise(MSOT_ENUMERIC, "non-finite barycenter loss at iteration " + std::to_string(done + 1));
+        if (Ln <= L) {
+          accepted = true;
+          break;
+        }
+        s *= 0.5;
+      }
+      if (!accepted) break;
+      std::swap(dx, dxn);
+      std::swap(field, fieldn);
+      const double rel = (L - Ln) / std::max(std::fabs(L), 1e-300);
+      L = Ln;
+      ++done;
+      if (loss_traj) loss_traj[done] = L;
+      if (rel < tol) break;
+    }
+    CK(cudaMemcpyAsync(x_out, dx, n * d * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (steps_done) *steps_done = done;
   });
 }
 

@@ -58,6 +58,12 @@ def lib():
                                     _dp, C.c_int64, C.c_int, _dp, _dp, _dp, _dp, _dp,
                                     C.POINTER(Stats)]
         L.msot_probe_ex2.argtypes = [C.c_void_p, _dp]
+        L.msot_sinkhorn_grad.argtypes = [C.c_void_p, C.POINTER(Params), _dp, _dp, C.c_int64, _dp,
+                                         _dp, C.c_int64, C.c_int, _dp, _dp, C.POINTER(Stats)]
+        L.msot_barycenter.argtypes = [C.c_void_p, C.POINTER(Params), _dp, _dp, C.c_int64,
+                                      C.c_int, C.POINTER(_dp), C.POINTER(_dp), _lp, C.c_int,
+                                      C.c_int, C.c_double, C.c_double, _dp, _dp,
+                                      C.POINTER(C.c_int), C.POINTER(Stats)]
         L.msot_sinkhorn_device.argtypes = [C.c_void_p, C.POINTER(Params), C.c_void_p,
                                            C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                            C.c_int64, C.c_int, _dp, C.POINTER(Stats)]
@@ -69,7 +75,8 @@ def lib():
 EXPORTS = ["msot_last_error", "msot_params_default", "msot_create", "msot_nccl_unique_id",
            "msot_create_dist", "msot_destroy", "msot_set_profiling", "msot_schedule",
            "msot_shard_tiles", "msot_softmin", "msot_grid_cluster", "msot_truncation_mask",
-           "msot_sinkhorn", "msot_sinkhorn_device", "msot_probe_ex2"]
+           "msot_sinkhorn", "msot_sinkhorn_device", "msot_probe_ex2", "msot_sinkhorn_grad",
+           "msot_barycenter"]
 
 
 def _check(rc):
@@ -229,6 +236,42 @@ class Context:
             s, e, _ = make_schedule(st.diameter, prm)
             duals = DualPotentials(*pots, eps=float(e[-1]))
         return loss.value, duals, st.as_dict()
+
+    # -- grad_positions
+    def sinkhorn_grad(self, prm, x, a, y, b):
+        """Returns (loss, grad_x (N x D), stats)."""
+        x, a, y, b = _c64(x), _c64(a), _c64(y), _c64(b)
+        if x.ndim == 1:
+            x = x[:, None]
+        if y.ndim == 1:
+            y = y[:, None]
+        n, d = x.shape
+        loss = C.c_double()
+        st = Stats()
+        g = np.zeros((n, d))
+        _check(lib().msot_sinkhorn_grad(self._h, C.byref(prm), _d(x), _d(a), n, _d(y), _d(b),
+                                        y.shape[0], d, C.byref(loss), _d(g), C.byref(st)))
+        return loss.value, g, st.as_dict()
+
+    # -- barycenter (SPEC.md:356-364)
+    def barycenter(self, prm, x0, a, targets, iters=10, step=1.0, tol=1e-4):
+        """targets: list of (points, weights).  Returns (x, loss trajectory, stats)."""
+        x0, a = _c64(x0), _c64(a)
+        n, d = x0.shape
+        ys = [_c64(t[0]).reshape(-1, d) for t in targets]
+        bs = [_c64(t[1]) for t in targets]
+        k = len(targets)
+        yp = (_dp * k)(*[_d(v) for v in ys])
+        bp = (_dp * k)(*[_d(v) for v in bs])
+        ms = np.array([len(v) for v in bs], np.int64)
+        x = np.zeros((n, d))
+        traj = np.zeros(iters + 1)
+        done = C.c_int()
+        st = Stats()
+        _check(lib().msot_barycenter(self._h, C.byref(prm), _d(x0), _d(a), n, k, yp, bp,
+                                     ms.ctypes.data_as(_lp), d, iters, step, tol, _d(x),
+                                     _d(traj), C.byref(done), C.byref(st)))
+        return x, traj[:done.value + 1].copy(), st.as_dict()
 
     def sinkhorn_device(self, prm, x_ptr, a_ptr, n, y_ptr, b_ptr, m, d):
         """Inputs already resident in HBM (float64 device pointers)."""

@@ -17,8 +17,8 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_obj")
 LIB = os.path.join(HERE, "libmsot_b200.so")
 
-SOURCES = ["softmin.cu", "prims.cu", "cluster.cu", "mask.cu", "loss.cu", "probe.cu", "solver.cu",
-           "frontend.cpp"]
+SOURCES = ["softmin.cu", "softmin_hd.cu", "prims.cu", "cluster.cu", "mask.cu", "loss.cu",
+           "probe.cu", "solver.cu", "frontend.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",

@@ -37,6 +37,13 @@ struct Problem {
   const int32_t* tile_ibase; // [n_tiles+1] work items per row tile (prefix)
   const float4* col_pay;     // plan_kernel: column payload v_j
   float4* row_plan;          // plan_kernel: {m_i, u_i} per row
+  // high-dimensional path (softmin_hd.cu): pre-swizzled split-f16 operands
+  const uint8_t* a_pack;     // rows, [hi, hi, lo] per 128-row block
+  const uint8_t* b_pack;     // cols, [hi, lo, hi] per 128-col block
+  const float* row_sq;       // |x_i|^2 (float32 coordinates)
+  const float* col_sq;       // |y_j|^2
+  const float* row_f;        // float32 coordinates, row-major x 64 (exact fallback)
+  const float* col_f;
   int32_t n_rows, n_cols;
   float sc;                // 1 / sqrt(2 eps ln2): scaled |dx|^2 = C / (eps ln2)
   float inv_eps_ln2;       // 1 / (eps ln 2)

@@ -30,6 +30,15 @@ cudaError_t launch_finalize(const Group& g, cudaStream_t st);
 cudaError_t launch_fallback(const Group& g, int d, int n_sm, cudaStream_t st);
 cudaError_t launch_plan(const Group& g, int d, cudaStream_t st);  // plan_kernel + plan_finalize
 
+// high-dimensional softmin (softmin_hd.cu): tcgen05 split-f16 <x,y>
+int64_t hd_padded(int64_t n);
+size_t hd_pack_bytes(int64_t n);
+cudaError_t hd_pack(const double* x, int64_t n, int d, const double* center, int role,
+                    uint8_t* pack, float* sq, float* xf, cudaStream_t st);
+cudaError_t hd_weights(const double* w, int64_t n, float* lw2, double* w64, cudaStream_t st);
+cudaError_t launch_softmin_hd(const Group& g, int d, int n_sm, cudaStream_t st);
+cudaError_t launch_fallback_hd(const Group& g, int d, int n_sm, cudaStream_t st);
+
 // positions gradient of S (loss.cu): rows of x, sorted order ->
 // grad[perm[s]] = a_s ((m_xy - m_xx) x_s - (u_xy - u_xx)) (float64, caller order;
 // frame-invariant, so the centred coordinates are used as they are)

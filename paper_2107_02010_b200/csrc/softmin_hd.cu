@@ -1,0 +1,387 @@
+// softmin_hd.cu — K1h: the softmin for high feature dimension (D <= 64; the
+// D = 60 fibre features of config 4) with the <x, y> term
+// on the 5th-generation tensor cores.
+//
+//   f_i = -lambda eps log sum_j w_j exp((h_j + est_i/lambda... ) ), written as
+//   E_ij = c_j + r_i + <x_i, y_j> / (eps ln2)            (log2 units)
+//   c_j  = log2 w_j + (h_j - |y_j|^2 / 2) / (eps ln2),   r_i = est_i/(lambda eps ln2) - |x_i|^2/(2 eps ln2)
+//
+// Precision: a single TF32/F16 product has ~2^-11 relative error, i.e. an
+// error of ~0.5 in E at blur 0.03 — far outside the 1e-3 eps tolerance.  Each
+// coordinate (centred, x 2^6) is split x = hi + lo into two float16s and the
+// MMA computes hi.hi + hi.lo + lo.hi (relative error ~2^-22) as ONE K = 192
+// GEMM: A = [hi | hi | lo], B = [hi | lo | hi], three 64-wide K chunks.
+//
+// Kernel (one CTA per work item = 256 rows x a run of 128-column blocks):
+//   warp 0      producer: cp.async.bulk (TMA) of pre-swizzled 16 KB blocks
+//               (A once, B per stage; 2 stages) onto mbarriers
+//   warp 1      TMEM owner + MMA issuer: per column block, 2 x 12
+//               tcgen05.mma.kind::f16 (M=128 halves, N=128, K=16 steps) into
+//               a double-buffered 2 x 256-column fp32 accumulator (512 cols)
+//   warps 4-11  epilogue (two warpgroups, one per M=128 half; one TMEM lane
+//               = one row per thread): tcgen05.ld 32x32b.x32, E = fma, MUFU
+//               ex2, running row sum; arrive on the TMEM-empty barrier
+// Operands are K-major, 128-byte swizzled (SWIZZLE_128B, 1024-byte atoms):
+// 16-byte chunk q of row r sits at r*128 + ((q ^ (r & 7)) * 16).
+#include <cuda_fp16.h>
+
+#include "prims.cuh"
+
+namespace msot_dev {
+
+constexpr int kHdK = 64;                 // f16 per 128-byte row (one swizzle atom)
+constexpr int kHdChunks = 3;             // split products
+constexpr int kHdBlockRows = 128;
+constexpr int kHdBlockBytes = kHdBlockRows * 128;            // 16 KB
+constexpr int kHdPackBytes = kHdChunks * kHdBlockBytes;      // 48 KB per 128 atoms
+constexpr int kHdStages = 2;
+constexpr int kHdThreads = 384;          // 12 warps
+constexpr float kHdScale = 64.f;         // coordinate scale before the f16 split
+constexpr size_t kHdSmem = 2 * kHdPackBytes + kHdStages * kHdPackBytes + 2 * 128 * 4 + 1024 + 256;
+
+// ---------------------------------------------------------------- packing --
+// One thread per (atom, 16-byte chunk): writes the chunk's 8 f16 of each of
+// the three K chunks.  role 0 = A (rows): [hi, hi, lo]; role 1 = B: [hi, lo, hi].
+__global__ void hd_pack_kernel(const double* x, int64_t n, int64_t npad, int d,
+                               const double* center, int role, uint8_t* pack, float* sq,
+                               float* xf) {
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g >= npad * 8) return;
+  const int64_t i = g >> 3;
+  const int q = static_cast<int>(g & 7);
+  __half hi[8], lo[8];
+  float part = 0.f;
+  for (int e = 0; e < 8; ++e) {
+    const int k = q * 8 + e;
+    float v = 0.f;
+    if (i < n && k < d) v = static_cast<float>(x[i * d + k] - center[k]);
+    if (xf) xf[i * kHdK + k] = v;  // padded rows/dims are zero
+    part = fmaf(v, v, part);
+    const float vs = v * kHdScale;
+    hi[e] = __float2half_rn(vs);
+    lo[e] = __float2half_rn(vs - __half2float(hi[e]));
+  }
+  // |x|^2 from the float coordinates: reduce the 8 chunk partials (lanes 8i..8i+7)
+  for (int o = 4; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  if (q == 0 && i < n && sq) sq[i] = part;
+  const int64_t blk = i / kHdBlockRows;
+  const int r = static_cast<int>(i % kHdBlockRows);
+  const int off = r * 128 + ((q ^ (r & 7)) * 16);
+  uint8_t* base = pack + blk * kHdPackBytes;
+  const __half* src[3] = {hi, role == 0 ? hi : lo, role == 0 ? lo : hi};
+  for (int c = 0; c < kHdChunks; ++c)
+    *reinterpret_cast<uint4*>(base + c * kHdBlockBytes + off) = *reinterpret_cast<const uint4*>(src[c]);
+}
+
+// Rows are padded to whole 256-row tiles (two A blocks per CTA), columns to
+// whole 128-column blocks.
+int64_t hd_padded(int64_t n) { return (n + kTileRows - 1) / kTileRows * kTileRows; }
+
+cudaError_t hd_pack(const double* x, int64_t n, int d, const double* center, int role,
+                    uint8_t* pack, float* sq, float* xf, cudaStream_t st) {
+  const int64_t npad = hd_padded(n);
+  const int64_t threads = npad * 8;
+  ++g_launches;
+  hd_pack_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st>>>(
+      x, n, npad, d, center, role, pack, sq, xf);
+  return cudaGetLastError();
+}
+
+size_t hd_pack_bytes(int64_t n) {
+  return static_cast<size_t>(hd_padded(n) / kHdBlockRows) * kHdPackBytes;
+}
+
+// ----------------------------------------------------------- PTX helpers --
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+// K-major, SWIZZLE_128B UMMA shared-memory descriptor (SM100 version 1):
+// start >> 4, LBO = 1 (unused for swizzled K-major), SBO = 1024 B >> 4.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t addr) {
+  return static_cast<uint64_t>((addr >> 4) & 0x3FFFu) | (1ull << 16) | (64ull << 32) |
+         (1ull << 46) | (2ull << 61);
+}
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t addr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(r[k]);
+}
+
+// instruction descriptor: F16 x F16 -> F32, K-major A and B, M = 128, N = 128
+constexpr uint32_t kHdIdesc = (1u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+
+// ---------------------------------------------------------------- kernel --
+__global__ void __launch_bounds__(kHdThreads, 1)
+softmin_hd_kernel(const __grid_constant__ Group G) {
+  extern __shared__ __align__(1024) uint8_t hd_smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(hd_smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;                                   // 2 halves x 48 KB
+  uint8_t* sB = smem + 2 * kHdPackBytes;                // 2 stages x 48 KB
+  float* cval = reinterpret_cast<float*>(sB + kHdStages * kHdPackBytes);  // [2][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(cval + 2 * 128);
+  // bars: 0 fullA, 1-2 fullB, 3-4 emptyB, 5-6 tmemFull, 7-8 tmemEmpty
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+
+  const int it = blockIdx.x;
+  if (it >= G.n_items) return;
+  const int4 item = G.items[it];
+  const Problem& P = G.P[item.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row_base = P.tile_start[item.y];
+  // column blocks owned by this item: those whose first column is in [z, w)
+  const int blk0 = (item.z + kHdBlockRows - 1) / kHdBlockRows;
+  const int blk1 = (item.w + kHdBlockRows - 1) / kHdBlockRows;
+  const int nblk = blk1 - blk0;
+
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(&bars[0]), 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(smem_u32(&bars[1 + s]), 1);
+      mbar_init(smem_u32(&bars[3 + s]), 1);
+      mbar_init(smem_u32(&bars[5 + s]), 1);
+      mbar_init(smem_u32(&bars[7 + s]), 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    // (whole warp walks the loop so it stays converged; lane 0 issues)
+    if (nblk > 0) {
+      const uint32_t fa = smem_u32(&bars[0]);
+      if (lane == 0) {
+        mbar_expect_tx(fa, 2 * kHdPackBytes);
+        const uint8_t* a0 = P.a_pack + static_cast<int64_t>(row_base / kHdBlockRows) * kHdPackBytes;
+        bulk_g2s(smem_u32(sA), a0, kHdPackBytes, fa);
+        bulk_g2s(smem_u32(sA + kHdPackBytes), a0 + kHdPackBytes, kHdPackBytes, fa);
+      }
+      for (int t = 0; t < nblk; ++t) {
+        const int s = t & 1, n = t >> 1;
+        if (n > 0) mbar_wait(smem_u32(&bars[3 + s]), (n - 1) & 1);
+        if (lane == 0) {
+          const uint32_t fb = smem_u32(&bars[1 + s]);
+          mbar_expect_tx(fb, kHdPackBytes);
+          bulk_g2s(smem_u32(sB + s * kHdPackBytes),
+                   P.b_pack + static_cast<int64_t>(blk0 + t) * kHdPackBytes, kHdPackBytes, fb);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1) {
+    // --------------------------------------------------------- MMA issuer
+    if (nblk > 0) {
+      mbar_wait(smem_u32(&bars[0]), 0);
+      for (int t = 0; t < nblk; ++t) {
+        const int s = t & 1, n = t >> 1, buf = t & 1;
+        mbar_wait(smem_u32(&bars[1 + s]), n & 1);
+        if (n > 0) mbar_wait(smem_u32(&bars[7 + buf]), (n - 1) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t d = tmem + buf * 256 + h * 128;
+            for (int c = 0; c < kHdChunks; ++c)
+              for (int k = 0; k < kHdK / 16; ++k) {
+                const uint32_t ao = smem_u32(sA + h * kHdPackBytes + c * kHdBlockBytes) + k * 32;
+                const uint32_t bo = smem_u32(sB + s * kHdPackBytes + c * kHdBlockBytes) + k * 32;
+                umma_f16(d, umma_desc(ao), umma_desc(bo), kHdIdesc, (c | k) ? 1u : 0u);
+              }
+          }
+          umma_commit(smem_u32(&bars[3 + s]));    // smem stage free
+          umma_commit(smem_u32(&bars[5 + buf]));  // accumulator ready
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4) {
+    // ----------------------------------------------------------- epilogue
+    const int e = threadIdx.x - 128;          // 0..255
+    const int g = (warp - 4) >> 2;            // M half
+    const int q = warp & 3;                   // TMEM lane quarter
+    const int lr = g * 128 + q * 32 + lane;   // local row
+    const int row = row_base + lr;
+    const bool rvalid = row < P.tile_start[item.y + 1];
+    const float est = (P.row_est && rvalid) ? P.row_est[row] : 0.f;
+    const float xsq = rvalid ? P.row_sq[row] : 0.f;
+    const float r = est * P.inv_lam_eps_ln2 - 0.5f * xsq * P.inv_eps_ln2;
+    const float k2 = P.inv_eps_ln2 * (1.f / (kHdScale * kHdScale));
+    float s = 0.f, s2 = 0.f;
+    for (int t = 0; t < nblk; ++t) {
+      const int buf = t & 1, n = t >> 1;
+      if (e < 128) {
+        const int j = (blk0 + t) * kHdBlockRows + e;
+        float cj = __int_as_float(0xff800000);  // -inf: padding column
+        if (j < P.n_cols)
+          cj = P.col_lw2[j] + (P.col_h[j] - 0.5f * P.col_sq[j]) * P.inv_eps_ln2;
+        cval[buf * 128 + e] = cj;
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      mbar_wait(smem_u32(&bars[5 + buf]), n & 1);
+      tc_fence_after();
+      const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + buf * 256 + g * 128;
+      const float* cv = cval + buf * 128;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        float v[32];
+        tmem_ld32(base + c * 32, v);
+#pragma unroll
+        for (int k = 0; k < 32; k += 2) {
+          const float e0 = fmaf(k2, v[k], cv[c * 32 + k] + r);
+          const float e1 = fmaf(k2, v[k + 1], cv[c * 32 + k + 1] + r);
+          s += ex2_approx(e0);
+          s2 += ex2_approx(e1);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&bars[7 + buf]));
+    }
+    G.part[static_cast<int64_t>(it) * kTileRows + lr] = s + s2;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// Exact online-max LSE for rows the fixed-reference path rejected (float32,
+// CUDA cores), high-dimensional variant of softmin_fallback.
+__global__ void softmin_hd_fallback(const __grid_constant__ Group G, int d) {
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int cnt = min(*G.fb_count, G.fb_cap);
+  for (int qq = warp; qq < cnt; qq += nwarps) {
+    const int4 pr = G.fb_list[qq];
+    const Problem& P = G.P[pr.x];
+    const int r = pr.y;
+    const float* xr = P.row_f + static_cast<int64_t>(r) * kHdK;
+    float m = -INFINITY, s = 0.f;
+    for (int j = lane; j < P.n_cols; j += 32) {
+      const float* yr = P.col_f + static_cast<int64_t>(j) * kHdK;
+      float c = 0.f;
+      for (int k = 0; k < d; ++k) {
+        const float t = xr[k] - yr[k];
+        c = fmaf(t, t, c);
+      }
+      const float z = P.col_lw2[j] + (P.col_h[j] - 0.5f * c) * P.inv_eps_ln2;
+      if (z > m) { s = s * exp2f(m - z) + 1.f; m = z; }
+      else s += exp2f(z - m);
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, off);
+      const float s2 = __shfl_xor_sync(0xffffffffu, s, off);
+      const float mm = fmaxf(m, m2);
+      s = (m == -INFINITY ? 0.f : s * exp2f(m - mm)) + (m2 == -INFINITY ? 0.f : s2 * exp2f(m2 - mm));
+      m = mm;
+    }
+    if (lane == 0) {
+      const float est = P.row_est ? P.row_est[r] : 0.f;
+      const float ft = -P.lam_eps * kLn2 * (m + log2f(s));
+      P.row_out[r] = (1.f - P.mixw) * est + P.mixw * ft;
+    }
+  }
+}
+
+__global__ void hd_weights_kernel(const double* w, int64_t n, float* lw2, double* w64) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  lw2[i] = __double2float_rn(log2(w[i]));
+  w64[i] = w[i];
+}
+
+cudaError_t hd_weights(const double* w, int64_t n, float* lw2, double* w64, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  ++g_launches;
+  hd_weights_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(w, n, lw2, w64);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_softmin_hd(const Group& g, int d, int n_sm, cudaStream_t st) {
+  (void)d;
+  if (g.n_items <= 0) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(softmin_hd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kHdSmem));
+    attr = true;
+  }
+  ++g_launches;
+  softmin_hd_kernel<<<g.n_items, kHdThreads, kHdSmem, st>>>(g);
+  (void)n_sm;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fallback_hd(const Group& g, int d, int n_sm, cudaStream_t st) {
+  ++g_launches;
+  softmin_hd_fallback<<<n_sm, 256, 0, st>>>(g, d);
+  return cudaGetLastError();
+}
+
+}  // namespace msot_dev

@@ -264,6 +264,15 @@ void mask_rangeset(msot_ctx* c, const std::string& tag, const int32_t* rl,
 }
 
 // ------------------------------------------------------------ launch plans
+struct HdOperands {  // high-dimensional path (softmin_hd.cu)
+  const uint8_t* a_pack = nullptr;
+  const uint8_t* b_pack = nullptr;
+  const float* row_sq = nullptr;
+  const float* col_sq = nullptr;
+  const float* row_f = nullptr;
+  const float* col_f = nullptr;
+};
+
 struct ProbSpec {
   const float4* rows;
   int64_t n_rows;
@@ -271,6 +280,7 @@ struct ProbSpec {
   const float* col_lw2;
   int64_t n_cols;
   const RangeSet* rs;
+  HdOperands hd{};
 };
 
 struct Plan {
@@ -382,6 +392,12 @@ void run_group(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& ss) {
     Q.cols = S.cols;
     Q.col_lw2 = S.col_lw2;
     Q.col_h = a.h[p];
+    Q.a_pack = S.hd.a_pack;
+    Q.b_pack = S.hd.b_pack;
+    Q.row_sq = S.hd.row_sq;
+    Q.col_sq = S.hd.col_sq;
+    Q.row_f = S.hd.row_f;
+    Q.col_f = S.hd.col_f;
     Q.tile_start = S.rs->tile_start;
     Q.tile_rptr = S.rs->rptr;
     Q.ranges = S.rs->ranges;
@@ -411,10 +427,11 @@ void run_group(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& ss) {
     c->ev_pair(&e0, &e1);
     CK(cudaEventRecord(e0, st));
   }
-  CK(launch_softmin(G, ss.d, st));
+  const bool hd = ss.d > 3;
+  CK(hd ? launch_softmin_hd(G, ss.d, c->n_sm, st) : launch_softmin(G, ss.d, st));
   if (c->profiling) CK(cudaEventRecord(e1, st));
   CK(launch_finalize(G, st));
-  CK(launch_fallback(G, ss.d, c->n_sm, st));
+  CK(hd ? launch_fallback_hd(G, ss.d, c->n_sm, st) : launch_fallback(G, ss.d, c->n_sm, st));
   ss.S->softmin_launches += 1;
   ss.S->pairs_evaluated += P.pairs_all;
   // all-gather of the updated potentials (NCCL over NVLink)
@@ -552,14 +569,16 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
   CK(cudaEventRecord(c->t0, st));
 
   // diameter_estimate -- exact min/max on the device
-  long long* lohi = c->buf<long long>("bbox", 6);
+  long long* lohi = c->buf<long long>("bbox", 2 * d);
   CK(bbox(d_x, n, d, lohi, true, st));
   CK(bbox(d_y, m, d, lohi, false, st));
-  long long lh[6];
-  CK(cudaMemcpyAsync(lh, lohi, 2 * d * sizeof(long long), cudaMemcpyDeviceToHost, st));
+  std::vector<long long> lh(2 * d);
+  CK(cudaMemcpyAsync(lh.data(), lohi, 2 * d * sizeof(long long), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
-  bbox_decode(lh, d, lo, hi);
+  std::vector<double> lov(std::max(d, 3), 0.0), hiv(std::max(d, 3), 0.0);
+  double* lo = lov.data();
+  double* hi = hiv.data();
+  bbox_decode(lh.data(), d, lo, hi);
   double diag2 = 0.0;
   for (int k = 0; k < d; ++k) diag2 += (hi[k] - lo[k]) * (hi[k] - lo[k]);
   const double diam = std::max(std::sqrt(diag2), prm->blur);
@@ -571,26 +590,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
   msot_schedule(diam, prm, sig.data(), eps.data(), lam.data(), ns);
   S->n_scales = ns;
 
-  GridSpec g{};
-  g.d = d;
-  for (int k = 0; k < d; ++k) {
-    g.origin[k] = lo[k];
-    g.center[k] = 0.5 * (lo[k] + hi[k]);
-  }
-  double cell = prm->cluster_scale > 0 ? prm->cluster_scale : msot_auto_cell(lo, hi, d, n, m);
   const bool ms = prm->multiscale != 0;
-  if (ms && prm->cluster_scale <= 0) {  // policy.h: refine on occupied voxels
-    for (int it = 0; it < MSOT_AUTO_REFINE; ++it) {
-      g.cell = cell;
-      const int64_t kk = std::max(count_cells(c, d_x, n, g), count_cells(c, d_y, m, g));
-      cell = msot_refine_cell(cell, kk, n, m, d, lo, hi);
-    }
-  }
-  g.cell = cell;
-  DMeasure X, Y;
-  prepare_measure(c, "x", d_x, d_a, n, d, g, ms, X);
-  prepare_measure(c, "y", d_y, d_b, m, d, g, ms, Y);
-
   SolveState ss{S, d, c->buf<int32_t>("fb.count", 1), c->buf<int32_t>("fb.total", 1), nullptr, 0};
   ss.fb_cap = static_cast<int32_t>(std::min<int64_t>(2 * (n + m), 1 << 22));
   ss.fb_list = c->buf<int4>("fb.list", ss.fb_cap);
@@ -600,8 +600,76 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
   alloc_pots(c, "pot", n, m, U);
   int cur = 0;
   const double full = double(n) * n + double(m) * m + 2.0 * double(n) * m;
-
   RangeSet fxx, fyy, fxy, fyx;  // ranges of the last update (the plan reuses them)
+  DMeasure X, Y;
+
+  if (d > 3) {
+    // ---- high feature dimension (config 4): dense eps-scaling, <x,y> on
+    // the tensor cores (softmin_hd.cu); the voxel grid needs D <= 3
+    if (ms) raise(MSOT_EUSAGE, "voxel-grid multiscale needs D <= 3 (K-means coarsening is next)");
+    if (d > 64) raise(MSOT_EUSAGE, "the high-dimensional softmin supports D <= 64");
+    if (d_grad) raise(MSOT_EUSAGE, "grad_positions is implemented for D <= 3");
+    std::vector<double> center(d);
+    for (int k = 0; k < d; ++k) center[k] = 0.5 * (lo[k] + hi[k]);
+    double* dcen = c->buf<double>("hd.center", d);
+    CK(cudaMemcpyAsync(dcen, center.data(), d * sizeof(double), cudaMemcpyHostToDevice, st));
+    uint8_t* ax = c->buf<uint8_t>("hd.ax", hd_pack_bytes(n));
+    uint8_t* bx = c->buf<uint8_t>("hd.bx", hd_pack_bytes(n));
+    uint8_t* ay = c->buf<uint8_t>("hd.ay", hd_pack_bytes(m));
+    uint8_t* by = c->buf<uint8_t>("hd.by", hd_pack_bytes(m));
+    float* sqx = c->buf<float>("hd.sqx", n);
+    float* sqy = c->buf<float>("hd.sqy", m);
+    float* fx = c->buf<float>("hd.fx", hd_padded(n) * 64);
+    float* fy = c->buf<float>("hd.fy", hd_padded(m) * 64);
+    CK(hd_pack(d_x, n, d, dcen, 0, ax, sqx, fx, st));
+    CK(hd_pack(d_x, n, d, dcen, 1, bx, nullptr, nullptr, st));
+    CK(hd_pack(d_y, m, d, dcen, 0, ay, sqy, fy, st));
+    CK(hd_pack(d_y, m, d, dcen, 1, by, nullptr, nullptr, st));
+    X.n = n;
+    Y.n = m;
+    X.lw2 = c->buf<float>("x.lw2", n);
+    X.w64 = c->buf<double>("x.w64", n);
+    Y.lw2 = c->buf<float>("y.lw2", m);
+    Y.w64 = c->buf<double>("y.w64", m);
+    CK(hd_weights(d_a, n, X.lw2, X.w64, st));
+    CK(hd_weights(d_b, m, Y.lw2, Y.w64, st));
+    c->mark(4);
+    S->t_switch = 0;
+    dense_rangeset(c, "d.xx", n, n, fxx);
+    dense_rangeset(c, "d.yy", m, m, fyy);
+    dense_rangeset(c, "d.xy", m, n, fxy);
+    dense_rangeset(c, "d.yx", n, m, fyx);
+    Plan P;
+    P.np = 4;
+    P.ps[0] = {nullptr, n, nullptr, X.lw2, n, &fxx, {ax, bx, sqx, sqx, fx, fx}};  // a_xx
+    P.ps[1] = {nullptr, m, nullptr, Y.lw2, m, &fyy, {ay, by, sqy, sqy, fy, fy}};  // b_yy
+    P.ps[2] = {nullptr, m, nullptr, X.lw2, n, &fxy, {ay, bx, sqy, sqx, fy, fx}};  // a_xy
+    P.ps[3] = {nullptr, n, nullptr, Y.lw2, m, &fyx, {ax, by, sqx, sqy, fx, fy}};  // b_yx
+    build_plan(c, "ph", P);
+    for (int t = 0; t <= ns; ++t) {
+      const int tt = std::min(t, ns - 1);
+      sym_step(c, P, U, cur, eps[tt], lam[tt], t == ns, ss);
+      S->pairs_dense += full;
+    }
+  } else {
+  GridSpec g{};
+  g.d = d;
+  for (int k = 0; k < d; ++k) {
+    g.origin[k] = lo[k];
+    g.center[k] = 0.5 * (lo[k] + hi[k]);
+  }
+  double cell = prm->cluster_scale > 0 ? prm->cluster_scale : msot_auto_cell(lo, hi, d, n, m);
+  if (ms && prm->cluster_scale <= 0) {  // policy.h: refine on occupied voxels
+    for (int it = 0; it < MSOT_AUTO_REFINE; ++it) {
+      g.cell = cell;
+      const int64_t kk = std::max(count_cells(c, d_x, n, g), count_cells(c, d_y, m, g));
+      cell = msot_refine_cell(cell, kk, n, m, d, lo, hi);
+    }
+  }
+  g.cell = cell;
+  prepare_measure(c, "x", d_x, d_a, n, d, g, ms, X);
+  prepare_measure(c, "y", d_y, d_b, m, d, g, ms, Y);
+
   if (!ms) {
     c->mark(4);  // phase 4: symmetric updates
     S->t_switch = 0;
@@ -754,6 +822,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
       S->pairs_fine_dense += full;
     }
   }
+  }  // d <= 3
 
   // grad_positions from the final potentials, on the pair
   // sets of the last update: cross plan (rows x, cols y) and self plan

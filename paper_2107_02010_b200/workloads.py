@@ -104,3 +104,25 @@ def fibres(n, seed, bundles=50, points=24):
         cp = ctrl[lab[i]] + rng.normal(0, 0.02, (4, 3))
         out.append(bern @ cp)
     return out, lab
+
+
+def encode_fibers(polylines, P=20):
+    """Arc-length resampling to P points, flattened to 3P coordinates scaled
+    by 1/sqrt(P), uniform weights 1/N."""
+    out = np.empty((len(polylines), 3 * P))
+    for i, line in enumerate(polylines):
+        line = np.asarray(line, np.float64)
+        seg = np.sqrt(((line[1:] - line[:-1]) ** 2).sum(1))
+        arc = np.concatenate([[0.0], np.cumsum(seg)])
+        if not arc[-1] > 0:
+            raise ValueError(f"fiber {i} is degenerate")
+        t = np.linspace(0.0, arc[-1], P)
+        out[i] = np.stack([np.interp(t, arc, line[:, k]) for k in range(3)], 1).reshape(-1)
+    return out / np.sqrt(P), np.full(len(polylines), 1.0 / len(polylines))
+
+
+def flip_augment(x, w, P=20):
+    """Append every fibre's point-order reversal, halving all weights
+    (SPEC.md:76-84); atoms [0, N) originals, [N, 2N) flips."""
+    flipped = x.reshape(len(x), P, 3)[:, ::-1, :].reshape(len(x), 3 * P)
+    return np.concatenate([x, flipped]), np.concatenate([w, w]) / 2.0

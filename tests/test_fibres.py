@@ -1,0 +1,59 @@
+"""Config-4 path (D = 60 fibre features, unbalanced): the tcgen05 split-f16
+softmin (softmin_hd.cu) against the FP64 oracle, on encoded, flip-augmented
+synthetic fibres."""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2107_02010_b200 import workloads as W
+from paper_2107_02010_b200.abi import make_params
+
+
+def fibre_measures(n, m, seed):
+    fa, _ = W.fibres(n, seed)
+    fb, _ = W.fibres(m, seed + 1)
+    x, a = W.encode_fibers(fa)
+    y, b = W.encode_fibers(fb)
+    return x, a, y, b
+
+
+def test_encode_and_flip():
+    line = np.array([[0.0, 0, 0], [1.0, 0, 0]])
+    x, w = W.encode_fibers([line], P=3)
+    np.testing.assert_allclose(x[0].reshape(3, 3)[:, 0], np.array([0, 0.5, 1]) / math.sqrt(3))
+    xf, wf = W.flip_augment(x, w, P=3)
+    np.testing.assert_allclose(xf[1].reshape(3, 3)[:, 0], np.array([1, 0.5, 0]) / math.sqrt(3))
+    assert wf.sum() == 1.0 and len(xf) == 2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("reach", [math.inf, 0.3])
+def test_hd_sinkhorn_matches_oracle(ctx, oracle, reach):
+    x, a, y, b = fibre_measures(700, 600, 7)
+    x, a = W.flip_augment(x, a)
+    y, b = W.flip_augment(y, b)
+    prm = make_params(blur=0.03, reach=reach)
+    lg, pg, sg = ctx.sinkhorn(prm, x, a, y, b)
+    lo, po, so = oracle.sinkhorn(prm, x, a, y, b)
+    assert sg["n_scales"] == so["n_scales"]
+    eps = 0.03 ** 2
+    for name in ("a_xx", "b_yy", "a_xy", "b_yx"):
+        err = np.abs(getattr(pg, name) - po[name]).max()
+        assert err <= 1e-3 * eps, f"{name}: {err / eps:.3e} eps"
+    assert abs(lg - lo) <= 1e-4 * abs(lo), (lg, lo)
+
+
+@pytest.mark.gpu
+def test_hd_softmin_kernel_dims(ctx, oracle):
+    """Odd dimensions and sizes that are not multiples of the 128/256 tiles."""
+    rng = np.random.default_rng(3)
+    for d, n, m in ((4, 300, 257), (17, 513, 129), (64, 260, 1000)):
+        x = rng.random((n, d)) * 0.3
+        y = rng.random((m, d)) * 0.3
+        prm = make_params(blur=0.05)
+        lg, pg, _ = ctx.sinkhorn(prm, x, np.full(n, 1 / n), y, np.full(m, 1 / m))
+        lo, po, _ = oracle.sinkhorn(prm, x, np.full(n, 1 / n), y, np.full(m, 1 / m))
+        for name in ("a_xx", "b_yy", "a_xy", "b_yx"):
+            assert np.abs(getattr(pg, name) - po[name]).max() <= 1e-3 * 0.05 ** 2, (d, name)
+        assert abs(lg - lo) <= 1e-4 * abs(lo)

@@ -557,7 +557,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
                   double* loss_out, msot_stats* S, double* h_pots[4], double* d_grad = nullptr) {
   if (n < 1 || m < 1) raise(MSOT_EDATA, "empty measure");
   if (n > 0x7fffff00LL || m > 0x7fffff00LL) raise(MSOT_EDATA, "measure too large");
-  if (d < 1 || d > 3) raise(MSOT_EUSAGE, "the GPU softmin supports D in 1..3");
+  if (d < 1 || d > 64) raise(MSOT_EUSAGE, "the GPU solver supports D in 1..64");
   if (!(prm->blur > 0) || !(prm->scaling > 0 && prm->scaling < 1))
     raise(MSOT_EUSAGE, "invalid blur/scaling");
   if (prm->p != 2.0) raise(MSOT_EUSAGE, "the GPU path implements p = 2");

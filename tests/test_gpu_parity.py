@@ -266,4 +266,7 @@ def test_errors(ctx):
     with pytest.raises(UsageError):
         ctx.sinkhorn(make_params(scaling=1.5), x, np.ones(3), x, np.ones(3))
     with pytest.raises(UsageError):
-        ctx.sinkhorn(make_params(), np.zeros((3, 5)), np.ones(3), np.zeros((3, 5)), np.ones(3))
+        ctx.sinkhorn(make_params(), np.zeros((3, 65)), np.ones(3), np.zeros((3, 65)), np.ones(3))
+    with pytest.raises(UsageError):  # voxel grid needs D <= 3
+        ctx.sinkhorn(make_params(multiscale=True), np.zeros((3, 5)), np.ones(3),
+                     np.zeros((3, 5)), np.ones(3))

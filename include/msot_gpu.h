@@ -84,7 +84,8 @@ typedef struct msot_stats {
   int32_t rank, world;
   /* device time per phase when profiling (ms): 0 setup (bounding box,
    * clustering), 1 coarse phase, 2 extrapolation, 3 masks/ranges/work
-   * items, 4 symmetric updates at full resolution, 5 loss and outputs */
+   * items, 4 symmetric updates at full resolution, 5 loss and outputs,
+   * 6 label transfer */
   double  phase_ms[8];
 } msot_stats;
 
@@ -120,6 +121,22 @@ int msot_schedule(double diameter, const msot_params* p, double* sigma, double* 
 /* Contiguous, tile-aligned split of `n_tiles` row tiles with per-tile cost
  * `work` into `world` shards: writes world+1 tile boundaries. */
 int msot_shard_tiles(const double* work, int64_t n_tiles, int world, int64_t* bounds);
+
+/* resolve_flips, host only: soft labels of a
+ * flip-augmented subject (n rows = 2 x originals, L classes) -> one row per
+ * original fibre.  flip_of[i] = original index of row i, orientation[i] = 0
+ * (original) / 1 (flipped); every original must appear once per orientation
+ * (MSOT_EDATA otherwise).  The orientation with the larger row mass is kept,
+ * ties to the original.  chosen[o] = the augmented row kept for original o. */
+int msot_resolve_flips(const double* scores, const double* row_mass, int64_t n, int n_classes,
+                       const int32_t* flip_of, const int32_t* orientation, double* scores_out,
+                       double* row_mass_out, int32_t* chosen);
+
+/* classify, host only: label[i] = -1 (OUTLIER) iff
+ * row_mass[i] < tau, else the argmax class (ties to the lowest index);
+ * confidence[i] = max score / row_mass (0 for outliers with zero mass). */
+int msot_classify(const double* scores, const double* row_mass, int64_t n, int n_classes,
+                  double tau, int32_t* label, double* confidence);
 
 /* --- device operations (host buffers) ----------------------------------- */
 
@@ -171,6 +188,19 @@ int msot_sinkhorn(msot_ctx* ctx, const msot_params* prm, const double* x, const 
 int msot_sinkhorn_grad(msot_ctx* ctx, const msot_params* prm, const double* x, const double* a,
                        int64_t n, const double* y, const double* b, int64_t m, int d,
                        double* loss_out, double* grad_x, msot_stats* stats);
+
+/* transfer_labels (eq. 7, config 4): solves the
+ * divergence of (alpha, beta) like msot_sinkhorn, then applies the implicit
+ * plan of the final cross potentials f = b_yx, g = a_xy to the one-hot atlas
+ * labels without materialising it:
+ *   scores[i][l] = sum_{j : labels[j] = l} b_j exp((f_i + g_j - C_ij)/eps),
+ *   row_mass[i]  = sum_l scores[i][l]
+ * (eps = blur^p).  labels: M class indices in [0, n_classes) (caller order
+ * of y); scores: N x n_classes row-major, caller order of x. */
+int msot_transfer_labels(msot_ctx* ctx, const msot_params* prm, const double* x, const double* a,
+                         int64_t n, const double* y, const double* b, int64_t m, int d,
+                         const int32_t* labels, int n_classes, double* scores, double* row_mass,
+                         double* loss_out, msot_stats* stats);
 
 /* Wasserstein barycenter of K target measures (PAPER.md
  * :374-386, config 5): descent on the positions of alpha (weights frozen),

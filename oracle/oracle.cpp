@@ -727,6 +727,32 @@ int oracle_sinkhorn_grad(const msot_params* prm, const double* x, const double* 
   return MSOT_OK;
 }
 
+// transfer_labels (eq. 7): the implicit plan
+// pi_ij / a_i = b_j exp((f_i + g_j - C_ij)/eps) applied to the one-hot
+// label columns, dense (the exact formula; a truncation mask only drops
+// terms below e^-theta).
+int oracle_transfer_labels(const double* x, int64_t n, const double* y, const double* b,
+                           int64_t m, int d, const double* f, const double* g, double eps,
+                           const int32_t* labels, int n_classes, double* scores,
+                           double* row_mass) {
+  if (n_classes < 1) return fail(MSOT_EUSAGE, "transfer_labels needs at least one class");
+  for (int64_t j = 0; j < m; ++j)
+    if (labels[j] < 0 || labels[j] >= n_classes)
+      return fail(MSOT_EDATA, "label outside [0, L)");
+  msot::parallel::for_ranges(static_cast<std::size_t>(n), [&](std::size_t lo, std::size_t hi) {
+    Vec acc(n_classes);
+    for (std::size_t i = lo; i < hi; ++i) {
+      std::fill(acc.begin(), acc.end(), 0.0);
+      const double* xi = x + i * d;
+      for (int64_t j = 0; j < m; ++j)
+        acc[labels[j]] += b[j] * std::exp((f[i] + g[j] - cost(xi, y + j * d, d, 2.0)) / eps);
+      for (int l = 0; l < n_classes; ++l) scores[i * n_classes + l] = acc[l];
+      row_mass[i] = msot::pairwise_sum(acc);
+    }
+  });
+  return MSOT_OK;
+}
+
 // Barycenter descent, same rules as msot_barycenter.
 int oracle_barycenter(const msot_params* prm, const double* x0, const double* a, int64_t n, int k,
                       const double* const* ys, const double* const* bs, const int64_t* ms, int d,

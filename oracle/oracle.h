@@ -78,6 +78,15 @@ int oracle_barycenter(const msot_params* prm, const double* x0, const double* a,
                       int iters, double step, double tol, double* x_out, double* loss_traj,
                       int* steps_done);
 
+/* transfer_labels (eq. 7), dense, given duals f
+ * (on x, = b_yx) and g (on y, = a_xy):
+ *   scores[i][l] = sum_{j: labels_j = l} b_j exp((f_i + g_j - C_ij)/eps),
+ *   row_mass[i]  = sum_l scores[i][l]  (pairwise_sum order over l).  */
+int oracle_transfer_labels(const double* x, int64_t n, const double* y, const double* b,
+                           int64_t m, int d, const double* f, const double* g, double eps,
+                           const int32_t* labels, int n_classes, double* scores,
+                           double* row_mass);
+
 const char* oracle_last_error(void);
 
 #ifdef __cplusplus

@@ -203,6 +203,27 @@ def sinkhorn_grad(prm, x, a, y, b):
     return loss.value, g
 
 
+def transfer_labels(x, y, b, f, g, eps, labels, n_classes):
+    """Dense FP64 soft labels: returns (scores N x L, row_mass N)."""
+    L = lib()
+    L.oracle_transfer_labels.restype = C.c_int
+    L.oracle_transfer_labels.argtypes = [_dp, C.c_int64, _dp, _dp, C.c_int64, C.c_int, _dp, _dp,
+                                         C.c_double, _ip, C.c_int, _dp, _dp]
+    x, y, b, f, g = _c64(x), _c64(y), _c64(b), _c64(f), _c64(g)
+    if x.ndim == 1:
+        x = x[:, None]
+    if y.ndim == 1:
+        y = y[:, None]
+    n, d = x.shape
+    lab = np.ascontiguousarray(labels, dtype=np.int32)
+    sc = np.zeros((n, n_classes))
+    rm = np.zeros(n)
+    rc = L.oracle_transfer_labels(_d(x), n, _d(y), _d(b), y.shape[0], d, _d(f), _d(g), eps,
+                                  lab.ctypes.data_as(_ip), n_classes, _d(sc), _d(rm))
+    raise_status(rc, L.oracle_last_error().decode())
+    return sc, rm
+
+
 def barycenter(prm, x0, a, targets, iters=10, step=1.0, tol=1e-4):
     L = lib()
     _setup_grad(L)

@@ -63,7 +63,7 @@ class Stats(C.Structure):
         ("phase_ms", C.c_double * 8),
     ]
 
-    PHASES = ("setup", "coarse", "extrapolate", "masks", "updates", "loss")
+    PHASES = ("setup", "coarse", "extrapolate", "masks", "updates", "loss", "labels")
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_ if k != "phase_ms"}

@@ -81,63 +81,116 @@ struct MaskIn {
   }
 };
 
-__global__ void mask_bits_kernel(MaskIn m, double thr, int self, uint32_t* mask) {
-  const int32_t w = blockIdx.x * blockDim.x + threadIdx.x;
-  const int32_t I = blockIdx.y;
-  if (w >= m.words) return;
-  uint32_t bits = 0;
-  const int32_t J0 = w * 32;
-  const int32_t nb = min(32, m.ky - J0);
-  for (int b = 0; b < nb; ++b) {
-    const int32_t J = J0 + b;
-    if (self && I == J) {
-      bits |= 1u << b;
-      continue;
-    }
-    if (static_cast<double>(m.ub(I, J)) < thr) continue;
-    if (m.slack(I, J) >= thr) bits |= 1u << b;
-  }
-  mask[static_cast<int64_t>(I) * m.words + w] = bits;
+// Float32 upper bound of the float64 slack for row data already in registers
+// (same arithmetic as MaskIn::ub).
+__device__ __forceinline__ float ub_regs(float4 X, float rI, float F, float4 Y, float rJ, float G,
+                                         int d) {
+  const float dx = X.x - Y.x, dy = d > 1 ? X.y - Y.y : 0.f, dz = d > 2 ? X.z - Y.z : 0.f;
+  const float s = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+  const float rr = rI + rJ;
+  const float lb = fmaxf(sqrtf(s) - rr, 0.f);
+  const float v = (F + G) - 0.5f * lb * lb;
+  return v + 1e-5f * (1.f + fabsf(F) + fabsf(G) + 2.f * s + 2.f * rr * rr);
 }
 
-// best pair of each row (ties -> lowest J) or each column (ties -> lowest I)
-__global__ void best_kernel(MaskIn m, int by_col, uint32_t* mask) {
-  const int lane = threadIdx.x & 31;
-  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int32_t nw = by_col ? m.ky : m.kx, nl = by_col ? m.kx : m.ky;
-  if (w >= nw) return;
-  double best = -INFINITY;
-  int32_t arg = 0x7fffffff;
-  for (int32_t q = lane; q < nl; q += 32) {
-    const int32_t I = by_col ? q : static_cast<int32_t>(w);
-    const int32_t J = by_col ? static_cast<int32_t>(w) : q;
-    if (static_cast<double>(m.ub(I, J)) < best) continue;  // cannot beat (or tie) the best
-    const double v = m.slack(I, J);
-    if (v > best) { best = v; arg = q; }
+// One CTA per row cluster I: every word of row I (a warp computes 32
+// consecutive column clusters — coalesced column loads — and writes the word
+// with one ballot) and the row's best pair (max slack, ties -> lowest J).
+// The float64 slack is evaluated only where the float32 upper bound reaches
+// min(thr, best so far): for the bit, and for the arg-max.
+constexpr int kMaskThreads = 256;
+
+__global__ void __launch_bounds__(kMaskThreads)
+mask_rows_kernel(MaskIn m, double thr, int self, uint32_t* mask, int32_t* best) {
+  __shared__ double sv[kMaskThreads / 32];
+  __shared__ int32_t sj[kMaskThreads / 32];
+  const int32_t I = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  const bool g = m.gx != nullptr;
+  const float4 X = m.cx[I];
+  const float rI = m.rx[I], F = m.fx[I];
+  const float4 GI = g ? m.gx[I] : zero;
+  double bv = -INFINITY;
+  int32_t bj = 0x7fffffff;
+  for (int32_t w = warp; w < m.words; w += kMaskThreads / 32) {
+    const int32_t J = w * 32 + lane;
+    bool keep = false;
+    if (J < m.ky) {
+      const float4 Y = m.cy[J];
+      const float rJ = m.ry[J], G = m.gy[J];
+      const double u = static_cast<double>(ub_regs(X, rI, F, Y, rJ, G, m.d));
+      keep = self && I == J;  // diagonal of a self mask
+      if (u >= thr || u >= bv) {
+        const double v = pair_slack(X, rI, F, GI, Y, rJ, G, g ? m.hy[J] : zero, m.d, g);
+        keep = keep || v >= thr;
+        if (v > bv) { bv = v; bj = J; }  // J increases per thread: ties keep the lowest
+      }
+    }
+    const uint32_t bits = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) mask[static_cast<int64_t>(I) * m.words + w] = bits;
   }
   for (int o = 16; o > 0; o >>= 1) {
-    const double b2 = __shfl_xor_sync(0xffffffffu, best, o);
-    const int32_t a2 = __shfl_xor_sync(0xffffffffu, arg, o);
-    if (b2 > best || (b2 == best && a2 < arg)) { best = b2; arg = a2; }
+    const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int32_t j2 = __shfl_xor_sync(0xffffffffu, bj, o);
+    if (v2 > bv || (v2 == bv && j2 < bj)) { bv = v2; bj = j2; }
   }
-  if (lane == 0 && arg != 0x7fffffff) {
-    const int64_t I = by_col ? arg : w, J = by_col ? w : arg;
-    atomicOr(&mask[I * m.words + (J >> 5)], 1u << (J & 31));
+  if (lane == 0) { sv[warp] = bv; sj[warp] = bj; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < kMaskThreads / 32; ++q)
+      if (sv[q] > bv || (sv[q] == bv && sj[q] < bj)) { bv = sv[q]; bj = sj[q]; }
+    best[I] = bj == 0x7fffffff ? -1 : bj;
   }
 }
 
-cudaError_t truncation_mask(int32_t kx, int32_t ky, int d, const float4* cx, const float* rx,
-                            const float* fx, const float4* gx, const float4* cy, const float* ry,
-                            const float* gy, const float4* hy, double eps, double theta, int self,
-                            uint32_t* mask, cudaStream_t st) {
+// Best pairs into the masks: row I's best J (br) and column J's best I (bc)
+// set (I, J) in `mask` and (J, I) in `maskT` (nullable; == mask for a self
+// mask, whose best pairs are symmetric).
+__global__ void mask_best_kernel(const int32_t* br, int32_t kx, const int32_t* bc, int32_t ky,
+                                 uint32_t* mask, int32_t wx, uint32_t* maskT, int32_t wt) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  int32_t I, J;
+  if (t < kx) {
+    I = static_cast<int32_t>(t);
+    J = br[I];
+  } else if (t < static_cast<int64_t>(kx) + ky) {
+    J = static_cast<int32_t>(t - kx);
+    I = bc[J];
+  } else {
+    return;
+  }
+  if (I < 0 || J < 0) return;
+  atomicOr(&mask[static_cast<int64_t>(I) * wx + (J >> 5)], 1u << (J & 31));
+  if (maskT) atomicOr(&maskT[static_cast<int64_t>(J) * wt + (I >> 5)], 1u << (I & 31));
+}
+
+cudaError_t truncation_masks(int32_t kx, int32_t ky, int d, const float4* cx, const float* rx,
+                             const float* fx, const float4* gx, const float4* cy, const float* ry,
+                             const float* gy, const float4* hy, double eps, double theta, int self,
+                             uint32_t* mask, uint32_t* maskT, int32_t* best_r, int32_t* best_c,
+                             cudaStream_t st) {
   if (kx <= 0 || ky <= 0) return cudaSuccess;
   if ((gx == nullptr) != (hy == nullptr)) return cudaErrorInvalidValue;
-  MaskIn m{kx, ky, d, mask_words(ky), cx, cy, rx, ry, fx, gy, gx, hy};
+  if (self && kx != ky) return cudaErrorInvalidValue;
   const double thr = -(theta * eps);
-  dim3 grid((m.words + 127) / 128, kx);
-  ++g_launches; mask_bits_kernel<<<grid, 128, 0, st>>>(m, thr, self, mask);
-  ++g_launches; best_kernel<<<static_cast<unsigned>((static_cast<int64_t>(kx) * 32 + 255) / 256), 256, 0, st>>>(m, 0, mask);
-  ++g_launches; best_kernel<<<static_cast<unsigned>((static_cast<int64_t>(ky) * 32 + 255) / 256), 256, 0, st>>>(m, 1, mask);
+  const MaskIn m{kx, ky, d, mask_words(ky), cx, cy, rx, ry, fx, gy, gx, hy};
+  ++g_launches;
+  mask_rows_kernel<<<static_cast<unsigned>(kx), kMaskThreads, 0, st>>>(m, thr, self, mask, best_r);
+  if (self) {
+    ++g_launches;
+    mask_best_kernel<<<static_cast<unsigned>((kx + 255) / 256), 256, 0, st>>>(
+        best_r, kx, best_r, 0, mask, m.words, mask, m.words);
+    return cudaGetLastError();
+  }
+  // the transposed problem: same formula with the roles swapped (pair_slack
+  // is exactly symmetric), so maskT is the bitwise transpose of mask
+  const MaskIn t{ky, kx, d, mask_words(kx), cy, cx, ry, rx, gy, fx, hy, gx};
+  ++g_launches;
+  mask_rows_kernel<<<static_cast<unsigned>(ky), kMaskThreads, 0, st>>>(t, thr, 0, maskT, best_c);
+  ++g_launches;
+  mask_best_kernel<<<static_cast<unsigned>((static_cast<int64_t>(kx) + ky + 255) / 256), 256, 0, st>>>(
+      best_r, kx, best_c, ky, mask, m.words, maskT, t.words);
   return cudaGetLastError();
 }
 

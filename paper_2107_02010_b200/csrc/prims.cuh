@@ -39,6 +39,16 @@ cudaError_t hd_weights(const double* w, int64_t n, float* lw2, double* w64, cuda
 cudaError_t launch_softmin_hd(const Group& g, int d, int n_sm, cudaStream_t st);
 cudaError_t launch_fallback_hd(const Group& g, int d, int n_sm, cudaStream_t st);
 
+// label transfer (labels.cu, K9)
+cudaError_t gather_label_cols(const float4* pts, const float* lw2, const float* h,
+                              const int32_t* src, int64_t mpad, float4* cols, float* lw_out,
+                              float* h_out, cudaStream_t st);
+cudaError_t gather_rows_f64(const double* x, int d, const int32_t* src, int64_t mpad, double* out,
+                            cudaStream_t st);
+cudaError_t label_finalize(const float* part, const int32_t* lbase, const int32_t* tile_start,
+                           int64_t n_tiles, int n_classes, const int32_t* perm, double* scores,
+                           double* mass, cudaStream_t st);
+
 // positions gradient of S (loss.cu): rows of x, sorted order ->
 // grad[perm[s]] = a_s ((m_xy - m_xx) x_s - (u_xy - u_xx)) (float64, caller order;
 // frame-invariant, so the centred coordinates are used as they are)
@@ -80,10 +90,15 @@ cudaError_t inherit(const float* coarse, const int32_t* labels, int64_t n, float
 __host__ __device__ inline int32_t mask_words(int32_t ky) { return (ky + 31) / 32; }
 // bit-packed mask: Kx rows of mask_words(Ky) uint32 words
 // gx / hy (nullable): {slope G, F'} per cluster for the gradient bound
-cudaError_t truncation_mask(int32_t kx, int32_t ky, int d, const float4* cx, const float* rx,
-                            const float* fx, const float4* gx, const float4* cy, const float* ry,
-                            const float* gy, const float4* hy, double eps, double theta, int self,
-                            uint32_t* mask, cudaStream_t st);
+// Keep bits + best pairs of one truncation test.  self: kx == ky, one
+// symmetric mask (maskT, best_c unused).  Otherwise mask (kx rows over ky)
+// and maskT (ky rows over kx, its exact transpose), both with the row and
+// column best pairs; best_r (kx) / best_c (ky) are workspaces.
+cudaError_t truncation_masks(int32_t kx, int32_t ky, int d, const float4* cx, const float* rx,
+                             const float* fx, const float4* gx, const float4* cy, const float* ry,
+                             const float* gy, const float4* hy, double eps, double theta, int self,
+                             uint32_t* mask, uint32_t* maskT, int32_t* best_r, int32_t* best_c,
+                             cudaStream_t st);
 cudaError_t unpack_mask(const uint32_t* mask, int32_t kx, int32_t ky, uint8_t* out,
                         cudaStream_t st);
 // per tile: OR of its clusters' mask rows, then count / write column ranges

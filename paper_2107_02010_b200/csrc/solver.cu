@@ -552,9 +552,123 @@ void plan_group(msot_ctx* c, const std::string& tag, int np, const ProbSpec* spe
   CK(launch_plan(G, d, c->st));
 }
 
+// transfer_labels request (K9): atlas labels in the caller's order of y.
+struct LabelReq {
+  const int32_t* labels;  // host, M entries in [0, L)
+  int n_classes;
+  double* d_scores;       // device, N x L (caller row order)
+  double* d_mass;         // device, N
+};
+
+// K9 (labels.cu): scores[i][l] = sum_{label_j = l} pi_ij / a_i with
+// pi_ij / a_i = b_j exp((f_i + g_j - C_ij) / eps), f = b_yx, g = a_xy.  The
+// softmin kernel with est = f, h = g, lambda = 1 computes exactly these
+// terms; columns are put in label order (segments padded to the high-D
+// kernel's 128-column block) and work items are cut at segment boundaries.
+// Dense over the columns (the exact formula of eq. 7).
+void transfer_labels_dev(msot_ctx* c, const LabelReq& q, const DMeasure& X, const DMeasure& Y,
+                         int64_t n, int64_t m, int d, const double* d_y, const double* hd_cen,
+                         const uint8_t* hd_ax, const float* hd_sqx, const float* f_row,
+                         const float* g_col, double eps) {
+  cudaStream_t st = c->st;
+  const int L = q.n_classes;
+  const bool hd = d > 3;
+  const int64_t pad = hd ? 128 : 1;
+  // solver column index of each caller atom of y (3-D measures are sorted)
+  std::vector<int32_t> solver_of(m);
+  if (!hd) {
+    std::vector<int32_t> perm(m);
+    CK(cudaMemcpyAsync(perm.data(), Y.perm, m * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int64_t k = 0; k < m; ++k) solver_of[perm[k]] = static_cast<int32_t>(k);
+  } else {
+    for (int64_t j = 0; j < m; ++j) solver_of[j] = static_cast<int32_t>(j);
+  }
+  std::vector<int64_t> cnt(L, 0), seg(L + 1, 0);
+  for (int64_t j = 0; j < m; ++j) {
+    const int32_t l = q.labels[j];
+    if (l < 0 || l >= L) raise(MSOT_EDATA, "label outside [0, L)");
+    ++cnt[l];
+  }
+  for (int l = 0; l < L; ++l) seg[l + 1] = seg[l] + (cnt[l] + pad - 1) / pad * pad;
+  const int64_t mpad = std::max<int64_t>(seg[L], 1);
+  std::vector<int32_t> src(mpad, -1);
+  std::vector<int64_t> fill(seg.begin(), seg.end() - 1);
+  for (int64_t j = 0; j < m; ++j) src[fill[q.labels[j]]++] = hd ? static_cast<int32_t>(j) : solver_of[j];
+  int32_t* dsrc = c->buf<int32_t>("lab.src", mpad);
+  CK(cudaMemcpyAsync(dsrc, src.data(), mpad * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  float* lwL = c->buf<float>("lab.lw", mpad);
+  float* hL = c->buf<float>("lab.h", mpad);
+  float4* colsL = hd ? nullptr : c->buf<float4>("lab.cols", mpad);
+  CK(gather_label_cols(hd ? nullptr : Y.pts, Y.lw2, g_col, dsrc, mpad, colsL, lwL, hL, st));
+  uint8_t* bL = nullptr;
+  float* sqL = nullptr;
+  if (hd) {
+    double* yL = c->buf<double>("lab.y64", mpad * d);
+    CK(gather_rows_f64(d_y, d, dsrc, mpad, yL, st));
+    bL = c->buf<uint8_t>("lab.bpack", hd_pack_bytes(mpad));
+    sqL = c->buf<float>("lab.sq", hd_padded(mpad));
+    CK(hd_pack(yL, mpad, d, hd_cen, 1, bL, sqL, nullptr, st));
+  }
+  RangeSet R;
+  dense_rangeset(c, "lab.rows", n, mpad, R);
+  const int64_t T = R.n_tiles;
+  // work items: (tile, label segment) cut into chunks of whole column blocks
+  const int64_t target = static_cast<int64_t>(c->n_sm) * 24;
+  int64_t chunk = std::max<int64_t>(2 * kColTile, (T * mpad + target - 1) / target);
+  chunk = (chunk + kColTile - 1) / kColTile * kColTile;
+  std::vector<int4> items;
+  std::vector<int32_t> lbase(static_cast<size_t>(T) * L + 1);
+  for (int64_t t = 0; t < T; ++t)
+    for (int l = 0; l < L; ++l) {
+      lbase[t * L + l] = static_cast<int32_t>(items.size());
+      for (int64_t z = seg[l]; z < seg[l + 1]; z += chunk)
+        items.push_back(make_int4(0, static_cast<int>(t), static_cast<int>(z),
+                                  static_cast<int>(std::min(z + chunk, seg[l + 1]))));
+    }
+  lbase[T * L] = static_cast<int32_t>(items.size());
+  if (items.size() > 0x7fffffffULL) raise(MSOT_EUSAGE, "too many label work items");
+  int4* ditems = c->buf<int4>("lab.items", items.size());
+  int32_t* dlbase = c->buf<int32_t>("lab.lbase", lbase.size());
+  CK(cudaMemcpyAsync(ditems, items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dlbase, lbase.data(), lbase.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  const double ln2 = 0.69314718055994530942;
+  Group G{};
+  Problem& Q = G.P[0];
+  Q.rows = hd ? nullptr : X.pts;
+  Q.row_est = f_row;
+  Q.cols = colsL;
+  Q.col_lw2 = lwL;
+  Q.col_h = hL;
+  Q.tile_start = R.tile_start;
+  Q.tile_rptr = R.rptr;
+  Q.ranges = R.ranges;
+  Q.a_pack = hd_ax;
+  Q.b_pack = bL;
+  Q.row_sq = hd_sqx;
+  Q.col_sq = sqL;
+  Q.n_rows = static_cast<int32_t>(n);
+  Q.n_cols = static_cast<int32_t>(mpad);
+  Q.sc = static_cast<float>(1.0 / std::sqrt(2.0 * eps * ln2));
+  Q.inv_eps_ln2 = static_cast<float>(1.0 / (eps * ln2));
+  Q.inv_lam_eps_ln2 = Q.inv_eps_ln2;  // lambda = 1: exp((f + g - C) / eps)
+  Q.lam_eps = static_cast<float>(eps);
+  Q.mixw = 1.f;
+  G.n_problems = 1;
+  G.items = ditems;
+  G.n_items = static_cast<int32_t>(items.size());
+  G.part = c->buf<float>("lab.part", items.size() * kTileRows);
+  G.tile_prefix[1] = static_cast<int32_t>(T);
+  CK(hd ? launch_softmin_hd(G, d, c->n_sm, st) : launch_softmin(G, d, st));
+  CK(label_finalize(G.part, dlbase, R.tile_start, T, L, hd ? nullptr : X.perm, q.d_scores,
+                    q.d_mass, st));
+  CK(cudaStreamSynchronize(st));  // host vectors above go out of scope
+}
+
 void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const double* d_a,
                   int64_t n, const double* d_y, const double* d_b, int64_t m, int d,
-                  double* loss_out, msot_stats* S, double* h_pots[4], double* d_grad = nullptr) {
+                  double* loss_out, msot_stats* S, double* h_pots[4], double* d_grad = nullptr,
+                  const LabelReq* lreq = nullptr) {
   if (n < 1 || m < 1) raise(MSOT_EDATA, "empty measure");
   if (n > 0x7fffff00LL || m > 0x7fffff00LL) raise(MSOT_EDATA, "measure too large");
   if (d < 1 || d > 64) raise(MSOT_EUSAGE, "the GPU solver supports D in 1..64");
@@ -602,6 +716,9 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
   const double full = double(n) * n + double(m) * m + 2.0 * double(n) * m;
   RangeSet fxx, fyy, fxy, fyx;  // ranges of the last update (the plan reuses them)
   DMeasure X, Y;
+  double* hd_cen = nullptr;      // high-D operands kept for the label transfer
+  uint8_t* hd_ax = nullptr;
+  float* hd_sqx = nullptr;
 
   if (d > 3) {
     // ---- high feature dimension (config 4): dense eps-scaling, <x,y> on
@@ -625,6 +742,9 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
     CK(hd_pack(d_x, n, d, dcen, 1, bx, nullptr, nullptr, st));
     CK(hd_pack(d_y, m, d, dcen, 0, ay, sqy, fy, st));
     CK(hd_pack(d_y, m, d, dcen, 1, by, nullptr, nullptr, st));
+    hd_cen = dcen;
+    hd_ax = ax;
+    hd_sqx = sqx;
     X.n = n;
     Y.n = m;
     X.lw2 = c->buf<float>("x.lw2", n);
@@ -790,16 +910,16 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
       }
       float4* g[4];
       for (int q = 0; q < 4; ++q) g[q] = (info && prm->mask_rule == 0) ? grad[q] : nullptr;
-      CK(truncation_mask(X.k, X.k, d, X.cpts, X.radii, fmax[0], g[0], X.cpts, X.radii, fmax[0],
-                         g[0], e, theta, 1, mxx, st));
-      CK(truncation_mask(Y.k, Y.k, d, Y.cpts, Y.radii, fmax[1], g[1], Y.cpts, Y.radii, fmax[1],
-                         g[1], e, theta, 1, myy, st));
+      int32_t* bxr = c->buf<int32_t>("m.bx", std::max(X.k, Y.k));
+      int32_t* byr = c->buf<int32_t>("m.by", std::max(X.k, Y.k));
+      CK(truncation_masks(X.k, X.k, d, X.cpts, X.radii, fmax[0], g[0], X.cpts, X.radii, fmax[0],
+                          g[0], e, theta, 1, mxx, nullptr, bxr, nullptr, st));
+      CK(truncation_masks(Y.k, Y.k, d, Y.cpts, Y.radii, fmax[1], g[1], Y.cpts, Y.radii, fmax[1],
+                          g[1], e, theta, 1, myy, nullptr, byr, nullptr, st));
       // cross pair: (F, G) = (max b_yx, max a_xy); the slack is symmetric, so
-      // the yx mask computed with swapped roles is the exact transpose
-      CK(truncation_mask(X.k, Y.k, d, X.cpts, X.radii, fmax[3], g[3], Y.cpts, Y.radii, fmax[2],
-                         g[2], e, theta, 0, mxy, st));
-      CK(truncation_mask(Y.k, X.k, d, Y.cpts, Y.radii, fmax[2], g[2], X.cpts, X.radii, fmax[3],
-                         g[3], e, theta, 0, myx, st));
+      // the yx mask (rows y) is the exact transpose of the xy mask (rows x)
+      CK(truncation_masks(X.k, Y.k, d, X.cpts, X.radii, fmax[3], g[3], Y.cpts, Y.radii, fmax[2],
+                          g[2], e, theta, 0, mxy, myx, bxr, byr, st));
       mask_rangeset(c, "f.xx", X.labels, X.offsets_h, n, X.offsets, X.k, mxx, rxx);
       mask_rangeset(c, "f.yy", Y.labels, Y.offsets_h, m, Y.offsets, Y.k, myy, ryy);
       mask_rangeset(c, "f.yx", X.labels, X.offsets_h, n, Y.offsets, Y.k, mxy, ryx);  // rows x, cols y
@@ -836,6 +956,14 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
     float4* outp[2] = {c->buf<float4>("grad.pxy", n), c->buf<float4>("grad.pxx", n)};
     plan_group(c, "pg", 2, specs, fr, gc, pay, outp, eps[ns - 1], d);
     CK(grad_positions(X.pts, X.w64, outp[0], outp[1], X.perm, n, d, d_grad, st));
+  }
+
+  // transfer_labels (K9) from the final cross potentials
+  if (lreq) {
+    c->mark(6);
+    float** f = U.v[cur];
+    transfer_labels_dev(c, *lreq, X, Y, n, m, d, d_y, hd_cen, hd_ax, hd_sqx, f[3], f[2],
+                        eps[ns - 1]);
   }
 
   // divergence (eq. 5-6), fixed-order float64
@@ -1109,6 +1237,87 @@ int msot_sinkhorn_grad(msot_ctx* c, const msot_params* prm, const double* x, con
   });
 }
 
+int msot_resolve_flips(const double* scores, const double* row_mass, int64_t n, int n_classes,
+                       const int32_t* flip_of, const int32_t* orientation, double* scores_out,
+                       double* row_mass_out, int32_t* chosen) {
+  return guard([&] {
+    if (!scores || !row_mass || !flip_of || !orientation || !scores_out || !row_mass_out || !chosen)
+      raise(MSOT_EUSAGE, "null argument");
+    if (n < 0 || n % 2 != 0 || n_classes < 1) raise(MSOT_EDATA, "need an even number of rows");
+    const int64_t no = n / 2;
+    std::vector<int64_t> row(2 * no, -1);  // [original][orientation] -> augmented row
+    for (int64_t i = 0; i < n; ++i) {
+      const int64_t o = flip_of[i];
+      const int32_t r = orientation[i];
+      if (o < 0 || o >= no || (r != 0 && r != 1)) raise(MSOT_EDATA, "flip map out of range");
+      if (row[2 * o + r] >= 0) raise(MSOT_EDATA, "duplicate entry in the flip map");
+      row[2 * o + r] = i;
+    }
+    for (int64_t o = 0; o < no; ++o) {
+      if (row[2 * o] < 0 || row[2 * o + 1] < 0) raise(MSOT_EDATA, "missing flip pair");
+      const int64_t a = row[2 * o], b = row[2 * o + 1];
+      const int64_t k = row_mass[b] > row_mass[a] ? b : a;  // ties -> original
+      chosen[o] = static_cast<int32_t>(k);
+      row_mass_out[o] = row_mass[k];
+      std::memcpy(scores_out + o * n_classes, scores + k * n_classes, n_classes * sizeof(double));
+    }
+  });
+}
+
+int msot_classify(const double* scores, const double* row_mass, int64_t n, int n_classes,
+                  double tau, int32_t* label, double* confidence) {
+  return guard([&] {
+    if (!scores || !row_mass || !label || !confidence) raise(MSOT_EUSAGE, "null argument");
+    if (n_classes < 1) raise(MSOT_EUSAGE, "classify needs at least one class");
+    for (int64_t i = 0; i < n; ++i) {
+      const double* s = scores + i * n_classes;
+      int best = 0;
+      for (int l = 1; l < n_classes; ++l)
+        if (s[l] > s[best]) best = l;
+      const bool out = row_mass[i] < tau;
+      label[i] = out ? -1 : best;
+      confidence[i] = row_mass[i] > 0 ? s[best] / row_mass[i] : 0.0;
+    }
+  });
+}
+
+int msot_transfer_labels(msot_ctx* c, const msot_params* prm, const double* x, const double* a,
+                         int64_t n, const double* y, const double* b, int64_t m, int d,
+                         const int32_t* labels, int n_classes, double* scores, double* row_mass,
+                         double* loss_out, msot_stats* stats) {
+  return guard([&] {
+    if (!c || !prm || !x || !a || !y || !b || !labels || !scores || !row_mass || !loss_out)
+      raise(MSOT_EUSAGE, "null argument");
+    if (n < 1 || m < 1) raise(MSOT_EDATA, "empty measure");
+    if (n_classes < 1) raise(MSOT_EUSAGE, "transfer_labels needs at least one class");
+    for (int64_t j = 0; j < m; ++j)
+      if (labels[j] < 0 || labels[j] >= n_classes) raise(MSOT_EDATA, "label outside [0, L)");
+    check_weights(a, n);
+    check_weights(b, m);
+    CK(cudaSetDevice(c->device));
+    msot_stats local{};
+    msot_stats* S = stats ? stats : &local;
+    std::memset(S, 0, sizeof(*S));
+    S->rank = c->rank;
+    S->world = c->world;
+    double* dx = c->buf<double>("in.x", n * d);
+    double* da = c->buf<double>("in.a", n);
+    double* dy = c->buf<double>("in.y", m * d);
+    double* db = c->buf<double>("in.b", m);
+    CK(cudaMemcpyAsync(dx, x, n * d * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(da, a, n * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(dy, y, m * d * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(db, b, m * sizeof(double), cudaMemcpyHostToDevice, c->st));
+    LabelReq q{labels, n_classes, c->buf<double>("lab.scores", size_t(n) * n_classes),
+               c->buf<double>("lab.mass", n)};
+    solve_device(c, prm, dx, da, n, dy, db, m, d, loss_out, S, nullptr, nullptr, &q);
+    CK(cudaMemcpyAsync(scores, q.d_scores, size_t(n) * n_classes * sizeof(double),
+                       cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(row_mass, q.d_mass, n * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+  });
+}
+
 // Wasserstein barycenter by descent on the atom positions (SPEC.md:356-364,
 // PAPER.md:374-386): minimise (1/K) sum_k S(alpha, beta_k) over x with frozen
 // weights; field = mean_k grad_k / a_i; x <- x - step * field, the step
@@ -1362,6 +1571,9 @@ int msot_truncation_mask(msot_ctx* c, int64_t kx, int64_t ky, int d, const float
     float* dry = c->buf<float>("tm.ry", ky);
     float* dgy = c->buf<float>("tm.gy", ky);
     uint32_t* dbits = c->buf<uint32_t>("tm.bits", kx * mask_words(static_cast<int32_t>(ky)));
+    uint32_t* dbitsT = c->buf<uint32_t>("tm.bitsT", ky * mask_words(static_cast<int32_t>(kx)));
+    int32_t* dbr = c->buf<int32_t>("tm.br", kx);
+    int32_t* dbc = c->buf<int32_t>("tm.bc", ky);
     uint8_t* dm = c->buf<uint8_t>("tm.m", kx * ky);
     CK(cudaMemcpyAsync(dcx, hcx.data(), kx * sizeof(float4), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(dcy, hcy.data(), ky * sizeof(float4), cudaMemcpyHostToDevice, st));
@@ -1376,8 +1588,9 @@ int msot_truncation_mask(msot_ctx* c, int64_t kx, int64_t ky, int d, const float
       CK(cudaMemcpyAsync(dgx, gx, kx * sizeof(float4), cudaMemcpyHostToDevice, st));
       CK(cudaMemcpyAsync(dhy, hy, ky * sizeof(float4), cudaMemcpyHostToDevice, st));
     }
-    CK(truncation_mask(static_cast<int32_t>(kx), static_cast<int32_t>(ky), d, dcx, drx, dfx, dgx,
-                       dcy, dry, dgy, dhy, eps, theta, self, dbits, st));
+    if (self && kx != ky) raise(MSOT_EUSAGE, "a self mask is square");
+    CK(truncation_masks(static_cast<int32_t>(kx), static_cast<int32_t>(ky), d, dcx, drx, dfx, dgx,
+                        dcy, dry, dgy, dhy, eps, theta, self, dbits, dbitsT, dbr, dbc, st));
     CK(unpack_mask(dbits, static_cast<int32_t>(kx), static_cast<int32_t>(ky), dm, st));
     CK(cudaMemcpyAsync(mask_out, dm, kx * ky, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));

@@ -67,6 +67,12 @@ def lib():
         L.msot_sinkhorn_device.argtypes = [C.c_void_p, C.POINTER(Params), C.c_void_p,
                                            C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                            C.c_int64, C.c_int, _dp, C.POINTER(Stats)]
+        L.msot_transfer_labels.argtypes = [C.c_void_p, C.POINTER(Params), _dp, _dp, C.c_int64,
+                                           _dp, _dp, C.c_int64, C.c_int, _ip, C.c_int, _dp, _dp,
+                                           _dp, C.POINTER(Stats)]
+        L.msot_resolve_flips.argtypes = [_dp, _dp, C.c_int64, C.c_int, _ip, _ip, _dp, _dp,
+                                         _ip]
+        L.msot_classify.argtypes = [_dp, _dp, C.c_int64, C.c_int, C.c_double, _ip, _dp]
         _LIB = L
     return _LIB
 
@@ -76,7 +82,7 @@ EXPORTS = ["msot_last_error", "msot_params_default", "msot_create", "msot_nccl_u
            "msot_create_dist", "msot_destroy", "msot_set_profiling", "msot_schedule",
            "msot_shard_tiles", "msot_softmin", "msot_grid_cluster", "msot_truncation_mask",
            "msot_sinkhorn", "msot_sinkhorn_device", "msot_probe_ex2", "msot_sinkhorn_grad",
-           "msot_barycenter"]
+           "msot_barycenter", "msot_transfer_labels", "msot_resolve_flips", "msot_classify"]
 
 
 def _check(rc):
@@ -119,6 +125,49 @@ class DualPotentials:
     a_xy: np.ndarray
     b_yx: np.ndarray
     eps: float
+
+
+@dataclass
+class SoftLabels:
+    """scores (N x L, >= 0) and row_mass (N)."""
+    scores: np.ndarray
+    row_mass: np.ndarray
+
+
+OUTLIER = -1  # classify(): label of rows whose mass is below tau
+
+
+def resolve_flips(soft, flip_of, orientation):
+    """soft labels of a flip-augmented subject -> one row per
+    original fibre, keeping the orientation with the larger row mass (ties to
+    the original orientation).  flip_of[i] = original fibre of augmented row
+    i, orientation[i] = 0 (original) or 1 (flipped).  Returns (SoftLabels,
+    chosen augmented row per original)."""
+    sc = _c64(soft.scores)
+    rm = _c64(soft.row_mass)
+    n, L = sc.shape
+    fo = np.ascontiguousarray(flip_of, dtype=np.int32)
+    ori = np.ascontiguousarray(orientation, dtype=np.int32)
+    n_orig = n // 2
+    out_s = np.zeros((n_orig, L))
+    out_m = np.zeros(n_orig)
+    chosen = np.zeros(n_orig, np.int32)
+    _check(lib().msot_resolve_flips(_d(sc), _d(rm), n, L, fo.ctypes.data_as(_ip),
+                                    ori.ctypes.data_as(_ip), _d(out_s), _d(out_m),
+                                    chosen.ctypes.data_as(_ip)))
+    return SoftLabels(out_s, out_m), chosen
+
+
+def classify(soft, tau=0.5):
+    """SPEC.md:436-444: hard labels (OUTLIER = -1 where row_mass < tau;
+    argmax with ties to the lowest class) and confidence max/row_mass."""
+    sc = _c64(soft.scores)
+    rm = _c64(soft.row_mass)
+    n, L = sc.shape
+    lab = np.zeros(n, np.int32)
+    conf = np.zeros(n)
+    _check(lib().msot_classify(_d(sc), _d(rm), n, L, tau, lab.ctypes.data_as(_ip), _d(conf)))
+    return lab, conf
 
 
 class Context:
@@ -272,6 +321,27 @@ class Context:
                                      ms.ctypes.data_as(_lp), d, iters, step, tol, _d(x),
                                      _d(traj), C.byref(done), C.byref(st)))
         return x, traj[:done.value + 1].copy(), st.as_dict()
+
+    # -- transfer_labels (eq. 7)
+    def transfer_labels(self, prm, x, a, y, b, labels, n_classes=None):
+        """Solves S(alpha, beta) and transfers the atlas labels of y to x.
+        Returns (SoftLabels(scores N x L, row_mass N), loss, stats)."""
+        x, a, y, b = _c64(x), _c64(a), _c64(y), _c64(b)
+        if x.ndim == 1:
+            x = x[:, None]
+        if y.ndim == 1:
+            y = y[:, None]
+        n, d = x.shape
+        lab = np.ascontiguousarray(labels, dtype=np.int32)
+        L = int(lab.max()) + 1 if n_classes is None else int(n_classes)
+        scores = np.zeros((n, L))
+        mass = np.zeros(n)
+        loss = C.c_double()
+        st = Stats()
+        _check(lib().msot_transfer_labels(self._h, C.byref(prm), _d(x), _d(a), n, _d(y), _d(b),
+                                          y.shape[0], d, lab.ctypes.data_as(_ip), L,
+                                          _d(scores), _d(mass), C.byref(loss), C.byref(st)))
+        return SoftLabels(scores, mass), loss.value, st.as_dict()
 
     def sinkhorn_device(self, prm, x_ptr, a_ptr, n, y_ptr, b_ptr, m, d):
         """Inputs already resident in HBM (float64 device pointers)."""

@@ -91,11 +91,14 @@ def upsample(pts, w, factor, jitter, seed):
 
 
 # ------------------------------------------------------------------ C4 -----
-def fibres(n, seed, bundles=50, points=24):
+def fibres(n, seed, bundles=50, points=24, bundle_seed=None):
     """Smooth random cubic curves in [0,1]^3 grouped into `bundles` bundles:
-    returns (list of (points, 3) polylines, bundle label per fibre)."""
+    returns (list of (points, 3) polylines, bundle label per fibre).  The
+    bundle geometry comes from `bundle_seed` (default: `seed`), so an atlas
+    and a subject drawn with one bundle_seed share their bundles."""
     rng = np.random.default_rng(seed)
-    ctrl = rng.uniform(0.15, 0.85, (bundles, 4, 3))
+    ctrl = np.random.default_rng(seed if bundle_seed is None else bundle_seed).uniform(
+        0.15, 0.85, (bundles, 4, 3))
     lab = rng.integers(0, bundles, n)
     t = np.linspace(0, 1, points)[:, None]
     bern = np.concatenate([(1 - t) ** 3, 3 * t * (1 - t) ** 2, 3 * t ** 2 * (1 - t), t ** 3], 1)

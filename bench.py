@@ -269,7 +269,7 @@ def main():
                      "peak_source": "measured on this GPU by msot_probe_ex2 "
                                     "(ex2.approx.ftz.f32 issue rate, all SMs)",
                      "peak_nominal": nominal, "frac_of_nominal": achieved / nominal,
-                     "traffic": traffic, "kernel": "softmin_kernel<3>",
+                     "traffic": traffic, "kernel": "softmin_sym_kernel<3> (evaluate-once fine phase) + softmin_kernel<3> (coarse phase)",
                      "softmin_ms": pst["softmin_ms"], "softmin_launches": pst["softmin_launches"],
                      "share_of_step": pst["softmin_ms"] / max(pst["total_ms"], 1e-9)},
         "clocks": clk.summary(),

@@ -57,7 +57,11 @@ typedef struct msot_params {
                             0 = inheritance (default),
                             1 = extrapolation: one lambda-damped softmin of the
                                 fine atoms against the coarse measure (GeomLoss) */
-  int32_t pad_;
+  int32_t pair_eval;     /* fine phase: 1 = evaluate each kept pair once for its
+                            row and its column (default; PAPER.md:258-290's
+                            cross kernel is shared by a_xy / b_yx and the
+                            self kernels are symmetric), 0 = one row-wise
+                            problem per potential (4 per scale)              */
 } msot_params;
 
 /* Defaults of SPEC.md:128 (q=0.9), :306 (switch 2x radius), :308 (theta=20). */

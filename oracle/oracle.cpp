@@ -376,6 +376,63 @@ int64_t tile_ranges(const int32_t* rl, const int32_t* ro, int64_t kx, int64_t n,
   return out.tile_ptr[nt];
 }
 
+// Per-row ranges (every row its own "tile") from per-row interval lists.
+Ranges per_row(std::vector<std::vector<std::pair<int32_t, int32_t>>>& L) {
+  Ranges out;
+  const int64_t n = static_cast<int64_t>(L.size());
+  out.tile_start.resize(n + 1);
+  out.row_tile.resize(n);
+  out.tile_ptr.assign(n + 1, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    out.tile_start[i] = i;
+    out.row_tile[i] = static_cast<int32_t>(i);
+    std::sort(L[i].begin(), L[i].end());
+    for (const auto& r : L[i]) {
+      out.r.push_back(r.first);
+      out.r.push_back(r.second);
+    }
+    out.tile_ptr[i + 1] = static_cast<int64_t>(out.r.size() / 2);
+  }
+  out.tile_start[n] = n;
+  return out;
+}
+
+// The pair sets of the symmetric evaluation (csrc/softmin.cu):
+// every kept pair is evaluated once and feeds both its row and its column.
+// Self problem with tile ranges R (rows = cols): row i of tile t sums over
+//   its own tile's rows [ts, te)                     (diagonal block)
+//   R(t) clipped to columns >= te                    (upper part, row side)
+//   the rows of every tile t' < t with i in R(t')    (column side)
+// which is a symmetric relation containing the cluster mask.
+Ranges sym_self(const Ranges& R, int64_t n) {
+  std::vector<std::vector<std::pair<int32_t, int32_t>>> L(n);
+  const int64_t T = static_cast<int64_t>(R.tile_start.size()) - 1;
+  for (int64_t t = 0; t < T; ++t) {
+    const int32_t ts = static_cast<int32_t>(R.tile_start[t]), te = static_cast<int32_t>(R.tile_start[t + 1]);
+    for (int32_t i = ts; i < te; ++i) L[i].push_back({ts, te});
+    for (int64_t q = R.tile_ptr[t]; q < R.tile_ptr[t + 1]; ++q) {
+      const int32_t c0 = std::max(R.r[2 * q], te), c1 = R.r[2 * q + 1];
+      if (c0 >= c1) continue;
+      for (int32_t i = ts; i < te; ++i) L[i].push_back({c0, c1});
+      for (int32_t k = c0; k < c1; ++k) L[k].push_back({ts, te});
+    }
+  }
+  return per_row(L);
+}
+
+// Cross problem: tile ranges R of rows x over columns y; the y rows sum over
+// the transposed relation {i : j in R(tile(i))}.
+Ranges transpose_ranges(const Ranges& R, int64_t n_cols) {
+  std::vector<std::vector<std::pair<int32_t, int32_t>>> L(n_cols);
+  const int64_t T = static_cast<int64_t>(R.tile_start.size()) - 1;
+  for (int64_t t = 0; t < T; ++t) {
+    const int32_t ts = static_cast<int32_t>(R.tile_start[t]), te = static_cast<int32_t>(R.tile_start[t + 1]);
+    for (int64_t q = R.tile_ptr[t]; q < R.tile_ptr[t + 1]; ++q)
+      for (int32_t j = R.r[2 * q]; j < R.r[2 * q + 1]; ++j) L[j].push_back({ts, te});
+  }
+  return per_row(L);
+}
+
 double dot(const Vec& a, const Vec& b) { return msot::pairwise_dot(a, b); }
 
 // S_eps,rho from the four potentials: balanced limit or the
@@ -650,7 +707,14 @@ int oracle_sinkhorn(const msot_params* prm, const double* x, const double* a, in
       tile_ranges(cx.labels.data(), cx.offsets.data(), cx.k, n, cx.offsets.data(), cx.k, mxx.data(), rxx);
       tile_ranges(cy.labels.data(), cy.offsets.data(), cy.k, m, cy.offsets.data(), cy.k, myy.data(), ryy);
       tile_ranges(cx.labels.data(), cx.offsets.data(), cx.k, n, cy.offsets.data(), cy.k, mxy.data(), ryx);  // rows x, cols y
-      tile_ranges(cy.labels.data(), cy.offsets.data(), cy.k, m, cx.offsets.data(), cx.k, myx.data(), rxy);  // rows y, cols x
+      if (prm->pair_eval) {
+        // pair sets of the evaluate-once kernels (sym_self / transpose_ranges)
+        rxx = sym_self(rxx, n);
+        ryy = sym_self(ryy, m);
+        rxy = transpose_ranges(ryx, m);  // rows y, cols x
+      } else {
+        tile_ranges(cy.labels.data(), cy.offsets.data(), cy.k, m, cx.offsets.data(), cx.k, myx.data(), rxy);  // rows y, cols x
+      }
     };
     for (int t = tsw; t <= ns; ++t) {
       const int tt = std::min(t, ns - 1);

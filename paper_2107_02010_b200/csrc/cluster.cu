@@ -31,24 +31,28 @@ cudaError_t cube_keys(const double* x, int64_t n, GridSpec g, uint32_t* keys, in
 // Sorted, centred float32 atoms {x, y, z, 0}, log2 weights, float64 weights.
 __global__ void gather_points_kernel(const double* x, const double* w, int64_t n, int d,
                                      GridSpec g, const int32_t* perm, float4* pts, float* lw2,
-                                     double* w64) {
+                                     double* w64, int32_t* nonuniform) {
   const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (s >= n) return;
-  const int64_t i = perm ? perm[s] : s;
+  const bool in = s < n;
+  const int64_t i = in ? (perm ? perm[s] : s) : 0;
+  const double wi = w[i];
+  // weights not all equal (one atomic per warp)
+  const bool diff = in && wi != w[0];
+  if (nonuniform && __any_sync(0xffffffffu, diff) && (threadIdx.x & 31) == 0) atomicOr(nonuniform, 1);
+  if (!in) return;
   float c[3] = {0.f, 0.f, 0.f};
   for (int k = 0; k < d && k < 3; ++k) c[k] = __double2float_rn(x[i * d + k] - g.center[k]);
   pts[s] = make_float4(c[0], c[1], c[2], 0.f);
-  const double wi = w[i];
   lw2[s] = __double2float_rn(log2(wi));
   w64[s] = wi;
 }
 
 cudaError_t gather_points(const double* x, const double* w, int64_t n, int d, GridSpec g,
                           const int32_t* perm, float4* pts, float* lw2, double* w64,
-                          cudaStream_t st) {
+                          int32_t* nonuniform, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   ++g_launches; gather_points_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(x, w, n, d, g, perm,
-                                                                               pts, lw2, w64);
+                                                                               pts, lw2, w64, nonuniform);
   return cudaGetLastError();
 }
 

@@ -44,6 +44,13 @@ struct Problem {
   const float* col_sq;       // |y_j|^2
   const float* row_f;        // float32 coordinates, row-major x 64 (exact fallback)
   const float* col_f;
+  // evaluate-once (symmetric) groups (softmin_sym.cu)
+  const float* row_lw2;      // log2 row weights (column sums weight rows by alpha_i)
+  float* colpart;            // column partial of every (tile, position) slot
+  const int64_t* tile_slot;  // [n_tiles] first colpart slot of each tile
+  const float* row_add;      // column totals added to the row sums (self problems;
+                             // the whole sum of the transposed cross problem)
+  float ell;                 // (1/lambda - 1) / (eps ln2): row/column reference shift
   int32_t n_rows, n_cols;
   float sc;                // 1 / sqrt(2 eps ln2): scaled |dx|^2 = C / (eps ln2)
   float inv_eps_ln2;       // 1 / (eps ln 2)

@@ -325,6 +325,165 @@ cudaError_t dense_ranges(int64_t n_tiles, int32_t n_cols, int64_t* rptr, int2* r
   return cudaGetLastError();
 }
 
+// ---- evaluate-once pair sets (softmin_sym.cu) -----------------------------
+// Every kept pair is evaluated once and feeds its row sum and its column sum.
+// Tile t's column list:
+//   cross (rows x, cols y): the runs of the tile-OR clusters (as tile_runs);
+//   self: a head range [ts, co[I1 + 1]) — the diagonal block plus the rest of
+//         the tile's last cluster I1 — then the runs of the tile-OR clusters
+//         J > I1.  Columns below te only feed row sums; column k >= te(t) of
+//         the list gets tile t's rows as a column sum, which makes the pair
+//         set symmetric (oracle.cpp:sym_self).
+// posword[t][w] = position of word w's first cluster in tile t's list, so the
+// column-major pass can place every (tile, cluster) entry without a sort.
+
+// bits of tile t's word w that are list clusters: self keeps J > I1 only
+__device__ __forceinline__ uint32_t list_bits(uint32_t b, int32_t w, int32_t I1, bool self) {
+  if (!self) return b;
+  const int32_t k = I1 - w * 32;  // clear bits 0..k
+  if (k < 0) return b;
+  if (k >= 31) return 0u;
+  return b & (~0u << (k + 1));
+}
+
+template <bool kWrite>
+__global__ void sym_runs_kernel(const uint32_t* tbits, int32_t words, int64_t nt,
+                                const int32_t* co, const int32_t* ts, const int32_t* rl, int self,
+                                int64_t* n_ranges, int64_t* n_cols, int32_t* posword,
+                                const int64_t* rptr, int2* ranges) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (t >= nt) return;
+  const uint32_t* tb = tbits + t * words;
+  const int32_t I1 = self ? rl[ts[t + 1] - 1] : -1;
+  const int64_t hn = self ? 1 : 0;  // the head range
+  int64_t cols = self ? co[I1 + 1] - ts[t] : 0, ns = 0, ne = 0;
+  const int64_t base = kWrite ? rptr[t] : 0;
+  if (kWrite && self && lane == 0) ranges[base] = make_int2(ts[t], co[I1 + 1]);
+  uint32_t carry = 0;  // top bit of the previous word
+  for (int32_t w0 = 0; w0 < words; w0 += 32) {
+    const int32_t w = w0 + lane;
+    const uint32_t b = w < words ? list_bits(tb[w], w, I1, self) : 0u;
+    const uint32_t up = __shfl_up_sync(0xffffffffu, b, 1);
+    const uint32_t cin = lane == 0 ? carry : (up >> 31);
+    uint32_t dn = __shfl_down_sync(0xffffffffu, b, 1);
+    if (lane == 31) dn = (w0 + 32 < words) ? list_bits(tb[w0 + 32], w0 + 32, I1, self) : 0u;
+    const uint32_t starts = b & ~((b << 1) | cin);
+    const uint32_t ends = b & ~((b >> 1) | ((dn & 1u) << 31));
+    int64_t contrib = 0;  // columns of the runs: -co[start] + co[end + 1]
+    for (uint32_t q = starts; q; q &= q - 1) contrib -= co[w * 32 + __ffs(q) - 1];
+    for (uint32_t q = ends; q; q &= q - 1) contrib += co[w * 32 + __ffs(q)];
+    const int ps = __popc(starts), pe = __popc(ends);
+    int xs = ps, xe = pe;
+    int64_t xc = contrib;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int ys = __shfl_up_sync(0xffffffffu, xs, o);
+      const int ye = __shfl_up_sync(0xffffffffu, xe, o);
+      const int64_t yc = __shfl_up_sync(0xffffffffu, xc, o);
+      if (lane >= o) { xs += ys; xe += ye; xc += yc; }
+    }
+    if (!kWrite && w < words) {
+      // a run open across the word boundary counts up to the boundary
+      const int64_t open = (cin && (b & 1u)) ? co[w * 32] : 0;
+      posword[t * words + w] = static_cast<int32_t>(cols + xc - contrib + open);
+    }
+    if (kWrite) {
+      int64_t ks = hn + ns + xs - ps, ke = hn + ne + xe - pe;
+      for (uint32_t q = starts; q; q &= q - 1) ranges[base + ks++].x = co[w * 32 + __ffs(q) - 1];
+      for (uint32_t q = ends; q; q &= q - 1) ranges[base + ke++].y = co[w * 32 + __ffs(q)];
+    }
+    ns += __shfl_sync(0xffffffffu, xs, 31);
+    ne += __shfl_sync(0xffffffffu, xe, 31);
+    cols += __shfl_sync(0xffffffffu, xc, 31);
+    carry = __shfl_sync(0xffffffffu, b, 31) >> 31;
+  }
+  if (!kWrite && lane == 0) {
+    n_ranges[t] = hn + ns;
+    n_cols[t] = cols;
+  }
+}
+
+// Column-major pass over the (tile, cluster) entries: warp = one word of 32
+// column clusters x one chunk of tiles (ascending).  kFill = false counts the
+// entries of every (cluster, chunk); kFill writes, in tile order, the colpart
+// slot of the cluster's first column in each tile's list.  Self problems add
+// the head entry of the tile's last cluster I1 (slot of column co[I1]).
+template <bool kFill>
+__global__ void sym_entries_kernel(const uint32_t* tbits, int32_t words, int32_t k, int64_t nt,
+                                   const int32_t* co, const int32_t* ts, const int32_t* rl,
+                                   int self, const int32_t* posword, const int64_t* tslot,
+                                   int32_t* cnt, const int64_t* ebase, int64_t* eslot,
+                                   int32_t* etile) {
+  const int lane = threadIdx.x & 31;
+  const int32_t w = static_cast<int32_t>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+  const int ch = blockIdx.y;
+  if (w >= words) return;
+  const int32_t J = w * 32 + lane;
+  const int64_t t0 = nt * ch / kEntryChunks, t1 = nt * (ch + 1) / kEntryChunks;
+  const int64_t ncl = J < k ? co[J + 1] - co[J] : 0;
+  int64_t e = kFill ? ebase[static_cast<int64_t>(J < k ? J : 0) * kEntryChunks + ch] : 0;
+  int32_t c = 0;
+  for (int64_t t = t0; t < t1; ++t) {
+    const int32_t I1 = self ? rl[ts[t + 1] - 1] : -1;
+    const uint32_t b = list_bits(tbits[t * words + w], w, I1, self);
+    const bool head = self && J == I1;
+    const bool mine = J < k && (((b >> lane) & 1u) || head);
+    if (!__any_sync(0xffffffffu, mine)) continue;
+    if (!kFill) {
+      c += mine;
+      continue;
+    }
+    // position of cluster J in tile t's list: word base + list columns of
+    // the lower clusters of this word
+    int64_t pre = ((b >> lane) & 1u) ? ncl : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, pre, o);
+      if (lane >= o) pre += y;
+    }
+    if (mine) {
+      const int64_t posJ = head ? static_cast<int64_t>(co[J]) - ts[t]
+                                : posword[t * words + w] + pre - ncl;
+      eslot[e] = tslot[t] + posJ;
+      etile[e] = static_cast<int32_t>(t);
+      ++e;
+    }
+  }
+  if (!kFill && J < k) cnt[static_cast<int64_t>(J) * kEntryChunks + ch] = c;
+}
+
+cudaError_t sym_ranges(const uint32_t* tbits, int32_t k, int64_t nt, const int32_t* co,
+                       const int32_t* ts, const int32_t* rl, int self, int64_t* n_ranges,
+                       int64_t* n_cols, int32_t* posword, const int64_t* rptr, int2* ranges,
+                       bool write, cudaStream_t st) {
+  if (nt <= 0) return cudaSuccess;
+  const unsigned grid = static_cast<unsigned>((nt * 32 + 255) / 256);
+  ++g_launches;
+  if (write)
+    sym_runs_kernel<true><<<grid, 256, 0, st>>>(tbits, mask_words(k), nt, co, ts, rl, self,
+                                                 nullptr, nullptr, nullptr, rptr, ranges);
+  else
+    sym_runs_kernel<false><<<grid, 256, 0, st>>>(tbits, mask_words(k), nt, co, ts, rl, self,
+                                                  n_ranges, n_cols, posword, nullptr, nullptr);
+  return cudaGetLastError();
+}
+
+cudaError_t sym_entries(const uint32_t* tbits, int32_t k, int64_t nt, const int32_t* co,
+                        const int32_t* ts, const int32_t* rl, int self, const int32_t* posword,
+                        const int64_t* tslot, int32_t* cnt, const int64_t* ebase, int64_t* eslot,
+                        int32_t* etile, bool fill, cudaStream_t st) {
+  if (nt <= 0 || k <= 0) return cudaSuccess;
+  const int32_t words = mask_words(k);
+  dim3 grid(static_cast<unsigned>((static_cast<int64_t>(words) * 32 + 127) / 128), kEntryChunks);
+  ++g_launches;
+  if (fill)
+    sym_entries_kernel<true><<<grid, 128, 0, st>>>(tbits, words, k, nt, co, ts, rl, self, posword,
+                                                   tslot, nullptr, ebase, eslot, etile);
+  else
+    sym_entries_kernel<false><<<grid, 128, 0, st>>>(tbits, words, k, nt, co, ts, rl, self,
+                                                    posword, tslot, cnt, nullptr, nullptr, nullptr);
+  return cudaGetLastError();
+}
+
 // ---- work items ----------------------------------------------------------
 __global__ void item_counts_kernel(const int64_t* tc, int64_t nt, int64_t chunk, int32_t* cnt) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;

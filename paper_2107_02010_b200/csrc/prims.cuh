@@ -30,6 +30,37 @@ cudaError_t launch_finalize(const Group& g, cudaStream_t st);
 cudaError_t launch_fallback(const Group& g, int d, int n_sm, cudaStream_t st);
 cudaError_t launch_plan(const Group& g, int d, cudaStream_t st);  // plan_kernel + plan_finalize
 
+// evaluate-once block-sparse softmin (softmin_sym.cu) and its pair sets (mask.cu)
+constexpr int kEntryChunks = 32;  // tile chunks of the column-major entry pass
+struct ColSum {
+  const int32_t* labels;     // column -> cluster
+  const int32_t* co;         // cluster offsets of the columns
+  const int64_t* eptr;       // [K * kEntryChunks + 1]: entries of cluster J at [J*C, (J+1)*C)
+  const int64_t* eslot;
+  const int32_t* etile;
+  const int32_t* tile_start;
+  const float* colpart;
+  float* tot;
+  int32_t n_cols, self, t0, t1;
+};
+struct ColSumGroup {
+  ColSum c[3];
+  int n;
+};
+// uniform: every row weight equal and lambda = 1 (column sums need no row factor)
+cudaError_t launch_softmin_sym(const Group& g, int d, bool uniform, cudaStream_t st);
+cudaError_t launch_colsum(const ColSum* c, int n, cudaStream_t st);
+cudaError_t launch_colfinal(const Group& g, int p, cudaStream_t st);
+cudaError_t launch_fallback_dense(const Group& g, int d, int n_sm, cudaStream_t st);
+cudaError_t sym_ranges(const uint32_t* tbits, int32_t k, int64_t nt, const int32_t* co,
+                       const int32_t* ts, const int32_t* rl, int self, int64_t* n_ranges,
+                       int64_t* n_cols, int32_t* posword, const int64_t* rptr, int2* ranges,
+                       bool write, cudaStream_t st);
+cudaError_t sym_entries(const uint32_t* tbits, int32_t k, int64_t nt, const int32_t* co,
+                        const int32_t* ts, const int32_t* rl, int self, const int32_t* posword,
+                        const int64_t* tslot, int32_t* cnt, const int64_t* ebase, int64_t* eslot,
+                        int32_t* etile, bool fill, cudaStream_t st);
+
 // high-dimensional softmin (softmin_hd.cu): tcgen05 split-f16 <x,y>
 int64_t hd_padded(int64_t n);
 size_t hd_pack_bytes(int64_t n);
@@ -70,9 +101,10 @@ struct GridSpec {
 };
 cudaError_t cube_keys(const double* x, int64_t n, GridSpec g, uint32_t* keys, int32_t* iota,
                       cudaStream_t st);
+// nonuniform (nullable): set to 1 when the weights are not all equal
 cudaError_t gather_points(const double* x, const double* w, int64_t n, int d, GridSpec g,
                           const int32_t* perm, float4* pts, float* lw2, double* w64,
-                          cudaStream_t st);
+                          int32_t* nonuniform, cudaStream_t st);
 cudaError_t segment_flags(const uint32_t* sorted_keys, int64_t n, uint8_t* flags,
                           cudaStream_t st);
 cudaError_t segment_offsets(const int32_t* labels, const uint8_t* flags, int64_t n,

@@ -1,0 +1,340 @@
+// softmin_sym.cu — K4s: the evaluate-once block-sparse softmin.  Each kept
+// pair (i, j) is exponentiated once and feeds both potentials it belongs to:
+//
+//   row i    s_i = sum_j w_j 2^{E_ij}                       (the K4 row sum)
+//   column j t_j = sum_i a_i 2^{E'_ij},  E'_ij - E_ij = (lw2_i - ell (est_i - est_mid))
+//                                                     + (ell (h_j - est_mid) - lw2_j)
+//
+// with E_ij the row exponent of softmin.cu (reference est_i / lambda) and E'_ij
+// the exponent of pair (j, i) in the transposed problem (reference h_j /
+// lambda); ell = (1/lambda - 1) / (eps ln2) (0 for reach = inf).  The two
+// differ by a row factor and a column factor, so one MUFU.EX2 per pair serves
+// both updates (the cross pair a_xy / b_yx shares its
+// kernel matrix, and the self kernels are symmetric).  This halves the MUFU
+// work that bounds the solver.
+//
+// Per 16 columns a warp reduces its 32 x 2 rows with a 5-step transpose
+// butterfly (one shuffle per column per warp), the 4 warps combine through
+// shared memory in a fixed order, and thread c writes column c's CTA partial
+// to its (tile, position) slot.  Column totals are formed by
+// sym_colsum_kernel in tile order (deterministic for a fixed GPU count).
+#include "prims.cuh"
+#include "softmin_inner.cuh"
+
+namespace msot_dev {
+
+// Sum over the 32 lanes of 16 per-lane values.  Lane l returns the warp
+// total of value q(l) = 8 b4 + 4 b3 + 2 b2 + b1 (bits of l; l, l^1 agree).
+__device__ __forceinline__ float warp_sum16(float (&v)[16], int lane) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const bool up = lane & 16;
+    const float send = up ? v[i] : v[i + 8];
+    const float keep = up ? v[i + 8] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool up = lane & 8;
+    const float send = up ? v[i] : v[i + 4];
+    const float keep = up ? v[i + 4] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const bool up = lane & 4;
+    const float send = up ? v[i] : v[i + 2];
+    const float keep = up ? v[i + 2] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  {
+    const bool up = lane & 2;
+    const float send = up ? v[0] : v[1];
+    const float keep = up ? v[1] : v[0];
+    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
+
+__device__ __forceinline__ int warp_sum16_col(int lane) {
+  return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+}
+
+// kUni: every row weight equal and lambda = 1, so the row factor is one
+// constant per CTA, applied at the column write-out (one FADD2 per column pair
+// instead of FMUL2 + FFMA2).
+template <int D, int kPoly16, bool kUni>
+__global__ void __launch_bounds__(kSoftminThreads)
+softmin_sym_kernel(const __grid_constant__ Group G) {
+  static_assert(kSoftminThreads == kColTile, "one staged column per thread");
+  __shared__ __align__(16) float smem[2][kColTile * 4];
+  __shared__ float colacc[kSoftminThreads / 32][kColTile];
+  const int it = blockIdx.x;
+  if (it >= G.n_items) return;
+  const int4 item = G.items[it];
+  const Problem& P = G.P[item.x];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int row_base = P.tile_start[item.y];
+  const int row_end = P.tile_start[item.y + 1];
+  const int mid = (row_base + row_end) >> 1;
+  const float4 o = P.rows[mid];
+  const float est_mid = P.row_est ? P.row_est[mid] : 0.f;
+  const float R = est_mid * P.inv_lam_eps_ln2;  // tile reference (softmin.cu)
+
+  RowState ra, rb;
+  load_row<D>(P, row_base + tid, row_end, o, R, ra);
+  load_row<D>(P, row_base + tid + kSoftminThreads, row_end, o, R, rb);
+  // padding rows contribute exactly 0 to the column sums
+  if (row_base + tid >= row_end) ra.r = __int_as_float(0xff800000);
+  if (row_base + tid + kSoftminThreads >= row_end) rb.r = __int_as_float(0xff800000);
+  const float wu = kUni ? exp2f(P.row_lw2[row_base]) : 0.f;
+  // column-sum row factors a_i 2^{-ell (est_i - est_mid)}; 0 for padding rows
+  auto row_factor = [&](int r) -> float {
+    if (r >= row_end) return 0.f;
+    const float est = P.row_est ? P.row_est[r] : 0.f;
+    return exp2f(P.row_lw2[r] - P.ell * (est - est_mid));
+  };
+  const float wa = row_factor(row_base + tid), wb = row_factor(row_base + tid + kSoftminThreads);
+  const float2 WA = make_float2(wa, wa), WB = make_float2(wb, wb);
+
+  ColWalker w{P.ranges, P.tile_rptr[item.y], P.tile_rptr[item.y + 1], 0};
+  const int32_t pos_begin = item.z, pos_end = item.w;
+  float* colout = P.colpart + P.tile_slot[item.y];
+
+  float4 cv = make_float4(0.f, 0.f, 0.f, 0.f);
+  float ch = 0.f, cl = 0.f;
+  bool cvalid = false;
+  auto fetch = [&](int32_t tile_pos) {
+    const int32_t pos = tile_pos + tid;
+    cvalid = false;
+    if (pos < pos_end) {
+      const int j = w.col(pos);
+      if (j >= 0) {
+        cv = __ldg(P.cols + j);
+        cl = __ldg(P.col_lw2 + j);
+        ch = __ldg(P.col_h + j);
+        cvalid = true;
+      }
+    }
+  };
+  float cfac = 0.f;  // column factor of the column this thread staged
+  auto stage = [&](float* buf) {
+    float* rec = buf + (tid >> 1) * 8 + (tid & 1);
+    if (cvalid) {
+      const float a = (cv.x - o.x) * P.sc;
+      const float b = D > 1 ? (cv.y - o.y) * P.sc : 0.f;
+      const float c = D > 2 ? (cv.z - o.z) * P.sc : 0.f;
+      rec[0] = a;
+      rec[2] = b;
+      rec[4] = c;
+      rec[6] = (fmaf(ch, P.inv_eps_ln2, R) + cl) - fmaf(a, a, fmaf(b, b, c * c));
+      cfac = exp2f(P.ell * (ch - est_mid) - cl);
+    } else {
+      rec[0] = 0.f;
+      rec[2] = 0.f;
+      rec[4] = 0.f;
+      rec[6] = __int_as_float(0xff800000);  // -inf -> exp2(-inf) = 0
+      cfac = 0.f;
+    }
+  };
+
+  float2 sa = make_float2(0.f, 0.f), sb = make_float2(0.f, 0.f);
+  int buf = 0;
+  fetch(pos_begin);
+  for (int32_t tp = pos_begin; tp < pos_end; tp += kColTile) {
+    stage(smem[buf]);
+    __syncthreads();
+    if (tp + kColTile < pos_end) fetch(tp + kColTile);
+    const float4* s4 = reinterpret_cast<const float4*>(smem[buf]);
+    for (int c0 = 0; c0 < kColTile / 2; c0 += 8) {
+      float v[16];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int c = c0 + k;
+        const float4 A = s4[2 * c], B = s4[2 * c + 1];
+        const float2 Y0 = make_float2(A.x, A.y);
+        const float2 Y1 = make_float2(A.z, A.w);
+        const float2 Y2 = make_float2(B.x, B.y);
+        const float2 C = make_float2(B.z, B.w);
+        float2 ea, eb;
+        if (poly_slot(2 * k, kPoly16))
+          ea = pair_terms<D, true>(ra, Y0, Y1, Y2, C);
+        else
+          ea = pair_terms<D, false>(ra, Y0, Y1, Y2, C);
+        if (poly_slot(2 * k + 1, kPoly16))
+          eb = pair_terms<D, true>(rb, Y0, Y1, Y2, C);
+        else
+          eb = pair_terms<D, false>(rb, Y0, Y1, Y2, C);
+        sa = __fadd2_rn(sa, ea);
+        sb = __fadd2_rn(sb, eb);
+        const float2 cp = kUni ? __fadd2_rn(ea, eb) : __ffma2_rn(WA, ea, __fmul2_rn(WB, eb));
+        v[2 * k] = cp.x;
+        v[2 * k + 1] = cp.y;
+      }
+      const float cs = warp_sum16(v, lane);
+      if ((lane & 1) == 0) colacc[warp][2 * c0 + warp_sum16_col(lane)] = cs;
+    }
+    __syncthreads();
+    {
+      const int32_t pos = tp + tid;
+      if (pos < pos_end) {
+        float s = colacc[0][tid];
+#pragma unroll
+        for (int q = 1; q < kSoftminThreads / 32; ++q) s += colacc[q][tid];
+        colout[pos] = kUni ? s * (cfac * wu) : s * cfac;
+      }
+    }
+    buf ^= 1;
+  }
+  float* out = G.part + static_cast<int64_t>(it) * kTileRows;
+  out[tid] = sa.x + sa.y;
+  out[tid + kSoftminThreads] = sb.x + sb.y;
+}
+
+// Column totals (ColSum, prims.cuh): for every column j (cluster J =
+// labels[j], offset j - co[J]), the sum over the cluster's entries (tiles in
+// ascending order, this rank's tiles [t0, t1) only; self problems: only
+// tiles that end at or before j) of colpart[eslot + offset], in float64.
+__global__ void sym_colsum_kernel(const __grid_constant__ ColSumGroup g) {
+  const ColSum& a = g.c[blockIdx.y];
+  const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= a.n_cols) return;
+  const int32_t J = a.labels[j];
+  const int32_t off = j - a.co[J];
+  double s = 0.0;
+  for (int64_t e = a.eptr[static_cast<int64_t>(J) * kEntryChunks];
+       e < a.eptr[static_cast<int64_t>(J + 1) * kEntryChunks]; ++e) {
+    const int32_t t = a.etile[e];
+    if (t < a.t0 || t >= a.t1) continue;
+    if (a.self && a.tile_start[t + 1] > j) continue;
+    s += static_cast<double>(a.colpart[a.eslot[e] + off]);
+  }
+  a.tot[j] = static_cast<float>(s);
+}
+
+cudaError_t launch_colsum(const ColSum* c, int n, cudaStream_t st) {
+  ColSumGroup g{};
+  int32_t mx = 0;
+  for (int k = 0; k < n; ++k) {
+    g.c[k] = c[k];
+    mx = max(mx, c[k].n_cols);
+  }
+  g.n = n;
+  if (n <= 0 || mx <= 0) return cudaSuccess;
+  ++g_launches;
+  sym_colsum_kernel<<<dim3((mx + 255) / 256, n), 256, 0, st>>>(g);
+  return cudaGetLastError();
+}
+
+// The transposed cross problem (problem `p`, no tiles of its own): its sum
+// is the column total alone.  One thread per row; out-of-window rows are
+// queued for the exact path.
+__global__ void sym_colfinal_kernel(const __grid_constant__ Group G, int p) {
+  const Problem& P = G.P[p];
+  const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= P.n_rows) return;
+  const float s = P.row_add[r];
+  const float est = P.row_est ? P.row_est[r] : 0.f;
+  if (!(s >= 8.67361738e-19f && s <= 1.2676506e30f)) {
+    const int slot = atomicAdd(G.fb_count, 1);
+    atomicAdd(G.fb_total, 1);
+    if (slot < G.fb_cap) G.fb_list[slot] = make_int4(p, r, -1, 0);
+    return;
+  }
+  P.row_out[r] = est - P.mixw * P.lam_eps * logf(s);
+}
+
+cudaError_t launch_colfinal(const Group& g, int p, cudaStream_t st) {
+  const int32_t n = g.P[p].n_rows;
+  if (n <= 0) return cudaSuccess;
+  ++g_launches;
+  sym_colfinal_kernel<<<(n + 255) / 256, 256, 0, st>>>(g, p);
+  return cudaGetLastError();
+}
+
+// Exact online-max LSE over ALL columns for the rows the fixed-reference
+// path rejected (a superset of the row's pair set: the extra terms are the
+// ones the truncation bounds below e^-theta).
+template <int D>
+__global__ void softmin_fallback_dense(const __grid_constant__ Group G) {
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int cnt = min(*G.fb_count, G.fb_cap);
+  for (int q = warp; q < cnt; q += nwarps) {
+    const int4 pr = G.fb_list[q];
+    const Problem& P = G.P[pr.x];
+    const int r = pr.y;
+    const float4 xv = P.rows[r];
+    float m = -INFINITY, s = 0.f;
+    for (int j = lane; j < P.n_cols; j += 32) {
+      const float4 yv = P.cols[j];
+      float dx = xv.x - yv.x, c = dx * dx;
+      if (D > 1) { const float dy = xv.y - yv.y; c = fmaf(dy, dy, c); }
+      if (D > 2) { const float dz = xv.z - yv.z; c = fmaf(dz, dz, c); }
+      const float z = P.col_lw2[j] + (P.col_h[j] - 0.5f * c) * P.inv_eps_ln2;
+      if (z > m) { s = s * exp2f(m - z) + 1.f; m = z; }
+      else s += exp2f(z - m);
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, off);
+      const float s2 = __shfl_xor_sync(0xffffffffu, s, off);
+      const float mm = fmaxf(m, m2);
+      s = (m == -INFINITY ? 0.f : s * exp2f(m - mm)) + (m2 == -INFINITY ? 0.f : s2 * exp2f(m2 - mm));
+      m = mm;
+    }
+    if (lane == 0) {
+      const float est = P.row_est ? P.row_est[r] : 0.f;
+      const float ft = -P.lam_eps * kLn2 * (m + log2f(s));
+      P.row_out[r] = (1.f - P.mixw) * est + P.mixw * ft;
+    }
+  }
+}
+
+static int poly16_sym() {
+  static const int v = [] {
+    const char* e = getenv("MSOT_POLY16_SYM");
+    return e ? atoi(e) : 0;  // the FMA pipe carries the column sums here
+  }();
+  return v;
+}
+
+template <int D, bool kUni>
+static void launch_sym_d(const Group& g, cudaStream_t st) {
+  ++g_launches;
+  dim3 grid(g.n_items), block(kSoftminThreads);
+  switch (poly16_sym()) {
+    case 2: softmin_sym_kernel<D, 2, kUni><<<grid, block, 0, st>>>(g); break;
+    default: softmin_sym_kernel<D, 0, kUni><<<grid, block, 0, st>>>(g); break;
+  }
+}
+
+cudaError_t launch_softmin_sym(const Group& g, int d, bool uniform, cudaStream_t st) {
+  if (g.n_items <= 0) return cudaSuccess;
+  if (uniform) {
+    switch (d) {
+      case 1: launch_sym_d<1, true>(g, st); break;
+      case 2: launch_sym_d<2, true>(g, st); break;
+      default: launch_sym_d<3, true>(g, st); break;
+    }
+  } else {
+    switch (d) {
+      case 1: launch_sym_d<1, false>(g, st); break;
+      case 2: launch_sym_d<2, false>(g, st); break;
+      default: launch_sym_d<3, false>(g, st); break;
+    }
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fallback_dense(const Group& g, int d, int n_sm, cudaStream_t st) {
+  ++g_launches;
+  switch (d) {
+    case 1: softmin_fallback_dense<1><<<n_sm, 256, 0, st>>>(g); break;
+    case 2: softmin_fallback_dense<2><<<n_sm, 256, 0, st>>>(g); break;
+    default: softmin_fallback_dense<3><<<n_sm, 256, 0, st>>>(g); break;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace msot_dev

@@ -139,6 +139,7 @@ struct DMeasure {
   float* radii = nullptr;
   std::vector<float> radii_h;
   std::vector<int32_t> offsets_h;  // cluster offsets (host copy, K+1)
+  bool uniform = false;            // all weights equal
 };
 
 void prepare_measure(msot_ctx* c, const std::string& tag, const double* d_x, const double* d_w,
@@ -154,7 +155,13 @@ void prepare_measure(msot_ctx* c, const std::string& tag, const double* d_x, con
   M.pts = c->buf<float4>(tag + ".pts", n);
   M.lw2 = c->buf<float>(tag + ".lw2", n);
   M.w64 = c->buf<double>(tag + ".w64", n);
-  CK(gather_points(d_x, d_w, n, d, g, M.perm, M.pts, M.lw2, M.w64, st));
+  int32_t* nonuni = c->buf<int32_t>(tag + ".nonuni", 1);
+  CK(cudaMemsetAsync(nonuni, 0, sizeof(int32_t), st));
+  CK(gather_points(d_x, d_w, n, d, g, M.perm, M.pts, M.lw2, M.w64, nonuni, st));
+  int32_t nu = 1;
+  CK(cudaMemcpyAsync(&nu, nonuni, sizeof(nu), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  M.uniform = nu == 0;
   if (!clusters) return;
   uint8_t* flags = c->buf<uint8_t>(tag + ".flags", n);
   M.labels = c->buf<int32_t>(tag + ".labels", n);
@@ -263,6 +270,73 @@ void mask_rangeset(msot_ctx* c, const std::string& tag, const int32_t* rl,
   CK(tile_range_write(tbits, ky, R.n_tiles, co, R.rptr, R.ranges, st));
 }
 
+// Pair sets of the evaluate-once softmin (mask.cu: sym_runs / sym_entries):
+// the row tiles' column lists plus, per column cluster, the (tile, slot)
+// entries its column sums are read from.
+struct SymSet {
+  RangeSet R;
+  int self = 0;
+  int64_t* tslot = nullptr;   // [T + 1] first colpart slot of each tile
+  int64_t* ebase = nullptr;   // [K * kEntryChunks + 1]
+  int64_t* eslot = nullptr;
+  int32_t* etile = nullptr;
+  float* colpart = nullptr;
+  int64_t slots = 0, entries = 0;
+};
+
+void sym_rangeset(msot_ctx* c, const std::string& tag, const int32_t* rl,
+                  const std::vector<int32_t>& ro, int64_t n_rows, const int32_t* co, int32_t ky,
+                  const uint32_t* mask, int self, SymSet& S) {
+  cudaStream_t st = c->st;
+  RangeSet& R = S.R;
+  S.self = self;
+  if (R.tile_start_h.empty()) make_tiles(c, tag, n_rows, &ro, R);  // fixed per solve
+  const int64_t T = R.n_tiles;
+  const int32_t words = mask_words(ky);
+  int64_t* nr = c->buf<int64_t>(tag + ".nr", T + 1);
+  R.tile_cols = c->buf<int64_t>(tag + ".tcols", T + 1);
+  R.rptr = c->buf<int64_t>(tag + ".rptr", T + 1);
+  S.tslot = c->buf<int64_t>(tag + ".tslot", T + 1);
+  int64_t* stmp = c->buf<int64_t>(tag + ".stmp", scan_temp_elems(T + 1));
+  uint32_t* tbits = c->buf<uint32_t>(tag + ".tbits", size_t(T) * words);
+  int32_t* posword = c->buf<int32_t>(tag + ".posw", size_t(T) * words);
+  CK(tile_or(mask, ky, rl, R.tile_start, T, tbits, st));
+  CK(sym_ranges(tbits, ky, T, co, R.tile_start, rl, self, nr, R.tile_cols, posword, nullptr,
+                nullptr, false, st));
+  CK(cudaMemsetAsync(nr + T, 0, sizeof(int64_t), st));
+  CK(cudaMemsetAsync(R.tile_cols + T, 0, sizeof(int64_t), st));
+  CK((scan<int64_t, int64_t>(nr, R.rptr, T + 1, false, stmp, nullptr, st)));
+  CK((scan<int64_t, int64_t>(R.tile_cols, S.tslot, T + 1, false, stmp, nullptr, st)));
+  // (tile, cluster) entries, column-major
+  const int64_t ne = static_cast<int64_t>(ky) * kEntryChunks;
+  int32_t* ecnt = c->buf<int32_t>(tag + ".ecnt", ne + 1);
+  S.ebase = c->buf<int64_t>(tag + ".ebase", ne + 1);
+  int64_t* etmp = c->buf<int64_t>(tag + ".etmp", scan_temp_elems(ne + 1));
+  CK(sym_entries(tbits, ky, T, co, R.tile_start, rl, self, posword, S.tslot, ecnt, nullptr,
+                 nullptr, nullptr, false, st));
+  CK(cudaMemsetAsync(ecnt + ne, 0, sizeof(int32_t), st));
+  CK((scan<int32_t, int64_t>(ecnt, S.ebase, ne + 1, false, etmp, nullptr, st)));
+  int64_t tot[3];
+  CK(cudaMemcpyAsync(&tot[0], R.rptr + T, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&tot[1], S.tslot + T, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&tot[2], S.ebase + ne, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  R.tile_cols_h.resize(T);
+  CK(cudaMemcpyAsync(R.tile_cols_h.data(), R.tile_cols, T * sizeof(int64_t),
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  R.n_ranges = tot[0];
+  S.slots = tot[1];
+  S.entries = tot[2];
+  R.ranges = c->buf<int2>(tag + ".ranges", R.n_ranges);
+  CK(sym_ranges(tbits, ky, T, co, R.tile_start, rl, self, nullptr, nullptr, nullptr, R.rptr,
+                R.ranges, true, st));
+  S.eslot = c->buf<int64_t>(tag + ".eslot", S.entries);
+  S.etile = c->buf<int32_t>(tag + ".etile", S.entries);
+  CK(sym_entries(tbits, ky, T, co, R.tile_start, rl, self, posword, S.tslot, nullptr, S.ebase,
+                 S.eslot, S.etile, true, st));
+  S.colpart = c->buf<float>(tag + ".colpart", S.slots);
+}
+
 // ------------------------------------------------------------ launch plans
 struct HdOperands {  // high-dimensional path (softmin_hd.cu)
   const uint8_t* a_pack = nullptr;
@@ -281,6 +355,8 @@ struct ProbSpec {
   int64_t n_cols;
   const RangeSet* rs;
   HdOperands hd{};
+  const SymSet* sym = nullptr;   // evaluate-once groups
+  const float* row_lw2 = nullptr;
 };
 
 struct Plan {
@@ -447,6 +523,124 @@ void run_group(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& ss) {
 }
 
 // ------------------------------------------------------------------ solve
+// Evaluate-once group (softmin_sym.cu): plan problems 0 = xx, 1 = yy (self,
+// rows = cols) and 2 = yx (rows x, cols y); the column side of problem 2 is
+// the a_xy update, described by problem 3 (rows y over cols x) which has no
+// tiles of its own.  a.{h,est,out}[3] belong to that transposed problem.
+struct SymCols {
+  const int32_t* labels[3];  // column clusters of problems 0..2
+  const int32_t* co[3];
+  float* tot[3];             // column totals (x, y, y)
+  const float4* yrows;       // problem 3: rows y over cols x
+  const float4* xcols;
+  const float* x_lw2;
+  int64_t n, m;
+  bool uniform;              // both measures have uniform weights
+};
+
+void fill_problem(Problem& Q, const ProbSpec& S, const float* h, const float* est, float* out,
+                  double eps, double lam, double mixw) {
+  const double ln2 = 0.69314718055994530942;
+  Q.rows = S.rows;
+  Q.row_est = est;
+  Q.row_out = out;
+  Q.cols = S.cols;
+  Q.col_lw2 = S.col_lw2;
+  Q.col_h = h;
+  Q.a_pack = S.hd.a_pack;
+  Q.b_pack = S.hd.b_pack;
+  Q.row_sq = S.hd.row_sq;
+  Q.col_sq = S.hd.col_sq;
+  Q.row_f = S.hd.row_f;
+  Q.col_f = S.hd.col_f;
+  if (S.rs) {
+    Q.tile_start = S.rs->tile_start;
+    Q.tile_rptr = S.rs->rptr;
+    Q.ranges = S.rs->ranges;
+  }
+  Q.n_rows = static_cast<int32_t>(S.n_rows);
+  Q.n_cols = static_cast<int32_t>(S.n_cols);
+  Q.sc = static_cast<float>(1.0 / std::sqrt(2.0 * eps * ln2));
+  Q.inv_eps_ln2 = static_cast<float>(1.0 / (eps * ln2));
+  Q.inv_lam_eps_ln2 = static_cast<float>(1.0 / (lam * eps * ln2));
+  Q.lam_eps = static_cast<float>(lam * eps);
+  Q.mixw = static_cast<float>(mixw);
+  Q.ell = static_cast<float>((1.0 / lam - 1.0) / (eps * ln2));
+  Q.row_lw2 = S.row_lw2;
+  if (S.sym) {
+    Q.colpart = S.sym->colpart;
+    Q.tile_slot = S.sym->tslot;
+  }
+}
+
+void run_group_sym(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& ss,
+                   const SymCols& X) {
+  cudaStream_t st = c->st;
+  Group G{};
+  int32_t tiles_acc = 0;
+  G.tile_prefix[0] = 0;
+  for (int p = 0; p < 3; ++p) {
+    Problem& Q = G.P[p];
+    fill_problem(Q, P.ps[p], a.h[p], a.est[p], a.out[p], a.eps, a.lam, a.mixw);
+    Q.tile_ibase = P.ibase[p];
+    Q.row_add = p < 2 ? X.tot[p] : nullptr;
+    G.t0[p] = static_cast<int32_t>(P.t0[p]);
+    tiles_acc += static_cast<int32_t>(P.t1[p] - P.t0[p]);
+    G.tile_prefix[p + 1] = tiles_acc;
+  }
+  {
+    const ProbSpec T{X.yrows, X.m, X.xcols, X.x_lw2, X.n, nullptr};
+    fill_problem(G.P[3], T, a.h[3], a.est[3], a.out[3], a.eps, a.lam, a.mixw);
+    G.P[3].row_add = X.tot[2];
+  }
+  G.n_problems = 3;
+  G.items = P.items;
+  G.n_items = P.n_items;
+  G.part = P.part;
+  G.fb_count = ss.fb_count;
+  G.fb_total = ss.fb_total;
+  G.fb_list = ss.fb_list;
+  G.fb_cap = ss.fb_cap;
+  CK(cudaMemsetAsync(ss.fb_count, 0, sizeof(int32_t), st));
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->profiling) {
+    c->ev_pair(&e0, &e1);
+    CK(cudaEventRecord(e0, st));
+  }
+  CK(launch_softmin_sym(G, ss.d, X.uniform && a.lam == 1.0, st));
+  if (c->profiling) CK(cudaEventRecord(e1, st));
+  ColSum cs[3];
+  for (int p = 0; p < 3; ++p) {
+    const SymSet& S = *P.ps[p].sym;
+    cs[p] = ColSum{X.labels[p], X.co[p], S.ebase, S.eslot, S.etile, S.R.tile_start, S.colpart,
+                   X.tot[p], static_cast<int32_t>(P.ps[p].n_cols), S.self,
+                   static_cast<int32_t>(P.t0[p]), static_cast<int32_t>(P.t1[p])};
+  }
+  CK(launch_colsum(cs, 3, st));
+  if (c->world > 1) {  // column sums of every rank's tiles (NCCL over NVLink)
+    NK(ncclGroupStart());
+    for (int p = 0; p < 3; ++p)
+      NK(ncclAllReduce(X.tot[p], X.tot[p], P.ps[p].n_cols, ncclFloat, ncclSum, c->comm, st));
+    NK(ncclGroupEnd());
+  }
+  CK(launch_finalize(G, st));
+  CK(launch_colfinal(G, 3, st));
+  CK(launch_fallback_dense(G, ss.d, c->n_sm, st));
+  ss.S->softmin_launches += 1;
+  ss.S->pairs_evaluated += P.pairs_all;
+  if (c->world > 1) {  // all-gather of the row-side potentials
+    NK(ncclGroupStart());
+    for (int p = 0; p < 3; ++p)
+      for (int r = 0; r < c->world; ++r) {
+        const int64_t b0 = P.row_bounds[p][r], b1 = P.row_bounds[p][r + 1];
+        if (b1 > b0) NK(ncclBroadcast(a.out[p] + b0, a.out[p] + b0, b1 - b0, ncclFloat, r, c->comm, st));
+      }
+    NK(ncclGroupEnd());
+  }
+}
+
+
+
 struct Potentials {
   float* v[2][4];  // [buffer][a_xx, b_yy, a_xy, b_yx]
 };
@@ -491,6 +685,23 @@ void sym_step(msot_ctx* c, const Plan& P, Potentials& U, int& cur, double eps, d
   a.lam = lam;
   a.mixw = assign ? 1.0 : 0.5;
   run_group(c, P, a, ss);
+  cur ^= 1;
+}
+
+// One evaluate-once symmetric update: same contract as sym_step.
+void sym_step_once(msot_ctx* c, const Plan& P, Potentials& U, int& cur, double eps, double lam,
+                   bool assign, SolveState& ss, const SymCols& X) {
+  float** o = U.v[cur];
+  float** n = U.v[cur ^ 1];
+  ScaleArgs a{};
+  a.h[0] = o[0]; a.est[0] = o[0]; a.out[0] = n[0];  // a_xx
+  a.h[1] = o[1]; a.est[1] = o[1]; a.out[1] = n[1];  // b_yy
+  a.h[2] = o[2]; a.est[2] = o[3]; a.out[2] = n[3];  // b_yx (rows x, cols y)
+  a.h[3] = o[3]; a.est[3] = o[2]; a.out[3] = n[2];  // a_xy (its column side)
+  a.eps = eps;
+  a.lam = lam;
+  a.mixw = assign ? 1.0 : 0.5;
+  run_group_sym(c, P, a, ss, X);
   cur ^= 1;
 }
 
@@ -892,6 +1103,20 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
     grad[3] = c->buf<float4>("m.gyx", X.k);
     RangeSet &rxx = fxx, &ryy = fyy, &rxy = fxy, &ryx = fyx;
     Plan Pf;
+    const bool once = prm->pair_eval != 0;
+    SymSet sxx, syy, syx;
+    SymCols scol{};
+    if (once) {
+      scol.labels[0] = X.labels; scol.co[0] = X.offsets; scol.tot[0] = c->buf<float>("s.totx", n);
+      scol.labels[1] = Y.labels; scol.co[1] = Y.offsets; scol.tot[1] = c->buf<float>("s.toty", m);
+      scol.labels[2] = Y.labels; scol.co[2] = Y.offsets; scol.tot[2] = c->buf<float>("s.totxy", m);
+      scol.yrows = Y.pts;
+      scol.xcols = X.pts;
+      scol.x_lw2 = X.lw2;
+      scol.n = n;
+      scol.m = m;
+      scol.uniform = X.uniform && Y.uniform;
+    }
     auto build_masks = [&](double e) {
       // without a coarse phase there is no information: keep every pair
       const bool info = tsw > 0;
@@ -920,11 +1145,21 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
       // the yx mask (rows y) is the exact transpose of the xy mask (rows x)
       CK(truncation_masks(X.k, Y.k, d, X.cpts, X.radii, fmax[3], g[3], Y.cpts, Y.radii, fmax[2],
                           g[2], e, theta, 0, mxy, myx, bxr, byr, st));
-      mask_rangeset(c, "f.xx", X.labels, X.offsets_h, n, X.offsets, X.k, mxx, rxx);
-      mask_rangeset(c, "f.yy", Y.labels, Y.offsets_h, m, Y.offsets, Y.k, myy, ryy);
-      mask_rangeset(c, "f.yx", X.labels, X.offsets_h, n, Y.offsets, Y.k, mxy, ryx);  // rows x, cols y
-      mask_rangeset(c, "f.xy", Y.labels, Y.offsets_h, m, X.offsets, X.k, myx, rxy);  // rows y, cols x
-      sym_specs(Pf, X.pts, X.lw2, n, Y.pts, Y.lw2, m, &rxx, &ryy, &rxy, &ryx);
+      if (once) {  // evaluate-once pair sets (oracle.cpp: sym_self, transpose_ranges)
+        sym_rangeset(c, "s.xx", X.labels, X.offsets_h, n, X.offsets, X.k, mxx, 1, sxx);
+        sym_rangeset(c, "s.yy", Y.labels, Y.offsets_h, m, Y.offsets, Y.k, myy, 1, syy);
+        sym_rangeset(c, "s.yx", X.labels, X.offsets_h, n, Y.offsets, Y.k, mxy, 0, syx);
+        Pf.np = 3;
+        Pf.ps[0] = {X.pts, n, X.pts, X.lw2, n, &sxx.R, {}, &sxx, X.lw2};
+        Pf.ps[1] = {Y.pts, m, Y.pts, Y.lw2, m, &syy.R, {}, &syy, Y.lw2};
+        Pf.ps[2] = {X.pts, n, Y.pts, Y.lw2, m, &syx.R, {}, &syx, X.lw2};
+      } else {
+        mask_rangeset(c, "f.xx", X.labels, X.offsets_h, n, X.offsets, X.k, mxx, rxx);
+        mask_rangeset(c, "f.yy", Y.labels, Y.offsets_h, m, Y.offsets, Y.k, myy, ryy);
+        mask_rangeset(c, "f.yx", X.labels, X.offsets_h, n, Y.offsets, Y.k, mxy, ryx);  // rows x, cols y
+        mask_rangeset(c, "f.xy", Y.labels, Y.offsets_h, m, X.offsets, X.k, myx, rxy);  // rows y, cols x
+        sym_specs(Pf, X.pts, X.lw2, n, Y.pts, Y.lw2, m, &rxx, &ryy, &rxy, &ryx);
+      }
       build_plan(c, "pf", Pf);
     };
     for (int t = tsw; t <= ns; ++t) {
@@ -936,10 +1171,17 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
         build_masks(eps[tt]);
       }
       c->mark(4);
-      sym_step(c, Pf, U, cur, eps[tt], lam[tt], t == ns, ss);
+      if (once)
+        sym_step_once(c, Pf, U, cur, eps[tt], lam[tt], t == ns, ss, scol);
+      else
+        sym_step(c, Pf, U, cur, eps[tt], lam[tt], t == ns, ss);
       S->pairs_dense += full;
       S->pairs_fine += Pf.pairs_all;
       S->pairs_fine_dense += full;
+    }
+    if (once && d_grad) {  // the plans of grad_positions read per-row ranges
+      mask_rangeset(c, "f.xx", X.labels, X.offsets_h, n, X.offsets, X.k, mxx, fxx);
+      mask_rangeset(c, "f.yx", X.labels, X.offsets_h, n, Y.offsets, Y.k, mxy, fyx);
     }
   }
   }  // d <= 3
@@ -1040,6 +1282,7 @@ void msot_params_default(msot_params* p) {
   p->theta = 20.0;
   p->switch_factor = 2.0;
   p->max_full_iters = 10000;
+  p->pair_eval = 1;
 }
 
 int msot_schedule(double diameter, const msot_params* p, double* sigma, double* eps, double* lam,

@@ -112,7 +112,16 @@ static void gpu_checks() {
   CHECK(std::fabs(divergence(c, c, p)) < 1e-9);
   SolverParams q = p;
   q.multiscale = true;
-  CHECK(std::fabs(divergence(c, c, q)) < 1e-9);
+  // multiscale fine phase evaluates each kept pair once: a_xy comes from
+  // column sums and b_yx from row sums, so S(c, c) is zero up to float32
+  // rounding of the potentials (1e-4 eps per unit mass; the contract allows
+  // 1e-3 eps per potential)
+  {
+    double mass = 0.0;
+    for (double v : w) mass += v;
+    const double s = divergence(c, c, q);
+    CHECK(std::fabs(s) < 1e-4 * 0.05 * 0.05 * mass);
+  }
   // softmin of SPEC.md:170
   DiscreteMeasure x({0.0}, {1.0}, 1), y({1.5}, {1.0}, 1);
   auto f = softmin(x, y, {0.0}, 0.3);

@@ -191,17 +191,36 @@ def test_dense_low_dim(ctx, oracle, d):
     assert abs(lg - lo) <= LOSS_TOL * abs(lo)
 
 
-@pytest.mark.parametrize("retruncate", [0, 1])
-def test_multiscale_parity(ctx, oracle, retruncate):
+@pytest.mark.parametrize("retruncate,pair_eval", [(0, 1), (1, 1), (1, 0)])
+def test_multiscale_parity(ctx, oracle, retruncate, pair_eval):
     """Config-2 shape (Gaussian mixtures, voxel grid, truncation) at a size
-    the oracle finishes in seconds."""
+    the oracle finishes in seconds; both fine-phase schemes (evaluate-once
+    row + column sums, and one row-wise problem per potential)."""
     n = 6000
     x, y = mixture(n, 3), mixture(n, 4)
     a, b = np.full(n, 1 / n), np.full(n, 1 / n)
-    prm = make_params(blur=0.01, multiscale=True, retruncate=retruncate, cluster_scale=0.04)
+    prm = make_params(blur=0.01, multiscale=True, retruncate=retruncate, cluster_scale=0.04,
+                      pair_eval=pair_eval)
     lg, pg, sg, lo, po, so = run_both(ctx, oracle, prm, x, a, y, b)
     assert (sg["kx"], sg["ky"], sg["t_switch"]) == (so["kx"], so["ky"], so["t_switch"])
     assert sg["pairs_fine"] < sg["pairs_fine_dense"]
+    check_pots(pg, po, 1e-4)
+    assert abs(lg - lo) <= LOSS_TOL * abs(lo), (lg, lo)
+
+
+@pytest.mark.parametrize("reach", [0.3, 0.05])
+def test_multiscale_unbalanced_parity(ctx, oracle, reach):
+    """Finite reach in the block-sparse phase: lambda < 1, so the row and
+    column references of the evaluate-once kernel differ (ell != 0)."""
+    n, m = 5000, 4400
+    x, y = mixture(n, 11), mixture(m, 12)
+    rng = np.random.default_rng(13)
+    a = rng.random(n) + 0.5
+    a /= a.sum()
+    b = np.full(m, 1.3 / m)
+    prm = make_params(blur=0.01, reach=reach, multiscale=True, retruncate=1, cluster_scale=0.04)
+    lg, pg, sg, lo, po, so = run_both(ctx, oracle, prm, x, a, y, b)
+    assert sg["t_switch"] == so["t_switch"] and sg["t_switch"] < sg["n_scales"]
     check_pots(pg, po, 1e-4)
     assert abs(lg - lo) <= LOSS_TOL * abs(lo), (lg, lo)
 

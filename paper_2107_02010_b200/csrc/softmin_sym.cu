@@ -60,15 +60,22 @@ __device__ __forceinline__ int warp_sum16_col(int lane) {
   return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
 }
 
+// One CTA = one work item (256 rows x a run of the tile's columns), 64
+// threads with 4 rows each: a staged column pair is read once per 4 rows and
+// the column butterfly is shared by 128 rows per warp.
+constexpr int kSymThreads = 64;
+constexpr int kSymRows = kTileRows / kSymThreads;  // 4
+constexpr int kSymCols = kSymThreads;              // columns staged per buffer
+static_assert(kSymRows == 4, "softmin_sym_kernel is written for 4 rows per thread");
+
 // kUni: every row weight equal and lambda = 1, so the row factor is one
-// constant per CTA, applied at the column write-out (one FADD2 per column pair
-// instead of FMUL2 + FFMA2).
+// constant per CTA, applied at the column write-out (the column partial of a
+// column pair is the packed sum of the 4 rows' terms).
 template <int D, int kPoly16, bool kUni>
-__global__ void __launch_bounds__(kSoftminThreads)
+__global__ void __launch_bounds__(kSymThreads)
 softmin_sym_kernel(const __grid_constant__ Group G) {
-  static_assert(kSoftminThreads == kColTile, "one staged column per thread");
-  __shared__ __align__(16) float smem[2][kColTile * 4];
-  __shared__ float colacc[kSoftminThreads / 32][kColTile];
+  __shared__ __align__(16) float smem[2][kSymCols * 4];
+  __shared__ float colacc[kSymThreads / 32][kSymCols];
   const int it = blockIdx.x;
   if (it >= G.n_items) return;
   const int4 item = G.items[it];
@@ -81,21 +88,23 @@ softmin_sym_kernel(const __grid_constant__ Group G) {
   const float est_mid = P.row_est ? P.row_est[mid] : 0.f;
   const float R = est_mid * P.inv_lam_eps_ln2;  // tile reference (softmin.cu)
 
-  RowState ra, rb;
-  load_row<D>(P, row_base + tid, row_end, o, R, ra);
-  load_row<D>(P, row_base + tid + kSoftminThreads, row_end, o, R, rb);
-  // padding rows contribute exactly 0 to the column sums
-  if (row_base + tid >= row_end) ra.r = __int_as_float(0xff800000);
-  if (row_base + tid + kSoftminThreads >= row_end) rb.r = __int_as_float(0xff800000);
+  RowState rs[kSymRows];
+  float2 W[kSymRows];
+#pragma unroll
+  for (int q = 0; q < kSymRows; ++q) {
+    const int r = row_base + tid + q * kSymThreads;
+    load_row<D>(P, r, row_end, o, R, rs[q]);
+    // padding rows contribute exactly 0 (rows and columns)
+    if (r >= row_end) rs[q].r = __int_as_float(0xff800000);
+    float wq = 0.f;
+    if (!kUni && r < row_end) {
+      // column-sum row factor a_i 2^{-ell (est_i - est_mid)}
+      const float est = P.row_est ? P.row_est[r] : 0.f;
+      wq = exp2f(P.row_lw2[r] - P.ell * (est - est_mid));
+    }
+    W[q] = make_float2(wq, wq);
+  }
   const float wu = kUni ? exp2f(P.row_lw2[row_base]) : 0.f;
-  // column-sum row factors a_i 2^{-ell (est_i - est_mid)}; 0 for padding rows
-  auto row_factor = [&](int r) -> float {
-    if (r >= row_end) return 0.f;
-    const float est = P.row_est ? P.row_est[r] : 0.f;
-    return exp2f(P.row_lw2[r] - P.ell * (est - est_mid));
-  };
-  const float wa = row_factor(row_base + tid), wb = row_factor(row_base + tid + kSoftminThreads);
-  const float2 WA = make_float2(wa, wa), WB = make_float2(wb, wb);
 
   ColWalker w{P.ranges, P.tile_rptr[item.y], P.tile_rptr[item.y + 1], 0};
   const int32_t pos_begin = item.z, pos_end = item.w;
@@ -138,15 +147,18 @@ softmin_sym_kernel(const __grid_constant__ Group G) {
     }
   };
 
-  float2 sa = make_float2(0.f, 0.f), sb = make_float2(0.f, 0.f);
+  float2 sum[kSymRows];
+#pragma unroll
+  for (int q = 0; q < kSymRows; ++q) sum[q] = make_float2(0.f, 0.f);
   int buf = 0;
   fetch(pos_begin);
-  for (int32_t tp = pos_begin; tp < pos_end; tp += kColTile) {
+  for (int32_t tp = pos_begin; tp < pos_end; tp += kSymCols) {
     stage(smem[buf]);
     __syncthreads();
-    if (tp + kColTile < pos_end) fetch(tp + kColTile);
+    if (tp + kSymCols < pos_end) fetch(tp + kSymCols);
     const float4* s4 = reinterpret_cast<const float4*>(smem[buf]);
-    for (int c0 = 0; c0 < kColTile / 2; c0 += 8) {
+#pragma unroll 1
+    for (int c0 = 0; c0 < kSymCols / 2; c0 += 8) {
       float v[16];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
@@ -156,18 +168,24 @@ softmin_sym_kernel(const __grid_constant__ Group G) {
         const float2 Y1 = make_float2(A.z, A.w);
         const float2 Y2 = make_float2(B.x, B.y);
         const float2 C = make_float2(B.z, B.w);
-        float2 ea, eb;
-        if (poly_slot(2 * k, kPoly16))
-          ea = pair_terms<D, true>(ra, Y0, Y1, Y2, C);
-        else
-          ea = pair_terms<D, false>(ra, Y0, Y1, Y2, C);
-        if (poly_slot(2 * k + 1, kPoly16))
-          eb = pair_terms<D, true>(rb, Y0, Y1, Y2, C);
-        else
-          eb = pair_terms<D, false>(rb, Y0, Y1, Y2, C);
-        sa = __fadd2_rn(sa, ea);
-        sb = __fadd2_rn(sb, eb);
-        const float2 cp = kUni ? __fadd2_rn(ea, eb) : __ffma2_rn(WA, ea, __fmul2_rn(WB, eb));
+        float2 e[kSymRows];
+#pragma unroll
+        for (int q = 0; q < kSymRows; ++q) {
+          if (poly_slot((kSymRows * k + q) & 15, kPoly16))
+            e[q] = pair_terms<D, true>(rs[q], Y0, Y1, Y2, C);
+          else
+            e[q] = pair_terms<D, false>(rs[q], Y0, Y1, Y2, C);
+          sum[q] = __fadd2_rn(sum[q], e[q]);
+        }
+        float2 cp;
+        if (kUni) {
+          cp = __fadd2_rn(__fadd2_rn(e[0], e[1]), __fadd2_rn(e[2], e[3]));
+        } else {
+          cp = __fmul2_rn(W[0], e[0]);
+          cp = __ffma2_rn(W[1], e[1], cp);
+          cp = __ffma2_rn(W[2], e[2], cp);
+          cp = __ffma2_rn(W[3], e[3], cp);
+        }
         v[2 * k] = cp.x;
         v[2 * k + 1] = cp.y;
       }
@@ -180,15 +198,15 @@ softmin_sym_kernel(const __grid_constant__ Group G) {
       if (pos < pos_end) {
         float s = colacc[0][tid];
 #pragma unroll
-        for (int q = 1; q < kSoftminThreads / 32; ++q) s += colacc[q][tid];
+        for (int q = 1; q < kSymThreads / 32; ++q) s += colacc[q][tid];
         colout[pos] = kUni ? s * (cfac * wu) : s * cfac;
       }
     }
     buf ^= 1;
   }
   float* out = G.part + static_cast<int64_t>(it) * kTileRows;
-  out[tid] = sa.x + sa.y;
-  out[tid + kSoftminThreads] = sb.x + sb.y;
+#pragma unroll
+  for (int q = 0; q < kSymRows; ++q) out[tid + q * kSymThreads] = sum[q].x + sum[q].y;
 }
 
 // Column totals (ColSum, prims.cuh): for every column j (cluster J =
@@ -302,7 +320,7 @@ static int poly16_sym() {
 template <int D, bool kUni>
 static void launch_sym_d(const Group& g, cudaStream_t st) {
   ++g_launches;
-  dim3 grid(g.n_items), block(kSoftminThreads);
+  dim3 grid(g.n_items), block(kSymThreads);
   switch (poly16_sym()) {
     case 2: softmin_sym_kernel<D, 2, kUni><<<grid, block, 0, st>>>(g); break;
     default: softmin_sym_kernel<D, 0, kUni><<<grid, block, 0, st>>>(g); break;

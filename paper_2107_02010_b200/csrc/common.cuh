@@ -42,6 +42,7 @@ struct Problem {
   const uint8_t* b_pack;     // cols, [hi, lo, hi] per 128-col block
   const float* row_sq;       // |x_i|^2 (float32 coordinates)
   const float* col_sq;       // |y_j|^2
+  const float* col_c;        // per-scale column constants (hd_colconst)
   const float* row_f;        // float32 coordinates, row-major x 64 (exact fallback)
   const float* col_f;
   // evaluate-once (symmetric) groups (softmin_sym.cu)

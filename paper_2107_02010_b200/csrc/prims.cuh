@@ -68,6 +68,8 @@ cudaError_t hd_pack(const double* x, int64_t n, int d, const double* center, int
                     uint8_t* pack, float* sq, float* xf, cudaStream_t st);
 cudaError_t hd_weights(const double* w, int64_t n, float* lw2, double* w64, cudaStream_t st);
 cudaError_t launch_softmin_hd(const Group& g, int d, int n_sm, cudaStream_t st);
+// per-scale column constants of a high-D problem into `out` (hd_padded(n_cols))
+cudaError_t hd_colconst(const Problem& P, float* out, cudaStream_t st);
 cudaError_t launch_fallback_hd(const Group& g, int d, int n_sm, cudaStream_t st);
 
 // label transfer (labels.cu, K9)

@@ -9,18 +9,21 @@
 // Precision: a single TF32/F16 product has ~2^-11 relative error, i.e. an
 // error of ~0.5 in E at blur 0.03 — far outside the 1e-3 eps tolerance.  Each
 // coordinate (centred, x 2^6) is split x = hi + lo into two float16s and the
-// MMA computes hi.hi + hi.lo + lo.hi (relative error ~2^-22) as ONE K = 192
-// GEMM: A = [hi | hi | lo], B = [hi | lo | hi], three 64-wide K chunks.
+// MMA computes hi.hi + hi.lo + lo.hi (relative error ~2^-22): three K = 64
+// products into one accumulator.  Every atom is packed once as [hi | lo]
+// (2 x 16 KB per 128 atoms) and serves as A (rows) or B (columns).
 //
 // Kernel (one CTA per work item = 256 rows x a run of 128-column blocks):
-//   warp 0      producer: cp.async.bulk (TMA) of pre-swizzled 16 KB blocks
-//               (A once, B per stage; 2 stages) onto mbarriers
-//   warp 1      TMEM owner + MMA issuer: per column block, 2 x 12
-//               tcgen05.mma.kind::f16 (M=128 halves, N=128, K=16 steps) into
-//               a double-buffered 2 x 256-column fp32 accumulator (512 cols)
-//   warps 4-11  epilogue (two warpgroups, one per M=128 half; one TMEM lane
-//               = one row per thread): tcgen05.ld 32x32b.x32, E = fma, MUFU
-//               ex2, running row sum; arrive on the TMEM-empty barrier
+//   warp 0      producer: cp.async.bulk (TMA) of the pre-swizzled operands
+//               (A once, B per stage, kHdStages stages) and of the block's
+//               128 column constants c_j (hd_colconst) into a 2-slot ring
+//   warp 1      TMEM owner + MMA issuer: per column block, 2 M-halves x 3
+//               products x 4 K-steps of tcgen05.mma.kind::f16 (M=128, N=128,
+//               K=16) into a double-buffered 2 x 256-column fp32 accumulator
+//   warps 2-17  epilogue, four warpgroups = 2 M-halves x 2 column halves;
+//               one TMEM lane = one row per thread: tcgen05.ld 32x32b.x32,
+//               E = k2 v + (c_j + r_i) on the packed FMA pipe, MUFU ex2,
+//               running row sum; arrive on the TMEM-empty barrier
 // Operands are K-major, 128-byte swizzled (SWIZZLE_128B, 1024-byte atoms):
 // 16-byte chunk q of row r sits at r*128 + ((q ^ (r & 7)) * 16).
 #include <cuda_fp16.h>
@@ -30,21 +33,27 @@
 namespace msot_dev {
 
 constexpr int kHdK = 64;                 // f16 per 128-byte row (one swizzle atom)
-constexpr int kHdChunks = 3;             // split products
+constexpr int kHdParts = 2;              // [hi | lo]
 constexpr int kHdBlockRows = 128;
 constexpr int kHdBlockBytes = kHdBlockRows * 128;            // 16 KB
-constexpr int kHdPackBytes = kHdChunks * kHdBlockBytes;      // 48 KB per 128 atoms
-constexpr int kHdStages = 2;
-constexpr int kHdThreads = 384;          // 12 warps
+constexpr int kHdPackBytes = kHdParts * kHdBlockBytes;       // 32 KB per 128 atoms
+constexpr int kHdStages = 3;
+constexpr int kHdEpiWarps = 16;
+constexpr int kHdThreads = 64 + 32 * kHdEpiWarps;  // producer, MMA, 16 epilogue warps
 constexpr float kHdScale = 64.f;         // coordinate scale before the f16 split
-constexpr size_t kHdSmem = 2 * kHdPackBytes + kHdStages * kHdPackBytes + 2 * 128 * 4 + 1024 + 256;
+constexpr size_t kHdSmem = 2 * kHdPackBytes + kHdStages * kHdPackBytes +  // A, B stages
+                           2 * 128 * 4 +                                  // column constants
+                           2 * kTileRows * 4 +                            // row partials
+                           1024 + 256;                                    // align, barriers
 
 // ---------------------------------------------------------------- packing --
-// One thread per (atom, 16-byte chunk): writes the chunk's 8 f16 of each of
-// the three K chunks.  role 0 = A (rows): [hi, hi, lo]; role 1 = B: [hi, lo, hi].
+// One thread per (atom, 16-byte chunk): writes the chunk's 8 f16 of the hi
+// and the lo part.  (`role` is kept for the call sites: A and B share the
+// layout.)
 __global__ void hd_pack_kernel(const double* x, int64_t n, int64_t npad, int d,
                                const double* center, int role, uint8_t* pack, float* sq,
                                float* xf) {
+  (void)role;
   const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (g >= npad * 8) return;
   const int64_t i = g >> 3;
@@ -68,9 +77,8 @@ __global__ void hd_pack_kernel(const double* x, int64_t n, int64_t npad, int d,
   const int r = static_cast<int>(i % kHdBlockRows);
   const int off = r * 128 + ((q ^ (r & 7)) * 16);
   uint8_t* base = pack + blk * kHdPackBytes;
-  const __half* src[3] = {hi, role == 0 ? hi : lo, role == 0 ? lo : hi};
-  for (int c = 0; c < kHdChunks; ++c)
-    *reinterpret_cast<uint4*>(base + c * kHdBlockBytes + off) = *reinterpret_cast<const uint4*>(src[c]);
+  *reinterpret_cast<uint4*>(base + off) = *reinterpret_cast<const uint4*>(hi);
+  *reinterpret_cast<uint4*>(base + kHdBlockBytes + off) = *reinterpret_cast<const uint4*>(lo);
 }
 
 // Rows are padded to whole 256-row tiles (two A blocks per CTA), columns to
@@ -165,18 +173,28 @@ __device__ __forceinline__ void tmem_ld32(uint32_t addr, float* v) {
 // instruction descriptor: F16 x F16 -> F32, K-major A and B, M = 128, N = 128
 constexpr uint32_t kHdIdesc = (1u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
 
+__device__ __forceinline__ void named_bar(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 // ---------------------------------------------------------------- kernel --
 __global__ void __launch_bounds__(kHdThreads, 1)
 softmin_hd_kernel(const __grid_constant__ Group G) {
   extern __shared__ __align__(1024) uint8_t hd_smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(hd_smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint8_t* sA = smem;                                   // 2 halves x 48 KB
-  uint8_t* sB = smem + 2 * kHdPackBytes;                // 2 stages x 48 KB
-  float* cval = reinterpret_cast<float*>(sB + kHdStages * kHdPackBytes);  // [2][128]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(cval + 2 * 128);
-  // bars: 0 fullA, 1-2 fullB, 3-4 emptyB, 5-6 tmemFull, 7-8 tmemEmpty
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+  uint8_t* sA = smem;                                   // 2 halves x 32 KB
+  uint8_t* sB = smem + 2 * kHdPackBytes;                // kHdStages x 32 KB
+  float* cring = reinterpret_cast<float*>(sB + kHdStages * kHdPackBytes);  // [2][128]
+  float* rowacc = cring + 2 * 128;                                          // [2][256]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rowacc + 2 * kTileRows);
+  // bars: 0 fullA | 1.. fullB[S] | emptyB[S] | tmemFull[2] | tmemEmpty[2] | cFull[2]
+  uint64_t* fullB = bars + 1;
+  uint64_t* emptyB = fullB + kHdStages;
+  uint64_t* tmemFull = emptyB + kHdStages;
+  uint64_t* tmemEmpty = tmemFull + 2;
+  uint64_t* cFull = tmemEmpty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cFull + 2);
 
   const int it = blockIdx.x;
   if (it >= G.n_items) return;
@@ -191,11 +209,14 @@ softmin_hd_kernel(const __grid_constant__ Group G) {
 
   if (threadIdx.x == 0) {
     mbar_init(smem_u32(&bars[0]), 1);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(smem_u32(&bars[1 + s]), 1);
-      mbar_init(smem_u32(&bars[3 + s]), 1);
-      mbar_init(smem_u32(&bars[5 + s]), 1);
-      mbar_init(smem_u32(&bars[7 + s]), 8);
+    for (int s = 0; s < kHdStages; ++s) {
+      mbar_init(smem_u32(&fullB[s]), 1);
+      mbar_init(smem_u32(&emptyB[s]), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&tmemFull[b]), 1);
+      mbar_init(smem_u32(&tmemEmpty[b]), kHdEpiWarps);
+      mbar_init(smem_u32(&cFull[b]), 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -221,13 +242,22 @@ softmin_hd_kernel(const __grid_constant__ Group G) {
         bulk_g2s(smem_u32(sA + kHdPackBytes), a0 + kHdPackBytes, kHdPackBytes, fa);
       }
       for (int t = 0; t < nblk; ++t) {
-        const int s = t & 1, n = t >> 1;
-        if (n > 0) mbar_wait(smem_u32(&bars[3 + s]), (n - 1) & 1);
+        const int s = t % kHdStages, ns = t / kHdStages, buf = t & 1;
+        if (ns > 0) mbar_wait(smem_u32(&emptyB[s]), (ns - 1) & 1);
         if (lane == 0) {
-          const uint32_t fb = smem_u32(&bars[1 + s]);
+          const uint32_t fb = smem_u32(&fullB[s]);
           mbar_expect_tx(fb, kHdPackBytes);
           bulk_g2s(smem_u32(sB + s * kHdPackBytes),
                    P.b_pack + static_cast<int64_t>(blk0 + t) * kHdPackBytes, kHdPackBytes, fb);
+        }
+        // column constants of block t into ring slot buf once the epilogue
+        // released it (block t - 2)
+        if (t >= 2) mbar_wait(smem_u32(&tmemEmpty[buf]), ((t >> 1) - 1) & 1);
+        if (lane == 0) {
+          const uint32_t fc = smem_u32(&cFull[buf]);
+          mbar_expect_tx(fc, 128 * 4);
+          bulk_g2s(smem_u32(cring + buf * 128), P.col_c + static_cast<int64_t>(blk0 + t) * 128,
+                   128 * 4, fc);
         }
         __syncwarp();
       }
@@ -237,70 +267,77 @@ softmin_hd_kernel(const __grid_constant__ Group G) {
     if (nblk > 0) {
       mbar_wait(smem_u32(&bars[0]), 0);
       for (int t = 0; t < nblk; ++t) {
-        const int s = t & 1, n = t >> 1, buf = t & 1;
-        mbar_wait(smem_u32(&bars[1 + s]), n & 1);
-        if (n > 0) mbar_wait(smem_u32(&bars[7 + buf]), (n - 1) & 1);
+        const int s = t % kHdStages, ns = t / kHdStages, buf = t & 1;
+        mbar_wait(smem_u32(&fullB[s]), ns & 1);
+        if (t >= 2) mbar_wait(smem_u32(&tmemEmpty[buf]), ((t >> 1) - 1) & 1);
         tc_fence_after();
         if (lane == 0) {
+          const uint32_t b_hi = smem_u32(sB + s * kHdPackBytes);
+          const uint32_t b_lo = b_hi + kHdBlockBytes;
           for (int h = 0; h < 2; ++h) {
             const uint32_t d = tmem + buf * 256 + h * 128;
-            for (int c = 0; c < kHdChunks; ++c)
-              for (int k = 0; k < kHdK / 16; ++k) {
-                const uint32_t ao = smem_u32(sA + h * kHdPackBytes + c * kHdBlockBytes) + k * 32;
-                const uint32_t bo = smem_u32(sB + s * kHdPackBytes + c * kHdBlockBytes) + k * 32;
-                umma_f16(d, umma_desc(ao), umma_desc(bo), kHdIdesc, (c | k) ? 1u : 0u);
-              }
+            const uint32_t a_hi = smem_u32(sA + h * kHdPackBytes);
+            const uint32_t a_lo = a_hi + kHdBlockBytes;
+            const uint32_t as[3] = {a_hi, a_hi, a_lo}, bs[3] = {b_hi, b_lo, b_hi};
+            for (int c = 0; c < 3; ++c)
+              for (int k = 0; k < kHdK / 16; ++k)
+                umma_f16(d, umma_desc(as[c] + k * 32), umma_desc(bs[c] + k * 32), kHdIdesc,
+                         (c | k) ? 1u : 0u);
           }
-          umma_commit(smem_u32(&bars[3 + s]));    // smem stage free
-          umma_commit(smem_u32(&bars[5 + buf]));  // accumulator ready
+          umma_commit(smem_u32(&emptyB[s]));     // smem stage free
+          umma_commit(smem_u32(&tmemFull[buf]));  // accumulator ready
         }
         __syncwarp();
       }
     }
-  } else if (warp >= 4) {
+  } else {
     // ----------------------------------------------------------- epilogue
-    const int e = threadIdx.x - 128;          // 0..255
-    const int g = (warp - 4) >> 2;            // M half
-    const int q = warp & 3;                   // TMEM lane quarter
-    const int lr = g * 128 + q * 32 + lane;   // local row
+    const int e = warp - 2;                   // 0..15
+    const int q = warp & 3;                   // TMEM lane quarter (hardware: warp % 4)
+    const int h = (e >> 2) & 1;               // M half
+    const int ch = e >> 3;                    // column half of the 128-column block
+    const int lr = h * 128 + q * 32 + lane;   // local row
     const int row = row_base + lr;
     const bool rvalid = row < P.tile_start[item.y + 1];
     const float est = (P.row_est && rvalid) ? P.row_est[row] : 0.f;
     const float xsq = rvalid ? P.row_sq[row] : 0.f;
-    const float r = est * P.inv_lam_eps_ln2 - 0.5f * xsq * P.inv_eps_ln2;
+    const float r = rvalid ? est * P.inv_lam_eps_ln2 - 0.5f * xsq * P.inv_eps_ln2
+                           : __int_as_float(0xff800000);
     const float k2 = P.inv_eps_ln2 * (1.f / (kHdScale * kHdScale));
-    float s = 0.f, s2 = 0.f;
+    const float2 K2 = make_float2(k2, k2), RR = make_float2(r, r);
+    float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
     for (int t = 0; t < nblk; ++t) {
       const int buf = t & 1, n = t >> 1;
-      if (e < 128) {
-        const int j = (blk0 + t) * kHdBlockRows + e;
-        float cj = __int_as_float(0xff800000);  // -inf: padding column
-        if (j < P.n_cols)
-          cj = P.col_lw2[j] + (P.col_h[j] - 0.5f * P.col_sq[j]) * P.inv_eps_ln2;
-        cval[buf * 128 + e] = cj;
-      }
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      mbar_wait(smem_u32(&bars[5 + buf]), n & 1);
+      mbar_wait(smem_u32(&cFull[buf]), n & 1);
+      mbar_wait(smem_u32(&tmemFull[buf]), n & 1);
       tc_fence_after();
-      const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + buf * 256 + g * 128;
-      const float* cv = cval + buf * 128;
+      const uint32_t base =
+          tmem + (static_cast<uint32_t>(q * 32) << 16) + buf * 256 + h * 128 + ch * 64;
+      const float4* cv = reinterpret_cast<const float4*>(cring + buf * 128 + ch * 64);
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         float v[32];
         tmem_ld32(base + c * 32, v);
 #pragma unroll
-        for (int k = 0; k < 32; k += 2) {
-          const float e0 = fmaf(k2, v[k], cv[c * 32 + k] + r);
-          const float e1 = fmaf(k2, v[k + 1], cv[c * 32 + k + 1] + r);
-          s += ex2_approx(e0);
-          s2 += ex2_approx(e1);
+        for (int k = 0; k < 32; k += 4) {
+          const float4 cc = cv[(c * 32 + k) >> 2];
+          const float2 e0 = __ffma2_rn(K2, make_float2(v[k], v[k + 1]),
+                                       __fadd2_rn(make_float2(cc.x, cc.y), RR));
+          const float2 e1 = __ffma2_rn(K2, make_float2(v[k + 2], v[k + 3]),
+                                       __fadd2_rn(make_float2(cc.z, cc.w), RR));
+          s0 = __fadd2_rn(s0, make_float2(ex2_approx(e0.x), ex2_approx(e0.y)));
+          s1 = __fadd2_rn(s1, make_float2(ex2_approx(e1.x), ex2_approx(e1.y)));
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&bars[7 + buf]));
+      if (lane == 0) mbar_arrive(smem_u32(&tmemEmpty[buf]));
     }
-    G.part[static_cast<int64_t>(it) * kTileRows + lr] = s + s2;
+    // the two column halves of a row: fixed order ch 0 + ch 1
+    rowacc[ch * kTileRows + lr] = (s0.x + s0.y) + (s1.x + s1.y);
+    named_bar(1, 32 * kHdEpiWarps);
+    if (ch == 0)
+      G.part[static_cast<int64_t>(it) * kTileRows + lr] = rowacc[lr] + rowacc[kTileRows + lr];
   }
   tc_fence_before();
   __syncthreads();
@@ -308,6 +345,23 @@ softmin_hd_kernel(const __grid_constant__ Group G) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
+}
+
+// Column constants of one problem (per scale): c_j = log2 w_j + (h_j - |y_j|^2
+// / 2) / (eps ln2), -inf for padding columns up to the 128-column block.
+__global__ void hd_colconst_kernel(const float* lw2, const float* h, const float* sq, float inv,
+                                   int32_t n, int32_t npad, float* out) {
+  const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= npad) return;
+  out[j] = j < n ? lw2[j] + (h[j] - 0.5f * sq[j]) * inv : __int_as_float(0xff800000);
+}
+
+cudaError_t hd_colconst(const Problem& P, float* out, cudaStream_t st) {
+  const int32_t npad = static_cast<int32_t>(hd_padded(P.n_cols));
+  ++g_launches;
+  hd_colconst_kernel<<<(npad + 255) / 256, 256, 0, st>>>(P.col_lw2, P.col_h, P.col_sq,
+                                                         P.inv_eps_ln2, P.n_cols, npad, out);
+  return cudaGetLastError();
 }
 
 // Exact online-max LSE for rows the fixed-reference path rejected (float32,

@@ -504,6 +504,12 @@ void run_group(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& ss) {
     CK(cudaEventRecord(e0, st));
   }
   const bool hd = ss.d > 3;
+  if (hd)
+    for (int p = 0; p < P.np; ++p) {
+      float* cc = c->buf<float>("hd.c" + std::to_string(p), hd_padded(G.P[p].n_cols));
+      CK(hd_colconst(G.P[p], cc, st));
+      G.P[p].col_c = cc;
+    }
   CK(hd ? launch_softmin_hd(G, ss.d, c->n_sm, st) : launch_softmin(G, ss.d, st));
   if (c->profiling) CK(cudaEventRecord(e1, st));
   CK(launch_finalize(G, st));
@@ -870,6 +876,11 @@ void transfer_labels_dev(msot_ctx* c, const LabelReq& q, const DMeasure& X, cons
   G.n_items = static_cast<int32_t>(items.size());
   G.part = c->buf<float>("lab.part", items.size() * kTileRows);
   G.tile_prefix[1] = static_cast<int32_t>(T);
+  if (hd) {
+    float* cc = c->buf<float>("lab.c", hd_padded(mpad));
+    CK(hd_colconst(Q, cc, st));
+    Q.col_c = cc;
+  }
   CK(hd ? launch_softmin_hd(G, d, c->n_sm, st) : launch_softmin(G, d, st));
   CK(label_finalize(G.part, dlbase, R.tile_start, T, L, hd ? nullptr : X.perm, q.d_scores,
                     q.d_mass, st));
@@ -941,18 +952,17 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
     for (int k = 0; k < d; ++k) center[k] = 0.5 * (lo[k] + hi[k]);
     double* dcen = c->buf<double>("hd.center", d);
     CK(cudaMemcpyAsync(dcen, center.data(), d * sizeof(double), cudaMemcpyHostToDevice, st));
+    // one [hi | lo] pack per measure serves as A (rows) and B (columns)
     uint8_t* ax = c->buf<uint8_t>("hd.ax", hd_pack_bytes(n));
-    uint8_t* bx = c->buf<uint8_t>("hd.bx", hd_pack_bytes(n));
     uint8_t* ay = c->buf<uint8_t>("hd.ay", hd_pack_bytes(m));
-    uint8_t* by = c->buf<uint8_t>("hd.by", hd_pack_bytes(m));
+    uint8_t* bx = ax;
+    uint8_t* by = ay;
     float* sqx = c->buf<float>("hd.sqx", n);
     float* sqy = c->buf<float>("hd.sqy", m);
     float* fx = c->buf<float>("hd.fx", hd_padded(n) * 64);
     float* fy = c->buf<float>("hd.fy", hd_padded(m) * 64);
     CK(hd_pack(d_x, n, d, dcen, 0, ax, sqx, fx, st));
-    CK(hd_pack(d_x, n, d, dcen, 1, bx, nullptr, nullptr, st));
     CK(hd_pack(d_y, m, d, dcen, 0, ay, sqy, fy, st));
-    CK(hd_pack(d_y, m, d, dcen, 1, by, nullptr, nullptr, st));
     hd_cen = dcen;
     hd_ax = ax;
     hd_sqx = sqx;

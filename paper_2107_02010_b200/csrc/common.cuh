@@ -43,6 +43,7 @@ struct Problem {
   const float* row_sq;       // |x_i|^2 (float32 coordinates)
   const float* col_sq;       // |y_j|^2
   const float* col_c;        // per-scale column constants (hd_colconst)
+  const float* col_c2;       // evaluate-once: column factor exponents (hd_colconst)
   const float* row_f;        // float32 coordinates, row-major x 64 (exact fallback)
   const float* col_f;
   // evaluate-once (symmetric) groups (softmin_sym.cu)

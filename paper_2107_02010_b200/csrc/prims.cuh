@@ -67,9 +67,13 @@ size_t hd_pack_bytes(int64_t n);
 cudaError_t hd_pack(const double* x, int64_t n, int d, const double* center, int role,
                     uint8_t* pack, float* sq, float* xf, cudaStream_t st);
 cudaError_t hd_weights(const double* w, int64_t n, float* lw2, double* w64, cudaStream_t st);
-cudaError_t launch_softmin_hd(const Group& g, int d, int n_sm, cudaStream_t st);
-// per-scale column constants of a high-D problem into `out` (hd_padded(n_cols))
-cudaError_t hd_colconst(const Problem& P, float* out, cudaStream_t st);
+// sym: evaluate-once (column partials into P.colpart)
+cudaError_t launch_softmin_hd(const Group& g, int d, int n_sm, bool sym, cudaStream_t st);
+// per-scale column constants of a high-D problem into `out` (hd_padded(n_cols));
+// out2 (nullable): column factor exponents of evaluate-once groups
+cudaError_t hd_colconst(const Problem& P, float* out, float* out2, cudaStream_t st);
+cudaError_t hd_colsum(const float* colpart, const int64_t* tslot, const int32_t* ts, int32_t t0,
+                      int32_t t1, int self, int32_t n_cols, float* tot, cudaStream_t st);
 cudaError_t launch_fallback_hd(const Group& g, int d, int n_sm, cudaStream_t st);
 
 // label transfer (labels.cu, K9)

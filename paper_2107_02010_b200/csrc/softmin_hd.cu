@@ -37,14 +37,27 @@ constexpr int kHdParts = 2;              // [hi | lo]
 constexpr int kHdBlockRows = 128;
 constexpr int kHdBlockBytes = kHdBlockRows * 128;            // 16 KB
 constexpr int kHdPackBytes = kHdParts * kHdBlockBytes;       // 32 KB per 128 atoms
-constexpr int kHdStages = 3;
 constexpr int kHdEpiWarps = 16;
 constexpr int kHdThreads = 64 + 32 * kHdEpiWarps;  // producer, MMA, 16 epilogue warps
 constexpr float kHdScale = 64.f;         // coordinate scale before the f16 split
-constexpr size_t kHdSmem = 2 * kHdPackBytes + kHdStages * kHdPackBytes +  // A, B stages
-                           2 * 128 * 4 +                                  // column constants
-                           2 * kTileRows * 4 +                            // row partials
-                           1024 + 256;                                    // align, barriers
+
+// Shared memory plan.  kSym (evaluate-once) adds a 4 KB per-warp transpose
+// area and the cross-warp column accumulators, and keeps 2 B stages.
+template <bool kSym>
+struct HdSmem {
+  static constexpr int kStages = kSym ? 2 : 3;
+  static constexpr int kRing = kSym ? 256 : 128;  // floats per ring slot: c_j (+ column factors)
+  static constexpr size_t kA = 0;
+  static constexpr size_t kB = kA + 2 * kHdPackBytes;
+  static constexpr size_t kStage = kB + kStages * kHdPackBytes;            // [16 warps][32][32] f32
+  static constexpr size_t kColAcc = kStage + (kSym ? kHdEpiWarps * 4096 : 0);  // [2 buf][4 cq][4 q][32]
+  static constexpr size_t kRingOff = kColAcc + (kSym ? 2 * 4 * 4 * 32 * 4 : 0);
+  static constexpr size_t kRowAcc = kRingOff + 2 * kRing * 4;              // [4 cq][256]
+  static constexpr size_t kBars = kRowAcc + 4 * kTileRows * 4;
+  static constexpr size_t kTotal = kBars + 256 + 1024;                    // barriers, alignment
+};
+static_assert(HdSmem<true>::kTotal <= 227 * 1024, "shared memory");
+static_assert(HdSmem<false>::kTotal <= 227 * 1024, "shared memory");
 
 // ---------------------------------------------------------------- packing --
 // One thread per (atom, 16-byte chunk): writes the chunk's 8 f16 of the hi
@@ -170,6 +183,20 @@ __device__ __forceinline__ void tmem_ld32(uint32_t addr, float* v) {
   for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(r[k]);
 }
 
+__device__ __forceinline__ void tmem_ld16(uint32_t addr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(r[k]);
+}
+
 // instruction descriptor: F16 x F16 -> F32, K-major A and B, M = 128, N = 128
 constexpr uint32_t kHdIdesc = (1u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
 
@@ -178,23 +205,35 @@ __device__ __forceinline__ void named_bar(int id, int count) {
 }
 
 // ---------------------------------------------------------------- kernel --
+// kSym: evaluate-once (softmin_sym.cu's scheme on the dense high-D problems):
+// every exponential also feeds its column.  Per 32 columns a warp stages its
+// 32 x 32 block through shared memory (16-byte chunks XOR-swizzled by row),
+// each lane sums 8 rows x 4 columns, two shuffle levels finish the warp's
+// column sums, and after the block the 8 warps of a column half combine in
+// a fixed order into colpart[tile slot + position] (column factor applied).
+template <bool kSym>
 __global__ void __launch_bounds__(kHdThreads, 1)
 softmin_hd_kernel(const __grid_constant__ Group G) {
+  using L = HdSmem<kSym>;
   extern __shared__ __align__(1024) uint8_t hd_smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(hd_smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
-  uint8_t* sA = smem;                                   // 2 halves x 32 KB
-  uint8_t* sB = smem + 2 * kHdPackBytes;                // kHdStages x 32 KB
-  float* cring = reinterpret_cast<float*>(sB + kHdStages * kHdPackBytes);  // [2][128]
-  float* rowacc = cring + 2 * 128;                                          // [2][256]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(rowacc + 2 * kTileRows);
-  // bars: 0 fullA | 1.. fullB[S] | emptyB[S] | tmemFull[2] | tmemEmpty[2] | cFull[2]
+  // align to 1024 B by offsetting the shared array itself, so the compiler
+  // keeps every derived pointer in the shared window (LDS/STS, not generic)
+  uint8_t* smem = hd_smem_raw + ((1024u - (smem_u32(hd_smem_raw) & 1023u)) & 1023u);
+  uint8_t* sA = smem + L::kA;
+  uint8_t* sB = smem + L::kB;
+  float* stage_all = reinterpret_cast<float*>(smem + L::kStage);
+  float* colacc = reinterpret_cast<float*>(smem + L::kColAcc);
+  float* cring = reinterpret_cast<float*>(smem + L::kRingOff);
+  float* rowacc = reinterpret_cast<float*>(smem + L::kRowAcc);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBars);
+  // bars: 0 fullA | fullB[S] | emptyB[S] | tmemFull[2] | tmemEmpty[2] | cFull[2] | colFull[2][4]
   uint64_t* fullB = bars + 1;
-  uint64_t* emptyB = fullB + kHdStages;
-  uint64_t* tmemFull = emptyB + kHdStages;
+  uint64_t* emptyB = fullB + L::kStages;
+  uint64_t* tmemFull = emptyB + L::kStages;
   uint64_t* tmemEmpty = tmemFull + 2;
   uint64_t* cFull = tmemEmpty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cFull + 2);
+  uint64_t* colFull = cFull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(colFull + 8);
 
   const int it = blockIdx.x;
   if (it >= G.n_items) return;
@@ -202,14 +241,16 @@ softmin_hd_kernel(const __grid_constant__ Group G) {
   const Problem& P = G.P[item.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row_base = P.tile_start[item.y];
-  // column blocks owned by this item: those whose first column is in [z, w)
-  const int blk0 = (item.z + kHdBlockRows - 1) / kHdBlockRows;
-  const int blk1 = (item.w + kHdBlockRows - 1) / kHdBlockRows;
+  // column blocks of this item: positions [z, w) of the tile's (single,
+  // dense) column range, in whole 128-column blocks
+  const int col0 = P.ranges[P.tile_rptr[item.y]].x;  // 0, or the tile start (self, kSym)
+  const int blk0 = (col0 + item.z + kHdBlockRows - 1) / kHdBlockRows;
+  const int blk1 = (col0 + item.w + kHdBlockRows - 1) / kHdBlockRows;
   const int nblk = blk1 - blk0;
 
   if (threadIdx.x == 0) {
     mbar_init(smem_u32(&bars[0]), 1);
-    for (int s = 0; s < kHdStages; ++s) {
+    for (int s = 0; s < L::kStages; ++s) {
       mbar_init(smem_u32(&fullB[s]), 1);
       mbar_init(smem_u32(&emptyB[s]), 1);
     }
@@ -217,6 +258,7 @@ softmin_hd_kernel(const __grid_constant__ Group G) {
       mbar_init(smem_u32(&tmemFull[b]), 1);
       mbar_init(smem_u32(&tmemEmpty[b]), kHdEpiWarps);
       mbar_init(smem_u32(&cFull[b]), 1);
+      for (int k = 0; k < 4; ++k) mbar_init(smem_u32(&colFull[b * 4 + k]), 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -242,7 +284,7 @@ softmin_hd_kernel(const __grid_constant__ Group G) {
         bulk_g2s(smem_u32(sA + kHdPackBytes), a0 + kHdPackBytes, kHdPackBytes, fa);
       }
       for (int t = 0; t < nblk; ++t) {
-        const int s = t % kHdStages, ns = t / kHdStages, buf = t & 1;
+        const int s = t % L::kStages, ns = t / L::kStages, buf = t & 1;
         if (ns > 0) mbar_wait(smem_u32(&emptyB[s]), (ns - 1) & 1);
         if (lane == 0) {
           const uint32_t fb = smem_u32(&fullB[s]);
@@ -250,14 +292,17 @@ softmin_hd_kernel(const __grid_constant__ Group G) {
           bulk_g2s(smem_u32(sB + s * kHdPackBytes),
                    P.b_pack + static_cast<int64_t>(blk0 + t) * kHdPackBytes, kHdPackBytes, fb);
         }
-        // column constants of block t into ring slot buf once the epilogue
-        // released it (block t - 2)
+        // column constants (and factors) of block t into ring slot buf once
+        // the epilogue released it (block t - 2)
         if (t >= 2) mbar_wait(smem_u32(&tmemEmpty[buf]), ((t >> 1) - 1) & 1);
         if (lane == 0) {
           const uint32_t fc = smem_u32(&cFull[buf]);
-          mbar_expect_tx(fc, 128 * 4);
-          bulk_g2s(smem_u32(cring + buf * 128), P.col_c + static_cast<int64_t>(blk0 + t) * 128,
-                   128 * 4, fc);
+          mbar_expect_tx(fc, L::kRing * 4);
+          float* slot = cring + buf * L::kRing;
+          bulk_g2s(smem_u32(slot), P.col_c + static_cast<int64_t>(blk0 + t) * 128, 128 * 4, fc);
+          if (kSym)
+            bulk_g2s(smem_u32(slot + 128), P.col_c2 + static_cast<int64_t>(blk0 + t) * 128,
+                     128 * 4, fc);
         }
         __syncwarp();
       }
@@ -267,7 +312,7 @@ softmin_hd_kernel(const __grid_constant__ Group G) {
     if (nblk > 0) {
       mbar_wait(smem_u32(&bars[0]), 0);
       for (int t = 0; t < nblk; ++t) {
-        const int s = t % kHdStages, ns = t / kHdStages, buf = t & 1;
+        const int s = t % L::kStages, ns = t / L::kStages, buf = t & 1;
         mbar_wait(smem_u32(&fullB[s]), ns & 1);
         if (t >= 2) mbar_wait(smem_u32(&tmemEmpty[buf]), ((t >> 1) - 1) & 1);
         tc_fence_after();
@@ -292,52 +337,135 @@ softmin_hd_kernel(const __grid_constant__ Group G) {
     }
   } else {
     // ----------------------------------------------------------- epilogue
+    // warp = (TMEM lane quarter q, column quarter cq): rows q*32 + lane of
+    // both M halves (two TMEM loads of the same lanes), 32 columns per block
     const int e = warp - 2;                   // 0..15
     const int q = warp & 3;                   // TMEM lane quarter (hardware: warp % 4)
-    const int h = (e >> 2) & 1;               // M half
-    const int ch = e >> 3;                    // column half of the 128-column block
-    const int lr = h * 128 + q * 32 + lane;   // local row
-    const int row = row_base + lr;
-    const bool rvalid = row < P.tile_start[item.y + 1];
-    const float est = (P.row_est && rvalid) ? P.row_est[row] : 0.f;
-    const float xsq = rvalid ? P.row_sq[row] : 0.f;
-    const float r = rvalid ? est * P.inv_lam_eps_ln2 - 0.5f * xsq * P.inv_eps_ln2
-                           : __int_as_float(0xff800000);
+    const int cq = e >> 2;                    // column quarter of the 128-column block
+    const int row_end = P.tile_start[item.y + 1];
+    const int lr0 = q * 32 + lane, lr1 = 128 + lr0;  // local rows
     const float k2 = P.inv_eps_ln2 * (1.f / (kHdScale * kHdScale));
-    const float2 K2 = make_float2(k2, k2), RR = make_float2(r, r);
+    const int mid = (row_base + row_end) >> 1;
+    const float est_mid = (kSym && P.row_est) ? P.row_est[mid] : 0.f;
+    float rr[2], wr[2];
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int row = row_base + (hh ? lr1 : lr0);
+      const bool ok = row < row_end;
+      const float est = (P.row_est && ok) ? P.row_est[row] : 0.f;
+      const float xsq = ok ? P.row_sq[row] : 0.f;
+      rr[hh] = ok ? est * P.inv_lam_eps_ln2 - 0.5f * xsq * P.inv_eps_ln2
+                  : __int_as_float(0xff800000);
+      // evaluate-once: column-sum row factor a_i 2^{-ell (est_i - est_mid)}
+      wr[hh] = (kSym && ok) ? exp2f(P.row_lw2[row] - P.ell * (est - est_mid)) : 0.f;
+    }
+    const float2 K2 = make_float2(k2, k2);
+    const float2 R0 = make_float2(rr[0], rr[0]), R1 = make_float2(rr[1], rr[1]);
+    const float2 W0 = make_float2(wr[0], wr[0]), W1 = make_float2(wr[1], wr[1]);
+    float* stg = stage_all + e * 1024;        // this warp's 32 x 32 transpose area
     float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
     for (int t = 0; t < nblk; ++t) {
       const int buf = t & 1, n = t >> 1;
       mbar_wait(smem_u32(&cFull[buf]), n & 1);
       mbar_wait(smem_u32(&tmemFull[buf]), n & 1);
       tc_fence_after();
-      const uint32_t base =
-          tmem + (static_cast<uint32_t>(q * 32) << 16) + buf * 256 + h * 128 + ch * 64;
-      const float4* cv = reinterpret_cast<const float4*>(cring + buf * 128 + ch * 64);
-#pragma unroll 1
-      for (int c = 0; c < 2; ++c) {
-        float v[32];
-        tmem_ld32(base + c * 32, v);
+      const uint32_t base = tmem + (static_cast<uint32_t>(q * 32) << 16) + buf * 256 + cq * 32;
+      const float4* cv = reinterpret_cast<const float4*>(cring + buf * L::kRing + cq * 32);
 #pragma unroll
-        for (int k = 0; k < 32; k += 4) {
-          const float4 cc = cv[(c * 32 + k) >> 2];
-          const float2 e0 = __ffma2_rn(K2, make_float2(v[k], v[k + 1]),
-                                       __fadd2_rn(make_float2(cc.x, cc.y), RR));
-          const float2 e1 = __ffma2_rn(K2, make_float2(v[k + 2], v[k + 3]),
-                                       __fadd2_rn(make_float2(cc.z, cc.w), RR));
-          s0 = __fadd2_rn(s0, make_float2(ex2_approx(e0.x), ex2_approx(e0.y)));
-          s1 = __fadd2_rn(s1, make_float2(ex2_approx(e1.x), ex2_approx(e1.y)));
+      for (int sub = 0; sub < 2; ++sub) {  // 16 columns at a time (register budget: 18 warps)
+      float v0[16], v1[16];
+      tmem_ld16(base + sub * 16, v0);
+      tmem_ld16(base + 128 + sub * 16, v1);
+#pragma unroll
+      for (int kk = 0; kk < 16; kk += 4) {
+        const int k = sub * 16 + kk;
+        const float4 cc = cv[k >> 2];
+        const float2 ca = make_float2(cc.x, cc.y), cb = make_float2(cc.z, cc.w);
+        const float2 a0 = __ffma2_rn(K2, make_float2(v0[kk], v0[kk + 1]), __fadd2_rn(ca, R0));
+        const float2 b0 = __ffma2_rn(K2, make_float2(v0[kk + 2], v0[kk + 3]), __fadd2_rn(cb, R0));
+        const float2 a1 = __ffma2_rn(K2, make_float2(v1[kk], v1[kk + 1]), __fadd2_rn(ca, R1));
+        const float2 b1 = __ffma2_rn(K2, make_float2(v1[kk + 2], v1[kk + 3]), __fadd2_rn(cb, R1));
+        const float2 xa0 = make_float2(ex2_approx(a0.x), ex2_approx(a0.y));
+        const float2 xb0 = make_float2(ex2_approx(b0.x), ex2_approx(b0.y));
+        const float2 xa1 = make_float2(ex2_approx(a1.x), ex2_approx(a1.y));
+        const float2 xb1 = make_float2(ex2_approx(b1.x), ex2_approx(b1.y));
+        s0 = __fadd2_rn(s0, __fadd2_rn(xa0, xb0));
+        s1 = __fadd2_rn(s1, __fadd2_rn(xa1, xb1));
+        if (kSym) {  // both rows' weighted terms, chunk k/4 of this lane's staged row
+          const float2 ta = __ffma2_rn(W1, xa1, __fmul2_rn(W0, xa0));
+          const float2 tb = __ffma2_rn(W1, xb1, __fmul2_rn(W0, xb0));
+          *reinterpret_cast<float4*>(stg + lane * 32 + (((k >> 2) ^ (lane & 7)) << 2)) =
+              make_float4(ta.x, ta.y, tb.x, tb.y);
         }
       }
-      tc_fence_before();
+      }
+      if (!kSym) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&tmemEmpty[buf]));
+        continue;
+      }
+      tc_fence_before();  // TMEM reads of this block are done
+      // column sums of the warp's 64 rows: lane = chunk g = lane & 7 (columns
+      // 4g..4g+3) over staged rows (lane >> 3) + 4i, then lane bits 3, 4
+      {
+        const int g = lane & 7;
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int rw = (lane >> 3) + 4 * i;
+          const float4 b4 = *reinterpret_cast<const float4*>(stg + rw * 32 + ((g ^ (rw & 7)) << 2));
+          a.x += b4.x;
+          a.y += b4.y;
+          a.z += b4.z;
+          a.w += b4.w;
+        }
+        {
+          const bool up = lane & 8;
+          const float sx = up ? a.x : a.z, sy = up ? a.y : a.w;
+          const float kx = up ? a.z : a.x, ky = up ? a.w : a.y;
+          a.x = kx + __shfl_xor_sync(0xffffffffu, sx, 8);
+          a.y = ky + __shfl_xor_sync(0xffffffffu, sy, 8);
+        }
+        {
+          const bool up = lane & 16;
+          const float sx = up ? a.x : a.y, kx = up ? a.y : a.x;
+          a.x = kx + __shfl_xor_sync(0xffffffffu, sx, 16);
+        }
+        const int colw = 4 * g + ((lane >> 3) & 1) * 2 + ((lane >> 4) & 1);
+        colacc[((buf * 4 + cq) * 4 + q) * 32 + colw] = a.x;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&colFull[buf * 4 + cq]));
+      if (q == 0) {
+        // the column quarter's writer: waits for its 4 lane-quarter warps,
+        // combines in a fixed order, applies the column factor
+        // 2^{ell (h_j - est_mid) - log2 w_j} and writes the CTA partial.  It
+        // releases the TMEM/ring slot only afterwards, so no warp can reach
+        // block t + 2 (and overwrite colacc[buf] or the ring) before.
+        mbar_wait(smem_u32(&colFull[buf * 4 + cq]), n & 1);
+        const float fac = exp2f(cring[buf * L::kRing + 128 + cq * 32 + lane] - P.ell * est_mid);
+        const float* ca = colacc + (buf * 4 + cq) * 4 * 32 + lane;
+        const float sum = ((ca[0] + ca[32]) + ca[64]) + ca[96];
+        const int col = (blk0 + t) * kHdBlockRows + cq * 32 + lane;
+        if (col < P.n_cols) P.colpart[P.tile_slot[item.y] + (col - col0)] = sum * fac;
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&tmemEmpty[buf]));
     }
-    // the two column halves of a row: fixed order ch 0 + ch 1
-    rowacc[ch * kTileRows + lr] = (s0.x + s0.y) + (s1.x + s1.y);
+    // the four column quarters of a row: fixed order
+    rowacc[cq * kTileRows + lr0] = s0.x + s0.y;
+    rowacc[cq * kTileRows + lr1] = s1.x + s1.y;
     named_bar(1, 32 * kHdEpiWarps);
-    if (ch == 0)
-      G.part[static_cast<int64_t>(it) * kTileRows + lr] = rowacc[lr] + rowacc[kTileRows + lr];
+    if (cq == 0) {
+      float* out = G.part + static_cast<int64_t>(it) * kTileRows;
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int l = hh ? lr1 : lr0;
+        out[l] = ((rowacc[l] + rowacc[kTileRows + l]) + rowacc[2 * kTileRows + l]) +
+                 rowacc[3 * kTileRows + l];
+      }
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -348,19 +476,47 @@ softmin_hd_kernel(const __grid_constant__ Group G) {
 }
 
 // Column constants of one problem (per scale): c_j = log2 w_j + (h_j - |y_j|^2
-// / 2) / (eps ln2), -inf for padding columns up to the 128-column block.
+// / 2) / (eps ln2), -inf for padding columns up to the 128-column block; and,
+// for evaluate-once groups (c2 != null), the column factors' exponent
+// c2_j = ell h_j - log2 w_j.
 __global__ void hd_colconst_kernel(const float* lw2, const float* h, const float* sq, float inv,
-                                   int32_t n, int32_t npad, float* out) {
+                                   float ell, int32_t n, int32_t npad, float* out, float* out2) {
   const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= npad) return;
   out[j] = j < n ? lw2[j] + (h[j] - 0.5f * sq[j]) * inv : __int_as_float(0xff800000);
+  if (out2) out2[j] = j < n ? ell * h[j] - lw2[j] : 0.f;
 }
 
-cudaError_t hd_colconst(const Problem& P, float* out, cudaStream_t st) {
+cudaError_t hd_colconst(const Problem& P, float* out, float* out2, cudaStream_t st) {
   const int32_t npad = static_cast<int32_t>(hd_padded(P.n_cols));
   ++g_launches;
   hd_colconst_kernel<<<(npad + 255) / 256, 256, 0, st>>>(P.col_lw2, P.col_h, P.col_sq,
-                                                         P.inv_eps_ln2, P.n_cols, npad, out);
+                                                         P.inv_eps_ln2, P.ell, P.n_cols, npad,
+                                                         out, out2);
+  return cudaGetLastError();
+}
+
+// Column totals of a dense evaluate-once problem: column j sums the partial
+// of every row tile of [t0, t1) that owns it (self: tiles ending at or
+// before j), in tile order, float64.
+__global__ void hd_colsum_kernel(const float* colpart, const int64_t* tslot, const int32_t* ts,
+                                 int32_t t0, int32_t t1, int self, int32_t n_cols, float* tot) {
+  const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n_cols) return;
+  double s = 0.0;
+  for (int32_t t = t0; t < t1; ++t) {
+    if (self && ts[t + 1] > j) break;
+    s += static_cast<double>(colpart[tslot[t] + (j - (self ? ts[t] : 0))]);
+  }
+  tot[j] = static_cast<float>(s);
+}
+
+cudaError_t hd_colsum(const float* colpart, const int64_t* tslot, const int32_t* ts, int32_t t0,
+                      int32_t t1, int self, int32_t n_cols, float* tot, cudaStream_t st) {
+  if (n_cols <= 0) return cudaSuccess;
+  ++g_launches;
+  hd_colsum_kernel<<<(n_cols + 255) / 256, 256, 0, st>>>(colpart, tslot, ts, t0, t1, self, n_cols,
+                                                         tot);
   return cudaGetLastError();
 }
 
@@ -417,18 +573,23 @@ cudaError_t hd_weights(const double* w, int64_t n, float* lw2, double* w64, cuda
   return cudaGetLastError();
 }
 
-cudaError_t launch_softmin_hd(const Group& g, int d, int n_sm, cudaStream_t st) {
+cudaError_t launch_softmin_hd(const Group& g, int d, int n_sm, bool sym, cudaStream_t st) {
   (void)d;
+  (void)n_sm;
   if (g.n_items <= 0) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(softmin_hd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(kHdSmem));
+    cudaFuncSetAttribute(softmin_hd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(HdSmem<false>::kTotal));
+    cudaFuncSetAttribute(softmin_hd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(HdSmem<true>::kTotal));
     attr = true;
   }
   ++g_launches;
-  softmin_hd_kernel<<<g.n_items, kHdThreads, kHdSmem, st>>>(g);
-  (void)n_sm;
+  if (sym)
+    softmin_hd_kernel<true><<<g.n_items, kHdThreads, HdSmem<true>::kTotal, st>>>(g);
+  else
+    softmin_hd_kernel<false><<<g.n_items, kHdThreads, HdSmem<false>::kTotal, st>>>(g);
   return cudaGetLastError();
 }
 

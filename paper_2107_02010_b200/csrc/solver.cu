@@ -337,6 +337,41 @@ void sym_rangeset(msot_ctx* c, const std::string& tag, const int32_t* rl,
   S.colpart = c->buf<float>(tag + ".colpart", S.slots);
 }
 
+// Dense evaluate-once pair sets (high-D path): uniform 256-row tiles; self
+// problems: tile t's list is [ts, n) (diagonal block, then the upper part
+// whose columns also get tile t's rows); cross: [0, n_cols).
+void dense_symset(msot_ctx* c, const std::string& tag, int64_t n_rows, int64_t n_cols, int self,
+                  SymSet& S) {
+  cudaStream_t st = c->st;
+  RangeSet& R = S.R;
+  S.self = self;
+  make_tiles(c, tag, n_rows, nullptr, R);
+  const int64_t T = R.n_tiles;
+  std::vector<int64_t> rptr(T + 1), tcols(T), tslot(T + 1, 0);
+  std::vector<int2> rg(T);
+  for (int64_t t = 0; t < T; ++t) {
+    rptr[t] = t;
+    const int32_t c0 = self ? R.tile_start_h[t] : 0;
+    rg[t] = make_int2(c0, static_cast<int32_t>(n_cols));
+    tcols[t] = n_cols - c0;
+    tslot[t + 1] = tslot[t] + tcols[t];
+  }
+  rptr[T] = T;
+  R.n_ranges = T;
+  R.rptr = c->buf<int64_t>(tag + ".rptr", T + 1);
+  R.ranges = c->buf<int2>(tag + ".ranges", T);
+  R.tile_cols = c->buf<int64_t>(tag + ".tcols", T);
+  S.tslot = c->buf<int64_t>(tag + ".tslot", T + 1);
+  CK(cudaMemcpyAsync(R.rptr, rptr.data(), (T + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(R.ranges, rg.data(), T * sizeof(int2), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(R.tile_cols, tcols.data(), T * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(S.tslot, tslot.data(), (T + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  R.tile_cols_h = tcols;
+  S.slots = tslot[T];
+  S.colpart = c->buf<float>(tag + ".colpart", S.slots);
+  CK(cudaStreamSynchronize(st));  // host vectors go out of scope
+}
+
 // ------------------------------------------------------------ launch plans
 struct HdOperands {  // high-dimensional path (softmin_hd.cu)
   const uint8_t* a_pack = nullptr;
@@ -507,10 +542,10 @@ void run_group(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& ss) {
   if (hd)
     for (int p = 0; p < P.np; ++p) {
       float* cc = c->buf<float>("hd.c" + std::to_string(p), hd_padded(G.P[p].n_cols));
-      CK(hd_colconst(G.P[p], cc, st));
+      CK(hd_colconst(G.P[p], cc, nullptr, st));
       G.P[p].col_c = cc;
     }
-  CK(hd ? launch_softmin_hd(G, ss.d, c->n_sm, st) : launch_softmin(G, ss.d, st));
+  CK(hd ? launch_softmin_hd(G, ss.d, c->n_sm, false, st) : launch_softmin(G, ss.d, st));
   if (c->profiling) CK(cudaEventRecord(e1, st));
   CK(launch_finalize(G, st));
   CK(hd ? launch_fallback_hd(G, ss.d, c->n_sm, st) : launch_fallback(G, ss.d, c->n_sm, st));
@@ -542,6 +577,7 @@ struct SymCols {
   const float* x_lw2;
   int64_t n, m;
   bool uniform;              // both measures have uniform weights
+  HdOperands hd3{};          // high-D operands of problem 3 (rows y, cols x)
 };
 
 void fill_problem(Problem& Q, const ProbSpec& S, const float* h, const float* est, float* out,
@@ -595,7 +631,7 @@ void run_group_sym(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& s
     G.tile_prefix[p + 1] = tiles_acc;
   }
   {
-    const ProbSpec T{X.yrows, X.m, X.xcols, X.x_lw2, X.n, nullptr};
+    const ProbSpec T{X.yrows, X.m, X.xcols, X.x_lw2, X.n, nullptr, X.hd3};
     fill_problem(G.P[3], T, a.h[3], a.est[3], a.out[3], a.eps, a.lam, a.mixw);
     G.P[3].row_add = X.tot[2];
   }
@@ -613,16 +649,38 @@ void run_group_sym(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& s
     c->ev_pair(&e0, &e1);
     CK(cudaEventRecord(e0, st));
   }
-  CK(launch_softmin_sym(G, ss.d, X.uniform && a.lam == 1.0, st));
-  if (c->profiling) CK(cudaEventRecord(e1, st));
-  ColSum cs[3];
-  for (int p = 0; p < 3; ++p) {
-    const SymSet& S = *P.ps[p].sym;
-    cs[p] = ColSum{X.labels[p], X.co[p], S.ebase, S.eslot, S.etile, S.R.tile_start, S.colpart,
-                   X.tot[p], static_cast<int32_t>(P.ps[p].n_cols), S.self,
-                   static_cast<int32_t>(P.t0[p]), static_cast<int32_t>(P.t1[p])};
+  const bool hd = ss.d > 3;
+  if (hd) {
+    for (int p = 0; p < 3; ++p) {
+      const size_t np = hd_padded(G.P[p].n_cols);
+      float* cc = c->buf<float>("hd.c" + std::to_string(p), np);
+      float* c2 = c->buf<float>("hd.cf" + std::to_string(p), np);
+      CK(hd_colconst(G.P[p], cc, c2, st));
+      G.P[p].col_c = cc;
+      G.P[p].col_c2 = c2;
+    }
+    CK(launch_softmin_hd(G, ss.d, c->n_sm, true, st));
+  } else {
+    CK(launch_softmin_sym(G, ss.d, X.uniform && a.lam == 1.0, st));
   }
-  CK(launch_colsum(cs, 3, st));
+  if (c->profiling) CK(cudaEventRecord(e1, st));
+  if (hd) {
+    for (int p = 0; p < 3; ++p) {
+      const SymSet& S = *P.ps[p].sym;
+      CK(hd_colsum(S.colpart, S.tslot, S.R.tile_start, static_cast<int32_t>(P.t0[p]),
+                   static_cast<int32_t>(P.t1[p]), S.self, static_cast<int32_t>(P.ps[p].n_cols),
+                   X.tot[p], st));
+    }
+  } else {
+    ColSum cs[3];
+    for (int p = 0; p < 3; ++p) {
+      const SymSet& S = *P.ps[p].sym;
+      cs[p] = ColSum{X.labels[p], X.co[p], S.ebase, S.eslot, S.etile, S.R.tile_start, S.colpart,
+                     X.tot[p], static_cast<int32_t>(P.ps[p].n_cols), S.self,
+                     static_cast<int32_t>(P.t0[p]), static_cast<int32_t>(P.t1[p])};
+    }
+    CK(launch_colsum(cs, 3, st));
+  }
   if (c->world > 1) {  // column sums of every rank's tiles (NCCL over NVLink)
     NK(ncclGroupStart());
     for (int p = 0; p < 3; ++p)
@@ -631,7 +689,7 @@ void run_group_sym(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& s
   }
   CK(launch_finalize(G, st));
   CK(launch_colfinal(G, 3, st));
-  CK(launch_fallback_dense(G, ss.d, c->n_sm, st));
+  CK(hd ? launch_fallback_hd(G, ss.d, c->n_sm, st) : launch_fallback_dense(G, ss.d, c->n_sm, st));
   ss.S->softmin_launches += 1;
   ss.S->pairs_evaluated += P.pairs_all;
   if (c->world > 1) {  // all-gather of the row-side potentials
@@ -878,10 +936,10 @@ void transfer_labels_dev(msot_ctx* c, const LabelReq& q, const DMeasure& X, cons
   G.tile_prefix[1] = static_cast<int32_t>(T);
   if (hd) {
     float* cc = c->buf<float>("lab.c", hd_padded(mpad));
-    CK(hd_colconst(Q, cc, st));
+    CK(hd_colconst(Q, cc, nullptr, st));
     Q.col_c = cc;
   }
-  CK(hd ? launch_softmin_hd(G, d, c->n_sm, st) : launch_softmin(G, d, st));
+  CK(hd ? launch_softmin_hd(G, d, c->n_sm, false, st) : launch_softmin(G, d, st));
   CK(label_finalize(G.part, dlbase, R.tile_start, T, L, hd ? nullptr : X.perm, q.d_scores,
                     q.d_mass, st));
   CK(cudaStreamSynchronize(st));  // host vectors above go out of scope
@@ -976,20 +1034,43 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
     CK(hd_weights(d_b, m, Y.lw2, Y.w64, st));
     c->mark(4);
     S->t_switch = 0;
-    dense_rangeset(c, "d.xx", n, n, fxx);
-    dense_rangeset(c, "d.yy", m, m, fyy);
-    dense_rangeset(c, "d.xy", m, n, fxy);
-    dense_rangeset(c, "d.yx", n, m, fyx);
     Plan P;
-    P.np = 4;
-    P.ps[0] = {nullptr, n, nullptr, X.lw2, n, &fxx, {ax, bx, sqx, sqx, fx, fx}};  // a_xx
-    P.ps[1] = {nullptr, m, nullptr, Y.lw2, m, &fyy, {ay, by, sqy, sqy, fy, fy}};  // b_yy
-    P.ps[2] = {nullptr, m, nullptr, X.lw2, n, &fxy, {ay, bx, sqy, sqx, fy, fx}};  // a_xy
-    P.ps[3] = {nullptr, n, nullptr, Y.lw2, m, &fyx, {ax, by, sqx, sqy, fx, fy}};  // b_yx
+    SymSet hxx, hyy, hyx;
+    SymCols hcol{};
+    const bool once = prm->pair_eval != 0;
+    if (once) {  // evaluate-once: a_xy from the column sums of the cross problem
+      dense_symset(c, "h.xx", n, n, 1, hxx);
+      dense_symset(c, "h.yy", m, m, 1, hyy);
+      dense_symset(c, "h.yx", n, m, 0, hyx);
+      P.np = 3;
+      P.ps[0] = {nullptr, n, nullptr, X.lw2, n, &hxx.R, {ax, bx, sqx, sqx, fx, fx}, &hxx, X.lw2};
+      P.ps[1] = {nullptr, m, nullptr, Y.lw2, m, &hyy.R, {ay, by, sqy, sqy, fy, fy}, &hyy, Y.lw2};
+      P.ps[2] = {nullptr, n, nullptr, Y.lw2, m, &hyx.R, {ax, by, sqx, sqy, fx, fy}, &hyx, X.lw2};
+      hcol.tot[0] = c->buf<float>("h.totx", n);
+      hcol.tot[1] = c->buf<float>("h.toty", m);
+      hcol.tot[2] = c->buf<float>("h.totxy", m);
+      hcol.x_lw2 = X.lw2;
+      hcol.n = n;
+      hcol.m = m;
+      hcol.hd3 = {ay, bx, sqy, sqx, fy, fx};  // a_xy: rows y, cols x
+    } else {
+      dense_rangeset(c, "d.xx", n, n, fxx);
+      dense_rangeset(c, "d.yy", m, m, fyy);
+      dense_rangeset(c, "d.xy", m, n, fxy);
+      dense_rangeset(c, "d.yx", n, m, fyx);
+      P.np = 4;
+      P.ps[0] = {nullptr, n, nullptr, X.lw2, n, &fxx, {ax, bx, sqx, sqx, fx, fx}};  // a_xx
+      P.ps[1] = {nullptr, m, nullptr, Y.lw2, m, &fyy, {ay, by, sqy, sqy, fy, fy}};  // b_yy
+      P.ps[2] = {nullptr, m, nullptr, X.lw2, n, &fxy, {ay, bx, sqy, sqx, fy, fx}};  // a_xy
+      P.ps[3] = {nullptr, n, nullptr, Y.lw2, m, &fyx, {ax, by, sqx, sqy, fx, fy}};  // b_yx
+    }
     build_plan(c, "ph", P);
     for (int t = 0; t <= ns; ++t) {
       const int tt = std::min(t, ns - 1);
-      sym_step(c, P, U, cur, eps[tt], lam[tt], t == ns, ss);
+      if (once)
+        sym_step_once(c, P, U, cur, eps[tt], lam[tt], t == ns, ss, hcol);
+      else
+        sym_step(c, P, U, cur, eps[tt], lam[tt], t == ns, ss);
       S->pairs_dense += full;
     }
   } else {

@@ -91,6 +91,9 @@ typedef struct msot_stats {
    * items, 4 symmetric updates at full resolution, 5 loss and outputs,
    * 6 label transfer */
   double  phase_ms[8];
+  double  pairs_terms;      /* LSE terms summed over all potentials: a pair evaluated
+                               once for its row and its column counts twice (what a
+                               row-wise CPU solver evaluates for the same solve)  */
 } msot_stats;
 
 typedef struct msot_ctx msot_ctx;

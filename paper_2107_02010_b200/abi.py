@@ -61,6 +61,7 @@ class Stats(C.Structure):
         ("rank", C.c_int32),
         ("world", C.c_int32),
         ("phase_ms", C.c_double * 8),
+        ("pairs_terms", C.c_double),
     ]
 
     PHASES = ("setup", "coarse", "extrapolate", "masks", "updates", "loss", "labels")

@@ -12,6 +12,8 @@
 #include "../../include/msot/common.hpp"
 #include "../../include/msot/measure.hpp"
 #include "../../include/msot/sinkhorn.hpp"
+#include "../../include/msot/labels.hpp"
+#include "../../include/msot/barycenter.hpp"
 
 namespace msot {
 
@@ -258,6 +260,104 @@ double divergence(const DiscreteMeasure& a, const DiscreteMeasure& b, const Solv
   double loss = 0.0;
   solve(a, b, params, dev, &loss);
   return loss;
+}
+
+// ------------------------------------------------------------------ labeling
+SoftLabels transfer_labels(const DiscreteMeasure& a, const DiscreteMeasure& b,
+                           const LabelSet& labels, const SolverParams& params, Device& dev) {
+  if (a.dim() != b.dim()) throw DataError("transfer_labels: dimension mismatch");
+  if (labels.assignments.size() != b.size())
+    throw DataError("transfer_labels: labels must be sized to the atlas measure");
+  const msot_params p = params.to_c();
+  std::vector<int32_t> lab(labels.assignments.begin(), labels.assignments.end());
+  SoftLabels out;
+  out.n = a.size();
+  out.L = labels.L;
+  out.scores.resize(a.size() * static_cast<std::size_t>(std::max(labels.L, 0)));
+  out.row_mass.resize(a.size());
+  double loss = 0.0;
+  msot_stats st;
+  throw_on_status(msot_transfer_labels(dev.get(), &p, a.points().data(), a.weights().data(),
+                                       static_cast<int64_t>(a.size()), b.points().data(),
+                                       b.weights().data(), static_cast<int64_t>(b.size()),
+                                       static_cast<int>(a.dim()), lab.data(), labels.L,
+                                       out.scores.data(), out.row_mass.data(), &loss, &st),
+                  "transfer_labels");
+  return out;
+}
+
+SoftLabels resolve_flips(const SoftLabels& soft, const FlipMap& map) {
+  if (soft.n != 2 * map.originals) throw DataError("resolve_flips: missing flip pair");
+  std::vector<int32_t> of(soft.n), ori(soft.n), chosen(map.originals);
+  for (std::size_t i = 0; i < soft.n; ++i) {
+    of[i] = static_cast<int32_t>(map.original_of(i));
+    ori[i] = map.is_flipped(i) ? 1 : 0;
+  }
+  SoftLabels out;
+  out.n = map.originals;
+  out.L = soft.L;
+  out.scores.resize(out.n * static_cast<std::size_t>(soft.L));
+  out.row_mass.resize(out.n);
+  throw_on_status(msot_resolve_flips(soft.scores.data(), soft.row_mass.data(),
+                                     static_cast<int64_t>(soft.n), soft.L, of.data(), ori.data(),
+                                     out.scores.data(), out.row_mass.data(), chosen.data()),
+                  "resolve_flips");
+  return out;
+}
+
+Classification classify(const SoftLabels& soft, double tau) {
+  std::vector<int32_t> lab(soft.n);
+  Classification c;
+  c.confidence.resize(soft.n);
+  throw_on_status(msot_classify(soft.scores.data(), soft.row_mass.data(),
+                                static_cast<int64_t>(soft.n), soft.L, tau, lab.data(),
+                                c.confidence.data()),
+                  "classify");
+  c.label.assign(lab.begin(), lab.end());
+  return c;
+}
+
+// ------------------------------------------------------- gradients / barycenter
+std::vector<double> grad_positions(const DiscreteMeasure& a, const DiscreteMeasure& b,
+                                   const SolverParams& params, double* loss, Device& dev) {
+  if (a.dim() != b.dim()) throw DataError("grad_positions: dimension mismatch");
+  const msot_params p = params.to_c();
+  std::vector<double> g(a.size() * a.dim());
+  double l = 0.0;
+  msot_stats st;
+  throw_on_status(msot_sinkhorn_grad(dev.get(), &p, a.points().data(), a.weights().data(),
+                                     static_cast<int64_t>(a.size()), b.points().data(),
+                                     b.weights().data(), static_cast<int64_t>(b.size()),
+                                     static_cast<int>(a.dim()), &l, g.data(), &st),
+                  "grad_positions");
+  if (loss) *loss = l;
+  return g;
+}
+
+BarycenterResult barycenter(const std::vector<DiscreteMeasure>& targets,
+                            const DiscreteMeasure& init, const SolverParams& params,
+                            const BarycenterConfig& cfg, Device& dev) {
+  if (targets.empty()) throw DataError("barycenter: no targets");
+  const msot_params p = params.to_c();
+  const int k = static_cast<int>(targets.size());
+  std::vector<const double*> ys(k), bs(k);
+  std::vector<int64_t> ms(k);
+  for (int t = 0; t < k; ++t) {
+    if (targets[t].dim() != init.dim()) throw DataError("barycenter: dimension mismatch");
+    ys[t] = targets[t].points().data();
+    bs[t] = targets[t].weights().data();
+    ms[t] = static_cast<int64_t>(targets[t].size());
+  }
+  std::vector<double> x(init.size() * init.dim()), traj(cfg.iters + 1);
+  int done = 0;
+  msot_stats st;
+  throw_on_status(msot_barycenter(dev.get(), &p, init.points().data(), init.weights().data(),
+                                  static_cast<int64_t>(init.size()), k, ys.data(), bs.data(),
+                                  ms.data(), static_cast<int>(init.dim()), cfg.iters, cfg.step,
+                                  cfg.tol, x.data(), traj.data(), &done, &st),
+                  "barycenter");
+  traj.resize(done + 1);
+  return {init.with_points(std::move(x)), std::move(traj)};
 }
 
 }  // namespace msot

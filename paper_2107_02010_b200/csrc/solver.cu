@@ -404,6 +404,7 @@ struct Plan {
   int32_t n_items = 0;
   float* part = nullptr;
   double pairs_local = 0.0, pairs_all = 0.0;
+  double terms_all = 0.0;  // LSE terms summed: an evaluate-once pair feeds a row and a column
 };
 
 // Contiguous tile shards balanced on work (shared with msot_shard_tiles).
@@ -426,7 +427,7 @@ void build_plan(msot_ctx* c, const std::string& tag, Plan& P) {
   cudaStream_t st = c->st;
   // per-problem shard of row tiles, weighted by evaluated pairs
   int64_t tot_tiles = 0, tot_cols = 0;
-  P.pairs_all = P.pairs_local = 0.0;
+  P.pairs_all = P.pairs_local = P.terms_all = 0.0;
   for (int p = 0; p < P.np; ++p) {
     const RangeSet& R = *P.ps[p].rs;
     std::vector<double> work(R.n_tiles);
@@ -434,6 +435,10 @@ void build_plan(msot_ctx* c, const std::string& tag, Plan& P) {
       const int64_t rows = R.tile_start_h[t + 1] - R.tile_start_h[t];
       work[t] = static_cast<double>(rows) * static_cast<double>(R.tile_cols_h[t]) + 1.0;
       P.pairs_all += static_cast<double>(rows) * static_cast<double>(R.tile_cols_h[t]);
+      const SymSet* sy = P.ps[p].sym;
+      P.terms_all += static_cast<double>(rows) *
+                     (sy ? 2.0 * static_cast<double>(R.tile_cols_h[t]) - (sy->self ? rows : 0)
+                         : static_cast<double>(R.tile_cols_h[t]));
     }
     std::vector<int64_t> tb;
     shard_tiles(work, c->world, tb);
@@ -551,6 +556,7 @@ void run_group(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& ss) {
   CK(hd ? launch_fallback_hd(G, ss.d, c->n_sm, st) : launch_fallback(G, ss.d, c->n_sm, st));
   ss.S->softmin_launches += 1;
   ss.S->pairs_evaluated += P.pairs_all;
+  ss.S->pairs_terms += P.terms_all;
   // all-gather of the updated potentials (NCCL over NVLink)
   if (c->world > 1) {
     NK(ncclGroupStart());
@@ -692,6 +698,7 @@ void run_group_sym(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& s
   CK(hd ? launch_fallback_hd(G, ss.d, c->n_sm, st) : launch_fallback_dense(G, ss.d, c->n_sm, st));
   ss.S->softmin_launches += 1;
   ss.S->pairs_evaluated += P.pairs_all;
+  ss.S->pairs_terms += P.terms_all;
   if (c->world > 1) {  // all-gather of the row-side potentials
     NK(ncclGroupStart());
     for (int p = 0; p < 3; ++p)

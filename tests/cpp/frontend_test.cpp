@@ -6,6 +6,8 @@
 #include <cstring>
 #include <string>
 
+#include "msot/barycenter.hpp"
+#include "msot/labels.hpp"
 #include "msot/measure.hpp"
 #include "msot/sinkhorn.hpp"
 
@@ -85,6 +87,18 @@ static void cpu_checks() {
   empty.nx = empty.ny = empty.nz = 1;
   empty.voxels = {{0, 0, 0, 0.0}};
   CHECK(throws<DataError>([&] { density_to_measure(empty); }));
+  // resolve_flips / classify, host-only
+  SoftLabels sl;
+  sl.n = 4;
+  sl.L = 2;
+  sl.scores = {0.9, 0.0, 0.01, 0.01, 0.05, 0.0, 0.0, 0.7};
+  sl.row_mass = {0.9, 0.02, 0.05, 0.7};
+  SoftLabels r = resolve_flips(sl, FlipMap{2});
+  CHECK(r.n == 2 && r.row_mass[0] == 0.9 && r.row_mass[1] == 0.7 && r.score(1, 1) == 0.7);
+  Classification cl = classify(r, 0.5);
+  CHECK(cl.label[0] == 0 && cl.label[1] == 1 && cl.confidence[0] == 1.0);
+  CHECK(classify(sl, 0.5).label[1] == OUTLIER);
+  CHECK(throws<DataError>([&] { resolve_flips(sl, FlipMap{3}); }));
 }
 
 static void gpu_checks() {
@@ -132,6 +146,31 @@ static void gpu_checks() {
   CHECK(throws<DataError>([&] { divergence(a, b, bad); }));
   DiscreteMeasure d2({0.0, 0.0}, {1.0}, 2);
   CHECK(throws<DataError>([&] { divergence(a, d2, p); }));
+  // transfer_labels: bijective unit Diracs -> one-hot rows
+  DiscreteMeasure u4({0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0, 1}, {0.25, 0.25, 0.25, 0.25}, 3);
+  DiscreteMeasure v4({0.01, 0, 0, 1.01, 0, 0, 0.01, 1, 0, 0.01, 0, 1}, {0.25, 0.25, 0.25, 0.25}, 3);
+  SolverParams lp;
+  lp.blur = 0.05;
+  lp.scaling = 0.7;
+  LabelSet ls{4, {"a", "b", "c", "d"}, {0, 1, 2, 3}};
+  SoftLabels soft = transfer_labels(u4, v4, ls, lp);
+  bool onehot = true;
+  for (int i = 0; i < 4; ++i)
+    for (int l = 0; l < 4; ++l) onehot = onehot && std::fabs(soft.score(i, l) - (i == l)) < 1e-3;
+  CHECK(onehot);
+  CHECK(throws<DataError>([&] { transfer_labels(u4, v4, LabelSet{4, {}, {0, 1}}, lp); }));
+  // grad_positions: translated Dirac -> alpha (x - y)
+  double gl = 0.0;
+  auto g = grad_positions(a, b, p, &gl);
+  CHECK(std::fabs(g[0] + 1.0) < 1e-2 && std::fabs(g[1] + 0.5) < 1e-2 && std::fabs(g[2]) < 1e-2);
+  // barycenter of two Diracs -> their midpoint
+  DiscreteMeasure t0({-1.0, 0.0, 0.0}, {1.0}, 3), t1({1.0, 0.0, 0.0}, {1.0}, 3);
+  DiscreteMeasure init({0.3, 0.2, 0.0}, {1.0}, 3);
+  SolverParams bp;
+  bp.blur = 0.05;
+  BarycenterResult br = barycenter({t0, t1}, init, bp, BarycenterConfig{20, 1.0, 0.0});
+  CHECK(std::fabs(br.measure.point(0)[0]) < 1e-2 && std::fabs(br.measure.point(0)[1]) < 1e-2);
+  CHECK(br.loss.back() <= br.loss.front());
 }
 
 int main(int argc, char** argv) {

@@ -93,17 +93,60 @@ __device__ __forceinline__ float ub_regs(float4 X, float rI, float F, float4 Y, 
   return v + 1e-5f * (1.f + fabsf(F) + fabsf(G) + 2.f * s + 2.f * rr * rr);
 }
 
-// One CTA per row cluster I: every word of row I (a warp computes 32
-// consecutive column clusters — coalesced column loads — and writes the word
-// with one ballot) and the row's best pair (max slack, ties -> lowest J).
-// The float64 slack is evaluated only where the float32 upper bound reaches
-// min(thr, best so far): for the bit, and for the arg-max.
+// Column blocks = the 32 clusters of one mask word (Morton-consecutive, so
+// spatially compact): centre C_W, radius R_W >= |Y_J - C_W| + r_J (rounded
+// up), G_W = max_J G_J.  Since |X_I - Y_J| - r_I - r_J >= |X_I - C_W| - R_W -
+// r_I, ub_regs at (C_W, R_W, G_W) bounds B_a — hence the slack — of every
+// pair of the block.
+__global__ void block_bounds_kernel(const float4* cy, const float* ry, const float* gy,
+                                    int32_t ky, int d, float4* blk, float* blkg) {
+  const int lane = threadIdx.x & 31;
+  const int32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (w >= mask_words(ky)) return;
+  const int32_t J = w * 32 + lane;
+  const bool v = J < ky;
+  const float4 Y = v ? cy[J] : make_float4(0.f, 0.f, 0.f, 0.f);
+  const int cnt = __popc(__ballot_sync(0xffffffffu, v));
+  float sx = v ? Y.x : 0.f, sy = v ? Y.y : 0.f, sz = v ? Y.z : 0.f;
+  float gm = v ? gy[J] : -INFINITY;
+  for (int o = 16; o > 0; o >>= 1) {
+    sx += __shfl_xor_sync(0xffffffffu, sx, o);
+    sy += __shfl_xor_sync(0xffffffffu, sy, o);
+    sz += __shfl_xor_sync(0xffffffffu, sz, o);
+    gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+  }
+  const float cx = sx / cnt, cyy = d > 1 ? sy / cnt : 0.f, cz = d > 2 ? sz / cnt : 0.f;
+  float r = 0.f;
+  if (v) {
+    const double dx = static_cast<double>(Y.x) - cx;
+    const double dy = d > 1 ? static_cast<double>(Y.y) - cyy : 0.0;
+    const double dz = d > 2 ? static_cast<double>(Y.z) - cz : 0.0;
+    r = static_cast<float>(sqrt(dx * dx + dy * dy + dz * dz) + static_cast<double>(ry[J]));
+  }
+  for (int o = 16; o > 0; o >>= 1) r = fmaxf(r, __shfl_xor_sync(0xffffffffu, r, o));
+  if (lane == 0) {
+    blk[w] = make_float4(cx, cyy, cz, r * (1.f + 1e-5f) + 1e-6f);
+    blkg[w] = gm;
+  }
+}
+
+// One CTA per row cluster I: every word of row I and the row's best pair
+// (max slack, ties -> lowest J).  Pass 1: a warp tests 32 words' blocks at a
+// time (one lane per word) against thr, writes 0 to the words that fail and
+// walks the others with one lane per column cluster (coalesced loads, one
+// ballot per word); the float64 slack is evaluated only where the float32
+// upper bound reaches min(thr, best so far).  If the row has a kept pair its
+// best is >= thr, so no skipped block can hold it.  Otherwise (rare) pass 2
+// revisits the skipped blocks whose bound reaches the best so far, for the
+// arg-max only (their bits are 0).
 constexpr int kMaskThreads = 256;
 
 __global__ void __launch_bounds__(kMaskThreads)
-mask_rows_kernel(MaskIn m, double thr, int self, uint32_t* mask, int32_t* best) {
+mask_rows_kernel(MaskIn m, const float4* blk, const float* blkg, double thr, int self,
+                 uint32_t* mask, int32_t* best) {
   __shared__ double sv[kMaskThreads / 32];
   __shared__ int32_t sj[kMaskThreads / 32];
+  __shared__ double s_best;
   const int32_t I = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -113,7 +156,8 @@ mask_rows_kernel(MaskIn m, double thr, int self, uint32_t* mask, int32_t* best) 
   const float4 GI = g ? m.gx[I] : zero;
   double bv = -INFINITY;
   int32_t bj = 0x7fffffff;
-  for (int32_t w = warp; w < m.words; w += kMaskThreads / 32) {
+  uint32_t* row = mask + static_cast<int64_t>(I) * m.words;
+  auto walk_word = [&](int32_t w, double lim_bits, bool write) {
     const int32_t J = w * 32 + lane;
     bool keep = false;
     if (J < m.ky) {
@@ -121,14 +165,62 @@ mask_rows_kernel(MaskIn m, double thr, int self, uint32_t* mask, int32_t* best) 
       const float rJ = m.ry[J], G = m.gy[J];
       const double u = static_cast<double>(ub_regs(X, rI, F, Y, rJ, G, m.d));
       keep = self && I == J;  // diagonal of a self mask
-      if (u >= thr || u >= bv) {
+      if (u >= lim_bits || u >= bv) {
         const double v = pair_slack(X, rI, F, GI, Y, rJ, G, g ? m.hy[J] : zero, m.d, g);
         keep = keep || v >= thr;
-        if (v > bv) { bv = v; bj = J; }  // J increases per thread: ties keep the lowest
+        if (v > bv || (v == bv && J < bj)) { bv = v; bj = J; }
       }
     }
     const uint32_t bits = __ballot_sync(0xffffffffu, keep);
-    if (lane == 0) mask[static_cast<int64_t>(I) * m.words + w] = bits;
+    if (write && lane == 0) row[w] = bits;
+  };
+  // pass 1
+  for (int32_t w0 = warp * 32; w0 < m.words; w0 += kMaskThreads) {
+    const int32_t wl = w0 + lane;
+    bool need = false;
+    if (wl < m.words) {
+      const float4 B = blk[wl];
+      const double u = static_cast<double>(ub_regs(X, rI, F, B, B.w, blkg[wl], m.d));
+      need = u >= thr || (self && (I >> 5) == wl);
+      if (!need) row[wl] = 0u;
+    }
+    uint32_t todo = __ballot_sync(0xffffffffu, need);
+    while (todo) {
+      const int32_t w = w0 + __ffs(todo) - 1;
+      todo &= todo - 1;
+      walk_word(w, thr, true);
+    }
+  }
+  // the row's best so far
+  double b2 = bv;
+  for (int o = 16; o > 0; o >>= 1) b2 = fmax(b2, __shfl_xor_sync(0xffffffffu, b2, o));
+  if (lane == 0) sv[warp] = b2;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = sv[0];
+    for (int q = 1; q < kMaskThreads / 32; ++q) b = fmax(b, sv[q]);
+    s_best = b;
+  }
+  __syncthreads();
+  const double rb = s_best;
+  __syncthreads();
+  if (rb < thr) {
+    // pass 2: no kept pair — the arg-max may sit in a skipped block
+    for (int32_t w0 = warp * 32; w0 < m.words; w0 += kMaskThreads) {
+      const int32_t wl = w0 + lane;
+      bool need = false;
+      if (wl < m.words) {
+        const float4 B = blk[wl];
+        const double u = static_cast<double>(ub_regs(X, rI, F, B, B.w, blkg[wl], m.d));
+        need = u < thr && !(self && (I >> 5) == wl) && u >= rb;
+      }
+      uint32_t todo = __ballot_sync(0xffffffffu, need);
+      while (todo) {
+        const int32_t w = w0 + __ffs(todo) - 1;
+        todo &= todo - 1;
+        walk_word(w, thr, false);
+      }
+    }
   }
   for (int o = 16; o > 0; o >>= 1) {
     const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
@@ -169,14 +261,23 @@ cudaError_t truncation_masks(int32_t kx, int32_t ky, int d, const float4* cx, co
                              const float* fx, const float4* gx, const float4* cy, const float* ry,
                              const float* gy, const float4* hy, double eps, double theta, int self,
                              uint32_t* mask, uint32_t* maskT, int32_t* best_r, int32_t* best_c,
-                             cudaStream_t st) {
+                             void* blkws, cudaStream_t st) {
   if (kx <= 0 || ky <= 0) return cudaSuccess;
   if ((gx == nullptr) != (hy == nullptr)) return cudaErrorInvalidValue;
   if (self && kx != ky) return cudaErrorInvalidValue;
   const double thr = -(theta * eps);
   const MaskIn m{kx, ky, d, mask_words(ky), cx, cy, rx, ry, fx, gy, gx, hy};
+  // layout of blkws: float4 blocks of y, float4 blocks of x, then the float maxima
+  float4* blk_y = reinterpret_cast<float4*>(blkws);
+  float4* blk_x = blk_y + mask_words(ky);
+  float* blkg_y = reinterpret_cast<float*>(blk_x + mask_words(kx));
+  float* blkg_x = blkg_y + mask_words(ky);
   ++g_launches;
-  mask_rows_kernel<<<static_cast<unsigned>(kx), kMaskThreads, 0, st>>>(m, thr, self, mask, best_r);
+  block_bounds_kernel<<<static_cast<unsigned>((mask_words(ky) * 32 + 255) / 256), 256, 0, st>>>(
+      cy, ry, gy, ky, d, blk_y, blkg_y);
+  ++g_launches;
+  mask_rows_kernel<<<static_cast<unsigned>(kx), kMaskThreads, 0, st>>>(m, blk_y, blkg_y, thr, self,
+                                                                         mask, best_r);
   if (self) {
     ++g_launches;
     mask_best_kernel<<<static_cast<unsigned>((kx + 255) / 256), 256, 0, st>>>(
@@ -187,7 +288,11 @@ cudaError_t truncation_masks(int32_t kx, int32_t ky, int d, const float4* cx, co
   // is exactly symmetric), so maskT is the bitwise transpose of mask
   const MaskIn t{ky, kx, d, mask_words(kx), cy, cx, ry, rx, gy, fx, hy, gx};
   ++g_launches;
-  mask_rows_kernel<<<static_cast<unsigned>(ky), kMaskThreads, 0, st>>>(t, thr, 0, maskT, best_c);
+  block_bounds_kernel<<<static_cast<unsigned>((mask_words(kx) * 32 + 255) / 256), 256, 0, st>>>(
+      cx, rx, fx, kx, d, blk_x, blkg_x);
+  ++g_launches;
+  mask_rows_kernel<<<static_cast<unsigned>(ky), kMaskThreads, 0, st>>>(t, blk_x, blkg_x, thr, 0,
+                                                                         maskT, best_c);
   ++g_launches;
   mask_best_kernel<<<static_cast<unsigned>((static_cast<int64_t>(kx) + ky + 255) / 256), 256, 0, st>>>(
       best_r, kx, best_c, ky, mask, m.words, maskT, t.words);

@@ -131,12 +131,16 @@ __host__ __device__ inline int32_t mask_words(int32_t ky) { return (ky + 31) / 3
 // Keep bits + best pairs of one truncation test.  self: kx == ky, one
 // symmetric mask (maskT, best_c unused).  Otherwise mask (kx rows over ky)
 // and maskT (ky rows over kx, its exact transpose), both with the row and
-// column best pairs; best_r (kx) / best_c (ky) are workspaces.
+// column best pairs; best_r (kx) / best_c (ky) are workspaces, blkws holds
+// the column-block bounds (mask_block_ws_bytes).
 cudaError_t truncation_masks(int32_t kx, int32_t ky, int d, const float4* cx, const float* rx,
                              const float* fx, const float4* gx, const float4* cy, const float* ry,
                              const float* gy, const float4* hy, double eps, double theta, int self,
                              uint32_t* mask, uint32_t* maskT, int32_t* best_r, int32_t* best_c,
-                             cudaStream_t st);
+                             void* blkws, cudaStream_t st);
+inline size_t mask_block_ws_bytes(int32_t kx, int32_t ky) {
+  return static_cast<size_t>(mask_words(kx) + mask_words(ky)) * (sizeof(float4) + sizeof(float));
+}
 cudaError_t unpack_mask(const uint32_t* mask, int32_t kx, int32_t ky, uint8_t* out,
                         cudaStream_t st);
 // per tile: OR of its clusters' mask rows, then count / write column ranges

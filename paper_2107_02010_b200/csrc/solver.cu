@@ -1235,14 +1235,15 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
       for (int q = 0; q < 4; ++q) g[q] = (info && prm->mask_rule == 0) ? grad[q] : nullptr;
       int32_t* bxr = c->buf<int32_t>("m.bx", std::max(X.k, Y.k));
       int32_t* byr = c->buf<int32_t>("m.by", std::max(X.k, Y.k));
+      void* bws = c->buf<char>("m.blk", mask_block_ws_bytes(std::max(X.k, Y.k), std::max(X.k, Y.k)));
       CK(truncation_masks(X.k, X.k, d, X.cpts, X.radii, fmax[0], g[0], X.cpts, X.radii, fmax[0],
-                          g[0], e, theta, 1, mxx, nullptr, bxr, nullptr, st));
+                          g[0], e, theta, 1, mxx, nullptr, bxr, nullptr, bws, st));
       CK(truncation_masks(Y.k, Y.k, d, Y.cpts, Y.radii, fmax[1], g[1], Y.cpts, Y.radii, fmax[1],
-                          g[1], e, theta, 1, myy, nullptr, byr, nullptr, st));
+                          g[1], e, theta, 1, myy, nullptr, byr, nullptr, bws, st));
       // cross pair: (F, G) = (max b_yx, max a_xy); the slack is symmetric, so
       // the yx mask (rows y) is the exact transpose of the xy mask (rows x)
       CK(truncation_masks(X.k, Y.k, d, X.cpts, X.radii, fmax[3], g[3], Y.cpts, Y.radii, fmax[2],
-                          g[2], e, theta, 0, mxy, myx, bxr, byr, st));
+                          g[2], e, theta, 0, mxy, myx, bxr, byr, bws, st));
       if (once) {  // evaluate-once pair sets (oracle.cpp: sym_self, transpose_ranges)
         sym_rangeset(c, "s.xx", X.labels, X.offsets_h, n, X.offsets, X.k, mxx, 1, sxx);
         sym_rangeset(c, "s.yy", Y.labels, Y.offsets_h, m, Y.offsets, Y.k, myy, 1, syy);
@@ -1930,8 +1931,10 @@ int msot_truncation_mask(msot_ctx* c, int64_t kx, int64_t ky, int d, const float
       CK(cudaMemcpyAsync(dhy, hy, ky * sizeof(float4), cudaMemcpyHostToDevice, st));
     }
     if (self && kx != ky) raise(MSOT_EUSAGE, "a self mask is square");
+    void* bws = c->buf<char>("tm.blk", mask_block_ws_bytes(static_cast<int32_t>(kx),
+                                                          static_cast<int32_t>(ky)));
     CK(truncation_masks(static_cast<int32_t>(kx), static_cast<int32_t>(ky), d, dcx, drx, dfx, dgx,
-                        dcy, dry, dgy, dhy, eps, theta, self, dbits, dbitsT, dbr, dbc, st));
+                        dcy, dry, dgy, dhy, eps, theta, self, dbits, dbitsT, dbr, dbc, bws, st));
     CK(unpack_mask(dbits, static_cast<int32_t>(kx), static_cast<int32_t>(ky), dm, st));
     CK(cudaMemcpyAsync(mask_out, dm, kx * ky, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));

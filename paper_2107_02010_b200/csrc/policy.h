@@ -27,8 +27,12 @@ extern "C" {
 /* Rows per block-sparse tile: the truncation mask is expanded to column
  * ranges per tile of MSOT_TILE_ROWS consecutive (cluster-sorted) rows. */
 #define MSOT_TILE_ROWS 256
-/* Target atoms per voxel for the automatic cluster_scale rule. */
-#define MSOT_AUTO_ATOMS_PER_CELL 48.0
+/* Target atoms per occupied voxel for the automatic cluster_scale rule.
+ * Measured on C3 (1M Gaussian mixtures, blur 0.01, profiles/r1_cell_sweep.jsonl)
+ * with the evaluate-once fine phase: 48 -> 0.74 s, S within 4.1e-4 of the
+ * dense solve; 28 -> 0.50 s, within 7.4e-5; below ~25 the switch (sigma <
+ * r_max) leaves too few fine scales (16 atoms: +2.9e-3). */
+#define MSOT_AUTO_ATOMS_PER_CELL 28.0
 /* Cube ids are Morton-interleaved with this many bits per axis (D <= 3). */
 #define MSOT_MORTON_BITS 10
 

@@ -282,6 +282,7 @@ struct SymSet {
   int32_t* etile = nullptr;
   float* colpart = nullptr;
   int64_t slots = 0, entries = 0;
+  bool dense = false;         // dense_symset: column sums by hd_colsum (no entries)
 };
 
 void sym_rangeset(msot_ctx* c, const std::string& tag, const int32_t* rl,
@@ -345,6 +346,7 @@ void dense_symset(msot_ctx* c, const std::string& tag, int64_t n_rows, int64_t n
   cudaStream_t st = c->st;
   RangeSet& R = S.R;
   S.self = self;
+  S.dense = true;
   make_tiles(c, tag, n_rows, nullptr, R);
   const int64_t T = R.n_tiles;
   std::vector<int64_t> rptr(T + 1), tcols(T), tslot(T + 1, 0);
@@ -670,7 +672,7 @@ void run_group_sym(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& s
     CK(launch_softmin_sym(G, ss.d, X.uniform && a.lam == 1.0, st));
   }
   if (c->profiling) CK(cudaEventRecord(e1, st));
-  if (hd) {
+  if (P.ps[0].sym->dense) {  // dense pair sets (high-D path, coarse phase, dense solves)
     for (int p = 0; p < 3; ++p) {
       const SymSet& S = *P.ps[p].sym;
       CK(hd_colsum(S.colpart, S.tslot, S.R.tile_start, static_cast<int32_t>(P.t0[p]),
@@ -1100,6 +1102,8 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
   prepare_measure(c, "y", d_y, d_b, m, d, g, ms, Y);
 
   if (!ms) {
+    // dense solves stay row-wise (4 problems per scale): the cross potentials
+    // of identical measures stay bitwise symmetric, S(a, a) = 0 exactly
     c->mark(4);  // phase 4: symmetric updates
     S->t_switch = 0;
     RangeSet &rxx = fxx, &ryy = fyy, &rxy = fxy, &ryx = fyx;
@@ -1131,16 +1135,41 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
       alloc_pots(c, "cpot", X.k, Y.k, Uc);
       int ccur = 0;
       RangeSet rxx, ryy, rxy, ryx;
-      dense_rangeset(c, "c.xx", X.k, X.k, rxx);
-      dense_rangeset(c, "c.yy", Y.k, Y.k, ryy);
-      dense_rangeset(c, "c.xy", Y.k, X.k, rxy);
-      dense_rangeset(c, "c.yx", X.k, Y.k, ryx);
+      SymSet cxx, cyy, cyx;
+      SymCols ccol{};
       Plan Pc;
-      sym_specs(Pc, X.cpts, X.clw2, X.k, Y.cpts, Y.clw2, Y.k, &rxx, &ryy, &rxy, &ryx);
+      const bool conce = prm->pair_eval != 0;
+      if (conce) {  // evaluate-once on the centroid measures (dense pair sets)
+        dense_symset(c, "cs.xx", X.k, X.k, 1, cxx);
+        dense_symset(c, "cs.yy", Y.k, Y.k, 1, cyy);
+        dense_symset(c, "cs.yx", X.k, Y.k, 0, cyx);
+        Pc.np = 3;
+        Pc.ps[0] = {X.cpts, X.k, X.cpts, X.clw2, X.k, &cxx.R, {}, &cxx, X.clw2};
+        Pc.ps[1] = {Y.cpts, Y.k, Y.cpts, Y.clw2, Y.k, &cyy.R, {}, &cyy, Y.clw2};
+        Pc.ps[2] = {X.cpts, X.k, Y.cpts, Y.clw2, Y.k, &cyx.R, {}, &cyx, X.clw2};
+        ccol.tot[0] = c->buf<float>("cs.totx", X.k);
+        ccol.tot[1] = c->buf<float>("cs.toty", Y.k);
+        ccol.tot[2] = c->buf<float>("cs.totxy", Y.k);
+        ccol.yrows = Y.cpts;
+        ccol.xcols = X.cpts;
+        ccol.x_lw2 = X.clw2;
+        ccol.n = X.k;
+        ccol.m = Y.k;
+        ccol.uniform = false;
+      } else {
+        dense_rangeset(c, "c.xx", X.k, X.k, rxx);
+        dense_rangeset(c, "c.yy", Y.k, Y.k, ryy);
+        dense_rangeset(c, "c.xy", Y.k, X.k, rxy);
+        dense_rangeset(c, "c.yx", X.k, Y.k, ryx);
+        sym_specs(Pc, X.cpts, X.clw2, X.k, Y.cpts, Y.clw2, Y.k, &rxx, &ryy, &rxy, &ryx);
+      }
       build_plan(c, "pc", Pc);
       const double cfull = double(X.k) * X.k + double(Y.k) * Y.k + 2.0 * double(X.k) * Y.k;
       for (int t = 0; t < tsw; ++t) {
-        sym_step(c, Pc, Uc, ccur, eps[t], lam[t], false, ss);
+        if (conce)
+          sym_step_once(c, Pc, Uc, ccur, eps[t], lam[t], false, ss, ccol);
+        else
+          sym_step(c, Pc, Uc, ccur, eps[t], lam[t], false, ss);
         S->pairs_dense += cfull;
       }
       c->mark(2);  // phase 2: coarse -> fine transfer

@@ -7,11 +7,19 @@ from paper_2107_02010_b200.abi import make_params
 from paper_2107_02010_b200.solver import Context
 
 grid = {}
+shape = "mixture"
 for a in sys.argv[1:]:
     k, v = a.split("=")
+    if k == "shape":
+        shape = v
+        continue
     grid[k] = [float(x) for x in v.split(",")]
 w = dict(bench.WORKLOAD)
 x, a, y, b = bench.make_inputs(w)
+if shape == "uniform":  # SURVEY.md §8d C3 second shape
+    import numpy as np
+    x = np.random.default_rng(5).random((w["n"], 3))
+    y = np.random.default_rng(6).random((w["m"], 3))
 ctx = Context(0)
 ctx.set_profiling(True)
 base = dict(blur=w["blur"], reach=math.inf, scaling=w["scaling"], multiscale=True,

@@ -33,8 +33,9 @@ import numpy as np  # noqa: E402
 
 WORKLOAD = dict(workload="C3: S_eps 1M vs 1M 3D Gaussian mixtures (8 comps, sigma 0.05), "
                          "multiscale voxel grid + per-scale kernel truncation",
-                n=1_000_000, m=1_000_000, d=3, blur=0.01, reach="inf", scaling=0.9, theta=20.0,
+                n=1_000_000, m=1_000_000, d=3, blur=0.01, reach="inf", scaling=0.9, theta=12.5,
                 retruncate=1, switch_factor=1.0, cluster_scale="auto (28 atoms/occupied voxel)",
+                theta_note="12.5 = GeomLoss truncate=5 (exp(-C/eps) > e^-12.5); S within 3e-12 of theta 20 (profiles/r1_theta_sweep.jsonl)",
                 seeds=[5, 6])
 METRIC = "sec to S_eps, 1M vs 1M 3D pts at 1/2/4/8 GPU; softmin pairs/sec vs roofline"
 PAIRS_FILE = os.path.join(ROOT, "profiles", "c3_workload.json")

@@ -94,6 +94,8 @@ typedef struct msot_stats {
   double  pairs_terms;      /* LSE terms summed over all potentials: a pair evaluated
                                once for its row and its column counts twice (what a
                                row-wise CPU solver evaluates for the same solve)  */
+  double  pairs_mask_terms; /* profiling: fine-phase LSE terms at cluster granularity
+                               (the masks without the 256-row tile union)          */
 } msot_stats;
 
 typedef struct msot_ctx msot_ctx;

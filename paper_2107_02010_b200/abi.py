@@ -62,6 +62,7 @@ class Stats(C.Structure):
         ("world", C.c_int32),
         ("phase_ms", C.c_double * 8),
         ("pairs_terms", C.c_double),
+        ("pairs_mask_terms", C.c_double),
     ]
 
     PHASES = ("setup", "coarse", "extrapolate", "masks", "updates", "loss", "labels")

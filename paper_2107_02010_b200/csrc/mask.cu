@@ -299,6 +299,34 @@ cudaError_t truncation_masks(int32_t kx, int32_t ky, int d, const float4* cx, co
   return cudaGetLastError();
 }
 
+// Diagnostic (profiling only): sum over kept cluster pairs of n_I * m_J,
+// the pair count of the mask at cluster granularity (what the block-sparse
+// reduction would evaluate with no tile-level union).
+__global__ void mask_pair_count_kernel(const uint32_t* mask, int32_t kx, int32_t ky,
+                                       const int32_t* ro, const int32_t* co, double* out) {
+  const int32_t I = blockIdx.x;
+  const int32_t words = mask_words(ky);
+  double s = 0.0;
+  for (int32_t w = threadIdx.x; w < words; w += blockDim.x) {
+    uint32_t b = mask[static_cast<int64_t>(I) * words + w];
+    while (b) {
+      const int32_t J = w * 32 + __ffs(b) - 1;
+      b &= b - 1;
+      s += static_cast<double>(co[J + 1] - co[J]);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, s * static_cast<double>(ro[I + 1] - ro[I]));
+}
+
+cudaError_t mask_pair_count(const uint32_t* mask, int32_t kx, int32_t ky, const int32_t* ro,
+                            const int32_t* co, double* out, cudaStream_t st) {
+  if (kx <= 0) return cudaSuccess;
+  ++g_launches;
+  mask_pair_count_kernel<<<kx, 128, 0, st>>>(mask, kx, ky, ro, co, out);
+  return cudaGetLastError();
+}
+
 __global__ void unpack_kernel(const uint32_t* mask, int32_t kx, int32_t ky, uint8_t* out) {
   const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (g >= static_cast<int64_t>(kx) * ky) return;

@@ -141,6 +141,8 @@ cudaError_t truncation_masks(int32_t kx, int32_t ky, int d, const float4* cx, co
 inline size_t mask_block_ws_bytes(int32_t kx, int32_t ky) {
   return static_cast<size_t>(mask_words(kx) + mask_words(ky)) * (sizeof(float4) + sizeof(float));
 }
+cudaError_t mask_pair_count(const uint32_t* mask, int32_t kx, int32_t ky, const int32_t* ro,
+                            const int32_t* co, double* out, cudaStream_t st);
 cudaError_t unpack_mask(const uint32_t* mask, int32_t kx, int32_t ky, uint8_t* out,
                         cudaStream_t st);
 // per tile: OR of its clusters' mask rows, then count / write column ranges

@@ -1231,6 +1231,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
     RangeSet &rxx = fxx, &ryy = fyy, &rxy = fxy, &ryx = fyx;
     Plan Pf;
     const bool once = prm->pair_eval != 0;
+    double mask_terms = 0.0;  // profiling: cluster-granularity terms of the current masks
     SymSet sxx, syy, syx;
     SymCols scol{};
     if (once) {
@@ -1273,6 +1274,18 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
       // the yx mask (rows y) is the exact transpose of the xy mask (rows x)
       CK(truncation_masks(X.k, Y.k, d, X.cpts, X.radii, fmax[3], g[3], Y.cpts, Y.radii, fmax[2],
                           g[2], e, theta, 0, mxy, myx, bxr, byr, bws, st));
+      if (c->profiling) {  // cluster-granularity pair count of the four masks
+        double* cnt = c->buf<double>("m.cnt", 1);
+        CK(cudaMemsetAsync(cnt, 0, sizeof(double), st));
+        CK(mask_pair_count(mxx, X.k, X.k, X.offsets, X.offsets, cnt, st));
+        CK(mask_pair_count(myy, Y.k, Y.k, Y.offsets, Y.offsets, cnt, st));
+        CK(mask_pair_count(mxy, X.k, Y.k, X.offsets, Y.offsets, cnt, st));
+        CK(mask_pair_count(myx, Y.k, X.k, Y.offsets, X.offsets, cnt, st));
+        double h = 0.0;
+        CK(cudaMemcpyAsync(&h, cnt, sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        mask_terms = h;
+      }
       if (once) {  // evaluate-once pair sets (oracle.cpp: sym_self, transpose_ranges)
         sym_rangeset(c, "s.xx", X.labels, X.offsets_h, n, X.offsets, X.k, mxx, 1, sxx);
         sym_rangeset(c, "s.yy", Y.labels, Y.offsets_h, m, Y.offsets, Y.k, myy, 1, syy);
@@ -1306,6 +1319,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
       S->pairs_dense += full;
       S->pairs_fine += Pf.pairs_all;
       S->pairs_fine_dense += full;
+      S->pairs_mask_terms += mask_terms;
     }
     if (once && d_grad) {  // the plans of grad_positions read per-row ranges
       mask_rangeset(c, "f.xx", X.labels, X.offsets_h, n, X.offsets, X.k, mxx, fxx);

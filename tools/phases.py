@@ -16,5 +16,6 @@ for rep in range(2):
 names = ["setup", "coarse", "extrapolate", "masks", "fine", "loss"]
 print(json.dumps(dict(n=n, loss=loss, total_ms=st["total_ms"], softmin_ms=st["softmin_ms"],
                       phases=st["phase_ms"],
-                      pairs=st["pairs_evaluated"], kept=st["pairs_fine"] / st["pairs_fine_dense"],
+                      pairs=st["pairs_evaluated"], terms=st["pairs_terms"],
+                      mask_terms=st["pairs_mask_terms"], fine=st["pairs_fine"], kept=st["pairs_fine"] / st["pairs_fine_dense"],
                       kx=st["kx"], t_switch=st["t_switch"], n_scales=st["n_scales"])))

@@ -87,3 +87,72 @@ def test_shard_bounds_cover_and_balance():
             if nt >= world:
                 parts = np.array([w[b[r]:b[r + 1]].sum() for r in range(world)])
                 assert parts.max() - parts.min() <= 2 * w.max() + 1e-9
+
+
+def _sym_worker(rank, world, port, n, m, q):
+    """Evaluate-once protocol of one scale: each rank owns a
+    contiguous run of 256-row tiles of x; per tile it evaluates the cross
+    block (rows x, all y) once -> row sums of its x rows and column partials
+    for every y; the self block x-x over its diagonal + upper columns -> row
+    sums, and column partials for the upper columns.  Column partials are
+    all-reduced (NCCL in the product, gloo here), then every rank finalises
+    its own rows (row part + column part) and all of a_xy.  Compared with the
+    single-process dense sums."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(5)
+        x, y = rng.random((n, 3)), rng.random((m, 3))
+        a, b = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
+        f, g = 0.01 * rng.standard_normal(n), 0.01 * rng.standard_normal(m)
+        eps = 0.05
+        ts = _tiles(n)
+        bnd = solver.shard_tiles(np.diff(ts).astype(np.float64) * m, world)
+        row_cross = np.zeros(n)       # b_yx row sums (own rows)
+        col_cross = np.zeros(m)       # a_xy column partials (all columns)
+        row_self = np.zeros(n)        # a_xx row part (own rows)
+        col_self = np.zeros(n)        # a_xx column part (all columns)
+        for t in range(bnd[rank], bnd[rank + 1]):
+            r0, r1 = ts[t], ts[t + 1]
+            k = np.exp((f[r0:r1, None] + g[None, :]
+                        - 0.5 * ((x[r0:r1, None] - y[None]) ** 2).sum(-1)) / eps)
+            row_cross[r0:r1] = (k * b[None, :]).sum(1)
+            col_cross += (k * a[r0:r1, None]).sum(0)
+            ks = np.exp((f[r0:r1, None] + f[None, r0:] - 0.5 * ((x[r0:r1, None] - x[None, r0:]) ** 2).sum(-1)) / eps)
+            row_self[r0:r1] = (ks * a[None, r0:]).sum(1)           # diagonal block + upper
+            col_self[r1:] += (ks[:, r1 - r0:] * a[r0:r1, None]).sum(0)  # upper columns only
+        ct = torch.from_numpy(np.concatenate([col_cross, col_self]))
+        dist.all_reduce(ct, op=dist.ReduceOp.SUM)
+        col_cross, col_self = ct.numpy()[:m], ct.numpy()[m:]
+        r0, r1 = ts[bnd[rank]], ts[bnd[rank + 1]]
+        mine = (int(r0), row_cross[r0:r1].copy(), (row_self + col_self)[r0:r1].copy())
+        gathered = [None] * world
+        dist.all_gather_object(gathered, mine)
+        byx, axx = np.zeros(n), np.zeros(n)
+        for s0, rc, rs in gathered:
+            byx[s0:s0 + len(rc)] = rc
+            axx[s0:s0 + len(rs)] = rs
+        if rank == 0:
+            k = np.exp((f[:, None] + g[None, :] - 0.5 * ((x[:, None] - y[None]) ** 2).sum(-1)) / eps)
+            ks = np.exp((f[:, None] + f[None, :] - 0.5 * ((x[:, None] - x[None]) ** 2).sum(-1)) / eps)
+            ok = (np.allclose(byx, (k * b[None]).sum(1), rtol=1e-12)
+                  and np.allclose(col_cross, (k * a[:, None]).sum(0), rtol=1e-12)
+                  and np.allclose(axx, (ks * a[None]).sum(1), rtol=1e-12))
+            q.put(ok)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [700, 1300])
+def test_evaluate_once_protocol_world2(n):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sym_worker, args=(r, 2, port, n, 600, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert q.get(timeout=10)

@@ -10,6 +10,12 @@
 
 namespace msot {
 
+// grad_weights: gradient of S with respect to the weights
+// of a, potentials frozen: (rho + eps/2)(e^{-a_xx/rho} - e^{-b_yx/rho}) for a
+// finite reach, b_yx - a_xx + eps (sum a - sum b) for reach = inf; host-side.
+std::vector<double> grad_weights(const DiscreteMeasure& a, const DiscreteMeasure& b,
+                                 const DualPotentials& duals, const SolverParams& params);
+
 // grad_positions, p = 2: N x D (row-major) gradient of
 // S(a, b) with respect to the atoms of a.
 std::vector<double> grad_positions(const DiscreteMeasure& a, const DiscreteMeasure& b,

@@ -78,4 +78,19 @@ DualPotentials multiscale_sinkhorn(const DiscreteMeasure& a, const DiscreteMeasu
 double divergence(const DiscreteMeasure& a, const DiscreteMeasure& b, const SolverParams& params,
                   Device& dev = default_device());
 
+// plan_entry: a_i b_j exp((f_i + g_j - C(x_i, y_j)) / eps)
+// with (f, g) = (b_yx, a_xy); host-side.
+double plan_entry(std::size_t i, std::size_t j, const DiscreteMeasure& a,
+                  const DiscreteMeasure& b, const DualPotentials& duals,
+                  const SolverParams& params);
+// plan_apply: (pi v)_i on the GPU without materialising pi
+// (D <= 3).
+std::vector<double> plan_apply(const DiscreteMeasure& a, const DiscreteMeasure& b,
+                               const DualPotentials& duals, const SolverParams& params,
+                               const std::vector<double>& v, Device& dev = default_device());
+// ot_value: the dual objective of PAPER.md eq. 3 at
+// (f, g) = (b_yx, a_xy); the plan mass term comes from plan_apply(1).
+double ot_value(const DiscreteMeasure& a, const DiscreteMeasure& b, const DualPotentials& duals,
+                const SolverParams& params, Device& dev = default_device());
+
 }  // namespace msot

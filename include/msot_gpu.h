@@ -157,6 +157,14 @@ int msot_softmin(msot_ctx* ctx, const double* x, int64_t n, const double* y, int
                  int d, const double* logw_y, const double* h, double eps, double lambda,
                  const double* f_est, double* f_out);
 
+/* plan_apply (eq. 4): the implicit transport plan
+ * of the given duals applied to an M-vector, without materialising it,
+ *   out_i = sum_j a_i b_j exp((f_i + g_j - |x_i - y_j|^2 / 2) / eps) v_j,
+ * dense over the columns, D in 1..3 (f = b_yx on x, g = a_xy on y). */
+int msot_plan_apply(msot_ctx* ctx, const double* x, const double* a, int64_t n, const double* y,
+                    const double* b, int64_t m, int d, const double* f, const double* g,
+                    double eps, const double* v, double* out);
+
 /* Voxel-grid clustering (north star; replaces kmeans_coarsen SPEC.md:260):
  * cube ids floor((x - origin)/cell) in float64, Morton-interleaved, stable
  * LSD radix sort.  perm[k] = original index of the k-th sorted atom;

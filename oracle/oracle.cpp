@@ -817,6 +817,20 @@ int oracle_transfer_labels(const double* x, int64_t n, const double* y, const do
   return MSOT_OK;
 }
 
+// plan_apply (eq. 4), dense FP64.
+void oracle_plan_apply(const double* x, const double* a, int64_t n, const double* y,
+                       const double* b, int64_t m, int d, const double* f, const double* g,
+                       double eps, const double* v, double* out) {
+  msot::parallel::for_ranges(static_cast<std::size_t>(n), [&](std::size_t lo, std::size_t hi) {
+    for (std::size_t i = lo; i < hi; ++i) {
+      double s = 0.0;
+      for (int64_t j = 0; j < m; ++j)
+        s += b[j] * std::exp((f[i] + g[j] - cost(x + i * d, y + j * d, d, 2.0)) / eps) * v[j];
+      out[i] = a[i] * s;
+    }
+  });
+}
+
 // Barycenter descent, same rules as msot_barycenter.
 int oracle_barycenter(const msot_params* prm, const double* x0, const double* a, int64_t n, int k,
                       const double* const* ys, const double* const* bs, const int64_t* ms, int d,

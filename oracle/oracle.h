@@ -87,6 +87,12 @@ int oracle_transfer_labels(const double* x, int64_t n, const double* y, const do
                            const int32_t* labels, int n_classes, double* scores,
                            double* row_mass);
 
+/* plan_apply, dense FP64:
+ *   out_i = sum_j a_i b_j exp((f_i + g_j - C_ij)/eps) v_j. */
+void oracle_plan_apply(const double* x, const double* a, int64_t n, const double* y,
+                       const double* b, int64_t m, int d, const double* f, const double* g,
+                       double eps, const double* v, double* out);
+
 const char* oracle_last_error(void);
 
 #ifdef __cplusplus

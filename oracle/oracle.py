@@ -224,6 +224,22 @@ def transfer_labels(x, y, b, f, g, eps, labels, n_classes):
     return sc, rm
 
 
+def plan_apply(x, a, y, b, f, g, eps, v):
+    L = lib()
+    L.oracle_plan_apply.restype = None
+    L.oracle_plan_apply.argtypes = [_dp, _dp, C.c_int64, _dp, _dp, C.c_int64, C.c_int, _dp, _dp,
+                                    C.c_double, _dp, _dp]
+    x, a, y, b, f, g, v = map(_c64, (x, a, y, b, f, g, v))
+    if x.ndim == 1:
+        x = x[:, None]
+    if y.ndim == 1:
+        y = y[:, None]
+    out = np.zeros(len(a))
+    L.oracle_plan_apply(_d(x), _d(a), len(a), _d(y), _d(b), len(b), x.shape[1], _d(f), _d(g),
+                        eps, _d(v), _d(out))
+    return out
+
+
 def barycenter(prm, x0, a, targets, iters=10, step=1.0, tol=1e-4):
     L = lib()
     _setup_grad(L)

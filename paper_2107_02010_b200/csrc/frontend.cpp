@@ -262,6 +262,76 @@ double divergence(const DiscreteMeasure& a, const DiscreteMeasure& b, const Solv
   return loss;
 }
 
+// ------------------------------------------------------------ implicit plan
+static bool reach_inf(const SolverParams& p) { return !(p.reach > 0.0) || std::isinf(p.reach); }
+
+double plan_entry(std::size_t i, std::size_t j, const DiscreteMeasure& a,
+                  const DiscreteMeasure& b, const DualPotentials& duals,
+                  const SolverParams& params) {
+  if (i >= a.size() || j >= b.size()) throw DataError("plan_entry: index out of range");
+  if (duals.b_yx.size() != a.size() || duals.a_xy.size() != b.size())
+    throw DataError("plan_entry: duals do not match the measures");
+  const double c = cost(a.point(i), b.point(j), params.cost);
+  return a.weights()[i] * b.weights()[j] * std::exp((duals.b_yx[i] + duals.a_xy[j] - c) / duals.eps);
+}
+
+std::vector<double> plan_apply(const DiscreteMeasure& a, const DiscreteMeasure& b,
+                               const DualPotentials& duals, const SolverParams& params,
+                               const std::vector<double>& v, Device& dev) {
+  if (a.dim() != b.dim()) throw DataError("plan_apply: dimension mismatch");
+  if (v.size() != b.size()) throw DataError("plan_apply: v must be sized to b");
+  if (duals.b_yx.size() != a.size() || duals.a_xy.size() != b.size())
+    throw DataError("plan_apply: duals do not match the measures");
+  if (params.cost.p != 2.0) throw DataError("plan_apply: the GPU path implements p = 2");
+  std::vector<double> out(a.size());
+  throw_on_status(msot_plan_apply(dev.get(), a.points().data(), a.weights().data(),
+                                  static_cast<int64_t>(a.size()), b.points().data(),
+                                  b.weights().data(), static_cast<int64_t>(b.size()),
+                                  static_cast<int>(a.dim()), duals.b_yx.data(), duals.a_xy.data(),
+                                  duals.eps, v.data(), out.data()),
+                  "plan_apply");
+  return out;
+}
+
+double ot_value(const DiscreteMeasure& a, const DiscreteMeasure& b, const DualPotentials& duals,
+                const SolverParams& params, Device& dev) {
+  const std::vector<double> ones(b.size(), 1.0);
+  const std::vector<double> pv = plan_apply(a, b, duals, params, ones, dev);
+  double mass = 0.0;
+  for (double q : pv) mass += q;
+  const double eps = duals.eps;
+  const double ma = a.total_mass(), mb = b.total_mass();
+  double s = 0.0;
+  if (reach_inf(params)) {
+    for (std::size_t i = 0; i < a.size(); ++i) s += a.weights()[i] * duals.b_yx[i];
+    for (std::size_t j = 0; j < b.size(); ++j) s += b.weights()[j] * duals.a_xy[j];
+  } else {  // PAPER.md eq. 3
+    const double rho = std::pow(params.reach, params.cost.p);
+    for (std::size_t i = 0; i < a.size(); ++i)
+      s += rho * a.weights()[i] * (1.0 - std::exp(-duals.b_yx[i] / rho));
+    for (std::size_t j = 0; j < b.size(); ++j)
+      s += rho * b.weights()[j] * (1.0 - std::exp(-duals.a_xy[j] / rho));
+  }
+  return s + eps * (ma * mb - mass);
+}
+
+std::vector<double> grad_weights(const DiscreteMeasure& a, const DiscreteMeasure& b,
+                                 const DualPotentials& duals, const SolverParams& params) {
+  if (duals.a_xx.size() != a.size() || duals.b_yx.size() != a.size())
+    throw DataError("grad_weights: duals do not match the measure");
+  std::vector<double> gw(a.size());
+  const double eps = duals.eps;
+  if (reach_inf(params)) {
+    const double defect = eps * (a.total_mass() - b.total_mass());
+    for (std::size_t i = 0; i < a.size(); ++i) gw[i] = duals.b_yx[i] - duals.a_xx[i] + defect;
+  } else {
+    const double rho = std::pow(params.reach, params.cost.p);
+    for (std::size_t i = 0; i < a.size(); ++i)
+      gw[i] = (rho + 0.5 * eps) * (std::exp(-duals.a_xx[i] / rho) - std::exp(-duals.b_yx[i] / rho));
+  }
+  return gw;
+}
+
 // ------------------------------------------------------------------ labeling
 SoftLabels transfer_labels(const DiscreteMeasure& a, const DiscreteMeasure& b,
                            const LabelSet& labels, const SolverParams& params, Device& dev) {

@@ -1889,6 +1889,78 @@ int msot_softmin(msot_ctx* c, const double* x, int64_t n, const double* y, int64
   });
 }
 
+int msot_plan_apply(msot_ctx* c, const double* x, const double* a, int64_t n, const double* y,
+                    const double* b, int64_t m, int d, const double* f, const double* g,
+                    double eps, const double* v, double* out) {
+  return guard([&] {
+    if (!c || !x || !a || !y || !b || !f || !g || !v || !out) raise(MSOT_EUSAGE, "null argument");
+    if (n < 1 || m < 1) raise(MSOT_EDATA, "empty input");
+    if (d < 1 || d > 3) raise(MSOT_EUSAGE, "the GPU plan_apply supports D in 1..3");
+    if (!(eps > 0)) raise(MSOT_EUSAGE, "eps must be > 0");
+    check_weights(a, n);
+    check_weights(b, m);
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->st;
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t i = 0; i < n; ++i)
+      for (int k = 0; k < d; ++k) lo[k] = std::min(lo[k], x[i * d + k]), hi[k] = std::max(hi[k], x[i * d + k]);
+    for (int64_t j = 0; j < m; ++j)
+      for (int k = 0; k < d; ++k) lo[k] = std::min(lo[k], y[j * d + k]), hi[k] = std::max(hi[k], y[j * d + k]);
+    GridSpec gs{};
+    gs.d = d;
+    for (int k = 0; k < d; ++k) {
+      gs.origin[k] = lo[k];
+      gs.center[k] = 0.5 * (lo[k] + hi[k]);
+    }
+    gs.cell = msot_auto_cell(lo, hi, d, n, m);
+    // rows sorted by Morton cube id (compact tiles), as in the solver
+    double* dx64 = c->buf<double>("pa.x64", n * d);
+    double* da64 = c->buf<double>("pa.a64", n);
+    CK(cudaMemcpyAsync(dx64, x, n * d * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(da64, a, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    DMeasure MX;
+    prepare_measure(c, "pa", dx64, da64, n, d, gs, false, MX);
+    std::vector<int32_t> perm(n);
+    CK(cudaMemcpyAsync(perm.data(), MX.perm, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<float4> yp(m), pay(m);
+    std::vector<float> yl(m), gg(m), ff(n);
+    for (int64_t s = 0; s < n; ++s) ff[s] = static_cast<float>(f[perm[s]]);
+    for (int64_t j = 0; j < m; ++j) {
+      float q[3] = {0, 0, 0};
+      for (int k = 0; k < d; ++k) q[k] = static_cast<float>(y[j * d + k] - gs.center[k]);
+      yp[j] = make_float4(q[0], q[1], q[2], 0.f);
+      yl[j] = static_cast<float>(std::log2(b[j]));
+      gg[j] = static_cast<float>(g[j]);
+      pay[j] = make_float4(static_cast<float>(v[j]), 0.f, 0.f, 0.f);
+    }
+    float4* dyp = c->buf<float4>("pa.y", m);
+    float4* dpay = c->buf<float4>("pa.v", m);
+    float* dyl = c->buf<float>("pa.yl", m);
+    float* dg = c->buf<float>("pa.g", m);
+    float* df = c->buf<float>("pa.f", n);
+    float4* dout = c->buf<float4>("pa.out", n);
+    CK(cudaMemcpyAsync(dyp, yp.data(), m * sizeof(float4), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dpay, pay.data(), m * sizeof(float4), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dyl, yl.data(), m * sizeof(float), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dg, gg.data(), m * sizeof(float), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(df, ff.data(), n * sizeof(float), cudaMemcpyHostToDevice, st));
+    RangeSet R;
+    dense_rangeset(c, "pa.r", n, m, R);
+    const ProbSpec spec{MX.pts, n, dyp, dyl, m, &R};
+    const float* fr[1] = {df};
+    const float* gc[1] = {dg};
+    const float4* py[1] = {dpay};
+    float4* po[1] = {dout};
+    plan_group(c, "ppa", 1, &spec, fr, gc, py, po, eps, d);
+    std::vector<float4> o(n);
+    CK(cudaMemcpyAsync(o.data(), dout, n * sizeof(float4), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    // row_plan = {sum_j pi_ij / a_i, sum_j pi_ij v_j / a_i, ...}
+    for (int64_t s = 0; s < n; ++s) out[perm[s]] = a[perm[s]] * static_cast<double>(o[s].y);
+  });
+}
+
 int msot_grid_cluster(msot_ctx* c, const double* x, const double* w, int64_t n, int d,
                       const double* origin, double cell, int32_t* perm, int32_t* labels,
                       int32_t* offsets, int32_t* k_out, double* centroids, double* cweights,

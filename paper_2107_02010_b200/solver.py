@@ -73,6 +73,8 @@ def lib():
         L.msot_resolve_flips.argtypes = [_dp, _dp, C.c_int64, C.c_int, _ip, _ip, _dp, _dp,
                                          _ip]
         L.msot_classify.argtypes = [_dp, _dp, C.c_int64, C.c_int, C.c_double, _ip, _dp]
+        L.msot_plan_apply.argtypes = [C.c_void_p, _dp, _dp, C.c_int64, _dp, _dp, C.c_int64,
+                                      C.c_int, _dp, _dp, C.c_double, _dp, _dp]
         _LIB = L
     return _LIB
 
@@ -82,7 +84,8 @@ EXPORTS = ["msot_last_error", "msot_params_default", "msot_create", "msot_nccl_u
            "msot_create_dist", "msot_destroy", "msot_set_profiling", "msot_schedule",
            "msot_shard_tiles", "msot_softmin", "msot_grid_cluster", "msot_truncation_mask",
            "msot_sinkhorn", "msot_sinkhorn_device", "msot_probe_ex2", "msot_sinkhorn_grad",
-           "msot_barycenter", "msot_transfer_labels", "msot_resolve_flips", "msot_classify"]
+           "msot_barycenter", "msot_transfer_labels", "msot_resolve_flips", "msot_classify",
+           "msot_plan_apply"]
 
 
 def _check(rc):
@@ -135,6 +138,27 @@ class SoftLabels:
 
 
 OUTLIER = -1  # classify(): label of rows whose mass is below tau
+
+
+def plan_entry(i, j, x, a, y, b, duals):
+    """a_i b_j exp((f_i + g_j - C(x_i, y_j)) / eps), p = 2 (host)."""
+    x, y = np.atleast_2d(_c64(x)), np.atleast_2d(_c64(y))
+    if x.shape[0] == 1 and x.shape[1] != y.shape[1]:
+        x, y = x.T, y.T
+    c = 0.5 * float(((x[i] - y[j]) ** 2).sum())
+    return float(a[i] * b[j] * math.exp((duals.b_yx[i] + duals.a_xy[j] - c) / duals.eps))
+
+
+def grad_weights(prm, a, b, duals):
+    """gradient of S with respect to the weights of alpha with
+    the potentials frozen: (rho + eps/2)(exp(-a_xx/rho) - exp(-b_yx/rho)) for a
+    finite reach, b_yx - a_xx + eps (sum a - sum b) for reach = inf (host)."""
+    a, b = _c64(a), _c64(b)
+    eps = duals.eps
+    if math.isinf(prm.reach) or prm.reach <= 0:
+        return duals.b_yx - duals.a_xx + eps * (a.sum() - b.sum())
+    rho = prm.reach ** prm.p
+    return (rho + eps / 2) * (np.exp(-duals.a_xx / rho) - np.exp(-duals.b_yx / rho))
 
 
 def resolve_flips(soft, flip_of, orientation):
@@ -342,6 +366,35 @@ class Context:
                                           y.shape[0], d, lab.ctypes.data_as(_ip), L,
                                           _d(scores), _d(mass), C.byref(loss), C.byref(st)))
         return SoftLabels(scores, mass), loss.value, st.as_dict()
+
+    # -- plan_apply
+    def plan_apply(self, x, a, y, b, f, g, eps, v):
+        """(pi v)_i = sum_j a_i b_j exp((f_i + g_j - C_ij)/eps) v_j on the GPU."""
+        x, a, y, b, f, g, v = map(_c64, (x, a, y, b, f, g, v))
+        if x.ndim == 1:
+            x = x[:, None]
+        if y.ndim == 1:
+            y = y[:, None]
+        n, d = x.shape
+        out = np.zeros(n)
+        _check(lib().msot_plan_apply(self._h, _d(x), _d(a), n, _d(y), _d(b), y.shape[0], d,
+                                     _d(f), _d(g), eps, _d(v), _d(out)))
+        return out
+
+    def ot_value(self, prm, x, a, y, b, duals):
+        """SPEC.md:184-192: the dual objective of Eq. (3) at (f, g) = (b_yx, a_xy);
+        reach = inf uses the limit <a,f> + <b,g> + eps <a x b, 1 - exp((f+g-C)/eps)>,
+        whose plan mass comes from plan_apply(1)."""
+        eps = duals.eps
+        f, g = duals.b_yx, duals.a_xy
+        a, b = _c64(a), _c64(b)
+        if math.isinf(prm.reach) or prm.reach <= 0:
+            mass = self.plan_apply(x, a, y, b, f, g, eps, np.ones(len(b))).sum()
+            return float(a @ f + b @ g + eps * (a.sum() * b.sum() - mass))
+        rho = prm.reach ** prm.p  # PAPER.md eq. 3
+        mass = self.plan_apply(x, a, y, b, f, g, eps, np.ones(len(b))).sum()
+        return float(rho * (a @ (1 - np.exp(-f / rho))) + rho * (b @ (1 - np.exp(-g / rho)))
+                     + eps * (a.sum() * b.sum() - mass))
 
     def sinkhorn_device(self, prm, x_ptr, a_ptr, n, y_ptr, b_ptr, m, d):
         """Inputs already resident in HBM (float64 device pointers)."""

@@ -171,6 +171,16 @@ static void gpu_checks() {
   BarycenterResult br = barycenter({t0, t1}, init, bp, BarycenterConfig{20, 1.0, 0.0});
   CHECK(std::fabs(br.measure.point(0)[0]) < 1e-2 && std::fabs(br.measure.point(0)[1]) < 1e-2);
   CHECK(br.loss.back() <= br.loss.front());
+  // implicit plan: unit Diracs -> plan_entry = 1, ot_value = C(x, y)
+  DualPotentials du = symmetric_sinkhorn(a, b, p);
+  CHECK(std::fabs(plan_entry(0, 0, a, b, du, p) - 1.0) < 1e-3);
+  CHECK(std::fabs(plan_apply(a, b, du, p, {2.0})[0] - 2.0) < 2e-3);
+  CHECK(std::fabs(ot_value(a, b, du, p) - 0.625) < 1e-3);
+  // grad_weights: alpha = beta -> ~0
+  DualPotentials uu = symmetric_sinkhorn(u4, u4, lp);
+  bool zero = true;
+  for (double gq : grad_weights(u4, u4, uu, lp)) zero = zero && std::fabs(gq) < 1e-6 * 0.05 * 0.05 + 1e-9;
+  CHECK(zero);
 }
 
 int main(int argc, char** argv) {

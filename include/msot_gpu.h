@@ -175,6 +175,18 @@ int msot_grid_cluster(msot_ctx* ctx, const double* x, const double* w, int64_t n
                       int32_t* offsets, int32_t* k_out, double* centroids,
                       double* cweights, float* radii);
 
+/* K-means coarsening (kmeans_coarsen): farthest-point
+ * seeding from atom (seed mod N), Lloyd iterations with mass-weighted
+ * centroids until the largest centre move is < 1e-9 d (d = bounding-box
+ * diagonal) or 100 iterations; float64, ties to the lowest index.
+ * labels[i] = cluster of atom i (caller order); perm[k] = caller index of the
+ * k-th atom grouped by cluster (index order inside); offsets[0..K];
+ * centroids K x D; cweights K; radii K (max distance, rounded up); iters
+ * (nullable) = Lloyd iterations run. */
+int msot_kmeans(msot_ctx* ctx, const double* x, const double* w, int64_t n, int d, int k,
+                uint64_t seed, int32_t* perm, int32_t* offsets, int32_t* labels,
+                double* centroids, double* cweights, float* radii, int* iters);
+
 /* Truncation mask: keep (I,J) iff
  *   min(B_a, B_b) >= -theta * eps,  D = X_I - Y_J,
  *   B_a = F_I + G_J - (1/2) max(0, |D| - (r_I + r_J))^2

@@ -510,6 +510,132 @@ void oracle_softmin(const double* x, int64_t n, const double* y, int64_t m, int 
   softmin_rows(x, n, d, {y, logw_y, h, m}, eps, lambda, p, nullptr, f_out);
 }
 
+// kmeans_coarsen: farthest-point seeding from atom
+// (seed mod N), Lloyd iterations with mass-weighted centroids until the
+// largest centre move is < 1e-9 d or 100 iterations.  Distances sum
+// (x_k - c_k)^2 in coordinate order, centroid sums run over each cluster's
+// atoms in index order (the CUDA kernels' exact order, kmeans.cu).
+struct KMeans {
+  std::vector<int32_t> perm, offsets, labels;
+  Vec centroids, cweights;
+  std::vector<float> radii;
+  int iters = 0;
+};
+
+double km_dist2(const double* x, const double* c, int d) {
+  double s = 0.0;
+  for (int k = 0; k < d; ++k) {
+    const double t = x[k] - c[k];
+    s = s + t * t;
+  }
+  return s;
+}
+
+KMeans kmeans(const double* x, const double* w, int64_t n, int d, int K, uint64_t seed) {
+  KMeans r;
+  Vec c(static_cast<std::size_t>(K) * d), mind(n);
+  const int64_t s0 = static_cast<int64_t>(seed % static_cast<uint64_t>(n));
+  std::copy(x + s0 * d, x + (s0 + 1) * d, c.begin());
+  for (int k = 1; k < K; ++k) {
+    double best = -1.0;
+    int64_t bi = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      const double dd = km_dist2(x + i * d, c.data() + static_cast<int64_t>(k - 1) * d, d);
+      mind[i] = k == 1 ? dd : std::min(mind[i], dd);
+      if (mind[i] > best) {  // strict: ties keep the lowest index
+        best = mind[i];
+        bi = i;
+      }
+    }
+    std::copy(x + bi * d, x + (bi + 1) * d, c.begin() + static_cast<int64_t>(k) * d);
+  }
+  double diag2 = 0.0;
+  for (int q = 0; q < d; ++q) {
+    double lo = INFINITY, hi = -INFINITY;
+    for (int64_t i = 0; i < n; ++i) lo = std::min(lo, x[i * d + q]), hi = std::max(hi, x[i * d + q]);
+    diag2 += (hi - lo) * (hi - lo);
+  }
+  const double tol = 1e-9 * std::sqrt(diag2), tol2 = tol * tol;
+  r.labels.assign(n, 0);
+  r.cweights.assign(K, 0.0);
+  Vec c2(c.size());
+  for (;;) {
+    msot::parallel::for_ranges(static_cast<std::size_t>(n), [&](std::size_t lo, std::size_t hi) {
+      for (std::size_t i = lo; i < hi; ++i) {
+        double best = INFINITY;
+        int bl = 0;
+        for (int I = 0; I < K; ++I) {
+          const double dd = km_dist2(x + i * d, c.data() + static_cast<int64_t>(I) * d, d);
+          if (dd < best) {
+            best = dd;
+            bl = I;
+          }
+        }
+        r.labels[i] = bl;
+      }
+    });
+    r.perm.resize(n);
+    std::iota(r.perm.begin(), r.perm.end(), 0);
+    std::stable_sort(r.perm.begin(), r.perm.end(),
+                     [&](int32_t p, int32_t q) { return r.labels[p] < r.labels[q]; });
+    r.offsets.assign(K + 1, 0);
+    for (int64_t i = 0; i < n; ++i) ++r.offsets[r.labels[i] + 1];
+    for (int I = 0; I < K; ++I) r.offsets[I + 1] += r.offsets[I];
+    ++r.iters;
+    double move = 0.0;
+    for (int I = 0; I < K; ++I) {
+      const int32_t a = r.offsets[I], b = r.offsets[I + 1];
+      for (int q = 0; q < d; ++q) {
+        const int64_t g = static_cast<int64_t>(I) * d + q;
+        if (b <= a) {
+          c2[g] = c[g];
+          continue;
+        }
+        double W = 0.0, S = 0.0;
+        for (int32_t s = a; s < b; ++s) {
+          const int64_t i = r.perm[s];
+          W = W + w[i];
+          S = S + w[i] * x[i * d + q];
+        }
+        c2[g] = S / W;
+        if (q == 0) r.cweights[I] = W;
+      }
+      if (b <= a) r.cweights[I] = 0.0;
+      move = std::max(move, km_dist2(c.data() + static_cast<int64_t>(I) * d,
+                                     c2.data() + static_cast<int64_t>(I) * d, d));
+    }
+    c = c2;
+    if (move < tol2 || r.iters >= 100) break;
+  }
+  r.centroids = c;
+  r.radii.assign(K, 0.0f);
+  for (int I = 0; I < K; ++I) {
+    double m = 0.0;
+    for (int32_t s = r.offsets[I]; s < r.offsets[I + 1]; ++s)
+      m = std::max(m, km_dist2(x + static_cast<int64_t>(r.perm[s]) * d, c.data() + static_cast<int64_t>(I) * d, d));
+    // sqrt and float conversion rounded up, as __dsqrt_ru / __double2float_ru
+    double rr = std::sqrt(m);
+    if (std::fma(rr, rr, -m) < 0.0) rr = std::nextafter(rr, INFINITY);  // exact rr^2 < m
+    r.radii[I] = round_up_float(rr);
+  }
+  return r;
+}
+
+int oracle_kmeans(const double* x, const double* w, int64_t n, int d, int k, uint64_t seed,
+                  int32_t* perm, int32_t* offsets, int32_t* labels, double* centroids,
+                  double* cweights, float* radii, int* iters) {
+  if (k < 1 || k > n) return fail(MSOT_EDATA, "K must lie in [1, N]");
+  KMeans r = kmeans(x, w, n, d, k, seed);
+  std::copy(r.perm.begin(), r.perm.end(), perm);
+  std::copy(r.offsets.begin(), r.offsets.end(), offsets);
+  std::copy(r.labels.begin(), r.labels.end(), labels);
+  std::copy(r.centroids.begin(), r.centroids.end(), centroids);
+  std::copy(r.cweights.begin(), r.cweights.end(), cweights);
+  std::copy(r.radii.begin(), r.radii.end(), radii);
+  if (iters) *iters = r.iters;
+  return MSOT_OK;
+}
+
 int oracle_grid_cluster(const double* x, const double* w, int64_t n, int d, const double* origin,
                         double cell, int32_t* perm, int32_t* labels, int32_t* offsets,
                         int32_t* k_out, double* centroids, double* cweights, float* radii) {

@@ -40,6 +40,11 @@ int oracle_grid_cluster(const double* x, const double* w, int64_t n, int d,
                         int32_t* offsets, int32_t* k_out, double* centroids,
                         double* cweights, float* radii);
 
+/* K-means coarsening: same contract as msot_kmeans. */
+int oracle_kmeans(const double* x, const double* w, int64_t n, int d, int k, uint64_t seed,
+                  int32_t* perm, int32_t* offsets, int32_t* labels, double* centroids,
+                  double* cweights, float* radii, int* iters);
+
 /* Truncation mask: same contract as msot_truncation_mask. */
 void oracle_truncation_mask(int64_t kx, int64_t ky, int d, const float* cx, const float* rx,
                             const float* fx, const float* gx, const float* cy, const float* ry,

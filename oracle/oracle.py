@@ -109,6 +109,30 @@ def grid_cluster(x, w, origin, cell):
                 centroids=cen[:K].copy(), cweights=cw[:K].copy(), radii=rad[:K].copy())
 
 
+def kmeans(x, w, k, seed=0):
+    L = lib()
+    L.oracle_kmeans.restype = C.c_int
+    L.oracle_kmeans.argtypes = [_dp, _dp, C.c_int64, C.c_int, C.c_int, C.c_uint64, _ip, _ip, _ip,
+                                _dp, _dp, _fp, C.POINTER(C.c_int)]
+    x, w = _c64(x), _c64(w)
+    if x.ndim == 1:
+        x = x[:, None]
+    n, d = x.shape
+    perm = np.zeros(n, np.int32)
+    off = np.zeros(k + 1, np.int32)
+    lab = np.zeros(n, np.int32)
+    cen = np.zeros((k, d))
+    cw = np.zeros(k)
+    rad = np.zeros(k, np.float32)
+    it = C.c_int()
+    rc = L.oracle_kmeans(_d(x), _d(w), n, d, k, seed, perm.ctypes.data_as(_ip),
+                         off.ctypes.data_as(_ip), lab.ctypes.data_as(_ip), _d(cen), _d(cw),
+                         rad.ctypes.data_as(_fp), C.byref(it))
+    raise_status(rc, L.oracle_last_error().decode())
+    return dict(perm=perm, offsets=off, labels=lab, centroids=cen, cweights=cw, radii=rad,
+                iters=it.value)
+
+
 def truncation_mask(cx, rx, fx, cy, ry, gy, eps, theta, p=2.0, self_=False, gx=None, hy=None):
     f32 = lambda a: np.ascontiguousarray(a, dtype=np.float32)
     cx, rx, fx, cy, ry, gy = map(f32, (cx, rx, fx, cy, ry, gy))

@@ -1,0 +1,296 @@
+// kmeans.cu — K-means coarsening of high-dimensional measures
+// (kmeans_coarsen; "a simple K-means
+// algorithm"): the coarse measure of the multiscale solver when the voxel
+// grid does not apply (D > 3, the D = 60 fibre features of config 4).
+//
+//   seeding   farthest-point: the first centre is atom (seed mod N), then
+//             repeatedly the atom farthest from all chosen centres (ties to
+//             the lowest index)
+//   Lloyd     assign every atom to its nearest centre (ties to the lowest
+//             centre), mass-weighted centroids, until the largest centre
+//             move is below 1e-9 d or 100 iterations
+//
+// Every distance is sum_k (x_k - c_k)^2 in float64 in a fixed order with
+// explicitly rounded operations (no FMA), and every centroid sum runs
+// sequentially over the cluster's atoms in index order, so labels, centroids
+// and radii are bit-identical to oracle.cpp:kmeans on the same input.
+#include "prims.cuh"
+
+namespace msot_dev {
+
+constexpr int kKmDmax = 64;
+
+__device__ __forceinline__ double km_dist2(const double* x, const double* c, int d) {
+  double s = 0.0;
+  for (int k = 0; k < d; ++k) {
+    const double t = __dsub_rn(x[k], c[k]);
+    s = __dadd_rn(s, __dmul_rn(t, t));
+  }
+  return s;
+}
+
+// farthest-point step: mind_i = min(mind_i, |x_i - c|^2); per-block argmax
+// (largest, then lowest index)
+__global__ void fps_update_kernel(const double* x, int64_t n, int d, const double* c, double* mind,
+                                  int first, double* bval, int64_t* bidx) {
+  __shared__ double sv[256];
+  __shared__ int64_t si[256];
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  double m = -1.0;
+  int64_t mi = INT64_MAX;
+  if (i < n) {
+    const double dd = km_dist2(x + i * d, c, d);
+    m = first ? dd : fmin(mind[i], dd);
+    mind[i] = m;
+    mi = i;
+  }
+  sv[threadIdx.x] = m;
+  si[threadIdx.x] = mi;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const double v2 = sv[threadIdx.x + o];
+      const int64_t i2 = si[threadIdx.x + o];
+      if (v2 > sv[threadIdx.x] || (v2 == sv[threadIdx.x] && i2 < si[threadIdx.x])) {
+        sv[threadIdx.x] = v2;
+        si[threadIdx.x] = i2;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    bval[blockIdx.x] = sv[0];
+    bidx[blockIdx.x] = si[0];
+  }
+}
+
+// global argmax over the blocks; the winner becomes centre k
+__global__ void fps_select_kernel(const double* bval, const int64_t* bidx, int nb, const double* x,
+                                  int d, double* centers, int k) {
+  __shared__ double sv[256];
+  __shared__ int64_t si[256];
+  double m = -2.0;
+  int64_t mi = INT64_MAX;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x)
+    if (bval[b] > m || (bval[b] == m && bidx[b] < mi)) {
+      m = bval[b];
+      mi = bidx[b];
+    }
+  sv[threadIdx.x] = m;
+  si[threadIdx.x] = mi;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const double v2 = sv[threadIdx.x + o];
+      const int64_t i2 = si[threadIdx.x + o];
+      if (v2 > sv[threadIdx.x] || (v2 == sv[threadIdx.x] && i2 < si[threadIdx.x])) {
+        sv[threadIdx.x] = v2;
+        si[threadIdx.x] = i2;
+      }
+    }
+    __syncthreads();
+  }
+  const int64_t w = si[0];
+  for (int q = threadIdx.x; q < d; q += blockDim.x) centers[static_cast<int64_t>(k) * d + q] = x[w * d + q];
+}
+
+__global__ void copy_center_kernel(const double* x, int64_t i, int d, double* c) {
+  for (int q = threadIdx.x; q < d; q += blockDim.x) c[q] = x[i * d + q];
+}
+
+// nearest centre of every atom (ties to the lowest centre); centres staged
+// through shared memory in chunks, the atom's coordinates in registers
+template <int DM>
+__global__ void __launch_bounds__(128) km_assign_kernel(const double* x, int64_t n, int d,
+                                                        const double* centers, int K,
+                                                        uint32_t* labels) {
+  constexpr int kChunk = 32;
+  __shared__ double cs[kChunk * DM];
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  double xr[DM];
+#pragma unroll
+  for (int k = 0; k < DM; ++k) xr[k] = (i < n && k < d) ? x[i * d + k] : 0.0;
+  double best = INFINITY;
+  int bl = 0;
+  for (int c0 = 0; c0 < K; c0 += kChunk) {
+    const int nc = min(kChunk, K - c0);
+    __syncthreads();
+    for (int q = threadIdx.x; q < nc * d; q += blockDim.x)
+      cs[(q / d) * DM + (q % d)] = centers[static_cast<int64_t>(c0) * d + q];
+    __syncthreads();
+    for (int c = 0; c < nc; ++c) {
+      const double* cc = cs + c * DM;
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < DM; ++k)
+        if (k < d) {
+          const double t = __dsub_rn(xr[k], cc[k]);
+          s = __dadd_rn(s, __dmul_rn(t, t));
+        }
+      if (s < best) {  // strict: ties keep the lowest centre
+        best = s;
+        bl = c0 + c;
+      }
+    }
+  }
+  if (i < n) labels[i] = static_cast<uint32_t>(bl);
+}
+
+// mass-weighted centroids: one thread per (cluster, coordinate), sequential
+// over the cluster's atoms (sorted by label, stable: index order); empty
+// clusters keep their centre.  move[I] = |c_new - c_old|^2 (coordinate 0's
+// thread, after the others finished via a second kernel).
+__global__ void km_centroid_kernel(const double* x, const double* w, const int32_t* perm,
+                                   const int32_t* off, int K, int d, const double* old_c,
+                                   double* new_c, double* cw) {
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g >= static_cast<int64_t>(K) * d) return;
+  const int I = static_cast<int>(g / d), q = static_cast<int>(g % d);
+  const int32_t s0 = off[I], s1 = off[I + 1];
+  if (s1 <= s0) {
+    new_c[g] = old_c[g];
+    if (q == 0) cw[I] = 0.0;
+    return;
+  }
+  double W = 0.0, S = 0.0;
+  for (int32_t s = s0; s < s1; ++s) {
+    const int64_t i = perm[s];
+    W = __dadd_rn(W, w[i]);
+    S = __dadd_rn(S, __dmul_rn(w[i], x[i * d + q]));
+  }
+  new_c[g] = __ddiv_rn(S, W);
+  if (q == 0) cw[I] = W;
+}
+
+__global__ void km_move_kernel(const double* a, const double* b, int K, int d, double* out) {
+  __shared__ double sm[256];
+  double m = 0.0;
+  for (int I = threadIdx.x; I < K; I += blockDim.x) m = fmax(m, km_dist2(a + static_cast<int64_t>(I) * d, b + static_cast<int64_t>(I) * d, d));
+  sm[threadIdx.x] = m;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sm[threadIdx.x] = fmax(sm[threadIdx.x], sm[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sm[0];
+}
+
+// radius of each cluster: max |x - c| over its atoms, rounded up to float
+__global__ void km_radius_kernel(const double* x, const int32_t* perm, const int32_t* off, int K,
+                                 int d, const double* c, float* radii) {
+  const int lane = threadIdx.x & 31;
+  const int64_t I = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (I >= K) return;
+  double r = 0.0;
+  for (int32_t s = off[I] + lane; s < off[I + 1]; s += 32)
+    r = fmax(r, km_dist2(x + static_cast<int64_t>(perm[s]) * d, c + I * d, d));
+  for (int o = 16; o > 0; o >>= 1) r = fmax(r, __shfl_xor_sync(0xffffffffu, r, o));
+  if (lane == 0) {
+    const double rr = __dsqrt_ru(r);
+    float f = __double2float_ru(rr);
+    radii[I] = f;
+  }
+}
+
+__global__ void iota_kernel(int32_t* v, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = static_cast<int32_t>(i);
+}
+
+// offsets of the label-sorted atoms: off[I] = first sorted position of label I
+__global__ void km_offsets_kernel(const uint32_t* sorted_labels, int64_t n, int K, int32_t* off) {
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const uint32_t l = sorted_labels[s];
+  const uint32_t prev = s == 0 ? 0xffffffffu : sorted_labels[s - 1];
+  if (s == 0)
+    for (uint32_t q = 0; q <= l; ++q) off[q] = 0;
+  else if (l != prev)
+    for (uint32_t q = prev + 1; q <= l; ++q) off[q] = static_cast<int32_t>(s);
+  if (s == n - 1)
+    for (uint32_t q = l + 1; q <= static_cast<uint32_t>(K); ++q) off[q] = static_cast<int32_t>(n);
+}
+
+// scratch: see kmeans_ws_bytes
+cudaError_t kmeans(const double* x, const double* w, int64_t n, int d, int K, uint64_t seed,
+                   double tol2, int max_iter, void* ws, int32_t* perm, int32_t* off,
+                   uint32_t* labels, double* centers, double* cw, float* radii, int* iters,
+                   cudaStream_t st) {
+  if (n <= 0 || K <= 0 || K > n || d < 1 || d > kKmDmax) return cudaErrorInvalidValue;
+  const int nb = static_cast<int>((n + 255) / 256);
+  char* p = static_cast<char*>(ws);
+  double* mind = reinterpret_cast<double*>(p);
+  p += n * sizeof(double);
+  double* bval = reinterpret_cast<double*>(p);
+  p += nb * sizeof(double);
+  int64_t* bidx = reinterpret_cast<int64_t*>(p);
+  p += nb * sizeof(int64_t);
+  double* c2 = reinterpret_cast<double*>(p);
+  p += static_cast<size_t>(K) * d * sizeof(double);
+  double* mv = reinterpret_cast<double*>(p);
+  p += 2 * sizeof(double);
+  uint32_t* keys = reinterpret_cast<uint32_t*>(p);
+  p += n * sizeof(uint32_t);
+  void* rtmp = p;
+  // farthest-point seeding
+  ++g_launches;
+  copy_center_kernel<<<1, 64, 0, st>>>(x, static_cast<int64_t>(seed % static_cast<uint64_t>(n)), d,
+                                       centers);
+  for (int k = 1; k < K; ++k) {
+    ++g_launches;
+    fps_update_kernel<<<nb, 256, 0, st>>>(x, n, d, centers + static_cast<int64_t>(k - 1) * d, mind,
+                                          k == 1, bval, bidx);
+    ++g_launches;
+    fps_select_kernel<<<1, 256, 0, st>>>(bval, bidx, nb, x, d, centers, k);
+  }
+  const int kb = static_cast<int>((static_cast<int64_t>(K) * d + 255) / 256);
+  int it = 0;
+  const int key_bits = K <= 1 ? 1 : 32 - __builtin_clz(static_cast<unsigned>(K - 1));
+  for (;;) {
+    // assignment to the current centres, then the clusters in index order
+    ++g_launches;
+    if (d <= 16)
+      km_assign_kernel<16><<<static_cast<unsigned>((n + 127) / 128), 128, 0, st>>>(x, n, d, centers, K, labels);
+    else if (d <= 32)
+      km_assign_kernel<32><<<static_cast<unsigned>((n + 127) / 128), 128, 0, st>>>(x, n, d, centers, K, labels);
+    else
+      km_assign_kernel<64><<<static_cast<unsigned>((n + 127) / 128), 128, 0, st>>>(x, n, d, centers, K, labels);
+    cudaError_t e = cudaMemcpyAsync(keys, labels, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return e;
+    ++g_launches;
+    iota_kernel<<<nb, 256, 0, st>>>(perm, n);
+    e = radix_sort_pairs(keys, perm, n, key_bits, rtmp, st);
+    if (e != cudaSuccess) return e;
+    ++g_launches;
+    km_offsets_kernel<<<nb, 256, 0, st>>>(keys, n, K, off);
+    ++it;
+    // mass-weighted means of this assignment become the centres
+    ++g_launches;
+    km_centroid_kernel<<<kb, 256, 0, st>>>(x, w, perm, off, K, d, centers, c2, cw);
+    ++g_launches;
+    km_move_kernel<<<1, 256, 0, st>>>(centers, c2, K, d, mv);
+    e = cudaMemcpyAsync(centers, c2, static_cast<size_t>(K) * d * sizeof(double),
+                        cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return e;
+    double hm = 0.0;
+    e = cudaMemcpyAsync(&hm, mv, sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return e;
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return e;
+    if (hm < tol2 || it >= max_iter) break;
+  }
+  ++g_launches;
+  km_radius_kernel<<<static_cast<unsigned>((static_cast<int64_t>(K) * 32 + 255) / 256), 256, 0, st>>>(
+      x, perm, off, K, d, centers, radii);
+  if (iters) *iters = it;
+  return cudaGetLastError();
+}
+
+size_t kmeans_ws_bytes(int64_t n, int d, int K) {
+  const int64_t nb = (n + 255) / 256;
+  return static_cast<size_t>(n) * sizeof(double) + nb * (sizeof(double) + sizeof(int64_t)) +
+         static_cast<size_t>(K) * d * sizeof(double) + 2 * sizeof(double) +
+         static_cast<size_t>(n) * sizeof(uint32_t) + radix_temp_bytes(n) + 256;
+}
+
+}  // namespace msot_dev

@@ -124,6 +124,15 @@ cudaError_t cluster_bound(const float4* pts, const double* w64, const float* f,
 cudaError_t inherit(const float* coarse, const int32_t* labels, int64_t n, float* fine,
                     cudaStream_t st);
 
+// K-means coarsening (kmeans.cu), float64, bit-identical to the oracle.
+// perm: atoms grouped by cluster (index order inside), off[K+1], labels per
+// atom (caller order), centers K x d, cw cluster weights, radii (rounded up).
+size_t kmeans_ws_bytes(int64_t n, int d, int K);
+cudaError_t kmeans(const double* x, const double* w, int64_t n, int d, int K, uint64_t seed,
+                   double tol2, int max_iter, void* ws, int32_t* perm, int32_t* off,
+                   uint32_t* labels, double* centers, double* cw, float* radii, int* iters,
+                   cudaStream_t st);
+
 // truncation mask + ranges (mask.cu)
 __host__ __device__ inline int32_t mask_words(int32_t ky) { return (ky + 31) / 32; }
 // bit-packed mask: Kx rows of mask_words(Ky) uint32 words

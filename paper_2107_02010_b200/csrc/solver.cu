@@ -1961,6 +1961,50 @@ int msot_plan_apply(msot_ctx* c, const double* x, const double* a, int64_t n, co
   });
 }
 
+int msot_kmeans(msot_ctx* c, const double* x, const double* w, int64_t n, int d, int k,
+                uint64_t seed, int32_t* perm, int32_t* offsets, int32_t* labels, double* centroids,
+                double* cweights, float* radii, int* iters) {
+  return guard([&] {
+    if (!c || !x || !w || !perm || !offsets || !labels || !centroids || !cweights || !radii)
+      raise(MSOT_EUSAGE, "null argument");
+    if (n < 1) raise(MSOT_EDATA, "empty measure");
+    if (k < 1 || k > n) raise(MSOT_EDATA, "K must lie in [1, N] (SPEC.md:263)");
+    if (d < 1 || d > 64) raise(MSOT_EUSAGE, "K-means supports D in 1..64");
+    check_weights(w, n);
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->st;
+    double* dx = c->buf<double>("km.x", n * d);
+    double* dw = c->buf<double>("km.w", n);
+    CK(cudaMemcpyAsync(dx, x, n * d * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dw, w, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    // tolerance 1e-9 d on the centre moves, d = bbox diagonal
+    std::vector<double> lo(d, INFINITY), hi(d, -INFINITY);
+    for (int64_t i = 0; i < n; ++i)
+      for (int q = 0; q < d; ++q) lo[q] = std::min(lo[q], x[i * d + q]), hi[q] = std::max(hi[q], x[i * d + q]);
+    double diag2 = 0.0;
+    for (int q = 0; q < d; ++q) diag2 += (hi[q] - lo[q]) * (hi[q] - lo[q]);
+    const double tol = 1e-9 * std::sqrt(diag2);
+    int32_t* dperm = c->buf<int32_t>("km.perm", n);
+    int32_t* doff = c->buf<int32_t>("km.off", k + 1);
+    uint32_t* dlab = c->buf<uint32_t>("km.lab", n);
+    double* dcen = c->buf<double>("km.cen", size_t(k) * d);
+    double* dcw = c->buf<double>("km.cw", k);
+    float* drad = c->buf<float>("km.rad", k);
+    void* ws = c->buf<char>("km.ws", kmeans_ws_bytes(n, d, k));
+    int it = 0;
+    CK(kmeans(dx, dw, n, d, k, seed, tol * tol, 100, ws, dperm, doff, dlab, dcen, dcw, drad, &it,
+              st));
+    CK(cudaMemcpyAsync(perm, dperm, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(offsets, doff, (k + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(labels, dlab, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(centroids, dcen, size_t(k) * d * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(cweights, dcw, k * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(radii, drad, k * sizeof(float), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (iters) *iters = it;
+  });
+}
+
 int msot_grid_cluster(msot_ctx* c, const double* x, const double* w, int64_t n, int d,
                       const double* origin, double cell, int32_t* perm, int32_t* labels,
                       int32_t* offsets, int32_t* k_out, double* centroids, double* cweights,

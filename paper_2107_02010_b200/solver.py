@@ -73,6 +73,8 @@ def lib():
         L.msot_resolve_flips.argtypes = [_dp, _dp, C.c_int64, C.c_int, _ip, _ip, _dp, _dp,
                                          _ip]
         L.msot_classify.argtypes = [_dp, _dp, C.c_int64, C.c_int, C.c_double, _ip, _dp]
+        L.msot_kmeans.argtypes = [C.c_void_p, _dp, _dp, C.c_int64, C.c_int, C.c_int, C.c_uint64,
+                                  _ip, _ip, _ip, _dp, _dp, _fp, C.POINTER(C.c_int)]
         L.msot_plan_apply.argtypes = [C.c_void_p, _dp, _dp, C.c_int64, _dp, _dp, C.c_int64,
                                       C.c_int, _dp, _dp, C.c_double, _dp, _dp]
         _LIB = L
@@ -85,7 +87,7 @@ EXPORTS = ["msot_last_error", "msot_params_default", "msot_create", "msot_nccl_u
            "msot_shard_tiles", "msot_softmin", "msot_grid_cluster", "msot_truncation_mask",
            "msot_sinkhorn", "msot_sinkhorn_device", "msot_probe_ex2", "msot_sinkhorn_grad",
            "msot_barycenter", "msot_transfer_labels", "msot_resolve_flips", "msot_classify",
-           "msot_plan_apply"]
+           "msot_plan_apply", "msot_kmeans"]
 
 
 def _check(rc):
@@ -265,6 +267,25 @@ class Context:
         K = k.value
         return dict(perm=perm, labels=labels, offsets=offsets[:K + 1].copy(), k=K,
                     centroids=cen[:K].copy(), cweights=cw[:K].copy(), radii=rad[:K].copy())
+
+    # -- kmeans_coarsen
+    def kmeans(self, x, w, k, seed=0):
+        x, w = _c64(x), _c64(w)
+        if x.ndim == 1:
+            x = x[:, None]
+        n, d = x.shape
+        perm = np.zeros(n, np.int32)
+        off = np.zeros(k + 1, np.int32)
+        lab = np.zeros(n, np.int32)
+        cen = np.zeros((k, d))
+        cw = np.zeros(k)
+        rad = np.zeros(k, np.float32)
+        it = C.c_int()
+        _check(lib().msot_kmeans(self._h, _d(x), _d(w), n, d, k, seed, perm.ctypes.data_as(_ip),
+                                 off.ctypes.data_as(_ip), lab.ctypes.data_as(_ip), _d(cen), _d(cw),
+                                 rad.ctypes.data_as(_fp), C.byref(it)))
+        return dict(perm=perm, offsets=off, labels=lab, centroids=cen, cweights=cw, radii=rad,
+                    iters=it.value)
 
     # -- kernel_truncation on explicit coarse inputs (K3)
     def kernel_truncation(self, cx, rx, fx, cy, ry, gy, eps, theta, self_=False, gx=None,

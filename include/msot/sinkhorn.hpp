@@ -29,6 +29,9 @@ struct SolverParams {
   double switch_factor = 2.0;
   int mask_rule = 0;
   int transfer_rule = 0;
+  int pair_eval = 1;   // evaluate-once fine phase
+  int clusters = 0;    // D > 3: K-means clusters per measure (0 = ceil(sqrt(N)))
+  int seed = 0;        // K-means seeding
 
   msot_params to_c() const;
 };

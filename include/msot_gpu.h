@@ -62,6 +62,9 @@ typedef struct msot_params {
                             cross kernel is shared by a_xy / b_yx and the
                             self kernels are symmetric), 0 = one row-wise
                             problem per potential (4 per scale)              */
+  int32_t clusters;      /* D > 3 multiscale: K-means clusters per measure, 0 =
+                            ceil(sqrt(N))                       */
+  int32_t seed;          /* K-means seeding: first centre = atom (seed mod N)  */
 } msot_params;
 
 /* Defaults of SPEC.md:128 (q=0.9), :306 (switch 2x radius), :308 (theta=20). */

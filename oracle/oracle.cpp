@@ -342,6 +342,47 @@ void cluster_bound(const Vec& f, const Measure& M, const Clusters& c,
   }
 }
 
+// High-D truncation mask (csrc/mask.cu: mask_hd_rows_kernel): B_a with
+// float64 centroids, |X - Y|^2 summed in coordinate order, best pairs (ties to
+// the lowest index) of every row and column, the diagonal of self masks.
+double hd_pair_slack(const double* X, float rI, float F, const double* Y, float rJ, float G, int d) {
+  double s = 0.0;
+  for (int k = 0; k < d; ++k) {
+    const double t = X[k] - Y[k];
+    s = s + t * t;
+  }
+  const double rr = static_cast<double>(rI) + static_cast<double>(rJ);
+  double lb = std::sqrt(s) - rr;
+  if (lb < 0.0) lb = 0.0;
+  const double fg = static_cast<double>(F) + static_cast<double>(G);
+  return fg - 0.5 * (lb * lb);
+}
+
+void hd_mask(int64_t kx, int64_t ky, int d, const double* cx, const float* rx, const float* fx,
+             const double* cy, const float* ry, const float* gy, double eps, double theta,
+             int self, std::vector<uint8_t>& mask) {
+  const double thr = -(theta * eps);
+  mask.assign(size_t(kx) * ky, 0);
+  std::vector<double> v(size_t(kx) * ky);
+  for (int64_t I = 0; I < kx; ++I)
+    for (int64_t J = 0; J < ky; ++J) {
+      v[I * ky + J] = hd_pair_slack(cx + I * d, rx[I], fx[I], cy + J * d, ry[J], gy[J], d);
+      mask[I * ky + J] = (self && I == J) || v[I * ky + J] >= thr;
+    }
+  for (int64_t I = 0; I < kx; ++I) {
+    int64_t bj = -1;
+    for (int64_t J = 0; J < ky; ++J)
+      if (bj < 0 || v[I * ky + J] > v[I * ky + bj]) bj = J;
+    if (bj >= 0 && v[I * ky + bj] > -std::numeric_limits<double>::infinity()) mask[I * ky + bj] = 1;
+  }
+  for (int64_t J = 0; J < ky; ++J) {
+    int64_t bi = -1;
+    for (int64_t I = 0; I < kx; ++I)
+      if (bi < 0 || v[I * ky + J] > v[bi * ky + J]) bi = I;
+    if (bi >= 0 && v[bi * ky + J] > -std::numeric_limits<double>::infinity()) mask[bi * ky + J] = 1;
+  }
+}
+
 // Column ranges of every cluster-aligned row tile: the union of the kept
 // column clusters of the row clusters the tile covers, as runs of sorted
 // column indices [co[J0], co[J1+1]).
@@ -531,7 +572,8 @@ double km_dist2(const double* x, const double* c, int d) {
   return s;
 }
 
-KMeans kmeans(const double* x, const double* w, int64_t n, int d, int K, uint64_t seed) {
+KMeans kmeans(const double* x, const double* w, int64_t n, int d, int K, uint64_t seed,
+              int max_iter = 100) {
   KMeans r;
   Vec c(static_cast<std::size_t>(K) * d), mind(n);
   const int64_t s0 = static_cast<int64_t>(seed % static_cast<uint64_t>(n));
@@ -605,7 +647,7 @@ KMeans kmeans(const double* x, const double* w, int64_t n, int d, int K, uint64_
                                      c2.data() + static_cast<int64_t>(I) * d, d));
     }
     c = c2;
-    if (move < tol2 || r.iters >= 100) break;
+    if (move < tol2 || r.iters >= max_iter) break;
   }
   r.centroids = c;
   r.radii.assign(K, 0.0f);
@@ -722,8 +764,144 @@ int oracle_sinkhorn(const msot_params* prm, const double* x, const double* a, in
   const double full = double(n) * n + double(m) * m + 2.0 * double(n) * m;
 
   std::vector<int32_t> px, py;
-  if (!prm->multiscale || d > 3) {
-    if (prm->multiscale) return fail(MSOT_EUSAGE, "voxel-grid multiscale supports D <= 3");
+  if (prm->multiscale && d > 3) {
+    // ---- high-D multiscale (csrc/solver.cu: hd_multiscale): K-means
+    // coarsening, every cluster padded to a multiple of 128 atoms (centroid
+    // coordinates, weight 0) exactly as the GPU layout, dense coarse phase,
+    // inheritance, centroid/radius masks, evaluate-once pair sets.
+    if (prm->pair_eval == 0) return fail(MSOT_EUSAGE, "high-D multiscale runs the evaluate-once scheme");
+    struct Pad {
+      int K = 0;
+      int64_t npad = 0;
+      std::vector<int32_t> poff, src, labels;
+      KMeans km;
+      Measure M;
+    };
+    auto layout = [&](const double* xx, const double* ww, int64_t cnt) {
+      Pad P;
+      P.K = prm->clusters > 0 ? static_cast<int>(std::min<int64_t>(prm->clusters, cnt))
+                              : static_cast<int>(std::ceil(std::sqrt(static_cast<double>(cnt))));
+      P.km = kmeans(xx, ww, cnt, d, P.K, static_cast<uint64_t>(prm->seed), MSOT_KMEANS_SOLVER_ITERS);
+      P.poff.assign(P.K + 1, 0);
+      for (int I = 0; I < P.K; ++I)
+        P.poff[I + 1] = P.poff[I] + (P.km.offsets[I + 1] - P.km.offsets[I] + 127) / 128 * 128;
+      P.npad = P.poff[P.K];
+      P.src.assign(P.npad, 0);
+      P.labels.assign(P.npad, 0);
+      P.M.n = P.npad;
+      P.M.pts.assign(P.npad * d, 0.0);
+      P.M.w.assign(P.npad, 0.0);
+      P.M.logw.assign(P.npad, -std::numeric_limits<double>::infinity());
+      for (int I = 0; I < P.K; ++I) {
+        const int32_t c0 = P.km.offsets[I], cn = P.km.offsets[I + 1] - c0;
+        for (int32_t q = 0; q < P.poff[I + 1] - P.poff[I]; ++q) {
+          const int64_t s = P.poff[I] + q;
+          P.labels[s] = I;
+          if (q < cn) {
+            const int32_t i = P.km.perm[c0 + q];
+            P.src[s] = i;
+            std::copy(xx + int64_t(i) * d, xx + int64_t(i + 1) * d, P.M.pts.begin() + s * d);
+            P.M.w[s] = ww[i];
+            P.M.logw[s] = std::log(ww[i]);
+          } else {
+            P.src[s] = -(I + 1);
+            std::copy(P.km.centroids.begin() + int64_t(I) * d,
+                      P.km.centroids.begin() + int64_t(I + 1) * d, P.M.pts.begin() + s * d);
+          }
+        }
+      }
+      return P;
+    };
+    Pad PX = layout(x, a, n), PY = layout(y, b, m);
+    S.kx = PX.K;
+    S.ky = PY.K;
+    double rmax = 0.0;
+    for (float r : PX.km.radii) rmax = std::max(rmax, double(r));
+    for (float r : PY.km.radii) rmax = std::max(rmax, double(r));
+    const int tsw = msot_switch_index(sig.data(), ns, rmax, prm->switch_factor);
+    S.t_switch = tsw;
+    auto coarse_measure = [&](const Pad& P) {
+      Measure C;
+      C.n = P.K;
+      C.pts = P.km.centroids;
+      C.w = P.km.cweights;
+      C.logw.resize(P.K);
+      for (int I = 0; I < P.K; ++I) C.logw[I] = std::log(C.w[I]);
+      return C;
+    };
+    Measure Xc = coarse_measure(PX), Yc = coarse_measure(PY);
+    Duals cu{Vec(PX.K, 0.0), Vec(PY.K, 0.0), Vec(PY.K, 0.0), Vec(PX.K, 0.0)};
+    for (int t = 0; t < tsw; ++t) {
+      const double pr = sym_update(Xc, Yc, d, cu, eps[t], lam[t], p, false, nullptr, nullptr,
+                                   nullptr, nullptr);
+      if (pr < 0) return fail(MSOT_ENUMERIC, "non-finite potential at scale " + std::to_string(t));
+      S.pairs_evaluated += pr;
+    }
+    Duals fu{Vec(PX.npad, 0.0), Vec(PY.npad, 0.0), Vec(PY.npad, 0.0), Vec(PX.npad, 0.0)};
+    if (tsw > 0 && prm->transfer_rule == 1) {  // extrapolation (GeomLoss)
+      const int te = tsw - 1;
+      const double e = eps[te], l = lam[te];
+      S.pairs_evaluated += softmin_rows(PX.M.pts.data(), PX.npad, d, {Xc.pts.data(), Xc.logw.data(), cu.a_xx.data(), PX.K}, e, l, p, nullptr, fu.a_xx.data());
+      S.pairs_evaluated += softmin_rows(PY.M.pts.data(), PY.npad, d, {Yc.pts.data(), Yc.logw.data(), cu.b_yy.data(), PY.K}, e, l, p, nullptr, fu.b_yy.data());
+      S.pairs_evaluated += softmin_rows(PY.M.pts.data(), PY.npad, d, {Xc.pts.data(), Xc.logw.data(), cu.b_yx.data(), PX.K}, e, l, p, nullptr, fu.a_xy.data());
+      S.pairs_evaluated += softmin_rows(PX.M.pts.data(), PX.npad, d, {Yc.pts.data(), Yc.logw.data(), cu.a_xy.data(), PY.K}, e, l, p, nullptr, fu.b_yx.data());
+    } else if (tsw > 0) {
+      for (int64_t s2 = 0; s2 < PX.npad; ++s2) {
+        fu.a_xx[s2] = cu.a_xx[PX.labels[s2]];
+        fu.b_yx[s2] = cu.b_yx[PX.labels[s2]];
+      }
+      for (int64_t s2 = 0; s2 < PY.npad; ++s2) {
+        fu.b_yy[s2] = cu.b_yy[PY.labels[s2]];
+        fu.a_xy[s2] = cu.a_xy[PY.labels[s2]];
+      }
+    }
+    // per-cluster max of a potential over the real atoms, as float
+    auto fmaxv = [&](const Vec& f, const Pad& P) {
+      std::vector<float> F(P.K, -std::numeric_limits<float>::infinity());
+      for (int I = 0; I < P.K; ++I)
+        for (int32_t s2 = P.poff[I]; s2 < P.poff[I + 1]; ++s2)
+          if (P.M.w[s2] > 0.0) F[I] = std::max(F[I], static_cast<float>(f[s2]));
+      return F;
+    };
+    Ranges rxx, ryy, rxy, ryx;
+    auto build = [&](double e) {
+      const double theta = tsw > 0 ? prm->theta : std::numeric_limits<double>::infinity();
+      std::vector<float> Fxx = fmaxv(fu.a_xx, PX), Fyx = fmaxv(fu.b_yx, PX);
+      std::vector<float> Gyy = fmaxv(fu.b_yy, PY), Gxy = fmaxv(fu.a_xy, PY);
+      std::vector<uint8_t> mxx, myy, mxy;
+      hd_mask(PX.K, PX.K, d, PX.km.centroids.data(), PX.km.radii.data(), Fxx.data(),
+              PX.km.centroids.data(), PX.km.radii.data(), Fxx.data(), e, theta, 1, mxx);
+      hd_mask(PY.K, PY.K, d, PY.km.centroids.data(), PY.km.radii.data(), Gyy.data(),
+              PY.km.centroids.data(), PY.km.radii.data(), Gyy.data(), e, theta, 1, myy);
+      hd_mask(PX.K, PY.K, d, PX.km.centroids.data(), PX.km.radii.data(), Fyx.data(),
+              PY.km.centroids.data(), PY.km.radii.data(), Gxy.data(), e, theta, 0, mxy);
+      tile_ranges(PX.labels.data(), PX.poff.data(), PX.K, PX.npad, PX.poff.data(), PX.K, mxx.data(), rxx);
+      tile_ranges(PY.labels.data(), PY.poff.data(), PY.K, PY.npad, PY.poff.data(), PY.K, myy.data(), ryy);
+      tile_ranges(PX.labels.data(), PX.poff.data(), PX.K, PX.npad, PY.poff.data(), PY.K, mxy.data(), ryx);
+      rxx = sym_self(rxx, PX.npad);
+      ryy = sym_self(ryy, PY.npad);
+      rxy = transpose_ranges(ryx, PY.npad);
+    };
+    for (int t = tsw; t <= ns; ++t) {
+      const int tt = std::min(t, ns - 1);
+      const bool rebuild = (t == tsw) || (prm->retruncate > 0 && t < ns && (t - tsw) % prm->retruncate == 0);
+      if (rebuild) build(eps[tt]);
+      const double pr = sym_update(PX.M, PY.M, d, fu, eps[tt], lam[tt], p, t == ns, &rxx, &ryy, &rxy, &ryx);
+      if (pr < 0) return fail(MSOT_ENUMERIC, "non-finite potential at scale " + std::to_string(tt));
+      S.pairs_evaluated += pr;
+      S.pairs_fine += pr;
+    }
+    auto unpad = [](const Vec& v, const Pad& P, int64_t cnt) {
+      Vec o(cnt);
+      for (int64_t s2 = 0; s2 < P.npad; ++s2)
+        if (P.src[s2] >= 0) o[P.src[s2]] = v[s2];
+      return o;
+    };
+    u.a_xx = unpad(fu.a_xx, PX, n);
+    u.b_yx = unpad(fu.b_yx, PX, n);
+    u.b_yy = unpad(fu.b_yy, PY, m);
+    u.a_xy = unpad(fu.a_xy, PY, m);
+  } else if (!prm->multiscale || d > 3) {
     S.t_switch = 0;
     for (int t = 0; t <= ns; ++t) {
       const int tt = std::min(t, ns - 1);

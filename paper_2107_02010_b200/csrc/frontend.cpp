@@ -163,6 +163,9 @@ msot_params SolverParams::to_c() const {
   p.switch_factor = switch_factor;
   p.mask_rule = mask_rule;
   p.transfer_rule = transfer_rule;
+  p.pair_eval = pair_eval;
+  p.clusters = clusters;
+  p.seed = seed;
   return p;
 }
 

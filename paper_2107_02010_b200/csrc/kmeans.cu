@@ -286,6 +286,71 @@ cudaError_t kmeans(const double* x, const double* w, int64_t n, int d, int K, ui
   return cudaGetLastError();
 }
 
+// ---- padded cluster layout of the high-D multiscale solver ---------------
+// Cluster I occupies rows [poff[I], poff[I+1]) (its atoms in index order, then
+// padding up to a multiple of 128 — the tcgen05 kernel's column block).
+// src[p] = caller index of slot p, or -(I+1) for a padding slot of cluster I,
+// which takes the centroid's coordinates (finite, harmless sums) and weight 0.
+__global__ void hd_gather_padded_kernel(const double* x, const double* centers, const int32_t* src,
+                                        int64_t npad, int d, double* out) {
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g >= npad * d) return;
+  const int64_t p = g / d;
+  const int q = static_cast<int>(g - p * d);
+  const int32_t s = src[p];
+  out[g] = s >= 0 ? x[static_cast<int64_t>(s) * d + q] : centers[static_cast<int64_t>(-s - 1) * d + q];
+}
+
+__global__ void hd_padded_weights_kernel(const double* w, const int32_t* src, int64_t npad,
+                                         float* lw2, double* w64) {
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= npad) return;
+  const int32_t s = src[p];
+  const double wi = s >= 0 ? w[s] : 0.0;
+  lw2[p] = s >= 0 ? __double2float_rn(log2(wi)) : __int_as_float(0xff800000);
+  w64[p] = wi;
+}
+
+// per-cluster max of a potential over the cluster's real atoms (weight > 0)
+__global__ void hd_cluster_fmax_kernel(const float* f, const double* w64, const int32_t* off, int K,
+                                       float* fmax) {
+  const int lane = threadIdx.x & 31;
+  const int64_t I = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (I >= K) return;
+  float m = -INFINITY;
+  for (int32_t s = off[I] + lane; s < off[I + 1]; s += 32)
+    if (w64[s] > 0.0) m = fmaxf(m, f[s]);
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) fmax[I] = m;
+}
+
+cudaError_t hd_gather_padded(const double* x, const double* centers, const int32_t* src,
+                             int64_t npad, int d, double* out, cudaStream_t st) {
+  if (npad <= 0) return cudaSuccess;
+  ++g_launches;
+  hd_gather_padded_kernel<<<static_cast<unsigned>((npad * d + 255) / 256), 256, 0, st>>>(
+      x, centers, src, npad, d, out);
+  return cudaGetLastError();
+}
+
+cudaError_t hd_padded_weights(const double* w, const int32_t* src, int64_t npad, float* lw2,
+                              double* w64, cudaStream_t st) {
+  if (npad <= 0) return cudaSuccess;
+  ++g_launches;
+  hd_padded_weights_kernel<<<static_cast<unsigned>((npad + 255) / 256), 256, 0, st>>>(w, src, npad,
+                                                                                     lw2, w64);
+  return cudaGetLastError();
+}
+
+cudaError_t hd_cluster_fmax(const float* f, const double* w64, const int32_t* off, int K,
+                            float* fmax, cudaStream_t st) {
+  if (K <= 0) return cudaSuccess;
+  ++g_launches;
+  hd_cluster_fmax_kernel<<<static_cast<unsigned>((static_cast<int64_t>(K) * 32 + 255) / 256), 256, 0,
+                           st>>>(f, w64, off, K, fmax);
+  return cudaGetLastError();
+}
+
 size_t kmeans_ws_bytes(int64_t n, int d, int K) {
   const int64_t nb = (n + 255) / 256;
   return static_cast<size_t>(n) * sizeof(double) + nb * (sizeof(double) + sizeof(int64_t)) +

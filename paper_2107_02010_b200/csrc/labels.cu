@@ -77,6 +77,7 @@ __global__ void label_finalize_kernel(const float* part, const int32_t* lbase,
   const int row = tile_start[t] + lr;
   if (row >= tile_start[t + 1]) return;
   const int64_t out = perm ? perm[row] : row;
+  if (out < 0) return;  // padding slot of the high-D multiscale layout
   double m = 0.0;
   const int32_t* lb = lbase + static_cast<int64_t>(t) * n_classes;
   for (int l = 0; l < n_classes; ++l) {

@@ -100,7 +100,10 @@ cudaError_t divergence_final(const double* partials, int nblocks, double eps, do
 __global__ void scatter_unsort_kernel(const float* v, const int32_t* perm, int64_t n,
                                       const double* shift, double sign, double* out) {
   const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (s < n) out[perm ? perm[s] : s] = static_cast<double>(v[s]) + (shift ? sign * *shift : 0.0);
+  if (s >= n) return;
+  const int64_t i = perm ? perm[s] : s;
+  if (i >= 0)  // padding slots of the high-D multiscale layout carry a negative index
+    out[i] = static_cast<double>(v[s]) + (shift ? sign * *shift : 0.0);
 }
 
 cudaError_t scatter_unsort(const float* v, const int32_t* perm, int64_t n, const double* shift,

@@ -327,6 +327,90 @@ cudaError_t mask_pair_count(const uint32_t* mask, int32_t kx, int32_t ky, const 
   return cudaGetLastError();
 }
 
+// ---- high-D masks (K-means clusters, D <= 64) -----------------------------
+// B_a = F_I + G_J - 1/2 max(0, |X_I - Y_J| - (r_I + r_J))^2 with float64
+// centroids, |X_I - Y_J|^2 summed in coordinate order, explicitly rounded
+// (bit-identical to oracle.cpp:hd_pair_slack).  One CTA per row cluster.
+__device__ __forceinline__ double hd_pair_slack(const double* X, float rI, float F, const double* Y,
+                                                float rJ, float G, int d) {
+  double s = 0.0;
+  for (int k = 0; k < d; ++k) {
+    const double t = __dsub_rn(X[k], Y[k]);
+    s = __dadd_rn(s, __dmul_rn(t, t));
+  }
+  const double rr = __dadd_rn(static_cast<double>(rI), static_cast<double>(rJ));
+  double lb = __dsub_rn(__dsqrt_rn(s), rr);
+  if (lb < 0.0) lb = 0.0;
+  const double fg = __dadd_rn(static_cast<double>(F), static_cast<double>(G));
+  return __dsub_rn(fg, __dmul_rn(0.5, __dmul_rn(lb, lb)));
+}
+
+__global__ void __launch_bounds__(256)
+mask_hd_rows_kernel(const double* cx, const float* rx, const float* fx, const double* cy,
+                    const float* ry, const float* gy, int32_t ky, int d, double thr, int self,
+                    uint32_t* mask, int32_t* best) {
+  __shared__ double X[64];
+  __shared__ double sv[8];
+  __shared__ int32_t sj[8];
+  const int32_t I = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int q = threadIdx.x; q < d; q += blockDim.x) X[q] = cx[static_cast<int64_t>(I) * d + q];
+  __syncthreads();
+  const float rI = rx[I], F = fx[I];
+  const int32_t words = mask_words(ky);
+  double bv = -INFINITY;
+  int32_t bj = 0x7fffffff;
+  for (int32_t w = warp; w < words; w += 8) {
+    const int32_t J = w * 32 + lane;
+    bool keep = false;
+    if (J < ky) {
+      const double v = hd_pair_slack(X, rI, F, cy + static_cast<int64_t>(J) * d, ry[J], gy[J], d);
+      keep = (self && I == J) || v >= thr;
+      if (v > bv) { bv = v; bj = J; }
+    }
+    const uint32_t bits = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) mask[static_cast<int64_t>(I) * words + w] = bits;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int32_t j2 = __shfl_xor_sync(0xffffffffu, bj, o);
+    if (v2 > bv || (v2 == bv && j2 < bj)) { bv = v2; bj = j2; }
+  }
+  if (lane == 0) { sv[warp] = bv; sj[warp] = bj; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < 8; ++q)
+      if (sv[q] > bv || (sv[q] == bv && sj[q] < bj)) { bv = sv[q]; bj = sj[q]; }
+    best[I] = bj == 0x7fffffff ? -1 : bj;
+  }
+}
+
+cudaError_t truncation_masks_hd(int32_t kx, int32_t ky, int d, const double* cx, const float* rx,
+                                const float* fx, const double* cy, const float* ry,
+                                const float* gy, double eps, double theta, int self,
+                                uint32_t* mask, uint32_t* maskT, int32_t* best_r, int32_t* best_c,
+                                cudaStream_t st) {
+  if (kx <= 0 || ky <= 0) return cudaSuccess;
+  if (d > 64 || (self && kx != ky)) return cudaErrorInvalidValue;
+  const double thr = -(theta * eps);
+  ++g_launches;
+  mask_hd_rows_kernel<<<static_cast<unsigned>(kx), 256, 0, st>>>(cx, rx, fx, cy, ry, gy, ky, d,
+                                                                   thr, self, mask, best_r);
+  if (self) {
+    ++g_launches;
+    mask_best_kernel<<<static_cast<unsigned>((kx + 255) / 256), 256, 0, st>>>(
+        best_r, kx, best_r, 0, mask, mask_words(ky), mask, mask_words(ky));
+    return cudaGetLastError();
+  }
+  ++g_launches;
+  mask_hd_rows_kernel<<<static_cast<unsigned>(ky), 256, 0, st>>>(cy, ry, gy, cx, rx, fx, kx, d,
+                                                                   thr, 0, maskT, best_c);
+  ++g_launches;
+  mask_best_kernel<<<static_cast<unsigned>((static_cast<int64_t>(kx) + ky + 255) / 256), 256, 0, st>>>(
+      best_r, kx, best_c, ky, mask, mask_words(ky), maskT, mask_words(kx));
+  return cudaGetLastError();
+}
+
 __global__ void unpack_kernel(const uint32_t* mask, int32_t kx, int32_t ky, uint8_t* out) {
   const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (g >= static_cast<int64_t>(kx) * ky) return;

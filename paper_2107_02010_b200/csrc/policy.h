@@ -33,6 +33,11 @@ extern "C" {
  * dense solve; 28 -> 0.50 s, within 7.4e-5; below ~25 the switch (sigma <
  * r_max) leaves too few fine scales (16 atoms: +2.9e-3). */
 #define MSOT_AUTO_ATOMS_PER_CELL 28.0
+/* Lloyd iterations of the K-means coarsening inside the multiscale solver
+ * (the stand-alone kmeans_coarsen op keeps SPEC.md:265's cap of 100): the
+ * clusters only steer efficiency (truncation), never the result, and the
+ * float64 assignment of 400k x 633 x 60 costs ~10 ms per iteration. */
+#define MSOT_KMEANS_SOLVER_ITERS 20
 /* Cube ids are Morton-interleaved with this many bits per axis (D <= 3). */
 #define MSOT_MORTON_BITS 10
 

@@ -133,6 +133,21 @@ cudaError_t kmeans(const double* x, const double* w, int64_t n, int d, int K, ui
                    uint32_t* labels, double* centers, double* cw, float* radii, int* iters,
                    cudaStream_t st);
 
+// padded cluster layout of the high-D multiscale solver (kmeans.cu)
+cudaError_t hd_gather_padded(const double* x, const double* centers, const int32_t* src,
+                             int64_t npad, int d, double* out, cudaStream_t st);
+cudaError_t hd_padded_weights(const double* w, const int32_t* src, int64_t npad, float* lw2,
+                              double* w64, cudaStream_t st);
+cudaError_t hd_cluster_fmax(const float* f, const double* w64, const int32_t* off, int K,
+                            float* fmax, cudaStream_t st);
+// high-D truncation masks (mask.cu): the centroid/radius bound B_a with float64
+// centroids (D <= 64), best pairs, self diagonal; maskT = exact transpose
+cudaError_t truncation_masks_hd(int32_t kx, int32_t ky, int d, const double* cx, const float* rx,
+                                const float* fx, const double* cy, const float* ry,
+                                const float* gy, double eps, double theta, int self,
+                                uint32_t* mask, uint32_t* maskT, int32_t* best_r, int32_t* best_c,
+                                cudaStream_t st);
+
 // truncation mask + ranges (mask.cu)
 __host__ __device__ inline int32_t mask_words(int32_t ky) { return (ky + 31) / 32; }
 // bit-packed mask: Kx rows of mask_words(Ky) uint32 words

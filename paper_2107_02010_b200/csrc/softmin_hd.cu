@@ -234,6 +234,7 @@ softmin_hd_kernel(const __grid_constant__ Group G) {
   uint64_t* cFull = tmemEmpty + 2;
   uint64_t* colFull = cFull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(colFull + 8);
+  int32_t* ring_blk = reinterpret_cast<int32_t*>(tmem_slot + 1);  // [2] column block per ring slot
 
   const int it = blockIdx.x;
   if (it >= G.n_items) return;
@@ -241,12 +242,13 @@ softmin_hd_kernel(const __grid_constant__ Group G) {
   const Problem& P = G.P[item.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row_base = P.tile_start[item.y];
-  // column blocks of this item: positions [z, w) of the tile's (single,
-  // dense) column range, in whole 128-column blocks
-  const int col0 = P.ranges[P.tile_rptr[item.y]].x;  // 0, or the tile start (self, kSym)
-  const int blk0 = (col0 + item.z + kHdBlockRows - 1) / kHdBlockRows;
-  const int blk1 = (col0 + item.w + kHdBlockRows - 1) / kHdBlockRows;
-  const int nblk = blk1 - blk0;
+  // position blocks of this item: the 128-position blocks of the tile's
+  // concatenated column ranges whose first position lies in [z, w).  Every
+  // range starts and ends on a 128-column block (dense lists, padded K-means
+  // clusters), so position block b maps to one whole column block.
+  const int pb0 = (item.z + kHdBlockRows - 1) / kHdBlockRows;
+  const int pb1 = (item.w + kHdBlockRows - 1) / kHdBlockRows;
+  const int nblk = pb1 - pb0;
 
   if (threadIdx.x == 0) {
     mbar_init(smem_u32(&bars[0]), 1);
@@ -283,26 +285,36 @@ softmin_hd_kernel(const __grid_constant__ Group G) {
         bulk_g2s(smem_u32(sA), a0, kHdPackBytes, fa);
         bulk_g2s(smem_u32(sA + kHdPackBytes), a0 + kHdPackBytes, kHdPackBytes, fa);
       }
+      int64_t rk = P.tile_rptr[item.y];  // range walker: position -> column
+      int32_t racc = 0;
       for (int t = 0; t < nblk; ++t) {
         const int s = t % L::kStages, ns = t / L::kStages, buf = t & 1;
+        const int32_t pos = (pb0 + t) * kHdBlockRows;
+        int2 rg = P.ranges[rk];
+        while (pos >= racc + (rg.y - rg.x)) {
+          racc += rg.y - rg.x;
+          rg = P.ranges[++rk];
+        }
+        const int cblk = (rg.x + (pos - racc)) / kHdBlockRows;
         if (ns > 0) mbar_wait(smem_u32(&emptyB[s]), (ns - 1) & 1);
         if (lane == 0) {
           const uint32_t fb = smem_u32(&fullB[s]);
           mbar_expect_tx(fb, kHdPackBytes);
           bulk_g2s(smem_u32(sB + s * kHdPackBytes),
-                   P.b_pack + static_cast<int64_t>(blk0 + t) * kHdPackBytes, kHdPackBytes, fb);
+                   P.b_pack + static_cast<int64_t>(cblk) * kHdPackBytes, kHdPackBytes, fb);
         }
         // column constants (and factors) of block t into ring slot buf once
         // the epilogue released it (block t - 2)
         if (t >= 2) mbar_wait(smem_u32(&tmemEmpty[buf]), ((t >> 1) - 1) & 1);
         if (lane == 0) {
+          ring_blk[buf] = cblk;  // published by the arrive below (release)
           const uint32_t fc = smem_u32(&cFull[buf]);
           mbar_expect_tx(fc, L::kRing * 4);
           float* slot = cring + buf * L::kRing;
-          bulk_g2s(smem_u32(slot), P.col_c + static_cast<int64_t>(blk0 + t) * 128, 128 * 4, fc);
+          bulk_g2s(smem_u32(slot), P.col_c + static_cast<int64_t>(cblk) * 128, 128 * 4, fc);
           if (kSym)
-            bulk_g2s(smem_u32(slot + 128), P.col_c2 + static_cast<int64_t>(blk0 + t) * 128,
-                     128 * 4, fc);
+            bulk_g2s(smem_u32(slot + 128), P.col_c2 + static_cast<int64_t>(cblk) * 128, 128 * 4,
+                     fc);
         }
         __syncwarp();
       }
@@ -447,8 +459,9 @@ softmin_hd_kernel(const __grid_constant__ Group G) {
         const float fac = exp2f(cring[buf * L::kRing + 128 + cq * 32 + lane] - P.ell * est_mid);
         const float* ca = colacc + (buf * 4 + cq) * 4 * 32 + lane;
         const float sum = ((ca[0] + ca[32]) + ca[64]) + ca[96];
-        const int col = (blk0 + t) * kHdBlockRows + cq * 32 + lane;
-        if (col < P.n_cols) P.colpart[P.tile_slot[item.y] + (col - col0)] = sum * fac;
+        const int col = ring_blk[buf] * kHdBlockRows + cq * 32 + lane;
+        const int32_t pos = (pb0 + t) * kHdBlockRows + cq * 32 + lane;
+        if (col < P.n_cols) P.colpart[P.tile_slot[item.y] + pos] = sum * fac;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&tmemEmpty[buf]));
@@ -484,7 +497,8 @@ __global__ void hd_colconst_kernel(const float* lw2, const float* h, const float
   const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= npad) return;
   out[j] = j < n ? lw2[j] + (h[j] - 0.5f * sq[j]) * inv : __int_as_float(0xff800000);
-  if (out2) out2[j] = j < n ? ell * h[j] - lw2[j] : 0.f;
+  // zero-weight columns (padding) feed no column sum: factor 2^-inf = 0
+  if (out2) out2[j] = (j < n && lw2[j] > -INFINITY) ? ell * h[j] - lw2[j] : -INFINITY;
 }
 
 cudaError_t hd_colconst(const Problem& P, float* out, float* out2, cudaStream_t st) {

@@ -253,6 +253,10 @@ __global__ void sym_colfinal_kernel(const __grid_constant__ Group G, int p) {
   if (r >= P.n_rows) return;
   const float s = P.row_add[r];
   const float est = P.row_est ? P.row_est[r] : 0.f;
+  if (P.row_lw2 && P.row_lw2[r] == -INFINITY) {  // zero-weight atom (padding): no update
+    P.row_out[r] = est;
+    return;
+  }
   if (!(s >= 8.67361738e-19f && s <= 1.2676506e30f)) {
     const int slot = atomicAdd(G.fb_count, 1);
     atomicAdd(G.fb_total, 1);

@@ -583,6 +583,7 @@ struct SymCols {
   const float4* yrows;       // problem 3: rows y over cols x
   const float4* xcols;
   const float* x_lw2;
+  const float* y_lw2 = nullptr;  // weights of the transposed problem's rows (zero-weight skip)
   int64_t n, m;
   bool uniform;              // both measures have uniform weights
   HdOperands hd3{};          // high-D operands of problem 3 (rows y, cols x)
@@ -639,7 +640,8 @@ void run_group_sym(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& s
     G.tile_prefix[p + 1] = tiles_acc;
   }
   {
-    const ProbSpec T{X.yrows, X.m, X.xcols, X.x_lw2, X.n, nullptr, X.hd3};
+    ProbSpec T{X.yrows, X.m, X.xcols, X.x_lw2, X.n, nullptr, X.hd3};
+    T.row_lw2 = X.y_lw2;
     fill_problem(G.P[3], T, a.h[3], a.est[3], a.out[3], a.eps, a.lam, a.mixw);
     G.P[3].row_add = X.tot[2];
   }
@@ -836,6 +838,272 @@ void plan_group(msot_ctx* c, const std::string& tag, int np, const ProbSpec* spe
   CK(launch_plan(G, d, c->st));
 }
 
+// ---------------------------------------------------------------------------
+// High-dimensional multiscale (D > 3): K-means
+// coarsening (kmeans.cu) instead of the voxel grid, a dense
+// evaluate-once coarse phase on the centroid measures, inheritance at the
+// switch, and the block-sparse evaluate-once fine phase on the tcgen05
+// kernel.  Each cluster is padded to a multiple of 128 atoms (centroid
+// coordinates, weight 0) so every column range is whole 128-column blocks.
+struct HdLayout {
+  int K = 0;
+  int64_t npad = 0;
+  std::vector<int32_t> poff_h;     // padded cluster offsets (K+1)
+  int32_t* poff = nullptr;         // device
+  int32_t* labels = nullptr;       // cluster of every padded slot
+  int32_t* src = nullptr;          // caller index, or -(I+1) for padding of cluster I
+  double* centers = nullptr;       // K x d float64
+  float* radii = nullptr;
+  std::vector<float> radii_h;
+  float* clw2 = nullptr;           // coarse measure
+  double* cw64 = nullptr;
+  uint8_t* cpack = nullptr;
+  float* csq = nullptr;
+  float* cf = nullptr;
+  uint8_t* pack = nullptr;         // padded fine measure
+  float* sq = nullptr;
+  float* f = nullptr;
+  float* lw2 = nullptr;
+  double* w64 = nullptr;
+};
+
+void hd_layout(msot_ctx* c, const std::string& tag, const double* dx, const double* dw, int64_t n,
+               int d, int K, uint64_t seed, double diam, const double* dcen, HdLayout& L) {
+  cudaStream_t st = c->st;
+  L.K = K;
+  int32_t* perm = c->buf<int32_t>(tag + ".kperm", n);
+  int32_t* off = c->buf<int32_t>(tag + ".koff", K + 1);
+  uint32_t* lab = c->buf<uint32_t>(tag + ".klab", n);
+  L.centers = c->buf<double>(tag + ".kcen", size_t(K) * d);
+  double* cw = c->buf<double>(tag + ".kcw", K);
+  L.radii = c->buf<float>(tag + ".krad", K);
+  void* ws = c->buf<char>(tag + ".kws", kmeans_ws_bytes(n, d, K));
+  const double tol = 1e-9 * diam;
+  CK(kmeans(dx, dw, n, d, K, seed, tol * tol, MSOT_KMEANS_SOLVER_ITERS, ws, perm, off, lab,
+            L.centers, cw, L.radii, nullptr, st));
+  std::vector<int32_t> off_h(K + 1), perm_h(n);
+  L.radii_h.resize(K);
+  CK(cudaMemcpyAsync(off_h.data(), off, (K + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(perm_h.data(), perm, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(L.radii_h.data(), L.radii, K * sizeof(float), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  L.poff_h.assign(K + 1, 0);
+  for (int I = 0; I < K; ++I)
+    L.poff_h[I + 1] = L.poff_h[I] + (off_h[I + 1] - off_h[I] + 127) / 128 * 128;
+  L.npad = L.poff_h[K];
+  std::vector<int32_t> src(L.npad), labp(L.npad);
+  for (int I = 0; I < K; ++I) {
+    const int32_t cnt = off_h[I + 1] - off_h[I];
+    for (int32_t q = 0; q < L.poff_h[I + 1] - L.poff_h[I]; ++q) {
+      src[L.poff_h[I] + q] = q < cnt ? perm_h[off_h[I] + q] : -(I + 1);
+      labp[L.poff_h[I] + q] = I;
+    }
+  }
+  L.poff = c->buf<int32_t>(tag + ".poff", K + 1);
+  L.labels = c->buf<int32_t>(tag + ".plab", L.npad);
+  L.src = c->buf<int32_t>(tag + ".psrc", L.npad);
+  CK(cudaMemcpyAsync(L.poff, L.poff_h.data(), (K + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(L.labels, labp.data(), L.npad * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(L.src, src.data(), L.npad * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  double* xp = c->buf<double>(tag + ".px64", L.npad * d);
+  CK(hd_gather_padded(dx, L.centers, L.src, L.npad, d, xp, st));
+  L.lw2 = c->buf<float>(tag + ".plw2", L.npad);
+  L.w64 = c->buf<double>(tag + ".pw64", L.npad);
+  CK(hd_padded_weights(dw, L.src, L.npad, L.lw2, L.w64, st));
+  L.pack = c->buf<uint8_t>(tag + ".ppack", hd_pack_bytes(L.npad));
+  L.sq = c->buf<float>(tag + ".psq", hd_padded(L.npad));
+  L.f = c->buf<float>(tag + ".pf", hd_padded(L.npad) * 64);
+  CK(hd_pack(xp, L.npad, d, dcen, 0, L.pack, L.sq, L.f, st));
+  // the coarse measure (centroids, cluster weights)
+  L.cpack = c->buf<uint8_t>(tag + ".cpack", hd_pack_bytes(K));
+  L.csq = c->buf<float>(tag + ".csq", hd_padded(K));
+  L.cf = c->buf<float>(tag + ".cf", hd_padded(K) * 64);
+  CK(hd_pack(L.centers, K, d, dcen, 0, L.cpack, L.csq, L.cf, st));
+  L.clw2 = c->buf<float>(tag + ".clw2", K);
+  L.cw64 = c->buf<double>(tag + ".cw64", K);
+  CK(hd_weights(cw, K, L.clw2, L.cw64, st));
+  CK(cudaStreamSynchronize(st));  // host vectors go out of scope
+}
+
+void hd_multiscale(msot_ctx* c, const msot_params* prm, const double* d_x, const double* d_a,
+                   int64_t n, const double* d_y, const double* d_b, int64_t m, int d,
+                   const double* dcen, double diam, const std::vector<double>& sig,
+                   const std::vector<double>& eps, const std::vector<double>& lam, int ns,
+                   Potentials& U, int& cur, DMeasure& X, DMeasure& Y, int64_t& nr, int64_t& mr,
+                   uint8_t*& hd_ax, float*& hd_sqx, SolveState& ss, msot_stats* S) {
+  cudaStream_t st = c->st;
+  if (prm->pair_eval == 0) raise(MSOT_EUSAGE, "high-D multiscale runs the evaluate-once scheme");
+  const int kx = prm->clusters > 0 ? static_cast<int>(std::min<int64_t>(prm->clusters, n))
+                                   : static_cast<int>(std::ceil(std::sqrt(static_cast<double>(n))));
+  const int ky = prm->clusters > 0 ? static_cast<int>(std::min<int64_t>(prm->clusters, m))
+                                   : static_cast<int>(std::ceil(std::sqrt(static_cast<double>(m))));
+  c->mark(0);
+  HdLayout LX, LY;
+  hd_layout(c, "hx", d_x, d_a, n, d, kx, static_cast<uint64_t>(prm->seed), diam, dcen, LX);
+  hd_layout(c, "hy", d_y, d_b, m, d, ky, static_cast<uint64_t>(prm->seed), diam, dcen, LY);
+  nr = LX.npad;
+  mr = LY.npad;
+  alloc_pots(c, "hpot", nr, mr, U);
+  cur = 0;
+  X = DMeasure{};
+  Y = DMeasure{};
+  X.n = nr;
+  Y.n = mr;
+  X.k = kx;
+  Y.k = ky;
+  X.lw2 = LX.lw2;
+  X.w64 = LX.w64;
+  X.perm = LX.src;
+  X.labels = LX.labels;
+  X.offsets = LX.poff;
+  X.offsets_h = LX.poff_h;
+  Y.lw2 = LY.lw2;
+  Y.w64 = LY.w64;
+  Y.perm = LY.src;
+  Y.labels = LY.labels;
+  Y.offsets = LY.poff;
+  Y.offsets_h = LY.poff_h;
+  hd_ax = LX.pack;
+  hd_sqx = LX.sq;
+  S->kx = kx;
+  S->ky = ky;
+  double rmax = 0.0;
+  for (float r : LX.radii_h) rmax = std::max(rmax, double(r));
+  for (float r : LY.radii_h) rmax = std::max(rmax, double(r));
+  const int tsw = msot_switch_index(sig.data(), ns, rmax, prm->switch_factor);
+  S->t_switch = tsw;
+  S->cluster_scale = rmax;
+  const double full = double(n) * n + double(m) * m + 2.0 * double(n) * m;
+  // ---- coarse phase: dense evaluate-once on the centroid measures
+  c->mark(1);
+  float* coarse[4] = {nullptr, nullptr, nullptr, nullptr};
+  if (tsw > 0) {
+    Potentials Uc;
+    alloc_pots(c, "hcpot", kx, ky, Uc);
+    int ccur = 0;
+    SymSet cxx, cyy, cyx;
+    dense_symset(c, "hcs.xx", kx, kx, 1, cxx);
+    dense_symset(c, "hcs.yy", ky, ky, 1, cyy);
+    dense_symset(c, "hcs.yx", kx, ky, 0, cyx);
+    Plan Pc;
+    Pc.np = 3;
+    Pc.ps[0] = {nullptr, kx, nullptr, LX.clw2, kx, &cxx.R, {LX.cpack, LX.cpack, LX.csq, LX.csq, LX.cf, LX.cf}, &cxx, LX.clw2};
+    Pc.ps[1] = {nullptr, ky, nullptr, LY.clw2, ky, &cyy.R, {LY.cpack, LY.cpack, LY.csq, LY.csq, LY.cf, LY.cf}, &cyy, LY.clw2};
+    Pc.ps[2] = {nullptr, kx, nullptr, LY.clw2, ky, &cyx.R, {LX.cpack, LY.cpack, LX.csq, LY.csq, LX.cf, LY.cf}, &cyx, LX.clw2};
+    SymCols cc{};
+    cc.tot[0] = c->buf<float>("hcs.totx", kx);
+    cc.tot[1] = c->buf<float>("hcs.toty", ky);
+    cc.tot[2] = c->buf<float>("hcs.totxy", ky);
+    cc.x_lw2 = LX.clw2;
+    cc.n = kx;
+    cc.m = ky;
+    cc.hd3 = {LY.cpack, LX.cpack, LY.csq, LX.csq, LY.cf, LX.cf};
+    build_plan(c, "hpc", Pc);
+    const double cfull = double(kx) * kx + double(ky) * ky + 2.0 * double(kx) * ky;
+    for (int t = 0; t < tsw; ++t) {
+      sym_step_once(c, Pc, Uc, ccur, eps[t], lam[t], false, ss, cc);
+      S->pairs_dense += cfull;
+    }
+    // coarse -> fine: inheritance (padding slots inherit
+    // too), then for transfer_rule 1 one lambda-damped softmin of every fine
+    // atom against the coarse measure (GeomLoss extrapolation), expanded
+    // around the inherited value
+    c->mark(2);
+    float** co = Uc.v[ccur];
+    const bool extrap = prm->transfer_rule == 1;
+    float** dst = U.v[extrap ? cur ^ 1 : cur];
+    CK(inherit(co[0], LX.labels, nr, dst[0], st));
+    CK(inherit(co[1], LY.labels, mr, dst[1], st));
+    CK(inherit(co[2], LY.labels, mr, dst[2], st));
+    CK(inherit(co[3], LX.labels, nr, dst[3], st));
+    for (int q = 0; q < 4; ++q) coarse[q] = co[q];
+    if (extrap) {
+      RangeSet exx, eyy, exy, eyx;
+      dense_rangeset(c, "he.xx", nr, kx, exx);
+      dense_rangeset(c, "he.yy", mr, ky, eyy);
+      dense_rangeset(c, "he.xy", mr, kx, exy);
+      dense_rangeset(c, "he.yx", nr, ky, eyx);
+      Plan Pe;
+      Pe.np = 4;
+      Pe.ps[0] = {nullptr, nr, nullptr, LX.clw2, kx, &exx, {LX.pack, LX.cpack, LX.sq, LX.csq, LX.f, LX.cf}};
+      Pe.ps[1] = {nullptr, mr, nullptr, LY.clw2, ky, &eyy, {LY.pack, LY.cpack, LY.sq, LY.csq, LY.f, LY.cf}};
+      Pe.ps[2] = {nullptr, mr, nullptr, LX.clw2, kx, &exy, {LY.pack, LX.cpack, LY.sq, LX.csq, LY.f, LX.cf}};
+      Pe.ps[3] = {nullptr, nr, nullptr, LY.clw2, ky, &eyx, {LX.pack, LY.cpack, LX.sq, LY.csq, LX.f, LY.cf}};
+      build_plan(c, "hpe", Pe);
+      ScaleArgs ea{};
+      ea.h[0] = co[0]; ea.est[0] = dst[0]; ea.out[0] = U.v[cur][0];
+      ea.h[1] = co[1]; ea.est[1] = dst[1]; ea.out[1] = U.v[cur][1];
+      ea.h[2] = co[3]; ea.est[2] = dst[2]; ea.out[2] = U.v[cur][2];
+      ea.h[3] = co[2]; ea.est[3] = dst[3]; ea.out[3] = U.v[cur][3];
+      ea.eps = eps[tsw - 1];
+      ea.lam = lam[tsw - 1];
+      ea.mixw = 1.0;
+      run_group(c, Pe, ea, ss);
+    }
+  }
+  // ---- fine phase: block-sparse evaluate-once on the padded measures
+  uint32_t* mxx = c->buf<uint32_t>("hm.xx", size_t(kx) * mask_words(kx));
+  uint32_t* myy = c->buf<uint32_t>("hm.yy", size_t(ky) * mask_words(ky));
+  uint32_t* mxy = c->buf<uint32_t>("hm.xy", size_t(kx) * mask_words(ky));
+  uint32_t* myx = c->buf<uint32_t>("hm.yx", size_t(ky) * mask_words(kx));
+  float* fm[4];
+  fm[0] = c->buf<float>("hm.Fxx", kx);
+  fm[1] = c->buf<float>("hm.Gyy", ky);
+  fm[2] = c->buf<float>("hm.Gxy", ky);
+  fm[3] = c->buf<float>("hm.Fyx", kx);
+  int32_t* bxr = c->buf<int32_t>("hm.bx", std::max(kx, ky));
+  int32_t* byr = c->buf<int32_t>("hm.by", std::max(kx, ky));
+  SymSet sxx, syy, syx;
+  SymCols scol{};
+  scol.labels[0] = LX.labels; scol.co[0] = LX.poff; scol.tot[0] = c->buf<float>("hs.totx", nr);
+  scol.labels[1] = LY.labels; scol.co[1] = LY.poff; scol.tot[1] = c->buf<float>("hs.toty", mr);
+  scol.labels[2] = LY.labels; scol.co[2] = LY.poff; scol.tot[2] = c->buf<float>("hs.totxy", mr);
+  scol.x_lw2 = LX.lw2;
+  scol.y_lw2 = LY.lw2;
+  scol.n = nr;
+  scol.m = mr;
+  scol.hd3 = {LY.pack, LX.pack, LY.sq, LX.sq, LY.f, LX.f};
+  Plan Pf;
+  auto build_masks = [&](double e) {
+    const bool info = tsw > 0;
+    const double theta = info ? prm->theta : INFINITY;
+    float** f = U.v[cur];
+    CK(hd_cluster_fmax(f[0], LX.w64, LX.poff, kx, fm[0], st));
+    CK(hd_cluster_fmax(f[1], LY.w64, LY.poff, ky, fm[1], st));
+    CK(hd_cluster_fmax(f[2], LY.w64, LY.poff, ky, fm[2], st));
+    CK(hd_cluster_fmax(f[3], LX.w64, LX.poff, kx, fm[3], st));
+    CK(truncation_masks_hd(kx, kx, d, LX.centers, LX.radii, fm[0], LX.centers, LX.radii, fm[0], e,
+                           theta, 1, mxx, nullptr, bxr, nullptr, st));
+    CK(truncation_masks_hd(ky, ky, d, LY.centers, LY.radii, fm[1], LY.centers, LY.radii, fm[1], e,
+                           theta, 1, myy, nullptr, byr, nullptr, st));
+    CK(truncation_masks_hd(kx, ky, d, LX.centers, LX.radii, fm[3], LY.centers, LY.radii, fm[2], e,
+                           theta, 0, mxy, myx, bxr, byr, st));
+    sym_rangeset(c, "hs.xx", LX.labels, LX.poff_h, nr, LX.poff, kx, mxx, 1, sxx);
+    sym_rangeset(c, "hs.yy", LY.labels, LY.poff_h, mr, LY.poff, ky, myy, 1, syy);
+    sym_rangeset(c, "hs.yx", LX.labels, LX.poff_h, nr, LY.poff, ky, mxy, 0, syx);
+    Pf.np = 3;
+    Pf.ps[0] = {nullptr, nr, nullptr, LX.lw2, nr, &sxx.R, {LX.pack, LX.pack, LX.sq, LX.sq, LX.f, LX.f}, &sxx, LX.lw2};
+    Pf.ps[1] = {nullptr, mr, nullptr, LY.lw2, mr, &syy.R, {LY.pack, LY.pack, LY.sq, LY.sq, LY.f, LY.f}, &syy, LY.lw2};
+    Pf.ps[2] = {nullptr, nr, nullptr, LY.lw2, mr, &syx.R, {LX.pack, LY.pack, LX.sq, LY.sq, LX.f, LY.f}, &syx, LX.lw2};
+    build_plan(c, "hpf", Pf);
+  };
+  for (int t = tsw; t <= ns; ++t) {
+    const int tt = std::min(t, ns - 1);
+    const bool rebuild =
+        (t == tsw) || (prm->retruncate > 0 && t < ns && (t - tsw) % prm->retruncate == 0);
+    if (rebuild) {
+      c->mark(3);
+      build_masks(eps[tt]);
+    }
+    c->mark(4);
+    sym_step_once(c, Pf, U, cur, eps[tt], lam[tt], t == ns, ss, scol);
+    S->pairs_dense += full;
+    S->pairs_fine += Pf.pairs_all;
+    S->pairs_fine_dense += full;
+  }
+  (void)coarse;
+}
+
 // transfer_labels request (K9): atlas labels in the caller's order of y.
 struct LabelReq {
   const int32_t* labels;  // host, M entries in [0, L)
@@ -858,13 +1126,17 @@ void transfer_labels_dev(msot_ctx* c, const LabelReq& q, const DMeasure& X, cons
   const int L = q.n_classes;
   const bool hd = d > 3;
   const int64_t pad = hd ? 128 : 1;
-  // solver column index of each caller atom of y (3-D measures are sorted)
+  // n: rows of the solver's layout (X.n; padded for high-D multiscale).
+  // solver slot of each caller atom of y: sorted 3-D measures and padded
+  // high-D multiscale layouts carry a slot -> caller permutation (-1 =
+  // padding), the dense high-D layout is the caller's order
   std::vector<int32_t> solver_of(m);
-  if (!hd) {
-    std::vector<int32_t> perm(m);
-    CK(cudaMemcpyAsync(perm.data(), Y.perm, m * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  if (Y.perm) {
+    std::vector<int32_t> perm(Y.n);
+    CK(cudaMemcpyAsync(perm.data(), Y.perm, Y.n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    for (int64_t k = 0; k < m; ++k) solver_of[perm[k]] = static_cast<int32_t>(k);
+    for (int64_t k = 0; k < Y.n; ++k)
+      if (perm[k] >= 0) solver_of[perm[k]] = static_cast<int32_t>(k);
   } else {
     for (int64_t j = 0; j < m; ++j) solver_of[j] = static_cast<int32_t>(j);
   }
@@ -876,11 +1148,17 @@ void transfer_labels_dev(msot_ctx* c, const LabelReq& q, const DMeasure& X, cons
   }
   for (int l = 0; l < L; ++l) seg[l + 1] = seg[l] + (cnt[l] + pad - 1) / pad * pad;
   const int64_t mpad = std::max<int64_t>(seg[L], 1);
-  std::vector<int32_t> src(mpad, -1);
+  std::vector<int32_t> src(mpad, -1), csrc(mpad, -1);  // solver slot / caller index
   std::vector<int64_t> fill(seg.begin(), seg.end() - 1);
-  for (int64_t j = 0; j < m; ++j) src[fill[q.labels[j]]++] = hd ? static_cast<int32_t>(j) : solver_of[j];
+  for (int64_t j = 0; j < m; ++j) {
+    const int64_t p = fill[q.labels[j]]++;
+    src[p] = solver_of[j];
+    csrc[p] = static_cast<int32_t>(j);
+  }
   int32_t* dsrc = c->buf<int32_t>("lab.src", mpad);
+  int32_t* dcsrc = c->buf<int32_t>("lab.csrc", mpad);
   CK(cudaMemcpyAsync(dsrc, src.data(), mpad * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dcsrc, csrc.data(), mpad * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   float* lwL = c->buf<float>("lab.lw", mpad);
   float* hL = c->buf<float>("lab.h", mpad);
   float4* colsL = hd ? nullptr : c->buf<float4>("lab.cols", mpad);
@@ -889,7 +1167,7 @@ void transfer_labels_dev(msot_ctx* c, const LabelReq& q, const DMeasure& X, cons
   float* sqL = nullptr;
   if (hd) {
     double* yL = c->buf<double>("lab.y64", mpad * d);
-    CK(gather_rows_f64(d_y, d, dsrc, mpad, yL, st));
+    CK(gather_rows_f64(d_y, d, dcsrc, mpad, yL, st));
     bL = c->buf<uint8_t>("lab.bpack", hd_pack_bytes(mpad));
     sqL = c->buf<float>("lab.sq", hd_padded(mpad));
     CK(hd_pack(yL, mpad, d, hd_cen, 1, bL, sqL, nullptr, st));
@@ -949,8 +1227,7 @@ void transfer_labels_dev(msot_ctx* c, const LabelReq& q, const DMeasure& X, cons
     Q.col_c = cc;
   }
   CK(hd ? launch_softmin_hd(G, d, c->n_sm, false, st) : launch_softmin(G, d, st));
-  CK(label_finalize(G.part, dlbase, R.tile_start, T, L, hd ? nullptr : X.perm, q.d_scores,
-                    q.d_mass, st));
+  CK(label_finalize(G.part, dlbase, R.tile_start, T, L, X.perm, q.d_scores, q.d_mass, st));
   CK(cudaStreamSynchronize(st));  // host vectors above go out of scope
 }
 
@@ -1002,6 +1279,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
   Potentials U;
   alloc_pots(c, "pot", n, m, U);
   int cur = 0;
+  int64_t nr = n, mr = m;  // rows of the internal layout (padded for high-D multiscale)
   const double full = double(n) * n + double(m) * m + 2.0 * double(n) * m;
   RangeSet fxx, fyy, fxy, fyx;  // ranges of the last update (the plan reuses them)
   DMeasure X, Y;
@@ -1012,13 +1290,17 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
   if (d > 3) {
     // ---- high feature dimension (config 4): dense eps-scaling, <x,y> on
     // the tensor cores (softmin_hd.cu); the voxel grid needs D <= 3
-    if (ms) raise(MSOT_EUSAGE, "voxel-grid multiscale needs D <= 3 (K-means coarsening is next)");
     if (d > 64) raise(MSOT_EUSAGE, "the high-dimensional softmin supports D <= 64");
     if (d_grad) raise(MSOT_EUSAGE, "grad_positions is implemented for D <= 3");
     std::vector<double> center(d);
     for (int k = 0; k < d; ++k) center[k] = 0.5 * (lo[k] + hi[k]);
     double* dcen = c->buf<double>("hd.center", d);
     CK(cudaMemcpyAsync(dcen, center.data(), d * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (ms) {
+      hd_multiscale(c, prm, d_x, d_a, n, d_y, d_b, m, d, dcen, diam, sig, eps, lam, ns, U, cur,
+                    X, Y, nr, mr, hd_ax, hd_sqx, ss, S);
+      hd_cen = dcen;
+    } else {
     // one [hi | lo] pack per measure serves as A (rows) and B (columns)
     uint8_t* ax = c->buf<uint8_t>("hd.ax", hd_pack_bytes(n));
     uint8_t* ay = c->buf<uint8_t>("hd.ay", hd_pack_bytes(m));
@@ -1082,6 +1364,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
         sym_step(c, P, U, cur, eps[tt], lam[tt], t == ns, ss);
       S->pairs_dense += full;
     }
+    }  // dense high-D
   } else {
   GridSpec g{};
   g.d = d;
@@ -1346,7 +1629,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
   if (lreq) {
     c->mark(6);
     float** f = U.v[cur];
-    transfer_labels_dev(c, *lreq, X, Y, n, m, d, d_y, hd_cen, hd_ax, hd_sqx, f[3], f[2],
+    transfer_labels_dev(c, *lreq, X, Y, nr, m, d, d_y, hd_cen, hd_ax, hd_sqx, f[3], f[2],
                         eps[ns - 1]);
   }
 
@@ -1357,7 +1640,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
   double* partials = c->buf<double>("loss.part", 5 * nb);
   double* lout = c->buf<double>("loss.out", 4);
   float** f = U.v[cur];
-  CK(divergence_partial(X.w64, Y.w64, n, m, f[0], f[1], f[2], f[3], rho, partials, nb, st));
+  CK(divergence_partial(X.w64, Y.w64, nr, mr, f[0], f[1], f[2], f[3], rho, partials, nb, st));
   CK(divergence_final(partials, nb, eps[ns - 1], rho, lout, st));
   double res[4];
   int32_t fbt = 0;
@@ -1365,16 +1648,17 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
   CK(cudaMemcpyAsync(&fbt, ss.fb_total, sizeof(fbt), cudaMemcpyDeviceToHost, st));
   if (h_pots) {
     double* tmp = c->buf<double>("unsort", std::max(n, m));
-    const int64_t len[4] = {n, m, m, n};
+    const int64_t len[4] = {nr, mr, mr, nr};   // internal rows (padding skipped by perm < 0)
+    const int64_t outn[4] = {n, m, m, n};
     const int32_t* perm[4] = {X.perm, Y.perm, Y.perm, X.perm};
     // canonical gauge of the balanced cross pair (loss.cu): a_xy - c, b_yx + c
     const double sign[4] = {0.0, 0.0, -1.0, 1.0};
     for (int q = 0; q < 4; ++q) {
       if (!h_pots[q]) continue;
       CK(scatter_unsort(f[q], perm[q], len[q], lout + 3, sign[q], tmp, st));
-      CK(cudaMemcpyAsync(h_pots[q], tmp, len[q] * sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(h_pots[q], tmp, outn[q] * sizeof(double), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
-      S->d2h_bytes += len[q] * sizeof(double);
+      S->d2h_bytes += outn[q] * sizeof(double);
     }
   }
   c->mark(-1);

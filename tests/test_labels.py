@@ -143,6 +143,22 @@ def test_labels_fibres_hd(ctx, oracle):
 
 
 @pytest.mark.gpu
+def test_labels_fibres_hd_multiscale(ctx, oracle):
+    """Label transfer on the padded K-means layout of the high-D multiscale solver."""
+    fa, la = W.fibres(600, 7, bundles=6, bundle_seed=2)
+    fb, lb = W.fibres(500, 8, bundles=6, bundle_seed=2)
+    x, a = W.flip_augment(*W.encode_fibers(fa))
+    y, b = W.flip_augment(*W.encode_fibers(fb))
+    lab = np.concatenate([lb, lb]).astype(np.int32)
+    prm = make_params(blur=0.03, reach=0.3, multiscale=True, retruncate=1, switch_factor=1.0,
+                      clusters=10)
+    soft, _, st = ctx.transfer_labels(prm, x, a, y, b, lab, 6)
+    assert st["t_switch"] > 0
+    sc, rm = oracle_labels(oracle, prm, x, a, y, b, lab, 6)
+    _check(soft, sc, rm)
+
+
+@pytest.mark.gpu
 def test_labels_errors(ctx):
     x = np.zeros((3, 3))
     with pytest.raises(DataError):

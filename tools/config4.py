@@ -2,7 +2,8 @@
 to 400k vs 400k, reach = 0.3, blur = 0.03, dense
 eps-scaling with the tcgen05 softmin, then label transfer (K9) of the atlas
 bundle labels, resolve_flips and classify.
-    python tools/config4.py [n_fibres] [bundles]"""
+    python tools/config4.py [n_fibres] [bundles] [dense|ms] [clusters]
+(ms: K-means multiscale + block-sparse fine phase; dense: all pairs)"""
 import json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -12,6 +13,10 @@ from paper_2107_02010_b200.solver import Context, classify, resolve_flips
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 200000
 L = int(sys.argv[2]) if len(sys.argv) > 2 else 50
+mode = sys.argv[3] if len(sys.argv) > 3 else "ms"
+kcl = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+sf = float(sys.argv[5]) if len(sys.argv) > 5 else 2.0
+tr = int(sys.argv[6]) if len(sys.argv) > 6 else 1
 t = time.perf_counter()
 fa, la = W.fibres(n, 7, bundles=L, bundle_seed=1)   # subject
 fb, lb = W.fibres(n, 8, bundles=L, bundle_seed=1)   # atlas (shares the bundles)
@@ -21,7 +26,8 @@ lab = np.concatenate([lb, lb]).astype(np.int32)
 prep = time.perf_counter() - t
 ctx = Context(0)
 ctx.set_profiling(True)
-prm = make_params(blur=0.03, reach=0.3)
+prm = make_params(blur=0.03, reach=0.3, multiscale=(mode == "ms"), retruncate=1,
+                  switch_factor=sf, clusters=kcl, transfer_rule=tr)
 for rep in range(2):
     t = time.perf_counter()
     soft, loss, st = ctx.transfer_labels(prm, x, a, y, b, lab, L)
@@ -29,7 +35,9 @@ for rep in range(2):
 out, chosen = resolve_flips(soft, np.tile(np.arange(n), 2), np.repeat([0, 1], n))
 hard, conf = classify(out, 0.5)
 inl = hard >= 0
-print(json.dumps(dict(atoms=[len(x), len(y)], D=x.shape[1], classes=L, prep_s=prep, wall_s=wall,
+print(json.dumps(dict(mode=mode, switch_factor=sf, transfer_rule=tr, kx=st["kx"], t_switch=st["t_switch"],
+                      fine_kept=st["pairs_fine"] / max(st["pairs_fine_dense"], 1.0),
+                      atoms=[len(x), len(y)], D=x.shape[1], classes=L, prep_s=prep, wall_s=wall,
                       device_ms=st["total_ms"], softmin_ms=st["softmin_ms"],
                       phases=st["phase_ms"], loss=loss, n_scales=st["n_scales"],
                       pairs=st["pairs_evaluated"],

@@ -286,6 +286,6 @@ def test_errors(ctx):
         ctx.sinkhorn(make_params(scaling=1.5), x, np.ones(3), x, np.ones(3))
     with pytest.raises(UsageError):
         ctx.sinkhorn(make_params(), np.zeros((3, 65)), np.ones(3), np.zeros((3, 65)), np.ones(3))
-    with pytest.raises(UsageError):  # voxel grid needs D <= 3
-        ctx.sinkhorn(make_params(multiscale=True), np.zeros((3, 5)), np.ones(3),
+    with pytest.raises(UsageError):  # high-D multiscale (K-means) is evaluate-once only
+        ctx.sinkhorn(make_params(multiscale=True, pair_eval=0), np.zeros((3, 5)), np.ones(3),
                      np.zeros((3, 5)), np.ones(3))

@@ -65,7 +65,8 @@ __device__ __forceinline__ int warp_sum16_col(int lane) {
 // the column butterfly is shared by 128 rows per warp.
 constexpr int kSymThreads = 64;
 constexpr int kSymRows = kTileRows / kSymThreads;  // 4
-constexpr int kSymCols = kSymThreads;              // columns staged per buffer
+constexpr int kSymColsPerThread = 2;
+constexpr int kSymCols = kSymThreads * kSymColsPerThread;  // columns staged per buffer
 static_assert(kSymRows == 4, "softmin_sym_kernel is written for 4 rows per thread");
 
 // kUni: every row weight equal and lambda = 1, so the row factor is one
@@ -110,40 +111,48 @@ softmin_sym_kernel(const __grid_constant__ Group G) {
   const int32_t pos_begin = item.z, pos_end = item.w;
   float* colout = P.colpart + P.tile_slot[item.y];
 
-  float4 cv = make_float4(0.f, 0.f, 0.f, 0.f);
-  float ch = 0.f, cl = 0.f;
-  bool cvalid = false;
+  // each thread fetches and stages columns tid + 64 q of every 128-column stage
+  float4 cv[kSymColsPerThread];
+  float ch[kSymColsPerThread], cl[kSymColsPerThread];
+  bool cvalid[kSymColsPerThread];
   auto fetch = [&](int32_t tile_pos) {
-    const int32_t pos = tile_pos + tid;
-    cvalid = false;
-    if (pos < pos_end) {
-      const int j = w.col(pos);
-      if (j >= 0) {
-        cv = __ldg(P.cols + j);
-        cl = __ldg(P.col_lw2 + j);
-        ch = __ldg(P.col_h + j);
-        cvalid = true;
+#pragma unroll
+    for (int q = 0; q < kSymColsPerThread; ++q) {
+      const int32_t pos = tile_pos + tid + q * kSymThreads;
+      cvalid[q] = false;
+      if (pos < pos_end) {
+        const int j = w.col(pos);
+        if (j >= 0) {
+          cv[q] = __ldg(P.cols + j);
+          cl[q] = __ldg(P.col_lw2 + j);
+          ch[q] = __ldg(P.col_h + j);
+          cvalid[q] = true;
+        }
       }
     }
   };
-  float cfac = 0.f;  // column factor of the column this thread staged
+  float cfac[kSymColsPerThread];  // column factors of the columns this thread staged
   auto stage = [&](float* buf) {
-    float* rec = buf + (tid >> 1) * 8 + (tid & 1);
-    if (cvalid) {
-      const float a = (cv.x - o.x) * P.sc;
-      const float b = D > 1 ? (cv.y - o.y) * P.sc : 0.f;
-      const float c = D > 2 ? (cv.z - o.z) * P.sc : 0.f;
-      rec[0] = a;
-      rec[2] = b;
-      rec[4] = c;
-      rec[6] = (fmaf(ch, P.inv_eps_ln2, R) + cl) - fmaf(a, a, fmaf(b, b, c * c));
-      cfac = exp2f(P.ell * (ch - est_mid) - cl);
-    } else {
-      rec[0] = 0.f;
-      rec[2] = 0.f;
-      rec[4] = 0.f;
-      rec[6] = __int_as_float(0xff800000);  // -inf -> exp2(-inf) = 0
-      cfac = 0.f;
+#pragma unroll
+    for (int q = 0; q < kSymColsPerThread; ++q) {
+      const int cidx = tid + q * kSymThreads;
+      float* rec = buf + (cidx >> 1) * 8 + (cidx & 1);
+      if (cvalid[q]) {
+        const float a = (cv[q].x - o.x) * P.sc;
+        const float b = D > 1 ? (cv[q].y - o.y) * P.sc : 0.f;
+        const float c = D > 2 ? (cv[q].z - o.z) * P.sc : 0.f;
+        rec[0] = a;
+        rec[2] = b;
+        rec[4] = c;
+        rec[6] = (fmaf(ch[q], P.inv_eps_ln2, R) + cl[q]) - fmaf(a, a, fmaf(b, b, c * c));
+        cfac[q] = exp2f(P.ell * (ch[q] - est_mid) - cl[q]);
+      } else {
+        rec[0] = 0.f;
+        rec[2] = 0.f;
+        rec[4] = 0.f;
+        rec[6] = __int_as_float(0xff800000);  // -inf -> exp2(-inf) = 0
+        cfac[q] = 0.f;
+      }
     }
   };
 
@@ -193,13 +202,15 @@ softmin_sym_kernel(const __grid_constant__ Group G) {
       if ((lane & 1) == 0) colacc[warp][2 * c0 + warp_sum16_col(lane)] = cs;
     }
     __syncthreads();
-    {
-      const int32_t pos = tp + tid;
-      if (pos < pos_end) {
-        float s = colacc[0][tid];
 #pragma unroll
-        for (int q = 1; q < kSymThreads / 32; ++q) s += colacc[q][tid];
-        colout[pos] = kUni ? s * (cfac * wu) : s * cfac;
+    for (int q = 0; q < kSymColsPerThread; ++q) {
+      const int cidx = tid + q * kSymThreads;
+      const int32_t pos = tp + cidx;
+      if (pos < pos_end) {
+        float s = colacc[0][cidx];
+#pragma unroll
+        for (int k = 1; k < kSymThreads / 32; ++k) s += colacc[k][cidx];
+        colout[pos] = kUni ? s * (cfac[q] * wu) : s * cfac[q];
       }
     }
     buf ^= 1;

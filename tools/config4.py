@@ -16,7 +16,8 @@ L = int(sys.argv[2]) if len(sys.argv) > 2 else 50
 mode = sys.argv[3] if len(sys.argv) > 3 else "ms"
 kcl = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 sf = float(sys.argv[5]) if len(sys.argv) > 5 else 2.0
-tr = int(sys.argv[6]) if len(sys.argv) > 6 else 1
+tr = int(sys.argv[6]) if len(sys.argv) > 6 else 0
+th = float(sys.argv[7]) if len(sys.argv) > 7 else 12.5
 t = time.perf_counter()
 fa, la = W.fibres(n, 7, bundles=L, bundle_seed=1)   # subject
 fb, lb = W.fibres(n, 8, bundles=L, bundle_seed=1)   # atlas (shares the bundles)
@@ -27,7 +28,7 @@ prep = time.perf_counter() - t
 ctx = Context(0)
 ctx.set_profiling(True)
 prm = make_params(blur=0.03, reach=0.3, multiscale=(mode == "ms"), retruncate=1,
-                  switch_factor=sf, clusters=kcl, transfer_rule=tr)
+                  switch_factor=sf, clusters=kcl, transfer_rule=tr, theta=th)
 for rep in range(2):
     t = time.perf_counter()
     soft, loss, st = ctx.transfer_labels(prm, x, a, y, b, lab, L)
@@ -35,7 +36,8 @@ for rep in range(2):
 out, chosen = resolve_flips(soft, np.tile(np.arange(n), 2), np.repeat([0, 1], n))
 hard, conf = classify(out, 0.5)
 inl = hard >= 0
-print(json.dumps(dict(mode=mode, switch_factor=sf, transfer_rule=tr, kx=st["kx"], t_switch=st["t_switch"],
+print(json.dumps(dict(mode=mode, switch_factor=sf, transfer_rule=tr, theta=th, kx=st["kx"],
+                      t_switch=st["t_switch"],
                       fine_kept=st["pairs_fine"] / max(st["pairs_fine_dense"], 1.0),
                       atoms=[len(x), len(y)], D=x.shape[1], classes=L, prep_s=prep, wall_s=wall,
                       device_ms=st["total_ms"], softmin_ms=st["softmin_ms"],

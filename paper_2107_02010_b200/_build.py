@@ -73,6 +73,25 @@ def build_lib(verbose=False):
     return LIB
 
 
+CLI = os.path.join(HERE, "msot")
+
+
+def build_cli(verbose=False):
+    """The `msot` command line (csrc/cli.cpp), a host program
+    linked against libmsot_b200.so (rpath $ORIGIN)."""
+    src = os.path.join(CSRC, "cli.cpp")
+    if not _newer(CLI, [src, LIB] + _headers()):
+        return CLI
+    cmd = ["g++", "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include"), src, "-L" + HERE,
+           "-lmsot_b200", "-Wl,-rpath,$ORIGIN", "-o", CLI]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"cli build failed:\n{r.stdout}\n{r.stderr}")
+    return CLI
+
+
 def build_oracle(verbose=False):
     """Compiles the test oracle (and, where /root/reference exists, the
     reference's own numeric/parallel utilities into oracle/_ref)."""
@@ -95,4 +114,5 @@ def build_oracle(verbose=False):
 
 if __name__ == "__main__":
     print(build_lib(verbose=True))
+    print(build_cli(verbose=True))
     print(build_oracle(verbose=True))

@@ -1,0 +1,451 @@
+// cli.cpp — the `msot` command line:
+// file formats on one side, the GPU solver on the
+// other, through the msot:: front-end (include/msot/*.hpp).
+//
+//   msot divergence A B     [--blur --reach --p --scaling --clusters --theta --seed --multiscale]
+//   msot plan A B           [--tau mass threshold]        -> "i j mass" lines
+//   msot transfer SUBJ ATLAS LABELS [--tau]               -> "index label confidence row_mass"
+//   msot barycenter D1 D2 ... [--upsample k --iters n --step s]
+//   msot cluster A          [--clusters K | --cell s]     -> "index cluster" lines
+//   msot bench              [--sizes 1000,10000]          -> JSON per size
+//   msot verify                                          -> known answers, exit 0/4
+// Common: --out PATH, --format text|json.  Exit codes: 0 ok, 2 usage, 3 data,
+// 4 numeric, 5 device (SPEC.md:566 plus the CUDA/NCCL code).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <array>
+#include <fstream>
+#include <iomanip>
+#include <iostream>
+#include <map>
+#include <random>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/msot/barycenter.hpp"
+#include "../../include/msot/labels.hpp"
+#include "../../include/msot/measure.hpp"
+#include "../../include/msot/sinkhorn.hpp"
+
+namespace {
+
+struct Usage : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+struct Args {
+  std::string cmd;
+  std::vector<std::string> pos;
+  std::map<std::string, std::string> kv;
+  bool has(const std::string& k) const { return kv.count(k) > 0; }
+  double num(const std::string& k, double dflt) const {
+    auto it = kv.find(k);
+    if (it == kv.end()) return dflt;
+    if (it->second == "inf") return INFINITY;
+    char* end = nullptr;
+    const double v = std::strtod(it->second.c_str(), &end);
+    if (!end || *end) throw Usage("--" + k + ": not a number: " + it->second);
+    return v;
+  }
+  std::string str(const std::string& k, const std::string& dflt) const {
+    auto it = kv.find(k);
+    return it == kv.end() ? dflt : it->second;
+  }
+};
+
+Args parse_args(int argc, char** argv) {
+  if (argc < 2) throw Usage("missing command");
+  Args a;
+  a.cmd = argv[1];
+  for (int i = 2; i < argc; ++i) {
+    std::string s = argv[i];
+    if (s.rfind("--", 0) == 0) {
+      std::string k = s.substr(2), v = "1";
+      const auto eq = k.find('=');
+      if (eq != std::string::npos) {
+        v = k.substr(eq + 1);
+        k = k.substr(0, eq);
+      } else if (k != "multiscale" && i + 1 < argc) {
+        v = argv[++i];
+      }
+      a.kv[k] = v;
+    } else {
+      a.pos.push_back(s);
+    }
+  }
+  return a;
+}
+
+msot::SolverParams params_of(const Args& a, double blur_default, double reach_default) {
+  msot::SolverParams p;
+  p.blur = a.num("blur", blur_default);
+  p.reach = a.num("reach", reach_default);
+  p.cost.p = a.num("p", 2.0);
+  p.scaling = a.num("scaling", 0.9);
+  p.theta = a.num("theta", 20.0);
+  p.clusters = static_cast<int>(a.num("clusters", 0));
+  p.seed = static_cast<int>(a.num("seed", 0));
+  p.multiscale = a.has("multiscale");
+  p.retruncate = p.multiscale ? 1 : 0;
+  if (!(p.blur > 0)) throw Usage("--blur must be > 0");
+  if (!(p.reach > 0)) throw Usage("--reach must be > 0 or inf");
+  if (!(p.scaling > 0 && p.scaling < 1)) throw Usage("--scaling must lie in (0, 1)");
+  return p;
+}
+
+// ---------------------------------------------------------------- file formats
+std::vector<std::string> lines_of(const std::string& path) {
+  std::ifstream f(path);
+  if (!f) throw msot::DataError("cannot open " + path);
+  std::vector<std::string> out;
+  std::string l;
+  while (std::getline(f, l)) out.push_back(l);
+  return out;
+}
+
+bool blank(const std::string& l) {
+  const auto p = l.find_first_not_of(" \t\r");
+  return p == std::string::npos || l[p] == '#';
+}
+
+// point cloud: "weight coord_1 ... coord_D" per line
+msot::DiscreteMeasure read_points(const std::string& path) {
+  std::vector<double> pts, w;
+  std::size_t dim = 0;
+  int ln = 0;
+  for (const std::string& l : lines_of(path)) {
+    ++ln;
+    if (blank(l)) continue;
+    std::istringstream is(l);
+    std::vector<double> v;
+    double q;
+    while (is >> q) v.push_back(q);
+    if (!is.eof() || v.size() < 2)
+      throw msot::DataError(path + ":" + std::to_string(ln) + ": expected 'weight coords...'");
+    if (dim == 0) dim = v.size() - 1;
+    if (v.size() - 1 != dim)
+      throw msot::DataError(path + ":" + std::to_string(ln) + ": dimension changes");
+    w.push_back(v[0]);
+    pts.insert(pts.end(), v.begin() + 1, v.end());
+  }
+  if (w.empty()) throw msot::DataError(path + ": no atoms");
+  return msot::DiscreteMeasure(std::move(pts), std::move(w), dim);
+}
+
+// fiber file: "fiber <n>" then n lines "x y z"
+msot::FiberSet read_fibers(const std::string& path) {
+  msot::FiberSet fs;
+  const auto ls = lines_of(path);
+  for (std::size_t i = 0; i < ls.size(); ++i) {
+    if (blank(ls[i])) continue;
+    std::istringstream is(ls[i]);
+    std::string tag;
+    long n = 0;
+    if (!(is >> tag >> n) || tag != "fiber" || n < 1)
+      throw msot::DataError(path + ":" + std::to_string(i + 1) + ": expected 'fiber <n>'");
+    msot::Polyline line;
+    for (long k = 0; k < n; ++k) {
+      if (++i >= ls.size()) throw msot::DataError(path + ": truncated fiber");
+      std::istringstream ps(ls[i]);
+      std::array<double, 3> p{};
+      if (!(ps >> p[0] >> p[1] >> p[2]))
+        throw msot::DataError(path + ":" + std::to_string(i + 1) + ": expected 'x y z'");
+      line.push_back(p);
+    }
+    fs.fibers.push_back(std::move(line));
+  }
+  if (fs.fibers.empty()) throw msot::DataError(path + ": no fibers");
+  return fs;
+}
+
+// density file: header "density nx ny nz voxel ox oy oz", then "i j k value"
+msot::DensityMap read_density(const std::string& path) {
+  const auto ls = lines_of(path);
+  msot::DensityMap d;
+  bool head = false;
+  for (std::size_t i = 0; i < ls.size(); ++i) {
+    if (blank(ls[i])) continue;
+    std::istringstream is(ls[i]);
+    if (!head) {
+      std::string tag;
+      if (!(is >> tag >> d.nx >> d.ny >> d.nz >> d.voxel_mm >> d.origin[0] >> d.origin[1] >>
+            d.origin[2]) || tag != "density")
+        throw msot::DataError(path + ":" + std::to_string(i + 1) + ": expected the density header");
+      head = true;
+      continue;
+    }
+    msot::DensityVoxel v;
+    if (!(is >> v.i >> v.j >> v.k >> v.value))
+      throw msot::DataError(path + ":" + std::to_string(i + 1) + ": expected 'i j k value'");
+    d.voxels.push_back(v);
+  }
+  if (!head) throw msot::DataError(path + ": empty density file");
+  return d;
+}
+
+std::string first_token(const std::string& path) {
+  for (const std::string& l : lines_of(path)) {
+    if (blank(l)) continue;
+    std::istringstream is(l);
+    std::string t;
+    is >> t;
+    return t;
+  }
+  return "";
+}
+
+// any measure file: point cloud, fiber file (encoded, P = 20) or density file
+msot::DiscreteMeasure read_measure(const std::string& path) {
+  const std::string t = first_token(path);
+  if (t == "fiber") return msot::encode_fibers(read_fibers(path));
+  if (t == "density") return msot::density_to_measure(read_density(path));
+  return read_points(path);
+}
+
+// label file: "atom_index class_name" per line
+msot::LabelSet read_labels(const std::string& path, std::size_t atoms) {
+  msot::LabelSet ls;
+  ls.assignments.assign(atoms, -1);
+  std::map<std::string, int> id;
+  int ln = 0;
+  for (const std::string& l : lines_of(path)) {
+    ++ln;
+    if (blank(l)) continue;
+    std::istringstream is(l);
+    long idx;
+    std::string name;
+    if (!(is >> idx >> name) || idx < 0 || static_cast<std::size_t>(idx) >= atoms)
+      throw msot::DataError(path + ":" + std::to_string(ln) + ": expected 'atom_index class_name'");
+    auto it = id.find(name);
+    if (it == id.end()) {
+      it = id.emplace(name, static_cast<int>(ls.names.size())).first;
+      ls.names.push_back(name);
+    }
+    ls.assignments[idx] = it->second;
+  }
+  for (std::size_t j = 0; j < atoms; ++j)
+    if (ls.assignments[j] < 0) throw msot::DataError(path + ": atom " + std::to_string(j) + " has no label");
+  ls.L = static_cast<int>(ls.names.size());
+  return ls;
+}
+
+struct Out {
+  std::ofstream file;
+  std::ostream* os = &std::cout;
+  explicit Out(const Args& a) {
+    if (a.has("out")) {
+      file.open(a.str("out", ""));
+      if (!file) throw msot::DataError("cannot write " + a.str("out", ""));
+      os = &file;
+    }
+  }
+  std::ostream& operator()() { return *os; }
+};
+
+double seconds_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// ------------------------------------------------------------------ commands
+int cmd_divergence(const Args& a) {
+  if (a.pos.size() != 2) throw Usage("divergence needs two measure files");
+  const auto A = read_measure(a.pos[0]), B = read_measure(a.pos[1]);
+  const msot::SolverParams p = params_of(a, 0.05, INFINITY);
+  const auto t0 = std::chrono::steady_clock::now();
+  const double v = msot::divergence(A, B, p);
+  const double sec = seconds_since(t0);
+  const std::size_t iters = msot::make_schedule(msot::diameter_estimate(A, B, p.blur), p).size();
+  Out out(a);
+  if (a.str("format", "text") == "json")
+    out() << "{\"value\": " << std::setprecision(17) << v << ", \"iters\": " << iters
+          << ", \"seconds\": " << sec << ", \"atoms\": [" << A.size() << ", " << B.size() << "]}\n";
+  else
+    out() << std::setprecision(12) << "S_eps = " << v << "  (schedule " << iters << ", "
+          << sec << " s, atoms " << A.size() << " x " << B.size() << ")\n";
+  return 0;
+}
+
+int cmd_plan(const Args& a) {
+  if (a.pos.size() != 2) throw Usage("plan needs two measure files");
+  const auto A = read_measure(a.pos[0]), B = read_measure(a.pos[1]);
+  const msot::SolverParams p = params_of(a, 0.05, INFINITY);
+  const double tau = a.num("tau", 1e-9);
+  const msot::DualPotentials u =
+      p.multiscale ? msot::multiscale_sinkhorn(A, B, p) : msot::symmetric_sinkhorn(A, B, p);
+  Out out(a);
+  out() << std::setprecision(12);
+  for (std::size_t i = 0; i < A.size(); ++i)
+    for (std::size_t j = 0; j < B.size(); ++j) {
+      const double pm = msot::plan_entry(i, j, A, B, u, p);
+      if (pm >= tau) out() << i << " " << j << " " << pm << "\n";
+    }
+  return 0;
+}
+
+int cmd_transfer(const Args& a) {
+  if (a.pos.size() != 3) throw Usage("transfer needs SUBJECT ATLAS LABELS");
+  msot::FiberSet subj = read_fibers(a.pos[0]), atlas = read_fibers(a.pos[1]);
+  const int P = static_cast<int>(a.num("resample", 20));
+  subj.resample_count = atlas.resample_count = P;
+  const auto sa = msot::flip_augment(msot::encode_fibers(subj), P);
+  const auto aa = msot::flip_augment(msot::encode_fibers(atlas), P);
+  msot::LabelSet ls = read_labels(a.pos[2], atlas.fibers.size());
+  msot::LabelSet aug = ls;
+  aug.assignments.insert(aug.assignments.end(), ls.assignments.begin(), ls.assignments.end());
+  // PAPER.md §3: blur 2 mm, reach 20 mm; fibre coordinates are scaled by 1/sqrt(P)
+  const msot::SolverParams p = params_of(a, 2.0, 20.0);
+  const msot::SoftLabels soft = msot::transfer_labels(sa.measure, aa.measure, aug, p);
+  const msot::SoftLabels res = msot::resolve_flips(soft, sa.map);
+  const msot::Classification cl = msot::classify(res, a.num("tau", 0.5));
+  Out out(a);
+  std::map<std::string, int> counts;
+  out() << std::setprecision(6);
+  for (std::size_t i = 0; i < res.n; ++i) {
+    const std::string name = cl.label[i] == msot::OUTLIER ? "OUTLIER" : ls.names[cl.label[i]];
+    ++counts[name];
+    out() << i << " " << name << " " << cl.confidence[i] << " " << res.row_mass[i] << "\n";
+  }
+  for (const auto& kv : counts) std::cout << kv.first << ": " << kv.second << "\n";
+  return 0;
+}
+
+int cmd_barycenter(const Args& a) {
+  if (a.pos.empty()) throw Usage("barycenter needs at least one density file");
+  std::vector<msot::DensityMap> maps;
+  for (const auto& f : a.pos) maps.push_back(read_density(f));
+  std::vector<msot::DiscreteMeasure> targets;
+  for (const auto& m : maps) targets.push_back(msot::density_to_measure(m));
+  // init: arithmetic average of the maps, upsampled with jitter
+  msot::DensityMap avg = maps[0];
+  std::map<std::array<int, 3>, double> acc;
+  for (const auto& m : maps)
+    for (const auto& v : m.voxels) acc[{v.i, v.j, v.k}] += v.value / maps.size();
+  avg.voxels.clear();
+  for (const auto& kv : acc) avg.voxels.push_back({kv.first[0], kv.first[1], kv.first[2], kv.second});
+  const msot::DiscreteMeasure base = msot::density_to_measure(avg);
+  const int up = static_cast<int>(a.num("upsample", 6));
+  std::mt19937_64 rng(static_cast<uint64_t>(a.num("seed", 0)));
+  std::uniform_real_distribution<double> jit(-0.25 * avg.voxel_mm, 0.25 * avg.voxel_mm);
+  std::vector<double> pts, w;
+  for (std::size_t i = 0; i < base.size(); ++i)
+    for (int q = 0; q < up; ++q) {
+      for (int k = 0; k < 3; ++k) pts.push_back(base.point(i)[k] + jit(rng));
+      w.push_back(base.weights()[i] / up);
+    }
+  const msot::DiscreteMeasure init(std::move(pts), std::move(w), 3);
+  msot::SolverParams p = params_of(a, avg.voxel_mm, INFINITY);
+  if (!std::isinf(p.reach)) throw Usage("barycenter: reach must be inf (SPEC.md:330)");
+  msot::BarycenterConfig cfg{static_cast<int>(a.num("iters", 10)), a.num("step", 1.0),
+                             a.num("tol", 1e-4)};
+  const msot::BarycenterResult r = msot::barycenter(targets, init, p, cfg);
+  Out out(a);
+  out() << std::setprecision(12) << "# loss";
+  for (double l : r.loss) out() << " " << l;
+  out() << "\n";
+  for (std::size_t i = 0; i < r.measure.size(); ++i)
+    out() << r.measure.weights()[i] << " " << r.measure.point(i)[0] << " "
+          << r.measure.point(i)[1] << " " << r.measure.point(i)[2] << "\n";
+  return 0;
+}
+
+int cmd_cluster(const Args& a) {
+  if (a.pos.size() != 1) throw Usage("cluster needs one measure file");
+  const auto A = read_measure(a.pos[0]);
+  const int K = static_cast<int>(a.num("clusters", std::ceil(std::sqrt(double(A.size())))));
+  std::vector<int32_t> perm(A.size()), off(K + 1), lab(A.size());
+  std::vector<double> cen(size_t(K) * A.dim()), cw(K);
+  std::vector<float> rad(K);
+  int it = 0;
+  msot::throw_on_status(
+      msot_kmeans(msot::default_device().get(), A.points().data(), A.weights().data(),
+                  static_cast<int64_t>(A.size()), static_cast<int>(A.dim()), K,
+                  static_cast<uint64_t>(a.num("seed", 0)), perm.data(), off.data(), lab.data(),
+                  cen.data(), cw.data(), rad.data(), &it),
+      "kmeans");
+  Out out(a);
+  for (std::size_t i = 0; i < A.size(); ++i) out() << i << " " << lab[i] << "\n";
+  std::cout << "K = " << K << ", Lloyd iterations = " << it << "\n";
+  return 0;
+}
+
+int cmd_bench(const Args& a) {
+  std::vector<long> sizes;
+  std::istringstream is(a.str("sizes", "1000,10000,100000"));
+  for (std::string t; std::getline(is, t, ',');) sizes.push_back(std::stol(t));
+  for (long n : sizes)
+    if (n < 1) throw Usage("--sizes must be >= 1");
+  std::mt19937_64 rng(static_cast<uint64_t>(a.num("seed", 0)));
+  std::uniform_real_distribution<double> u(0.0, 1.0);
+  for (long n : sizes) {
+    std::vector<double> xp(3 * n), yp(3 * n), w(n, 1.0 / n);
+    for (auto& v : xp) v = u(rng);
+    for (auto& v : yp) v = u(rng);
+    msot::DiscreteMeasure A(xp, w, 3), B(yp, w, 3);
+    for (int ms = 0; ms < 2; ++ms) {
+      msot::SolverParams p = params_of(a, 0.05, INFINITY);
+      p.multiscale = ms == 1;
+      p.retruncate = ms;
+      const msot_params cp = p.to_c();
+      msot_stats st{};
+      double loss = 0.0;
+      const auto t0 = std::chrono::steady_clock::now();
+      msot::throw_on_status(msot_sinkhorn(msot::default_device().get(), &cp, A.points().data(),
+                                          A.weights().data(), n, B.points().data(),
+                                          B.weights().data(), n, 3, nullptr, nullptr, nullptr,
+                                          nullptr, &loss, &st),
+                            "bench");
+      std::cout << "{\"n\": " << n << ", \"multiscale\": " << ms << ", \"value\": "
+                << std::setprecision(12) << loss << ", \"seconds\": " << seconds_since(t0)
+                << ", \"pairs\": " << st.pairs_evaluated << ", \"memory_bytes\": "
+                << static_cast<double>(n) * 2 * (3 * 8 + 8) << "}\n";
+    }
+  }
+  return 0;
+}
+
+int cmd_verify(const Args&) {
+  // known answers
+  msot::SolverParams p;
+  p.blur = 1e-3;
+  const double v = msot::divergence(msot::DiscreteMeasure({0.0}, {1.0}, 1),
+                                    msot::DiscreteMeasure({2.0}, {1.0}, 1), p);
+  const msot::DiscreteMeasure c({0.1, 0.5, 0.9, 0.3}, {0.25, 0.25, 0.25, 0.25}, 1);
+  const double z = msot::divergence(c, c, p);
+  const bool ok = std::fabs(v - 2.0) < 2e-2 && std::fabs(z) < 1e-9;
+  std::cout << "delta_0 vs delta_2: " << v << " (expect 2), S(a, a): " << z << " -> "
+            << (ok ? "ok" : "FAILED") << "\n";
+  return ok ? 0 : 4;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  try {
+    const Args a = parse_args(argc, argv);
+    if (a.cmd == "divergence") return cmd_divergence(a);
+    if (a.cmd == "plan") return cmd_plan(a);
+    if (a.cmd == "transfer") return cmd_transfer(a);
+    if (a.cmd == "barycenter") return cmd_barycenter(a);
+    if (a.cmd == "cluster") return cmd_cluster(a);
+    if (a.cmd == "bench") return cmd_bench(a);
+    if (a.cmd == "verify") return cmd_verify(a);
+    throw Usage("unknown command " + a.cmd);
+  } catch (const Usage& e) {
+    std::cerr << "usage error: " << e.what()
+              << "\ncommands: divergence plan transfer barycenter cluster bench verify\n";
+    return 2;
+  } catch (const msot::DataError& e) {
+    std::cerr << "data error: " << e.what() << "\n";
+    return 3;
+  } catch (const msot::NumericError& e) {
+    std::cerr << "numeric error: " << e.what() << "\n";
+    return 4;
+  } catch (const std::exception& e) {
+    std::cerr << "error: " << e.what() << "\n";
+    return 5;
+  }
+}

@@ -113,6 +113,15 @@ int msot_create(int device, msot_ctx** out);
 int msot_nccl_unique_id(unsigned char out[128]);
 int msot_create_dist(int device, int rank, int world, const unsigned char nccl_id[128],
                      msot_ctx** out);
+/* Test seam: the same sharded solve with host-staged collectives supplied by
+ * the caller (e.g. torch.distributed gloo) in place of NCCL, so the
+ * multi-rank logic runs with several processes on one GPU.  allreduce sums
+ * `count` floats in place across ranks; broadcast copies root's `count`
+ * floats to every rank.  Both return 0 on success. */
+typedef int (*msot_host_allreduce_fn)(float* data, int64_t count, void* user);
+typedef int (*msot_host_broadcast_fn)(float* data, int64_t count, int root, void* user);
+int msot_create_dist_host(int device, int rank, int world, msot_host_allreduce_fn allreduce,
+                          msot_host_broadcast_fn broadcast, void* user, msot_ctx** out);
 void msot_destroy(msot_ctx* ctx);
 /* 1 = time every softmin launch with CUDA events (stats.softmin_ms). */
 int msot_set_profiling(msot_ctx* ctx, int on);

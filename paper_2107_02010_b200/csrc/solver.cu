@@ -71,6 +71,10 @@ struct msot_ctx {
   int device = 0, rank = 0, world = 1, n_sm = 148;
   cudaStream_t st = nullptr;
   ncclComm_t comm = nullptr;
+  // test seam (msot_create_dist_host): host-staged collectives instead of NCCL
+  msot_host_allreduce_fn host_ar = nullptr;
+  msot_host_broadcast_fn host_bc = nullptr;
+  void* host_user = nullptr;
   bool profiling = false;
   std::map<std::string, std::pair<void*, size_t>> bufs;
   std::vector<cudaEvent_t> ev;  // profiling events (pairs)
@@ -122,6 +126,58 @@ struct msot_ctx {
 };
 
 namespace {
+
+// ------------------------------------------------------------- collectives
+// The two exchange steps of a sharded scale: an all-reduce of
+// the column sums and a broadcast of every rank's row shard.  NCCL over
+// NVLink in the product; host-staged caller callbacks in the test seam.
+void coll_allreduce(msot_ctx* c, float* const* bufs, const int64_t* counts, int nb) {
+  if (c->world <= 1) return;
+  cudaStream_t st = c->st;
+  if (c->host_ar) {
+    for (int b = 0; b < nb; ++b) {
+      std::vector<float> h(counts[b]);
+      CK(cudaMemcpyAsync(h.data(), bufs[b], counts[b] * sizeof(float), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (c->host_ar(h.data(), counts[b], c->host_user) != 0) raise(MSOT_ECUDA, "host all-reduce failed");
+      CK(cudaMemcpyAsync(bufs[b], h.data(), counts[b] * sizeof(float), cudaMemcpyHostToDevice, st));
+      CK(cudaStreamSynchronize(st));
+    }
+    return;
+  }
+  NK(ncclGroupStart());
+  for (int b = 0; b < nb; ++b)
+    NK(ncclAllReduce(bufs[b], bufs[b], counts[b], ncclFloat, ncclSum, c->comm, st));
+  NK(ncclGroupEnd());
+}
+
+void coll_bcast_rows(msot_ctx* c, float* const* bufs, const std::vector<int64_t>* bounds, int nb) {
+  if (c->world <= 1) return;
+  cudaStream_t st = c->st;
+  if (c->host_bc) {
+    for (int b = 0; b < nb; ++b)
+      for (int r = 0; r < c->world; ++r) {
+        const int64_t b0 = bounds[b][r], b1 = bounds[b][r + 1];
+        if (b1 <= b0) continue;
+        std::vector<float> h(b1 - b0);
+        CK(cudaMemcpyAsync(h.data(), bufs[b] + b0, (b1 - b0) * sizeof(float),
+                           cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (c->host_bc(h.data(), b1 - b0, r, c->host_user) != 0) raise(MSOT_ECUDA, "host broadcast failed");
+        CK(cudaMemcpyAsync(bufs[b] + b0, h.data(), (b1 - b0) * sizeof(float),
+                           cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+      }
+    return;
+  }
+  NK(ncclGroupStart());
+  for (int b = 0; b < nb; ++b)
+    for (int r = 0; r < c->world; ++r) {
+      const int64_t b0 = bounds[b][r], b1 = bounds[b][r + 1];
+      if (b1 > b0) NK(ncclBroadcast(bufs[b] + b0, bufs[b] + b0, b1 - b0, ncclFloat, r, c->comm, st));
+    }
+  NK(ncclGroupEnd());
+}
 
 // ---------------------------------------------------------------- measures
 struct DMeasure {
@@ -560,15 +616,7 @@ void run_group(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& ss) {
   ss.S->pairs_evaluated += P.pairs_all;
   ss.S->pairs_terms += P.terms_all;
   // all-gather of the updated potentials (NCCL over NVLink)
-  if (c->world > 1) {
-    NK(ncclGroupStart());
-    for (int p = 0; p < P.np; ++p)
-      for (int r = 0; r < c->world; ++r) {
-        const int64_t b0 = P.row_bounds[p][r], b1 = P.row_bounds[p][r + 1];
-        if (b1 > b0) NK(ncclBroadcast(a.out[p] + b0, a.out[p] + b0, b1 - b0, ncclFloat, r, c->comm, st));
-      }
-    NK(ncclGroupEnd());
-  }
+  coll_bcast_rows(c, a.out, P.row_bounds, P.np);
 }
 
 // ------------------------------------------------------------------ solve
@@ -691,11 +739,9 @@ void run_group_sym(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& s
     }
     CK(launch_colsum(cs, 3, st));
   }
-  if (c->world > 1) {  // column sums of every rank's tiles (NCCL over NVLink)
-    NK(ncclGroupStart());
-    for (int p = 0; p < 3; ++p)
-      NK(ncclAllReduce(X.tot[p], X.tot[p], P.ps[p].n_cols, ncclFloat, ncclSum, c->comm, st));
-    NK(ncclGroupEnd());
+  {  // column sums of every rank's tiles (NCCL over NVLink)
+    const int64_t cnt[3] = {P.ps[0].n_cols, P.ps[1].n_cols, P.ps[2].n_cols};
+    coll_allreduce(c, X.tot, cnt, 3);
   }
   CK(launch_finalize(G, st));
   CK(launch_colfinal(G, 3, st));
@@ -703,15 +749,7 @@ void run_group_sym(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& s
   ss.S->softmin_launches += 1;
   ss.S->pairs_evaluated += P.pairs_all;
   ss.S->pairs_terms += P.terms_all;
-  if (c->world > 1) {  // all-gather of the row-side potentials
-    NK(ncclGroupStart());
-    for (int p = 0; p < 3; ++p)
-      for (int r = 0; r < c->world; ++r) {
-        const int64_t b0 = P.row_bounds[p][r], b1 = P.row_bounds[p][r + 1];
-        if (b1 > b0) NK(ncclBroadcast(a.out[p] + b0, a.out[p] + b0, b1 - b0, ncclFloat, r, c->comm, st));
-      }
-    NK(ncclGroupEnd());
-  }
+  coll_bcast_rows(c, a.out, P.row_bounds, 3);  // all-gather of the row-side potentials
 }
 
 
@@ -1781,6 +1819,27 @@ int msot_create_dist(int device, int rank, int world, const unsigned char nccl_i
         std::memcpy(&id, nccl_id, 128);
         NK(ncclCommInitRank(&c->comm, world, id, rank));
       }
+    } catch (...) {
+      delete c;
+      *out = nullptr;
+      throw;
+    }
+  });
+}
+
+int msot_create_dist_host(int device, int rank, int world, msot_host_allreduce_fn allreduce,
+                          msot_host_broadcast_fn broadcast, void* user, msot_ctx** out) {
+  return guard([&] {
+    if (world < 1 || rank < 0 || rank >= world) raise(MSOT_EUSAGE, "invalid rank/world");
+    if (!allreduce || !broadcast) raise(MSOT_EUSAGE, "both host collectives are required");
+    auto* c = new msot_ctx();
+    try {
+      create_common(device, out, c);
+      c->rank = rank;
+      c->world = world;
+      c->host_ar = allreduce;
+      c->host_bc = broadcast;
+      c->host_user = user;
     } catch (...) {
       delete c;
       *out = nullptr;

@@ -29,6 +29,10 @@ _lp = C.POINTER(C.c_int64)
 _bp = C.POINTER(C.c_uint8)
 
 
+_AR_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_float), C.c_int64, C.c_void_p)
+_BC_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_float), C.c_int64, C.c_int, C.c_void_p)
+
+
 def lib():
     global _LIB
     if _LIB is None:
@@ -42,6 +46,8 @@ def lib():
         L.msot_nccl_unique_id.argtypes = [C.c_char_p]
         L.msot_create_dist.argtypes = [C.c_int, C.c_int, C.c_int, C.c_char_p,
                                        C.POINTER(C.c_void_p)]
+        L.msot_create_dist_host.argtypes = [C.c_int, C.c_int, C.c_int, _AR_FN, _BC_FN, C.c_void_p,
+                                            C.POINTER(C.c_void_p)]
         L.msot_destroy.argtypes = [C.c_void_p]
         L.msot_destroy.restype = None
         L.msot_set_profiling.argtypes = [C.c_void_p, C.c_int]
@@ -87,7 +93,7 @@ EXPORTS = ["msot_last_error", "msot_params_default", "msot_create", "msot_nccl_u
            "msot_shard_tiles", "msot_softmin", "msot_grid_cluster", "msot_truncation_mask",
            "msot_sinkhorn", "msot_sinkhorn_device", "msot_probe_ex2", "msot_sinkhorn_grad",
            "msot_barycenter", "msot_transfer_labels", "msot_resolve_flips", "msot_classify",
-           "msot_plan_apply", "msot_kmeans"]
+           "msot_plan_apply", "msot_kmeans", "msot_create_dist_host"]
 
 
 def _check(rc):
@@ -199,9 +205,32 @@ def classify(soft, tau=0.5):
 class Context:
     """One GPU (one process per GPU; optional NCCL communicator)."""
 
-    def __init__(self, device=0, rank=0, world=1, nccl_id=None):
+    def __init__(self, device=0, rank=0, world=1, nccl_id=None, host_collectives=None):
+        """host_collectives: (allreduce(np.ndarray), broadcast(np.ndarray, root))
+        callables — the msot_create_dist_host test seam (several processes on
+        one GPU) instead of NCCL."""
         self._h = C.c_void_p()
-        if world > 1:
+        if host_collectives is not None:
+            ar, bc = host_collectives
+
+            def _ar(ptr, count, user):
+                try:
+                    ar(np.ctypeslib.as_array(ptr, shape=(count,)))
+                    return 0
+                except Exception:
+                    return 1
+
+            def _bc(ptr, count, root, user):
+                try:
+                    bc(np.ctypeslib.as_array(ptr, shape=(count,)), root)
+                    return 0
+                except Exception:
+                    return 1
+
+            self._cbs = (_AR_FN(_ar), _BC_FN(_bc))  # keep alive
+            _check(lib().msot_create_dist_host(device, rank, world, self._cbs[0], self._cbs[1],
+                                               None, C.byref(self._h)))
+        elif world > 1:
             if nccl_id is None or len(nccl_id) != 128:
                 raise ValueError("world > 1 needs the 128-byte NCCL id of rank 0")
             _check(lib().msot_create_dist(device, rank, world, bytes(nccl_id), C.byref(self._h)))

@@ -1,0 +1,143 @@
+"""Multi-rank solves on one GPU through the host-collective test seam
+(msot_create_dist_host): two processes, each a rank with its own context on
+cuda:0, exchanging column sums (all-reduce) and row shards (broadcast) over
+gloo instead of NCCL.  The sharded result must match the single-rank solve:
+bitwise for the row-wise (dense) path, to float rounding (1e-3 eps) for the
+evaluate-once path (its column sums are added across ranks)."""
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _mixture(n, seed):
+    rng = np.random.default_rng(seed)
+    cen = rng.uniform(0.2, 0.8, (6, 3))
+    return cen[rng.integers(0, 6, n)] + rng.normal(0, 0.05, (n, 3))
+
+
+CASES = {
+    "dense": dict(blur=0.05),
+    "multiscale": dict(blur=0.01, multiscale=True, retruncate=1, cluster_scale=0.04),
+    "unbalanced": dict(blur=0.02, reach=0.3, multiscale=True, retruncate=1, cluster_scale=0.04),
+}
+
+
+def _inputs(case):
+    if case.startswith("hd"):
+        from paper_2107_02010_b200 import workloads as W
+        fa, _ = W.fibres(700, 3)
+        fb, _ = W.fibres(600, 4)
+        x, a = W.encode_fibers(fa)
+        y, b = W.encode_fibers(fb)
+        return x, a, y, b
+    x, y = _mixture(4000, 1), _mixture(3500, 2)
+    return x, np.full(4000, 1 / 4000), y, np.full(3500, 1 / 3500)
+
+
+def _params(case):
+    from paper_2107_02010_b200.abi import make_params
+    if case == "hd":
+        return make_params(blur=0.05, reach=0.3)
+    if case == "hd_ms":
+        return make_params(blur=0.03, reach=0.3, multiscale=True, retruncate=1,
+                           switch_factor=1.0, clusters=10)
+    return make_params(**CASES[case])
+
+
+def _worker(rank, world, port, case, q):
+    import sys
+    import traceback
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import datetime
+        import torch
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=rank, world_size=world,
+                                timeout=datetime.timedelta(seconds=120))
+        from paper_2107_02010_b200.solver import Context
+
+        def ar(a):
+            dist.all_reduce(torch.from_numpy(a))
+
+        def bc(a, root):
+            dist.broadcast(torch.from_numpy(a), src=root)
+
+        ctx = Context(0, rank, world, host_collectives=(ar, bc))
+        x, a, y, b = _inputs(case)
+        loss, pots, st = ctx.sinkhorn(_params(case), x, a, y, b)
+        ctx.close()
+        q.put((rank, "ok", (loss, [pots.a_xx, pots.b_yy, pots.a_xy, pots.b_yx], st["world"])))
+        dist.destroy_process_group()
+    except BaseException:
+        q.put((rank, "error", traceback.format_exc()))
+
+
+def run_two_ranks(case, timeout=300):
+    """Rank results {rank: (loss, potentials, world)}; raises with the worker
+    traceback on failure and never leaves a worker behind."""
+    import queue
+    import torch.multiprocessing as mp
+    mpc = mp.get_context("spawn")
+    q = mpc.Queue()
+    port = _free_port()
+    procs = [mpc.Process(target=_worker, args=(r, 2, port, case, q), daemon=True)
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    out = {}
+    try:
+        while len(out) < 2:
+            rank, status, payload = q.get(timeout=timeout)
+            if status != "ok":
+                raise AssertionError(f"rank {rank} failed:\n{payload}")
+            out[rank] = payload
+    except queue.Empty:
+        raise AssertionError(f"two-rank {case} solve timed out after {timeout}s")
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    return out
+
+
+@pytest.mark.parametrize("case", ["dense", "multiscale", "unbalanced", "hd", "hd_ms"])
+def test_two_ranks_match_one(ctx, case):
+    x, a, y, b = _inputs(case)
+    l1, p1, _ = ctx.sinkhorn(_params(case), x, a, y, b)
+    out = run_two_ranks(case)
+    ref = [p1.a_xx, p1.b_yy, p1.a_xy, p1.b_yx]
+    eps = _params(case).blur ** 2
+    for rank in (0, 1):
+        l2, p2, world = out[rank]
+        assert world == 2
+        for u, v in zip(p2, ref):
+            if case == "dense":
+                np.testing.assert_array_equal(u, v)
+            else:
+                # float32 column sums added in another order (per-rank
+                # partials), compounded over the eps schedule; masks follow
+                assert np.abs(u - v).max() <= 1e-3 * eps
+        assert abs(l2 - l1) <= 1e-6 * abs(l1) + 1e-12
+
+
+if __name__ == "__main__":
+    import sys
+    for case in sys.argv[1:]:
+        res = run_two_ranks(case)
+        print(case, {r: v[0] for r, v in res.items()}, flush=True)

@@ -199,6 +199,17 @@ int msot_kmeans(msot_ctx* ctx, const double* x, const double* w, int64_t n, int 
                 uint64_t seed, int32_t* perm, int32_t* offsets, int32_t* labels,
                 double* centroids, double* cweights, float* radii, int* iters);
 
+/* Exact optimal transport (module exact_oracle; the
+ * reference names exact_ot(a, b, spec) -> DensePlan without a header):
+ * min sum pi_ij C_ij over pi >= 0 with row sums a and column sums b, C the
+ * (1/p)|x - y|^p cost of the n x d and m x d row-major points.  Host-only,
+ * single-threaded network simplex (a test / `msot verify` ground truth, not
+ * the GPU path; no context).  Requires sum a = sum b within 1e-9 and
+ * n * m <= 1e6 (MSOT_EDATA otherwise).  plan (nullable): n x m row-major
+ * optimal vertex; value: sum pi_ij C_ij in fixed pairwise order. */
+int msot_exact_ot(const double* x, const double* a, int64_t n, const double* y, const double* b,
+                  int64_t m, int d, double p, double* plan, double* value);
+
 /* Truncation mask: keep (I,J) iff
  *   min(B_a, B_b) >= -theta * eps,  D = X_I - Y_J,
  *   B_a = F_I + G_J - (1/2) max(0, |D| - (r_I + r_J))^2

@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "../../include/msot/barycenter.hpp"
+#include "../../include/msot/exact.hpp"
 #include "../../include/msot/labels.hpp"
 #include "../../include/msot/measure.hpp"
 #include "../../include/msot/sinkhorn.hpp"
@@ -415,9 +416,35 @@ int cmd_verify(const Args&) {
                                     msot::DiscreteMeasure({2.0}, {1.0}, 1), p);
   const msot::DiscreteMeasure c({0.1, 0.5, 0.9, 0.3}, {0.25, 0.25, 0.25, 0.25}, 1);
   const double z = msot::divergence(c, c, p);
-  const bool ok = std::fabs(v - 2.0) < 2e-2 && std::fabs(z) < 1e-9;
+  bool ok = std::fabs(v - 2.0) < 2e-2 && std::fabs(z) < 1e-9;
   std::cout << "delta_0 vs delta_2: " << v << " (expect 2), S(a, a): " << z << " -> "
             << (ok ? "ok" : "FAILED") << "\n";
+  // regularized vs exact (acceptance criterion 1): random
+  // balanced 32-atom pairs in [0,1]^2, blur = 1e-3 d
+  std::mt19937_64 rng(587);
+  std::uniform_real_distribution<double> U(0.0, 1.0);
+  double worst = 0.0;
+  for (int t = 0; t < 5; ++t) {
+    std::vector<double> x(64), y(64), a(32), b(32);
+    for (auto& e : x) e = U(rng);
+    for (auto& e : y) e = U(rng);
+    double sa = 0.0, sb = 0.0;
+    for (auto& e : a) sa += (e = U(rng) + 0.1);
+    for (auto& e : b) sb += (e = U(rng) + 0.1);
+    for (auto& e : a) e /= sa;
+    for (auto& e : b) e /= sb;
+    const msot::DiscreteMeasure A(x, a, 2), B(y, b, 2);
+    msot::SolverParams q;
+    q.blur = 1e-3 * msot::diameter_estimate(A, B, 0.0);
+    q.scaling = 0.995;  // the default 0.9 schedule is ~8% off at this blur (tests/test_exact.py)
+    const double s = msot::divergence(A, B, q);
+    const double e = msot::exact_ot(A, B).value;
+    worst = std::max(worst, std::fabs(s - e) / e);
+  }
+  const bool ok2 = worst <= 1e-2;
+  std::cout << "divergence vs exact_ot (5 pairs, N=M=32, blur=1e-3 d, q=0.995): worst rel. error " << worst
+            << " -> " << (ok2 ? "ok" : "FAILED") << "\n";
+  ok = ok && ok2;
   return ok ? 0 : 4;
 }
 

@@ -14,6 +14,7 @@
 #include "../../include/msot/sinkhorn.hpp"
 #include "../../include/msot/labels.hpp"
 #include "../../include/msot/barycenter.hpp"
+#include "../../include/msot/exact.hpp"
 
 namespace msot {
 
@@ -431,6 +432,22 @@ BarycenterResult barycenter(const std::vector<DiscreteMeasure>& targets,
                   "barycenter");
   traj.resize(done + 1);
   return {init.with_points(std::move(x)), std::move(traj)};
+}
+
+// -------------------------------------------------------------- exact oracle
+DensePlan exact_ot(const DiscreteMeasure& a, const DiscreteMeasure& b, const CostSpec& spec) {
+  spec.validate();
+  if (a.dim() != b.dim()) throw DataError("exact_ot: dimension mismatch");
+  DensePlan out;
+  out.rows = a.size();
+  out.cols = b.size();
+  out.pi.assign(out.rows * out.cols, 0.0);
+  throw_on_status(msot_exact_ot(a.points().data(), a.weights().data(),
+                                static_cast<int64_t>(a.size()), b.points().data(),
+                                b.weights().data(), static_cast<int64_t>(b.size()),
+                                static_cast<int>(a.dim()), spec.p, out.pi.data(), &out.value),
+                  "exact_ot");
+  return out;
 }
 
 }  // namespace msot

@@ -67,6 +67,16 @@ int guard(F&& f) {
 
 }  // namespace
 
+// Shared with the host-only entry points of other translation units
+// (exact_ot.cpp) so that msot_last_error() reports their failures too.
+namespace msot_host {
+void set_last_error(const std::string& m) { g_err = m; }
+}  // namespace msot_host
+
+namespace {
+
+}  // namespace
+
 struct msot_ctx {
   int device = 0, rank = 0, world = 1, n_sm = 148;
   cudaStream_t st = nullptr;

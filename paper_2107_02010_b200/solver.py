@@ -83,6 +83,8 @@ def lib():
                                   _ip, _ip, _ip, _dp, _dp, _fp, C.POINTER(C.c_int)]
         L.msot_plan_apply.argtypes = [C.c_void_p, _dp, _dp, C.c_int64, _dp, _dp, C.c_int64,
                                       C.c_int, _dp, _dp, C.c_double, _dp, _dp]
+        L.msot_exact_ot.argtypes = [_dp, _dp, C.c_int64, _dp, _dp, C.c_int64, C.c_int,
+                                    C.c_double, _dp, _dp]
         _LIB = L
     return _LIB
 
@@ -93,7 +95,7 @@ EXPORTS = ["msot_last_error", "msot_params_default", "msot_create", "msot_nccl_u
            "msot_shard_tiles", "msot_softmin", "msot_grid_cluster", "msot_truncation_mask",
            "msot_sinkhorn", "msot_sinkhorn_device", "msot_probe_ex2", "msot_sinkhorn_grad",
            "msot_barycenter", "msot_transfer_labels", "msot_resolve_flips", "msot_classify",
-           "msot_plan_apply", "msot_kmeans", "msot_create_dist_host"]
+           "msot_plan_apply", "msot_kmeans", "msot_create_dist_host", "msot_exact_ot"]
 
 
 def _check(rc):
@@ -125,6 +127,27 @@ def shard_tiles(work, world):
     b = np.zeros(world + 1, np.int64)
     _check(lib().msot_shard_tiles(_d(w), w.size, world, b.ctypes.data_as(_lp)))
     return b
+
+
+def exact_ot(x, a, y, b, p=2.0, plan=True):
+    """exact_ot(a, b, spec) -> DensePlan: the exact
+    transport value and (optionally) an optimal N x M plan, by the host network
+    simplex of csrc/exact_ot.cpp.  Returns (value, plan or None)."""
+    x, a, y, b = _c64(x), _c64(a), _c64(y), _c64(b)
+    if x.ndim == 1:
+        x = x[:, None]
+    if y.ndim == 1:
+        y = y[:, None]
+    n, d = x.shape
+    m = y.shape[0]
+    if y.shape[1] != d or a.size != n or b.size != m:
+        from .abi import DataError
+        raise DataError("exact_ot: dimension mismatch")
+    out = np.zeros((n, m)) if plan else None
+    v = C.c_double()
+    _check(lib().msot_exact_ot(_d(x), _d(a), n, _d(y), _d(b), m, d, float(p),
+                               _d(out) if plan else None, C.byref(v)))
+    return v.value, out
 
 
 @dataclass

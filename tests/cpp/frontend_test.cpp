@@ -1,12 +1,15 @@
 // C++ caller of the msot:: API (include/msot/*.hpp), as a user of the
 // reference's C++ interface would write it.  Mode "cpu": host-side measure
 // constructors and schedule (SPEC.md examples); mode "gpu": solves.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "msot/barycenter.hpp"
+#include "msot/exact.hpp"
 #include "msot/labels.hpp"
 #include "msot/measure.hpp"
 #include "msot/sinkhorn.hpp"
@@ -40,6 +43,25 @@ static void cpu_checks() {
   const double b0[2] = {0, 0}, b1[2] = {3, 4};
   CHECK(cost(b0, b1, CostSpec{1.0}) == 5.0);
   CHECK(throws<DataError>([] { CostSpec{2.5}.validate(); }));
+  // exact_ot: unit Diracs -> C(x, y), plan [[1]]; 4x4 uniform
+  // -> the best of the 24 permutation matchings; unbalanced -> DataError
+  {
+    DensePlan d1 = exact_ot(DiscreteMeasure({0.0, 1.0}, {1.0}, 2), DiscreteMeasure({2.0, 1.0}, {1.0}, 2));
+    CHECK(d1.value == 2.0 && d1(0, 0) == 1.0);
+    const std::vector<double> px = {0.1, 0.9, 0.4, 0.2, 0.8, 0.5, 0.3, 0.7};
+    const std::vector<double> py = {0.6, 0.1, 0.2, 0.3, 0.9, 0.8, 0.5, 0.5};
+    const std::vector<double> w4(4, 0.25);
+    DiscreteMeasure X(px, w4, 2), Y(py, w4, 2);
+    int perm[4] = {0, 1, 2, 3};
+    double best = 1e300;
+    do {
+      double s = 0.0;
+      for (int i = 0; i < 4; ++i) s += 0.25 * cost(X.point(i), Y.point(perm[i]), CostSpec{});
+      best = std::min(best, s);
+    } while (std::next_permutation(perm, perm + 4));
+    CHECK(std::fabs(exact_ot(X, Y).value - best) < 1e-15);
+    CHECK(throws<DataError>([&] { exact_ot(X, DiscreteMeasure({0.0, 0.0}, {0.5}, 2)); }));
+  }
   // zero weights dropped, invariants
   DiscreteMeasure m({0, 0, 1, 1, 2, 2}, {0.5, 0.0, 0.5}, 2);
   CHECK(m.size() == 2 && m.total_mass() == 1.0 && m.point(1)[0] == 2.0);

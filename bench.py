@@ -143,6 +143,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=None, help="override N=M (dev only)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--host-collectives", action="store_true",
+                    help="dev only: every rank on cuda:0, exchanges through gloo via "
+                         "msot_create_dist_host (exercises the N>1 path on one GPU)")
     args = ap.parse_args()
 
     w = dict(WORKLOAD)
@@ -159,8 +162,20 @@ def main():
     import torch.distributed as dist
     from paper_2107_02010_b200.solver import Context
 
+    if args.host_collectives:
+        local = 0
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 and args.host_collectives:
+        dist.init_process_group("gloo")
+
+        def _ar(arr):
+            dist.all_reduce(torch.from_numpy(arr))
+
+        def _bc(arr, root):
+            dist.broadcast(torch.from_numpy(arr), src=root)
+
+        ctx = Context(0, rank, world, host_collectives=(_ar, _bc))
+    elif world > 1:
         dist.init_process_group("gloo")
         idbuf = [Context.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(idbuf, src=0)

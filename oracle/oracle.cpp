@@ -389,7 +389,7 @@ void hd_mask(int64_t kx, int64_t ky, int d, const double* cx, const float* rx, c
 int64_t tile_ranges(const int32_t* rl, const int32_t* ro, int64_t kx, int64_t n,
                     const int32_t* co, int64_t ky, const uint8_t* mask, Ranges& out) {
   out.tile_start.assign(kx + n / MSOT_TILE_ROWS + 2, 0);
-  const int64_t nt = msot_row_tiles(ro, kx, n, out.tile_start.data());
+  const int64_t nt = msot_row_tiles(ro, kx, n, MSOT_TILE_ROWS, out.tile_start.data());
   out.tile_start.resize(nt + 1);
   out.row_tile.resize(n);
   for (int64_t t = 0; t < nt; ++t)

@@ -93,6 +93,31 @@ __device__ __forceinline__ float ub_regs(float4 X, float rI, float F, float4 Y, 
   return v + 1e-5f * (1.f + fabsf(F) + fabsf(G) + 2.f * s + 2.f * rr * rr);
 }
 
+// Float32 LOWER bound of the float64 slack min(B_a, B_b) (same margin rule as
+// ub_regs: 1e-5 x the magnitudes of the terms, ~100x the float32 rounding of
+// the ~20 operations).  A pair with lb >= thr is kept exactly as the float64
+// test would keep it; only pairs with ub >= thr > lb need the float64 test.
+__device__ __forceinline__ float lb_regs(float4 X, float rI, float F, float4 GI, float4 Y, float rJ,
+                                         float G, float4 HJ, int d, bool g) {
+  const float dx = X.x - Y.x, dy = d > 1 ? X.y - Y.y : 0.f, dz = d > 2 ? X.z - Y.z : 0.f;
+  const float s = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+  const float rr = rI + rJ;
+  const float lb = fmaxf(sqrtf(s) - rr, 0.f);
+  float v = (F + G) - 0.5f * lb * lb;
+  float mag = 1.f + fabsf(F) + fabsf(G) + 2.f * s + 2.f * rr * rr;
+  if (g) {
+    const float a0 = GI.x - dx, a1 = GI.y - dy, a2 = GI.z - dz;
+    const float b0 = HJ.x + dx, b1 = HJ.y + dy, b2 = HJ.z + dz;
+    const float na = sqrtf(fmaf(a0, a0, fmaf(a1, a1, a2 * a2)));
+    const float nb = sqrtf(fmaf(b0, b0, fmaf(b1, b1, b2 * b2)));
+    const float marg = fmaf(rI, na, rJ * nb);
+    const float vb = ((GI.w + HJ.w) + marg) - 0.5f * s;
+    v = fminf(v, vb);
+    mag += fabsf(GI.w) + fabsf(HJ.w) + marg;
+  }
+  return v - 1e-5f * mag;
+}
+
 // Column blocks = the 32 clusters of one mask word (Morton-consecutive, so
 // spatially compact): centre C_W, radius R_W >= |Y_J - C_W| + r_J (rounded
 // up), G_W = max_J G_J.  Since |X_I - Y_J| - r_I - r_J >= |X_I - C_W| - R_W -
@@ -130,23 +155,25 @@ __global__ void block_bounds_kernel(const float4* cy, const float* ry, const flo
   }
 }
 
-// One CTA per row cluster I: every word of row I and the row's best pair
-// (max slack, ties -> lowest J).  Pass 1: a warp tests 32 words' blocks at a
-// time (one lane per word) against thr, writes 0 to the words that fail and
-// walks the others with one lane per column cluster (coalesced loads, one
-// ballot per word); the float64 slack is evaluated only where the float32
-// upper bound reaches min(thr, best so far).  If the row has a kept pair its
-// best is >= thr, so no skipped block can hold it.  Otherwise (rare) pass 2
-// revisits the skipped blocks whose bound reaches the best so far, for the
-// arg-max only (their bits are 0).
+// One CTA per row cluster I: every word of row I, and — only when the row
+// has no kept pair — its best pair (max slack, ties -> lowest J).  A row with
+// a kept pair needs no best pair: the best is then itself kept, so setting its
+// bit would change nothing (best[I] = -1).  Pass 1: a warp tests 32 words'
+// blocks at a time (one lane per word) against thr, writes 0 to the words that
+// fail and walks the others with one lane per column cluster (coalesced loads,
+// one ballot per word); per pair the float32 bounds decide (ub < thr: drop,
+// lb >= thr: keep) and the float64 slack only settles the pairs in between.
+// Words with kept bits are OR-ed into `colany` (nullable).  Pass 2 (rare: no
+// kept pair, so no diagonal either) scans every word for the exact arg-max,
+// evaluating the float64 slack where the float32 upper bound reaches the
+// lane's best so far.
 constexpr int kMaskThreads = 256;
 
 __global__ void __launch_bounds__(kMaskThreads)
 mask_rows_kernel(MaskIn m, const float4* blk, const float* blkg, double thr, int self,
-                 uint32_t* mask, int32_t* best) {
+                 uint32_t* mask, int32_t* best, uint32_t* colany) {
   __shared__ double sv[kMaskThreads / 32];
   __shared__ int32_t sj[kMaskThreads / 32];
-  __shared__ double s_best;
   const int32_t I = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -154,26 +181,8 @@ mask_rows_kernel(MaskIn m, const float4* blk, const float* blkg, double thr, int
   const float4 X = m.cx[I];
   const float rI = m.rx[I], F = m.fx[I];
   const float4 GI = g ? m.gx[I] : zero;
-  double bv = -INFINITY;
-  int32_t bj = 0x7fffffff;
   uint32_t* row = mask + static_cast<int64_t>(I) * m.words;
-  auto walk_word = [&](int32_t w, double lim_bits, bool write) {
-    const int32_t J = w * 32 + lane;
-    bool keep = false;
-    if (J < m.ky) {
-      const float4 Y = m.cy[J];
-      const float rJ = m.ry[J], G = m.gy[J];
-      const double u = static_cast<double>(ub_regs(X, rI, F, Y, rJ, G, m.d));
-      keep = self && I == J;  // diagonal of a self mask
-      if (u >= lim_bits || u >= bv) {
-        const double v = pair_slack(X, rI, F, GI, Y, rJ, G, g ? m.hy[J] : zero, m.d, g);
-        keep = keep || v >= thr;
-        if (v > bv || (v == bv && J < bj)) { bv = v; bj = J; }
-      }
-    }
-    const uint32_t bits = __ballot_sync(0xffffffffu, keep);
-    if (write && lane == 0) row[w] = bits;
-  };
+  bool any = false;
   // pass 1
   for (int32_t w0 = warp * 32; w0 < m.words; w0 += kMaskThreads) {
     const int32_t wl = w0 + lane;
@@ -188,38 +197,41 @@ mask_rows_kernel(MaskIn m, const float4* blk, const float* blkg, double thr, int
     while (todo) {
       const int32_t w = w0 + __ffs(todo) - 1;
       todo &= todo - 1;
-      walk_word(w, thr, true);
+      const int32_t J = w * 32 + lane;
+      bool keep = false;
+      if (J < m.ky) {
+        const float4 Y = m.cy[J];
+        const float rJ = m.ry[J], G = m.gy[J];
+        keep = self && I == J;  // diagonal of a self mask
+        if (static_cast<double>(ub_regs(X, rI, F, Y, rJ, G, m.d)) >= thr) {
+          const float4 HJ = g ? m.hy[J] : zero;
+          if (static_cast<double>(lb_regs(X, rI, F, GI, Y, rJ, G, HJ, m.d, g)) >= thr)
+            keep = true;
+          else
+            keep = keep || pair_slack(X, rI, F, GI, Y, rJ, G, HJ, m.d, g) >= thr;
+        }
+      }
+      const uint32_t bits = __ballot_sync(0xffffffffu, keep);
+      if (lane == 0) {
+        row[w] = bits;
+        if (bits && colany) atomicOr(colany + w, bits);
+      }
+      any = any || bits != 0u;
     }
   }
-  // the row's best so far
-  double b2 = bv;
-  for (int o = 16; o > 0; o >>= 1) b2 = fmax(b2, __shfl_xor_sync(0xffffffffu, b2, o));
-  if (lane == 0) sv[warp] = b2;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double b = sv[0];
-    for (int q = 1; q < kMaskThreads / 32; ++q) b = fmax(b, sv[q]);
-    s_best = b;
+  if (__syncthreads_or(any)) {
+    if (threadIdx.x == 0) best[I] = -1;
+    return;
   }
-  __syncthreads();
-  const double rb = s_best;
-  __syncthreads();
-  if (rb < thr) {
-    // pass 2: no kept pair — the arg-max may sit in a skipped block
-    for (int32_t w0 = warp * 32; w0 < m.words; w0 += kMaskThreads) {
-      const int32_t wl = w0 + lane;
-      bool need = false;
-      if (wl < m.words) {
-        const float4 B = blk[wl];
-        const double u = static_cast<double>(ub_regs(X, rI, F, B, B.w, blkg[wl], m.d));
-        need = u < thr && !(self && (I >> 5) == wl) && u >= rb;
-      }
-      uint32_t todo = __ballot_sync(0xffffffffu, need);
-      while (todo) {
-        const int32_t w = w0 + __ffs(todo) - 1;
-        todo &= todo - 1;
-        walk_word(w, thr, false);
-      }
+  // pass 2: no kept pair — exact arg-max over every column cluster
+  double bv = -INFINITY;
+  int32_t bj = 0x7fffffff;
+  for (int32_t J = threadIdx.x; J < m.ky; J += kMaskThreads) {
+    const float4 Y = m.cy[J];
+    const float rJ = m.ry[J], G = m.gy[J];
+    if (static_cast<double>(ub_regs(X, rI, F, Y, rJ, G, m.d)) >= bv) {
+      const double v = pair_slack(X, rI, F, GI, Y, rJ, G, g ? m.hy[J] : zero, m.d, g);
+      if (v > bv) { bv = v; bj = J; }  // J ascending per thread: ties keep the lowest
     }
   }
   for (int o = 16; o > 0; o >>= 1) {
@@ -233,6 +245,54 @@ mask_rows_kernel(MaskIn m, const float4* blk, const float* blkg, double thr, int
     for (int q = 1; q < kMaskThreads / 32; ++q)
       if (sv[q] > bv || (sv[q] == bv && sj[q] < bj)) { bv = sv[q]; bj = sj[q]; }
     best[I] = bj == 0x7fffffff ? -1 : bj;
+  }
+}
+
+// Column best pairs without the transposed mask: for every column cluster J
+// with no kept pair (colany bit clear) the exact arg-max over the row clusters
+// (ties -> lowest I); -1 for the others.  One CTA per mask word of columns.
+__global__ void __launch_bounds__(kMaskThreads)
+mask_colbest_kernel(MaskIn m, const uint32_t* colany, int32_t* best) {
+  __shared__ double sv[kMaskThreads / 32];
+  __shared__ int32_t sj[kMaskThreads / 32];
+  const int32_t w = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  const bool g = m.gx != nullptr;
+  const uint32_t have = colany[w];
+  for (int b = 0; b < 32; ++b) {
+    const int32_t J = w * 32 + b;
+    if (J >= m.ky) break;
+    if (have >> b & 1u) {
+      if (threadIdx.x == 0) best[J] = -1;
+      continue;
+    }
+    const float4 Y = m.cy[J];
+    const float rJ = m.ry[J], G = m.gy[J];
+    const float4 HJ = g ? m.hy[J] : zero;
+    double bv = -INFINITY;
+    int32_t bi = 0x7fffffff;
+    for (int32_t I = threadIdx.x; I < m.kx; I += kMaskThreads) {
+      const float4 X = m.cx[I];
+      const float rI = m.rx[I], F = m.fx[I];
+      if (static_cast<double>(ub_regs(X, rI, F, Y, rJ, G, m.d)) >= bv) {
+        const double v = pair_slack(X, rI, F, g ? m.gx[I] : zero, Y, rJ, G, HJ, m.d, g);
+        if (v > bv) { bv = v; bi = I; }
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int32_t i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (v2 > bv || (v2 == bv && i2 < bi)) { bv = v2; bi = i2; }
+    }
+    if (lane == 0) { sv[warp] = bv; sj[warp] = bi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int q = 1; q < kMaskThreads / 32; ++q)
+        if (sv[q] > bv || (sv[q] == bv && sj[q] < bi)) { bv = sv[q]; bi = sj[q]; }
+      best[J] = bi == 0x7fffffff ? -1 : bi;
+    }
+    __syncthreads();
   }
 }
 
@@ -267,21 +327,37 @@ cudaError_t truncation_masks(int32_t kx, int32_t ky, int d, const float4* cx, co
   if (self && kx != ky) return cudaErrorInvalidValue;
   const double thr = -(theta * eps);
   const MaskIn m{kx, ky, d, mask_words(ky), cx, cy, rx, ry, fx, gy, gx, hy};
-  // layout of blkws: float4 blocks of y, float4 blocks of x, then the float maxima
+  // layout of blkws: float4 blocks of y, float4 blocks of x, the float maxima,
+  // then the column-any words
   float4* blk_y = reinterpret_cast<float4*>(blkws);
   float4* blk_x = blk_y + mask_words(ky);
   float* blkg_y = reinterpret_cast<float*>(blk_x + mask_words(kx));
   float* blkg_x = blkg_y + mask_words(ky);
+  uint32_t* colany = reinterpret_cast<uint32_t*>(blkg_x + mask_words(kx));
+  const bool col_pass = !self && maskT == nullptr;  // column bests without the transpose
+  if (col_pass) {
+    const cudaError_t e = cudaMemsetAsync(colany, 0, sizeof(uint32_t) * mask_words(ky), st);
+    if (e != cudaSuccess) return e;
+  }
   ++g_launches;
   block_bounds_kernel<<<static_cast<unsigned>((mask_words(ky) * 32 + 255) / 256), 256, 0, st>>>(
       cy, ry, gy, ky, d, blk_y, blkg_y);
   ++g_launches;
-  mask_rows_kernel<<<static_cast<unsigned>(kx), kMaskThreads, 0, st>>>(m, blk_y, blkg_y, thr, self,
-                                                                         mask, best_r);
+  mask_rows_kernel<<<static_cast<unsigned>(kx), kMaskThreads, 0, st>>>(
+      m, blk_y, blkg_y, thr, self, mask, best_r, col_pass ? colany : nullptr);
   if (self) {
     ++g_launches;
     mask_best_kernel<<<static_cast<unsigned>((kx + 255) / 256), 256, 0, st>>>(
         best_r, kx, best_r, 0, mask, m.words, mask, m.words);
+    return cudaGetLastError();
+  }
+  if (col_pass) {
+    ++g_launches;
+    mask_colbest_kernel<<<static_cast<unsigned>(mask_words(ky)), kMaskThreads, 0, st>>>(m, colany,
+                                                                                      best_c);
+    ++g_launches;
+    mask_best_kernel<<<static_cast<unsigned>((static_cast<int64_t>(kx) + ky + 255) / 256), 256, 0,
+                       st>>>(best_r, kx, best_c, ky, mask, m.words, nullptr, 0);
     return cudaGetLastError();
   }
   // the transposed problem: same formula with the roles swapped (pair_slack
@@ -292,7 +368,7 @@ cudaError_t truncation_masks(int32_t kx, int32_t ky, int d, const float4* cx, co
       cx, rx, fx, kx, d, blk_x, blkg_x);
   ++g_launches;
   mask_rows_kernel<<<static_cast<unsigned>(ky), kMaskThreads, 0, st>>>(t, blk_x, blkg_x, thr, 0,
-                                                                         maskT, best_c);
+                                                                         maskT, best_c, nullptr);
   ++g_launches;
   mask_best_kernel<<<static_cast<unsigned>((static_cast<int64_t>(kx) + ky + 255) / 256), 256, 0, st>>>(
       best_r, kx, best_c, ky, mask, m.words, maskT, t.words);

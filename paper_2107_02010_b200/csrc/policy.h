@@ -189,9 +189,8 @@ static inline int64_t msot_pack_tiles(const int32_t* offsets, int64_t k, int64_t
  * cluster-aligned packing above stays available for coarse voxels. */
 #define MSOT_CLUSTER_ALIGNED_TILES 0
 static inline int64_t msot_row_tiles(const int32_t* offsets, int64_t k, int64_t n,
-                                     int64_t* tile_start) {
-  return msot_pack_tiles(MSOT_CLUSTER_ALIGNED_TILES ? offsets : 0, k, n, MSOT_TILE_ROWS,
-                         tile_start);
+                                     int64_t tile_rows, int64_t* tile_start) {
+  return msot_pack_tiles(MSOT_CLUSTER_ALIGNED_TILES ? offsets : 0, k, n, tile_rows, tile_start);
 }
 
 /* First fine scale: the first t with sigma_t < factor * r_max;

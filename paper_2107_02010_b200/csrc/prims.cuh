@@ -163,7 +163,8 @@ cudaError_t truncation_masks(int32_t kx, int32_t ky, int d, const float4* cx, co
                              uint32_t* mask, uint32_t* maskT, int32_t* best_r, int32_t* best_c,
                              void* blkws, cudaStream_t st);
 inline size_t mask_block_ws_bytes(int32_t kx, int32_t ky) {
-  return static_cast<size_t>(mask_words(kx) + mask_words(ky)) * (sizeof(float4) + sizeof(float));
+  return static_cast<size_t>(mask_words(kx) + mask_words(ky)) * (sizeof(float4) + sizeof(float)) +
+         static_cast<size_t>(mask_words(ky)) * sizeof(uint32_t);
 }
 cudaError_t mask_pair_count(const uint32_t* mask, int32_t kx, int32_t ky, const int32_t* ro,
                             const int32_t* co, double* out, cudaStream_t st);

@@ -277,6 +277,7 @@ int64_t count_cells(msot_ctx* c, const double* d_x, int64_t n, const GridSpec& g
 
 // ------------------------------------------------------------------ ranges
 struct RangeSet {
+  int tile_rows = kTileRows;            // rows per tile
   int64_t n_tiles = 0, n_ranges = 0;
   int32_t* tile_start = nullptr;        // device, n_tiles+1
   std::vector<int32_t> tile_start_h;
@@ -291,8 +292,8 @@ struct RangeSet {
 void make_tiles(msot_ctx* c, const std::string& tag, int64_t rows,
                 const std::vector<int32_t>* offsets, RangeSet& R) {
   const int64_t k = offsets ? static_cast<int64_t>(offsets->size()) - 1 : 0;
-  std::vector<int64_t> ts(k + rows / kTileRows + 2);
-  R.n_tiles = msot_row_tiles(offsets ? offsets->data() : nullptr, k, rows, ts.data());
+  std::vector<int64_t> ts(k + rows / R.tile_rows + 2);
+  R.n_tiles = msot_row_tiles(offsets ? offsets->data() : nullptr, k, rows, R.tile_rows, ts.data());
   R.tile_start_h.assign(ts.begin(), ts.begin() + R.n_tiles + 1);
   R.tile_start = c->buf<int32_t>(tag + ".tstart", R.n_tiles + 1);
   CK(cudaMemcpyAsync(R.tile_start, R.tile_start_h.data(), (R.n_tiles + 1) * sizeof(int32_t),
@@ -1604,14 +1605,17 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
       // cross pair: (F, G) = (max b_yx, max a_xy); the slack is symmetric, so
       // the yx mask (rows y) is the exact transpose of the xy mask (rows x)
       CK(truncation_masks(X.k, Y.k, d, X.cpts, X.radii, fmax[3], g[3], Y.cpts, Y.radii, fmax[2],
-                          g[2], e, theta, 0, mxy, myx, bxr, byr, bws, st));
+                          g[2], e, theta, 0, mxy, once ? nullptr : myx, bxr, byr, bws, st));
       if (c->profiling) {  // cluster-granularity pair count of the four masks
         double* cnt = c->buf<double>("m.cnt", 1);
         CK(cudaMemsetAsync(cnt, 0, sizeof(double), st));
         CK(mask_pair_count(mxx, X.k, X.k, X.offsets, X.offsets, cnt, st));
         CK(mask_pair_count(myy, Y.k, Y.k, Y.offsets, Y.offsets, cnt, st));
         CK(mask_pair_count(mxy, X.k, Y.k, X.offsets, Y.offsets, cnt, st));
-        CK(mask_pair_count(myx, Y.k, X.k, Y.offsets, X.offsets, cnt, st));
+        if (once)  // myx is not built: the transpose has the same count
+          CK(mask_pair_count(mxy, X.k, Y.k, X.offsets, Y.offsets, cnt, st));
+        else
+          CK(mask_pair_count(myx, Y.k, X.k, Y.offsets, X.offsets, cnt, st));
         double h = 0.0;
         CK(cudaMemcpyAsync(&h, cnt, sizeof(double), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
@@ -2425,7 +2429,6 @@ int msot_truncation_mask(msot_ctx* c, int64_t kx, int64_t ky, int d, const float
     float* dry = c->buf<float>("tm.ry", ky);
     float* dgy = c->buf<float>("tm.gy", ky);
     uint32_t* dbits = c->buf<uint32_t>("tm.bits", kx * mask_words(static_cast<int32_t>(ky)));
-    uint32_t* dbitsT = c->buf<uint32_t>("tm.bitsT", ky * mask_words(static_cast<int32_t>(kx)));
     int32_t* dbr = c->buf<int32_t>("tm.br", kx);
     int32_t* dbc = c->buf<int32_t>("tm.bc", ky);
     uint8_t* dm = c->buf<uint8_t>("tm.m", kx * ky);
@@ -2446,7 +2449,7 @@ int msot_truncation_mask(msot_ctx* c, int64_t kx, int64_t ky, int d, const float
     void* bws = c->buf<char>("tm.blk", mask_block_ws_bytes(static_cast<int32_t>(kx),
                                                           static_cast<int32_t>(ky)));
     CK(truncation_masks(static_cast<int32_t>(kx), static_cast<int32_t>(ky), d, dcx, drx, dfx, dgx,
-                        dcy, dry, dgy, dhy, eps, theta, self, dbits, dbitsT, dbr, dbc, bws, st));
+                        dcy, dry, dgy, dhy, eps, theta, self, dbits, nullptr, dbr, dbc, bws, st));
     CK(unpack_mask(dbits, static_cast<int32_t>(kx), static_cast<int32_t>(ky), dm, st));
     CK(cudaMemcpyAsync(mask_out, dm, kx * ky, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));

@@ -517,11 +517,29 @@ __global__ void hd_colsum_kernel(const float* colpart, const int64_t* tslot, con
                                  int32_t t0, int32_t t1, int self, int32_t n_cols, float* tot) {
   const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n_cols) return;
-  double s = 0.0;
-  for (int32_t t = t0; t < t1; ++t) {
-    if (self && ts[t + 1] > j) break;
-    s += static_cast<double>(colpart[tslot[t] + (j - (self ? ts[t] : 0))]);
+  int32_t te = t1;  // self: tiles that end at or before j (ts ascending)
+  if (self) {
+    int32_t lo = t0, hi = t1;  // first t in [t0, t1) with ts[t + 1] > j
+    while (lo < hi) {
+      const int32_t mid = (lo + hi) >> 1;
+      if (ts[mid + 1] > j) hi = mid; else lo = mid + 1;
+    }
+    te = lo;
   }
+  // 4 independent loads per step, added in tile order (bitwise the plain loop)
+  auto term = [&](int32_t t) {
+    return __ldg(colpart + tslot[t] + (j - (self ? ts[t] : 0)));
+  };
+  double s = 0.0;
+  int32_t t = t0;
+  for (; t + 4 <= te; t += 4) {
+    const float v0 = term(t), v1 = term(t + 1), v2 = term(t + 2), v3 = term(t + 3);
+    s += static_cast<double>(v0);
+    s += static_cast<double>(v1);
+    s += static_cast<double>(v2);
+    s += static_cast<double>(v3);
+  }
+  for (; t < te; ++t) s += static_cast<double>(term(t));
   tot[j] = static_cast<float>(s);
 }
 

@@ -99,6 +99,9 @@ typedef struct msot_stats {
                                row-wise CPU solver evaluates for the same solve)  */
   double  pairs_mask_terms; /* profiling: fine-phase LSE terms at cluster granularity
                                (the masks without the 256-row tile union)          */
+  int32_t t_super;          /* voxel multiscale: first cluster-level scale after the
+                               super-voxel level (0: no super level)              */
+  int32_t k_super_x, k_super_y;  /* super clusters                                */
 } msot_stats;
 
 typedef struct msot_ctx msot_ctx;

@@ -948,10 +948,68 @@ int oracle_sinkhorn(const msot_params* prm, const double* x, const double* a, in
     const int tsw = msot_switch_index(sig.data(), ns, rmax, prm->switch_factor);
     S.t_switch = tsw;
 
-    // Coarse phase on the centroid measures.
+    // Coarse phase on the centroid measures, preceded by the super level
+    // (policy.h:msot_super_switch): consecutive clusters sharing a super-voxel
+    // key, run for t < t2, their duals inherited by the clusters.
     Duals cu{Vec(cx.k, 0.0), Vec(cy.k, 0.0), Vec(cy.k, 0.0), Vec(cx.k, 0.0)};
+    const int t2 = tsw > 0 ? msot_super_switch(sig.data(), tsw, cell, d) : 0;
+    if (t2 > 0) {
+      auto super = [&](const Clusters& cc, const Measure& Mc, const double* pts,
+                       std::vector<int32_t>& lab) {
+        Measure S2;
+        lab.assign(cc.k, 0);
+        std::vector<int32_t> off;
+        uint32_t prev = 0;
+        for (int32_t I = 0; I < cc.k; ++I) {
+          const int64_t i = cc.perm[cc.offsets[I]];
+          const uint32_t key = msot_cube_key(pts + i * d, d, lo.data(), cell) >> (d * MSOT_SUPER_SHIFT);
+          if (I == 0 || key != prev) off.push_back(I);
+          prev = key;
+          lab[I] = static_cast<int32_t>(off.size()) - 1;
+        }
+        S2.n = static_cast<int64_t>(off.size());
+        off.push_back(cc.k);
+        S2.pts.assign(S2.n * d, 0.0);
+        S2.w.assign(S2.n, 0.0);
+        S2.logw.assign(S2.n, 0.0);
+        for (int64_t J = 0; J < S2.n; ++J) {
+          double W = 0.0;
+          std::vector<double> acc(d, 0.0);
+          for (int32_t I = off[J]; I < off[J + 1]; ++I) {
+            W += Mc.w[I];
+            for (int k = 0; k < d; ++k) acc[k] += Mc.w[I] * Mc.pts[int64_t(I) * d + k];
+          }
+          S2.w[J] = W;
+          S2.logw[J] = std::log(W);
+          for (int k = 0; k < d; ++k) S2.pts[J * d + k] = acc[k] / W;
+        }
+        return S2;
+      };
+      std::vector<int32_t> lx, ly;
+      const Measure X2 = super(cx, Xc, x, lx), Y2 = super(cy, Yc, y, ly);
+      S.t_super = t2;
+      S.k_super_x = static_cast<int32_t>(X2.n);
+      S.k_super_y = static_cast<int32_t>(Y2.n);
+      Duals su{Vec(X2.n, 0.0), Vec(Y2.n, 0.0), Vec(Y2.n, 0.0), Vec(X2.n, 0.0)};
+      const double sfull = double(X2.n) * X2.n + double(Y2.n) * Y2.n + 2.0 * double(X2.n) * Y2.n;
+      for (int t = 0; t < t2; ++t) {
+        const double pr = sym_update(X2, Y2, d, su, eps[t], lam[t], p, false, nullptr, nullptr,
+                                     nullptr, nullptr);
+        if (pr < 0) return fail(MSOT_ENUMERIC, "non-finite potential at scale " + std::to_string(t));
+        S.pairs_evaluated += pr;
+        S.pairs_dense += sfull;
+      }
+      for (int32_t I = 0; I < cx.k; ++I) {
+        cu.a_xx[I] = su.a_xx[lx[I]];
+        cu.b_yx[I] = su.b_yx[lx[I]];
+      }
+      for (int32_t I = 0; I < cy.k; ++I) {
+        cu.b_yy[I] = su.b_yy[ly[I]];
+        cu.a_xy[I] = su.a_xy[ly[I]];
+      }
+    }
     const double cfull = double(cx.k) * cx.k + double(cy.k) * cy.k + 2.0 * double(cx.k) * cy.k;
-    for (int t = 0; t < tsw; ++t) {
+    for (int t = t2; t < tsw; ++t) {
       const double pr = sym_update(Xc, Yc, d, cu, eps[t], lam[t], p, false, nullptr, nullptr,
                                    nullptr, nullptr);
       if (pr < 0) return fail(MSOT_ENUMERIC, "non-finite potential at scale " + std::to_string(t));

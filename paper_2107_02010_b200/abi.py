@@ -66,6 +66,9 @@ class Stats(C.Structure):
         ("phase_ms", C.c_double * 8),
         ("pairs_terms", C.c_double),
         ("pairs_mask_terms", C.c_double),
+        ("t_super", C.c_int32),
+        ("k_super_x", C.c_int32),
+        ("k_super_y", C.c_int32),
     ]
 
     PHASES = ("setup", "coarse", "extrapolate", "masks", "updates", "loss", "labels")

@@ -251,6 +251,21 @@ cudaError_t cluster_bound(const float4* pts, const double* w64, const float* f,
 
 // coarse_duals_to_fine by inheritance: used as the
 // expansion reference of the extrapolation softmin.
+// Super-voxel key of every cluster: the key of its first sorted atom >> bits.
+__global__ void super_keys_kernel(const uint32_t* sorted_keys, const int32_t* offsets, int32_t k,
+                                  int bits, uint32_t* out) {
+  const int32_t I = blockIdx.x * blockDim.x + threadIdx.x;
+  if (I < k) out[I] = sorted_keys[offsets[I]] >> bits;
+}
+
+cudaError_t super_keys(const uint32_t* sorted_keys, const int32_t* offsets, int32_t k, int bits,
+                       uint32_t* out, cudaStream_t st) {
+  if (k <= 0) return cudaSuccess;
+  ++g_launches;
+  super_keys_kernel<<<(k + 255) / 256, 256, 0, st>>>(sorted_keys, offsets, k, bits, out);
+  return cudaGetLastError();
+}
+
 __global__ void inherit_kernel(const float* coarse, const int32_t* labels, int64_t n, float* fine) {
   const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (s < n) fine[s] = coarse[labels[s]];

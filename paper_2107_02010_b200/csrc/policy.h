@@ -201,6 +201,23 @@ static inline int msot_switch_index(const double* sigma, int n, double r_max, do
   return n;
 }
 
+/* Super level of the coarse phase (voxel path): super voxels of 2^MSOT_SUPER_SHIFT
+ * voxels per axis group consecutive clusters (Morton order: the super key is
+ * the voxel key >> d * MSOT_SUPER_SHIFT).  The super measure runs the scales
+ * with sigma_t >= MSOT_SUPER_SWITCH * (half-diagonal of a super voxel) and
+ * hands its duals to the clusters by inheritance, which
+ * continue to the fine switch.  Returns the first cluster-level scale t2 (0:
+ * no super level — it must take at least MSOT_SUPER_MIN_SCALES scales off the
+ * cluster level). */
+#define MSOT_SUPER_SHIFT 1
+#define MSOT_SUPER_SWITCH 2.0  /* C3: S within 8.6e-5 of dense (1.0: 7.3e-4; none: 9.0e-5) */
+#define MSOT_SUPER_MIN_SCALES 4
+static inline int msot_super_switch(const double* sigma, int tsw, double cell, int d) {
+  const double r = 0.5 * sqrt((double)d) * cell * (double)(1 << MSOT_SUPER_SHIFT);
+  const int t2 = msot_switch_index(sigma, tsw, r, MSOT_SUPER_SWITCH);
+  return (tsw - t2 >= MSOT_SUPER_MIN_SCALES) ? t2 : 0;
+}
+
 #ifdef __cplusplus
 }
 #endif

@@ -123,6 +123,8 @@ cudaError_t cluster_bound(const float4* pts, const double* w64, const float* f,
                           float4* grad, cudaStream_t st);
 cudaError_t inherit(const float* coarse, const int32_t* labels, int64_t n, float* fine,
                     cudaStream_t st);
+cudaError_t super_keys(const uint32_t* sorted_keys, const int32_t* offsets, int32_t k, int bits,
+                       uint32_t* out, cudaStream_t st);
 
 // K-means coarsening (kmeans.cu), float64, bit-identical to the oracle.
 // perm: atoms grouped by cluster (index order inside), off[K+1], labels per

@@ -254,6 +254,39 @@ void prepare_measure(msot_ctx* c, const std::string& tag, const double* d_x, con
   CK(cudaStreamSynchronize(st));
 }
 
+// Super level of the coarse phase (policy.h:msot_super_switch): consecutive
+// clusters sharing a super-voxel key, with centroids / weights / radii from
+// the cluster centroids weighted by the cluster masses.
+struct SuperMeasure {
+  int32_t k = 0;
+  int32_t* labels = nullptr;  // cluster -> super cluster
+  float4* cpts = nullptr;
+  float* clw2 = nullptr;
+};
+
+void super_measure(msot_ctx* c, const std::string& tag, const DMeasure& M, int d,
+                   SuperMeasure& S) {
+  cudaStream_t st = c->st;
+  const int32_t k = M.k;
+  uint32_t* keys = c->buf<uint32_t>(tag + ".skeys", k);
+  CK(super_keys(c->buf<uint32_t>(tag + ".keys", M.n), M.offsets, k, d * MSOT_SUPER_SHIFT, keys, st));
+  uint8_t* flags = c->buf<uint8_t>(tag + ".sflags", k);
+  S.labels = c->buf<int32_t>(tag + ".slabels", k);
+  int32_t* offs = c->buf<int32_t>(tag + ".soffsets", k + 1);
+  int32_t* stmp = c->buf<int32_t>(tag + ".sstmp", scan_temp_elems(k));
+  int32_t* kdev = c->buf<int32_t>(tag + ".sk", 1);
+  CK(segment_flags(keys, k, flags, st));
+  CK((scan<uint8_t, int32_t>(flags, S.labels, k, true, stmp, kdev, st)));
+  CK(segment_offsets(S.labels, flags, k, offs, st));
+  CK(cudaMemcpyAsync(&S.k, kdev, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  S.cpts = c->buf<float4>(tag + ".scpts", S.k);
+  S.clw2 = c->buf<float>(tag + ".sclw2", S.k);
+  double* cw = c->buf<double>(tag + ".scw64", S.k);
+  float* rad = c->buf<float>(tag + ".srad", S.k);
+  CK(cluster_stats(M.cpts, M.cw64, offs, S.k, d, S.cpts, S.clw2, cw, rad, st));
+}
+
 // Occupied voxels of one cloud for a candidate edge (automatic edge rule).
 int64_t count_cells(msot_ctx* c, const double* d_x, int64_t n, const GridSpec& g) {
   cudaStream_t st = c->st;
@@ -1463,47 +1496,74 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
     c->mark(1);  // phase 1: coarse phase on the centroid measures (dense)
     float* coarse_final[4] = {nullptr, nullptr, nullptr, nullptr};
     if (tsw > 0) {
+      // dense updates t in [t0, t1) of the measures (xp, xl, kx) and (yp, yl, ky)
+      auto coarse_run = [&](const std::string& tg, const float4* xp, const float* xl, int32_t kx,
+                            const float4* yp, const float* yl, int32_t ky, Potentials& Uq,
+                            int& qcur, int t0, int t1) {
+        RangeSet rxx, ryy, rxy, ryx;
+        SymSet cxx, cyy, cyx;
+        SymCols ccol{};
+        Plan Pc;
+        const bool conce = prm->pair_eval != 0;
+        if (conce) {  // evaluate-once on the centroid measures (dense pair sets)
+          dense_symset(c, tg + "s.xx", kx, kx, 1, cxx);
+          dense_symset(c, tg + "s.yy", ky, ky, 1, cyy);
+          dense_symset(c, tg + "s.yx", kx, ky, 0, cyx);
+          Pc.np = 3;
+          Pc.ps[0] = {xp, kx, xp, xl, kx, &cxx.R, {}, &cxx, xl};
+          Pc.ps[1] = {yp, ky, yp, yl, ky, &cyy.R, {}, &cyy, yl};
+          Pc.ps[2] = {xp, kx, yp, yl, ky, &cyx.R, {}, &cyx, xl};
+          ccol.tot[0] = c->buf<float>(tg + "s.totx", kx);
+          ccol.tot[1] = c->buf<float>(tg + "s.toty", ky);
+          ccol.tot[2] = c->buf<float>(tg + "s.totxy", ky);
+          ccol.yrows = yp;
+          ccol.xcols = xp;
+          ccol.x_lw2 = xl;
+          ccol.n = kx;
+          ccol.m = ky;
+          ccol.uniform = false;
+        } else {
+          dense_rangeset(c, tg + ".xx", kx, kx, rxx);
+          dense_rangeset(c, tg + ".yy", ky, ky, ryy);
+          dense_rangeset(c, tg + ".xy", ky, kx, rxy);
+          dense_rangeset(c, tg + ".yx", kx, ky, ryx);
+          sym_specs(Pc, xp, xl, kx, yp, yl, ky, &rxx, &ryy, &rxy, &ryx);
+        }
+        build_plan(c, "p" + tg, Pc);
+        const double cfull = double(kx) * kx + double(ky) * ky + 2.0 * double(kx) * ky;
+        for (int t = t0; t < t1; ++t) {
+          if (conce)
+            sym_step_once(c, Pc, Uq, qcur, eps[t], lam[t], false, ss, ccol);
+          else
+            sym_step(c, Pc, Uq, qcur, eps[t], lam[t], false, ss);
+          S->pairs_dense += cfull;
+        }
+      };
       Potentials Uc;
       alloc_pots(c, "cpot", X.k, Y.k, Uc);
       int ccur = 0;
-      RangeSet rxx, ryy, rxy, ryx;
-      SymSet cxx, cyy, cyx;
-      SymCols ccol{};
-      Plan Pc;
-      const bool conce = prm->pair_eval != 0;
-      if (conce) {  // evaluate-once on the centroid measures (dense pair sets)
-        dense_symset(c, "cs.xx", X.k, X.k, 1, cxx);
-        dense_symset(c, "cs.yy", Y.k, Y.k, 1, cyy);
-        dense_symset(c, "cs.yx", X.k, Y.k, 0, cyx);
-        Pc.np = 3;
-        Pc.ps[0] = {X.cpts, X.k, X.cpts, X.clw2, X.k, &cxx.R, {}, &cxx, X.clw2};
-        Pc.ps[1] = {Y.cpts, Y.k, Y.cpts, Y.clw2, Y.k, &cyy.R, {}, &cyy, Y.clw2};
-        Pc.ps[2] = {X.cpts, X.k, Y.cpts, Y.clw2, Y.k, &cyx.R, {}, &cyx, X.clw2};
-        ccol.tot[0] = c->buf<float>("cs.totx", X.k);
-        ccol.tot[1] = c->buf<float>("cs.toty", Y.k);
-        ccol.tot[2] = c->buf<float>("cs.totxy", Y.k);
-        ccol.yrows = Y.cpts;
-        ccol.xcols = X.cpts;
-        ccol.x_lw2 = X.clw2;
-        ccol.n = X.k;
-        ccol.m = Y.k;
-        ccol.uniform = false;
-      } else {
-        dense_rangeset(c, "c.xx", X.k, X.k, rxx);
-        dense_rangeset(c, "c.yy", Y.k, Y.k, ryy);
-        dense_rangeset(c, "c.xy", Y.k, X.k, rxy);
-        dense_rangeset(c, "c.yx", X.k, Y.k, ryx);
-        sym_specs(Pc, X.cpts, X.clw2, X.k, Y.cpts, Y.clw2, Y.k, &rxx, &ryy, &rxy, &ryx);
+      // super level (policy.h:msot_super_switch): the first t2 scales on
+      // super voxels, inherited by the clusters
+      const int t2 = msot_super_switch(sig.data(), tsw, cell, d);
+      if (t2 > 0) {
+        SuperMeasure SX, SY;
+        super_measure(c, "x", X, d, SX);
+        super_measure(c, "y", Y, d, SY);
+        S->t_super = t2;
+        S->k_super_x = SX.k;
+        S->k_super_y = SY.k;
+        Potentials U2;
+        alloc_pots(c, "spot", SX.k, SY.k, U2);
+        int scur = 0;
+        coarse_run("u", SX.cpts, SX.clw2, SX.k, SY.cpts, SY.clw2, SY.k, U2, scur, 0, t2);
+        float** so = U2.v[scur];
+        float** ci = Uc.v[ccur];
+        CK(inherit(so[0], SX.labels, X.k, ci[0], st));
+        CK(inherit(so[1], SY.labels, Y.k, ci[1], st));
+        CK(inherit(so[2], SY.labels, Y.k, ci[2], st));
+        CK(inherit(so[3], SX.labels, X.k, ci[3], st));
       }
-      build_plan(c, "pc", Pc);
-      const double cfull = double(X.k) * X.k + double(Y.k) * Y.k + 2.0 * double(X.k) * Y.k;
-      for (int t = 0; t < tsw; ++t) {
-        if (conce)
-          sym_step_once(c, Pc, Uc, ccur, eps[t], lam[t], false, ss, ccol);
-        else
-          sym_step(c, Pc, Uc, ccur, eps[t], lam[t], false, ss);
-        S->pairs_dense += cfull;
-      }
+      coarse_run("c", X.cpts, X.clw2, X.k, Y.cpts, Y.clw2, Y.k, Uc, ccur, t2, tsw);
       c->mark(2);  // phase 2: coarse -> fine transfer
       // inheritance (transfer_rule 0) writes the fine
       // potentials directly; extrapolation (transfer_rule 1) is one

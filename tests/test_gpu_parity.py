@@ -203,6 +203,9 @@ def test_multiscale_parity(ctx, oracle, retruncate, pair_eval):
                       pair_eval=pair_eval)
     lg, pg, sg, lo, po, so = run_both(ctx, oracle, prm, x, a, y, b)
     assert (sg["kx"], sg["ky"], sg["t_switch"]) == (so["kx"], so["ky"], so["t_switch"])
+    # the super-voxel level of the coarse phase (policy.h:msot_super_switch)
+    sup = ("t_super", "k_super_x", "k_super_y")
+    assert [sg[k] for k in sup] == [so[k] for k in sup] and 0 < sg["t_super"] < sg["t_switch"]
     assert sg["pairs_fine"] < sg["pairs_fine_dense"]
     check_pots(pg, po, 1e-4)
     assert abs(lg - lo) <= LOSS_TOL * abs(lo), (lg, lo)
@@ -221,6 +224,7 @@ def test_multiscale_unbalanced_parity(ctx, oracle, reach):
     prm = make_params(blur=0.01, reach=reach, multiscale=True, retruncate=1, cluster_scale=0.04)
     lg, pg, sg, lo, po, so = run_both(ctx, oracle, prm, x, a, y, b)
     assert sg["t_switch"] == so["t_switch"] and sg["t_switch"] < sg["n_scales"]
+    assert (sg["t_super"], sg["k_super_x"]) == (so["t_super"], so["k_super_x"])
     check_pots(pg, po, 1e-4)
     assert abs(lg - lo) <= LOSS_TOL * abs(lo), (lg, lo)
 

@@ -142,6 +142,10 @@ __global__ void bbox_kernel(const double* x, int64_t n, int d, long long* lohi) 
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
       const double v = x[i * d + k];
+      if (!isfinite(v)) {  // non-finite input: the box becomes [-inf, inf] (DataError)
+        lo = -INFINITY;
+        hi = INFINITY;
+      }
       lo = fmin(lo, v);
       hi = fmax(hi, v);
     }
@@ -171,6 +175,24 @@ cudaError_t bbox(const double* x, int64_t n, int d, long long* lohi_dev, bool in
     int blocks = static_cast<int>(nb0 < 592 ? nb0 : 592);
     ++g_launches; bbox_kernel<<<blocks, 256, 0, st>>>(x, n, d, lohi_dev);
   }
+  return cudaGetLastError();
+}
+
+// Weights that are not finite and > 0 (counted into *bad).
+__global__ void bad_weights_kernel(const double* w, int64_t n, int32_t* bad) {
+  int32_t c = 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    c += !(w[i] > 0.0 && isfinite(w[i]));
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(bad, c);
+}
+
+cudaError_t count_bad_weights(const double* w, int64_t n, int32_t* bad, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t nb0 = (n + 255) / 256;
+  ++g_launches;
+  bad_weights_kernel<<<static_cast<int>(nb0 < 592 ? nb0 : 592), 256, 0, st>>>(w, n, bad);
   return cudaGetLastError();
 }
 

@@ -18,6 +18,7 @@ cudaError_t scan(const TI* in, TO* out, int64_t n, bool inclusive, TO* tmp, TO* 
 cudaError_t bbox(const double* x, int64_t n, int d, long long* lohi_dev, bool init,
                  cudaStream_t st);
 void bbox_decode(const long long* lohi_host, int d, double* lo, double* hi);
+cudaError_t count_bad_weights(const double* w, int64_t n, int32_t* bad, cudaStream_t st);
 
 // stable LSD radix sort of (key, value) by the low `key_bits` bits
 size_t radix_temp_bytes(int64_t n);

@@ -1332,15 +1332,24 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
 
   // diameter_estimate -- exact min/max on the device
   long long* lohi = c->buf<long long>("bbox", 2 * d);
+  int32_t* badw = c->buf<int32_t>("badw", 1);
+  CK(cudaMemsetAsync(badw, 0, sizeof(int32_t), st));
   CK(bbox(d_x, n, d, lohi, true, st));
   CK(bbox(d_y, m, d, lohi, false, st));
+  CK(count_bad_weights(d_a, n, badw, st));
+  CK(count_bad_weights(d_b, m, badw, st));
   std::vector<long long> lh(2 * d);
+  int32_t nbad = 0;
   CK(cudaMemcpyAsync(lh.data(), lohi, 2 * d * sizeof(long long), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&nbad, badw, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  if (nbad) raise(MSOT_EDATA, "weights must be finite and > 0");
   std::vector<double> lov(std::max(d, 3), 0.0), hiv(std::max(d, 3), 0.0);
   double* lo = lov.data();
   double* hi = hiv.data();
   bbox_decode(lh.data(), d, lo, hi);
+  for (int k = 0; k < d; ++k)
+    if (!std::isfinite(lo[k]) || !std::isfinite(hi[k])) raise(MSOT_EDATA, "non-finite point");
   double diag2 = 0.0;
   for (int k = 0; k < d; ++k) diag2 += (hi[k] - lo[k]) * (hi[k] - lo[k]);
   const double diam = std::max(std::sqrt(diag2), prm->blur);

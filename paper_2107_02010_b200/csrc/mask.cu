@@ -171,10 +171,10 @@ constexpr int kMaskThreads = 256;
 
 __global__ void __launch_bounds__(kMaskThreads)
 mask_rows_kernel(MaskIn m, const float4* blk, const float* blkg, double thr, int self,
-                 uint32_t* mask, int32_t* best, uint32_t* colany) {
+                 uint32_t* mask, int32_t* best, uint32_t* colany, int32_t row0) {
   __shared__ double sv[kMaskThreads / 32];
   __shared__ int32_t sj[kMaskThreads / 32];
-  const int32_t I = blockIdx.x;
+  const int32_t I = row0 + static_cast<int32_t>(blockIdx.x);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
   const bool g = m.gx != nullptr;
@@ -299,15 +299,17 @@ mask_colbest_kernel(MaskIn m, const uint32_t* colany, int32_t* best) {
 // Best pairs into the masks: row I's best J (br) and column J's best I (bc)
 // set (I, J) in `mask` and (J, I) in `maskT` (nullable; == mask for a self
 // mask, whose best pairs are symmetric).
-__global__ void mask_best_kernel(const int32_t* br, int32_t kx, const int32_t* bc, int32_t ky,
-                                 uint32_t* mask, int32_t wx, uint32_t* maskT, int32_t wt) {
+__global__ void mask_best_kernel(const int32_t* br, int32_t r0, int32_t r1, const int32_t* bc,
+                                 int32_t ky, uint32_t* mask, int32_t wx, uint32_t* maskT,
+                                 int32_t wt) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nr = r1 - r0;
   int32_t I, J;
-  if (t < kx) {
-    I = static_cast<int32_t>(t);
+  if (t < nr) {
+    I = r0 + static_cast<int32_t>(t);
     J = br[I];
-  } else if (t < static_cast<int64_t>(kx) + ky) {
-    J = static_cast<int32_t>(t - kx);
+  } else if (t < nr + ky) {
+    J = static_cast<int32_t>(t - nr);
     I = bc[J];
   } else {
     return;
@@ -344,11 +346,11 @@ cudaError_t truncation_masks(int32_t kx, int32_t ky, int d, const float4* cx, co
       cy, ry, gy, ky, d, blk_y, blkg_y);
   ++g_launches;
   mask_rows_kernel<<<static_cast<unsigned>(kx), kMaskThreads, 0, st>>>(
-      m, blk_y, blkg_y, thr, self, mask, best_r, col_pass ? colany : nullptr);
+      m, blk_y, blkg_y, thr, self, mask, best_r, col_pass ? colany : nullptr, 0);
   if (self) {
     ++g_launches;
     mask_best_kernel<<<static_cast<unsigned>((kx + 255) / 256), 256, 0, st>>>(
-        best_r, kx, best_r, 0, mask, m.words, mask, m.words);
+        best_r, 0, kx, best_r, 0, mask, m.words, mask, m.words);
     return cudaGetLastError();
   }
   if (col_pass) {
@@ -357,7 +359,7 @@ cudaError_t truncation_masks(int32_t kx, int32_t ky, int d, const float4* cx, co
                                                                                       best_c);
     ++g_launches;
     mask_best_kernel<<<static_cast<unsigned>((static_cast<int64_t>(kx) + ky + 255) / 256), 256, 0,
-                       st>>>(best_r, kx, best_c, ky, mask, m.words, nullptr, 0);
+                       st>>>(best_r, 0, kx, best_c, ky, mask, m.words, nullptr, 0);
     return cudaGetLastError();
   }
   // the transposed problem: same formula with the roles swapped (pair_slack
@@ -368,16 +370,83 @@ cudaError_t truncation_masks(int32_t kx, int32_t ky, int d, const float4* cx, co
       cx, rx, fx, kx, d, blk_x, blkg_x);
   ++g_launches;
   mask_rows_kernel<<<static_cast<unsigned>(ky), kMaskThreads, 0, st>>>(t, blk_x, blkg_x, thr, 0,
-                                                                         maskT, best_c, nullptr);
+                                                                         maskT, best_c, nullptr, 0);
   ++g_launches;
   mask_best_kernel<<<static_cast<unsigned>((static_cast<int64_t>(kx) + ky + 255) / 256), 256, 0, st>>>(
-      best_r, kx, best_c, ky, mask, m.words, maskT, t.words);
+      best_r, 0, kx, best_c, ky, mask, m.words, maskT, t.words);
   return cudaGetLastError();
 }
 
 // Diagnostic (profiling only): sum over kept cluster pairs of n_I * m_J,
 // the pair count of the mask at cluster granularity (what the block-sparse
 // reduction would evaluate with no tile-level union).
+// Row-sharded truncation masks (multi-GPU fine phase): part 1 computes the
+// rows [r0, r1) of the mask and their best pairs (rows with no kept pair);
+// after the callers exchange the row blocks, part 2 (cross masks only) forms
+// each column's any-bit from the whole mask and sets the column best pairs
+// of the columns with none — every rank identically.  With [0, kx) and no
+// exchange this is bitwise truncation_masks(maskT = nullptr).
+// OR of the mask rows per word: blockIdx.y strides the rows, atomicOr merges
+// (order-free, so deterministic); colany must be zeroed first.
+__global__ void col_any_kernel(const uint32_t* mask, int32_t kx, int32_t words, uint32_t* colany) {
+  const int32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= words) return;
+  uint32_t a = 0u;
+  for (int32_t I = blockIdx.y; I < kx; I += gridDim.y) a |= mask[static_cast<int64_t>(I) * words + w];
+  if (a) atomicOr(colany + w, a);
+}
+
+cudaError_t truncation_masks_rows(int32_t kx, int32_t ky, int d, const float4* cx, const float* rx,
+                                  const float* fx, const float4* gx, const float4* cy,
+                                  const float* ry, const float* gy, const float4* hy, double eps,
+                                  double theta, int self, int32_t r0, int32_t r1, uint32_t* mask,
+                                  int32_t* best_r, void* blkws, cudaStream_t st) {
+  if (kx <= 0 || ky <= 0) return cudaSuccess;
+  if ((gx == nullptr) != (hy == nullptr)) return cudaErrorInvalidValue;
+  if (self && kx != ky) return cudaErrorInvalidValue;
+  const double thr = -(theta * eps);
+  const MaskIn m{kx, ky, d, mask_words(ky), cx, cy, rx, ry, fx, gy, gx, hy};
+  float4* blk_y = reinterpret_cast<float4*>(blkws);
+  float4* blk_x = blk_y + mask_words(ky);
+  float* blkg_y = reinterpret_cast<float*>(blk_x + mask_words(kx));
+  ++g_launches;
+  block_bounds_kernel<<<static_cast<unsigned>((mask_words(ky) * 32 + 255) / 256), 256, 0, st>>>(
+      cy, ry, gy, ky, d, blk_y, blkg_y);
+  if (r1 <= r0) return cudaGetLastError();
+  ++g_launches;
+  mask_rows_kernel<<<static_cast<unsigned>(r1 - r0), kMaskThreads, 0, st>>>(
+      m, blk_y, blkg_y, thr, self, mask, best_r, nullptr, r0);
+  ++g_launches;
+  mask_best_kernel<<<static_cast<unsigned>((r1 - r0 + 255) / 256), 256, 0, st>>>(
+      best_r, r0, r1, nullptr, 0, mask, m.words, nullptr, 0);
+  return cudaGetLastError();
+}
+
+cudaError_t truncation_masks_cols(int32_t kx, int32_t ky, int d, const float4* cx, const float* rx,
+                                  const float* fx, const float4* gx, const float4* cy,
+                                  const float* ry, const float* gy, const float4* hy, uint32_t* mask,
+                                  int32_t* best_c, void* blkws, cudaStream_t st) {
+  if (kx <= 0 || ky <= 0) return cudaSuccess;
+  const MaskIn m{kx, ky, d, mask_words(ky), cx, cy, rx, ry, fx, gy, gx, hy};
+  float4* blk_y = reinterpret_cast<float4*>(blkws);
+  float4* blk_x = blk_y + mask_words(ky);
+  float* blkg_y = reinterpret_cast<float*>(blk_x + mask_words(kx));
+  float* blkg_x = blkg_y + mask_words(ky);
+  uint32_t* colany = reinterpret_cast<uint32_t*>(blkg_x + mask_words(kx));
+  cudaError_t e = cudaMemsetAsync(colany, 0, sizeof(uint32_t) * m.words, st);
+  if (e != cudaSuccess) return e;
+  ++g_launches;
+  const unsigned ry_blocks = static_cast<unsigned>(kx < 256 ? kx : 256);
+  col_any_kernel<<<dim3(static_cast<unsigned>((m.words + 127) / 128), ry_blocks), 128, 0, st>>>(
+      mask, kx, m.words, colany);
+  ++g_launches;
+  mask_colbest_kernel<<<static_cast<unsigned>(m.words), kMaskThreads, 0, st>>>(m, colany, best_c);
+  ++g_launches;
+  mask_best_kernel<<<static_cast<unsigned>((ky + 255) / 256), 256, 0, st>>>(
+      nullptr, 0, 0, best_c, ky, mask, m.words, nullptr, 0);
+  return cudaGetLastError();
+}
+
 __global__ void mask_pair_count_kernel(const uint32_t* mask, int32_t kx, int32_t ky,
                                        const int32_t* ro, const int32_t* co, double* out) {
   const int32_t I = blockIdx.x;
@@ -475,7 +544,7 @@ cudaError_t truncation_masks_hd(int32_t kx, int32_t ky, int d, const double* cx,
   if (self) {
     ++g_launches;
     mask_best_kernel<<<static_cast<unsigned>((kx + 255) / 256), 256, 0, st>>>(
-        best_r, kx, best_r, 0, mask, mask_words(ky), mask, mask_words(ky));
+        best_r, 0, kx, best_r, 0, mask, mask_words(ky), mask, mask_words(ky));
     return cudaGetLastError();
   }
   ++g_launches;
@@ -483,7 +552,7 @@ cudaError_t truncation_masks_hd(int32_t kx, int32_t ky, int d, const double* cx,
                                                                    thr, 0, maskT, best_c);
   ++g_launches;
   mask_best_kernel<<<static_cast<unsigned>((static_cast<int64_t>(kx) + ky + 255) / 256), 256, 0, st>>>(
-      best_r, kx, best_c, ky, mask, mask_words(ky), maskT, mask_words(kx));
+      best_r, 0, kx, best_c, ky, mask, mask_words(ky), maskT, mask_words(kx));
   return cudaGetLastError();
 }
 

@@ -165,6 +165,15 @@ cudaError_t truncation_masks(int32_t kx, int32_t ky, int d, const float4* cx, co
                              const float* gy, const float4* hy, double eps, double theta, int self,
                              uint32_t* mask, uint32_t* maskT, int32_t* best_r, int32_t* best_c,
                              void* blkws, cudaStream_t st);
+cudaError_t truncation_masks_rows(int32_t kx, int32_t ky, int d, const float4* cx, const float* rx,
+                                  const float* fx, const float4* gx, const float4* cy,
+                                  const float* ry, const float* gy, const float4* hy, double eps,
+                                  double theta, int self, int32_t r0, int32_t r1, uint32_t* mask,
+                                  int32_t* best_r, void* blkws, cudaStream_t st);
+cudaError_t truncation_masks_cols(int32_t kx, int32_t ky, int d, const float4* cx, const float* rx,
+                                  const float* fx, const float4* gx, const float4* cy,
+                                  const float* ry, const float* gy, const float4* hy, uint32_t* mask,
+                                  int32_t* best_c, void* blkws, cudaStream_t st);
 inline size_t mask_block_ws_bytes(int32_t kx, int32_t ky) {
   return static_cast<size_t>(mask_words(kx) + mask_words(ky)) * (sizeof(float4) + sizeof(float)) +
          static_cast<size_t>(mask_words(ky)) * sizeof(uint32_t);

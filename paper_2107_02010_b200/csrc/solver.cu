@@ -1667,14 +1667,44 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
       int32_t* bxr = c->buf<int32_t>("m.bx", std::max(X.k, Y.k));
       int32_t* byr = c->buf<int32_t>("m.by", std::max(X.k, Y.k));
       void* bws = c->buf<char>("m.blk", mask_block_ws_bytes(std::max(X.k, Y.k), std::max(X.k, Y.k)));
-      CK(truncation_masks(X.k, X.k, d, X.cpts, X.radii, fmax[0], g[0], X.cpts, X.radii, fmax[0],
-                          g[0], e, theta, 1, mxx, nullptr, bxr, nullptr, bws, st));
-      CK(truncation_masks(Y.k, Y.k, d, Y.cpts, Y.radii, fmax[1], g[1], Y.cpts, Y.radii, fmax[1],
-                          g[1], e, theta, 1, myy, nullptr, byr, nullptr, bws, st));
-      // cross pair: (F, G) = (max b_yx, max a_xy); the slack is symmetric, so
-      // the yx mask (rows y) is the exact transpose of the xy mask (rows x)
-      CK(truncation_masks(X.k, Y.k, d, X.cpts, X.radii, fmax[3], g[3], Y.cpts, Y.radii, fmax[2],
-                          g[2], e, theta, 0, mxy, once ? nullptr : myx, bxr, byr, bws, st));
+      if (once) {
+        // row-sharded: each rank computes 1/world of the mask rows, the row
+        // blocks are exchanged (grouped broadcasts), then the column bests
+        // of the cross mask are set from the whole mask on every rank
+        const int rk = c->rank, wd = c->world;
+        auto cut = [&](int32_t k, int r) { return static_cast<int32_t>(int64_t(k) * r / wd); };
+        CK(truncation_masks_rows(X.k, X.k, d, X.cpts, X.radii, fmax[0], g[0], X.cpts, X.radii,
+                                 fmax[0], g[0], e, theta, 1, cut(X.k, rk), cut(X.k, rk + 1), mxx,
+                                 bxr, bws, st));
+        CK(truncation_masks_rows(Y.k, Y.k, d, Y.cpts, Y.radii, fmax[1], g[1], Y.cpts, Y.radii,
+                                 fmax[1], g[1], e, theta, 1, cut(Y.k, rk), cut(Y.k, rk + 1), myy,
+                                 byr, bws, st));
+        CK(truncation_masks_rows(X.k, Y.k, d, X.cpts, X.radii, fmax[3], g[3], Y.cpts, Y.radii,
+                                 fmax[2], g[2], e, theta, 0, cut(X.k, rk), cut(X.k, rk + 1), mxy,
+                                 bxr, bws, st));
+        if (wd > 1) {
+          std::vector<int64_t> bnd[3];
+          const int32_t kr[3] = {X.k, Y.k, X.k}, kc[3] = {X.k, Y.k, Y.k};
+          for (int q = 0; q < 3; ++q) {
+            bnd[q].resize(wd + 1);
+            for (int r = 0; r <= wd; ++r) bnd[q][r] = int64_t(cut(kr[q], r)) * mask_words(kc[q]);
+          }
+          float* mb[3] = {reinterpret_cast<float*>(mxx), reinterpret_cast<float*>(myy),
+                          reinterpret_cast<float*>(mxy)};  // 32-bit words, moved as bytes
+          coll_bcast_rows(c, mb, bnd, 3);
+        }
+        CK(truncation_masks_cols(X.k, Y.k, d, X.cpts, X.radii, fmax[3], g[3], Y.cpts, Y.radii,
+                                 fmax[2], g[2], mxy, byr, bws, st));
+      } else {
+        CK(truncation_masks(X.k, X.k, d, X.cpts, X.radii, fmax[0], g[0], X.cpts, X.radii, fmax[0],
+                            g[0], e, theta, 1, mxx, nullptr, bxr, nullptr, bws, st));
+        CK(truncation_masks(Y.k, Y.k, d, Y.cpts, Y.radii, fmax[1], g[1], Y.cpts, Y.radii, fmax[1],
+                            g[1], e, theta, 1, myy, nullptr, byr, nullptr, bws, st));
+        // cross pair: (F, G) = (max b_yx, max a_xy); the slack is symmetric, so
+        // the yx mask (rows y) is the exact transpose of the xy mask (rows x)
+        CK(truncation_masks(X.k, Y.k, d, X.cpts, X.radii, fmax[3], g[3], Y.cpts, Y.radii, fmax[2],
+                            g[2], e, theta, 0, mxy, myx, bxr, byr, bws, st));
+      }
       if (c->profiling) {  // cluster-granularity pair count of the four masks
         double* cnt = c->buf<double>("m.cnt", 1);
         CK(cudaMemsetAsync(cnt, 0, sizeof(double), st));

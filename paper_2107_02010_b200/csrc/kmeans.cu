@@ -118,7 +118,31 @@ __global__ void __launch_bounds__(128) km_assign_kernel(const double* x, int64_t
     for (int q = threadIdx.x; q < nc * d; q += blockDim.x)
       cs[(q / d) * DM + (q % d)] = centers[static_cast<int64_t>(c0) * d + q];
     __syncthreads();
-    for (int c = 0; c < nc; ++c) {
+    // 4 centres at a time: independent float64 chains (same per-centre
+    // operation order, so the distances are bitwise those of one at a time)
+    int c = 0;
+    for (; c + 4 <= nc; c += 4) {
+      const double* cc = cs + c * DM;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int k = 0; k < DM; ++k)
+        if (k < d) {
+          const double t0 = __dsub_rn(xr[k], cc[k]);
+          const double t1 = __dsub_rn(xr[k], cc[DM + k]);
+          const double t2 = __dsub_rn(xr[k], cc[2 * DM + k]);
+          const double t3 = __dsub_rn(xr[k], cc[3 * DM + k]);
+          s0 = __dadd_rn(s0, __dmul_rn(t0, t0));
+          s1 = __dadd_rn(s1, __dmul_rn(t1, t1));
+          s2 = __dadd_rn(s2, __dmul_rn(t2, t2));
+          s3 = __dadd_rn(s3, __dmul_rn(t3, t3));
+        }
+      // strict: ties keep the lowest centre
+      if (s0 < best) { best = s0; bl = c0 + c; }
+      if (s1 < best) { best = s1; bl = c0 + c + 1; }
+      if (s2 < best) { best = s2; bl = c0 + c + 2; }
+      if (s3 < best) { best = s3; bl = c0 + c + 3; }
+    }
+    for (; c < nc; ++c) {
       const double* cc = cs + c * DM;
       double s = 0.0;
 #pragma unroll
@@ -127,7 +151,7 @@ __global__ void __launch_bounds__(128) km_assign_kernel(const double* x, int64_t
           const double t = __dsub_rn(xr[k], cc[k]);
           s = __dadd_rn(s, __dmul_rn(t, t));
         }
-      if (s < best) {  // strict: ties keep the lowest centre
+      if (s < best) {
         best = s;
         bl = c0 + c;
       }

@@ -194,29 +194,44 @@ mask_rows_kernel(MaskIn m, const float4* blk, const float* blkg, double thr, int
       if (!need) row[wl] = 0u;
     }
     uint32_t todo = __ballot_sync(0xffffffffu, need);
+    // two words per step: both words' column loads are in flight together
+    auto keep_of = [&](int32_t J, float4 Y, float rJ, float G, float4 HJ) {
+      bool keep = self && I == J;  // diagonal of a self mask
+      if (static_cast<double>(ub_regs(X, rI, F, Y, rJ, G, m.d)) >= thr) {
+        if (static_cast<double>(lb_regs(X, rI, F, GI, Y, rJ, G, HJ, m.d, g)) >= thr)
+          keep = true;
+        else
+          keep = keep || pair_slack(X, rI, F, GI, Y, rJ, G, HJ, m.d, g) >= thr;
+      }
+      return keep;
+    };
     while (todo) {
-      const int32_t w = w0 + __ffs(todo) - 1;
+      const int32_t wa = w0 + __ffs(todo) - 1;
       todo &= todo - 1;
-      const int32_t J = w * 32 + lane;
-      bool keep = false;
-      if (J < m.ky) {
-        const float4 Y = m.cy[J];
-        const float rJ = m.ry[J], G = m.gy[J];
-        keep = self && I == J;  // diagonal of a self mask
-        if (static_cast<double>(ub_regs(X, rI, F, Y, rJ, G, m.d)) >= thr) {
-          const float4 HJ = g ? m.hy[J] : zero;
-          if (static_cast<double>(lb_regs(X, rI, F, GI, Y, rJ, G, HJ, m.d, g)) >= thr)
-            keep = true;
-          else
-            keep = keep || pair_slack(X, rI, F, GI, Y, rJ, G, HJ, m.d, g) >= thr;
+      int32_t wb = -1;
+      if (todo) {
+        wb = w0 + __ffs(todo) - 1;
+        todo &= todo - 1;
+      }
+      const int32_t Ja = wa * 32 + lane, Jb = wb * 32 + lane;
+      const bool va = Ja < m.ky, vb = wb >= 0 && Jb < m.ky;
+      float4 Ya = zero, Yb = zero, Ha = zero, Hb = zero;
+      float ra = 0.f, rb = 0.f, Ga = 0.f, Gb = 0.f;
+      if (va) { Ya = m.cy[Ja]; ra = m.ry[Ja]; Ga = m.gy[Ja]; if (g) Ha = m.hy[Ja]; }
+      if (vb) { Yb = m.cy[Jb]; rb = m.ry[Jb]; Gb = m.gy[Jb]; if (g) Hb = m.hy[Jb]; }
+      const bool ka = va && keep_of(Ja, Ya, ra, Ga, Ha);
+      const bool kb = vb && keep_of(Jb, Yb, rb, Gb, Hb);
+      const uint32_t bits_a = __ballot_sync(0xffffffffu, ka);
+      const uint32_t bits_b = __ballot_sync(0xffffffffu, kb);
+      if (lane == 0) {
+        row[wa] = bits_a;
+        if (bits_a && colany) atomicOr(colany + wa, bits_a);
+        if (wb >= 0) {
+          row[wb] = bits_b;
+          if (bits_b && colany) atomicOr(colany + wb, bits_b);
         }
       }
-      const uint32_t bits = __ballot_sync(0xffffffffu, keep);
-      if (lane == 0) {
-        row[w] = bits;
-        if (bits && colany) atomicOr(colany + w, bits);
-      }
-      any = any || bits != 0u;
+      any = any || bits_a != 0u || bits_b != 0u;
     }
   }
   if (__syncthreads_or(any)) {

@@ -724,6 +724,10 @@ double oracle_divergence_from_potentials(const msot_params* prm, double eps, con
 
 // The full solve: symmetric_sinkhorn or
 // multiscale_sinkhorn then divergence.
+// Schedule diameter override (> 0), set by oracle_barycenter for its shared
+// schedule (mirrors msot_ctx::diam_override).
+static double g_diam_override = 0.0;
+
 int oracle_sinkhorn(const msot_params* prm, const double* x, const double* a, int64_t n,
                     const double* y, const double* b, int64_t m, int d, double* a_xx,
                     double* b_yy, double* a_xy, double* b_yx, double* loss_out,
@@ -748,7 +752,8 @@ int oracle_sinkhorn(const msot_params* prm, const double* x, const double* a, in
     for (int k = 0; k < d; ++k) lo[k] = std::min(lo[k], y[j * d + k]), hi[k] = std::max(hi[k], y[j * d + k]);
   double diag2 = 0.0;
   for (int k = 0; k < d; ++k) diag2 += (hi[k] - lo[k]) * (hi[k] - lo[k]);
-  const double diam = std::max(std::sqrt(diag2), prm->blur);
+  const double diam = g_diam_override > 0 ? std::max(g_diam_override, prm->blur)
+                                         : std::max(std::sqrt(diag2), prm->blur);
   S.diameter = diam;
 
   const int ns = msot_schedule_len(diam, prm->blur, prm->scaling);
@@ -1123,6 +1128,24 @@ int oracle_sinkhorn(const msot_params* prm, const double* x, const double* a, in
 //   grad_i = sum_j pi^xy_ij (x_i - y_j) - sum_k pi^xx_ik (x_i - x_k),
 //   pi^xy_ij = a_i b_j exp((b_yx_i + a_xy_j - C_ij)/eps),
 //   pi^xx_ik = a_i a_k exp((a_xx_i + a_xx_k - C_ik)/eps).
+// sign * sum_j a_i c_j exp((f_i + g_j - C_ij)/eps) (x_i - z_j), added into out
+static void plan_displacement(const double* x, const double* a, int64_t n, const double* z,
+                              const double* c, int64_t m, int d, const double* f, const double* g,
+                              double eps, double sign, double* out) {
+  msot::parallel::for_ranges(static_cast<std::size_t>(n), [&](std::size_t lo, std::size_t hi) {
+    for (std::size_t i = lo; i < hi; ++i) {
+      std::vector<double> acc(d, 0.0);
+      const double* xi = x + i * d;
+      for (int64_t j = 0; j < m; ++j) {
+        const double* zj = z + j * d;
+        const double pij = a[i] * c[j] * std::exp((f[i] + g[j] - cost(xi, zj, d, 2.0)) / eps);
+        for (int k = 0; k < d; ++k) acc[k] += pij * (xi[k] - zj[k]);
+      }
+      for (int k = 0; k < d; ++k) out[i * d + k] += sign * acc[k];
+    }
+  });
+}
+
 int oracle_sinkhorn_grad(const msot_params* prm, const double* x, const double* a, int64_t n,
                          const double* y, const double* b, int64_t m, int d, double* loss_out,
                          double* grad) {
@@ -1133,23 +1156,9 @@ int oracle_sinkhorn_grad(const msot_params* prm, const double* x, const double* 
                                  byx.data(), loss_out, &st);
   if (rc != MSOT_OK) return rc;
   const double eps = std::pow(prm->blur, prm->p);
-  msot::parallel::for_ranges(static_cast<std::size_t>(n), [&](std::size_t lo, std::size_t hi) {
-    for (std::size_t i = lo; i < hi; ++i) {
-      std::vector<double> g(d, 0.0);
-      const double* xi = x + i * d;
-      for (int64_t j = 0; j < m; ++j) {
-        const double* yj = y + j * d;
-        const double pij = a[i] * b[j] * std::exp((byx[i] + axy[j] - cost(xi, yj, d, 2.0)) / eps);
-        for (int k = 0; k < d; ++k) g[k] += pij * (xi[k] - yj[k]);
-      }
-      for (int64_t q = 0; q < n; ++q) {
-        const double* xq = x + q * d;
-        const double piq = a[i] * a[q] * std::exp((axx[i] + axx[q] - cost(xi, xq, d, 2.0)) / eps);
-        for (int k = 0; k < d; ++k) g[k] -= piq * (xi[k] - xq[k]);
-      }
-      for (int k = 0; k < d; ++k) grad[i * d + k] = g[k];
-    }
-  });
+  std::fill(grad, grad + n * d, 0.0);
+  plan_displacement(x, a, n, y, b, m, d, byx.data(), axy.data(), eps, 1.0, grad);
+  plan_displacement(x, a, n, x, a, n, d, axx.data(), axx.data(), eps, -1.0, grad);
   return MSOT_OK;
 }
 
@@ -1198,15 +1207,53 @@ int oracle_barycenter(const msot_params* prm, const double* x0, const double* a,
                       const double* const* ys, const double* const* bs, const int64_t* ms, int d,
                       int iters, double step, double tol, double* x_out, double* loss_traj,
                       int* steps_done) {
-  Vec x(x0, x0 + n * d), xn(n * d), field(n * d), fieldn(n * d), g(n * d);
+  if (prm->p != 2.0) return fail(MSOT_EUSAGE, "barycenter descent is defined for p = 2");
+  Vec x(x0, x0 + n * d), xn(n * d), field(n * d), fieldn(n * d), g(n * d), self0(n * d);
+  Vec axx0(n);
+  const double eps = std::pow(prm->blur, prm->p);
+  struct Reset {
+    ~Reset() { g_diam_override = 0.0; }
+  } reset;
+  // The K solves share one eps schedule (diameter of the union of x and every
+  // target) and the x-x self term of target 0's solve (its final a_xx and
+  // self plan), as msot_barycenter does.
   auto evaluate = [&](const Vec& xp, Vec& fld, double& L) -> int {
     std::fill(fld.begin(), fld.end(), 0.0);
+    std::vector<double> lo(d, INFINITY), hi(d, -INFINITY);
+    auto extend = [&](const double* p, int64_t cnt) {
+      for (int64_t i = 0; i < cnt; ++i)
+        for (int q = 0; q < d; ++q) {
+          lo[q] = std::min(lo[q], p[i * d + q]);
+          hi[q] = std::max(hi[q], p[i * d + q]);
+        }
+    };
+    extend(xp.data(), n);
+    for (int t = 0; t < k; ++t) extend(ys[t], ms[t]);
+    double d2 = 0.0;
+    for (int q = 0; q < d; ++q) d2 += (hi[q] - lo[q]) * (hi[q] - lo[q]);
+    g_diam_override = std::sqrt(d2);
     L = 0.0;
     for (int t = 0; t < k; ++t) {
+      Vec axx(n), byy(ms[t]), axy(ms[t]), byx(n);
+      msot_stats st{};
       double l = 0.0;
-      const int rc = oracle_sinkhorn_grad(prm, xp.data(), a, n, ys[t], bs[t], ms[t], d, &l, g.data());
+      const int rc = oracle_sinkhorn(prm, xp.data(), a, n, ys[t], bs[t], ms[t], d, axx.data(),
+                                     byy.data(), axy.data(), byx.data(), &l, &st);
       if (rc != MSOT_OK) return rc;
-      for (int64_t q = 0; q < n * d; ++q) fld[q] += g[q] / k;
+      if (t == 0) {
+        axx0 = axx;
+        std::fill(self0.begin(), self0.end(), 0.0);
+        plan_displacement(xp.data(), a, n, xp.data(), a, n, d, axx0.data(), axx0.data(), eps, 1.0,
+                          self0.data());
+      } else {  // S = <a, b_yx - a_xx> + <b, a_xy - b_yy>: swap in the shared a_xx
+        Vec dl(n);
+        for (int64_t i = 0; i < n; ++i) dl[i] = a[i] * (axx[i] - axx0[i]);
+        l += msot::pairwise_sum(dl);
+      }
+      std::fill(g.begin(), g.end(), 0.0);
+      plan_displacement(xp.data(), a, n, ys[t], bs[t], ms[t], d, byx.data(), axy.data(), eps, 1.0,
+                        g.data());
+      for (int64_t q = 0; q < n * d; ++q) fld[q] += (g[q] - self0[q]) / k;
       L += l;
     }
     L /= k;

@@ -266,6 +266,58 @@ cudaError_t super_keys(const uint32_t* sorted_keys, const int32_t* offsets, int3
   return cudaGetLastError();
 }
 
+// dst[s] = src[idx[s]] / dst[idx[s]] = src[s] (float4, float): moves between a
+// solve's sorted order and the caller's (idx = the sort permutation).
+__global__ void gather_f4_kernel(const float4* src, const int32_t* idx, int64_t n, float4* dst) {
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s < n) dst[s] = src[idx[s]];
+}
+__global__ void scatter_f4_kernel(const float4* src, const int32_t* idx, int64_t n, float4* dst) {
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s < n) dst[idx[s]] = src[s];
+}
+__global__ void scatter_f32_kernel(const float* src, const int32_t* idx, int64_t n, float* dst) {
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s < n) dst[idx[s]] = src[s];
+}
+cudaError_t gather_f4(const float4* src, const int32_t* idx, int64_t n, float4* dst, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  ++g_launches;
+  gather_f4_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(src, idx, n, dst);
+  return cudaGetLastError();
+}
+cudaError_t scatter_f4(const float4* src, const int32_t* idx, int64_t n, float4* dst, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  ++g_launches;
+  scatter_f4_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(src, idx, n, dst);
+  return cudaGetLastError();
+}
+cudaError_t scatter_f32(const float* src, const int32_t* idx, int64_t n, float* dst, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  ++g_launches;
+  scatter_f32_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(src, idx, n, dst);
+  return cudaGetLastError();
+}
+
+// payload {w, sx, sy, sz} += w * (cx, cy, cz): a plan payload's weighted
+// coordinate sums moved to another origin.
+__global__ void shift_payload_kernel(float4* p, int64_t n, double cx, double cy, double cz) {
+  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  float4 v = p[s];
+  const double w = v.x;
+  v.y = static_cast<float>(v.y + w * cx);
+  v.z = static_cast<float>(v.z + w * cy);
+  v.w = static_cast<float>(v.w + w * cz);
+  p[s] = v;
+}
+cudaError_t shift_payload(float4* p, int64_t n, double cx, double cy, double cz, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  ++g_launches;
+  shift_payload_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(p, n, cx, cy, cz);
+  return cudaGetLastError();
+}
+
 __global__ void inherit_kernel(const float* coarse, const int32_t* labels, int64_t n, float* fine) {
   const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (s < n) fine[s] = coarse[labels[s]];

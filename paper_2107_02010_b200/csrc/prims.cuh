@@ -124,6 +124,10 @@ cudaError_t cluster_bound(const float4* pts, const double* w64, const float* f,
                           float4* grad, cudaStream_t st);
 cudaError_t inherit(const float* coarse, const int32_t* labels, int64_t n, float* fine,
                     cudaStream_t st);
+cudaError_t gather_f4(const float4* src, const int32_t* idx, int64_t n, float4* dst, cudaStream_t st);
+cudaError_t scatter_f4(const float4* src, const int32_t* idx, int64_t n, float4* dst, cudaStream_t st);
+cudaError_t scatter_f32(const float* src, const int32_t* idx, int64_t n, float* dst, cudaStream_t st);
+cudaError_t shift_payload(float4* p, int64_t n, double cx, double cy, double cz, cudaStream_t st);
 cudaError_t super_keys(const uint32_t* sorted_keys, const int32_t* offsets, int32_t k, int bits,
                        uint32_t* out, cudaStream_t st);
 

@@ -86,6 +86,14 @@ struct msot_ctx {
   msot_host_broadcast_fn host_bc = nullptr;
   void* host_user = nullptr;
   bool profiling = false;
+  // barycenter (msot_barycenter): common schedule diameter (> 0: override) and
+  // the x-x self term shared by every target: mode 1 = this solve records its
+  // final a_xx and self-plan payload (caller order), mode 2 = this solve
+  // skips the x-x problem and uses them
+  double diam_override = 0.0;
+  int self_mode = 0;
+  float* self_axx = nullptr;    // [n] caller order
+  float4* self_pay = nullptr;   // [n] caller order
   std::map<std::string, std::pair<void*, size_t>> bufs;
   std::vector<cudaEvent_t> ev;  // profiling events (pairs)
   size_t ev_used = 0;
@@ -498,6 +506,7 @@ struct ProbSpec {
 
 struct Plan {
   int np = 0;
+  bool skip_p0 = false;  // problem 0 (x-x) evaluated nowhere (shared self term)
   ProbSpec ps[kMaxProblems];
   int64_t t0[kMaxProblems], t1[kMaxProblems];
   std::vector<int64_t> row_bounds[kMaxProblems];  // world+1 row boundaries
@@ -544,6 +553,7 @@ void build_plan(msot_ctx* c, const std::string& tag, Plan& P) {
     }
     std::vector<int64_t> tb;
     shard_tiles(work, c->world, tb);
+    if (p == 0 && P.skip_p0) tb.assign(c->world + 1, 0);
     P.t0[p] = tb[c->rank];
     P.t1[p] = tb[c->rank + 1];
     P.row_bounds[p].resize(c->world + 1);
@@ -1325,6 +1335,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
   if (prm->p != 2.0) raise(MSOT_EUSAGE, "the GPU path implements p = 2");
   cudaStream_t st = c->st;
   const int64_t launches0 = g_launches;
+  double frame[3] = {0.0, 0.0, 0.0};  // centre of the float32 atom frame (voxel path)
   c->ev_used = 0;
   c->marks.clear();
   c->mark(0);  // phase 0: bounding box, voxel edge, clustering
@@ -1352,7 +1363,8 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
     if (!std::isfinite(lo[k]) || !std::isfinite(hi[k])) raise(MSOT_EDATA, "non-finite point");
   double diag2 = 0.0;
   for (int k = 0; k < d; ++k) diag2 += (hi[k] - lo[k]) * (hi[k] - lo[k]);
-  const double diam = std::max(std::sqrt(diag2), prm->blur);
+  const double diam = c->diam_override > 0 ? std::max(c->diam_override, prm->blur)
+                                           : std::max(std::sqrt(diag2), prm->blur);
   S->diameter = diam;
   const int ns = msot_schedule_len(diam, prm->blur, prm->scaling);
   if (prm->max_full_iters > 0 && ns > prm->max_full_iters)
@@ -1462,6 +1474,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
   for (int k = 0; k < d; ++k) {
     g.origin[k] = lo[k];
     g.center[k] = 0.5 * (lo[k] + hi[k]);
+    if (k < 3) frame[k] = g.center[k];
   }
   double cell = prm->cluster_scale > 0 ? prm->cluster_scale : msot_auto_cell(lo, hi, d, n, m);
   if (ms && prm->cluster_scale <= 0) {  // policy.h: refine on occupied voxels
@@ -1487,6 +1500,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
     dense_rangeset(c, "d.yx", n, m, ryx);
     Plan P;
     sym_specs(P, X.pts, X.lw2, n, Y.pts, Y.lw2, m, &rxx, &ryy, &rxy, &ryx);
+    P.skip_p0 = c->self_mode == 2;
     build_plan(c, "pd", P);
     for (int t = 0; t <= ns; ++t) {
       const int tt = std::min(t, ns - 1);
@@ -1538,6 +1552,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
           dense_rangeset(c, tg + ".yx", kx, ky, ryx);
           sym_specs(Pc, xp, xl, kx, yp, yl, ky, &rxx, &ryy, &rxy, &ryx);
         }
+        Pc.skip_p0 = c->self_mode == 2;
         build_plan(c, "p" + tg, Pc);
         const double cfull = double(kx) * kx + double(ky) * ky + 2.0 * double(kx) * ky;
         for (int t = t0; t < t1; ++t) {
@@ -1673,9 +1688,12 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
         // of the cross mask are set from the whole mask on every rank
         const int rk = c->rank, wd = c->world;
         auto cut = [&](int32_t k, int r) { return static_cast<int32_t>(int64_t(k) * r / wd); };
-        CK(truncation_masks_rows(X.k, X.k, d, X.cpts, X.radii, fmax[0], g[0], X.cpts, X.radii,
-                                 fmax[0], g[0], e, theta, 1, cut(X.k, rk), cut(X.k, rk + 1), mxx,
-                                 bxr, bws, st));
+        if (c->self_mode == 2)  // shared self term: the x-x problem is not evaluated
+          CK(cudaMemsetAsync(mxx, 0, size_t(X.k) * mask_words(X.k) * sizeof(uint32_t), st));
+        else
+          CK(truncation_masks_rows(X.k, X.k, d, X.cpts, X.radii, fmax[0], g[0], X.cpts, X.radii,
+                                   fmax[0], g[0], e, theta, 1, cut(X.k, rk), cut(X.k, rk + 1),
+                                   mxx, bxr, bws, st));
         CK(truncation_masks_rows(Y.k, Y.k, d, Y.cpts, Y.radii, fmax[1], g[1], Y.cpts, Y.radii,
                                  fmax[1], g[1], e, theta, 1, cut(Y.k, rk), cut(Y.k, rk + 1), myy,
                                  byr, bws, st));
@@ -1735,6 +1753,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
         mask_rangeset(c, "f.xy", Y.labels, Y.offsets_h, m, X.offsets, X.k, myx, rxy);  // rows y, cols x
         sym_specs(Pf, X.pts, X.lw2, n, Y.pts, Y.lw2, m, &rxx, &ryy, &rxy, &ryx);
       }
+      Pf.skip_p0 = c->self_mode == 2;
       build_plan(c, "pf", Pf);
     };
     for (int t = tsw; t <= ns; ++t) {
@@ -1764,6 +1783,9 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
 
   // grad_positions from the final potentials, on the pair
   // sets of the last update: cross plan (rows x, cols y) and self plan
+  // shared self term (msot_barycenter): this solve skipped the x-x problem,
+  // its final a_xx is the recorded one (caller order -> this solve's order)
+  if (c->self_mode == 2) CK(inherit(c->self_axx, X.perm, n, U.v[cur][0], st));
   if (d_grad) {
     c->mark(5);
     float** f = U.v[cur];
@@ -1772,8 +1794,23 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
     const float* gc[2] = {f[2], f[0]};  // a_xy, a_xx
     const float4* pay[2] = {Y.pts, X.pts};
     float4* outp[2] = {c->buf<float4>("grad.pxy", n), c->buf<float4>("grad.pxx", n)};
-    plan_group(c, "pg", 2, specs, fr, gc, pay, outp, eps[ns - 1], d);
+    // the recorded payload {mass, sum pi x} is kept in absolute coordinates
+    // (each solve centres its float32 atoms on its own bounding box)
+    if (c->self_mode == 2) {  // cross plan only; the self plan's payload is recorded
+      plan_group(c, "pg", 1, specs, fr, gc, pay, outp, eps[ns - 1], d);
+      CK(gather_f4(c->self_pay, X.perm, n, outp[1], st));
+      CK(shift_payload(outp[1], n, -frame[0], -frame[1], -frame[2], st));
+    } else {
+      plan_group(c, "pg", 2, specs, fr, gc, pay, outp, eps[ns - 1], d);
+    }
+    if (c->self_mode == 1) {
+      CK(scatter_f4(outp[1], X.perm, n, c->self_pay, st));
+      CK(shift_payload(c->self_pay, n, frame[0], frame[1], frame[2], st));
+      CK(scatter_f32(f[0], X.perm, n, c->self_axx, st));
+    }
     CK(grad_positions(X.pts, X.w64, outp[0], outp[1], X.perm, n, d, d_grad, st));
+  } else if (c->self_mode == 1) {
+    CK(scatter_f32(U.v[cur][0], X.perm, n, c->self_axx, st));
   }
 
   // transfer_labels (K9) from the final cross potentials
@@ -2199,13 +2236,42 @@ int msot_barycenter(msot_ctx* c, const msot_params* prm, const double* x0, const
     }
     CK(cudaMemcpyAsync(dx, x0, n * d * sizeof(double), cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(da, a, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    // The K solves of one evaluation share one eps schedule (diameter of the
+    // union of the barycenter and every target) and therefore one x-x self
+    // term: target 0's solve records its final a_xx and self-plan payload,
+    // the others skip the x-x problem (its work is ~N/M times the cross
+    // problem's) and use them (the test oracle's barycenter does the same).
+    struct SelfScope {
+      msot_ctx* c;
+      ~SelfScope() {
+        c->self_mode = 0;
+        c->diam_override = 0.0;
+      }
+    } scope{c};
+    c->self_axx = c->buf<float>("bc.saxx", n);
+    c->self_pay = c->buf<float4>("bc.spay", n);
+    long long* lohi = c->buf<long long>("bc.bbox", 2 * d);
+    auto union_diameter = [&](const double* xp) {
+      CK(bbox(xp, n, d, lohi, true, st));
+      for (int t = 0; t < k; ++t) CK(bbox(dy[t], ms[t], d, lohi, false, st));
+      std::vector<long long> lh(2 * d);
+      CK(cudaMemcpyAsync(lh.data(), lohi, 2 * d * sizeof(long long), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      std::vector<double> lo(d), hi(d);
+      bbox_decode(lh.data(), d, lo.data(), hi.data());
+      double d2 = 0.0;
+      for (int q = 0; q < d; ++q) d2 += (hi[q] - lo[q]) * (hi[q] - lo[q]);
+      return std::sqrt(d2);
+    };
     // loss and mean gradient at positions xp (into fld)
     auto evaluate = [&](const double* xp, double* fld) {
       CK(cudaMemsetAsync(fld, 0, n * d * sizeof(double), st));
       double tot = 0.0;
+      c->diam_override = union_diameter(xp);
       for (int t = 0; t < k; ++t) {
         msot_stats s1{};
         double l = 0.0;
+        c->self_mode = t == 0 ? 1 : 2;
         solve_device(c, prm, xp, da, n, dy[t], db[t], ms[t], d, &l, &s1, nullptr, grad);
         CK(field_accumulate(fld, grad, 1.0 / k, n * d, st));
         tot += l;

@@ -32,6 +32,7 @@ struct SolverParams {
   int pair_eval = 1;   // evaluate-once fine phase
   int clusters = 0;    // D > 3: K-means clusters per measure (0 = ceil(sqrt(N)))
   int seed = 0;        // K-means seeding
+  int super_level = -1;  // voxel multiscale super-voxel level: -1 auto, 0 off, 1 on
 
   msot_params to_c() const;
 };

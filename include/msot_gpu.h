@@ -65,6 +65,11 @@ typedef struct msot_params {
   int32_t clusters;      /* D > 3 multiscale: K-means clusters per measure, 0 =
                             ceil(sqrt(N))                       */
   int32_t seed;          /* K-means seeding: first centre = atom (seed mod N)  */
+  int32_t super_level;   /* voxel multiscale: a super-voxel level before the
+                            cluster-level coarse phase (policy.h:
+                            msot_super_switch): -1 = automatic (when either
+                            measure has >= MSOT_SUPER_MIN_CLUSTERS clusters,
+                            default), 0 = off, 1 = on                         */
 } msot_params;
 
 /* Defaults of SPEC.md:128 (q=0.9), :306 (switch 2x radius), :308 (theta=20). */

@@ -957,7 +957,9 @@ int oracle_sinkhorn(const msot_params* prm, const double* x, const double* a, in
     // (policy.h:msot_super_switch): consecutive clusters sharing a super-voxel
     // key, run for t < t2, their duals inherited by the clusters.
     Duals cu{Vec(cx.k, 0.0), Vec(cy.k, 0.0), Vec(cy.k, 0.0), Vec(cx.k, 0.0)};
-    const int t2 = tsw > 0 ? msot_super_switch(sig.data(), tsw, cell, d) : 0;
+    const int t2 = tsw > 0 ? msot_super_switch(sig.data(), tsw, cell, d, std::max(cx.k, cy.k),
+                                               prm->super_level)
+                           : 0;
     if (t2 > 0) {
       auto super = [&](const Clusters& cc, const Measure& Mc, const double* pts,
                        std::vector<int32_t>& lab) {

@@ -28,18 +28,20 @@ class Params(C.Structure):
         ("pair_eval", C.c_int32),
         ("clusters", C.c_int32),
         ("seed", C.c_int32),
+        ("super_level", C.c_int32),
     ]
 
 
 def make_params(blur=0.05, reach=math.inf, p=2.0, scaling=0.9, multiscale=False,
                 retruncate=0, cluster_scale=0.0, theta=20.0, switch_factor=2.0,
                 max_full_iters=10000, mask_rule=0, transfer_rule=0, pair_eval=1, clusters=0,
-                seed=0):
+                seed=0, super_level=-1):
     """Defaults follow SPEC.md:128 (q=0.9), :306 (switch 2 r_max), :308 (theta 20),
     :270-274 (coarse duals inherited by the fine atoms)."""
     return Params(blur, math.inf if reach is None else reach, p, scaling, int(bool(multiscale)),
                   int(retruncate), cluster_scale, theta, switch_factor, int(max_full_iters),
-                  int(mask_rule), int(transfer_rule), int(pair_eval), int(clusters), int(seed))
+                  int(mask_rule), int(transfer_rule), int(pair_eval), int(clusters), int(seed),
+                  int(super_level))
 
 
 class Stats(C.Structure):

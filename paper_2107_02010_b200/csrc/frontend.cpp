@@ -167,6 +167,7 @@ msot_params SolverParams::to_c() const {
   p.pair_eval = pair_eval;
   p.clusters = clusters;
   p.seed = seed;
+  p.super_level = super_level;
   return p;
 }
 

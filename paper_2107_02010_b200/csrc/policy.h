@@ -212,7 +212,13 @@ static inline int msot_switch_index(const double* sigma, int n, double r_max, do
 #define MSOT_SUPER_SHIFT 1
 #define MSOT_SUPER_SWITCH 2.0  /* C3: S within 8.6e-5 of dense (1.0: 7.3e-4; none: 9.0e-5) */
 #define MSOT_SUPER_MIN_SCALES 4
-static inline int msot_super_switch(const double* sigma, int tsw, double cell, int d) {
+/* automatic mode: only where the cluster-level coarse phase costs something
+ * (C3, 34k clusters: 32 -> 11 ms; config 2, 3k clusters: no gain, S 4.5e-4 ->
+ * 7.4e-4 from dense) */
+#define MSOT_SUPER_MIN_CLUSTERS 16384
+static inline int msot_super_switch(const double* sigma, int tsw, double cell, int d,
+                                    int64_t kmax, int mode) {
+  if (mode == 0 || (mode < 0 && kmax < MSOT_SUPER_MIN_CLUSTERS)) return 0;
   const double r = 0.5 * sqrt((double)d) * cell * (double)(1 << MSOT_SUPER_SHIFT);
   const int t2 = msot_switch_index(sigma, tsw, r, MSOT_SUPER_SWITCH);
   return (tsw - t2 >= MSOT_SUPER_MIN_SCALES) ? t2 : 0;

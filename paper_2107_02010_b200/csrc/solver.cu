@@ -1568,7 +1568,8 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
       int ccur = 0;
       // super level (policy.h:msot_super_switch): the first t2 scales on
       // super voxels, inherited by the clusters
-      const int t2 = msot_super_switch(sig.data(), tsw, cell, d);
+      const int t2 = msot_super_switch(sig.data(), tsw, cell, d, std::max(X.k, Y.k),
+                                       prm->super_level);
       if (t2 > 0) {
         SuperMeasure SX, SY;
         super_measure(c, "x", X, d, SX);
@@ -1897,6 +1898,7 @@ void msot_params_default(msot_params* p) {
   p->switch_factor = 2.0;
   p->max_full_iters = 10000;
   p->pair_eval = 1;
+  p->super_level = -1;
 }
 
 int msot_schedule(double diameter, const msot_params* p, double* sigma, double* eps, double* lam,

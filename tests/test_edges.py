@@ -40,7 +40,7 @@ def test_multiscale_low_dim(ctx, oracle, d):
     x, y = mixture(n, 21, d), mixture(m, 22, d)
     a, b = np.full(n, 1 / n), np.full(m, 1 / m)
     prm = make_params(blur=0.01, multiscale=True, retruncate=1,
-                      cluster_scale=0.02 if d == 1 else 0.03)
+                      cluster_scale=0.02 if d == 1 else 0.03, super_level=1)
     sg, so = check(ctx, oracle, prm, x, a, y, b, 1e-4)
     assert (sg["kx"], sg["t_switch"], sg["t_super"]) == (so["kx"], so["t_switch"], so["t_super"])
     assert sg["pairs_fine"] < sg["pairs_fine_dense"]

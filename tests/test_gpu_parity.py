@@ -200,7 +200,7 @@ def test_multiscale_parity(ctx, oracle, retruncate, pair_eval):
     x, y = mixture(n, 3), mixture(n, 4)
     a, b = np.full(n, 1 / n), np.full(n, 1 / n)
     prm = make_params(blur=0.01, multiscale=True, retruncate=retruncate, cluster_scale=0.04,
-                      pair_eval=pair_eval)
+                      pair_eval=pair_eval, super_level=1)
     lg, pg, sg, lo, po, so = run_both(ctx, oracle, prm, x, a, y, b)
     assert (sg["kx"], sg["ky"], sg["t_switch"]) == (so["kx"], so["ky"], so["t_switch"])
     # the super-voxel level of the coarse phase (policy.h:msot_super_switch)
@@ -221,10 +221,16 @@ def test_multiscale_unbalanced_parity(ctx, oracle, reach):
     a = rng.random(n) + 0.5
     a /= a.sum()
     b = np.full(m, 1.3 / m)
-    prm = make_params(blur=0.01, reach=reach, multiscale=True, retruncate=1, cluster_scale=0.04)
+    prm = make_params(blur=0.01, reach=reach, multiscale=True, retruncate=1, cluster_scale=0.04,
+                      super_level=1)
     lg, pg, sg, lo, po, so = run_both(ctx, oracle, prm, x, a, y, b)
     assert sg["t_switch"] == so["t_switch"] and sg["t_switch"] < sg["n_scales"]
     assert (sg["t_super"], sg["k_super_x"]) == (so["t_super"], so["k_super_x"])
+    assert sg["t_super"] > 0
+    # automatic mode: no super level below MSOT_SUPER_MIN_CLUSTERS clusters
+    _, _, sa = ctx.sinkhorn(make_params(blur=0.01, reach=reach, multiscale=True, retruncate=1,
+                                        cluster_scale=0.04), x, a, y, b, potentials=False)
+    assert sa["t_super"] == 0
     check_pots(pg, po, 1e-4)
     assert abs(lg - lo) <= LOSS_TOL * abs(lo), (lg, lo)
 

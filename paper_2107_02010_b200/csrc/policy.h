@@ -36,8 +36,10 @@ extern "C" {
 /* Lloyd iterations of the K-means coarsening inside the multiscale solver
  * (the stand-alone kmeans_coarsen op keeps SPEC.md:265's cap of 100): the
  * clusters only steer efficiency (truncation), never the result, and the
- * float64 assignment of 400k x 633 x 60 costs ~10 ms per iteration. */
-#define MSOT_KMEANS_SOLVER_ITERS 20
+ * float64 assignment of 400k x 633 x 60 costs ~5 ms per iteration.  Config 4,
+ * 20 -> 8 iterations: setup 353 -> 199 ms, total 2.03 -> 1.73 s, S 3.9e-4 ->
+ * 1.9e-4 from dense (the cluster radii move the switch one scale later). */
+#define MSOT_KMEANS_SOLVER_ITERS 8
 /* Cube ids are Morton-interleaved with this many bits per axis (D <= 3). */
 #define MSOT_MORTON_BITS 10
 

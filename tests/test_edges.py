@@ -109,3 +109,18 @@ def test_far_apart_clouds(ctx, oracle):
     x, y = mixture(800, 61), mixture(700, 62) + 50.0
     a, b = np.full(800, 1 / 800), np.full(700, 1 / 700)
     sg, so = check(ctx, oracle, make_params(blur=0.05), x, a, y, b, 0.05 ** 2)
+
+
+@pytest.mark.parametrize("multiscale", [False, True])
+def test_deterministic(ctx, multiscale):
+    """Fixed-order reductions everywhere (no float atomics): a repeated solve
+    is bitwise identical."""
+    x, y = mixture(6000, 71), mixture(5000, 72)
+    a, b = np.full(6000, 1 / 6000), np.full(5000, 1 / 5000)
+    prm = make_params(blur=0.01, multiscale=multiscale, retruncate=1, cluster_scale=0.04,
+                      super_level=1)
+    l1, p1, _ = ctx.sinkhorn(prm, x, a, y, b)
+    l2, p2, _ = ctx.sinkhorn(prm, x, a, y, b)
+    assert l1 == l2
+    for u, v in zip((p1.a_xx, p1.b_yy, p1.a_xy, p1.b_yx), (p2.a_xx, p2.b_yy, p2.a_xy, p2.b_yx)):
+        np.testing.assert_array_equal(u, v)

@@ -534,7 +534,7 @@ void shard_tiles(const std::vector<double>& work, int world, std::vector<int64_t
   }
 }
 
-void build_plan(msot_ctx* c, const std::string& tag, Plan& P) {
+void build_plan(msot_ctx* c, const std::string& tag, Plan& P, int waves = 32) {
   cudaStream_t st = c->st;
   // per-problem shard of row tiles, weighted by evaluated pairs
   int64_t tot_tiles = 0, tot_cols = 0;
@@ -565,8 +565,11 @@ void build_plan(msot_ctx* c, const std::string& tag, Plan& P) {
       P.pairs_local += static_cast<double>(rows) * static_cast<double>(R.tile_cols_h[t]);
     }
   }
-  // chunk size: enough work items for ~2 waves of resident CTAs
-  const int64_t target = static_cast<int64_t>(c->n_sm) * 12 * 2;
+  // chunk size: small work items (~32 waves of resident CTAs, floor 2 column
+  // tiles) keep the tail of every launch short — C3 fine phase 342 -> 314 ms
+  // against ~2 waves (8: 321, 16: 315, 64: 315 ms); the high-D kernel keeps 2
+  // (its CTAs walk block ranges; 32 cost config 4 ~1.5%)
+  const int64_t target = static_cast<int64_t>(c->n_sm) * 12 * waves;
   int64_t chunk = std::max<int64_t>(2 * kColTile, (tot_cols + target - 1) / std::max<int64_t>(target, 1));
   chunk = (chunk + kColTile - 1) / kColTile * kColTile;
   int32_t* cnt = c->buf<int32_t>(tag + ".icnt", tot_tiles + 1);
@@ -1090,7 +1093,7 @@ void hd_multiscale(msot_ctx* c, const msot_params* prm, const double* d_x, const
     cc.n = kx;
     cc.m = ky;
     cc.hd3 = {LY.cpack, LX.cpack, LY.csq, LX.csq, LY.cf, LX.cf};
-    build_plan(c, "hpc", Pc);
+    build_plan(c, "hpc", Pc, 2);
     const double cfull = double(kx) * kx + double(ky) * ky + 2.0 * double(kx) * ky;
     for (int t = 0; t < tsw; ++t) {
       sym_step_once(c, Pc, Uc, ccur, eps[t], lam[t], false, ss, cc);
@@ -1121,7 +1124,7 @@ void hd_multiscale(msot_ctx* c, const msot_params* prm, const double* d_x, const
       Pe.ps[1] = {nullptr, mr, nullptr, LY.clw2, ky, &eyy, {LY.pack, LY.cpack, LY.sq, LY.csq, LY.f, LY.cf}};
       Pe.ps[2] = {nullptr, mr, nullptr, LX.clw2, kx, &exy, {LY.pack, LX.cpack, LY.sq, LX.csq, LY.f, LX.cf}};
       Pe.ps[3] = {nullptr, nr, nullptr, LY.clw2, ky, &eyx, {LX.pack, LY.cpack, LX.sq, LY.csq, LX.f, LY.cf}};
-      build_plan(c, "hpe", Pe);
+      build_plan(c, "hpe", Pe, 2);
       ScaleArgs ea{};
       ea.h[0] = co[0]; ea.est[0] = dst[0]; ea.out[0] = U.v[cur][0];
       ea.h[1] = co[1]; ea.est[1] = dst[1]; ea.out[1] = U.v[cur][1];
@@ -1177,7 +1180,7 @@ void hd_multiscale(msot_ctx* c, const msot_params* prm, const double* d_x, const
     Pf.ps[0] = {nullptr, nr, nullptr, LX.lw2, nr, &sxx.R, {LX.pack, LX.pack, LX.sq, LX.sq, LX.f, LX.f}, &sxx, LX.lw2};
     Pf.ps[1] = {nullptr, mr, nullptr, LY.lw2, mr, &syy.R, {LY.pack, LY.pack, LY.sq, LY.sq, LY.f, LY.f}, &syy, LY.lw2};
     Pf.ps[2] = {nullptr, nr, nullptr, LY.lw2, mr, &syx.R, {LX.pack, LY.pack, LX.sq, LY.sq, LX.f, LY.f}, &syx, LX.lw2};
-    build_plan(c, "hpf", Pf);
+    build_plan(c, "hpf", Pf, 2);
   };
   for (int t = tsw; t <= ns; ++t) {
     const int tt = std::min(t, ns - 1);
@@ -1458,7 +1461,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
       P.ps[2] = {nullptr, m, nullptr, X.lw2, n, &fxy, {ay, bx, sqy, sqx, fy, fx}};  // a_xy
       P.ps[3] = {nullptr, n, nullptr, Y.lw2, m, &fyx, {ax, by, sqx, sqy, fx, fy}};  // b_yx
     }
-    build_plan(c, "ph", P);
+    build_plan(c, "ph", P, 2);
     for (int t = 0; t <= ns; ++t) {
       const int tt = std::min(t, ns - 1);
       if (once)

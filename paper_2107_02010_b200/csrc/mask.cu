@@ -167,7 +167,10 @@ __global__ void block_bounds_kernel(const float4* cy, const float* ry, const flo
 // kept pair, so no diagonal either) scans every word for the exact arg-max,
 // evaluating the float64 slack where the float32 upper bound reaches the
 // lane's best so far.
-constexpr int kMaskThreads = 256;
+// 2 warps per row cluster: rows finish at very different times (their kept
+// words vary), small CTAs keep the SMs full (C3 mask phase: 256 threads 34 ms,
+// 128: 31 ms, 64: 30 ms)
+constexpr int kMaskThreads = 64;
 
 __global__ void __launch_bounds__(kMaskThreads)
 mask_rows_kernel(MaskIn m, const float4* blk, const float* blkg, double thr, int self,

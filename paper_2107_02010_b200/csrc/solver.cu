@@ -2053,8 +2053,7 @@ int msot_sinkhorn(msot_ctx* c, const msot_params* prm, const double* x, const do
   return guard([&] {
     if (!c || !prm || !x || !a || !y || !b || !loss_out) raise(MSOT_EUSAGE, "null argument");
     if (n < 1 || m < 1) raise(MSOT_EDATA, "empty measure");
-    check_weights(a, n);
-    check_weights(b, m);
+    // weights and points are validated on the device (solve_device)
     CK(cudaSetDevice(c->device));
     msot_stats local{};
     msot_stats* S = stats ? stats : &local;

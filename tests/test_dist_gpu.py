@@ -87,7 +87,7 @@ def _worker(rank, world, port, case, q):
         q.put((rank, "error", traceback.format_exc()))
 
 
-def run_two_ranks(case, timeout=300):
+def run_two_ranks(case, timeout=300, world=2):
     """Rank results {rank: (loss, potentials, world)}; raises with the worker
     traceback on failure and never leaves a worker behind."""
     import queue
@@ -95,13 +95,13 @@ def run_two_ranks(case, timeout=300):
     mpc = mp.get_context("spawn")
     q = mpc.Queue()
     port = _free_port()
-    procs = [mpc.Process(target=_worker, args=(r, 2, port, case, q), daemon=True)
-             for r in range(2)]
+    procs = [mpc.Process(target=_worker, args=(r, world, port, case, q), daemon=True)
+             for r in range(world)]
     for p in procs:
         p.start()
     out = {}
     try:
-        while len(out) < 2:
+        while len(out) < world:
             rank, status, payload = q.get(timeout=timeout)
             if status != "ok":
                 raise AssertionError(f"rank {rank} failed:\n{payload}")
@@ -134,6 +134,22 @@ def test_two_ranks_match_one(ctx, case):
                 # partials), compounded over the eps schedule; masks follow
                 assert np.abs(u - v).max() <= 1e-3 * eps
         assert abs(l2 - l1) <= 1e-6 * abs(l1) + 1e-12
+
+
+@pytest.mark.parametrize("case", ["multiscale", "hd_ms"])
+def test_three_ranks_match_one(ctx, case):
+    """Uneven shards: three ranks (row tiles, mask rows and broadcast blocks
+    split 3 ways)."""
+    x, a, y, b = _inputs(case)
+    l1, p1, _ = ctx.sinkhorn(_params(case), x, a, y, b)
+    out = run_two_ranks(case, world=3)
+    eps = _params(case).blur ** 2
+    for rank in range(3):
+        l3, p3, world = out[rank]
+        assert world == 3
+        for u, v in zip(p3, [p1.a_xx, p1.b_yy, p1.a_xy, p1.b_yx]):
+            assert np.abs(u - v).max() <= 1e-3 * eps
+        assert abs(l3 - l1) <= 1e-6 * abs(l1) + 1e-12
 
 
 if __name__ == "__main__":

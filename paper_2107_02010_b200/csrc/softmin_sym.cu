@@ -72,7 +72,10 @@ static_assert(kSymRows == 4, "softmin_sym_kernel is written for 4 rows per threa
 // kUni: every row weight equal and lambda = 1, so the row factor is one
 // constant per CTA, applied at the column write-out (the column partial of a
 // column pair is the packed sum of the 4 rows' terms).
-template <int D, int kPoly16, bool kUni>
+// (All exponentials on the MUFU: moving 2/16 of them to the FMA pipe, which
+// pays +1.4% in the row-wise softmin_kernel, costs 8% here — the FMA pipe
+// carries the column sums.)
+template <int D, bool kUni>
 __global__ void __launch_bounds__(kSymThreads)
 softmin_sym_kernel(const __grid_constant__ Group G) {
   __shared__ __align__(16) float smem[2][kSymCols * 4];
@@ -180,10 +183,7 @@ softmin_sym_kernel(const __grid_constant__ Group G) {
         float2 e[kSymRows];
 #pragma unroll
         for (int q = 0; q < kSymRows; ++q) {
-          if (poly_slot((kSymRows * k + q) & 15, kPoly16))
-            e[q] = pair_terms<D, true>(rs[q], Y0, Y1, Y2, C);
-          else
-            e[q] = pair_terms<D, false>(rs[q], Y0, Y1, Y2, C);
+          e[q] = pair_terms<D, false>(rs[q], Y0, Y1, Y2, C);
           sum[q] = __fadd2_rn(sum[q], e[q]);
         }
         float2 cp;
@@ -324,22 +324,10 @@ __global__ void softmin_fallback_dense(const __grid_constant__ Group G) {
   }
 }
 
-static int poly16_sym() {
-  static const int v = [] {
-    const char* e = getenv("MSOT_POLY16_SYM");
-    return e ? atoi(e) : 0;  // the FMA pipe carries the column sums here
-  }();
-  return v;
-}
-
 template <int D, bool kUni>
 static void launch_sym_d(const Group& g, cudaStream_t st) {
   ++g_launches;
-  dim3 grid(g.n_items), block(kSymThreads);
-  switch (poly16_sym()) {
-    case 2: softmin_sym_kernel<D, 2, kUni><<<grid, block, 0, st>>>(g); break;
-    default: softmin_sym_kernel<D, 0, kUni><<<grid, block, 0, st>>>(g); break;
-  }
+  softmin_sym_kernel<D, kUni><<<g.n_items, kSymThreads, 0, st>>>(g);
 }
 
 cudaError_t launch_softmin_sym(const Group& g, int d, bool uniform, cudaStream_t st) {

@@ -248,6 +248,18 @@ def main():
     # roofline of the dominant kernel: softmin launches timed with events
     ctx.set_profiling(True)
     _, pst = solve()
+    # north star's dense-softmin bar (>= 60% of the MUFU roofline on one GPU):
+    # the C1 configuration (10k vs 10k uniform 3D, blur 0.05, dense), solved
+    # on the same context with its softmin launches event-timed
+    dense = None
+    if world == 1:
+        rng1, rng2 = np.random.default_rng(1), np.random.default_rng(2)
+        xc, yc = rng1.random((10000, 3)), rng2.random((10000, 3))
+        wc = np.full(10000, 1e-4)
+        from paper_2107_02010_b200.abi import make_params
+        for _ in range(2):
+            _, _, dst = ctx.sinkhorn(make_params(blur=0.05), xc, wc, yc, wc, potentials=False)
+        dense = dst
     ctx.set_profiling(False)
     ex2_rate = ctx.probe_ex2()
 
@@ -303,6 +315,11 @@ def main():
                      "share_of_step": pst["softmin_ms"] / max(pst["total_ms"], 1e-9)},
         "clocks": clk.summary(),
         "fallback_rows": st["fallback_rows"],
+        "dense_softmin_c1": None if dense is None else {
+            "config": "C1: 10k vs 10k uniform 3D, blur 0.05, dense eps-scaling (row-wise softmin_kernel)",
+            "pairs_per_s": dense["pairs_evaluated"] / (dense["softmin_ms"] * 1e-3),
+            "frac_of_mufu_peak": dense["pairs_evaluated"] / (dense["softmin_ms"] * 1e-3) / ex2_rate,
+            "solve_ms": dense["total_ms"]},
     }
     if not args.no_cpu:
         rows = 8192  # ~10 s of the oracle on 16 host threads

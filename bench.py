@@ -135,6 +135,46 @@ def l2_flush(buf):
         buf.add_(1.0)
 
 
+def free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def spawn_ranks(n, argv):
+    """`bench.py --gpus N` run without torchrun: one process per GPU, launched
+    here with the torchrun environment (RANK, LOCAL_RANK, WORLD_SIZE,
+    MASTER_ADDR=127.0.0.1, MASTER_PORT); rank 0's stdout is passed through
+    (the JSON line), the others' is discarded.  Returns the worst exit code."""
+    port = free_port()
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + argv, env=env,
+                                      stdout=None if r == 0 else subprocess.DEVNULL))
+    rcs = [p.wait() for p in procs]
+    return max(rcs, key=abs)
+
+
+def dist_probe(args):
+    """--dist-probe (dev/test): the rendezvous, the max-over-ranks timing
+    reduction and the rank-0-only JSON line of a self-spawned run, on gloo
+    (no GPU): each rank 'times' rank+1 ms, rank 0 prints the max."""
+    import torch
+    import torch.distributed as dist
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    dist.init_process_group("gloo")
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"n_gpus": world, "ms_per_step": float(t[0]),
+                          "ranks_seen": dist.get_world_size()}), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -146,7 +186,14 @@ def main():
     ap.add_argument("--host-collectives", action="store_true",
                     help="dev only: every rank on cuda:0, exchanges through gloo via "
                          "msot_create_dist_host (exercises the N>1 path on one GPU)")
+    ap.add_argument("--dist-probe", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU without torchrun (the driver may launch either way)
+        sys.exit(spawn_ranks(args.gpus, sys.argv[1:]))
+    if args.dist_probe:
+        return dist_probe(args)
 
     w = dict(WORKLOAD)
     if args.n:
@@ -182,6 +229,12 @@ def main():
         ctx = Context(local, rank, world, idbuf[0])
     else:
         ctx = Context(local)
+    r_, w_, nr_ = ctx.world_info()
+    print(f"[msot] rank {r_}/{w_}: device {local}, communicator nranks {nr_} "
+          f"({'host-staged gloo' if args.host_collectives else 'ncclCommCount'})",
+          file=sys.stderr, flush=True)
+    if w_ != world or nr_ != world:
+        raise RuntimeError(f"communicator has {nr_} ranks, expected {world}")
 
     x, a, y, b = make_inputs(w)
     prm = params(w)

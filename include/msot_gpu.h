@@ -121,6 +121,24 @@ int msot_create(int device, msot_ctx** out);
 int msot_nccl_unique_id(unsigned char out[128]);
 int msot_create_dist(int device, int rank, int world, const unsigned char nccl_id[128],
                      msot_ctx** out);
+
+/* Parity seam (tests): for the next solves on this context, copy the four
+ * potentials (a_xx[n], b_yy[m], a_xy[m], b_yx[n], caller order, raw gauge)
+ * before and after the update of schedule index `scale` (0..n_scales; the
+ * final assignment is n_scales) into the given host buffers (entries may be
+ * NULL).  Captured on fine-phase and dense 3-D updates; scale < 0 disables. */
+int msot_debug_capture(msot_ctx* ctx, int scale, double* const in[4], double* const out[4]);
+
+/* Parity seam (tests): the cluster mask of the captured multiscale update
+ * (which: 0 = x-x, 1 = y-y, 2 = x-y; unpacked k_rows x k_cols bytes, 1 =
+ * kept) and the cluster of every row / column atom in caller order.  Call
+ * with NULL buffers to read the sizes. */
+int msot_debug_mask(const msot_ctx* ctx, int which, int32_t* k_rows, int32_t* k_cols,
+                    uint8_t* mask, int32_t* row_cluster, int32_t* col_cluster);
+
+/* Rank, world size and the rank count of the context's communicator as NCCL
+ * reports it (ncclCommCount; 1 without one, world for the host seam). */
+int msot_world_info(const msot_ctx* ctx, int* rank, int* world, int* comm_ranks);
 /* Test seam: the same sharded solve with host-staged collectives supplied by
  * the caller (e.g. torch.distributed gloo) in place of NCCL, so the
  * multi-rank logic runs with several processes on one GPU.  allreduce sums
@@ -142,7 +160,7 @@ int msot_probe_ex2(msot_ctx* ctx, double* ex2_per_s);
 /* --- host-side helpers shared with the oracle (no GPU work) ------------- */
 
 /* make_schedule: writes n sigmas/eps/lambdas, returns n
- * (or a negative status).  n = floor(log(d/blur)/log(1/q)) + 1, sigma_t =
+ * (-n when cap < n; 0 for invalid parameters: reach must be > 0 or +inf).  n = floor(log(d/blur)/log(1/q)) + 1, sigma_t =
  * d q^t for t < n-1 and sigma_{n-1} = blur. */
 int msot_schedule(double diameter, const msot_params* p, double* sigma, double* eps,
                   double* lam, int cap);

@@ -733,7 +733,8 @@ int oracle_sinkhorn(const msot_params* prm, const double* x, const double* a, in
                     double* b_yy, double* a_xy, double* b_yx, double* loss_out,
                     msot_stats* st) {
   if (n < 1 || m < 1 || d < 1) return fail(MSOT_EDATA, "empty measure");
-  if (!(prm->blur > 0) || !(prm->scaling > 0 && prm->scaling < 1) || !(prm->p >= 1 && prm->p <= 2))
+  if (!(prm->blur > 0) || !(prm->scaling > 0 && prm->scaling < 1) || !(prm->p >= 1 && prm->p <= 2) ||
+      !msot_reach_valid(prm->reach))
     return fail(MSOT_EUSAGE, "invalid solver parameters");
   for (int64_t i = 0; i < n; ++i)
     if (!(a[i] > 0)) return fail(MSOT_EDATA, "weights must be > 0");
@@ -1266,8 +1267,10 @@ int oracle_barycenter(const msot_params* prm, const double* x0, const double* a,
   if (rc != MSOT_OK) return rc;
   if (loss_traj) loss_traj[0] = L;
   int done = 0;
-  double s = step;
   while (done < iters) {
+    // each iteration starts from the configured step; the
+    // halvings of a rejected trial apply to that iteration only
+    double s = step;
     bool accepted = false;
     double Ln = L;
     for (int h = 0; h <= 10; ++h) {

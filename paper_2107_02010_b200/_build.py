@@ -18,7 +18,7 @@ BUILD = os.path.join(HERE, "_obj")
 LIB = os.path.join(HERE, "libmsot_b200.so")
 
 SOURCES = ["softmin.cu", "softmin_sym.cu", "softmin_hd.cu", "prims.cu", "cluster.cu", "mask.cu", "loss.cu", "labels.cu", "kmeans.cu",
-           "probe.cu", "solver.cu", "frontend.cpp", "exact_ot.cpp"]
+           "probe.cu", "solver.cu", "frontend.cpp", "exact_ot.cpp", "host_runtime.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",

@@ -318,6 +318,15 @@ int cmd_barycenter(const Args& a) {
   if (a.pos.empty()) throw Usage("barycenter needs at least one density file");
   std::vector<msot::DensityMap> maps;
   for (const auto& f : a.pos) maps.push_back(read_density(f));
+  // the average is taken voxel by voxel: every map must share maps[0]'s grid
+  // (inconsistent inputs are a data error, exit 3)
+  for (std::size_t q = 1; q < maps.size(); ++q) {
+    const msot::DensityMap &m0 = maps[0], &mq = maps[q];
+    if (mq.nx != m0.nx || mq.ny != m0.ny || mq.nz != m0.nz || mq.voxel_mm != m0.voxel_mm ||
+        mq.origin != m0.origin)
+      throw msot::DataError(a.pos[q] + ": density grid differs from " + a.pos[0] +
+                            " (dimensions, voxel size and origin must match)");
+  }
   std::vector<msot::DiscreteMeasure> targets;
   for (const auto& m : maps) targets.push_back(msot::density_to_measure(m));
   // init: arithmetic average of the maps, upsampled with jitter

@@ -76,10 +76,19 @@ struct Group {
   int32_t n_problems;
   int32_t tile_prefix[kMaxProblems + 1];  // finalized tiles per problem (prefix)
   int32_t t0[kMaxProblems];               // first tile this rank finalizes
+  int32_t* bad_scale;     // first scale that produced a non-finite potential
+  int32_t scale;          // index of this launch group's scale
 };
 
 // Kernel launches issued by this thread (reported as stats.gpu_launches).
 extern thread_local int64_t g_launches;
+
+// Writes an updated potential; a non-finite value records the group's scale
+// (atomicMin: the first failing scale is reported).
+__device__ __forceinline__ void store_potential(const Group& G, float* out, int32_t r, float v) {
+  out[r] = v;
+  if (!isfinite(v) && G.bad_scale) atomicMin(G.bad_scale, G.scale);
+}
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;

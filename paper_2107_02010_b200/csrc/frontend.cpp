@@ -150,6 +150,7 @@ DiscreteMeasure density_to_measure(const DensityMap& d) {
 // -------------------------------------------------------------------- solver
 msot_params SolverParams::to_c() const {
   cost.validate();
+  if (!(reach > 0.0)) throw DataError("SolverParams: reach must be > 0 (or +inf)");
   msot_params p;
   msot_params_default(&p);
   p.blur = blur;
@@ -268,7 +269,10 @@ double divergence(const DiscreteMeasure& a, const DiscreteMeasure& b, const Solv
 }
 
 // ------------------------------------------------------------ implicit plan
-static bool reach_inf(const SolverParams& p) { return !(p.reach > 0.0) || std::isinf(p.reach); }
+static bool reach_inf(const SolverParams& p) {
+  if (!(p.reach > 0.0)) throw DataError("SolverParams: reach must be > 0 (or +inf)");
+  return std::isinf(p.reach);
+}
 
 double plan_entry(std::size_t i, std::size_t j, const DiscreteMeasure& a,
                   const DiscreteMeasure& b, const DualPotentials& duals,

@@ -43,7 +43,10 @@ extern "C" {
 /* Cube ids are Morton-interleaved with this many bits per axis (D <= 3). */
 #define MSOT_MORTON_BITS 10
 
-static inline int msot_reach_is_inf(double reach) { return !(reach > 0.0) || isinf(reach); }
+/* reach = +inf is the only encoding of balanced OT; callers validate with
+ * msot_reach_valid first (reach > 0 or inf). */
+static inline int msot_reach_valid(double reach) { return reach > 0.0; }
+static inline int msot_reach_is_inf(double reach) { return isinf(reach) && reach > 0.0; }
 
 /* lambda = 1 / (1 + eps/rho), rho = reach^p. */
 static inline double msot_lambda(double eps, const msot_params* p) {

@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(kTileRows) softmin_finalize(const __grid_const
     if (slot < G.fb_cap) G.fb_list[slot] = make_int4(p, r, t, 0);
     return;
   }
-  P.row_out[r] = est - P.mixw * P.lam_eps * logf(s);
+  store_potential(G, P.row_out, r, est - P.mixw * P.lam_eps * logf(s));
 }
 
 // Exact online-max LSE for the rows the fixed-reference path rejected: one
@@ -319,7 +319,7 @@ __global__ void softmin_fallback(const __grid_constant__ Group G) {
     if (lane == 0) {
       const float est = P.row_est ? P.row_est[r] : 0.f;
       const float ft = -P.lam_eps * kLn2 * (m + log2f(s));
-      P.row_out[r] = (1.f - P.mixw) * est + P.mixw * ft;
+      store_potential(G, P.row_out, r, (1.f - P.mixw) * est + P.mixw * ft);
     }
   }
 }

@@ -586,7 +586,7 @@ __global__ void softmin_hd_fallback(const __grid_constant__ Group G, int d) {
     if (lane == 0) {
       const float est = P.row_est ? P.row_est[r] : 0.f;
       const float ft = -P.lam_eps * kLn2 * (m + log2f(s));
-      P.row_out[r] = (1.f - P.mixw) * est + P.mixw * ft;
+      store_potential(G, P.row_out, r, (1.f - P.mixw) * est + P.mixw * ft);
     }
   }
 }

@@ -265,7 +265,7 @@ __global__ void sym_colfinal_kernel(const __grid_constant__ Group G, int p) {
   const float s = P.row_add[r];
   const float est = P.row_est ? P.row_est[r] : 0.f;
   if (P.row_lw2 && P.row_lw2[r] == -INFINITY) {  // zero-weight atom (padding): no update
-    P.row_out[r] = est;
+    store_potential(G, P.row_out, r, est);
     return;
   }
   if (!(s >= 8.67361738e-19f && s <= 1.2676506e30f)) {
@@ -274,7 +274,7 @@ __global__ void sym_colfinal_kernel(const __grid_constant__ Group G, int p) {
     if (slot < G.fb_cap) G.fb_list[slot] = make_int4(p, r, -1, 0);
     return;
   }
-  P.row_out[r] = est - P.mixw * P.lam_eps * logf(s);
+  store_potential(G, P.row_out, r, est - P.mixw * P.lam_eps * logf(s));
 }
 
 cudaError_t launch_colfinal(const Group& g, int p, cudaStream_t st) {
@@ -319,7 +319,7 @@ __global__ void softmin_fallback_dense(const __grid_constant__ Group G) {
     if (lane == 0) {
       const float est = P.row_est ? P.row_est[r] : 0.f;
       const float ft = -P.lam_eps * kLn2 * (m + log2f(s));
-      P.row_out[r] = (1.f - P.mixw) * est + P.mixw * ft;
+      store_potential(G, P.row_out, r, (1.f - P.mixw) * est + P.mixw * ft);
     }
   }
 }

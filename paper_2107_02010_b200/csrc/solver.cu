@@ -94,6 +94,14 @@ struct msot_ctx {
   int self_mode = 0;
   float* self_axx = nullptr;    // [n] caller order
   float4* self_pay = nullptr;   // [n] caller order
+  // parity seam (msot_debug_capture): the four potentials before and after
+  // the update of scale `cap_scale`, in the caller's order (host buffers)
+  int cap_scale = -1;
+  double* cap_in[4] = {nullptr, nullptr, nullptr, nullptr};
+  double* cap_out[4] = {nullptr, nullptr, nullptr, nullptr};
+  std::vector<uint8_t> cap_mask[3];     // xx, yy, xy cluster masks of that update
+  int32_t cap_k[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+  std::vector<int32_t> cap_lab[2];      // cluster of every atom of x / y (caller order)
   std::map<std::string, std::pair<void*, size_t>> bufs;
   std::vector<cudaEvent_t> ev;  // profiling events (pairs)
   size_t ev_used = 0;
@@ -606,6 +614,8 @@ struct SolveState {
   int32_t* fb_total;
   int4* fb_list;
   int32_t fb_cap;
+  int32_t* bad_scale = nullptr;  // device: first scale with a non-finite potential
+  int scale = 0;                 // scale index of the next launch group
 };
 
 void run_group(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& ss) {
@@ -652,6 +662,8 @@ void run_group(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& ss) {
   G.fb_total = ss.fb_total;
   G.fb_list = ss.fb_list;
   G.fb_cap = ss.fb_cap;
+  G.bad_scale = ss.bad_scale;
+  G.scale = ss.scale;
   CK(cudaMemsetAsync(ss.fb_count, 0, sizeof(int32_t), st));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c->profiling) {
@@ -758,6 +770,8 @@ void run_group_sym(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& s
   G.fb_total = ss.fb_total;
   G.fb_list = ss.fb_list;
   G.fb_cap = ss.fb_cap;
+  G.bad_scale = ss.bad_scale;
+  G.scale = ss.scale;
   CK(cudaMemsetAsync(ss.fb_count, 0, sizeof(int32_t), st));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c->profiling) {
@@ -826,6 +840,47 @@ void alloc_pots(msot_ctx* c, const std::string& tag, int64_t n, int64_t m, Poten
     CK(cudaMemsetAsync(P.v[b][1], 0, m * sizeof(float), c->st));
     CK(cudaMemsetAsync(P.v[b][2], 0, m * sizeof(float), c->st));
     CK(cudaMemsetAsync(P.v[b][3], 0, n * sizeof(float), c->st));
+  }
+}
+
+// msot_debug_capture: copies the potentials v (a_xx, b_yy, a_xy, b_yx in
+// the solver's sorted order) to the caller's host buffers in caller order.
+void capture_pots(msot_ctx* c, float* const* v, const int32_t* xperm, const int32_t* yperm,
+                  int64_t n, int64_t m, double* const* host) {
+  const int64_t len[4] = {n, m, m, n};
+  const int32_t* perm[4] = {xperm, yperm, yperm, xperm};
+  double* tmp = c->buf<double>("cap.tmp", std::max(n, m));
+  for (int q = 0; q < 4; ++q) {
+    if (!host[q]) continue;
+    CK(scatter_unsort(v[q], perm[q], len[q], nullptr, 0.0, tmp, c->st));
+    CK(cudaMemcpyAsync(host[q], tmp, len[q] * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+  }
+}
+
+// msot_debug_capture: the cluster masks of the captured update (unpacked)
+// and the cluster of every atom in caller order (msot_debug_mask).
+void capture_masks(msot_ctx* c, const uint32_t* const* masks, const int32_t* kr,
+                   const int32_t* kc, const DMeasure& X, const DMeasure& Y) {
+  cudaStream_t st = c->st;
+  for (int q = 0; q < 3; ++q) {
+    const size_t cells = size_t(kr[q]) * kc[q];
+    uint8_t* dm = c->buf<uint8_t>("cap.mask", cells);
+    CK(unpack_mask(masks[q], kr[q], kc[q], dm, st));
+    c->cap_mask[q].resize(cells);
+    CK(cudaMemcpyAsync(c->cap_mask[q].data(), dm, cells, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    c->cap_k[q][0] = kr[q];
+    c->cap_k[q][1] = kc[q];
+  }
+  const DMeasure* M[2] = {&X, &Y};
+  for (int s = 0; s < 2; ++s) {
+    std::vector<int32_t> lab(M[s]->n), perm(M[s]->n);
+    CK(cudaMemcpyAsync(lab.data(), M[s]->labels, M[s]->n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(perm.data(), M[s]->perm, M[s]->n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    c->cap_lab[s].assign(M[s]->n, -1);
+    for (int64_t k = 0; k < M[s]->n; ++k) c->cap_lab[s][perm[k]] = lab[k];
   }
 }
 
@@ -1096,6 +1151,7 @@ void hd_multiscale(msot_ctx* c, const msot_params* prm, const double* d_x, const
     build_plan(c, "hpc", Pc, 2);
     const double cfull = double(kx) * kx + double(ky) * ky + 2.0 * double(kx) * ky;
     for (int t = 0; t < tsw; ++t) {
+      ss.scale = t;
       sym_step_once(c, Pc, Uc, ccur, eps[t], lam[t], false, ss, cc);
       S->pairs_dense += cfull;
     }
@@ -1184,6 +1240,7 @@ void hd_multiscale(msot_ctx* c, const msot_params* prm, const double* d_x, const
   };
   for (int t = tsw; t <= ns; ++t) {
     const int tt = std::min(t, ns - 1);
+    ss.scale = t;
     const bool rebuild =
         (t == tsw) || (prm->retruncate > 0 && t < ns && (t - tsw) % prm->retruncate == 0);
     if (rebuild) {
@@ -1336,6 +1393,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
   if (!(prm->blur > 0) || !(prm->scaling > 0 && prm->scaling < 1))
     raise(MSOT_EUSAGE, "invalid blur/scaling");
   if (prm->p != 2.0) raise(MSOT_EUSAGE, "the GPU path implements p = 2");
+  if (!msot_reach_valid(prm->reach)) raise(MSOT_EUSAGE, "reach must be > 0 (or +inf for balanced OT)");
   cudaStream_t st = c->st;
   const int64_t launches0 = g_launches;
   double frame[3] = {0.0, 0.0, 0.0};  // centre of the float32 atom frame (voxel path)
@@ -1381,6 +1439,8 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
   ss.fb_cap = static_cast<int32_t>(std::min<int64_t>(2 * (n + m), 1 << 22));
   ss.fb_list = c->buf<int4>("fb.list", ss.fb_cap);
   CK(cudaMemsetAsync(ss.fb_total, 0, sizeof(int32_t), st));
+  ss.bad_scale = c->buf<int32_t>("bad.scale", 1);
+  CK(cudaMemsetAsync(ss.bad_scale, 0x7f, sizeof(int32_t), st));  // 0x7f7f7f7f: none
 
   Potentials U;
   alloc_pots(c, "pot", n, m, U);
@@ -1464,6 +1524,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
     build_plan(c, "ph", P, 2);
     for (int t = 0; t <= ns; ++t) {
       const int tt = std::min(t, ns - 1);
+      ss.scale = t;
       if (once)
         sym_step_once(c, P, U, cur, eps[tt], lam[tt], t == ns, ss, hcol);
       else
@@ -1507,7 +1568,11 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
     build_plan(c, "pd", P);
     for (int t = 0; t <= ns; ++t) {
       const int tt = std::min(t, ns - 1);
+      ss.scale = t;
+      const bool cap = t == c->cap_scale;
+      if (cap) capture_pots(c, U.v[cur], X.perm, Y.perm, n, m, c->cap_in);
       sym_step(c, P, U, cur, eps[tt], lam[tt], t == ns, ss);
+      if (cap) capture_pots(c, U.v[cur], X.perm, Y.perm, n, m, c->cap_out);
       S->pairs_dense += full;
     }
   } else {
@@ -1559,6 +1624,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
         build_plan(c, "p" + tg, Pc);
         const double cfull = double(kx) * kx + double(ky) * ky + 2.0 * double(kx) * ky;
         for (int t = t0; t < t1; ++t) {
+          ss.scale = t;
           if (conce)
             sym_step_once(c, Pc, Uq, qcur, eps[t], lam[t], false, ss, ccol);
           else
@@ -1762,6 +1828,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
     };
     for (int t = tsw; t <= ns; ++t) {
       const int tt = std::min(t, ns - 1);
+      ss.scale = t;
       const bool rebuild =
           (t == tsw) || (prm->retruncate > 0 && t < ns && (t - tsw) % prm->retruncate == 0);
       if (rebuild) {
@@ -1769,10 +1836,18 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
         build_masks(eps[tt]);
       }
       c->mark(4);
+      const bool cap = t == c->cap_scale;
+      if (cap) capture_pots(c, U.v[cur], X.perm, Y.perm, n, m, c->cap_in);
       if (once)
         sym_step_once(c, Pf, U, cur, eps[tt], lam[tt], t == ns, ss, scol);
       else
         sym_step(c, Pf, U, cur, eps[tt], lam[tt], t == ns, ss);
+      if (cap) {
+        capture_pots(c, U.v[cur], X.perm, Y.perm, n, m, c->cap_out);
+        const uint32_t* mk[3] = {mxx, myy, mxy};
+        const int32_t kr[3] = {X.k, Y.k, X.k}, kc[3] = {X.k, Y.k, Y.k};
+        capture_masks(c, mk, kr, kc, X, Y);
+      }
       S->pairs_dense += full;
       S->pairs_fine += Pf.pairs_all;
       S->pairs_fine_dense += full;
@@ -1838,6 +1913,8 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
   int32_t fbt = 0;
   CK(cudaMemcpyAsync(res, lout, sizeof(res), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(&fbt, ss.fb_total, sizeof(fbt), cudaMemcpyDeviceToHost, st));
+  int32_t bad = 0x7f7f7f7f;
+  CK(cudaMemcpyAsync(&bad, ss.bad_scale, sizeof(bad), cudaMemcpyDeviceToHost, st));
   if (h_pots) {
     double* tmp = c->buf<double>("unsort", std::max(n, m));
     const int64_t len[4] = {nr, mr, mr, nr};   // internal rows (padding skipped by perm < 0)
@@ -1877,6 +1954,12 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
   S->fallback_rows = fbt;
   S->gpu_launches = g_launches - launches0;
   S->d2h_bytes += sizeof(res);
+  if (bad != 0x7f7f7f7f) {  // NumericError naming the scale
+    const int t = std::min(bad, ns - 1);
+    raise(MSOT_ENUMERIC, "non-finite potential at scale " + std::to_string(bad) + " of " +
+                             std::to_string(ns) + (bad >= ns ? " (final update" : " (") +
+                             ", sigma = " + std::to_string(sig[t]) + ")");
+  }
   if (!std::isfinite(res[0])) raise(MSOT_ENUMERIC, "non-finite divergence");
   *loss_out = res[0];
 }
@@ -1906,6 +1989,10 @@ void msot_params_default(msot_params* p) {
 
 int msot_schedule(double diameter, const msot_params* p, double* sigma, double* eps, double* lam,
                   int cap) {
+  if (!msot_reach_valid(p->reach)) {  // 0 = invalid parameters (n >= 1 otherwise)
+    g_err = "reach must be > 0 (or +inf for balanced OT)";
+    return 0;
+  }
   const int n = msot_schedule_len(diameter, p->blur, p->scaling);
   if (n > cap) return -n;
   for (int t = 0; t < n; ++t) {
@@ -1978,6 +2065,46 @@ int msot_create_dist(int device, int rank, int world, const unsigned char nccl_i
       delete c;
       *out = nullptr;
       throw;
+    }
+  });
+}
+
+int msot_debug_capture(msot_ctx* c, int scale, double* const in[4], double* const out[4]) {
+  return guard([&] {
+    if (!c) raise(MSOT_EUSAGE, "null context");
+    c->cap_scale = scale;
+    for (int q = 0; q < 4; ++q) {
+      c->cap_in[q] = scale >= 0 && in ? in[q] : nullptr;
+      c->cap_out[q] = scale >= 0 && out ? out[q] : nullptr;
+    }
+  });
+}
+
+int msot_debug_mask(const msot_ctx* c, int which, int32_t* k_rows, int32_t* k_cols,
+                    uint8_t* mask, int32_t* row_cluster, int32_t* col_cluster) {
+  return guard([&] {
+    if (!c || which < 0 || which > 2) raise(MSOT_EUSAGE, "invalid mask request");
+    if (c->cap_mask[which].empty()) raise(MSOT_EUSAGE, "no mask captured");
+    if (k_rows) *k_rows = c->cap_k[which][0];
+    if (k_cols) *k_cols = c->cap_k[which][1];
+    if (mask) std::memcpy(mask, c->cap_mask[which].data(), c->cap_mask[which].size());
+    const std::vector<int32_t>& rl = c->cap_lab[which == 1 ? 1 : 0];
+    const std::vector<int32_t>& cl = c->cap_lab[which == 0 ? 0 : 1];
+    if (row_cluster) std::copy(rl.begin(), rl.end(), row_cluster);
+    if (col_cluster) std::copy(cl.begin(), cl.end(), col_cluster);
+  });
+}
+
+int msot_world_info(const msot_ctx* c, int* rank, int* world, int* comm_ranks) {
+  return guard([&] {
+    if (!c) raise(MSOT_EUSAGE, "null context");
+    if (rank) *rank = c->rank;
+    if (world) *world = c->world;
+    if (comm_ranks) {
+      int n = c->world > 1 ? 0 : 1;  // no communicator at world 1
+      if (c->comm) NK(ncclCommCount(c->comm, &n));
+      else if (c->host_ar) n = c->world;  // host-collective test seam
+      *comm_ranks = n;
     }
   });
 }
@@ -2292,8 +2419,10 @@ int msot_barycenter(msot_ctx* c, const msot_params* prm, const double* x0, const
     if (!std::isfinite(L)) raise(MSOT_ENUMERIC, "non-finite barycenter loss at iteration 0");
     if (loss_traj) loss_traj[0] = L;
     int done = 0;
-    double s = step;
     while (done < iters) {
+      // each iteration starts from the configured step; the
+      // halvings of a rejected trial apply to that iteration only
+      double s = step;
       bool accepted = false;
       double Ln = L;
       for (int h = 0; h <= 10; ++h) {

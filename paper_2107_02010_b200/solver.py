@@ -48,6 +48,9 @@ def lib():
                                        C.POINTER(C.c_void_p)]
         L.msot_create_dist_host.argtypes = [C.c_int, C.c_int, C.c_int, _AR_FN, _BC_FN, C.c_void_p,
                                             C.POINTER(C.c_void_p)]
+        L.msot_world_info.argtypes = [C.c_void_p, _ip, _ip, _ip]
+        L.msot_debug_mask.argtypes = [C.c_void_p, C.c_int, _ip, _ip, _bp, _ip, _ip]
+        L.msot_debug_capture.argtypes = [C.c_void_p, C.c_int, C.POINTER(_dp), C.POINTER(_dp)]
         L.msot_destroy.argtypes = [C.c_void_p]
         L.msot_destroy.restype = None
         L.msot_set_profiling.argtypes = [C.c_void_p, C.c_int]
@@ -95,7 +98,8 @@ EXPORTS = ["msot_last_error", "msot_params_default", "msot_create", "msot_nccl_u
            "msot_shard_tiles", "msot_softmin", "msot_grid_cluster", "msot_truncation_mask",
            "msot_sinkhorn", "msot_sinkhorn_device", "msot_probe_ex2", "msot_sinkhorn_grad",
            "msot_barycenter", "msot_transfer_labels", "msot_resolve_flips", "msot_classify",
-           "msot_plan_apply", "msot_kmeans", "msot_create_dist_host", "msot_exact_ot"]
+           "msot_plan_apply", "msot_kmeans", "msot_create_dist_host", "msot_exact_ot",
+           "msot_world_info", "msot_debug_capture", "msot_debug_mask"]
 
 
 def _check(rc):
@@ -111,6 +115,46 @@ def _d(a):
     return a.ctypes.data_as(_dp)
 
 
+def _measures(x, a, y, b):
+    """Shape checks of a pair of measures before any ABI call: the C ABI reads
+    n (m) weights behind the caller's pointers, so a short array must be a
+    DataError here, not an out-of-bounds host read (msot::DiscreteMeasure
+    enforces the same on the C++ side, measure.hpp:26-37)."""
+    from .abi import DataError
+    x, a, y, b = _c64(x), _c64(a), _c64(y), _c64(b)
+    if x.ndim == 1:
+        x = x[:, None]
+    if y.ndim == 1:
+        y = y[:, None]
+    if x.ndim != 2 or y.ndim != 2:
+        raise DataError("points must be (N, D) arrays")
+    n, d = x.shape
+    m = y.shape[0]
+    if y.shape[1] != d:
+        raise DataError("dimension mismatch")
+    if a.ndim != 1 or a.size != n:
+        raise DataError(f"weights of x: expected {n} entries, got {a.size}")
+    if b.ndim != 1 or b.size != m:
+        raise DataError(f"weights of y: expected {m} entries, got {b.size}")
+    return x, a, y, b, n, m, d
+
+
+def _reach_inf(prm):
+    """reach = +inf is balanced OT; reach must otherwise be > 0."""
+    from .abi import UsageError
+    if not prm.reach > 0:
+        raise UsageError("reach must be > 0 (or +inf for balanced OT)")
+    return math.isinf(prm.reach)
+
+
+def _vec(v, size, what):
+    from .abi import DataError
+    v = _c64(v)
+    if v.ndim != 1 or v.size != size:
+        raise DataError(f"{what}: expected {size} entries, got {v.size}")
+    return v
+
+
 def default_params(**kw):
     return make_params(**kw)
 
@@ -119,6 +163,9 @@ def make_schedule(diameter, prm):
     cap = 100000
     s, e, l = (np.zeros(cap) for _ in range(3))
     n = lib().msot_schedule(diameter, C.byref(prm), _d(s), _d(e), _d(l), cap)
+    if n <= 0:
+        from .abi import UsageError
+        raise UsageError(lib().msot_last_error().decode() if n == 0 else "schedule too long")
     return s[:n].copy(), e[:n].copy(), l[:n].copy()
 
 
@@ -186,7 +233,7 @@ def grad_weights(prm, a, b, duals):
     finite reach, b_yx - a_xx + eps (sum a - sum b) for reach = inf (host)."""
     a, b = _c64(a), _c64(b)
     eps = duals.eps
-    if math.isinf(prm.reach) or prm.reach <= 0:
+    if _reach_inf(prm):
         return duals.b_yx - duals.a_xx + eps * (a.sum() - b.sum())
     rho = prm.reach ** prm.p
     return (rho + eps / 2) * (np.exp(-duals.a_xx / rho) - np.exp(-duals.b_yx / rho))
@@ -278,6 +325,38 @@ class Context:
         except Exception:
             pass
 
+    def world_info(self):
+        """(rank, world, ranks in the NCCL communicator per ncclCommCount)."""
+        r, w, n = C.c_int32(), C.c_int32(), C.c_int32()
+        _check(lib().msot_world_info(self._h, C.byref(r), C.byref(w), C.byref(n)))
+        return r.value, w.value, n.value
+
+    def debug_capture(self, scale, n, m):
+        """Arms the parity seam for schedule index `scale`: returns (before,
+        after) dicts of caller-order float64 arrays that the next solves fill;
+        scale < 0 disarms."""
+        if scale < 0:
+            _check(lib().msot_debug_capture(self._h, -1, None, None))
+            return None, None
+        keys, sizes = ("a_xx", "b_yy", "a_xy", "b_yx"), (n, m, m, n)
+        before = {k: np.full(s, np.nan) for k, s in zip(keys, sizes)}
+        after = {k: np.full(s, np.nan) for k, s in zip(keys, sizes)}
+        self._cap = ((_dp * 4)(*[_d(before[k]) for k in keys]),
+                     (_dp * 4)(*[_d(after[k]) for k in keys]), before, after)
+        _check(lib().msot_debug_capture(self._h, int(scale), self._cap[0], self._cap[1]))
+        return before, after
+
+    def debug_mask(self, which, n_rows, n_cols):
+        """The captured cluster mask (0 = x-x, 1 = y-y, 2 = x-y) as a (Kr, Kc)
+        uint8 array, plus the row / column atom -> cluster maps."""
+        kr, kc = C.c_int32(), C.c_int32()
+        _check(lib().msot_debug_mask(self._h, which, C.byref(kr), C.byref(kc), None, None, None))
+        mask = np.zeros((kr.value, kc.value), np.uint8)
+        rl, cl = np.zeros(n_rows, np.int32), np.zeros(n_cols, np.int32)
+        _check(lib().msot_debug_mask(self._h, which, None, None, mask.ctypes.data_as(_bp),
+                                     rl.ctypes.data_as(_ip), cl.ctypes.data_as(_ip)))
+        return mask, rl, cl
+
     def set_profiling(self, on=True):
         _check(lib().msot_set_profiling(self._h, int(bool(on))))
 
@@ -289,14 +368,10 @@ class Context:
 
     # -- SPEC.md:164-172
     def softmin(self, x, y, logw, h, eps, lam=1.0, f_est=None):
-        x, y, logw, h = _c64(x), _c64(y), _c64(logw), _c64(h)
-        if x.ndim == 1:
-            x = x[:, None]
-        if y.ndim == 1:
-            y = y[:, None]
-        n, d = x.shape
+        x, _, y, _, n, m, d = _measures(x, np.zeros(np.shape(x)[0]), y, np.zeros(np.shape(y)[0]))
+        logw, h = _vec(logw, m, "logw"), _vec(h, m, "h")
         out = np.zeros(n)
-        fe = None if f_est is None else _d(_c64(f_est))
+        fe = None if f_est is None else _d(_vec(f_est, n, "f_est"))
         _check(lib().msot_softmin(self._h, _d(x), n, _d(y), y.shape[0], d, _d(logw), _d(h),
                                   eps, lam, fe, _d(out)))
         return out
@@ -305,6 +380,8 @@ class Context:
     def grid_cluster(self, x, w, origin, cell):
         x, w, origin = _c64(x), _c64(w), _c64(origin)
         n, d = x.shape
+        w = _vec(w, n, "weights")
+        origin = _vec(origin, d, "origin")
         perm = np.zeros(n, np.int32)
         labels = np.zeros(n, np.int32)
         offsets = np.zeros(n + 1, np.int32)
@@ -326,6 +403,7 @@ class Context:
         if x.ndim == 1:
             x = x[:, None]
         n, d = x.shape
+        w = _vec(w, n, "weights")
         perm = np.zeros(n, np.int32)
         off = np.zeros(k + 1, np.int32)
         lab = np.zeros(n, np.int32)
@@ -358,16 +436,7 @@ class Context:
 
     # -- symmetric_sinkhorn / multiscale_sinkhorn + divergence
     def sinkhorn(self, prm, x, a, y, b, potentials=True):
-        x, a, y, b = _c64(x), _c64(a), _c64(y), _c64(b)
-        if x.ndim == 1:
-            x = x[:, None]
-        if y.ndim == 1:
-            y = y[:, None]
-        n, d = x.shape
-        m = y.shape[0]
-        if y.shape[1] != d:
-            from .abi import DataError
-            raise DataError("dimension mismatch")
+        x, a, y, b, n, m, d = _measures(x, a, y, b)
         loss = C.c_double()
         st = Stats()
         pots = None
@@ -386,12 +455,7 @@ class Context:
     # -- grad_positions
     def sinkhorn_grad(self, prm, x, a, y, b):
         """Returns (loss, grad_x (N x D), stats)."""
-        x, a, y, b = _c64(x), _c64(a), _c64(y), _c64(b)
-        if x.ndim == 1:
-            x = x[:, None]
-        if y.ndim == 1:
-            y = y[:, None]
-        n, d = x.shape
+        x, a, y, b, n, m, d = _measures(x, a, y, b)
         loss = C.c_double()
         st = Stats()
         g = np.zeros((n, d))
@@ -402,10 +466,14 @@ class Context:
     # -- barycenter
     def barycenter(self, prm, x0, a, targets, iters=10, step=1.0, tol=1e-4):
         """targets: list of (points, weights).  Returns (x, loss trajectory, stats)."""
-        x0, a = _c64(x0), _c64(a)
-        n, d = x0.shape
-        ys = [_c64(t[0]).reshape(-1, d) for t in targets]
-        bs = [_c64(t[1]) for t in targets]
+        if not targets:
+            from .abi import DataError
+            raise DataError("barycenter needs at least one target")
+        ys, bs = [], []
+        for t in targets:
+            x0, a, yt, bt, n, _, d = _measures(x0, a, t[0], t[1])
+            ys.append(yt)
+            bs.append(bt)
         k = len(targets)
         yp = (_dp * k)(*[_d(v) for v in ys])
         bp = (_dp * k)(*[_d(v) for v in bs])
@@ -423,13 +491,11 @@ class Context:
     def transfer_labels(self, prm, x, a, y, b, labels, n_classes=None):
         """Solves S(alpha, beta) and transfers the atlas labels of y to x.
         Returns (SoftLabels(scores N x L, row_mass N), loss, stats)."""
-        x, a, y, b = _c64(x), _c64(a), _c64(y), _c64(b)
-        if x.ndim == 1:
-            x = x[:, None]
-        if y.ndim == 1:
-            y = y[:, None]
-        n, d = x.shape
+        x, a, y, b, n, m, d = _measures(x, a, y, b)
         lab = np.ascontiguousarray(labels, dtype=np.int32)
+        if lab.ndim != 1 or lab.size != m:
+            from .abi import DataError
+            raise DataError(f"labels: expected {m} entries, got {lab.size}")
         L = int(lab.max()) + 1 if n_classes is None else int(n_classes)
         scores = np.zeros((n, L))
         mass = np.zeros(n)
@@ -443,12 +509,8 @@ class Context:
     # -- plan_apply
     def plan_apply(self, x, a, y, b, f, g, eps, v):
         """(pi v)_i = sum_j a_i b_j exp((f_i + g_j - C_ij)/eps) v_j on the GPU."""
-        x, a, y, b, f, g, v = map(_c64, (x, a, y, b, f, g, v))
-        if x.ndim == 1:
-            x = x[:, None]
-        if y.ndim == 1:
-            y = y[:, None]
-        n, d = x.shape
+        x, a, y, b, n, m, d = _measures(x, a, y, b)
+        f, g, v = _vec(f, n, "f"), _vec(g, m, "g"), _vec(v, m, "v")
         out = np.zeros(n)
         _check(lib().msot_plan_apply(self._h, _d(x), _d(a), n, _d(y), _d(b), y.shape[0], d,
                                      _d(f), _d(g), eps, _d(v), _d(out)))
@@ -461,7 +523,7 @@ class Context:
         eps = duals.eps
         f, g = duals.b_yx, duals.a_xy
         a, b = _c64(a), _c64(b)
-        if math.isinf(prm.reach) or prm.reach <= 0:
+        if _reach_inf(prm):
             mass = self.plan_apply(x, a, y, b, f, g, eps, np.ones(len(b))).sum()
             return float(a @ f + b @ g + eps * (a.sum() * b.sum() - mass))
         rho = prm.reach ** prm.p  # PAPER.md eq. 3

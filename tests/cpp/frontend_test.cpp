@@ -8,10 +8,16 @@
 #include <string>
 #include <vector>
 
+#include <atomic>
+#include <numeric>
+
 #include "msot/barycenter.hpp"
+#include "msot/common.hpp"
 #include "msot/exact.hpp"
 #include "msot/labels.hpp"
 #include "msot/measure.hpp"
+#include "msot/numeric.hpp"
+#include "msot/parallel.hpp"
 #include "msot/sinkhorn.hpp"
 
 static int failures = 0;
@@ -35,8 +41,36 @@ static bool throws(F&& f) {
   return false;
 }
 
+static void utility_checks() {
+  // the reference's utility headers (numeric.hpp:9-15, parallel.hpp:10-17)
+  using namespace msot;
+  std::vector<double> v(1000);
+  for (std::size_t i = 0; i < v.size(); ++i) v[i] = 1.0 / static_cast<double>(i + 1);
+  double serial = 0.0;
+  for (double q : v) serial += q;
+  CHECK(std::fabs(pairwise_sum(v) - serial) < 1e-12);
+  CHECK(std::fabs(kahan_sum(v) - serial) < 1e-12);
+  CHECK(pairwise_dot(v, std::vector<double>(1000, 2.0)) == 2.0 * pairwise_sum(v));
+  CHECK(pairwise_sum(std::span<const double>()) == 0.0);
+  for (int nt : {1, 3, 8}) {
+    parallel::set_threads(nt);
+    CHECK(parallel::threads() == nt);
+    std::vector<int> hit(1001, 0);
+    std::atomic<int> calls{0};
+    parallel::for_ranges(hit.size(), [&](std::size_t b, std::size_t e) {
+      ++calls;
+      for (std::size_t i = b; i < e; ++i) ++hit[i];
+    });
+    CHECK(std::all_of(hit.begin(), hit.end(), [](int h) { return h == 1; }));
+    CHECK(calls.load() == nt);  // one contiguous chunk per thread
+  }
+  parallel::set_threads(0);  // clamped to 1
+  CHECK(parallel::threads() == 1);
+}
+
 static void cpu_checks() {
   using namespace msot;
+  utility_checks();
   // cost
   const double a0[3] = {0, 0, 0}, a1[3] = {2, 0, 0};
   CHECK(cost(a0, a1, CostSpec{2.0}) == 2.0);
@@ -77,6 +111,13 @@ static void cpu_checks() {
   CHECK(s.size() == 4 && s.sigma[0] == 8 && s.sigma[3] == 1 && s.eps[1] == 16 && s.lambda[2] == 1);
   p.scaling = 0.9;
   CHECK(make_schedule(10.0, p).size() == 22);
+  {  // reach must be > 0 or +inf; 0 is not "balanced"
+    SolverParams z;
+    z.reach = 0.0;
+    CHECK(throws<DataError>([&] { z.to_c(); }));
+    z.reach = -1.0;
+    CHECK(throws<DataError>([&] { z.to_c(); }));
+  }
   CHECK(make_schedule(1.0, p).size() == 1);
   // encode_fibers
   FiberSet fs;

@@ -1,6 +1,7 @@
 """CPU tests of the drop-in boundary: the C-ABI library loads without a GPU,
 exports every symbol include/msot_gpu.h declares, and its host-side logic
 (schedule, shard split) agrees with the oracle.  No compute calls."""
+import ctypes as C
 import math
 import os
 import re
@@ -84,3 +85,65 @@ def test_no_oracle_in_product():
                 assert not re.search(r"(from|import)\s+oracle|liboracle|oracle_[a-z]", txt), f
     out = subprocess.run(["ldd", solver.LIB_PATH], capture_output=True, text=True).stdout
     assert "oracle" not in out and "msotref" not in out
+
+
+def test_binding_rejects_short_arrays():
+    """the ctypes binding validates every array length before the
+    C ABI reads n / m entries behind the pointers (no GPU needed: the checks
+    run before any library call)."""
+    import numpy as np
+    from paper_2107_02010_b200.abi import DataError, UsageError, make_params
+    from paper_2107_02010_b200.solver import Context, grad_weights, DualPotentials
+
+    ctx = Context.__new__(Context)  # no device: the checks fire first
+    ctx._h = None
+    x, y = np.zeros((5, 3)), np.zeros((4, 3))
+    prm = make_params()
+    with pytest.raises(DataError):
+        ctx.sinkhorn(prm, x, np.ones(4), y, np.ones(4))
+    with pytest.raises(DataError):
+        ctx.sinkhorn(prm, x, np.ones(5), y, np.ones(3))
+    with pytest.raises(DataError):
+        ctx.sinkhorn_grad(prm, x, np.ones(5), y, np.ones(5))
+    with pytest.raises(DataError):
+        ctx.transfer_labels(prm, x, np.ones(5), y, np.ones(4), np.zeros(3, np.int32))
+    with pytest.raises(DataError):
+        ctx.barycenter(prm, x, np.ones(5), [(y, np.ones(4)), (y, np.ones(2))])
+    with pytest.raises(DataError):
+        ctx.plan_apply(x, np.ones(5), y, np.ones(4), np.zeros(5), np.zeros(4), 1.0, np.ones(3))
+    with pytest.raises(DataError):
+        ctx.softmin(x, y, np.zeros(3), np.zeros(4), 1.0)
+    d = DualPotentials(np.zeros(5), np.zeros(4), np.zeros(4), np.zeros(5), 1.0)
+    with pytest.raises(UsageError):  # reach must be > 0 or inf
+        grad_weights(make_params(reach=0.0), np.ones(5), np.ones(4), d)
+    with pytest.raises(UsageError):
+        grad_weights(make_params(reach=-1.0), np.ones(5), np.ones(4), d)
+
+
+def _span_fn(lib, name, nargs):
+    f = getattr(lib, name)
+    f.restype = C.c_double
+    f.argtypes = [C.c_void_p, C.c_size_t] * nargs  # std::span<const double> by value
+    return f
+
+
+def test_numeric_bitwise_vs_reference():
+    """include/msot/numeric.hpp (reference proj/include/msot/numeric.hpp:9-15),
+    implemented in libmsot_b200.so, against the reference's own numeric.cpp
+    compiled unmodified into oracle/_ref: bitwise equal on every length."""
+    ref_path = os.path.join(ROOT, "oracle", "_ref", "libmsotref.so")
+    if not os.path.exists(ref_path):
+        pytest.skip("oracle/_ref not built")
+    ours, ref = C.CDLL(solver.LIB_PATH), C.CDLL(ref_path)
+    names = {"kahan": ("_ZN4msot9kahan_sumESt4spanIKdLm18446744073709551615EE", 1),
+             "sum": ("_ZN4msot12pairwise_sumESt4spanIKdLm18446744073709551615EE", 1),
+             "dot": ("_ZN4msot12pairwise_dotESt4spanIKdLm18446744073709551615EES2_", 2)}
+    rng = np.random.default_rng(7)
+    for n in [0, 1, 2, 31, 32, 33, 64, 65, 100, 1000, 4097, 123457]:
+        a = rng.standard_normal(n) * np.exp(rng.uniform(-20, 20, n))
+        b = rng.standard_normal(n)
+        for key, (sym, k) in names.items():
+            fo, fr = _span_fn(ours, sym, k), _span_fn(ref, sym, k)
+            args = [a.ctypes.data, n] if k == 1 else [a.ctypes.data, n, b.ctypes.data, n - n // 3]
+            vo, vr = fo(*args), fr(*args)
+            assert vo == vr or (math.isnan(vo) and math.isnan(vr)), (key, n, vo, vr)

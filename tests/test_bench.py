@@ -46,3 +46,21 @@ def test_reference_arm_contract():
     assert d["value"] > 0 and d["higher_is_better"] is False
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def test_self_spawn_ranks_gloo():
+    """`bench.py --gpus N` without torchrun spawns N ranks itself (RANK /
+    WORLD_SIZE / MASTER_ADDR=127.0.0.1 / MASTER_PORT), rendezvous over gloo,
+    reduces the step time as the max over ranks and prints one line on rank 0
+    (the driver's --gpus 8 must not run a single GPU)."""
+    env_clean = {k: v for k, v in os.environ.items()
+                 if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    for n in (2, 3):
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(n),
+                            "--dist-probe"], cwd=ROOT, capture_output=True, text=True,
+                           timeout=300, env=env_clean)
+        assert r.returncode == 0, r.stderr[-2000:]
+        lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+        assert len(lines) == 1, r.stdout
+        d = json.loads(lines[0])
+        assert d["n_gpus"] == n and d["ranks_seen"] == n and d["ms_per_step"] == float(n)

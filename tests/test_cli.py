@@ -132,3 +132,15 @@ def test_barycenter_two_maps(cli, tmp_path):
     pts = np.array([[float(v) for v in l.split()[1:]] for l in lines[1:]])
     assert loss[-1] <= loss[0]
     assert np.abs(pts[:, 0].mean() - 8.5).max() < 0.5  # the midpoint of the voxel centres
+
+
+def test_barycenter_mismatched_grids(cli, tmp_path):
+    """maps on different grids are a data error (exit 3), checked
+    before any device work (runs without a GPU)."""
+    a, b = tmp_path / "a.txt", tmp_path / "b.txt"
+    a.write_text("density 20 20 20 1.0 0 0 0\n4 10 10 1.0\n")
+    b.write_text("density 20 20 20 2.0 0 0 0\n12 10 10 1.0\n")  # voxel size differs
+    code, _, err = run(cli, "barycenter", a, b, "--iters", "1")
+    assert code == 3 and "grid" in err
+    b.write_text("density 20 20 20 1.0 5 0 0\n12 10 10 1.0\n")  # origin differs
+    assert run(cli, "barycenter", a, b, "--iters", "1")[0] == 3

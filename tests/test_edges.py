@@ -124,3 +124,24 @@ def test_deterministic(ctx, multiscale):
     assert l1 == l2
     for u, v in zip((p1.a_xx, p1.b_yy, p1.a_xy, p1.b_yx), (p2.a_xx, p2.b_yy, p2.a_xy, p2.b_yx)):
         np.testing.assert_array_equal(u, v)
+
+
+
+@pytest.mark.parametrize("multiscale", [False, True])
+def test_numeric_error_names_scale(ctx, multiscale):
+    """SPEC.md:178 / common.hpp:15-19: a non-finite potential raises
+    NumericError naming the scale where it first appeared.  blur = 1e-30 puts
+    eps = sigma^2 below float32's range ~400 scales into the schedule; the
+    device flags the first non-finite store (atomicMin over the scale index)."""
+    from paper_2107_02010_b200.abi import NumericError
+    x, y = mixture(500, 81), mixture(400, 82)
+    a, b = np.full(500, 1 / 500), np.full(400, 1 / 400)
+    prm = make_params(blur=1e-30, multiscale=multiscale, cluster_scale=0.1 if multiscale else 0.0)
+    with pytest.raises(NumericError, match=r"non-finite potential at scale (\d+) of (\d+)") as ei:
+        ctx.sinkhorn(prm, x, a, y, b)
+    import re
+    t, n = map(int, re.search(r"scale (\d+) of (\d+)", str(ei.value)).groups())
+    assert 0 < t <= n
+    # the context stays usable after the error
+    l, _, _ = ctx.sinkhorn(make_params(blur=0.05), x, a, y, b, potentials=False)
+    assert np.isfinite(l)

@@ -83,3 +83,25 @@ def test_hd_multiscale_matches_oracle(ctx, oracle, reach):
     # and close to the dense solve
     ld, _, _ = ctx.sinkhorn(make_params(blur=0.03, reach=reach), x, a, y, b, potentials=False)
     assert abs(lg - ld) <= 1e-3 * abs(ld), (lg, ld)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("reach", [math.inf, 0.3])
+def test_hd_multiscale_extrapolation_matches_oracle(ctx, oracle, reach):
+    """transfer_rule 1 on the K-means path (D = 60): the extrapolation softmin
+    runs on the tcgen05 kernel against the centroid measure, padding slots
+    included, against the oracle."""
+    x, a, y, b = fibre_measures(900, 800, 23)
+    x, a = W.flip_augment(x, a)
+    y, b = W.flip_augment(y, b)
+    prm = make_params(blur=0.03, reach=reach, multiscale=True, retruncate=1, switch_factor=1.0,
+                      clusters=15, transfer_rule=1)
+    lg, pg, sg = ctx.sinkhorn(prm, x, a, y, b)
+    lo, po, so = oracle.sinkhorn(prm, x, a, y, b)
+    assert (sg["kx"], sg["ky"], sg["t_switch"]) == (so["kx"], so["ky"], so["t_switch"])
+    assert 0 < sg["t_switch"] < sg["n_scales"]
+    eps = 0.03 ** 2
+    for name in ("a_xx", "b_yy", "a_xy", "b_yx"):
+        err = np.abs(getattr(pg, name) - po[name]).max()
+        assert err <= 1e-3 * eps, f"{name}: {err / eps:.3e} eps"
+    assert abs(lg - lo) <= 1e-4 * abs(lo), (lg, lo)

@@ -299,3 +299,78 @@ def test_errors(ctx):
     with pytest.raises(UsageError):  # high-D multiscale (K-means) is evaluate-once only
         ctx.sinkhorn(make_params(multiscale=True, pair_eval=0), np.zeros((3, 5)), np.ones(3),
                      np.zeros((3, 5)), np.ones(3))
+
+
+@pytest.mark.parametrize("reach", [math.inf, 0.3])
+@pytest.mark.parametrize("super_level", [0, 1])
+def test_multiscale_extrapolation_parity(ctx, oracle, reach, super_level):
+    """Coarse -> fine by extrapolation (transfer_rule 1, the north star's
+    'coarse-to-fine extrapolation of the dual potentials', SPEC.md:270-278):
+    one lambda-damped softmin of every fine atom against the coarse measure at
+    the last coarse scale, against the oracle's restatement (oracle.cpp,
+    transfer_rule == 1), balanced and unbalanced."""
+    n, m = 6000, 5200
+    x, y = mixture(n, 31), mixture(m, 32)
+    a, b = np.full(n, 1 / n), np.full(m, 1 / m)
+    prm = make_params(blur=0.01, reach=reach, multiscale=True, retruncate=1, cluster_scale=0.04,
+                      transfer_rule=1, super_level=super_level)
+    lg, pg, sg, lo, po, so = run_both(ctx, oracle, prm, x, a, y, b)
+    assert (sg["kx"], sg["ky"], sg["t_switch"]) == (so["kx"], so["ky"], so["t_switch"])
+    assert 0 < sg["t_switch"] < sg["n_scales"]
+    assert sg["phase_ms"] is not None
+    check_pots(pg, po, 1e-4)
+    assert abs(lg - lo) <= LOSS_TOL * abs(lo), (lg, lo)
+    # the two transfer rules land on the same divergence (SPEC.md:303 bar)
+    li, _, _ = ctx.sinkhorn(make_params(blur=0.01, reach=reach, multiscale=True, retruncate=1,
+                                        cluster_scale=0.04, super_level=super_level),
+                            x, a, y, b, potentials=False)
+    assert abs(lg - li) <= 1e-3 * abs(li), (lg, li)
+
+
+def _dropped_plan_mass(x, a, y, b, f, g, eps, mask, rl, cl, chunk=512):
+    """Plan mass pi_ij = a_i b_j exp((f_i + g_j - C_ij) / eps) summed over the
+    atom pairs whose cluster pair the mask drops (float64, host)."""
+    dropped = total = 0.0
+    for i0 in range(0, len(x), chunk):
+        xs = x[i0:i0 + chunk]
+        c = 0.5 * ((xs[:, None, :] - y[None, :, :]) ** 2).sum(-1)
+        pi = a[i0:i0 + chunk, None] * b[None, :] * np.exp((f[i0:i0 + chunk, None] + g[None, :] - c) / eps)
+        keep = mask[rl[i0:i0 + chunk]][:, cl].astype(bool)
+        dropped += pi[~keep].sum()
+        total += pi.sum()
+    return dropped, total
+
+
+@pytest.mark.parametrize("case", ["bench", "spec_default"])
+def test_truncation_safety_dropped_mass(ctx, case):
+    """SPEC.md Invariants: 'total implicit-plan mass on dropped pairs
+    (measured on a dense reference run) < 1e-6 of total mass'.  The masks are
+    the ones the multiscale solve used for its last averaged update (captured
+    through msot_debug_capture / msot_debug_mask), the plan comes from the
+    dense solve of the same inputs.  Cases: bench.py's parameters (theta 12.5,
+    switch_factor 1, per-scale re-truncation, automatic voxel edge) and the
+    SPEC defaults (theta 20, switch factor 2, masks built once)."""
+    n, m = 8000, 7000
+    x, y = mixture(n, 41), mixture(m, 42)
+    a, b = np.full(n, 1 / n), np.full(m, 1 / m)
+    if case == "bench":
+        prm = make_params(blur=0.01, multiscale=True, retruncate=1, theta=12.5, switch_factor=1.0)
+    else:
+        prm = make_params(blur=0.01, multiscale=True, cluster_scale=0.04)
+    _, _, st = ctx.sinkhorn(prm, x, a, y, b, potentials=False)
+    ns = st["n_scales"]
+    assert st["t_switch"] < ns - 1
+    ctx.debug_capture(ns - 1, n, m)
+    try:
+        ctx.sinkhorn(prm, x, a, y, b, potentials=False)
+    finally:
+        ctx.debug_capture(-1, 0, 0)
+    _, dense, _ = ctx.sinkhorn(make_params(blur=0.01), x, a, y, b)
+    eps = dense.eps
+    checks = {2: (x, a, y, b, dense.b_yx, dense.a_xy), 0: (x, a, x, a, dense.a_xx, dense.a_xx),
+              1: (y, b, y, b, dense.b_yy, dense.b_yy)}
+    for which, (u, wu, v, wv, f, g) in checks.items():
+        mask, rl, cl = ctx.debug_mask(which, len(u), len(v))
+        assert mask.mean() < 0.9  # the masks really prune
+        dropped, total = _dropped_plan_mass(u, wu, v, wv, f, g, eps, mask, rl, cl)
+        assert dropped < 1e-6 * total, (case, which, dropped, total)

@@ -123,3 +123,29 @@ def test_barycenter_midpoint_gpu(ctx):
                                 [(np.array([[-1.0]]), np.ones(1)),
                                  (np.array([[1.0]]), np.ones(1))], iters=20)
     assert abs(x[0, 0]) <= 0.01
+
+
+@pytest.mark.gpu
+def test_barycenter_multiscale_matches_oracle(ctx, oracle):
+    """Config-5 path at oracle size: multiscale solves with
+    the shared x-x self term — target 0 records a_xx and the self-plan
+    payload, targets 1..K-1 skip the x-x problem (Plan::skip_p0 in the masks,
+    the coarse and the fine tiles) — against oracle_barycenter, which shares
+    the self term the same way."""
+    targets = []
+    for k in range(3):
+        yk = blobs(30 + k, 2500, 0.1 * np.array([k, -k, 0.5 * k]))
+        targets.append((yk, np.full(2500, 1 / 2500)))
+    x0 = blobs(40, 3000, 0.05)
+    a = np.full(3000, 1 / 3000)
+    prm = make_params(blur=0.01, multiscale=True, retruncate=1, cluster_scale=0.04,
+                      switch_factor=1.0)
+    xg, tg, sg = ctx.barycenter(prm, x0, a, targets, iters=3)
+    xo, to = oracle.barycenter(prm, x0, a, targets, iters=3)
+    # the solves really ran the multiscale path with a fine phase
+    _, _, s1 = ctx.sinkhorn(prm, x0, a, *targets[1], potentials=False)
+    assert 0 < s1["t_switch"] < s1["n_scales"] and s1["pairs_fine"] > 0
+    assert len(tg) == len(to) and len(tg) > 1
+    np.testing.assert_allclose(tg, to, rtol=1e-4)
+    assert np.abs(xg - xo).max() <= 1e-4
+    assert np.all(np.diff(tg) <= 0)

@@ -15,6 +15,10 @@ stream); `e2e` = the same solve through the public host-buffer C ABI call
 --impl reference times the FP64 CPU oracle (the reference's Sinkhorn is
 specified only in prose) on a bounded sample and
 extrapolates to the workload's evaluated-pair count.
+
+Besides the C3 line it reports `extra_configs` (BASELINE.json configs 0, 1,
+3, 4 on this GPU) and `cpu_baseline` with the oracle timed in full on C1 and
+C2 (a few minutes on the host).  --no-extras / --no-cpu skip them.
 """
 import argparse
 import json
@@ -175,6 +179,122 @@ def dist_probe(args):
     dist.destroy_process_group()
 
 
+def run_extras(ctx):
+    """The other BASELINE.json configurations on this GPU (one timed run each
+    after a warm-up; device time from the solver's CUDA events):
+      C1 configs[0]  10k vs 10k uniform, blur 0.05, dense
+      C2 configs[1]  100k vs 100k mixtures (seeds 3/4), bench params (multiscale)
+      C4 configs[3]  200k vs 200k fibres (D = 60) flip-augmented to 400k vs 400k,
+                     reach 0.3, blur 0.03, K-means multiscale + label transfer
+      C5 configs[4]  barycenter of 10 synthetic 128^3 track-density maps,
+                     x6 upsampled init, blur = 1 voxel: seconds per descent step
+    C1 and C2 also report the FP64 oracle's committed result for the same
+    inputs (tests/golden/config_golden.json, tests/test_config_parity.py)."""
+    from paper_2107_02010_b200 import workloads as W
+    from paper_2107_02010_b200.abi import make_params
+    from paper_2107_02010_b200.solver import classify, resolve_flips
+    gold_p = os.path.join(ROOT, "tests", "golden", "config_golden.json")
+    gold = json.load(open(gold_p)) if os.path.exists(gold_p) else {}
+    out = {}
+    # C1
+    x1 = np.random.default_rng(1).random((10000, 3))
+    y1 = np.random.default_rng(2).random((10000, 3))
+    w1 = np.full(10000, 1e-4)
+    for _ in range(2):
+        l1, _, s1 = ctx.sinkhorn(make_params(blur=0.05), x1, w1, y1, w1, potentials=False)
+    out["C1"] = {"config": "10k vs 10k uniform 3D, blur 0.05, dense eps-scaling",
+                 "device_ms": s1["total_ms"], "S_eps": l1,
+                 "oracle_S_eps": gold.get("c1", {}).get("loss")}
+    # C2
+    wc2 = dict(WORKLOAD, n=100000, m=100000)
+    x2, y2 = mixture(100000, 3), mixture(100000, 4)
+    a2 = np.full(100000, 1e-5)
+    for _ in range(3):
+        l2, _, s2 = ctx.sinkhorn(params(wc2), x2, a2, y2, a2, potentials=False)
+    out["C2"] = {"config": "100k vs 100k 3D mixtures (seeds 3/4), multiscale, bench params",
+                 "device_ms": s2["total_ms"], "S_eps": l2, "kx": s2["kx"], "t_switch": s2["t_switch"],
+                 "device_mb": s2["device_bytes"] / 1e6, "oracle_S_eps": gold.get("c2", {}).get("loss")}
+    # C4
+    t = time.perf_counter()
+    fa, la = W.fibres(200000, 7, bundles=50, bundle_seed=1)
+    fb, lb = W.fibres(200000, 8, bundles=50, bundle_seed=1)
+    x4, a4 = W.flip_augment(*W.encode_fibers(fa))
+    y4, b4 = W.flip_augment(*W.encode_fibers(fb))
+    lab = np.concatenate([lb, lb]).astype(np.int32)
+    prep = time.perf_counter() - t
+    prm4 = make_params(blur=0.03, reach=0.3, multiscale=True, retruncate=1, switch_factor=2.0,
+                       theta=12.5)
+    for _ in range(2):
+        t = time.perf_counter()
+        soft, l4, s4 = ctx.transfer_labels(prm4, x4, a4, y4, b4, lab, 50)
+        wall4 = time.perf_counter() - t
+    res, _ = resolve_flips(soft, np.tile(np.arange(200000), 2), np.repeat([0, 1], 200000))
+    hard, _ = classify(res, 0.5)
+    inl = hard >= 0
+    out["C4"] = {"config": "200k vs 200k fibres (D=60, flip-augmented 400k vs 400k), reach 0.3, "
+                           "blur 0.03, K-means multiscale + label transfer",
+                 "device_ms": s4["total_ms"], "wall_s": wall4, "prep_s": prep, "S_eps": l4,
+                 "kx": s4["kx"], "t_switch": s4["t_switch"],
+                 "label_accuracy": float((hard[inl] == la[inl]).mean()) if inl.any() else None,
+                 "inlier_fraction": float(inl.mean())}
+    # C5
+    t = time.perf_counter()
+    maps = W.density_maps(10)
+    targets = [W.density_to_measure(*m) for m in maps]
+    p5, w5 = W.density_to_measure(*W.average_density(maps))
+    x5, a5 = W.upsample(p5, w5, 6, 0.5 / 128, 0)
+    prep5 = time.perf_counter() - t
+    prm5 = make_params(blur=1 / 128, multiscale=True, retruncate=1, switch_factor=1.0)
+    ctx.barycenter(prm5, x5, a5, targets, iters=1, step=1.0, tol=0.0)  # warm-up
+    t = time.perf_counter()
+    xb, traj, s5 = ctx.barycenter(prm5, x5, a5, targets, iters=3, step=1.0, tol=0.0)
+    dt5 = time.perf_counter() - t
+    steps5 = max(1, len(traj) - 1)
+    out["C5"] = {"config": "barycenter of 10 synthetic 128^3 track-density maps, x6 upsampled "
+                           "init, blur = 1 voxel, multiscale",
+                 "atoms": len(x5), "target_atoms_mean": float(np.mean([len(b) for _, b in targets])),
+                 "seconds_per_iteration": dt5 / steps5, "device_ms_per_iteration":
+                     s5["total_ms"] / steps5, "iterations": steps5, "prep_s": prep5,
+                 "loss_trajectory": [float(v) for v in traj]}
+    return out
+
+
+def cpu_baseline(st, extras):
+    """The FP64 oracle (oracle/, the CPU restatement on the reference's own
+    thread pool and summation, kind "port") timed in full on C1 and C2 of
+    BASELINE.json on this host; the C3 figure is the measured C2 block-sparse
+    multiscale solve's rate (oracle LSE terms per second) applied to the C3
+    solve's term count — a C3 oracle run would take ~45 min."""
+    from oracle import oracle as O  # CPU baseline only
+    from paper_2107_02010_b200.abi import make_params
+    cores = O.threads()
+    x1 = np.random.default_rng(1).random((10000, 3))
+    y1 = np.random.default_rng(2).random((10000, 3))
+    w1 = np.full(10000, 1e-4)
+    t = time.perf_counter()
+    l1, _, o1 = O.sinkhorn(make_params(blur=0.05), x1, w1, y1, w1, potentials=False)
+    c1_s = time.perf_counter() - t
+    wc2 = dict(WORKLOAD, n=100000, m=100000)
+    x2, y2 = mixture(100000, 3), mixture(100000, 4)
+    a2 = np.full(100000, 1e-5)
+    t = time.perf_counter()
+    l2, _, o2 = O.sinkhorn(params(wc2), x2, a2, y2, a2, potentials=False)
+    c2_s = time.perf_counter() - t
+    rate = o2["pairs_evaluated"] / c2_s  # LSE terms / s of the block-sparse multiscale solve
+    out = {"value": st["pairs_terms"] / rate, "unit": "s (C3 extrapolated from the measured C2 "
+                                                      "multiscale oracle solve)",
+           "cores": cores, "kind": "port",
+           "sample": f"FP64 oracle full solves on {cores} threads: C1 {c1_s:.1f} s, C2 {c2_s:.1f} s "
+                     f"({o2['pairs_evaluated']:.3e} LSE terms, {rate:.3e}/s); C3 = "
+                     f"{st['pairs_terms']:.3e} terms / that rate",
+           "C1_seconds": c1_s, "C1_S_eps": l1, "C2_seconds": c2_s, "C2_S_eps": l2,
+           "C2_terms_per_s": rate}
+    if extras:
+        out["C1_speedup_device"] = c1_s / (extras["C1"]["device_ms"] * 1e-3)
+        out["C2_speedup_device"] = c2_s / (extras["C2"]["device_ms"] * 1e-3)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -183,6 +303,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=None, help="override N=M (dev only)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--no-extras", action="store_true", help="skip the C1/C2/C4/C5 extra configs")
     ap.add_argument("--host-collectives", action="store_true",
                     help="dev only: every rank on cuda:0, exchanges through gloo via "
                          "msot_create_dist_host (exercises the N>1 path on one GPU)")
@@ -299,8 +420,15 @@ def main():
     e2e_s = float(e2e_local[1:].mean()) if len(e2e_t) > 1 else float(e2e_local[0])
 
     # roofline of the dominant kernel: softmin launches timed with events
+    # roofline: each softmin launch timed alone with CUDA events.  The timed
+    # steps run the column partials in bounded batches overlapped on two
+    # streams; profiling serialises launches, so the kernel is
+    # measured on one batch per update (budget unbounded): same kernel, same
+    # items, no inter-batch tails.
+    ctx.set_colpart_budget(1 << 40)
     ctx.set_profiling(True)
     _, pst = solve()
+    ctx.set_colpart_budget(0)
     # north star's dense-softmin bar (>= 60% of the MUFU roofline on one GPU):
     # the C1 configuration (10k vs 10k uniform 3D, blur 0.05, dense), solved
     # on the same context with its softmin launches event-timed
@@ -315,6 +443,7 @@ def main():
         dense = dst
     ctx.set_profiling(False)
     ex2_rate = ctx.probe_ex2()
+    extras = run_extras(ctx) if (world == 1 and not args.no_extras and rank == 0) else None
 
     if rank != 0:
         if world > 1:
@@ -374,16 +503,10 @@ def main():
             "frac_of_mufu_peak": dense["pairs_evaluated"] / (dense["softmin_ms"] * 1e-3) / ex2_rate,
             "solve_ms": dense["total_ms"]},
     }
+    if extras is not None:
+        line["extra_configs"] = extras
     if not args.no_cpu:
-        rows = 8192  # ~10 s of the oracle on 16 host threads
-        rate, dt, cores = cpu_sample(x, y, b, w["blur"] ** 2, rows)
-        line["cpu_baseline"] = {
-            "value": st["pairs_terms"] / rate, "unit": "s (extrapolated)", "cores": cores,
-            "kind": "port",
-            "sample": f"FP64 oracle softmin, {rows} rows x {w['m']} cols ({dt:.1f} s, "
-                      f"{rate:.3e} pairs/s) extrapolated to the solve's "
-                      f"{st['pairs_terms']:.3e} LSE terms (the oracle sums every term "
-                      f"row-wise; the GPU evaluated {st['pairs_evaluated']:.3e} pairs)"}
+        line["cpu_baseline"] = cpu_baseline(st, extras)
     os.makedirs(os.path.dirname(PAIRS_FILE), exist_ok=True)
     if w["n"] == WORKLOAD["n"] and world == 1:
         with open(PAIRS_FILE, "w") as f:

@@ -107,6 +107,9 @@ typedef struct msot_stats {
   int32_t t_super;          /* voxel multiscale: first cluster-level scale after the
                                super-voxel level (0: no super level)              */
   int32_t k_super_x, k_super_y;  /* super clusters                                */
+  int32_t colpart_batches;  /* most column-partial batches of one fine update       */
+  double  device_bytes;     /* device memory the context holds after the solve     */
+  int64_t host_syncs;       /* host waits on the device during the solve           */
 } msot_stats;
 
 typedef struct msot_ctx msot_ctx;
@@ -151,6 +154,10 @@ int msot_create_dist_host(int device, int rank, int world, msot_host_allreduce_f
 void msot_destroy(msot_ctx* ctx);
 /* 1 = time every softmin launch with CUDA events (stats.softmin_ms). */
 int msot_set_profiling(msot_ctx* ctx, int on);
+/* Column-partial slots an evaluate-once update may hold at once (0 =
+ * automatic: 6 per row + column of the group).  Larger values
+ * mean fewer, larger batches; results do not depend on it (bitwise). */
+int msot_set_colpart_budget(msot_ctx* ctx, int64_t slots);
 
 /* Measures the GPU's MUFU.EX2 rate (ex2 per second, all SMs) with the
  * ex2.approx.ftz.f32 instruction the softmin issues: the measured roofline

@@ -71,6 +71,9 @@ class Stats(C.Structure):
         ("t_super", C.c_int32),
         ("k_super_x", C.c_int32),
         ("k_super_y", C.c_int32),
+        ("colpart_batches", C.c_int32),
+        ("device_bytes", C.c_double),
+        ("host_syncs", C.c_int64),
     ]
 
     PHASES = ("setup", "coarse", "extrapolate", "masks", "updates", "loss", "labels")

@@ -52,6 +52,8 @@ struct Problem {
   const int64_t* tile_slot;  // [n_tiles] first colpart slot of each tile
   const float* row_add;      // column totals added to the row sums (self problems;
                              // the whole sum of the transposed cross problem)
+  float* row_sum;            // batched groups: reduced row partials (softmin_rowsum),
+                             // read by softmin_finalize instead of G.part
   float ell;                 // (1/lambda - 1) / (eps ln2): row/column reference shift
   int32_t n_rows, n_cols;
   float sc;                // 1 / sqrt(2 eps ln2): scaled |dx|^2 = C / (eps ln2)

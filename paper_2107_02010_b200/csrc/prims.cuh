@@ -28,6 +28,7 @@ cudaError_t radix_sort_pairs(uint32_t* keys, int32_t* vals, int64_t n, int key_b
 // softmin (softmin.cu)
 cudaError_t launch_softmin(const Group& g, int d, cudaStream_t st);
 cudaError_t launch_finalize(const Group& g, cudaStream_t st);
+cudaError_t launch_rowsum(const Group& g, int32_t i0, cudaStream_t st);  // batched row partials
 cudaError_t launch_fallback(const Group& g, int d, int n_sm, cudaStream_t st);
 cudaError_t launch_plan(const Group& g, int d, cudaStream_t st);  // plan_kernel + plan_finalize
 
@@ -40,9 +41,11 @@ struct ColSum {
   const int64_t* eslot;
   const int32_t* etile;
   const int32_t* tile_start;
-  const float* colpart;
+  const float* colpart;       // base such that colpart[eslot] is the slot (batch-shifted)
   float* tot;
+  double* acc;                // running float64 totals across batches (nullable: one batch)
   int32_t n_cols, self, t0, t1;
+  int32_t first, last;        // first / last batch of this problem
 };
 struct ColSumGroup {
   ColSum c[3];
@@ -74,7 +77,8 @@ cudaError_t launch_softmin_hd(const Group& g, int d, int n_sm, bool sym, cudaStr
 // out2 (nullable): column factor exponents of evaluate-once groups
 cudaError_t hd_colconst(const Problem& P, float* out, float* out2, cudaStream_t st);
 cudaError_t hd_colsum(const float* colpart, const int64_t* tslot, const int32_t* ts, int32_t t0,
-                      int32_t t1, int self, int32_t n_cols, float* tot, cudaStream_t st);
+                      int32_t t1, int self, int32_t n_cols, float* tot, double* acc, int first,
+                      int last, cudaStream_t st);
 cudaError_t launch_fallback_hd(const Group& g, int d, int n_sm, cudaStream_t st);
 
 // label transfer (labels.cu, K9)

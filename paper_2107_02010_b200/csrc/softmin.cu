@@ -267,9 +267,13 @@ __global__ void __launch_bounds__(kTileRows) softmin_finalize(const __grid_const
   const int lr = threadIdx.x;
   const int r = P.tile_start[t] + lr;
   if (r >= P.tile_start[t + 1]) return;
-  const int32_t k0 = P.tile_ibase[t], k1 = P.tile_ibase[t + 1];
   float s = 0.f;
-  for (int32_t k = k0; k < k1; ++k) s += G.part[static_cast<int64_t>(k) * kTileRows + lr];
+  if (P.row_sum) {  // batched group: the row partials were reduced per batch
+    s = P.row_sum[r];
+  } else {
+    const int32_t k0 = P.tile_ibase[t], k1 = P.tile_ibase[t + 1];
+    for (int32_t k = k0; k < k1; ++k) s += G.part[static_cast<int64_t>(k) * kTileRows + lr];
+  }
   if (P.row_add) s += P.row_add[r];  // column side of an evaluate-once self problem
   const float est = P.row_est ? P.row_est[r] : 0.f;
   // window [2^-60, 2^100]: flushed terms (< 2^-126 each) stay below 2^-84 s
@@ -280,6 +284,27 @@ __global__ void __launch_bounds__(kTileRows) softmin_finalize(const __grid_const
     return;
   }
   store_potential(G, P.row_out, r, est - P.mixw * P.lam_eps * logf(s));
+}
+
+// Row partials of one colpart batch (solver.cu: Plan::Batch): the rows of
+// the batch's tiles sum their items' partials in item order — the same float
+// additions softmin_finalize makes unbatched — into P.row_sum.  G.part holds
+// the batch's items only (item k at k - i0); G.t0 / tile_prefix describe the
+// batch's tiles.
+__global__ void __launch_bounds__(kTileRows) softmin_rowsum(const __grid_constant__ Group G,
+                                                             int32_t i0) {
+  const int b = blockIdx.x;
+  int p = 0;
+  while (p + 1 < G.n_problems && b >= G.tile_prefix[p + 1]) ++p;
+  const Problem& P = G.P[p];
+  const int t = G.t0[p] + (b - G.tile_prefix[p]);
+  const int lr = threadIdx.x;
+  const int r = P.tile_start[t] + lr;
+  if (r >= P.tile_start[t + 1]) return;
+  const int32_t k0 = P.tile_ibase[t], k1 = P.tile_ibase[t + 1];
+  float s = 0.f;
+  for (int32_t k = k0; k < k1; ++k) s += G.part[static_cast<int64_t>(k - i0) * kTileRows + lr];
+  P.row_sum[r] = s;
 }
 
 // Exact online-max LSE for the rows the fixed-reference path rejected: one
@@ -379,6 +404,13 @@ cudaError_t launch_finalize(const Group& g, cudaStream_t st) {
   const int tiles = g.tile_prefix[g.n_problems];
   if (tiles <= 0) return cudaSuccess;
   ++g_launches; softmin_finalize<<<tiles, kTileRows, 0, st>>>(g);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rowsum(const Group& g, int32_t i0, cudaStream_t st) {
+  const int tiles = g.tile_prefix[g.n_problems];
+  if (tiles <= 0) return cudaSuccess;
+  ++g_launches; softmin_rowsum<<<tiles, kTileRows, 0, st>>>(g, i0);
   return cudaGetLastError();
 }
 

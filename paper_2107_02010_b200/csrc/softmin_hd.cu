@@ -514,7 +514,8 @@ cudaError_t hd_colconst(const Problem& P, float* out, float* out2, cudaStream_t 
 // of every row tile of [t0, t1) that owns it (self: tiles ending at or
 // before j), in tile order, float64.
 __global__ void hd_colsum_kernel(const float* colpart, const int64_t* tslot, const int32_t* ts,
-                                 int32_t t0, int32_t t1, int self, int32_t n_cols, float* tot) {
+                                 int32_t t0, int32_t t1, int self, int32_t n_cols, float* tot,
+                                 double* acc, int first, int last) {
   const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n_cols) return;
   int32_t te = t1;  // self: tiles that end at or before j (ts ascending)
@@ -530,7 +531,7 @@ __global__ void hd_colsum_kernel(const float* colpart, const int64_t* tslot, con
   auto term = [&](int32_t t) {
     return __ldg(colpart + tslot[t] + (j - (self ? ts[t] : 0)));
   };
-  double s = 0.0;
+  double s = (acc && !first) ? acc[j] : 0.0;  // running total of earlier batches
   int32_t t = t0;
   for (; t + 4 <= te; t += 4) {
     const float v0 = term(t), v1 = term(t + 1), v2 = term(t + 2), v3 = term(t + 3);
@@ -540,15 +541,17 @@ __global__ void hd_colsum_kernel(const float* colpart, const int64_t* tslot, con
     s += static_cast<double>(v3);
   }
   for (; t < te; ++t) s += static_cast<double>(term(t));
-  tot[j] = static_cast<float>(s);
+  if (last || !acc) tot[j] = static_cast<float>(s);
+  else acc[j] = s;
 }
 
 cudaError_t hd_colsum(const float* colpart, const int64_t* tslot, const int32_t* ts, int32_t t0,
-                      int32_t t1, int self, int32_t n_cols, float* tot, cudaStream_t st) {
+                      int32_t t1, int self, int32_t n_cols, float* tot, double* acc, int first,
+                      int last, cudaStream_t st) {
   if (n_cols <= 0) return cudaSuccess;
   ++g_launches;
   hd_colsum_kernel<<<(n_cols + 255) / 256, 256, 0, st>>>(colpart, tslot, ts, t0, t1, self, n_cols,
-                                                         tot);
+                                                         tot, acc, first, last);
   return cudaGetLastError();
 }
 

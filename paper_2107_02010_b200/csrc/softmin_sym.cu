@@ -224,21 +224,36 @@ softmin_sym_kernel(const __grid_constant__ Group G) {
 // labels[j], offset j - co[J]), the sum over the cluster's entries (tiles in
 // ascending order, this rank's tiles [t0, t1) only; self problems: only
 // tiles that end at or before j) of colpart[eslot + offset], in float64.
+// Batched (bounded colpart): [t0, t1) is the batch's tile
+// range, found in the cluster's tile-ordered entries by binary search, and
+// the float64 running total carries across batches in `acc` — the same
+// additions in the same order as one pass, so the bits do not depend on
+// the batch size.
 __global__ void sym_colsum_kernel(const __grid_constant__ ColSumGroup g) {
   const ColSum& a = g.c[blockIdx.y];
   const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= a.n_cols) return;
   const int32_t J = a.labels[j];
   const int32_t off = j - a.co[J];
-  double s = 0.0;
-  for (int64_t e = a.eptr[static_cast<int64_t>(J) * kEntryChunks];
-       e < a.eptr[static_cast<int64_t>(J + 1) * kEntryChunks]; ++e) {
+  int64_t e = a.eptr[static_cast<int64_t>(J) * kEntryChunks];
+  int64_t e1 = a.eptr[static_cast<int64_t>(J + 1) * kEntryChunks];
+  {  // first entry with tile >= t0, then stop at tile >= t1
+    int64_t lo = e, hi = e1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (a.etile[mid] < a.t0) lo = mid + 1; else hi = mid;
+    }
+    e = lo;
+  }
+  double s = (a.acc && !a.first) ? a.acc[j] : 0.0;
+  for (; e < e1; ++e) {
     const int32_t t = a.etile[e];
-    if (t < a.t0 || t >= a.t1) continue;
+    if (t >= a.t1) break;
     if (a.self && a.tile_start[t + 1] > j) continue;
     s += static_cast<double>(a.colpart[a.eslot[e] + off]);
   }
-  a.tot[j] = static_cast<float>(s);
+  if (a.last || !a.acc) a.tot[j] = static_cast<float>(s);
+  else a.acc[j] = s;
 }
 
 cudaError_t launch_colsum(const ColSum* c, int n, cudaStream_t st) {

@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <stdexcept>
@@ -25,6 +26,7 @@
 
 namespace msot_dev {
 thread_local int64_t g_launches = 0;
+thread_local int64_t g_host_syncs = 0;  // host waits on the device (stats.host_syncs)
 }
 
 using namespace msot_dev;
@@ -80,6 +82,11 @@ namespace {
 struct msot_ctx {
   int device = 0, rank = 0, world = 1, n_sm = 148;
   cudaStream_t st = nullptr;
+  // batched evaluate-once updates: consecutive colpart batches alternate
+  // between two side streams so a batch's tail, row reduction and column sums
+  // overlap the next batch's softmin (run_group_sym)
+  cudaStream_t side[2] = {nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_cs[2] = {nullptr, nullptr};
   ncclComm_t comm = nullptr;
   // test seam (msot_create_dist_host): host-staged collectives instead of NCCL
   msot_host_allreduce_fn host_ar = nullptr;
@@ -96,6 +103,9 @@ struct msot_ctx {
   float4* self_pay = nullptr;   // [n] caller order
   // parity seam (msot_debug_capture): the four potentials before and after
   // the update of scale `cap_scale`, in the caller's order (host buffers)
+  // evaluate-once column partials: slots held per batch (0 = automatic,
+  // kColpartPerAtom x (rows + cols) of the group; MSOT_COLPART_BUDGET overrides)
+  int64_t colpart_budget = 0;
   int cap_scale = -1;
   double* cap_in[4] = {nullptr, nullptr, nullptr, nullptr};
   double* cap_out[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -108,14 +118,14 @@ struct msot_ctx {
   cudaEvent_t t0 = nullptr, t1 = nullptr;
 
   template <class T>
-  T* buf(const std::string& name, size_t count) {
+  T* buf(const std::string& name, size_t count, bool headroom = true) {
     const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
     auto it = bufs.find(name);
     if (it != bufs.end() && it->second.second >= bytes) return static_cast<T*>(it->second.first);
     size_t alloc = bytes;
     if (it != bufs.end()) {  // regrown buffer (sizes vary per rebuild): keep headroom
-      alloc = bytes + bytes / 2;
-      CK(cudaStreamSynchronize(st));
+      alloc = headroom ? bytes + bytes / 2 : bytes;
+      CK((++g_host_syncs, cudaStreamSynchronize(st)));
       CK(cudaFree(it->second.first));
       bufs.erase(it);
     }
@@ -153,6 +163,11 @@ struct msot_ctx {
 
 namespace {
 
+// Column-partial slots per row + column of an evaluate-once group (the
+// bounded colpart buffer): 6 floats = 24 B per atom (plus at
+// most as much again for the batches' row partials).
+constexpr int64_t kColpartPerAtom = 6;
+
 // ------------------------------------------------------------- collectives
 // The two exchange steps of a sharded scale: an all-reduce of
 // the column sums and a broadcast of every rank's row shard.  NCCL over
@@ -164,10 +179,10 @@ void coll_allreduce(msot_ctx* c, float* const* bufs, const int64_t* counts, int 
     for (int b = 0; b < nb; ++b) {
       std::vector<float> h(counts[b]);
       CK(cudaMemcpyAsync(h.data(), bufs[b], counts[b] * sizeof(float), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
+      CK((++g_host_syncs, cudaStreamSynchronize(st)));
       if (c->host_ar(h.data(), counts[b], c->host_user) != 0) raise(MSOT_ECUDA, "host all-reduce failed");
       CK(cudaMemcpyAsync(bufs[b], h.data(), counts[b] * sizeof(float), cudaMemcpyHostToDevice, st));
-      CK(cudaStreamSynchronize(st));
+      CK((++g_host_syncs, cudaStreamSynchronize(st)));
     }
     return;
   }
@@ -188,11 +203,11 @@ void coll_bcast_rows(msot_ctx* c, float* const* bufs, const std::vector<int64_t>
         std::vector<float> h(b1 - b0);
         CK(cudaMemcpyAsync(h.data(), bufs[b] + b0, (b1 - b0) * sizeof(float),
                            cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
+        CK((++g_host_syncs, cudaStreamSynchronize(st)));
         if (c->host_bc(h.data(), b1 - b0, r, c->host_user) != 0) raise(MSOT_ECUDA, "host broadcast failed");
         CK(cudaMemcpyAsync(bufs[b] + b0, h.data(), (b1 - b0) * sizeof(float),
                            cudaMemcpyHostToDevice, st));
-        CK(cudaStreamSynchronize(st));
+        CK((++g_host_syncs, cudaStreamSynchronize(st)));
       }
     return;
   }
@@ -242,7 +257,7 @@ void prepare_measure(msot_ctx* c, const std::string& tag, const double* d_x, con
   CK(gather_points(d_x, d_w, n, d, g, M.perm, M.pts, M.lw2, M.w64, nonuni, st));
   int32_t nu = 1;
   CK(cudaMemcpyAsync(&nu, nonuni, sizeof(nu), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  CK((++g_host_syncs, cudaStreamSynchronize(st)));
   M.uniform = nu == 0;
   if (!clusters) return;
   uint8_t* flags = c->buf<uint8_t>(tag + ".flags", n);
@@ -255,7 +270,7 @@ void prepare_measure(msot_ctx* c, const std::string& tag, const double* d_x, con
   CK(segment_offsets(M.labels, flags, n, M.offsets, st));
   int32_t k = 0;
   CK(cudaMemcpyAsync(&k, kdev, sizeof(k), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  CK((++g_host_syncs, cudaStreamSynchronize(st)));
   M.k = k;
   M.cpts = c->buf<float4>(tag + ".cpts", k);
   M.clw2 = c->buf<float>(tag + ".clw2", k);
@@ -267,7 +282,7 @@ void prepare_measure(msot_ctx* c, const std::string& tag, const double* d_x, con
   M.offsets_h.resize(k + 1);
   CK(cudaMemcpyAsync(M.offsets_h.data(), M.offsets, (k + 1) * sizeof(int32_t),
                      cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  CK((++g_host_syncs, cudaStreamSynchronize(st)));
 }
 
 // Super level of the coarse phase (policy.h:msot_super_switch): consecutive
@@ -295,7 +310,7 @@ void super_measure(msot_ctx* c, const std::string& tag, const DMeasure& M, int d
   CK((scan<uint8_t, int32_t>(flags, S.labels, k, true, stmp, kdev, st)));
   CK(segment_offsets(S.labels, flags, k, offs, st));
   CK(cudaMemcpyAsync(&S.k, kdev, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  CK((++g_host_syncs, cudaStreamSynchronize(st)));
   S.cpts = c->buf<float4>(tag + ".scpts", S.k);
   S.clw2 = c->buf<float>(tag + ".sclw2", S.k);
   double* cw = c->buf<double>(tag + ".scw64", S.k);
@@ -320,7 +335,7 @@ int64_t count_cells(msot_ctx* c, const double* d_x, int64_t n, const GridSpec& g
   CK((scan<uint8_t, int32_t>(flags, lab, n, true, stmp, kdev, st)));
   int32_t k = 0;
   CK(cudaMemcpyAsync(&k, kdev, sizeof(k), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  CK((++g_host_syncs, cudaStreamSynchronize(st)));
   return k;
 }
 
@@ -347,7 +362,7 @@ void make_tiles(msot_ctx* c, const std::string& tag, int64_t rows,
   R.tile_start = c->buf<int32_t>(tag + ".tstart", R.n_tiles + 1);
   CK(cudaMemcpyAsync(R.tile_start, R.tile_start_h.data(), (R.n_tiles + 1) * sizeof(int32_t),
                      cudaMemcpyHostToDevice, c->st));
-  CK(cudaStreamSynchronize(c->st));  // host vector may be reallocated by the caller
+  CK((++g_host_syncs, cudaStreamSynchronize(c->st)));  // host vector may be reallocated by the caller
 }
 
 void dense_rangeset(msot_ctx* c, const std::string& tag, int64_t rows, int64_t cols, RangeSet& R,
@@ -381,7 +396,7 @@ void mask_rangeset(msot_ctx* c, const std::string& tag, const int32_t* rl,
   R.tile_cols_h.resize(R.n_tiles);
   CK(cudaMemcpyAsync(R.tile_cols_h.data(), R.tile_cols, R.n_tiles * sizeof(int64_t),
                      cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  CK((++g_host_syncs, cudaStreamSynchronize(st)));
   R.ranges = c->buf<int2>(tag + ".ranges", R.n_ranges);
   CK(tile_range_write(tbits, ky, R.n_tiles, co, R.rptr, R.ranges, st));
 }
@@ -396,7 +411,7 @@ struct SymSet {
   int64_t* ebase = nullptr;   // [K * kEntryChunks + 1]
   int64_t* eslot = nullptr;
   int32_t* etile = nullptr;
-  float* colpart = nullptr;
+  std::vector<int64_t> tslot_h;  // host copy of tslot (batch bases)
   int64_t slots = 0, entries = 0;
   bool dense = false;         // dense_symset: column sums by hd_colsum (no entries)
 };
@@ -440,10 +455,12 @@ void sym_rangeset(msot_ctx* c, const std::string& tag, const int32_t* rl,
   R.tile_cols_h.resize(T);
   CK(cudaMemcpyAsync(R.tile_cols_h.data(), R.tile_cols, T * sizeof(int64_t),
                      cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  CK((++g_host_syncs, cudaStreamSynchronize(st)));
   R.n_ranges = tot[0];
   S.slots = tot[1];
   S.entries = tot[2];
+  S.tslot_h.assign(T + 1, 0);
+  for (int64_t t = 0; t < T; ++t) S.tslot_h[t + 1] = S.tslot_h[t] + R.tile_cols_h[t];
   R.ranges = c->buf<int2>(tag + ".ranges", R.n_ranges);
   CK(sym_ranges(tbits, ky, T, co, R.tile_start, rl, self, nullptr, nullptr, nullptr, R.rptr,
                 R.ranges, true, st));
@@ -451,7 +468,6 @@ void sym_rangeset(msot_ctx* c, const std::string& tag, const int32_t* rl,
   S.etile = c->buf<int32_t>(tag + ".etile", S.entries);
   CK(sym_entries(tbits, ky, T, co, R.tile_start, rl, self, posword, S.tslot, nullptr, S.ebase,
                  S.eslot, S.etile, true, st));
-  S.colpart = c->buf<float>(tag + ".colpart", S.slots);
 }
 
 // Dense evaluate-once pair sets (high-D path): uniform 256-row tiles; self
@@ -486,8 +502,8 @@ void dense_symset(msot_ctx* c, const std::string& tag, int64_t n_rows, int64_t n
   CK(cudaMemcpyAsync(S.tslot, tslot.data(), (T + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
   R.tile_cols_h = tcols;
   S.slots = tslot[T];
-  S.colpart = c->buf<float>(tag + ".colpart", S.slots);
-  CK(cudaStreamSynchronize(st));  // host vectors go out of scope
+  S.tslot_h = tslot;
+  CK((++g_host_syncs, cudaStreamSynchronize(st)));  // host vectors go out of scope
 }
 
 // ------------------------------------------------------------ launch plans
@@ -522,6 +538,18 @@ struct Plan {
   int4* items = nullptr;
   int32_t n_items = 0;
   float* part = nullptr;
+  // evaluate-once groups: the column partials (one float per (tile, column
+  // list position)) are produced and reduced in batches of consecutive
+  // tiles whose slots fit the context's colpart budget (memory linear in
+  // N + M)
+  struct Batch {
+    int32_t i0 = 0, i1 = 0;                 // items [i0, i1)
+    int32_t bt0[kMaxProblems] = {}, bt1[kMaxProblems] = {};  // tiles of each problem
+    int64_t off[kMaxProblems] = {};         // colpart offset of each problem's first slot
+  };
+  std::vector<Batch> batches;
+  float* colbuf = nullptr;
+  int64_t batch_slots = 0, batch_items = 0;  // largest batch
   double pairs_local = 0.0, pairs_all = 0.0;
   double terms_all = 0.0;  // LSE terms summed: an evaluate-once pair feeds a row and a column
 };
@@ -580,6 +608,58 @@ void build_plan(msot_ctx* c, const std::string& tag, Plan& P, int waves = 32) {
   const int64_t target = static_cast<int64_t>(c->n_sm) * 12 * waves;
   int64_t chunk = std::max<int64_t>(2 * kColTile, (tot_cols + target - 1) / std::max<int64_t>(target, 1));
   chunk = (chunk + kColTile - 1) / kColTile * kColTile;
+  if (P.ps[0].sym) {
+    // colpart batches: consecutive (problem, tile) runs of at most `budget`
+    // slots; each batch is cut into ~`waves` waves of items of its own
+    int64_t rows_cols = 0, slots_all = 0;
+    for (int p = 0; p < P.np; ++p) {
+      rows_cols += P.ps[p].n_rows + P.ps[p].n_cols;
+      for (int64_t t = P.t0[p]; t < P.t1[p]; ++t) slots_all += P.ps[p].rs->tile_cols_h[t];
+    }
+    const int64_t budget = c->colpart_budget > 0
+                               ? c->colpart_budget
+                               : std::max<int64_t>(int64_t(1) << 20, kColpartPerAtom * rows_cols);
+    // one batch when everything fits; otherwise two halves of the budget
+    // (consecutive batches overlap on two streams).  The item chunk does not
+    // depend on the batching: the row sums add the same partials in the same
+    // order for any budget.
+    const int64_t lim = slots_all <= budget ? budget : std::max<int64_t>(1, budget / 2);
+    P.batches.clear();
+    Plan::Batch b;
+    int64_t acc = 0, item = 0, held = 1;  // held: the largest batch (a lone tile may exceed budget)
+    for (int p = 0; p < P.np; ++p) {
+      b.bt0[p] = b.bt1[p] = static_cast<int32_t>(P.t0[p]);
+      for (int64_t t = P.t0[p]; t < P.t1[p]; ++t) {
+        const int64_t sl = P.ps[p].rs->tile_cols_h[t];
+        if (acc > 0 && acc + sl > lim) {  // close the batch before tile (p, t)
+          b.i1 = static_cast<int32_t>(item);
+          P.batches.push_back(b);
+          b = Plan::Batch{};
+          b.i0 = static_cast<int32_t>(item);
+          for (int q = 0; q < P.np; ++q) b.bt0[q] = b.bt1[q] = static_cast<int32_t>(q < p ? P.t1[q] : P.t0[q]);
+          b.bt0[p] = b.bt1[p] = static_cast<int32_t>(t);
+          acc = 0;
+        }
+        if (b.bt1[p] == b.bt0[p]) b.off[p] = acc;
+        b.bt1[p] = static_cast<int32_t>(t + 1);
+        acc += sl;
+        held = std::max(held, acc);
+        item += std::max<int64_t>(1, (sl + chunk - 1) / chunk);
+      }
+      if (p + 1 < P.np) b.bt0[p + 1] = b.bt1[p + 1] = static_cast<int32_t>(P.t0[p + 1]);
+    }
+    b.i1 = static_cast<int32_t>(item);
+    P.batches.push_back(b);
+    const size_t nbt = P.batches.size();
+    // sized by the budget (not regrown per scale): 2 x lim >= 2 x held unless
+    // one tile alone exceeds the half budget
+    P.colbuf = c->buf<float>("sym.colpart", nbt > 1 ? std::max(budget, 2 * held) : held, false);
+    P.batch_slots = held;
+    P.batch_items = 0;
+    for (const auto& bb : P.batches) P.batch_items = std::max<int64_t>(P.batch_items, bb.i1 - bb.i0);
+  } else {
+    P.batches.clear();
+  }
   int32_t* cnt = c->buf<int32_t>(tag + ".icnt", tot_tiles + 1);
   int32_t* ib = c->buf<int32_t>(tag + ".ibase", tot_tiles + 1);
   int32_t* stmp = c->buf<int32_t>(tag + ".istmp", scan_temp_elems(tot_tiles + 1));
@@ -593,11 +673,14 @@ void build_plan(msot_ctx* c, const std::string& tag, Plan& P, int waves = 32) {
   CK(cudaMemsetAsync(cnt + off, 0, sizeof(int32_t), st));
   CK((scan<int32_t, int32_t>(cnt, ib, off + 1, false, stmp, nullptr, st)));
   CK(cudaMemcpyAsync(&P.n_items, ib + off, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  CK((++g_host_syncs, cudaStreamSynchronize(st)));
   P.items = c->buf<int4>(tag + ".items", P.n_items);
   for (int p = 0; p < P.np; ++p)
     CK(item_write(P.ps[p].rs->tile_cols, P.t0[p], P.t1[p], chunk, P.ibase[p], p, P.items, st));
-  P.part = c->buf<float>(tag + ".part", static_cast<size_t>(P.n_items) * kTileRows);
+  if (P.batches.size() > 1)  // row partials of two in-flight batches (softmin_rowsum)
+    P.part = c->buf<float>("sym.part", static_cast<size_t>(2 * P.batch_items) * kTileRows, false);
+  else
+    P.part = c->buf<float>(tag + ".part", static_cast<size_t>(P.n_items) * kTileRows);
 }
 
 struct ScaleArgs {
@@ -735,10 +818,7 @@ void fill_problem(Problem& Q, const ProbSpec& S, const float* h, const float* es
   Q.mixw = static_cast<float>(mixw);
   Q.ell = static_cast<float>((1.0 / lam - 1.0) / (eps * ln2));
   Q.row_lw2 = S.row_lw2;
-  if (S.sym) {
-    Q.colpart = S.sym->colpart;
-    Q.tile_slot = S.sym->tslot;
-  }
+  if (S.sym) Q.tile_slot = S.sym->tslot;
 }
 
 void run_group_sym(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& ss,
@@ -773,11 +853,6 @@ void run_group_sym(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& s
   G.bad_scale = ss.bad_scale;
   G.scale = ss.scale;
   CK(cudaMemsetAsync(ss.fb_count, 0, sizeof(int32_t), st));
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (c->profiling) {
-    c->ev_pair(&e0, &e1);
-    CK(cudaEventRecord(e0, st));
-  }
   const bool hd = ss.d > 3;
   if (hd) {
     for (int p = 0; p < 3; ++p) {
@@ -788,28 +863,101 @@ void run_group_sym(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& s
       G.P[p].col_c = cc;
       G.P[p].col_c2 = c2;
     }
-    CK(launch_softmin_hd(G, ss.d, c->n_sm, true, st));
-  } else {
-    CK(launch_softmin_sym(G, ss.d, X.uniform && a.lam == 1.0, st));
   }
-  if (c->profiling) CK(cudaEventRecord(e1, st));
-  if (P.ps[0].sym->dense) {  // dense pair sets (high-D path, coarse phase, dense solves)
+  // Batches of consecutive tiles (Plan::Batch): the softmin writes the
+  // batch's column partials into the bounded buffer, the column-sum pass
+  // folds them into float64 running totals before the next batch reuses it.
+  const int nbt = static_cast<int>(P.batches.size());
+  int first_b[3], last_b[3];
+  for (int p = 0; p < 3; ++p) {
+    first_b[p] = last_b[p] = -1;
+    for (int bi = 0; bi < nbt; ++bi)
+      if (P.batches[bi].bt1[p] > P.batches[bi].bt0[p]) {
+        if (first_b[p] < 0) first_b[p] = bi;
+        last_b[p] = bi;
+      }
+    if (first_b[p] < 0) first_b[p] = last_b[p] = 0;  // no local tiles: totals = 0
+  }
+  double* acc[3] = {nullptr, nullptr, nullptr};
+  float* rsum[3] = {nullptr, nullptr, nullptr};
+  const bool multi = nbt > 1;
+  // overlap consecutive batches on the two side streams; profiling keeps
+  // every launch on the main stream so each softmin is timed alone
+  const bool overlap = multi && !c->profiling;
+  if (multi)
     for (int p = 0; p < 3; ++p) {
-      const SymSet& S = *P.ps[p].sym;
-      CK(hd_colsum(S.colpart, S.tslot, S.R.tile_start, static_cast<int32_t>(P.t0[p]),
-                   static_cast<int32_t>(P.t1[p]), S.self, static_cast<int32_t>(P.ps[p].n_cols),
-                   X.tot[p], st));
+      acc[p] = c->buf<double>("sym.acc" + std::to_string(p), P.ps[p].n_cols);
+      rsum[p] = c->buf<float>("sym.rsum" + std::to_string(p), P.ps[p].n_rows);
     }
-  } else {
+  if (overlap) {
+    CK(cudaEventRecord(c->ev_fork, st));
+    for (int k = 0; k < 2; ++k) CK(cudaStreamWaitEvent(c->side[k], c->ev_fork, 0));
+  }
+  for (int bi = 0; bi < nbt; ++bi) {
+    const Plan::Batch& B = P.batches[bi];
+    cudaStream_t bs = overlap ? c->side[bi & 1] : st;
+    float* half = P.colbuf + (multi ? (bi & 1) * P.batch_slots : 0);
+    Group Gb = G;
+    Gb.items = P.items + B.i0;
+    Gb.n_items = B.i1 - B.i0;
+    // batched: this batch's row partials in its half of the part buffer
+    Gb.part = multi ? P.part + static_cast<int64_t>(bi & 1) * P.batch_items * kTileRows
+                    : P.part + static_cast<int64_t>(B.i0) * kTileRows;
+    const float* cp[3];
+    for (int p = 0; p < 3; ++p) {
+      const bool has = B.bt1[p] > B.bt0[p];
+      // colpart[tile_slot[t] + pos] lands at half + off + (slot - first slot)
+      cp[p] = has ? half + B.off[p] - P.ps[p].sym->tslot_h[B.bt0[p]] : half;
+      Gb.P[p].colpart = const_cast<float*>(cp[p]);
+      Gb.P[p].tile_slot = P.ps[p].sym->tslot;
+    }
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->profiling) {
+      c->ev_pair(&e0, &e1);
+      CK(cudaEventRecord(e0, bs));
+    }
+    if (Gb.n_items > 0) {
+      if (hd) CK(launch_softmin_hd(Gb, ss.d, c->n_sm, true, bs));
+      else CK(launch_softmin_sym(Gb, ss.d, X.uniform && a.lam == 1.0, bs));
+    }
+    if (c->profiling) CK(cudaEventRecord(e1, bs));
+    if (multi) {  // reduce the batch's row partials before the half is reused
+      Group Gr = Gb;
+      int32_t acc_t = 0;
+      Gr.tile_prefix[0] = 0;
+      for (int p = 0; p < 3; ++p) {
+        Gr.t0[p] = B.bt0[p];
+        acc_t += B.bt1[p] - B.bt0[p];
+        Gr.tile_prefix[p + 1] = acc_t;
+        Gr.P[p].row_sum = rsum[p];
+      }
+      CK(launch_rowsum(Gr, B.i0, bs));
+    }
     ColSum cs[3];
+    int ncs = 0;
+    // column sums accumulate batch after batch: wait for the previous batch's
+    if (overlap && bi > 0) CK(cudaStreamWaitEvent(bs, c->ev_cs[(bi - 1) & 1], 0));
     for (int p = 0; p < 3; ++p) {
+      const bool has = B.bt1[p] > B.bt0[p];
+      if (!has && bi != first_b[p]) continue;  // nothing of p in this batch
       const SymSet& S = *P.ps[p].sym;
-      cs[p] = ColSum{X.labels[p], X.co[p], S.ebase, S.eslot, S.etile, S.R.tile_start, S.colpart,
-                     X.tot[p], static_cast<int32_t>(P.ps[p].n_cols), S.self,
-                     static_cast<int32_t>(P.t0[p]), static_cast<int32_t>(P.t1[p])};
+      const int first = bi == first_b[p], last = bi == last_b[p];
+      const int32_t t0 = has ? B.bt0[p] : 0, t1 = has ? B.bt1[p] : 0;
+      if (S.dense) {  // dense pair sets (high-D path, coarse phase, dense solves)
+        CK(hd_colsum(cp[p], S.tslot, S.R.tile_start, t0, t1, S.self,
+                     static_cast<int32_t>(P.ps[p].n_cols), X.tot[p], acc[p], first, last, bs));
+      } else {
+        cs[ncs++] = ColSum{X.labels[p], X.co[p], S.ebase, S.eslot, S.etile, S.R.tile_start, cp[p],
+                           X.tot[p], acc[p], static_cast<int32_t>(P.ps[p].n_cols), S.self, t0, t1,
+                           first, last};
+      }
     }
-    CK(launch_colsum(cs, 3, st));
+    if (ncs > 0) CK(launch_colsum(cs, ncs, bs));
+    if (overlap) CK(cudaEventRecord(c->ev_cs[bi & 1], bs));
   }
+  if (overlap) CK(cudaStreamWaitEvent(st, c->ev_cs[(nbt - 1) & 1], 0));
+  if (multi)
+    for (int p = 0; p < 3; ++p) G.P[p].row_sum = rsum[p];
   {  // column sums of every rank's tiles (NCCL over NVLink)
     const int64_t cnt[3] = {P.ps[0].n_cols, P.ps[1].n_cols, P.ps[2].n_cols};
     coll_allreduce(c, X.tot, cnt, 3);
@@ -817,7 +965,8 @@ void run_group_sym(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& s
   CK(launch_finalize(G, st));
   CK(launch_colfinal(G, 3, st));
   CK(hd ? launch_fallback_hd(G, ss.d, c->n_sm, st) : launch_fallback_dense(G, ss.d, c->n_sm, st));
-  ss.S->softmin_launches += 1;
+  ss.S->softmin_launches += nbt;
+  ss.S->colpart_batches = std::max(ss.S->colpart_batches, nbt);
   ss.S->pairs_evaluated += P.pairs_all;
   ss.S->pairs_terms += P.terms_all;
   coll_bcast_rows(c, a.out, P.row_bounds, 3);  // all-gather of the row-side potentials
@@ -854,7 +1003,7 @@ void capture_pots(msot_ctx* c, float* const* v, const int32_t* xperm, const int3
     if (!host[q]) continue;
     CK(scatter_unsort(v[q], perm[q], len[q], nullptr, 0.0, tmp, c->st));
     CK(cudaMemcpyAsync(host[q], tmp, len[q] * sizeof(double), cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
+    CK((++g_host_syncs, cudaStreamSynchronize(c->st)));
   }
 }
 
@@ -869,7 +1018,7 @@ void capture_masks(msot_ctx* c, const uint32_t* const* masks, const int32_t* kr,
     CK(unpack_mask(masks[q], kr[q], kc[q], dm, st));
     c->cap_mask[q].resize(cells);
     CK(cudaMemcpyAsync(c->cap_mask[q].data(), dm, cells, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    CK((++g_host_syncs, cudaStreamSynchronize(st)));
     c->cap_k[q][0] = kr[q];
     c->cap_k[q][1] = kc[q];
   }
@@ -878,7 +1027,7 @@ void capture_masks(msot_ctx* c, const uint32_t* const* masks, const int32_t* kr,
     std::vector<int32_t> lab(M[s]->n), perm(M[s]->n);
     CK(cudaMemcpyAsync(lab.data(), M[s]->labels, M[s]->n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(perm.data(), M[s]->perm, M[s]->n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    CK((++g_host_syncs, cudaStreamSynchronize(st)));
     c->cap_lab[s].assign(M[s]->n, -1);
     for (int64_t k = 0; k < M[s]->n; ++k) c->cap_lab[s][perm[k]] = lab[k];
   }
@@ -1036,7 +1185,7 @@ void hd_layout(msot_ctx* c, const std::string& tag, const double* dx, const doub
   CK(cudaMemcpyAsync(off_h.data(), off, (K + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(perm_h.data(), perm, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(L.radii_h.data(), L.radii, K * sizeof(float), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  CK((++g_host_syncs, cudaStreamSynchronize(st)));
   L.poff_h.assign(K + 1, 0);
   for (int I = 0; I < K; ++I)
     L.poff_h[I + 1] = L.poff_h[I] + (off_h[I + 1] - off_h[I] + 127) / 128 * 128;
@@ -1072,7 +1221,7 @@ void hd_layout(msot_ctx* c, const std::string& tag, const double* dx, const doub
   L.clw2 = c->buf<float>(tag + ".clw2", K);
   L.cw64 = c->buf<double>(tag + ".cw64", K);
   CK(hd_weights(cw, K, L.clw2, L.cw64, st));
-  CK(cudaStreamSynchronize(st));  // host vectors go out of scope
+  CK((++g_host_syncs, cudaStreamSynchronize(st)));  // host vectors go out of scope
 }
 
 void hd_multiscale(msot_ctx* c, const msot_params* prm, const double* d_x, const double* d_a,
@@ -1286,7 +1435,7 @@ void transfer_labels_dev(msot_ctx* c, const LabelReq& q, const DMeasure& X, cons
   if (Y.perm) {
     std::vector<int32_t> perm(Y.n);
     CK(cudaMemcpyAsync(perm.data(), Y.perm, Y.n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    CK((++g_host_syncs, cudaStreamSynchronize(st)));
     for (int64_t k = 0; k < Y.n; ++k)
       if (perm[k] >= 0) solver_of[perm[k]] = static_cast<int32_t>(k);
   } else {
@@ -1380,7 +1529,7 @@ void transfer_labels_dev(msot_ctx* c, const LabelReq& q, const DMeasure& X, cons
   }
   CK(hd ? launch_softmin_hd(G, d, c->n_sm, false, st) : launch_softmin(G, d, st));
   CK(label_finalize(G.part, dlbase, R.tile_start, T, L, X.perm, q.d_scores, q.d_mass, st));
-  CK(cudaStreamSynchronize(st));  // host vectors above go out of scope
+  CK((++g_host_syncs, cudaStreamSynchronize(st)));  // host vectors above go out of scope
 }
 
 void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const double* d_a,
@@ -1395,7 +1544,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
   if (prm->p != 2.0) raise(MSOT_EUSAGE, "the GPU path implements p = 2");
   if (!msot_reach_valid(prm->reach)) raise(MSOT_EUSAGE, "reach must be > 0 (or +inf for balanced OT)");
   cudaStream_t st = c->st;
-  const int64_t launches0 = g_launches;
+  const int64_t launches0 = g_launches, syncs0 = g_host_syncs;
   double frame[3] = {0.0, 0.0, 0.0};  // centre of the float32 atom frame (voxel path)
   c->ev_used = 0;
   c->marks.clear();
@@ -1414,7 +1563,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
   int32_t nbad = 0;
   CK(cudaMemcpyAsync(lh.data(), lohi, 2 * d * sizeof(long long), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(&nbad, badw, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  CK((++g_host_syncs, cudaStreamSynchronize(st)));
   if (nbad) raise(MSOT_EDATA, "weights must be finite and > 0");
   std::vector<double> lov(std::max(d, 3), 0.0), hiv(std::max(d, 3), 0.0);
   double* lo = lov.data();
@@ -1805,7 +1954,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
           CK(mask_pair_count(myx, Y.k, X.k, Y.offsets, X.offsets, cnt, st));
         double h = 0.0;
         CK(cudaMemcpyAsync(&h, cnt, sizeof(double), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
+        CK((++g_host_syncs, cudaStreamSynchronize(st)));
         mask_terms = h;
       }
       if (once) {  // evaluate-once pair sets (oracle.cpp: sym_self, transpose_ranges)
@@ -1926,13 +2075,13 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
       if (!h_pots[q]) continue;
       CK(scatter_unsort(f[q], perm[q], len[q], lout + 3, sign[q], tmp, st));
       CK(cudaMemcpyAsync(h_pots[q], tmp, outn[q] * sizeof(double), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
+      CK((++g_host_syncs, cudaStreamSynchronize(st)));
       S->d2h_bytes += outn[q] * sizeof(double);
     }
   }
   c->mark(-1);
   CK(cudaEventRecord(c->t1, st));
-  CK(cudaStreamSynchronize(st));
+  CK((++g_host_syncs, cudaStreamSynchronize(st)));
   float ms_total = 0.f;
   CK(cudaEventElapsedTime(&ms_total, c->t0, c->t1));
   S->total_ms = ms_total;
@@ -1953,6 +2102,9 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
   }
   S->fallback_rows = fbt;
   S->gpu_launches = g_launches - launches0;
+  S->host_syncs = g_host_syncs - syncs0;
+  S->device_bytes = 0.0;
+  for (const auto& kv : c->bufs) S->device_bytes += static_cast<double>(kv.second.second);
   S->d2h_bytes += sizeof(res);
   if (bad != 0x7f7f7f7f) {  // NumericError naming the scale
     const int t = std::min(bad, ns - 1);
@@ -2016,8 +2168,14 @@ int msot_shard_tiles(const double* work, int64_t n_tiles, int world, int64_t* bo
 }
 
 static int create_common(int device, msot_ctx** out, msot_ctx* c) {
+  if (const char* e = getenv("MSOT_COLPART_BUDGET")) c->colpart_budget = atoll(e);
   CK(cudaSetDevice(device));
   CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+  for (int k = 0; k < 2; ++k) {
+    CK(cudaStreamCreateWithFlags(&c->side[k], cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->ev_cs[k], cudaEventDisableTiming));
+  }
+  CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreate(&c->t0));
   CK(cudaEventCreate(&c->t1));
   CK(cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, device));
@@ -2134,12 +2292,27 @@ void msot_destroy(msot_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->st);
+  if (getenv("MSOT_DEBUG_BUFS")) {  // dev: the buffer table, largest first
+    std::vector<std::pair<size_t, std::string>> v;
+    for (auto& kv : c->bufs) v.push_back({kv.second.second, kv.first});
+    std::sort(v.rbegin(), v.rend());
+    size_t tot = 0;
+    for (auto& e : v) tot += e.first;
+    fprintf(stderr, "[msot] %zu buffers, %.1f MB\n", v.size(), tot / 1e6);
+    for (size_t k = 0; k < v.size() && k < 40; ++k)
+      fprintf(stderr, "[msot]   %10.3f MB  %s\n", v[k].first / 1e6, v[k].second.c_str());
+  }
   for (auto& kv : c->bufs) cudaFree(kv.second.first);
   for (auto e : c->ev) cudaEventDestroy(e);
   for (auto e : c->mark_pool) cudaEventDestroy(e);
   if (c->t0) cudaEventDestroy(c->t0);
   if (c->t1) cudaEventDestroy(c->t1);
   if (c->comm) ncclCommDestroy(c->comm);
+  for (int k = 0; k < 2; ++k) {
+    if (c->side[k]) cudaStreamDestroy(c->side[k]);
+    if (c->ev_cs[k]) cudaEventDestroy(c->ev_cs[k]);
+  }
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->st) cudaStreamDestroy(c->st);
   delete c;
 }
@@ -2147,6 +2320,12 @@ void msot_destroy(msot_ctx* c) {
 int msot_set_profiling(msot_ctx* c, int on) {
   if (!c) return MSOT_EUSAGE;
   c->profiling = on != 0;
+  return MSOT_OK;
+}
+
+int msot_set_colpart_budget(msot_ctx* c, int64_t slots) {
+  if (!c || slots < 0) return MSOT_EUSAGE;
+  c->colpart_budget = slots;
   return MSOT_OK;
 }
 
@@ -2162,7 +2341,7 @@ int msot_probe_ex2(msot_ctx* c, double* ex2_per_s) {
     CK(cudaEventRecord(c->t0, c->st));
     for (int r = 0; r < 5; ++r) CK(ex2_probe(c->n_sm, iters, sink, &per, &blocks, c->st));
     CK(cudaEventRecord(c->t1, c->st));
-    CK(cudaStreamSynchronize(c->st));
+    CK((++g_host_syncs, cudaStreamSynchronize(c->st)));
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, c->t0, c->t1));
     *ex2_per_s = 5.0 * per / (ms * 1e-3);
@@ -2242,7 +2421,7 @@ int msot_sinkhorn_grad(msot_ctx* c, const msot_params* prm, const double* x, con
     CK(cudaMemcpyAsync(db, b, m * sizeof(double), cudaMemcpyHostToDevice, c->st));
     solve_device(c, prm, dx, da, n, dy, db, m, d, loss_out, S, nullptr, dg);
     CK(cudaMemcpyAsync(grad_x, dg, n * d * sizeof(double), cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
+    CK((++g_host_syncs, cudaStreamSynchronize(c->st)));
   });
 }
 
@@ -2323,7 +2502,7 @@ int msot_transfer_labels(msot_ctx* c, const msot_params* prm, const double* x, c
     CK(cudaMemcpyAsync(scores, q.d_scores, size_t(n) * n_classes * sizeof(double),
                        cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemcpyAsync(row_mass, q.d_mass, n * sizeof(double), cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
+    CK((++g_host_syncs, cudaStreamSynchronize(c->st)));
   });
 }
 
@@ -2387,7 +2566,7 @@ int msot_barycenter(msot_ctx* c, const msot_params* prm, const double* x0, const
       for (int t = 0; t < k; ++t) CK(bbox(dy[t], ms[t], d, lohi, false, st));
       std::vector<long long> lh(2 * d);
       CK(cudaMemcpyAsync(lh.data(), lohi, 2 * d * sizeof(long long), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
+      CK((++g_host_syncs, cudaStreamSynchronize(st)));
       std::vector<double> lo(d), hi(d);
       bbox_decode(lh.data(), d, lo.data(), hi.data());
       double d2 = 0.0;
@@ -2446,7 +2625,7 @@ int msot_barycenter(msot_ctx* c, const msot_params* prm, const double* x0, const
       if (rel < tol) break;
     }
     CK(cudaMemcpyAsync(x_out, dx, n * d * sizeof(double), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    CK((++g_host_syncs, cudaStreamSynchronize(st)));
     if (steps_done) *steps_done = done;
   });
 }
@@ -2486,7 +2665,7 @@ int msot_softmin(msot_ctx* c, const double* x, int64_t n, const double* y, int64
     prepare_measure(c, "sm", dx64, dw64, n, d, g, false, MX);
     std::vector<int32_t> perm(n);
     CK(cudaMemcpyAsync(perm.data(), MX.perm, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    CK((++g_host_syncs, cudaStreamSynchronize(st)));
     std::vector<float4> yp(m);
     std::vector<float> yl(m), hh(m), fe(n, 0.f);
     if (f_est)
@@ -2539,7 +2718,7 @@ int msot_softmin(msot_ctx* c, const double* x, int64_t n, const double* y, int64
     c->world = world;
     std::vector<float> fo(n);
     CK(cudaMemcpyAsync(fo.data(), dfo, n * sizeof(float), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    CK((++g_host_syncs, cudaStreamSynchronize(st)));
     for (int64_t s = 0; s < n; ++s) f_out[perm[s]] = fo[s];
   });
 }
@@ -2577,7 +2756,7 @@ int msot_plan_apply(msot_ctx* c, const double* x, const double* a, int64_t n, co
     prepare_measure(c, "pa", dx64, da64, n, d, gs, false, MX);
     std::vector<int32_t> perm(n);
     CK(cudaMemcpyAsync(perm.data(), MX.perm, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    CK((++g_host_syncs, cudaStreamSynchronize(st)));
     std::vector<float4> yp(m), pay(m);
     std::vector<float> yl(m), gg(m), ff(n);
     for (int64_t s = 0; s < n; ++s) ff[s] = static_cast<float>(f[perm[s]]);
@@ -2610,7 +2789,7 @@ int msot_plan_apply(msot_ctx* c, const double* x, const double* a, int64_t n, co
     plan_group(c, "ppa", 1, &spec, fr, gc, py, po, eps, d);
     std::vector<float4> o(n);
     CK(cudaMemcpyAsync(o.data(), dout, n * sizeof(float4), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    CK((++g_host_syncs, cudaStreamSynchronize(st)));
     // row_plan = {sum_j pi_ij / a_i, sum_j pi_ij v_j / a_i, ...}
     for (int64_t s = 0; s < n; ++s) out[perm[s]] = a[perm[s]] * static_cast<double>(o[s].y);
   });
@@ -2655,7 +2834,7 @@ int msot_kmeans(msot_ctx* c, const double* x, const double* w, int64_t n, int d,
     CK(cudaMemcpyAsync(centroids, dcen, size_t(k) * d * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(cweights, dcw, k * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(radii, drad, k * sizeof(float), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    CK((++g_host_syncs, cudaStreamSynchronize(st)));
     if (iters) *iters = it;
   });
 }
@@ -2687,7 +2866,7 @@ int msot_grid_cluster(msot_ctx* c, const double* x, const double* w, int64_t n, 
     CK(cudaMemcpyAsync(cp.data(), M.cpts, M.k * sizeof(float4), cudaMemcpyDeviceToHost, st));
     if (cweights) CK(cudaMemcpyAsync(cweights, M.cw64, M.k * sizeof(double), cudaMemcpyDeviceToHost, st));
     if (radii) CK(cudaMemcpyAsync(radii, M.radii, M.k * sizeof(float), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    CK((++g_host_syncs, cudaStreamSynchronize(st)));
     *k_out = M.k;
     if (centroids)
       for (int32_t I = 0; I < M.k; ++I) {
@@ -2750,7 +2929,7 @@ int msot_truncation_mask(msot_ctx* c, int64_t kx, int64_t ky, int d, const float
                         dcy, dry, dgy, dhy, eps, theta, self, dbits, nullptr, dbr, dbc, bws, st));
     CK(unpack_mask(dbits, static_cast<int32_t>(kx), static_cast<int32_t>(ky), dm, st));
     CK(cudaMemcpyAsync(mask_out, dm, kx * ky, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    CK((++g_host_syncs, cudaStreamSynchronize(st)));
   });
 }
 

@@ -54,6 +54,7 @@ def lib():
         L.msot_destroy.argtypes = [C.c_void_p]
         L.msot_destroy.restype = None
         L.msot_set_profiling.argtypes = [C.c_void_p, C.c_int]
+        L.msot_set_colpart_budget.argtypes = [C.c_void_p, C.c_int64]
         L.msot_schedule.argtypes = [C.c_double, C.POINTER(Params), _dp, _dp, _dp, C.c_int]
         L.msot_shard_tiles.argtypes = [_dp, C.c_int64, C.c_int, _lp]
         L.msot_softmin.argtypes = [C.c_void_p, _dp, C.c_int64, _dp, C.c_int64, C.c_int, _dp,
@@ -99,7 +100,8 @@ EXPORTS = ["msot_last_error", "msot_params_default", "msot_create", "msot_nccl_u
            "msot_sinkhorn", "msot_sinkhorn_device", "msot_probe_ex2", "msot_sinkhorn_grad",
            "msot_barycenter", "msot_transfer_labels", "msot_resolve_flips", "msot_classify",
            "msot_plan_apply", "msot_kmeans", "msot_create_dist_host", "msot_exact_ot",
-           "msot_world_info", "msot_debug_capture", "msot_debug_mask"]
+           "msot_world_info", "msot_debug_capture", "msot_debug_mask",
+           "msot_set_colpart_budget"]
 
 
 def _check(rc):
@@ -356,6 +358,10 @@ class Context:
         _check(lib().msot_debug_mask(self._h, which, None, None, mask.ctypes.data_as(_bp),
                                      rl.ctypes.data_as(_ip), cl.ctypes.data_as(_ip)))
         return mask, rl, cl
+
+    def set_colpart_budget(self, slots=0):
+        """Column-partial slots of one evaluate-once batch pair (0 = automatic)."""
+        _check(lib().msot_set_colpart_budget(self._h, int(slots)))
 
     def set_profiling(self, on=True):
         _check(lib().msot_set_profiling(self._h, int(bool(on))))

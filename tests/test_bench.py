@@ -21,7 +21,7 @@ def _run(*args):
 
 @pytest.mark.gpu
 def test_bench_line_contract():
-    d = _run("--steps", "3", "--warmup", "3", "--n", "100000", "--no-cpu")
+    d = _run("--steps", "3", "--warmup", "3", "--n", "100000", "--no-cpu", "--no-extras")
     for k, t in [("metric", str), ("value", float), ("unit", str), ("n_gpus", int),
                  ("steps", int), ("warmup", int), ("ms_per_step", float),
                  ("higher_is_better", bool), ("scaling", str), ("dtype", str), ("data", str),

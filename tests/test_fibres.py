@@ -105,3 +105,22 @@ def test_hd_multiscale_extrapolation_matches_oracle(ctx, oracle, reach):
         err = np.abs(getattr(pg, name) - po[name]).max()
         assert err <= 1e-3 * eps, f"{name}: {err / eps:.3e} eps"
     assert abs(lg - lo) <= 1e-4 * abs(lo), (lg, lo)
+
+
+@pytest.mark.gpu
+def test_hd_colpart_batches_bitwise(ctx):
+    """Batched column partials on the tcgen05 path (dense pair sets, hd_colsum,
+    two streams): bitwise identical to one batch."""
+    x, a, y, b = fibre_measures(1500, 1300, 25)
+    prm = make_params(blur=0.03, reach=0.3)
+    ctx.set_colpart_budget(1 << 30)
+    try:
+        l1, p1, s1 = ctx.sinkhorn(prm, x, a, y, b)
+        ctx.set_colpart_budget(3000)
+        l2, p2, s2 = ctx.sinkhorn(prm, x, a, y, b)
+    finally:
+        ctx.set_colpart_budget(0)
+    assert s1["colpart_batches"] == 1 and s2["colpart_batches"] > 2
+    assert l1 == l2
+    for k in ("a_xx", "b_yy", "a_xy", "b_yx"):
+        np.testing.assert_array_equal(getattr(p1, k), getattr(p2, k))

@@ -140,12 +140,25 @@ def test_barycenter_multiscale_matches_oracle(ctx, oracle):
     a = np.full(3000, 1 / 3000)
     prm = make_params(blur=0.01, multiscale=True, retruncate=1, cluster_scale=0.04,
                       switch_factor=1.0)
-    xg, tg, sg = ctx.barycenter(prm, x0, a, targets, iters=3)
-    xo, to = oracle.barycenter(prm, x0, a, targets, iters=3)
     # the solves really ran the multiscale path with a fine phase
     _, _, s1 = ctx.sinkhorn(prm, x0, a, *targets[1], potentials=False)
     assert 0 < s1["t_switch"] < s1["n_scales"] and s1["pairs_fine"] > 0
-    assert len(tg) == len(to) and len(tg) > 1
+    # every descent step from identical positions agrees to 1e-4 (x0 and the
+    # GPU's own second iterate)
+    x2, _, _ = ctx.barycenter(prm, x0, a, targets, iters=2)
+    for xs in (x0, x2):
+        xg, tg, _ = ctx.barycenter(prm, xs, a, targets, iters=1)
+        xo, to = oracle.barycenter(prm, xs, a, targets, iters=1)
+        np.testing.assert_allclose(tg, to, rtol=1e-4)
+        assert np.abs(xg - xo).max() <= 1e-4
+    # three chained steps: the loss trajectory stays within 1e-4.  Positions
+    # drift further apart: the float32/float64 difference of one step (~3e-5)
+    # moves atoms across voxel faces in one run and not the other, so later
+    # solves use different clusters and tiles (measured 1.4e-3 max after 3
+    # steps, tools/diag_bary.py); bounded here by blur / 4.
+    xg, tg, _ = ctx.barycenter(prm, x0, a, targets, iters=3)
+    xo, to = oracle.barycenter(prm, x0, a, targets, iters=3)
+    assert len(tg) == len(to) == 4
     np.testing.assert_allclose(tg, to, rtol=1e-4)
-    assert np.abs(xg - xo).max() <= 1e-4
+    assert np.abs(xg - xo).max() <= 0.25 * 0.01
     assert np.all(np.diff(tg) <= 0)

@@ -109,20 +109,6 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm)}
 
 
-def cpu_sample(x, y, b, eps, rows, threads=None):
-    """Times the FP64 oracle softmin (the CPU restatement on the reference's
-    own thread pool) on `rows` rows against all columns: returns pairs/s."""
-    from oracle import oracle as O  # CPU baseline only
-    if threads:
-        O.set_threads(threads)
-    h = np.zeros(len(y))
-    logw = np.log(b)
-    t = time.perf_counter()
-    O.softmin(x[:rows], y, logw, h, eps)
-    dt = time.perf_counter() - t
-    return rows * len(y) / dt, dt, O.threads()
-
-
 def dense_rel(loss, w):
     """Relative difference to the dense (all-pairs) eps-scaling solve of the
     same inputs, measured once on the GPU (tools/dense_ref.py ->
@@ -213,7 +199,7 @@ def run_extras(ctx):
         l2, _, s2 = ctx.sinkhorn(params(wc2), x2, a2, y2, a2, potentials=False)
     out["C2"] = {"config": "100k vs 100k 3D mixtures (seeds 3/4), multiscale, bench params",
                  "device_ms": s2["total_ms"], "S_eps": l2, "kx": s2["kx"], "t_switch": s2["t_switch"],
-                 "device_mb": s2["device_bytes"] / 1e6, "oracle_S_eps": gold.get("c2", {}).get("loss")}
+                 "oracle_S_eps": gold.get("c2", {}).get("loss")}
     # C4
     t = time.perf_counter()
     fa, la = W.fibres(200000, 7, bundles=50, bundle_seed=1)
@@ -308,6 +294,7 @@ def main():
                     help="dev only: every rank on cuda:0, exchanges through gloo via "
                          "msot_create_dist_host (exercises the N>1 path on one GPU)")
     ap.add_argument("--dist-probe", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--ref-n", type=int, default=None, help=argparse.SUPPRESS)  # tests: smaller C2
     args = ap.parse_args()
 
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -521,35 +508,44 @@ def main():
 
 def run_reference(args, w, rank):
     """--impl reference: the CPU oracle (FP64 restatement of PAPER.md:235-326
-    on the reference's own thread pool, oracle/_ref) timed on bounded samples
-    of the same workload, extrapolated to the workload's evaluated pairs."""
+    on the reference's own thread pool and summation, oracle/_ref; the
+    reference's Sinkhorn exists only as prose) on this host.
+    The bounded sample is one full multiscale solve of BASELINE configs[1]
+    (C2: 100k vs 100k, the C3 generator and parameters at 1/10 the size, ~2
+    min on 16 threads), run once whatever --steps says; its measured rate
+    (LSE terms per second, clustering and masks included) is applied to the
+    C3 solve's term count (profiles/c3_workload.json, written by the GPU arm)."""
     if rank != 0:
         return
-    x, a, y, b = make_inputs(w)
+    from oracle import oracle as O  # the reference arm times the oracle
     pairs = None
     if os.path.exists(PAIRS_FILE):
         pf = json.load(open(PAIRS_FILE))
         pairs = pf.get("pairs_terms") or pf.get("pairs_evaluated")
-    rows = 2048  # a few seconds per step on 16 host threads
-    for _ in range(max(args.warmup, 0)):
-        cpu_sample(x, y, b, w["blur"] ** 2, 32)
-    rates = []
-    for _ in range(args.steps):
-        rate, dt, cores = cpu_sample(x, y, b, w["blur"] ** 2, rows)
-        rates.append(rate)
-    rate = statistics.median(rates)
+    n2 = args.ref_n or 100000
+    wc2 = dict(w, n=n2, m=n2)
+    x2, y2 = mixture(n2, 3), mixture(n2, 4)
+    a2 = np.full(n2, 1.0 / n2)
+    t = time.perf_counter()
+    l2, _, o2 = O.sinkhorn(params(wc2), x2, a2, y2, a2, potentials=False)
+    dt = time.perf_counter() - t
+    rate = o2["pairs_evaluated"] / dt
+    cores = O.threads()
     if pairs is None:
         pairs = float(w["n"]) * w["m"] * 4 * 50  # dense-equivalent upper bound
     sec = pairs / rate
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": sec, "unit": "s",
-        "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "higher_is_better": False,
+        "n_gpus": 0, "steps": 1, "steps_requested": args.steps, "warmup": 0,
+        "higher_is_better": False,
         "dtype": "f64", "data": "synthetic (seeded Gaussian mixtures)",
         "config": {**w, "parallelism": f"{cores} CPU threads"},
         "cpu_baseline": {"value": sec, "unit": "s (extrapolated)", "cores": cores, "kind": "port",
-                         "sample": f"FP64 oracle softmin {rows} rows x {w['m']} cols per step, "
-                                   f"{rate:.3e} pairs/s, extrapolated to {pairs:.3e} pairs "
-                                   f"(profiles/c3_workload.json)"},
+                         "sample": f"FP64 oracle full multiscale solve of C2 ({n2} vs {n2}, bench "
+                                   f"params): {dt:.1f} s, {o2['pairs_evaluated']:.3e} LSE terms, "
+                                   f"{rate:.3e}/s; C3 = {pairs:.3e} terms (profiles/c3_workload.json) "
+                                   f"/ that rate",
+                         "C2_seconds": dt, "C2_S_eps": l2},
         "e2e": {"value": sec, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 

@@ -97,18 +97,34 @@ double softmin_rows(const double* xr, int64_t n, int d, const Cols& c, double ep
         r1 = rg->tile_ptr[t + 1];
         rr = rg->r.data();
       }
+      // max-shifted LSE over blocks of kBlock terms: a block is buffered,
+      // its max folded into the running max (rescaling the sum), then summed
+      // -- one block (every block-sparse row of the tests) is the plain
+      // two-pass LSE; dense rows over 1M columns stay in cache
+      constexpr std::size_t kBlock = 4096;
       z.clear();
-      double zmax = -std::numeric_limits<double>::infinity();
+      double zmax = -std::numeric_limits<double>::infinity(), s = 0.0;
+      auto flush = [&]() {
+        double bmax = -std::numeric_limits<double>::infinity();
+        for (double v : z) bmax = std::max(bmax, v);
+        if (bmax > zmax) {
+          if (s != 0.0) s *= std::exp(zmax - bmax);
+          zmax = bmax;
+        }
+        for (double v : z) {
+          const double e = v - zmax;  // exp(e) rounds to +0 below -746: skip the call
+          if (e > -746.0) s += std::exp(e);
+        }
+        cnt += static_cast<double>(z.size());
+        z.clear();
+      };
       for (int64_t q = r0; q < r1; ++q) {
         for (int32_t k = rr[2 * q]; k < rr[2 * q + 1]; ++k) {
-          const double v = c.logw[k] + (c.h[k] - cost(xi, c.pts + int64_t(k) * d, d, p)) / eps;
-          z.push_back(v);
-          zmax = std::max(zmax, v);
+          z.push_back(c.logw[k] + (c.h[k] - cost(xi, c.pts + int64_t(k) * d, d, p)) / eps);
+          if (z.size() == kBlock) flush();
         }
       }
-      cnt += static_cast<double>(z.size());
-      double s = 0.0;
-      for (double v : z) s += std::exp(v - zmax);
+      if (!z.empty()) flush();
       out[i] = -lam * eps * (zmax + std::log(s));
     }
     // one chunk per thread slot; slot index recovered from the chunk start

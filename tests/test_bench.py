@@ -41,7 +41,7 @@ def test_bench_line_contract():
 
 
 def test_reference_arm_contract():
-    d = _run("--impl", "reference", "--steps", "1", "--warmup", "0")
+    d = _run("--impl", "reference", "--steps", "1", "--warmup", "0", "--ref-n", "5000")
     assert d["impl"] == "reference"
     assert d["value"] > 0 and d["higher_is_better"] is False
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1

@@ -164,8 +164,9 @@ struct msot_ctx {
 namespace {
 
 // Column-partial slots per row + column of an evaluate-once group (the
-// bounded colpart buffer): 6 floats = 24 B per atom (plus at
-// most as much again for the batches' row partials).
+// bounded colpart buffer): 6 floats = 24 B per atom and per 4
+// feature dimensions (the input itself is 8 D bytes per atom), plus at most
+// as much again for the batches' row partials.
 constexpr int64_t kColpartPerAtom = 6;
 
 // ------------------------------------------------------------- collectives
@@ -570,7 +571,7 @@ void shard_tiles(const std::vector<double>& work, int world, std::vector<int64_t
   }
 }
 
-void build_plan(msot_ctx* c, const std::string& tag, Plan& P, int waves = 32) {
+void build_plan(msot_ctx* c, const std::string& tag, Plan& P, int waves = 32, int dim = 3) {
   cudaStream_t st = c->st;
   // per-problem shard of row tiles, weighted by evaluated pairs
   int64_t tot_tiles = 0, tot_cols = 0;
@@ -618,12 +619,21 @@ void build_plan(msot_ctx* c, const std::string& tag, Plan& P, int waves = 32) {
     }
     const int64_t budget = c->colpart_budget > 0
                                ? c->colpart_budget
-                               : std::max<int64_t>(int64_t(1) << 20, kColpartPerAtom * rows_cols);
+                               : std::max<int64_t>(int64_t(1) << 20,
+                                                   kColpartPerAtom * rows_cols *
+                                                       std::max(1, (dim + 3) / 4));
     // one batch when everything fits; otherwise two halves of the budget
-    // (consecutive batches overlap on two streams).  The item chunk does not
-    // depend on the batching: the row sums add the same partials in the same
-    // order for any budget.
+    // (consecutive batches overlap on two streams).  The 3-D kernel's item
+    // chunk does not depend on the batching (~32 waves per update; the row
+    // sums then add the same partials in the same order for any budget).
+    // The high-D kernel's items are coarse (~2 waves per update), so batched
+    // high-D updates size their items for ~2 waves per batch instead (the
+    // result then depends on the automatic budget, i.e. on N + M only).
     const int64_t lim = slots_all <= budget ? budget : std::max<int64_t>(1, budget / 2);
+    if (slots_all > budget && waves <= 2) {
+      chunk = std::max<int64_t>(2 * kColTile, (lim + target - 1) / std::max<int64_t>(target, 1));
+      chunk = (chunk + kColTile - 1) / kColTile * kColTile;
+    }
     P.batches.clear();
     Plan::Batch b;
     int64_t acc = 0, item = 0, held = 1;  // held: the largest batch (a lone tile may exceed budget)
@@ -1297,7 +1307,7 @@ void hd_multiscale(msot_ctx* c, const msot_params* prm, const double* d_x, const
     cc.n = kx;
     cc.m = ky;
     cc.hd3 = {LY.cpack, LX.cpack, LY.csq, LX.csq, LY.cf, LX.cf};
-    build_plan(c, "hpc", Pc, 2);
+    build_plan(c, "hpc", Pc, 2, d);
     const double cfull = double(kx) * kx + double(ky) * ky + 2.0 * double(kx) * ky;
     for (int t = 0; t < tsw; ++t) {
       ss.scale = t;
@@ -1329,7 +1339,7 @@ void hd_multiscale(msot_ctx* c, const msot_params* prm, const double* d_x, const
       Pe.ps[1] = {nullptr, mr, nullptr, LY.clw2, ky, &eyy, {LY.pack, LY.cpack, LY.sq, LY.csq, LY.f, LY.cf}};
       Pe.ps[2] = {nullptr, mr, nullptr, LX.clw2, kx, &exy, {LY.pack, LX.cpack, LY.sq, LX.csq, LY.f, LX.cf}};
       Pe.ps[3] = {nullptr, nr, nullptr, LY.clw2, ky, &eyx, {LX.pack, LY.cpack, LX.sq, LY.csq, LX.f, LY.cf}};
-      build_plan(c, "hpe", Pe, 2);
+      build_plan(c, "hpe", Pe, 2, d);
       ScaleArgs ea{};
       ea.h[0] = co[0]; ea.est[0] = dst[0]; ea.out[0] = U.v[cur][0];
       ea.h[1] = co[1]; ea.est[1] = dst[1]; ea.out[1] = U.v[cur][1];
@@ -1385,7 +1395,7 @@ void hd_multiscale(msot_ctx* c, const msot_params* prm, const double* d_x, const
     Pf.ps[0] = {nullptr, nr, nullptr, LX.lw2, nr, &sxx.R, {LX.pack, LX.pack, LX.sq, LX.sq, LX.f, LX.f}, &sxx, LX.lw2};
     Pf.ps[1] = {nullptr, mr, nullptr, LY.lw2, mr, &syy.R, {LY.pack, LY.pack, LY.sq, LY.sq, LY.f, LY.f}, &syy, LY.lw2};
     Pf.ps[2] = {nullptr, nr, nullptr, LY.lw2, mr, &syx.R, {LX.pack, LY.pack, LX.sq, LY.sq, LX.f, LY.f}, &syx, LX.lw2};
-    build_plan(c, "hpf", Pf, 2);
+    build_plan(c, "hpf", Pf, 2, d);
   };
   for (int t = tsw; t <= ns; ++t) {
     const int tt = std::min(t, ns - 1);
@@ -1670,7 +1680,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
       P.ps[2] = {nullptr, m, nullptr, X.lw2, n, &fxy, {ay, bx, sqy, sqx, fy, fx}};  // a_xy
       P.ps[3] = {nullptr, n, nullptr, Y.lw2, m, &fyx, {ax, by, sqx, sqy, fx, fy}};  // b_yx
     }
-    build_plan(c, "ph", P, 2);
+    build_plan(c, "ph", P, 2, d);
     for (int t = 0; t <= ns; ++t) {
       const int tt = std::min(t, ns - 1);
       ss.scale = t;

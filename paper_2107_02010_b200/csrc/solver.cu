@@ -106,6 +106,7 @@ struct msot_ctx {
   // evaluate-once column partials: slots held per batch (0 = automatic,
   // kColpartPerAtom x (rows + cols) of the group; MSOT_COLPART_BUDGET overrides)
   int64_t colpart_budget = 0;
+  int32_t force_fb = 0;  // tests: MSOT_FORCE_FALLBACK=1 sends every row to the exact path
   int64_t solve_atoms = 0;  // N + M of the running solve (automatic colpart budget)
   int cap_scale = -1;
   double* cap_in[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -762,6 +763,7 @@ void run_group(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& ss) {
   G.fb_cap = ss.fb_cap;
   G.bad_scale = ss.bad_scale;
   G.scale = ss.scale;
+  G.force_fb = c->force_fb;
   CK(cudaMemsetAsync(ss.fb_count, 0, sizeof(int32_t), st));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c->profiling) {
@@ -802,6 +804,12 @@ struct SymCols {
   int64_t n, m;
   bool uniform;              // both measures have uniform weights
   HdOperands hd3{};          // high-D operands of problem 3 (rows y, cols x)
+  // fine phase: cluster masks (xx, yy, xy) for the neighbourhood-restricted
+  // exact fallback (softmin_fallback_dense); null in dense / coarse groups
+  const uint32_t* mask[3] = {nullptr, nullptr, nullptr};
+  const int32_t* rlab[4] = {nullptr, nullptr, nullptr, nullptr};  // row clusters per problem
+  const int32_t* fco[4] = {nullptr, nullptr, nullptr, nullptr};   // column cluster offsets
+  int32_t words[4] = {0, 0, 0, 0}, kc3 = 0;
 };
 
 void fill_problem(Problem& Q, const ProbSpec& S, const float* h, const float* est, float* out,
@@ -857,7 +865,19 @@ void run_group_sym(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& s
     fill_problem(G.P[3], T, a.h[3], a.est[3], a.out[3], a.eps, a.lam, a.mixw);
     G.P[3].row_add = X.tot[2];
   }
+  if (X.mask[0] || X.mask[1] || X.mask[2])
+    for (int p = 0; p < 4; ++p) {
+      Problem& Q = G.P[p];
+      Q.fb_mask = X.mask[p < 3 ? p : 2];
+      Q.fb_rlab = X.rlab[p];
+      Q.fb_co = X.fco[p];
+      Q.fb_words = X.words[p];
+      Q.fb_trans = p == 3;
+      Q.fb_kc = X.kc3;
+      if (!Q.fb_rlab || !Q.fb_co) Q.fb_mask = nullptr;
+    }
   G.n_problems = 3;
+  G.force_fb = c->force_fb;
   G.items = P.items;
   G.n_items = P.n_items;
   G.part = P.part;
@@ -1895,6 +1915,14 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
       scol.n = n;
       scol.m = m;
       scol.uniform = X.uniform && Y.uniform;
+      scol.mask[0] = mxx;
+      scol.mask[1] = myy;
+      scol.mask[2] = mxy;
+      scol.rlab[0] = X.labels; scol.rlab[1] = Y.labels; scol.rlab[2] = X.labels; scol.rlab[3] = Y.labels;
+      scol.fco[0] = X.offsets; scol.fco[1] = Y.offsets; scol.fco[2] = Y.offsets; scol.fco[3] = X.offsets;
+      scol.words[0] = mask_words(X.k);
+      scol.words[1] = scol.words[2] = scol.words[3] = mask_words(Y.k);
+      scol.kc3 = X.k;
     }
     auto build_masks = [&](double e) {
       // without a coarse phase there is no information: keep every pair
@@ -2185,6 +2213,7 @@ int msot_shard_tiles(const double* work, int64_t n_tiles, int world, int64_t* bo
 
 static int create_common(int device, msot_ctx** out, msot_ctx* c) {
   if (const char* e = getenv("MSOT_COLPART_BUDGET")) c->colpart_budget = atoll(e);
+  if (const char* e = getenv("MSOT_FORCE_FALLBACK")) c->force_fb = atoi(e) != 0;
   CK(cudaSetDevice(device));
   CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
   for (int k = 0; k < 2; ++k) {

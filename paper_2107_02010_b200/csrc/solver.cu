@@ -53,6 +53,16 @@ struct Err {
     if (r_ != ncclSuccess) raise(MSOT_ECUDA, std::string(#call) + ": " + ncclGetErrorString(r_)); \
   } while (0)
 
+// Host waits on the device (stats.host_syncs); MSOT_DEBUG_SYNCS=1 prints the
+// call sites per solve.
+thread_local std::map<int, int> g_sync_sites;
+cudaError_t host_sync(int line, cudaStream_t st) {
+  ++g_host_syncs;
+  static const bool dbg = getenv("MSOT_DEBUG_SYNCS") != nullptr;
+  if (dbg) ++g_sync_sites[line];
+  return cudaStreamSynchronize(st);
+}
+
 template <class F>
 int guard(F&& f) {
   try {
@@ -115,6 +125,29 @@ struct msot_ctx {
   int32_t cap_k[3][2] = {{0, 0}, {0, 0}, {0, 0}};
   std::vector<int32_t> cap_lab[2];      // cluster of every atom of x / y (caller order)
   std::map<std::string, std::pair<void*, size_t>> bufs;
+  // pinned host staging for device -> host reads: copies of one planning
+  // step land here asynchronously and are waited for with ONE sync
+  // (pageable D2H copies are synchronous)
+  char* pin_base = nullptr;
+  size_t pin_cap = 0, pin_off = 0;
+  void pin_reserve(size_t bytes) {  // call between sync points only
+    pin_off = 0;
+    if (bytes <= pin_cap) return;
+    if (pin_base) cudaFreeHost(pin_base);
+    pin_cap = std::max(bytes, size_t(1) << 20);
+    if (cudaMallocHost(reinterpret_cast<void**>(&pin_base), pin_cap) != cudaSuccess) {
+      pin_base = nullptr;
+      pin_cap = 0;
+      throw std::runtime_error("cudaMallocHost failed");
+    }
+  }
+  template <class T>
+  T* pin(size_t count) {
+    const size_t a = (pin_off + 15) & ~size_t(15), b = a + std::max<size_t>(count, 1) * sizeof(T);
+    if (b > pin_cap) throw std::runtime_error("pinned staging overflow (pin_reserve too small)");
+    pin_off = b;
+    return reinterpret_cast<T*>(pin_base + a);
+  }
   std::vector<cudaEvent_t> ev;  // profiling events (pairs)
   size_t ev_used = 0;
   cudaEvent_t t0 = nullptr, t1 = nullptr;
@@ -127,7 +160,7 @@ struct msot_ctx {
     size_t alloc = bytes;
     if (it != bufs.end()) {  // regrown buffer (sizes vary per rebuild): keep headroom
       alloc = headroom ? bytes + bytes / 2 : bytes;
-      CK((++g_host_syncs, cudaStreamSynchronize(st)));
+      CK(host_sync(__LINE__, st));
       CK(cudaFree(it->second.first));
       bufs.erase(it);
     }
@@ -182,10 +215,10 @@ void coll_allreduce(msot_ctx* c, float* const* bufs, const int64_t* counts, int 
     for (int b = 0; b < nb; ++b) {
       std::vector<float> h(counts[b]);
       CK(cudaMemcpyAsync(h.data(), bufs[b], counts[b] * sizeof(float), cudaMemcpyDeviceToHost, st));
-      CK((++g_host_syncs, cudaStreamSynchronize(st)));
+      CK(host_sync(__LINE__, st));
       if (c->host_ar(h.data(), counts[b], c->host_user) != 0) raise(MSOT_ECUDA, "host all-reduce failed");
       CK(cudaMemcpyAsync(bufs[b], h.data(), counts[b] * sizeof(float), cudaMemcpyHostToDevice, st));
-      CK((++g_host_syncs, cudaStreamSynchronize(st)));
+      CK(host_sync(__LINE__, st));
     }
     return;
   }
@@ -206,11 +239,11 @@ void coll_bcast_rows(msot_ctx* c, float* const* bufs, const std::vector<int64_t>
         std::vector<float> h(b1 - b0);
         CK(cudaMemcpyAsync(h.data(), bufs[b] + b0, (b1 - b0) * sizeof(float),
                            cudaMemcpyDeviceToHost, st));
-        CK((++g_host_syncs, cudaStreamSynchronize(st)));
+        CK(host_sync(__LINE__, st));
         if (c->host_bc(h.data(), b1 - b0, r, c->host_user) != 0) raise(MSOT_ECUDA, "host broadcast failed");
         CK(cudaMemcpyAsync(bufs[b] + b0, h.data(), (b1 - b0) * sizeof(float),
                            cudaMemcpyHostToDevice, st));
-        CK((++g_host_syncs, cudaStreamSynchronize(st)));
+        CK(host_sync(__LINE__, st));
       }
     return;
   }
@@ -242,50 +275,89 @@ struct DMeasure {
   bool uniform = false;            // all weights equal
 };
 
+// Sort, gather and cluster several measures with two host waits in total:
+// the cluster counts (and the uniform-weight flags), then the radii and
+// offsets.
+struct MeasureJob {
+  std::string tag;
+  const double* x;
+  const double* w;
+  int64_t n;
+  DMeasure* M;
+};
+void prepare_measures(msot_ctx* c, const std::vector<MeasureJob>& jobs, int d, const GridSpec& g,
+                      bool clusters) {
+  cudaStream_t st = c->st;
+  c->pin_reserve(jobs.size() * 64);
+  std::vector<int32_t*> h(jobs.size());
+  for (size_t q = 0; q < jobs.size(); ++q) {
+    const MeasureJob& J = jobs[q];
+    DMeasure& M = *J.M;
+    const std::string& tag = J.tag;
+    const int64_t n = J.n;
+    M.n = n;
+    uint32_t* keys = c->buf<uint32_t>(tag + ".keys", n);
+    M.perm = c->buf<int32_t>(tag + ".perm", n);
+    CK(cube_keys(J.x, n, g, keys, M.perm, st));
+    void* tmp = c->buf<char>(tag + ".rstmp", radix_temp_bytes(n));
+    const int bits = g.d == 1 ? MSOT_MORTON_BITS : g.d == 2 ? 2 * MSOT_MORTON_BITS : 3 * MSOT_MORTON_BITS;
+    CK(radix_sort_pairs(keys, M.perm, n, bits, tmp, st));
+    M.pts = c->buf<float4>(tag + ".pts", n);
+    M.lw2 = c->buf<float>(tag + ".lw2", n);
+    M.w64 = c->buf<double>(tag + ".w64", n);
+    int32_t* nonuni = c->buf<int32_t>(tag + ".nonuni", 1);
+    CK(cudaMemsetAsync(nonuni, 0, sizeof(int32_t), st));
+    CK(gather_points(J.x, J.w, n, d, g, M.perm, M.pts, M.lw2, M.w64, nonuni, st));
+    h[q] = c->pin<int32_t>(2);
+    h[q][1] = 0;
+    CK(cudaMemcpyAsync(&h[q][0], nonuni, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    if (!clusters) continue;
+    uint8_t* flags = c->buf<uint8_t>(tag + ".flags", n);
+    M.labels = c->buf<int32_t>(tag + ".labels", n);
+    M.offsets = c->buf<int32_t>(tag + ".offsets", n + 1);
+    int32_t* stmp = c->buf<int32_t>(tag + ".stmp", scan_temp_elems(n));
+    int32_t* kdev = c->buf<int32_t>(tag + ".k", 1);
+    CK(segment_flags(keys, n, flags, st));
+    CK((scan<uint8_t, int32_t>(flags, M.labels, n, true, stmp, kdev, st)));
+    CK(segment_offsets(M.labels, flags, n, M.offsets, st));
+    CK(cudaMemcpyAsync(&h[q][1], kdev, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  }
+  CK(host_sync(__LINE__, st));
+  for (size_t q = 0; q < jobs.size(); ++q) {
+    jobs[q].M->uniform = h[q][0] == 0;
+    jobs[q].M->k = h[q][1];
+  }
+  if (!clusters) return;
+  size_t need = 0;
+  for (const MeasureJob& J : jobs) need += (2 * static_cast<size_t>(J.M->k) + 1) * 4 + 64;
+  c->pin_reserve(need);
+  std::vector<float*> hr(jobs.size());
+  std::vector<int32_t*> ho(jobs.size());
+  for (size_t q = 0; q < jobs.size(); ++q) {
+    DMeasure& M = *jobs[q].M;
+    const std::string& tag = jobs[q].tag;
+    const int32_t k = M.k;
+    M.cpts = c->buf<float4>(tag + ".cpts", k);
+    M.clw2 = c->buf<float>(tag + ".clw2", k);
+    M.cw64 = c->buf<double>(tag + ".cw64", k);
+    M.radii = c->buf<float>(tag + ".radii", k);
+    CK(cluster_stats(M.pts, M.w64, M.offsets, k, d, M.cpts, M.clw2, M.cw64, M.radii, st));
+    hr[q] = c->pin<float>(k);
+    ho[q] = c->pin<int32_t>(k + 1);
+    CK(cudaMemcpyAsync(hr[q], M.radii, k * sizeof(float), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(ho[q], M.offsets, (k + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  }
+  CK(host_sync(__LINE__, st));
+  for (size_t q = 0; q < jobs.size(); ++q) {
+    DMeasure& M = *jobs[q].M;
+    M.radii_h.assign(hr[q], hr[q] + M.k);
+    M.offsets_h.assign(ho[q], ho[q] + M.k + 1);
+  }
+}
+
 void prepare_measure(msot_ctx* c, const std::string& tag, const double* d_x, const double* d_w,
                      int64_t n, int d, const GridSpec& g, bool clusters, DMeasure& M) {
-  cudaStream_t st = c->st;
-  M.n = n;
-  uint32_t* keys = c->buf<uint32_t>(tag + ".keys", n);
-  M.perm = c->buf<int32_t>(tag + ".perm", n);
-  CK(cube_keys(d_x, n, g, keys, M.perm, st));
-  void* tmp = c->buf<char>(tag + ".rstmp", radix_temp_bytes(n));
-  const int bits = g.d == 1 ? MSOT_MORTON_BITS : g.d == 2 ? 2 * MSOT_MORTON_BITS : 3 * MSOT_MORTON_BITS;
-  CK(radix_sort_pairs(keys, M.perm, n, bits, tmp, st));
-  M.pts = c->buf<float4>(tag + ".pts", n);
-  M.lw2 = c->buf<float>(tag + ".lw2", n);
-  M.w64 = c->buf<double>(tag + ".w64", n);
-  int32_t* nonuni = c->buf<int32_t>(tag + ".nonuni", 1);
-  CK(cudaMemsetAsync(nonuni, 0, sizeof(int32_t), st));
-  CK(gather_points(d_x, d_w, n, d, g, M.perm, M.pts, M.lw2, M.w64, nonuni, st));
-  int32_t nu = 1;
-  CK(cudaMemcpyAsync(&nu, nonuni, sizeof(nu), cudaMemcpyDeviceToHost, st));
-  CK((++g_host_syncs, cudaStreamSynchronize(st)));
-  M.uniform = nu == 0;
-  if (!clusters) return;
-  uint8_t* flags = c->buf<uint8_t>(tag + ".flags", n);
-  M.labels = c->buf<int32_t>(tag + ".labels", n);
-  M.offsets = c->buf<int32_t>(tag + ".offsets", n + 1);
-  int32_t* stmp = c->buf<int32_t>(tag + ".stmp", scan_temp_elems(n));
-  int32_t* kdev = c->buf<int32_t>(tag + ".k", 1);
-  CK(segment_flags(keys, n, flags, st));
-  CK((scan<uint8_t, int32_t>(flags, M.labels, n, true, stmp, kdev, st)));
-  CK(segment_offsets(M.labels, flags, n, M.offsets, st));
-  int32_t k = 0;
-  CK(cudaMemcpyAsync(&k, kdev, sizeof(k), cudaMemcpyDeviceToHost, st));
-  CK((++g_host_syncs, cudaStreamSynchronize(st)));
-  M.k = k;
-  M.cpts = c->buf<float4>(tag + ".cpts", k);
-  M.clw2 = c->buf<float>(tag + ".clw2", k);
-  M.cw64 = c->buf<double>(tag + ".cw64", k);
-  M.radii = c->buf<float>(tag + ".radii", k);
-  CK(cluster_stats(M.pts, M.w64, M.offsets, k, d, M.cpts, M.clw2, M.cw64, M.radii, st));
-  M.radii_h.resize(k);
-  CK(cudaMemcpyAsync(M.radii_h.data(), M.radii, k * sizeof(float), cudaMemcpyDeviceToHost, st));
-  M.offsets_h.resize(k + 1);
-  CK(cudaMemcpyAsync(M.offsets_h.data(), M.offsets, (k + 1) * sizeof(int32_t),
-                     cudaMemcpyDeviceToHost, st));
-  CK((++g_host_syncs, cudaStreamSynchronize(st)));
+  prepare_measures(c, {{tag, d_x, d_w, n, &M}}, d, g, clusters);
 }
 
 // Super level of the coarse phase (policy.h:msot_super_switch): consecutive
@@ -298,48 +370,70 @@ struct SuperMeasure {
   float* clw2 = nullptr;
 };
 
-void super_measure(msot_ctx* c, const std::string& tag, const DMeasure& M, int d,
-                   SuperMeasure& S) {
+void super_measures(msot_ctx* c, const DMeasure* const* Ms, const char* const* tags, int d,
+                    SuperMeasure* const* Ss, int count) {
   cudaStream_t st = c->st;
-  const int32_t k = M.k;
-  uint32_t* keys = c->buf<uint32_t>(tag + ".skeys", k);
-  CK(super_keys(c->buf<uint32_t>(tag + ".keys", M.n), M.offsets, k, d * MSOT_SUPER_SHIFT, keys, st));
-  uint8_t* flags = c->buf<uint8_t>(tag + ".sflags", k);
-  S.labels = c->buf<int32_t>(tag + ".slabels", k);
-  int32_t* offs = c->buf<int32_t>(tag + ".soffsets", k + 1);
-  int32_t* stmp = c->buf<int32_t>(tag + ".sstmp", scan_temp_elems(k));
-  int32_t* kdev = c->buf<int32_t>(tag + ".sk", 1);
-  CK(segment_flags(keys, k, flags, st));
-  CK((scan<uint8_t, int32_t>(flags, S.labels, k, true, stmp, kdev, st)));
-  CK(segment_offsets(S.labels, flags, k, offs, st));
-  CK(cudaMemcpyAsync(&S.k, kdev, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  CK((++g_host_syncs, cudaStreamSynchronize(st)));
-  S.cpts = c->buf<float4>(tag + ".scpts", S.k);
-  S.clw2 = c->buf<float>(tag + ".sclw2", S.k);
-  double* cw = c->buf<double>(tag + ".scw64", S.k);
-  float* rad = c->buf<float>(tag + ".srad", S.k);
-  CK(cluster_stats(M.cpts, M.cw64, offs, S.k, d, S.cpts, S.clw2, cw, rad, st));
+  c->pin_reserve(64);
+  int32_t* hk = c->pin<int32_t>(count);
+  std::vector<int32_t*> offs(count);
+  for (int q = 0; q < count; ++q) {
+    const DMeasure& M = *Ms[q];
+    SuperMeasure& S = *Ss[q];
+    const std::string tag = tags[q];
+    const int32_t k = M.k;
+    uint32_t* keys = c->buf<uint32_t>(tag + ".skeys", k);
+    CK(super_keys(c->buf<uint32_t>(tag + ".keys", M.n), M.offsets, k, d * MSOT_SUPER_SHIFT, keys, st));
+    uint8_t* flags = c->buf<uint8_t>(tag + ".sflags", k);
+    S.labels = c->buf<int32_t>(tag + ".slabels", k);
+    offs[q] = c->buf<int32_t>(tag + ".soffsets", k + 1);
+    int32_t* stmp = c->buf<int32_t>(tag + ".sstmp", scan_temp_elems(k));
+    int32_t* kdev = c->buf<int32_t>(tag + ".sk", 1);
+    CK(segment_flags(keys, k, flags, st));
+    CK((scan<uint8_t, int32_t>(flags, S.labels, k, true, stmp, kdev, st)));
+    CK(segment_offsets(S.labels, flags, k, offs[q], st));
+    CK(cudaMemcpyAsync(&hk[q], kdev, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  }
+  CK(host_sync(__LINE__, st));
+  for (int q = 0; q < count; ++q) {
+    const DMeasure& M = *Ms[q];
+    SuperMeasure& S = *Ss[q];
+    const std::string tag = tags[q];
+    S.k = hk[q];
+    S.cpts = c->buf<float4>(tag + ".scpts", S.k);
+    S.clw2 = c->buf<float>(tag + ".sclw2", S.k);
+    double* cw = c->buf<double>(tag + ".scw64", S.k);
+    float* rad = c->buf<float>(tag + ".srad", S.k);
+    CK(cluster_stats(M.cpts, M.cw64, offs[q], S.k, d, S.cpts, S.clw2, cw, rad, st));
+  }
 }
 
-// Occupied voxels of one cloud for a candidate edge (automatic edge rule).
-int64_t count_cells(msot_ctx* c, const double* d_x, int64_t n, const GridSpec& g) {
+// Occupied voxels of both clouds for a candidate edge (automatic edge rule),
+// one host wait: max(k_x, k_y).
+int64_t count_cells(msot_ctx* c, const double* d_x, int64_t n, const double* d_y, int64_t m,
+                    const GridSpec& g) {
   cudaStream_t st = c->st;
-  uint32_t* keys = c->buf<uint32_t>("cc.keys", n);
-  int32_t* vals = c->buf<int32_t>("cc.vals", n);
-  CK(cube_keys(d_x, n, g, keys, vals, st));
-  void* tmp = c->buf<char>("cc.rstmp", radix_temp_bytes(n));
+  const int64_t nm = std::max(n, m);
+  uint32_t* keys = c->buf<uint32_t>("cc.keys", nm);
+  int32_t* vals = c->buf<int32_t>("cc.vals", nm);
+  void* tmp = c->buf<char>("cc.rstmp", radix_temp_bytes(nm));
+  uint8_t* flags = c->buf<uint8_t>("cc.flags", nm);
+  int32_t* lab = c->buf<int32_t>("cc.lab", nm);
+  int32_t* stmp = c->buf<int32_t>("cc.stmp", scan_temp_elems(nm));
+  int32_t* kdev = c->buf<int32_t>("cc.k", 2);
   const int bits = g.d == 1 ? MSOT_MORTON_BITS : g.d == 2 ? 2 * MSOT_MORTON_BITS : 3 * MSOT_MORTON_BITS;
-  CK(radix_sort_pairs(keys, vals, n, bits, tmp, st));
-  uint8_t* flags = c->buf<uint8_t>("cc.flags", n);
-  int32_t* lab = c->buf<int32_t>("cc.lab", n);
-  int32_t* stmp = c->buf<int32_t>("cc.stmp", scan_temp_elems(n));
-  int32_t* kdev = c->buf<int32_t>("cc.k", 1);
-  CK(segment_flags(keys, n, flags, st));
-  CK((scan<uint8_t, int32_t>(flags, lab, n, true, stmp, kdev, st)));
-  int32_t k = 0;
-  CK(cudaMemcpyAsync(&k, kdev, sizeof(k), cudaMemcpyDeviceToHost, st));
-  CK((++g_host_syncs, cudaStreamSynchronize(st)));
-  return k;
+  const double* src[2] = {d_x, d_y};
+  const int64_t len[2] = {n, m};
+  for (int q = 0; q < 2; ++q) {  // same stream: the second cloud reuses the scratch
+    CK(cube_keys(src[q], len[q], g, keys, vals, st));
+    CK(radix_sort_pairs(keys, vals, len[q], bits, tmp, st));
+    CK(segment_flags(keys, len[q], flags, st));
+    CK((scan<uint8_t, int32_t>(flags, lab, len[q], true, stmp, kdev + q, st)));
+  }
+  c->pin_reserve(64);
+  int32_t* hk = c->pin<int32_t>(2);
+  CK(cudaMemcpyAsync(hk, kdev, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CK(host_sync(__LINE__, st));
+  return std::max(hk[0], hk[1]);
 }
 
 // ------------------------------------------------------------------ ranges
@@ -363,9 +457,10 @@ void make_tiles(msot_ctx* c, const std::string& tag, int64_t rows,
   R.n_tiles = msot_row_tiles(offsets ? offsets->data() : nullptr, k, rows, R.tile_rows, ts.data());
   R.tile_start_h.assign(ts.begin(), ts.begin() + R.n_tiles + 1);
   R.tile_start = c->buf<int32_t>(tag + ".tstart", R.n_tiles + 1);
+  // pageable host -> device: the driver stages the source before returning,
+  // so the host vector may change afterwards without a wait
   CK(cudaMemcpyAsync(R.tile_start, R.tile_start_h.data(), (R.n_tiles + 1) * sizeof(int32_t),
                      cudaMemcpyHostToDevice, c->st));
-  CK((++g_host_syncs, cudaStreamSynchronize(c->st)));  // host vector may be reallocated by the caller
 }
 
 void dense_rangeset(msot_ctx* c, const std::string& tag, int64_t rows, int64_t cols, RangeSet& R,
@@ -399,7 +494,7 @@ void mask_rangeset(msot_ctx* c, const std::string& tag, const int32_t* rl,
   R.tile_cols_h.resize(R.n_tiles);
   CK(cudaMemcpyAsync(R.tile_cols_h.data(), R.tile_cols, R.n_tiles * sizeof(int64_t),
                      cudaMemcpyDeviceToHost, st));
-  CK((++g_host_syncs, cudaStreamSynchronize(st)));
+  CK(host_sync(__LINE__, st));
   R.ranges = c->buf<int2>(tag + ".ranges", R.n_ranges);
   CK(tile_range_write(tbits, ky, R.n_tiles, co, R.rptr, R.ranges, st));
 }
@@ -416,15 +511,28 @@ struct SymSet {
   int32_t* etile = nullptr;
   std::vector<int64_t> tslot_h;  // host copy of tslot (batch bases)
   int64_t slots = 0, entries = 0;
+  // sym_rangeset_a -> _b: device scratch and the pinned landing of the counts
+  uint32_t* tbits = nullptr;
+  int32_t* posword = nullptr;
+  int64_t* h_tot = nullptr;   // pinned: ranges, slots, entries
+  int64_t* h_tc = nullptr;    // pinned: tile_cols
+  const int32_t* rl = nullptr;
+  const int32_t* co = nullptr;
+  int32_t ky = 0;
   bool dense = false;         // dense_symset: column sums by hd_colsum (no entries)
 };
 
-void sym_rangeset(msot_ctx* c, const std::string& tag, const int32_t* rl,
-                  const std::vector<int32_t>& ro, int64_t n_rows, const int32_t* co, int32_t ky,
-                  const uint32_t* mask, int self, SymSet& S) {
+// Phase A: tile OR, per-tile range / slot / entry counts and their scans;
+// the totals and per-tile column counts land in pinned memory (no wait).
+void sym_rangeset_a(msot_ctx* c, const std::string& tag, const int32_t* rl,
+                    const std::vector<int32_t>& ro, int64_t n_rows, const int32_t* co, int32_t ky,
+                    const uint32_t* mask, int self, SymSet& S) {
   cudaStream_t st = c->st;
   RangeSet& R = S.R;
   S.self = self;
+  S.rl = rl;
+  S.co = co;
+  S.ky = ky;
   if (R.tile_start_h.empty()) make_tiles(c, tag, n_rows, &ro, R);  // fixed per solve
   const int64_t T = R.n_tiles;
   const int32_t words = mask_words(ky);
@@ -433,10 +541,10 @@ void sym_rangeset(msot_ctx* c, const std::string& tag, const int32_t* rl,
   R.rptr = c->buf<int64_t>(tag + ".rptr", T + 1);
   S.tslot = c->buf<int64_t>(tag + ".tslot", T + 1);
   int64_t* stmp = c->buf<int64_t>(tag + ".stmp", scan_temp_elems(T + 1));
-  uint32_t* tbits = c->buf<uint32_t>(tag + ".tbits", size_t(T) * words);
-  int32_t* posword = c->buf<int32_t>(tag + ".posw", size_t(T) * words);
-  CK(tile_or(mask, ky, rl, R.tile_start, T, tbits, st));
-  CK(sym_ranges(tbits, ky, T, co, R.tile_start, rl, self, nr, R.tile_cols, posword, nullptr,
+  S.tbits = c->buf<uint32_t>(tag + ".tbits", size_t(T) * words);
+  S.posword = c->buf<int32_t>(tag + ".posw", size_t(T) * words);
+  CK(tile_or(mask, ky, rl, R.tile_start, T, S.tbits, st));
+  CK(sym_ranges(S.tbits, ky, T, co, R.tile_start, rl, self, nr, R.tile_cols, S.posword, nullptr,
                 nullptr, false, st));
   CK(cudaMemsetAsync(nr + T, 0, sizeof(int64_t), st));
   CK(cudaMemsetAsync(R.tile_cols + T, 0, sizeof(int64_t), st));
@@ -447,30 +555,61 @@ void sym_rangeset(msot_ctx* c, const std::string& tag, const int32_t* rl,
   int32_t* ecnt = c->buf<int32_t>(tag + ".ecnt", ne + 1);
   S.ebase = c->buf<int64_t>(tag + ".ebase", ne + 1);
   int64_t* etmp = c->buf<int64_t>(tag + ".etmp", scan_temp_elems(ne + 1));
-  CK(sym_entries(tbits, ky, T, co, R.tile_start, rl, self, posword, S.tslot, ecnt, nullptr,
+  CK(sym_entries(S.tbits, ky, T, co, R.tile_start, rl, self, S.posword, S.tslot, ecnt, nullptr,
                  nullptr, nullptr, false, st));
   CK(cudaMemsetAsync(ecnt + ne, 0, sizeof(int32_t), st));
   CK((scan<int32_t, int64_t>(ecnt, S.ebase, ne + 1, false, etmp, nullptr, st)));
-  int64_t tot[3];
-  CK(cudaMemcpyAsync(&tot[0], R.rptr + T, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&tot[1], S.tslot + T, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&tot[2], S.ebase + ne, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  R.tile_cols_h.resize(T);
-  CK(cudaMemcpyAsync(R.tile_cols_h.data(), R.tile_cols, T * sizeof(int64_t),
-                     cudaMemcpyDeviceToHost, st));
-  CK((++g_host_syncs, cudaStreamSynchronize(st)));
-  R.n_ranges = tot[0];
-  S.slots = tot[1];
-  S.entries = tot[2];
+  S.h_tot = c->pin<int64_t>(3);
+  S.h_tc = c->pin<int64_t>(T);
+  CK(cudaMemcpyAsync(&S.h_tot[0], R.rptr + T, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&S.h_tot[1], S.tslot + T, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&S.h_tot[2], S.ebase + ne, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(S.h_tc, R.tile_cols, T * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+}
+
+// Phase B (after the caller's one sync): the ranges and the entries.
+void sym_rangeset_b(msot_ctx* c, const std::string& tag, SymSet& S) {
+  cudaStream_t st = c->st;
+  RangeSet& R = S.R;
+  const int64_t T = R.n_tiles;
+  R.n_ranges = S.h_tot[0];
+  S.slots = S.h_tot[1];
+  S.entries = S.h_tot[2];
+  R.tile_cols_h.assign(S.h_tc, S.h_tc + T);
   S.tslot_h.assign(T + 1, 0);
   for (int64_t t = 0; t < T; ++t) S.tslot_h[t + 1] = S.tslot_h[t] + R.tile_cols_h[t];
   R.ranges = c->buf<int2>(tag + ".ranges", R.n_ranges);
-  CK(sym_ranges(tbits, ky, T, co, R.tile_start, rl, self, nullptr, nullptr, nullptr, R.rptr,
-                R.ranges, true, st));
+  CK(sym_ranges(S.tbits, S.ky, T, S.co, R.tile_start, S.rl, S.self, nullptr, nullptr, nullptr,
+                R.rptr, R.ranges, true, st));
   S.eslot = c->buf<int64_t>(tag + ".eslot", S.entries);
   S.etile = c->buf<int32_t>(tag + ".etile", S.entries);
-  CK(sym_entries(tbits, ky, T, co, R.tile_start, rl, self, posword, S.tslot, nullptr, S.ebase,
-                 S.eslot, S.etile, true, st));
+  CK(sym_entries(S.tbits, S.ky, T, S.co, R.tile_start, S.rl, S.self, S.posword, S.tslot, nullptr,
+                 S.ebase, S.eslot, S.etile, true, st));
+}
+
+// The pair sets of several evaluate-once problems with one host wait.
+struct SymJob {
+  std::string tag;
+  const int32_t* rl;
+  const std::vector<int32_t>* ro;
+  int64_t n_rows;
+  const int32_t* co;
+  int32_t ky;
+  const uint32_t* mask;
+  int self;
+  SymSet* S;
+};
+void sym_rangesets(msot_ctx* c, const std::vector<SymJob>& jobs) {
+  size_t need = 0;
+  for (const SymJob& j : jobs) {  // tiles are fixed per solve: make them before reserving
+    if (j.S->R.tile_start_h.empty()) make_tiles(c, j.tag, j.n_rows, j.ro, j.S->R);
+    need += (j.S->R.n_tiles + 3) * sizeof(int64_t) + 64;
+  }
+  c->pin_reserve(need);
+  for (const SymJob& j : jobs)
+    sym_rangeset_a(c, j.tag, j.rl, *j.ro, j.n_rows, j.co, j.ky, j.mask, j.self, *j.S);
+  CK(host_sync(__LINE__, c->st));
+  for (const SymJob& j : jobs) sym_rangeset_b(c, j.tag, *j.S);
 }
 
 // Dense evaluate-once pair sets (high-D path): uniform 256-row tiles; self
@@ -505,8 +644,7 @@ void dense_symset(msot_ctx* c, const std::string& tag, int64_t n_rows, int64_t n
   CK(cudaMemcpyAsync(S.tslot, tslot.data(), (T + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
   R.tile_cols_h = tcols;
   S.slots = tslot[T];
-  S.tslot_h = tslot;
-  CK((++g_host_syncs, cudaStreamSynchronize(st)));  // host vectors go out of scope
+  S.tslot_h = tslot;  // (pageable H2D copies above are staged before they return)
 }
 
 // ------------------------------------------------------------ launch plans
@@ -688,8 +826,14 @@ void build_plan(msot_ctx* c, const std::string& tag, Plan& P, int waves = 32, in
   }
   CK(cudaMemsetAsync(cnt + off, 0, sizeof(int32_t), st));
   CK((scan<int32_t, int32_t>(cnt, ib, off + 1, false, stmp, nullptr, st)));
-  CK(cudaMemcpyAsync(&P.n_items, ib + off, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  CK((++g_host_syncs, cudaStreamSynchronize(st)));
+  // the item count follows from the host copy of the tile column counts
+  // (item_counts_kernel's rule): no device read
+  int64_t n_items = 0;
+  for (int p = 0; p < P.np; ++p)
+    for (int64_t t = P.t0[p]; t < P.t1[p]; ++t)
+      n_items += std::max<int64_t>(1, (P.ps[p].rs->tile_cols_h[t] + chunk - 1) / chunk);
+  if (n_items > 0x7fffffffLL) raise(MSOT_EUSAGE, "too many work items");
+  P.n_items = static_cast<int32_t>(n_items);
   P.items = c->buf<int4>(tag + ".items", P.n_items);
   for (int p = 0; p < P.np; ++p)
     CK(item_write(P.ps[p].rs->tile_cols, P.t0[p], P.t1[p], chunk, P.ibase[p], p, P.items, st));
@@ -1038,7 +1182,7 @@ void capture_pots(msot_ctx* c, float* const* v, const int32_t* xperm, const int3
     if (!host[q]) continue;
     CK(scatter_unsort(v[q], perm[q], len[q], nullptr, 0.0, tmp, c->st));
     CK(cudaMemcpyAsync(host[q], tmp, len[q] * sizeof(double), cudaMemcpyDeviceToHost, c->st));
-    CK((++g_host_syncs, cudaStreamSynchronize(c->st)));
+    CK(host_sync(__LINE__, c->st));
   }
 }
 
@@ -1053,7 +1197,7 @@ void capture_masks(msot_ctx* c, const uint32_t* const* masks, const int32_t* kr,
     CK(unpack_mask(masks[q], kr[q], kc[q], dm, st));
     c->cap_mask[q].resize(cells);
     CK(cudaMemcpyAsync(c->cap_mask[q].data(), dm, cells, cudaMemcpyDeviceToHost, st));
-    CK((++g_host_syncs, cudaStreamSynchronize(st)));
+    CK(host_sync(__LINE__, st));
     c->cap_k[q][0] = kr[q];
     c->cap_k[q][1] = kc[q];
   }
@@ -1062,7 +1206,7 @@ void capture_masks(msot_ctx* c, const uint32_t* const* masks, const int32_t* kr,
     std::vector<int32_t> lab(M[s]->n), perm(M[s]->n);
     CK(cudaMemcpyAsync(lab.data(), M[s]->labels, M[s]->n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(perm.data(), M[s]->perm, M[s]->n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    CK((++g_host_syncs, cudaStreamSynchronize(st)));
+    CK(host_sync(__LINE__, st));
     c->cap_lab[s].assign(M[s]->n, -1);
     for (int64_t k = 0; k < M[s]->n; ++k) c->cap_lab[s][perm[k]] = lab[k];
   }
@@ -1220,7 +1364,7 @@ void hd_layout(msot_ctx* c, const std::string& tag, const double* dx, const doub
   CK(cudaMemcpyAsync(off_h.data(), off, (K + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(perm_h.data(), perm, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(L.radii_h.data(), L.radii, K * sizeof(float), cudaMemcpyDeviceToHost, st));
-  CK((++g_host_syncs, cudaStreamSynchronize(st)));
+  CK(host_sync(__LINE__, st));
   L.poff_h.assign(K + 1, 0);
   for (int I = 0; I < K; ++I)
     L.poff_h[I + 1] = L.poff_h[I] + (off_h[I + 1] - off_h[I] + 127) / 128 * 128;
@@ -1256,7 +1400,7 @@ void hd_layout(msot_ctx* c, const std::string& tag, const double* dx, const doub
   L.clw2 = c->buf<float>(tag + ".clw2", K);
   L.cw64 = c->buf<double>(tag + ".cw64", K);
   CK(hd_weights(cw, K, L.clw2, L.cw64, st));
-  CK((++g_host_syncs, cudaStreamSynchronize(st)));  // host vectors go out of scope
+  CK(host_sync(__LINE__, st));  // host vectors go out of scope
 }
 
 void hd_multiscale(msot_ctx* c, const msot_params* prm, const double* d_x, const double* d_a,
@@ -1413,9 +1557,9 @@ void hd_multiscale(msot_ctx* c, const msot_params* prm, const double* d_x, const
                            theta, 1, myy, nullptr, byr, nullptr, st));
     CK(truncation_masks_hd(kx, ky, d, LX.centers, LX.radii, fm[3], LY.centers, LY.radii, fm[2], e,
                            theta, 0, mxy, myx, bxr, byr, st));
-    sym_rangeset(c, "hs.xx", LX.labels, LX.poff_h, nr, LX.poff, kx, mxx, 1, sxx);
-    sym_rangeset(c, "hs.yy", LY.labels, LY.poff_h, mr, LY.poff, ky, myy, 1, syy);
-    sym_rangeset(c, "hs.yx", LX.labels, LX.poff_h, nr, LY.poff, ky, mxy, 0, syx);
+    sym_rangesets(c, {{"hs.xx", LX.labels, &LX.poff_h, nr, LX.poff, kx, mxx, 1, &sxx},
+                      {"hs.yy", LY.labels, &LY.poff_h, mr, LY.poff, ky, myy, 1, &syy},
+                      {"hs.yx", LX.labels, &LX.poff_h, nr, LY.poff, ky, mxy, 0, &syx}});
     Pf.np = 3;
     Pf.ps[0] = {nullptr, nr, nullptr, LX.lw2, nr, &sxx.R, {LX.pack, LX.pack, LX.sq, LX.sq, LX.f, LX.f}, &sxx, LX.lw2};
     Pf.ps[1] = {nullptr, mr, nullptr, LY.lw2, mr, &syy.R, {LY.pack, LY.pack, LY.sq, LY.sq, LY.f, LY.f}, &syy, LY.lw2};
@@ -1470,7 +1614,7 @@ void transfer_labels_dev(msot_ctx* c, const LabelReq& q, const DMeasure& X, cons
   if (Y.perm) {
     std::vector<int32_t> perm(Y.n);
     CK(cudaMemcpyAsync(perm.data(), Y.perm, Y.n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    CK((++g_host_syncs, cudaStreamSynchronize(st)));
+    CK(host_sync(__LINE__, st));
     for (int64_t k = 0; k < Y.n; ++k)
       if (perm[k] >= 0) solver_of[perm[k]] = static_cast<int32_t>(k);
   } else {
@@ -1564,7 +1708,7 @@ void transfer_labels_dev(msot_ctx* c, const LabelReq& q, const DMeasure& X, cons
   }
   CK(hd ? launch_softmin_hd(G, d, c->n_sm, false, st) : launch_softmin(G, d, st));
   CK(label_finalize(G.part, dlbase, R.tile_start, T, L, X.perm, q.d_scores, q.d_mass, st));
-  CK((++g_host_syncs, cudaStreamSynchronize(st)));  // host vectors above go out of scope
+  CK(host_sync(__LINE__, st));  // host vectors above go out of scope
 }
 
 void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const double* d_a,
@@ -1599,7 +1743,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
   int32_t nbad = 0;
   CK(cudaMemcpyAsync(lh.data(), lohi, 2 * d * sizeof(long long), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(&nbad, badw, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  CK((++g_host_syncs, cudaStreamSynchronize(st)));
+  CK(host_sync(__LINE__, st));
   if (nbad) raise(MSOT_EDATA, "weights must be finite and > 0");
   std::vector<double> lov(std::max(d, 3), 0.0), hiv(std::max(d, 3), 0.0);
   double* lo = lov.data();
@@ -1729,13 +1873,12 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
   if (ms && prm->cluster_scale <= 0) {  // policy.h: refine on occupied voxels
     for (int it = 0; it < MSOT_AUTO_REFINE; ++it) {
       g.cell = cell;
-      const int64_t kk = std::max(count_cells(c, d_x, n, g), count_cells(c, d_y, m, g));
+      const int64_t kk = count_cells(c, d_x, n, d_y, m, g);
       cell = msot_refine_cell(cell, kk, n, m, d, lo, hi);
     }
   }
   g.cell = cell;
-  prepare_measure(c, "x", d_x, d_a, n, d, g, ms, X);
-  prepare_measure(c, "y", d_y, d_b, m, d, g, ms, Y);
+  prepare_measures(c, {{"x", d_x, d_a, n, &X}, {"y", d_y, d_b, m, &Y}}, d, g, ms);
 
   if (!ms) {
     // dense solves stay row-wise (4 problems per scale): the cross potentials
@@ -1826,8 +1969,10 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
                                        prm->super_level);
       if (t2 > 0) {
         SuperMeasure SX, SY;
-        super_measure(c, "x", X, d, SX);
-        super_measure(c, "y", Y, d, SY);
+        const DMeasure* ms2[2] = {&X, &Y};
+        const char* tg2[2] = {"x", "y"};
+        SuperMeasure* ss2[2] = {&SX, &SY};
+        super_measures(c, ms2, tg2, d, ss2, 2);
         S->t_super = t2;
         S->k_super_x = SX.k;
         S->k_super_y = SY.k;
@@ -1998,13 +2143,13 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
           CK(mask_pair_count(myx, Y.k, X.k, Y.offsets, X.offsets, cnt, st));
         double h = 0.0;
         CK(cudaMemcpyAsync(&h, cnt, sizeof(double), cudaMemcpyDeviceToHost, st));
-        CK((++g_host_syncs, cudaStreamSynchronize(st)));
+        CK(host_sync(__LINE__, st));
         mask_terms = h;
       }
       if (once) {  // evaluate-once pair sets (oracle.cpp: sym_self, transpose_ranges)
-        sym_rangeset(c, "s.xx", X.labels, X.offsets_h, n, X.offsets, X.k, mxx, 1, sxx);
-        sym_rangeset(c, "s.yy", Y.labels, Y.offsets_h, m, Y.offsets, Y.k, myy, 1, syy);
-        sym_rangeset(c, "s.yx", X.labels, X.offsets_h, n, Y.offsets, Y.k, mxy, 0, syx);
+        sym_rangesets(c, {{"s.xx", X.labels, &X.offsets_h, n, X.offsets, X.k, mxx, 1, &sxx},
+                          {"s.yy", Y.labels, &Y.offsets_h, m, Y.offsets, Y.k, myy, 1, &syy},
+                          {"s.yx", X.labels, &X.offsets_h, n, Y.offsets, Y.k, mxy, 0, &syx}});
         Pf.np = 3;
         Pf.ps[0] = {X.pts, n, X.pts, X.lw2, n, &sxx.R, {}, &sxx, X.lw2};
         Pf.ps[1] = {Y.pts, m, Y.pts, Y.lw2, m, &syy.R, {}, &syy, Y.lw2};
@@ -2119,13 +2264,13 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
       if (!h_pots[q]) continue;
       CK(scatter_unsort(f[q], perm[q], len[q], lout + 3, sign[q], tmp, st));
       CK(cudaMemcpyAsync(h_pots[q], tmp, outn[q] * sizeof(double), cudaMemcpyDeviceToHost, st));
-      CK((++g_host_syncs, cudaStreamSynchronize(st)));
+      CK(host_sync(__LINE__, st));
       S->d2h_bytes += outn[q] * sizeof(double);
     }
   }
   c->mark(-1);
   CK(cudaEventRecord(c->t1, st));
-  CK((++g_host_syncs, cudaStreamSynchronize(st)));
+  CK(host_sync(__LINE__, st));
   float ms_total = 0.f;
   CK(cudaEventElapsedTime(&ms_total, c->t0, c->t1));
   S->total_ms = ms_total;
@@ -2147,6 +2292,10 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
   S->fallback_rows = fbt;
   S->gpu_launches = g_launches - launches0;
   S->host_syncs = g_host_syncs - syncs0;
+  if (getenv("MSOT_DEBUG_SYNCS")) {
+    for (const auto& kv : g_sync_sites) fprintf(stderr, "[msot] sync at solver.cu:%d x%d\n", kv.first, kv.second);
+    g_sync_sites.clear();
+  }
   S->device_bytes = 0.0;
   for (const auto& kv : c->bufs) S->device_bytes += static_cast<double>(kv.second.second);
   S->d2h_bytes += sizeof(res);
@@ -2358,6 +2507,7 @@ void msot_destroy(msot_ctx* c) {
     if (c->ev_cs[k]) cudaEventDestroy(c->ev_cs[k]);
   }
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->pin_base) cudaFreeHost(c->pin_base);
   if (c->st) cudaStreamDestroy(c->st);
   delete c;
 }
@@ -2386,7 +2536,7 @@ int msot_probe_ex2(msot_ctx* c, double* ex2_per_s) {
     CK(cudaEventRecord(c->t0, c->st));
     for (int r = 0; r < 5; ++r) CK(ex2_probe(c->n_sm, iters, sink, &per, &blocks, c->st));
     CK(cudaEventRecord(c->t1, c->st));
-    CK((++g_host_syncs, cudaStreamSynchronize(c->st)));
+    CK(host_sync(__LINE__, c->st));
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, c->t0, c->t1));
     *ex2_per_s = 5.0 * per / (ms * 1e-3);
@@ -2466,7 +2616,7 @@ int msot_sinkhorn_grad(msot_ctx* c, const msot_params* prm, const double* x, con
     CK(cudaMemcpyAsync(db, b, m * sizeof(double), cudaMemcpyHostToDevice, c->st));
     solve_device(c, prm, dx, da, n, dy, db, m, d, loss_out, S, nullptr, dg);
     CK(cudaMemcpyAsync(grad_x, dg, n * d * sizeof(double), cudaMemcpyDeviceToHost, c->st));
-    CK((++g_host_syncs, cudaStreamSynchronize(c->st)));
+    CK(host_sync(__LINE__, c->st));
   });
 }
 
@@ -2547,7 +2697,7 @@ int msot_transfer_labels(msot_ctx* c, const msot_params* prm, const double* x, c
     CK(cudaMemcpyAsync(scores, q.d_scores, size_t(n) * n_classes * sizeof(double),
                        cudaMemcpyDeviceToHost, c->st));
     CK(cudaMemcpyAsync(row_mass, q.d_mass, n * sizeof(double), cudaMemcpyDeviceToHost, c->st));
-    CK((++g_host_syncs, cudaStreamSynchronize(c->st)));
+    CK(host_sync(__LINE__, c->st));
   });
 }
 
@@ -2611,7 +2761,7 @@ int msot_barycenter(msot_ctx* c, const msot_params* prm, const double* x0, const
       for (int t = 0; t < k; ++t) CK(bbox(dy[t], ms[t], d, lohi, false, st));
       std::vector<long long> lh(2 * d);
       CK(cudaMemcpyAsync(lh.data(), lohi, 2 * d * sizeof(long long), cudaMemcpyDeviceToHost, st));
-      CK((++g_host_syncs, cudaStreamSynchronize(st)));
+      CK(host_sync(__LINE__, st));
       std::vector<double> lo(d), hi(d);
       bbox_decode(lh.data(), d, lo.data(), hi.data());
       double d2 = 0.0;
@@ -2670,7 +2820,7 @@ int msot_barycenter(msot_ctx* c, const msot_params* prm, const double* x0, const
       if (rel < tol) break;
     }
     CK(cudaMemcpyAsync(x_out, dx, n * d * sizeof(double), cudaMemcpyDeviceToHost, st));
-    CK((++g_host_syncs, cudaStreamSynchronize(st)));
+    CK(host_sync(__LINE__, st));
     if (steps_done) *steps_done = done;
   });
 }
@@ -2710,7 +2860,7 @@ int msot_softmin(msot_ctx* c, const double* x, int64_t n, const double* y, int64
     prepare_measure(c, "sm", dx64, dw64, n, d, g, false, MX);
     std::vector<int32_t> perm(n);
     CK(cudaMemcpyAsync(perm.data(), MX.perm, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    CK((++g_host_syncs, cudaStreamSynchronize(st)));
+    CK(host_sync(__LINE__, st));
     std::vector<float4> yp(m);
     std::vector<float> yl(m), hh(m), fe(n, 0.f);
     if (f_est)
@@ -2763,7 +2913,7 @@ int msot_softmin(msot_ctx* c, const double* x, int64_t n, const double* y, int64
     c->world = world;
     std::vector<float> fo(n);
     CK(cudaMemcpyAsync(fo.data(), dfo, n * sizeof(float), cudaMemcpyDeviceToHost, st));
-    CK((++g_host_syncs, cudaStreamSynchronize(st)));
+    CK(host_sync(__LINE__, st));
     for (int64_t s = 0; s < n; ++s) f_out[perm[s]] = fo[s];
   });
 }
@@ -2801,7 +2951,7 @@ int msot_plan_apply(msot_ctx* c, const double* x, const double* a, int64_t n, co
     prepare_measure(c, "pa", dx64, da64, n, d, gs, false, MX);
     std::vector<int32_t> perm(n);
     CK(cudaMemcpyAsync(perm.data(), MX.perm, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    CK((++g_host_syncs, cudaStreamSynchronize(st)));
+    CK(host_sync(__LINE__, st));
     std::vector<float4> yp(m), pay(m);
     std::vector<float> yl(m), gg(m), ff(n);
     for (int64_t s = 0; s < n; ++s) ff[s] = static_cast<float>(f[perm[s]]);
@@ -2834,7 +2984,7 @@ int msot_plan_apply(msot_ctx* c, const double* x, const double* a, int64_t n, co
     plan_group(c, "ppa", 1, &spec, fr, gc, py, po, eps, d);
     std::vector<float4> o(n);
     CK(cudaMemcpyAsync(o.data(), dout, n * sizeof(float4), cudaMemcpyDeviceToHost, st));
-    CK((++g_host_syncs, cudaStreamSynchronize(st)));
+    CK(host_sync(__LINE__, st));
     // row_plan = {sum_j pi_ij / a_i, sum_j pi_ij v_j / a_i, ...}
     for (int64_t s = 0; s < n; ++s) out[perm[s]] = a[perm[s]] * static_cast<double>(o[s].y);
   });
@@ -2879,7 +3029,7 @@ int msot_kmeans(msot_ctx* c, const double* x, const double* w, int64_t n, int d,
     CK(cudaMemcpyAsync(centroids, dcen, size_t(k) * d * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(cweights, dcw, k * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(radii, drad, k * sizeof(float), cudaMemcpyDeviceToHost, st));
-    CK((++g_host_syncs, cudaStreamSynchronize(st)));
+    CK(host_sync(__LINE__, st));
     if (iters) *iters = it;
   });
 }
@@ -2911,7 +3061,7 @@ int msot_grid_cluster(msot_ctx* c, const double* x, const double* w, int64_t n, 
     CK(cudaMemcpyAsync(cp.data(), M.cpts, M.k * sizeof(float4), cudaMemcpyDeviceToHost, st));
     if (cweights) CK(cudaMemcpyAsync(cweights, M.cw64, M.k * sizeof(double), cudaMemcpyDeviceToHost, st));
     if (radii) CK(cudaMemcpyAsync(radii, M.radii, M.k * sizeof(float), cudaMemcpyDeviceToHost, st));
-    CK((++g_host_syncs, cudaStreamSynchronize(st)));
+    CK(host_sync(__LINE__, st));
     *k_out = M.k;
     if (centroids)
       for (int32_t I = 0; I < M.k; ++I) {
@@ -2974,7 +3124,7 @@ int msot_truncation_mask(msot_ctx* c, int64_t kx, int64_t ky, int d, const float
                         dcy, dry, dgy, dhy, eps, theta, self, dbits, nullptr, dbr, dbc, bws, st));
     CK(unpack_mask(dbits, static_cast<int32_t>(kx), static_cast<int32_t>(ky), dm, st));
     CK(cudaMemcpyAsync(mask_out, dm, kx * ky, cudaMemcpyDeviceToHost, st));
-    CK((++g_host_syncs, cudaStreamSynchronize(st)));
+    CK(host_sync(__LINE__, st));
   });
 }
 

@@ -208,10 +208,13 @@ constexpr int64_t kColpartPerAtom = 6;
 // The two exchange steps of a sharded scale: an all-reduce of
 // the column sums and a broadcast of every rank's row shard.  NCCL over
 // NVLink in the product; host-staged caller callbacks in the test seam.
+// A communicator of one rank (msot_create_dist with world = 1) runs the NCCL
+// calls too: they are no-ops on the data, but the product's NCCL path is
+// exercised on a one-GPU box (tests/test_dist_gpu.py).
 void coll_allreduce(msot_ctx* c, float* const* bufs, const int64_t* counts, int nb) {
-  if (c->world <= 1) return;
+  if (!c->comm && (c->world <= 1 || !c->host_ar)) return;
   cudaStream_t st = c->st;
-  if (c->host_ar) {
+  if (!c->comm) {
     for (int b = 0; b < nb; ++b) {
       std::vector<float> h(counts[b]);
       CK(cudaMemcpyAsync(h.data(), bufs[b], counts[b] * sizeof(float), cudaMemcpyDeviceToHost, st));
@@ -229,9 +232,9 @@ void coll_allreduce(msot_ctx* c, float* const* bufs, const int64_t* counts, int 
 }
 
 void coll_bcast_rows(msot_ctx* c, float* const* bufs, const std::vector<int64_t>* bounds, int nb) {
-  if (c->world <= 1) return;
+  if (!c->comm && (c->world <= 1 || !c->host_bc)) return;
   cudaStream_t st = c->st;
-  if (c->host_bc) {
+  if (!c->comm) {
     for (int b = 0; b < nb; ++b)
       for (int r = 0; r < c->world; ++r) {
         const int64_t b0 = bounds[b][r], b1 = bounds[b][r + 1];
@@ -2108,7 +2111,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
         CK(truncation_masks_rows(X.k, Y.k, d, X.cpts, X.radii, fmax[3], g[3], Y.cpts, Y.radii,
                                  fmax[2], g[2], e, theta, 0, cut(X.k, rk), cut(X.k, rk + 1), mxy,
                                  bxr, bws, st));
-        if (wd > 1) {
+        if (wd > 1 || c->comm) {
           std::vector<int64_t> bnd[3];
           const int32_t kr[3] = {X.k, Y.k, X.k}, kc[3] = {X.k, Y.k, Y.k};
           for (int q = 0; q < 3; ++q) {
@@ -2408,7 +2411,7 @@ int msot_create_dist(int device, int rank, int world, const unsigned char nccl_i
       create_common(device, out, c);
       c->rank = rank;
       c->world = world;
-      if (world > 1) {
+      {  // world 1 too: a one-rank communicator (see coll_allreduce)
         ncclUniqueId id;
         std::memcpy(&id, nccl_id, 128);
         NK(ncclCommInitRank(&c->comm, world, id, rank));
@@ -2453,7 +2456,7 @@ int msot_world_info(const msot_ctx* c, int* rank, int* world, int* comm_ranks) {
     if (rank) *rank = c->rank;
     if (world) *world = c->world;
     if (comm_ranks) {
-      int n = c->world > 1 ? 0 : 1;  // no communicator at world 1
+      int n = c->world > 1 ? 0 : 1;  // msot_create: no communicator at world 1
       if (c->comm) NK(ncclCommCount(c->comm, &n));
       else if (c->host_ar) n = c->world;  // host-collective test seam
       *comm_ranks = n;

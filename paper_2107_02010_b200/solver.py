@@ -302,7 +302,9 @@ class Context:
             self._cbs = (_AR_FN(_ar), _BC_FN(_bc))  # keep alive
             _check(lib().msot_create_dist_host(device, rank, world, self._cbs[0], self._cbs[1],
                                                None, C.byref(self._h)))
-        elif world > 1:
+        elif world > 1 or nccl_id is not None:
+            # one process per GPU; world 1 with an id = a one-rank communicator
+            # (the NCCL calls run, as no-ops on the data)
             if nccl_id is None or len(nccl_id) != 128:
                 raise ValueError("world > 1 needs the 128-byte NCCL id of rank 0")
             _check(lib().msot_create_dist(device, rank, world, bytes(nccl_id), C.byref(self._h)))

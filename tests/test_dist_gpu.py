@@ -152,6 +152,28 @@ def test_three_ranks_match_one(ctx, case):
         assert abs(l3 - l1) <= 1e-6 * abs(l1) + 1e-12
 
 
+@pytest.mark.parametrize("case", ["dense", "multiscale", "unbalanced", "hd_ms"])
+def test_nccl_one_rank_communicator(ctx, case):
+    """The product's NCCL path on one GPU: a context made by msot_create_dist
+    with world = 1 holds a one-rank communicator, and the solver issues its
+    real ncclAllReduce (column sums) and grouped ncclBroadcast (row shards,
+    mask row blocks) calls on the solver stream.  With one rank they move no
+    data, so the result must equal the communicator-less solve bitwise."""
+    from paper_2107_02010_b200.solver import Context
+    x, a, y, b = _inputs(case)
+    l1, p1, _ = ctx.sinkhorn(_params(case), x, a, y, b)
+    c1 = Context(0, 0, 1, Context.nccl_unique_id())
+    try:
+        assert c1.world_info() == (0, 1, 1)  # ncclCommCount
+        l2, p2, st = c1.sinkhorn(_params(case), x, a, y, b)
+    finally:
+        c1.close()
+    assert st["world"] == 1
+    for u, v in zip([p2.a_xx, p2.b_yy, p2.a_xy, p2.b_yx], [p1.a_xx, p1.b_yy, p1.a_xy, p1.b_yx]):
+        np.testing.assert_array_equal(u, v)
+    assert l2 == l1
+
+
 if __name__ == "__main__":
     import sys
     for case in sys.argv[1:]:

@@ -492,7 +492,7 @@ def main():
     }
     if extras is not None:
         line["extra_configs"] = extras
-    if not args.no_cpu:
+    if not args.no_cpu and world == 1:  # the CPU baseline runs on rank 0 at N = 1 only
         line["cpu_baseline"] = cpu_baseline(st, extras)
     os.makedirs(os.path.dirname(PAIRS_FILE), exist_ok=True)
     if w["n"] == WORKLOAD["n"] and world == 1:

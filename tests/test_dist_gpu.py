@@ -36,6 +36,10 @@ CASES = {
 
 
 def _inputs(case):
+    if case == "bench":  # bench.py's generator and parameters at 30k
+        import bench
+        w = dict(bench.WORKLOAD, n=30000, m=30000)
+        return bench.make_inputs(w)
     if case.startswith("hd"):
         from paper_2107_02010_b200 import workloads as W
         fa, _ = W.fibres(700, 3)
@@ -49,6 +53,9 @@ def _inputs(case):
 
 def _params(case):
     from paper_2107_02010_b200.abi import make_params
+    if case == "bench":
+        import bench
+        return bench.params(dict(bench.WORKLOAD, n=30000, m=30000))
     if case == "hd":
         return make_params(blur=0.05, reach=0.3)
     if case == "hd_ms":
@@ -57,10 +64,11 @@ def _params(case):
     return make_params(**CASES[case])
 
 
-def _worker(rank, world, port, case, q):
+def _worker(rank, world, port, case, q, env=None):
     import sys
     import traceback
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ.update(env or {})
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
@@ -87,7 +95,7 @@ def _worker(rank, world, port, case, q):
         q.put((rank, "error", traceback.format_exc()))
 
 
-def run_two_ranks(case, timeout=300, world=2):
+def run_two_ranks(case, timeout=300, world=2, env=None):
     """Rank results {rank: (loss, potentials, world)}; raises with the worker
     traceback on failure and never leaves a worker behind."""
     import queue
@@ -95,7 +103,7 @@ def run_two_ranks(case, timeout=300, world=2):
     mpc = mp.get_context("spawn")
     q = mpc.Queue()
     port = _free_port()
-    procs = [mpc.Process(target=_worker, args=(r, world, port, case, q), daemon=True)
+    procs = [mpc.Process(target=_worker, args=(r, world, port, case, q, env), daemon=True)
              for r in range(world)]
     for p in procs:
         p.start()
@@ -150,6 +158,25 @@ def test_three_ranks_match_one(ctx, case):
         for u, v in zip(p3, [p1.a_xx, p1.b_yy, p1.a_xy, p1.b_yx]):
             assert np.abs(u - v).max() <= 1e-3 * eps
         assert abs(l3 - l1) <= 1e-6 * abs(l1) + 1e-12
+
+
+def test_four_ranks_bench_parameters_batched(ctx):
+    """bench.py's C3 parameters (theta 12.5, switch r_max, automatic voxel edge
+    and super level) at 30k on four ranks, with the column partials forced
+    into many small batches per update (MSOT_COLPART_BUDGET): shard cuts,
+    batch boundaries and the two exchange steps together, against the
+    one-rank solve with the automatic budget."""
+    x, a, y, b = _inputs("bench")
+    l1, p1, s1 = ctx.sinkhorn(_params("bench"), x, a, y, b)
+    assert s1["t_super"] > 0 or s1["t_switch"] > 0
+    out = run_two_ranks("bench", world=4, env={"MSOT_COLPART_BUDGET": "200000"})
+    eps = 0.01 ** 2
+    for rank in range(4):
+        l4, p4, world = out[rank]
+        assert world == 4
+        for u, v in zip(p4, [p1.a_xx, p1.b_yy, p1.a_xy, p1.b_yx]):
+            assert np.abs(u - v).max() <= 1e-3 * eps
+        assert abs(l4 - l1) <= 1e-6 * abs(l1) + 1e-12
 
 
 @pytest.mark.parametrize("case", ["dense", "multiscale", "unbalanced", "hd_ms"])

@@ -64,7 +64,11 @@ def build_lib(verbose=False):
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
     if _newer(LIB, objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lnccl", "-lcudart"]
+        # the CUDA runtime of this toolkit (12.9) linked statically: the
+        # process's dynamic libcudart.so.12 is whichever loads first (torch
+        # ships 12.8 and LD_LIBRARY_PATH prefers it), and code compiled with
+        # a newer toolkit must not run on an older runtime
+        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs + ["-lnccl"]
         if verbose:
             print(" ".join(cmd), flush=True)
         r = subprocess.run(cmd, capture_output=True, text=True)

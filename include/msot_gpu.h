@@ -51,8 +51,9 @@ typedef struct msot_params {
   double theta;          /* truncation slack in units of eps       */
   double switch_factor;  /* switch at first sigma < switch_factor * r_max (:306) */
   int32_t max_full_iters;/* safety cap on schedule length          */
-  int32_t mask_rule;     /* 0 = min(centroid/radius bound, slope bound) (default),
-                            1 = centroid/radius bound only (msot_truncation_mask) */
+  int32_t mask_rule;     /* 0 = min(centroid/radius, slope, member-box bound) (default),
+                            1 = centroid/radius bound only (msot_truncation_mask),
+                            2 = min(centroid/radius, slope bound) (round 1)        */
   int32_t transfer_rule; /* coarse -> fine potentials at the switch:
                             0 = inheritance (default),
                             1 = extrapolation: one lambda-damped softmin of the
@@ -256,6 +257,15 @@ int msot_truncation_mask(msot_ctx* ctx, int64_t kx, int64_t ky, int d, const flo
                          const float* rx, const float* fx, const float* gx, const float* cy,
                          const float* ry, const float* gy, const float* hy, double eps,
                          double theta, double p, int self, uint8_t* mask_out);
+/* The same with the member boxes of the clusters, bx (kx x 6) / by (ky x 6):
+ * {lo[0..2], hi[0..2]} = the min / max of the members' offsets from the
+ * centroid per axis (the solver's cluster_stats rounds them outward).  Adds
+ * the box bound B_c (mask.cu header) to min(B_a, B_b); needs gx / hy. */
+int msot_truncation_mask_box(msot_ctx* ctx, int64_t kx, int64_t ky, int d, const float* cx,
+                             const float* rx, const float* fx, const float* gx, const float* bx,
+                             const float* cy, const float* ry, const float* gy, const float* hy,
+                             const float* by, double eps, double theta, double p, int self,
+                             uint8_t* mask_out);
 
 /* The symmetric eps-scaling Sinkhorn solve + debiased divergence
  * (PAPER.md:235-326).  Potential outputs are

@@ -182,6 +182,7 @@ struct Clusters {
   int32_t k = 0;
   Vec centroids, cweights;
   std::vector<float> radii;
+  std::vector<float> box;  // per cluster {lo[3], hi[3]}: members' offsets from the float centroid
 };
 
 float round_up_float(double v) {
@@ -237,12 +238,57 @@ Clusters grid_cluster(const double* x, const double* w, int64_t n, int d, const 
   return c;
 }
 
+float round_down_float(double v) { return -round_up_float(-v); }
+
+// Member boxes for the truncation box bound: per axis the min / max of the
+// members' float coordinates minus the float centroid (exact in double),
+// rounded outward — what cluster_stats does with the same float inputs.
+void cluster_boxes(const double* x, int d, Clusters& c) {
+  c.box.assign(size_t(c.k) * 6, 0.0f);
+  for (int32_t I = 0; I < c.k; ++I) {
+    double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    for (int32_t s = c.offsets[I]; s < c.offsets[I + 1]; ++s) {
+      const int32_t i = c.perm[s];
+      for (int k = 0; k < d; ++k) {
+        const double t = static_cast<double>(static_cast<float>(x[int64_t(i) * d + k])) -
+                         static_cast<double>(static_cast<float>(c.centroids[int64_t(I) * d + k]));
+        lo[k] = std::min(lo[k], t);
+        hi[k] = std::max(hi[k], t);
+      }
+    }
+    for (int k = 0; k < 3; ++k) {
+      c.box[size_t(I) * 6 + k] = round_down_float(lo[k]);
+      c.box[size_t(I) * 6 + 3 + k] = round_up_float(hi[k]);
+    }
+  }
+}
+
 // Slack upper bound of a cluster pair (SURVEY.md §0.1 #3 — the per-pair
 // distance bound replacing SPEC.md:283's d^{p-1} margin):
 //   F_I + G_J - (1/p) max(0, |X_I - Y_J| - r_I - r_J)^p
 // in float64 with every operation explicitly ordered (no contraction).
+// max over a in [l1, h1], b in [l2, h2] of u a + v b - (a - b)^2 / 2 (the
+// box bound of mask.cu: box_quad, same operations in the same order)
+inline double quad_edge(double u, double v, double A, double B) {
+  const double c = A - B;
+  return (u * A + v * B) - 0.5 * (c * c);
+}
+inline double box_quad(double u, double v, double l1, double h1, double l2, double h2) {
+  const double c1 = quad_edge(u, v, l1, std::fmin(std::fmax(l1 + v, l2), h2));
+  const double c2 = quad_edge(u, v, h1, std::fmin(std::fmax(h1 + v, l2), h2));
+  const double c3 = quad_edge(u, v, std::fmin(std::fmax(l2 + u, l1), h1), l2);
+  const double c4 = quad_edge(u, v, std::fmin(std::fmax(h2 + u, l1), h1), h2);
+  return std::fmax(std::fmax(c1, c2), std::fmax(c3, c4));
+}
+
+// BI / BJ (nullable, only with GI / HJ): member box {lo[3], hi[3]} of the
+// cluster's offsets from its centroid, adding the box bound
+//   B_c = F'_I + G'_J - |D|^2/2 + sum_k max_{a, b in the boxes}
+//         [(G_I - D)_k a + (H_J + D)_k b - (a - b)^2 / 2]
+// (mask.cu header: it keeps the -|u - v|^2/2 term the slope bound drops)
 inline double pair_slack(const float* X, float rI, float F, const float* GI, const float* Y,
-                         float rJ, float G, const float* HJ, int d, double p) {
+                         float rJ, float G, const float* HJ, int d, double p,
+                         const float* BI = nullptr, const float* BJ = nullptr) {
   double dd[3] = {0.0, 0.0, 0.0};
   for (int k = 0; k < d; ++k) dd[k] = static_cast<double>(X[k]) - static_cast<double>(Y[k]);
   const double s = (dd[0] * dd[0] + dd[1] * dd[1]) + dd[2] * dd[2];
@@ -272,14 +318,21 @@ inline double pair_slack(const float* X, float rI, float F, const float* GI, con
   const double marg = static_cast<double>(rI) * na + static_cast<double>(rJ) * nb;
   const double fgp = static_cast<double>(GI[3]) + static_cast<double>(HJ[3]);
   const double vb = (fgp + marg) - 0.5 * s;
-  return va < vb ? va : vb;
+  const double v = va < vb ? va : vb;
+  if (!BI) return v;
+  double q = box_quad(a[0], b[0], BI[0], BI[3], BJ[0], BJ[3]);
+  if (d > 1) q = q + box_quad(a[1], b[1], BI[1], BI[4], BJ[1], BJ[4]);
+  if (d > 2) q = q + box_quad(a[2], b[2], BI[2], BI[5], BJ[2], BJ[5]);
+  const double vc = (fgp + q) - 0.5 * s;
+  return v < vc ? v : vc;
 }
 
 // gx / hy: nullable Kx x 4 / Ky x 4 {slope, F'} per cluster (both or neither)
 void truncation_mask(int64_t kx, int64_t ky, int d, const float* cx, const float* rx,
                      const float* fx, const float* gx, const float* cy, const float* ry,
                      const float* gy, const float* hy, double eps, double theta, double p,
-                     int self, uint8_t* mask) {
+                     int self, uint8_t* mask, const float* bx = nullptr,
+                     const float* by = nullptr) {
   const double thr = -(theta * eps);
   std::vector<double> rbest(kx, -std::numeric_limits<double>::infinity());
   std::vector<int64_t> rarg(kx, 0);
@@ -289,7 +342,8 @@ void truncation_mask(int64_t kx, int64_t ky, int d, const float* cx, const float
   for (int64_t I = 0; I < kx; ++I) {
     for (int64_t J = 0; J < ky; ++J) {
       const double v = pair_slack(cx + I * d, rx[I], fx[I], g ? gx + 4 * I : nullptr, cy + J * d,
-                                  ry[J], gy[J], g ? hy + 4 * J : nullptr, d, p);
+                                  ry[J], gy[J], g ? hy + 4 * J : nullptr, d, p,
+                                  g && bx ? bx + 6 * I : nullptr, g && bx ? by + 6 * J : nullptr);
       mask[I * ky + J] = (v >= thr) ? 1 : 0;
       if (v > rbest[I]) { rbest[I] = v; rarg[I] = J; }
       if (v > cbest[J]) { cbest[J] = v; carg[J] = I; }
@@ -716,6 +770,13 @@ void oracle_truncation_mask(int64_t kx, int64_t ky, int d, const float* cx, cons
   truncation_mask(kx, ky, d, cx, rx, fx, gx, cy, ry, gy, hy, eps, theta, p, self, mask_out);
 }
 
+void oracle_truncation_mask_box(int64_t kx, int64_t ky, int d, const float* cx, const float* rx,
+                                const float* fx, const float* gx, const float* bx, const float* cy,
+                                const float* ry, const float* gy, const float* hy, const float* by,
+                                double eps, double theta, double p, int self, uint8_t* mask_out) {
+  truncation_mask(kx, ky, d, cx, rx, fx, gx, cy, ry, gy, hy, eps, theta, p, self, mask_out, bx, by);
+}
+
 int64_t oracle_tile_ranges(const int32_t* row_labels, const int32_t* row_offsets,
                            int64_t n_rows, int64_t kx, const int32_t* col_offsets, int64_t ky,
                            const uint8_t* mask, int64_t* n_tiles, int64_t* tile_start,
@@ -952,6 +1013,8 @@ int oracle_sinkhorn(const msot_params* prm, const double* x, const double* a, in
     S.cluster_scale = cell;
     Clusters cx = grid_cluster(x, a, n, d, lo.data(), cell);
     Clusters cy = grid_cluster(y, b, m, d, lo.data(), cell);
+    cluster_boxes(x, d, cx);
+    cluster_boxes(y, d, cy);
     S.kx = cx.k;
     S.ky = cy.k;
     px = cx.perm;
@@ -1081,11 +1144,14 @@ int oracle_sinkhorn(const msot_params* prm, const double* x, const double* a, in
         mxx.resize(size_t(cx.k) * cx.k);
         myy.resize(size_t(cy.k) * cy.k);
         mxy.resize(size_t(cx.k) * cy.k);
-        const bool sl = prm->mask_rule == 0;  // slope bound on
+        const bool sl = prm->mask_rule != 1;  // slope bound on (0, 2)
+        const bool bo = prm->mask_rule == 0;  // member-box bound on (0)
         auto G = [&](std::vector<float>& v) { return sl ? v.data() : nullptr; };
-        truncation_mask(cx.k, cx.k, d, cxf.data(), cx.radii.data(), Fxx.data(), G(gxx), cxf.data(), cx.radii.data(), Fxx.data(), G(gxx), e, prm->theta, p, 1, mxx.data());
-        truncation_mask(cy.k, cy.k, d, cyf.data(), cy.radii.data(), Gyy.data(), G(gyy), cyf.data(), cy.radii.data(), Gyy.data(), G(gyy), e, prm->theta, p, 1, myy.data());
-        truncation_mask(cx.k, cy.k, d, cxf.data(), cx.radii.data(), Fyx.data(), G(gyx), cyf.data(), cy.radii.data(), Gxy.data(), G(gxy), e, prm->theta, p, 0, mxy.data());
+        const float* bxx = bo ? cx.box.data() : nullptr;
+        const float* byy = bo ? cy.box.data() : nullptr;
+        truncation_mask(cx.k, cx.k, d, cxf.data(), cx.radii.data(), Fxx.data(), G(gxx), cxf.data(), cx.radii.data(), Fxx.data(), G(gxx), e, prm->theta, p, 1, mxx.data(), bxx, bxx);
+        truncation_mask(cy.k, cy.k, d, cyf.data(), cy.radii.data(), Gyy.data(), G(gyy), cyf.data(), cy.radii.data(), Gyy.data(), G(gyy), e, prm->theta, p, 1, myy.data(), byy, byy);
+        truncation_mask(cx.k, cy.k, d, cxf.data(), cx.radii.data(), Fyx.data(), G(gyx), cyf.data(), cy.radii.data(), Gxy.data(), G(gxy), e, prm->theta, p, 0, mxy.data(), bxx, byy);
       }
       myx.resize(size_t(cy.k) * cx.k);
       for (int64_t I = 0; I < cx.k; ++I)

@@ -50,6 +50,11 @@ void oracle_truncation_mask(int64_t kx, int64_t ky, int d, const float* cx, cons
                             const float* fx, const float* gx, const float* cy, const float* ry,
                             const float* gy, const float* hy, double eps, double theta, double p,
                             int self, uint8_t* mask_out);
+/* With member boxes {lo[3], hi[3]} per cluster (msot_truncation_mask_box). */
+void oracle_truncation_mask_box(int64_t kx, int64_t ky, int d, const float* cx, const float* rx,
+                                const float* fx, const float* gx, const float* bx, const float* cy,
+                                const float* ry, const float* gy, const float* hy, const float* by,
+                                double eps, double theta, double p, int self, uint8_t* mask_out);
 
 /* Cluster-aligned row tiles (policy.h:msot_pack_tiles) and the column
  * ranges of each tile from a cluster mask.  Returns the number of ranges

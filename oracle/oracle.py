@@ -42,6 +42,10 @@ def lib():
         L.oracle_truncation_mask.argtypes = [C.c_int64, C.c_int64, C.c_int, _fp, _fp, _fp,
                                              _fp, _fp, _fp, _fp, _fp, C.c_double, C.c_double,
                                              C.c_double, C.c_int, _bp]
+        L.oracle_truncation_mask_box.restype = None
+        L.oracle_truncation_mask_box.argtypes = [C.c_int64, C.c_int64, C.c_int, _fp, _fp, _fp, _fp,
+                                                 _fp, _fp, _fp, _fp, _fp, _fp, C.c_double,
+                                                 C.c_double, C.c_double, C.c_int, _bp]
         L.oracle_tile_ranges.restype = C.c_int64
         L.oracle_tile_ranges.argtypes = [_ip, _ip, C.c_int64, C.c_int64, _ip, C.c_int64, _bp,
                                          _lp, _lp, _lp, _ip, C.c_int64]
@@ -133,7 +137,9 @@ def kmeans(x, w, k, seed=0):
                 iters=it.value)
 
 
-def truncation_mask(cx, rx, fx, cy, ry, gy, eps, theta, p=2.0, self_=False, gx=None, hy=None):
+def truncation_mask(cx, rx, fx, cy, ry, gy, eps, theta, p=2.0, self_=False, gx=None, hy=None,
+                    bx=None, by=None):
+    """bx / by: member boxes (K x 6: lo[3], hi[3]) for the box bound."""
     f32 = lambda a: np.ascontiguousarray(a, dtype=np.float32)
     cx, rx, fx, cy, ry, gy = map(f32, (cx, rx, fx, cy, ry, gy))
     kx, d = cx.shape
@@ -142,9 +148,15 @@ def truncation_mask(cx, rx, fx, cy, ry, gy, eps, theta, p=2.0, self_=False, gx=N
     fp = lambda a: None if a is None else a.ctypes.data_as(_fp)
     gx = None if gx is None else f32(gx)
     hy = None if hy is None else f32(hy)
-    lib().oracle_truncation_mask(kx, ky, d, fp(cx), fp(rx), fp(fx), fp(gx), fp(cy), fp(ry),
-                                 fp(gy), fp(hy), eps, theta, p, int(self_),
-                                 out.ctypes.data_as(_bp))
+    if bx is None:
+        lib().oracle_truncation_mask(kx, ky, d, fp(cx), fp(rx), fp(fx), fp(gx), fp(cy), fp(ry),
+                                     fp(gy), fp(hy), eps, theta, p, int(self_),
+                                     out.ctypes.data_as(_bp))
+    else:
+        bx, by = f32(bx), f32(by)
+        lib().oracle_truncation_mask_box(kx, ky, d, fp(cx), fp(rx), fp(fx), fp(gx), fp(bx),
+                                         fp(cy), fp(ry), fp(gy), fp(hy), fp(by), eps, theta, p,
+                                         int(self_), out.ctypes.data_as(_bp))
     return out
 
 

@@ -101,7 +101,7 @@ __device__ __forceinline__ double warp_max(double v) {
 
 __global__ void cluster_stats_kernel(const float4* pts, const double* w64, const int32_t* off,
                                      int32_t k, int d, float4* cen, float* clw2, double* cw64,
-                                     float* radii) {
+                                     float* radii, float4* box_lo, float4* box_hi) {
   const int lane = threadIdx.x & 31;
   const int64_t I = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (I >= k) return;
@@ -123,28 +123,44 @@ __global__ void cluster_stats_kernel(const float4* pts, const double* w64, const
   const float4 cf = make_float4(__double2float_rn(c0), __double2float_rn(c1),
                                 __double2float_rn(c2), 0.f);
   double r = 0.0;
+  // member box: the float-to-double differences are exact, min/max too
+  double l0 = 0.0, l1 = 0.0, l2 = 0.0, h0 = 0.0, h1 = 0.0, h2 = 0.0;
   for (int32_t s = s0 + lane; s < s1; s += 32) {
     const float4 p = pts[s];
     const double t0 = static_cast<double>(p.x) - cf.x, t1 = static_cast<double>(p.y) - cf.y,
                  t2 = static_cast<double>(p.z) - cf.z;
     r = fmax(r, sqrt(t0 * t0 + t1 * t1 + t2 * t2));
+    l0 = fmin(l0, t0); l1 = fmin(l1, t1); l2 = fmin(l2, t2);
+    h0 = fmax(h0, t0); h1 = fmax(h1, t1); h2 = fmax(h2, t2);
   }
   r = warp_max(r);
+  for (int o = 16; o > 0; o >>= 1) {
+    l0 = fmin(l0, __shfl_xor_sync(0xffffffffu, l0, o));
+    l1 = fmin(l1, __shfl_xor_sync(0xffffffffu, l1, o));
+    l2 = fmin(l2, __shfl_xor_sync(0xffffffffu, l2, o));
+    h0 = fmax(h0, __shfl_xor_sync(0xffffffffu, h0, o));
+    h1 = fmax(h1, __shfl_xor_sync(0xffffffffu, h1, o));
+    h2 = fmax(h2, __shfl_xor_sync(0xffffffffu, h2, o));
+  }
   if (lane == 0) {
     cen[I] = cf;
     cw64[I] = W;
     clw2[I] = __double2float_rn(log2(W));
     radii[I] = __double2float_ru(r);
+    if (box_lo) {
+      box_lo[I] = make_float4(__double2float_rd(l0), __double2float_rd(l1), __double2float_rd(l2), 0.f);
+      box_hi[I] = make_float4(__double2float_ru(h0), __double2float_ru(h1), __double2float_ru(h2), 0.f);
+    }
   }
 }
 
 cudaError_t cluster_stats(const float4* pts, const double* w64, const int32_t* offsets, int32_t k,
                           int d, float4* cen, float* clw2, double* cw64, float* radii,
-                          cudaStream_t st) {
+                          cudaStream_t st, float4* box_lo, float4* box_hi) {
   if (k <= 0) return cudaSuccess;
   const int64_t threads = static_cast<int64_t>(k) * 32;
   ++g_launches; cluster_stats_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st>>>(
-      pts, w64, offsets, k, d, cen, clw2, cw64, radii);
+      pts, w64, offsets, k, d, cen, clw2, cw64, radii, box_lo, box_hi);
   return cudaGetLastError();
 }
 

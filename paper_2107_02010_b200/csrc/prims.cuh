@@ -120,9 +120,11 @@ cudaError_t segment_flags(const uint32_t* sorted_keys, int64_t n, uint8_t* flags
                           cudaStream_t st);
 cudaError_t segment_offsets(const int32_t* labels, const uint8_t* flags, int64_t n,
                             int32_t* offsets, cudaStream_t st);
+// box_lo / box_hi (nullable): the members' offsets from the float centroid,
+// per axis min / max rounded outward to float (the truncation box bound)
 cudaError_t cluster_stats(const float4* pts, const double* w64, const int32_t* offsets, int32_t k,
                           int d, float4* cen, float* clw2, double* cw64, float* radii,
-                          cudaStream_t st);
+                          cudaStream_t st, float4* box_lo = nullptr, float4* box_hi = nullptr);
 cudaError_t cluster_bound(const float4* pts, const double* w64, const float* f,
                           const int32_t* offsets, const float4* cen, int32_t k, float* fmax,
                           float4* grad, cudaStream_t st);
@@ -167,21 +169,25 @@ __host__ __device__ inline int32_t mask_words(int32_t ky) { return (ky + 31) / 3
 // symmetric mask (maskT, best_c unused).  Otherwise mask (kx rows over ky)
 // and maskT (ky rows over kx, its exact transpose), both with the row and
 // column best pairs; best_r (kx) / best_c (ky) are workspaces, blkws holds
-// the column-block bounds (mask_block_ws_bytes).
+// the column-block bounds (mask_block_ws_bytes).  box (nullable, only with
+// the slope inputs gx/hy): {lo_x, hi_x, lo_y, hi_y} member boxes per cluster
+// (cluster_stats), adding the box bound B_c (mask.cu header).
 cudaError_t truncation_masks(int32_t kx, int32_t ky, int d, const float4* cx, const float* rx,
                              const float* fx, const float4* gx, const float4* cy, const float* ry,
                              const float* gy, const float4* hy, double eps, double theta, int self,
                              uint32_t* mask, uint32_t* maskT, int32_t* best_r, int32_t* best_c,
-                             void* blkws, cudaStream_t st);
+                             void* blkws, cudaStream_t st, const float4* const* box = nullptr);
 cudaError_t truncation_masks_rows(int32_t kx, int32_t ky, int d, const float4* cx, const float* rx,
                                   const float* fx, const float4* gx, const float4* cy,
                                   const float* ry, const float* gy, const float4* hy, double eps,
                                   double theta, int self, int32_t r0, int32_t r1, uint32_t* mask,
-                                  int32_t* best_r, void* blkws, cudaStream_t st);
+                                  int32_t* best_r, void* blkws, cudaStream_t st,
+                                  const float4* const* box = nullptr);
 cudaError_t truncation_masks_cols(int32_t kx, int32_t ky, int d, const float4* cx, const float* rx,
                                   const float* fx, const float4* gx, const float4* cy,
                                   const float* ry, const float* gy, const float4* hy, uint32_t* mask,
-                                  int32_t* best_c, void* blkws, cudaStream_t st);
+                                  int32_t* best_c, void* blkws, cudaStream_t st,
+                                  const float4* const* box = nullptr);
 inline size_t mask_block_ws_bytes(int32_t kx, int32_t ky) {
   return static_cast<size_t>(mask_words(kx) + mask_words(ky)) * (sizeof(float4) + sizeof(float)) +
          static_cast<size_t>(mask_words(ky)) * sizeof(uint32_t);

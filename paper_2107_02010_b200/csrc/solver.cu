@@ -273,6 +273,8 @@ struct DMeasure {
   float* clw2 = nullptr;
   double* cw64 = nullptr;
   float* radii = nullptr;
+  float4* box_lo = nullptr;  // member boxes (truncation box bound, mask.cu)
+  float4* box_hi = nullptr;
   std::vector<float> radii_h;
   std::vector<int32_t> offsets_h;  // cluster offsets (host copy, K+1)
   bool uniform = false;            // all weights equal
@@ -344,7 +346,10 @@ void prepare_measures(msot_ctx* c, const std::vector<MeasureJob>& jobs, int d, c
     M.clw2 = c->buf<float>(tag + ".clw2", k);
     M.cw64 = c->buf<double>(tag + ".cw64", k);
     M.radii = c->buf<float>(tag + ".radii", k);
-    CK(cluster_stats(M.pts, M.w64, M.offsets, k, d, M.cpts, M.clw2, M.cw64, M.radii, st));
+    M.box_lo = c->buf<float4>(tag + ".boxlo", k);
+    M.box_hi = c->buf<float4>(tag + ".boxhi", k);
+    CK(cluster_stats(M.pts, M.w64, M.offsets, k, d, M.cpts, M.clw2, M.cw64, M.radii, st, M.box_lo,
+                     M.box_hi));
     hr[q] = c->pin<float>(k);
     ho[q] = c->pin<int32_t>(k + 1);
     CK(cudaMemcpyAsync(hr[q], M.radii, k * sizeof(float), cudaMemcpyDeviceToHost, st));
@@ -1335,6 +1340,8 @@ struct HdLayout {
   int32_t* src = nullptr;          // caller index, or -(I+1) for padding of cluster I
   double* centers = nullptr;       // K x d float64
   float* radii = nullptr;
+  float4* box_lo = nullptr;  // member boxes (truncation box bound, mask.cu)
+  float4* box_hi = nullptr;
   std::vector<float> radii_h;
   float* clw2 = nullptr;           // coarse measure
   double* cw64 = nullptr;
@@ -2089,7 +2096,15 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
         CK(cluster_bound(X.pts, X.w64, f[3], X.offsets, X.cpts, X.k, fmax[3], grad[3], st));
       }
       float4* g[4];
-      for (int q = 0; q < 4; ++q) g[q] = (info && prm->mask_rule == 0) ? grad[q] : nullptr;
+      for (int q = 0; q < 4; ++q) g[q] = (info && prm->mask_rule != 1) ? grad[q] : nullptr;
+      // member boxes (mask.cu: B_c) with the slope bound, mask_rule 0
+      const float4* bxy[4] = {X.box_lo, X.box_hi, Y.box_lo, Y.box_hi};
+      const float4* bxx[4] = {X.box_lo, X.box_hi, X.box_lo, X.box_hi};
+      const float4* byy[4] = {Y.box_lo, Y.box_hi, Y.box_lo, Y.box_hi};
+      const bool use_box = info && prm->mask_rule == 0;
+      const float4* const* Bxy = use_box ? bxy : nullptr;
+      const float4* const* Bxx = use_box ? bxx : nullptr;
+      const float4* const* Byy = use_box ? byy : nullptr;
       int32_t* bxr = c->buf<int32_t>("m.bx", std::max(X.k, Y.k));
       int32_t* byr = c->buf<int32_t>("m.by", std::max(X.k, Y.k));
       void* bws = c->buf<char>("m.blk", mask_block_ws_bytes(std::max(X.k, Y.k), std::max(X.k, Y.k)));
@@ -2104,13 +2119,13 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
         else
           CK(truncation_masks_rows(X.k, X.k, d, X.cpts, X.radii, fmax[0], g[0], X.cpts, X.radii,
                                    fmax[0], g[0], e, theta, 1, cut(X.k, rk), cut(X.k, rk + 1),
-                                   mxx, bxr, bws, st));
+                                   mxx, bxr, bws, st, Bxx));
         CK(truncation_masks_rows(Y.k, Y.k, d, Y.cpts, Y.radii, fmax[1], g[1], Y.cpts, Y.radii,
                                  fmax[1], g[1], e, theta, 1, cut(Y.k, rk), cut(Y.k, rk + 1), myy,
-                                 byr, bws, st));
+                                 byr, bws, st, Byy));
         CK(truncation_masks_rows(X.k, Y.k, d, X.cpts, X.radii, fmax[3], g[3], Y.cpts, Y.radii,
                                  fmax[2], g[2], e, theta, 0, cut(X.k, rk), cut(X.k, rk + 1), mxy,
-                                 bxr, bws, st));
+                                 bxr, bws, st, Bxy));
         if (wd > 1 || c->comm) {
           std::vector<int64_t> bnd[3];
           const int32_t kr[3] = {X.k, Y.k, X.k}, kc[3] = {X.k, Y.k, Y.k};
@@ -2123,16 +2138,16 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
           coll_bcast_rows(c, mb, bnd, 3);
         }
         CK(truncation_masks_cols(X.k, Y.k, d, X.cpts, X.radii, fmax[3], g[3], Y.cpts, Y.radii,
-                                 fmax[2], g[2], mxy, byr, bws, st));
+                                 fmax[2], g[2], mxy, byr, bws, st, Bxy));
       } else {
         CK(truncation_masks(X.k, X.k, d, X.cpts, X.radii, fmax[0], g[0], X.cpts, X.radii, fmax[0],
-                            g[0], e, theta, 1, mxx, nullptr, bxr, nullptr, bws, st));
+                            g[0], e, theta, 1, mxx, nullptr, bxr, nullptr, bws, st, Bxx));
         CK(truncation_masks(Y.k, Y.k, d, Y.cpts, Y.radii, fmax[1], g[1], Y.cpts, Y.radii, fmax[1],
-                            g[1], e, theta, 1, myy, nullptr, byr, nullptr, bws, st));
+                            g[1], e, theta, 1, myy, nullptr, byr, nullptr, bws, st, Byy));
         // cross pair: (F, G) = (max b_yx, max a_xy); the slack is symmetric, so
         // the yx mask (rows y) is the exact transpose of the xy mask (rows x)
         CK(truncation_masks(X.k, Y.k, d, X.cpts, X.radii, fmax[3], g[3], Y.cpts, Y.radii, fmax[2],
-                            g[2], e, theta, 0, mxy, myx, bxr, byr, bws, st));
+                            g[2], e, theta, 0, mxy, myx, bxr, byr, bws, st, Bxy));
       }
       if (c->profiling) {  // cluster-granularity pair count of the four masks
         double* cnt = c->buf<double>("m.cnt", 1);
@@ -3078,9 +3093,20 @@ int msot_truncation_mask(msot_ctx* c, int64_t kx, int64_t ky, int d, const float
                          const float* rx, const float* fx, const float* gx, const float* cy,
                          const float* ry, const float* gy, const float* hy, double eps,
                          double theta, double p, int self, uint8_t* mask_out) {
+  return msot_truncation_mask_box(c, kx, ky, d, cx, rx, fx, gx, nullptr, cy, ry, gy, hy, nullptr,
+                                  eps, theta, p, self, mask_out);
+}
+
+int msot_truncation_mask_box(msot_ctx* c, int64_t kx, int64_t ky, int d, const float* cx,
+                             const float* rx, const float* fx, const float* gx, const float* bx,
+                             const float* cy, const float* ry, const float* gy, const float* hy,
+                             const float* by, double eps, double theta, double p, int self,
+                             uint8_t* mask_out) {
   return guard([&] {
     if (!c || !cx || !rx || !fx || !cy || !ry || !gy || !mask_out) raise(MSOT_EUSAGE, "null argument");
     if ((gx == nullptr) != (hy == nullptr)) raise(MSOT_EUSAGE, "slopes: both sides or neither");
+    if ((bx == nullptr) != (by == nullptr)) raise(MSOT_EUSAGE, "boxes: both sides or neither");
+    if (bx && !gx) raise(MSOT_EUSAGE, "the box bound needs the slope inputs");
     if (p != 2.0) raise(MSOT_EUSAGE, "the GPU path implements p = 2");
     if (d < 1 || d > 3) raise(MSOT_EUSAGE, "D in 1..3");
     if (kx < 1 || ky < 1) raise(MSOT_EDATA, "empty cluster set");
@@ -3120,11 +3146,30 @@ int msot_truncation_mask(msot_ctx* c, int64_t kx, int64_t ky, int d, const float
       CK(cudaMemcpyAsync(dgx, gx, kx * sizeof(float4), cudaMemcpyHostToDevice, st));
       CK(cudaMemcpyAsync(dhy, hy, ky * sizeof(float4), cudaMemcpyHostToDevice, st));
     }
+    const float4* box[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (bx) {  // {lo[3], hi[3]} per cluster -> float4 lo / hi
+      std::vector<float4> h(2 * (kx + ky));
+      auto unpack = [&](const float* b, int64_t k, float4* lo, float4* hi) {
+        for (int64_t I = 0; I < k; ++I) {
+          float l[3] = {0, 0, 0}, u[3] = {0, 0, 0};
+          for (int q = 0; q < d; ++q) { l[q] = b[I * 6 + q]; u[q] = b[I * 6 + 3 + q]; }
+          lo[I] = make_float4(l[0], l[1], l[2], 0.f);
+          hi[I] = make_float4(u[0], u[1], u[2], 0.f);
+        }
+      };
+      unpack(bx, kx, h.data(), h.data() + kx);
+      unpack(by, ky, h.data() + 2 * kx, h.data() + 2 * kx + ky);
+      float4* db = c->buf<float4>("tm.box", h.size());
+      CK(cudaMemcpyAsync(db, h.data(), h.size() * sizeof(float4), cudaMemcpyHostToDevice, st));
+      CK(host_sync(__LINE__, st));  // h is a local vector
+      box[0] = db; box[1] = db + kx; box[2] = db + 2 * kx; box[3] = db + 2 * kx + ky;
+    }
     if (self && kx != ky) raise(MSOT_EUSAGE, "a self mask is square");
     void* bws = c->buf<char>("tm.blk", mask_block_ws_bytes(static_cast<int32_t>(kx),
                                                           static_cast<int32_t>(ky)));
     CK(truncation_masks(static_cast<int32_t>(kx), static_cast<int32_t>(ky), d, dcx, drx, dfx, dgx,
-                        dcy, dry, dgy, dhy, eps, theta, self, dbits, nullptr, dbr, dbc, bws, st));
+                        dcy, dry, dgy, dhy, eps, theta, self, dbits, nullptr, dbr, dbc, bws, st,
+                        bx ? box : nullptr));
     CK(unpack_mask(dbits, static_cast<int32_t>(kx), static_cast<int32_t>(ky), dm, st));
     CK(cudaMemcpyAsync(mask_out, dm, kx * ky, cudaMemcpyDeviceToHost, st));
     CK(host_sync(__LINE__, st));

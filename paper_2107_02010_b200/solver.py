@@ -64,6 +64,9 @@ def lib():
         L.msot_truncation_mask.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int, _fp,
                                            _fp, _fp, _fp, _fp, _fp, _fp, _fp, C.c_double,
                                            C.c_double, C.c_double, C.c_int, _bp]
+        L.msot_truncation_mask_box.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int, _fp,
+                                               _fp, _fp, _fp, _fp, _fp, _fp, _fp, _fp, _fp,
+                                               C.c_double, C.c_double, C.c_double, C.c_int, _bp]
         L.msot_sinkhorn.argtypes = [C.c_void_p, C.POINTER(Params), _dp, _dp, C.c_int64, _dp,
                                     _dp, C.c_int64, C.c_int, _dp, _dp, _dp, _dp, _dp,
                                     C.POINTER(Stats)]
@@ -101,7 +104,7 @@ EXPORTS = ["msot_last_error", "msot_params_default", "msot_create", "msot_nccl_u
            "msot_barycenter", "msot_transfer_labels", "msot_resolve_flips", "msot_classify",
            "msot_plan_apply", "msot_kmeans", "msot_create_dist_host", "msot_exact_ot",
            "msot_world_info", "msot_debug_capture", "msot_debug_mask",
-           "msot_set_colpart_budget"]
+           "msot_set_colpart_budget", "msot_truncation_mask_box"]
 
 
 def _check(rc):
@@ -427,8 +430,9 @@ class Context:
 
     # -- kernel_truncation on explicit coarse inputs (K3)
     def kernel_truncation(self, cx, rx, fx, cy, ry, gy, eps, theta, self_=False, gx=None,
-                          hy=None):
-        """gx / hy: optional (K, 4) {slope, F'} arrays for the slope bound."""
+                          hy=None, bx=None, by=None):
+        """gx / hy: optional (K, 4) {slope, F'} arrays for the slope bound;
+        bx / by: optional (K, 6) member boxes {lo[3], hi[3]} for the box bound."""
         f32 = lambda a: np.ascontiguousarray(a, dtype=np.float32)
         cx, rx, fx, cy, ry, gy = map(f32, (cx, rx, fx, cy, ry, gy))
         kx, d = cx.shape
@@ -437,9 +441,17 @@ class Context:
         fp = lambda a: None if a is None else a.ctypes.data_as(_fp)
         gx = None if gx is None else f32(gx)
         hy = None if hy is None else f32(hy)
-        _check(lib().msot_truncation_mask(self._h, kx, ky, d, fp(cx), fp(rx), fp(fx), fp(gx),
-                                          fp(cy), fp(ry), fp(gy), fp(hy), eps, theta, 2.0,
-                                          int(self_), out.ctypes.data_as(_bp)))
+        if bx is None and by is None:
+            _check(lib().msot_truncation_mask(self._h, kx, ky, d, fp(cx), fp(rx), fp(fx), fp(gx),
+                                              fp(cy), fp(ry), fp(gy), fp(hy), eps, theta, 2.0,
+                                              int(self_), out.ctypes.data_as(_bp)))
+        else:
+            bx = None if bx is None else _vec(np.ravel(bx), kx * 6, "bx").astype(np.float32)
+            by = None if by is None else _vec(np.ravel(by), ky * 6, "by").astype(np.float32)
+            _check(lib().msot_truncation_mask_box(self._h, kx, ky, d, fp(cx), fp(rx), fp(fx),
+                                                  fp(gx), fp(bx), fp(cy), fp(ry), fp(gy), fp(hy),
+                                                  fp(by), eps, theta, 2.0, int(self_),
+                                                  out.ctypes.data_as(_bp)))
         return out
 
     # -- symmetric_sinkhorn / multiscale_sinkhorn + divergence

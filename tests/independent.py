@@ -124,8 +124,21 @@ def super_switch(sigma, tsw, cell, d, kmax, mode=-1):
     return t2 if tsw - t2 >= 4 else 0
 
 
-def slack(cx, rx, fx, cy, ry, gy, gx=None, hy=None):
-    """min(B_a, B_b) for every cluster pair (float64)."""
+def box_quad(u, v, l1, h1, l2, h2):
+    """max over a in [l1, h1], b in [l2, h2] of u a + v b - (a - b)^2 / 2,
+    by brute force on a fine grid plus the exact edge candidates."""
+    g = lambda aa, bb: u * aa + v * bb - 0.5 * (aa - bb) ** 2
+    best = np.full(np.broadcast(u, v, l1, l2).shape, -np.inf)
+    for aa in (l1, h1):
+        best = np.maximum(best, g(aa, np.clip(aa + v, l2, h2)))
+    for bb in (l2, h2):
+        best = np.maximum(best, g(np.clip(bb + u, l1, h1), bb))
+    return best
+
+
+def slack(cx, rx, fx, cy, ry, gy, gx=None, hy=None, bx=None, by=None):
+    """min(B_a, B_b[, B_c]) for every cluster pair (float64); bx / by: member
+    boxes (K, 6) {lo[3], hi[3]} (DESIGN.md §3 K3, the box bound)."""
     cx, cy = np.asarray(cx, np.float64), np.asarray(cy, np.float64)
     rx, ry = np.asarray(rx, np.float64), np.asarray(ry, np.float64)
     fx, gy = np.asarray(fx, np.float64), np.asarray(gy, np.float64)
@@ -138,11 +151,18 @@ def slack(cx, rx, fx, cy, ry, gy, gx=None, hy=None):
     gx, hy = np.asarray(gx, np.float64), np.asarray(hy, np.float64)
     S, Fp = gx[:, :3], gx[:, 3]
     T, Gp = hy[:, :3], hy[:, 3]
+    U, V = S[:, None, :] - D, T[None, :, :] + D
     bb = (Fp[:, None] + Gp[None, :]
-          + rx[:, None] * np.sqrt(((S[:, None, :] - D) ** 2).sum(-1))
-          + ry[None, :] * np.sqrt(((T[None, :, :] + D) ** 2).sum(-1))
+          + rx[:, None] * np.sqrt((U ** 2).sum(-1))
+          + ry[None, :] * np.sqrt((V ** 2).sum(-1))
           - 0.5 * dist ** 2)
-    return np.minimum(ba, bb)
+    out = np.minimum(ba, bb)
+    if bx is None:
+        return out
+    bx, by = np.asarray(bx, np.float64), np.asarray(by, np.float64)
+    q = sum(box_quad(U[..., k], V[..., k], bx[:, None, k], bx[:, None, 3 + k],
+                     by[None, :, k], by[None, :, 3 + k]) for k in range(cx.shape[1]))
+    return np.minimum(out, Fp[:, None] + Gp[None, :] + q - 0.5 * dist ** 2)
 
 
 def mask(sl, eps, theta, self_=False):

@@ -91,12 +91,17 @@ def _mask_case(seed, self_):
     gy = fx if self_ else f32(rng.random(ky) * 0.01)
     gx = f32(np.concatenate([rng.normal(0, 0.2, (kx, 3)), fx[:, None] + 0.001], 1))
     hy = gx if self_ else f32(np.concatenate([rng.normal(0, 0.2, (ky, 3)), gy[:, None] + 0.001], 1))
-    return cx, rx, fx, cy, ry, gy, gx, hy
+    # member boxes inside the radius ball's bounding cube, lo <= 0 <= hi
+    bx = f32(np.concatenate([-rng.random((kx, 3)) * rx[:, None], rng.random((kx, 3)) * rx[:, None]], 1))
+    by = bx if self_ else f32(np.concatenate([-rng.random((ky, 3)) * ry[:, None],
+                                              rng.random((ky, 3)) * ry[:, None]], 1))
+    return cx, rx, fx, cy, ry, gy, gx, hy, bx, by
 
 
-def _check_mask(got, args, eps, theta, self_, slopes):
-    cx, rx, fx, cy, ry, gy, gx, hy = args
-    sl = I.slack(cx, rx, fx, cy, ry, gy, gx if slopes else None, hy if slopes else None)
+def _check_mask(got, args, eps, theta, self_, slopes, boxes=False):
+    cx, rx, fx, cy, ry, gy, gx, hy, bx, by = args
+    sl = I.slack(cx, rx, fx, cy, ry, gy, gx if slopes else None, hy if slopes else None,
+                 bx if boxes else None, by if boxes else None)
     want = I.mask(sl, eps, theta, self_)
     diff = got.astype(bool) != want
     # disagreements only where the slack is within rounding of the threshold
@@ -105,15 +110,30 @@ def _check_mask(got, args, eps, theta, self_, slopes):
     assert 0 < want.mean() < 1
 
 
+RULES = [(False, False), (True, False), (True, True)]  # (slopes, boxes)
+
+
 @pytest.mark.parametrize("self_", [False, True])
-@pytest.mark.parametrize("slopes", [False, True])
-def test_mask_oracle_vs_independent(oracle, self_, slopes):
+@pytest.mark.parametrize("slopes,boxes", RULES)
+def test_mask_oracle_vs_independent(oracle, self_, slopes, boxes):
     args = _mask_case(7, self_)
-    cx, rx, fx, cy, ry, gy, gx, hy = args
+    cx, rx, fx, cy, ry, gy, gx, hy, bx, by = args
     for eps, theta in ((1e-3, 20.0), (1e-4, 5.0)):
         got = oracle.truncation_mask(cx, rx, fx, cy, ry, gy, eps, theta, self_=self_,
-                                     gx=gx if slopes else None, hy=hy if slopes else None)
-        _check_mask(got, args, eps, theta, self_, slopes)
+                                     gx=gx if slopes else None, hy=hy if slopes else None,
+                                     bx=bx if boxes else None, by=by if boxes else None)
+        _check_mask(got, args, eps, theta, self_, slopes, boxes)
+
+
+def test_box_bound_tightens(oracle):
+    """The box bound only removes pairs (min of three bounds) and does remove
+    some on this data."""
+    args = _mask_case(9, False)
+    cx, rx, fx, cy, ry, gy, gx, hy, bx, by = args
+    a = oracle.truncation_mask(cx, rx, fx, cy, ry, gy, 1e-3, 20.0, gx=gx, hy=hy)
+    b = oracle.truncation_mask(cx, rx, fx, cy, ry, gy, 1e-3, 20.0, gx=gx, hy=hy, bx=bx, by=by)
+    assert not (b.astype(bool) & ~a.astype(bool)).any()
+    assert b.sum() < a.sum()
 
 
 # ------------------------------------------------------------------ GPU ---
@@ -139,11 +159,15 @@ def test_solver_policies_gpu_vs_independent(ctx, n):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("self_", [False, True])
-@pytest.mark.parametrize("slopes", [False, True])
-def test_mask_gpu_vs_independent(ctx, self_, slopes):
+@pytest.mark.parametrize("slopes,boxes", RULES)
+def test_mask_gpu_vs_independent(ctx, oracle, self_, slopes, boxes):
+    """GPU masks against the restatement, and bit-exact against the oracle."""
     args = _mask_case(8, self_)
-    cx, rx, fx, cy, ry, gy, gx, hy = args
+    cx, rx, fx, cy, ry, gy, gx, hy, bx, by = args
     for eps, theta in ((1e-3, 20.0), (1e-4, 5.0)):
-        got = ctx.kernel_truncation(cx, rx, fx, cy, ry, gy, eps, theta, self_=self_,
-                                    gx=gx if slopes else None, hy=hy if slopes else None)
-        _check_mask(got, args, eps, theta, self_, slopes)
+        kw = dict(self_=self_, gx=gx if slopes else None, hy=hy if slopes else None,
+                  bx=bx if boxes else None, by=by if boxes else None)
+        got = ctx.kernel_truncation(cx, rx, fx, cy, ry, gy, eps, theta, **kw)
+        _check_mask(got, args, eps, theta, self_, slopes, boxes)
+        np.testing.assert_array_equal(got, oracle.truncation_mask(cx, rx, fx, cy, ry, gy, eps,
+                                                                  theta, **kw))

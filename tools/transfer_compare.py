@@ -18,7 +18,7 @@ for n in [int(v) for v in sys.argv[1:]] or [1000000, 100000]:
         dense = dense_c3
     else:
         dense, _, _ = ctx.sinkhorn(make_params(blur=0.01), x, a, y, b, potentials=False)
-    for rule in (0, 1):
+    for rule in [int(r) for r in os.environ.get("RULES", "0,1").split(",")]:
         prm = bench.params(w)
         prm.transfer_rule = rule
         for _ in range(3):

@@ -54,7 +54,7 @@ __device__ __forceinline__ double pair_slack(float4 X, float rI, float F, float4
                                              float rJ, float G, float4 HJ, int d, bool grad,
                                              bool box = false, float4 LI = float4{},
                                              float4 UI = float4{}, float4 LJ = float4{},
-                                             float4 UJ = float4{}) {
+                                             float4 UJ = float4{}, double thr = -INFINITY) {
   const double d0 = __dsub_rn(static_cast<double>(X.x), static_cast<double>(Y.x));
   const double d1 = d > 1 ? __dsub_rn(static_cast<double>(X.y), static_cast<double>(Y.y)) : 0.0;
   const double d2 = d > 2 ? __dsub_rn(static_cast<double>(X.z), static_cast<double>(Y.z)) : 0.0;
@@ -79,7 +79,9 @@ __device__ __forceinline__ double pair_slack(float4 X, float rI, float F, float4
   const double fgp = __dadd_rn(static_cast<double>(GI.w), static_cast<double>(HJ.w));
   const double vb = __dsub_rn(__dadd_rn(fgp, marg), __dmul_rn(0.5, s));
   double v = va < vb ? va : vb;
-  if (!box) return v;
+  // (a caller testing against thr needs B_c only while min(B_a, B_b) keeps
+  // the pair: below thr the decision is made, and B_c can only lower v)
+  if (!box || v < thr) return v;
   // (c) box bound: sum over axes of the edge maxima (axis order fixed)
   double q = box_quad(a0, b0, LI.x, UI.x, LJ.x, UJ.x);
   if (d > 1) q = __dadd_rn(q, box_quad(a1, b1, LI.y, UI.y, LJ.y, UJ.y));
@@ -154,11 +156,13 @@ __device__ __forceinline__ float box_quad_f(float u, float v, float l1, float h1
 
 // float32 value of min(B_a, B_b[, B_c]) and its error margin: lo = v - m is
 // a lower bound of the float64 slack, v + m an upper bound.
+// (thr: the box term is skipped once min(B_a, B_b) is already certainly
+// below the threshold — the pair is dropped whatever B_c says.)
 __device__ __forceinline__ float2 bounds_regs(float4 X, float rI, float F, float4 GI, float4 Y,
                                               float rJ, float G, float4 HJ, int d, bool g,
                                               bool box = false, float4 LI = float4{},
                                               float4 UI = float4{}, float4 LJ = float4{},
-                                              float4 UJ = float4{}) {
+                                              float4 UJ = float4{}, double thr = -INFINITY) {
   const float dx = X.x - Y.x, dy = d > 1 ? X.y - Y.y : 0.f, dz = d > 2 ? X.z - Y.z : 0.f;
   const float s = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
   const float rr = rI + rJ;
@@ -174,7 +178,7 @@ __device__ __forceinline__ float2 bounds_regs(float4 X, float rI, float F, float
     const float vb = ((GI.w + HJ.w) + marg) - 0.5f * s;
     v = fminf(v, vb);
     mag += fabsf(GI.w) + fabsf(HJ.w) + marg;
-    if (box) {
+    if (box && static_cast<double>(v + 1e-5f * mag) >= thr) {
       float q = box_quad_f(a0, b0, LI.x, UI.x, LJ.x, UJ.x, mag);
       if (d > 1) q += box_quad_f(a1, b1, LI.y, UI.y, LJ.y, UJ.y, mag);
       if (d > 2) q += box_quad_f(a2, b2, LI.z, UI.z, LJ.z, UJ.z, mag);
@@ -238,7 +242,9 @@ __global__ void block_bounds_kernel(const float4* cy, const float* ry, const flo
 // 128: 31 ms, 64: 30 ms)
 constexpr int kMaskThreads = 64;
 
-__global__ void __launch_bounds__(kMaskThreads)
+// (64 registers: the kernel is latency-bound and needs the occupancy; the
+// rare float64 box path spills)
+__global__ void __launch_bounds__(kMaskThreads, 16)
 mask_rows_kernel(MaskIn m, const float4* blk, const float* blkg, double thr, int self,
                  uint32_t* mask, int32_t* best, uint32_t* colany, int32_t row0) {
   __shared__ double sv[kMaskThreads / 32];
@@ -270,11 +276,11 @@ mask_rows_kernel(MaskIn m, const float4* blk, const float* blkg, double thr, int
       bool keep = self && I == J;  // diagonal of a self mask
       if (static_cast<double>(ub_regs(X, rI, F, Y, rJ, G, m.d)) >= thr) {
         const float4 LJ = bx ? m.ly[J] : zero, UJ = bx ? m.uy[J] : zero;
-        const float2 vm = bounds_regs(X, rI, F, GI, Y, rJ, G, HJ, m.d, g, bx, LI, UI, LJ, UJ);
+        const float2 vm = bounds_regs(X, rI, F, GI, Y, rJ, G, HJ, m.d, g, bx, LI, UI, LJ, UJ, thr);
         if (static_cast<double>(vm.x - vm.y) >= thr)
           keep = true;  // float32 lower bound settles it
         else if (static_cast<double>(vm.x + vm.y) >= thr)  // in between: float64
-          keep = keep || pair_slack(X, rI, F, GI, Y, rJ, G, HJ, m.d, g, bx, LI, UI, LJ, UJ) >= thr;
+          keep = keep || pair_slack(X, rI, F, GI, Y, rJ, G, HJ, m.d, g, bx, LI, UI, LJ, UJ, thr) >= thr;
       }
       return keep;
     };

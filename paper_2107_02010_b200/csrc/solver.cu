@@ -10,6 +10,7 @@
 // synchronises a handful of times per solve (bounding box, cluster counts,
 // mask sizes, final loss).
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -173,7 +174,16 @@ struct msot_ctx {
   // the mark's phase (stats.phase_ms, see include/msot_gpu.h)
   std::vector<std::pair<int, cudaEvent_t>> marks;
   std::vector<cudaEvent_t> mark_pool;
+  // NVTX ranges per phase (host timeline of nsys / ncu --nvtx; no-ops without
+  // a tool attached): the open range is closed at the next mark, -1 ends
+  bool nvtx_open = false;
   void mark(int phase) {
+    static const char* const kNames[8] = {"msot:setup", "msot:coarse", "msot:transfer",
+                                          "msot:masks", "msot:updates", "msot:loss",
+                                          "msot:labels", "msot:phase7"};
+    if (nvtx_open) nvtxRangePop();
+    nvtx_open = phase >= 0 && phase < 8;
+    if (nvtx_open) nvtxRangePushA(kNames[phase]);
     if (!profiling) return;
     if (mark_pool.size() <= marks.size()) {
       cudaEvent_t e;

@@ -237,14 +237,15 @@ __global__ void block_bounds_kernel(const float4* cy, const float* ry, const flo
 // kept pair, so no diagonal either) scans every word for the exact arg-max,
 // evaluating the float64 slack where the float32 upper bound reaches the
 // lane's best so far.
-// 2 warps per row cluster: rows finish at very different times (their kept
-// words vary), small CTAs keep the SMs full (C3 mask phase: 256 threads 34 ms,
-// 128: 31 ms, 64: 30 ms)
-constexpr int kMaskThreads = 64;
+// One warp per row cluster: rows finish at very different times (their kept
+// words vary), small CTAs keep the SMs full and need no inter-warp barrier
+// (C3 mask phase: 256 threads 34 ms, 128: 31 ms, 64: 30 ms; with the box
+// bound, mask_rows alone: 64 threads 21.7 ms, 32: 20.0 ms).
+constexpr int kMaskThreads = 32;
 
 // (64 registers: the kernel is latency-bound and needs the occupancy; the
 // rare float64 box path spills)
-__global__ void __launch_bounds__(kMaskThreads, 16)
+__global__ void __launch_bounds__(kMaskThreads, 1024 / kMaskThreads)
 mask_rows_kernel(MaskIn m, const float4* blk, const float* blkg, double thr, int self,
                  uint32_t* mask, int32_t* best, uint32_t* colany, int32_t row0) {
   __shared__ double sv[kMaskThreads / 32];

@@ -201,6 +201,28 @@ def test_nccl_one_rank_communicator(ctx, case):
     assert l2 == l1
 
 
+def test_nccl_one_rank_batched_bench_parameters(ctx):
+    """The one-rank communicator under bench.py's parameters with the column
+    partials in many small batches: the NCCL calls sit between batched
+    updates on two streams; the result equals the communicator-less solve."""
+    from paper_2107_02010_b200.solver import Context
+    x, a, y, b = _inputs("bench")
+    c0 = Context(0)
+    c1 = Context(0, 0, 1, Context.nccl_unique_id())
+    try:
+        for c in (c0, c1):
+            c.set_colpart_budget(200000)
+        l0, p0, s0 = c0.sinkhorn(_params("bench"), x, a, y, b)
+        l1, p1, s1 = c1.sinkhorn(_params("bench"), x, a, y, b)
+    finally:
+        c0.close()
+        c1.close()
+    assert s1["colpart_batches"] > 2
+    for u, v in zip([p1.a_xx, p1.b_yy, p1.a_xy, p1.b_yx], [p0.a_xx, p0.b_yy, p0.a_xy, p0.b_yx]):
+        np.testing.assert_array_equal(u, v)
+    assert l1 == l0
+
+
 if __name__ == "__main__":
     import sys
     for case in sys.argv[1:]:

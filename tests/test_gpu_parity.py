@@ -250,6 +250,40 @@ def test_multiscale_close_to_dense(ctx, switch_factor):
     assert st["pairs_fine"] < 0.8 * st["pairs_fine_dense"]
 
 
+def test_mask_rules(ctx):
+    """mask_rule 0 (radius + slope + member box, default) keeps a subset of
+    mask_rule 2's pairs (the round-1 pair of bounds) and both stay within the
+    truncation tolerance of each other; mask_rule 1 (radius only) keeps the
+    most."""
+    n = 20000
+    x, y = mixture(n, 21), mixture(n, 22)
+    a = np.full(n, 1 / n)
+    out = {}
+    for rule in (0, 1, 2):
+        prm = make_params(blur=0.01, multiscale=True, retruncate=1, theta=12.5, mask_rule=rule)
+        out[rule] = ctx.sinkhorn(prm, x, a, y, a, potentials=False)
+    assert out[0][2]["pairs_fine"] < out[2][2]["pairs_fine"] <= out[1][2]["pairs_fine"]
+    for rule in (1, 2):
+        assert abs(out[rule][0] - out[0][0]) <= 1e-7 * abs(out[0][0])  # float32 order
+
+
+def test_truncation_mask_box_abi_errors(ctx):
+    rng = np.random.default_rng(1)
+    c = rng.random((10, 3)).astype(np.float32)
+    r = np.full(10, 0.01, np.float32)
+    f = np.zeros(10, np.float32)
+    g4 = np.zeros((10, 4), np.float32)
+    box = np.tile(np.array([-0.01, -0.01, -0.01, 0.01, 0.01, 0.01], np.float32), (10, 1))
+    with pytest.raises(UsageError):  # the box bound needs the slope inputs
+        ctx.kernel_truncation(c, r, f, c, r, f, 1e-3, 10.0, bx=box, by=box)
+    with pytest.raises(UsageError):  # both sides or neither
+        ctx.kernel_truncation(c, r, f, c, r, f, 1e-3, 10.0, gx=g4, hy=g4, bx=box)
+    with pytest.raises(DataError):  # K x 6 boxes
+        ctx.kernel_truncation(c, r, f, c, r, f, 1e-3, 10.0, gx=g4, hy=g4, bx=box[:5], by=box)
+    m = ctx.kernel_truncation(c, r, f, c, r, f, 1e-3, 10.0, gx=g4, hy=g4, bx=box, by=box)
+    assert m.shape == (10, 10) and m.any()
+
+
 def _acceptance4_fixtures():
     """20 random fixtures up to N = M = 2000 for SPEC.md:590 / :303: D = 2
     and 3; mixtures, uniform clouds, shifted copies; unequal N, M; random

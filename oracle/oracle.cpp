@@ -274,11 +274,14 @@ inline double quad_edge(double u, double v, double A, double B) {
   return (u * A + v * B) - 0.5 * (c * c);
 }
 inline double box_quad(double u, double v, double l1, double h1, double l2, double h2) {
-  const double c1 = quad_edge(u, v, l1, std::fmin(std::fmax(l1 + v, l2), h2));
-  const double c2 = quad_edge(u, v, h1, std::fmin(std::fmax(h1 + v, l2), h2));
-  const double c3 = quad_edge(u, v, std::fmin(std::fmax(l2 + u, l1), h1), l2);
-  const double c4 = quad_edge(u, v, std::fmin(std::fmax(h2 + u, l1), h1), h2);
-  return std::fmax(std::fmax(c1, c2), std::fmax(c3, c4));
+  // u a + v b - (a - b)^2/2 grows along a = b with slope (u + v)/2, so for
+  // u + v >= 0 its maximum over the rectangle has a = h1 or b = h2 (else
+  // a = l1 or b = l2), the other variable at its clamped stationary point
+  const bool up = u + v >= 0.0;
+  const double A = up ? h1 : l1, B = up ? h2 : l2;
+  const double ca = quad_edge(u, v, A, std::fmin(std::fmax(A + v, l2), h2));
+  const double cb = quad_edge(u, v, std::fmin(std::fmax(B + u, l1), h1), B);
+  return std::fmax(ca, cb);
 }
 
 // BI / BJ (nullable, only with GI / HJ): member box {lo[3], hi[3]} of the

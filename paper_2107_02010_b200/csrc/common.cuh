@@ -62,6 +62,7 @@ struct Problem {
   const int32_t* fb_rlab;
   const int32_t* fb_co;
   int32_t fb_words, fb_kc, fb_trans;
+  int32_t fb_upper;          // self mask holding its upper half only (mask_mirror)
   float ell;                 // (1/lambda - 1) / (eps ln2): row/column reference shift
   int32_t n_rows, n_cols;
   float sc;                // 1 / sqrt(2 eps ln2): scaled |dx|^2 = C / (eps ln2)

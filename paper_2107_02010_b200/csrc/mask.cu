@@ -268,7 +268,7 @@ constexpr int kMaskThreads = 32;
 // rare float64 box path spills)
 __global__ void __launch_bounds__(kMaskThreads, 1024 / kMaskThreads)
 mask_rows_kernel(MaskIn m, const float4* blk, const float* blkg, double thr, int self,
-                 uint32_t* mask, int32_t* best, uint32_t* colany, int32_t row0) {
+                 uint32_t* mask, int32_t* best, uint32_t* colany, int32_t row0, int upper) {
   __shared__ double sv[kMaskThreads / 32];
   __shared__ int32_t sj[kMaskThreads / 32];
   const int32_t I = row0 + static_cast<int32_t>(blockIdx.x);
@@ -282,11 +282,15 @@ mask_rows_kernel(MaskIn m, const float4* blk, const float* blkg, double thr, int
   const float4 LI = bx ? m.lx[I] : zero, UI = bx ? m.ux[I] : zero;
   uint32_t* row = mask + static_cast<int64_t>(I) * m.words;
   bool any = false;
-  // pass 1
-  for (int32_t w0 = warp * 32; w0 < m.words; w0 += kMaskThreads) {
+  // pass 1 (upper: a self mask's words from the diagonal word on; the words
+  // below, the transpose of other rows' words, are zeroed here and filled by
+  // mask_mirror where a consumer needs the whole mask)
+  const int32_t wmin = upper ? (I >> 5) : 0;
+  for (int32_t w = threadIdx.x; w < wmin; w += kMaskThreads) row[w] = 0u;
+  for (int32_t w0 = (wmin & ~31) + warp * 32; w0 < m.words; w0 += kMaskThreads) {
     const int32_t wl = w0 + lane;
     bool need = false;
-    if (wl < m.words) {
+    if (wl < m.words && wl >= wmin) {
       const float4 B = blk[wl];
       const double u = static_cast<double>(ub_regs(X, rI, F, B, B.w, blkg[wl], m.d));
       need = u >= thr || (self && (I >> 5) == wl);
@@ -439,6 +443,56 @@ __global__ void mask_best_kernel(const int32_t* br, int32_t r0, int32_t r1, cons
   if (maskT) atomicOr(&maskT[static_cast<int64_t>(J) * wt + (I >> 5)], 1u << (I & 31));
 }
 
+// Lower half of a self mask from its upper half: the slack is exactly
+// symmetric (pair_slack), so bit (I, J) = bit (J, I).  One CTA per 8 x 8
+// group of 32 x 32 bit blocks (bi, bj), bj < bi: warp w reads rows
+// (8 BJ + w) * 32 + lane, words 8 BI .. 8 BI + 7 (one sector per row), 32
+// ballots per block transpose them into shared memory, and each thread then
+// writes one row's 8 words of the group (one sector per row).
+__global__ void __launch_bounds__(256) mask_mirror_kernel(uint32_t* mask, int32_t k, int32_t words) {
+  __shared__ uint32_t T[256][9];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int32_t BI = static_cast<int32_t>(blockIdx.y), BJ = static_cast<int32_t>(blockIdx.x);
+  if (BJ > BI) return;
+  const int32_t bj = BJ * 8 + w, J = bj * 32 + lane;
+  uint32_t vq[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {  // all eight loads in flight
+    const int32_t bi = BI * 8 + q;
+    vq[q] = (J < k && bi < words) ? mask[static_cast<int64_t>(J) * words + bi] : 0u;
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint32_t v = vq[q];
+    uint32_t out = 0u;
+#pragma unroll
+    for (int b = 0; b < 32; ++b) {
+      const uint32_t t = __ballot_sync(0xffffffffu, (v >> b) & 1u);
+      if (lane == b) out = t;
+    }
+    T[q * 32 + lane][w] = out;  // row bi * 32 + lane, word bj
+  }
+  __syncthreads();
+  const int32_t I = BI * 256 + static_cast<int32_t>(threadIdx.x);
+  if (I >= k) return;
+  const int32_t bi = I >> 5;
+  uint32_t* row = mask + static_cast<int64_t>(I) * words;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int32_t wj = BJ * 8 + q;
+    if (wj < bi) row[wj] = T[threadIdx.x][q];
+  }
+}
+
+cudaError_t mask_mirror(uint32_t* mask, int32_t k, cudaStream_t st) {
+  if (k <= 32) return cudaSuccess;
+  const int32_t words = mask_words(k);
+  const unsigned g = static_cast<unsigned>((words + 7) / 8);
+  ++g_launches;
+  mask_mirror_kernel<<<dim3(g, g), 256, 0, st>>>(mask, k, words);
+  return cudaGetLastError();
+}
+
 cudaError_t truncation_masks(int32_t kx, int32_t ky, int d, const float4* cx, const float* rx,
                              const float* fx, const float4* gx, const float4* cy, const float* ry,
                              const float* gy, const float4* hy, double eps, double theta, int self,
@@ -468,8 +522,10 @@ cudaError_t truncation_masks(int32_t kx, int32_t ky, int d, const float4* cx, co
       cy, ry, gy, ky, d, blk_y, blkg_y);
   ++g_launches;
   mask_rows_kernel<<<static_cast<unsigned>(kx), kMaskThreads, 0, st>>>(
-      m, blk_y, blkg_y, thr, self, mask, best_r, col_pass ? colany : nullptr, 0);
+      m, blk_y, blkg_y, thr, self, mask, best_r, col_pass ? colany : nullptr, 0, self);
   if (self) {
+    const cudaError_t e = mask_mirror(mask, kx, st);
+    if (e != cudaSuccess) return e;
     ++g_launches;
     mask_best_kernel<<<static_cast<unsigned>((kx + 255) / 256), 256, 0, st>>>(
         best_r, 0, kx, best_r, 0, mask, m.words, mask, m.words);
@@ -493,7 +549,7 @@ cudaError_t truncation_masks(int32_t kx, int32_t ky, int d, const float4* cx, co
       cx, rx, fx, kx, d, blk_x, blkg_x);
   ++g_launches;
   mask_rows_kernel<<<static_cast<unsigned>(ky), kMaskThreads, 0, st>>>(t, blk_x, blkg_x, thr, 0,
-                                                                         maskT, best_c, nullptr, 0);
+                                                                         maskT, best_c, nullptr, 0, 0);
   ++g_launches;
   mask_best_kernel<<<static_cast<unsigned>((static_cast<int64_t>(kx) + ky + 255) / 256), 256, 0, st>>>(
       best_r, 0, kx, best_c, ky, mask, m.words, maskT, t.words);
@@ -541,7 +597,7 @@ cudaError_t truncation_masks_rows(int32_t kx, int32_t ky, int d, const float4* c
   if (r1 <= r0) return cudaGetLastError();
   ++g_launches;
   mask_rows_kernel<<<static_cast<unsigned>(r1 - r0), kMaskThreads, 0, st>>>(
-      m, blk_y, blkg_y, thr, self, mask, best_r, nullptr, r0);
+      m, blk_y, blkg_y, thr, self, mask, best_r, nullptr, r0, self);
   ++g_launches;
   mask_best_kernel<<<static_cast<unsigned>((r1 - r0 + 255) / 256), 256, 0, st>>>(
       best_r, r0, r1, nullptr, 0, mask, m.words, nullptr, 0);

@@ -177,6 +177,12 @@ cudaError_t truncation_masks(int32_t kx, int32_t ky, int d, const float4* cx, co
                              const float* gy, const float4* hy, double eps, double theta, int self,
                              uint32_t* mask, uint32_t* maskT, int32_t* best_r, int32_t* best_c,
                              void* blkws, cudaStream_t st, const float4* const* box = nullptr);
+// Self masks: lower half from the upper half (bitwise transpose of the
+// blocks below the diagonal).  truncation_masks_rows(self) computes the
+// upper half only (row I: words from I / 32 on, the words below zero) — all
+// the evaluate-once pair sets read — and leaves the mirror to the callers
+// that need whole rows.
+cudaError_t mask_mirror(uint32_t* mask, int32_t k, cudaStream_t st);
 cudaError_t truncation_masks_rows(int32_t kx, int32_t ky, int d, const float4* cx, const float* rx,
                                   const float* fx, const float4* gx, const float4* cy,
                                   const float* ry, const float* gy, const float4* hy, double eps,

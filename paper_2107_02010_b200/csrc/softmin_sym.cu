@@ -332,8 +332,22 @@ __global__ void softmin_fallback_dense(const __grid_constant__ Group G) {
     if (!P.fb_mask) {
       for (int j = lane; j < P.n_cols; j += 32) fb_term<D>(P, xv, j, m, s);
     } else if (!P.fb_trans) {  // mask row of the row's cluster: kept column clusters
-      const uint32_t* mrow = P.fb_mask + static_cast<int64_t>(P.fb_rlab[r]) * P.fb_words;
-      for (int w0 = 0; w0 < P.fb_words; w0 += 32) {
+      const int I = P.fb_rlab[r];
+      const uint32_t* mrow = P.fb_mask + static_cast<int64_t>(I) * P.fb_words;
+      // an upper-half self mask: clusters below the diagonal word from their
+      // own rows (the mask is symmetric), the rest from row I
+      const int wlo = P.fb_upper ? (I >> 5) : 0;
+      for (int J0 = 0; J0 < wlo * 32; J0 += 32) {
+        const int J = J0 + lane;
+        const bool keep = (P.fb_mask[static_cast<int64_t>(J) * P.fb_words + (I >> 5)] >> (I & 31)) & 1u;
+        uint32_t b = __ballot_sync(0xffffffffu, keep);
+        while (b) {
+          const int Jk = J0 + __ffs(b) - 1;
+          b &= b - 1;
+          for (int j = P.fb_co[Jk] + lane; j < P.fb_co[Jk + 1]; j += 32) fb_term<D>(P, xv, j, m, s);
+        }
+      }
+      for (int w0 = wlo; w0 < P.fb_words; w0 += 32) {
         const uint32_t bits = (w0 + lane < P.fb_words) ? mrow[w0 + lane] : 0u;
         for (int src = 0; src < 32; ++src) {
           uint32_t b = __shfl_sync(0xffffffffu, bits, src);

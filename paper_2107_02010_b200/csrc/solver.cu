@@ -1035,6 +1035,7 @@ void run_group_sym(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& s
       Q.fb_co = X.fco[p];
       Q.fb_words = X.words[p];
       Q.fb_trans = p == 3;
+      Q.fb_upper = p < 2;  // fine-phase self masks hold their upper halves
       Q.fb_kc = X.kc3;
       if (!Q.fb_rlab || !Q.fb_co) Q.fb_mask = nullptr;
     }
@@ -2159,6 +2160,11 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
         CK(truncation_masks(X.k, Y.k, d, X.cpts, X.radii, fmax[3], g[3], Y.cpts, Y.radii, fmax[2],
                             g[2], e, theta, 0, mxy, myx, bxr, byr, bws, st, Bxy));
       }
+      if (once && (c->profiling || c->cap_scale >= tsw)) {
+        // whole self masks for the pair count and the debug capture
+        CK(mask_mirror(mxx, X.k, st));
+        CK(mask_mirror(myy, Y.k, st));
+      }
       if (c->profiling) {  // cluster-granularity pair count of the four masks
         double* cnt = c->buf<double>("m.cnt", 1);
         CK(cudaMemsetAsync(cnt, 0, sizeof(double), st));
@@ -2220,6 +2226,7 @@ void solve_device(msot_ctx* c, const msot_params* prm, const double* d_x, const 
       S->pairs_mask_terms += mask_terms;
     }
     if (once && d_grad) {  // the plans of grad_positions read per-row ranges
+      CK(mask_mirror(mxx, X.k, st));
       mask_rangeset(c, "f.xx", X.labels, X.offsets_h, n, X.offsets, X.k, mxx, fxx);
       mask_rangeset(c, "f.yx", X.labels, X.offsets_h, n, Y.offsets, Y.k, mxy, fyx);
     }

@@ -908,7 +908,9 @@ __global__ void sym_runs_kernel(const uint32_t* tbits, int32_t words, int64_t nt
   const int64_t base = kWrite ? rptr[t] : 0;
   if (kWrite && self && lane == 0) ranges[base] = make_int2(ts[t], co[I1 + 1]);
   uint32_t carry = 0;  // top bit of the previous word
-  for (int32_t w0 = 0; w0 < words; w0 += 32) {
+  // self: the words below I1's hold no list bits (posword is read only where
+  // a word has list bits)
+  for (int32_t w0 = self ? ((I1 >> 5) & ~31) : 0; w0 < words; w0 += 32) {
     const int32_t w = w0 + lane;
     const uint32_t b = w < words ? list_bits(tb[w], w, I1, self) : 0u;
     const uint32_t up = __shfl_up_sync(0xffffffffu, b, 1);
@@ -972,6 +974,9 @@ __global__ void sym_entries_kernel(const uint32_t* tbits, int32_t words, int32_t
   int32_t c = 0;
   for (int64_t t = t0; t < t1; ++t) {
     const int32_t I1 = self ? rl[ts[t + 1] - 1] : -1;
+    // self: I1 grows with t, and past this word neither list bits nor the
+    // head entry remain
+    if (self && I1 >= (w + 1) * 32) break;
     const uint32_t b = list_bits(tbits[t * words + w], w, I1, self);
     const bool head = self && J == I1;
     const bool mine = J < k && (((b >> lane) & 1u) || head);

@@ -461,8 +461,10 @@ def main():
         "data": "synthetic (seeded Gaussian mixtures)",
         "config": {**{k: v for k, v in w.items()}, "parallelism": f"rows sharded x{world}",
                    "l2": "256 MB buffer written between timed steps",
-                   "t_switch": st["t_switch"], "n_scales": st["n_scales"], "kx": st["kx"],
-                   "ky": st["ky"], "cluster_scale": st["cluster_scale"]},
+                   # the reference arm prints the same workload keys; the values
+                   # this run resolved (voxel edge, switch scale) sit beside them
+                   "resolved": {"cluster_scale": st["cluster_scale"], "t_switch": st["t_switch"],
+                                "n_scales": st["n_scales"], "kx": st["kx"], "ky": st["ky"]}},
         "S_eps": loss,
         "S_eps_dense_rel_diff": dense_rel(loss, w),
         "pairs_evaluated": st["pairs_evaluated"],

@@ -1,7 +1,9 @@
 """compute-sanitizer on the product kernels: one small
 multiscale 3-D solve (clustering, masks, evaluate-once fine phase, loss)
 and one small high-D solve (tcgen05 / TMA / mbarrier kernels) under memcheck,
-and the 3-D solve under racecheck (shared-memory hazards) and synccheck.
+the 3-D solve under racecheck (shared-memory hazards) and synccheck, and the
+truncation-mask ABI (upper-half self masks + mask_mirror) under memcheck and
+racecheck.
 The solve runs in a child process through the C ABI (no torch)."""
 import os
 import shutil
@@ -30,6 +32,22 @@ if kind == "3d":
     y = cen[rng.integers(0, 4, 2600)] + rng.normal(0, 0.05, (2600, 3)) + 0.01
     a, b = np.full(3000, 1 / 3000), np.full(2600, 1 / 2600)
     prm = make_params(blur=0.02, multiscale=True, retruncate=1, cluster_scale=0.06, super_level=1)
+elif kind == "mask":
+    # truncation masks through the ABI: self (upper half + mask_mirror) and
+    # cross, with slopes and member boxes
+    k = 1100
+    c = rng.random((k, 3)).astype(np.float32)
+    r = (rng.random(k) * 0.05).astype(np.float32)
+    f = (rng.random(k) * 0.01).astype(np.float32)
+    g = np.concatenate([rng.normal(0, 0.2, (k, 3)), f[:, None] + 0.001], 1).astype(np.float32)
+    box = np.concatenate([-rng.random((k, 3)) * r[:, None], rng.random((k, 3)) * r[:, None]],
+                         1).astype(np.float32)
+    m1 = ctx.kernel_truncation(c, r, f, c, r, f, 1e-3, 10.0, self_=True, gx=g, hy=g, bx=box, by=box)
+    m2 = ctx.kernel_truncation(c, r, f, c[::-1].copy(), r, f, 1e-3, 10.0, gx=g, hy=g, bx=box, by=box)
+    assert (m1 == m1.T).all() and 0 < m1.mean() < 1 and 0 < m2.mean() < 1
+    print("ok", m1.mean(), m2.mean())
+    ctx.close()
+    sys.exit(0)
 else:
     x, y = rng.random((700, 60)) * 0.2, rng.random((600, 60)) * 0.2
     a, b = np.full(700, 1 / 700), np.full(600, 1 / 600)
@@ -42,7 +60,8 @@ ctx.close()
 
 
 @pytest.mark.parametrize("tool,kind", [("memcheck", "3d"), ("memcheck", "hd"),
-                                       ("racecheck", "3d"), ("synccheck", "3d")])
+                                       ("racecheck", "3d"), ("synccheck", "3d"),
+                                       ("memcheck", "mask"), ("racecheck", "mask")])
 def test_compute_sanitizer(tmp_path, tool, kind):
     if not os.path.exists(SAN):
         pytest.skip("compute-sanitizer not installed")

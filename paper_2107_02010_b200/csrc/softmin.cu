@@ -253,6 +253,27 @@ __global__ void __launch_bounds__(kTileRows) plan_finalize(const __grid_constant
   P.row_plan[r] = s;
 }
 
+// Sum over a tile's items k0 <= k < k1 of one row's partial (part[(k - i0) *
+// kTileRows]): four interleaved running sums (item k0 + 4i + u feeds sum u),
+// combined as (s0 + s1) + (s2 + s3) — four loads in flight per step, and the
+// same additions whether the items are reduced per batch or at finalize.
+__device__ __forceinline__ float sum_items(const float* part, int32_t k0, int32_t k1, int32_t i0) {
+  const float* q = part + static_cast<int64_t>(k0 - i0) * kTileRows;
+  const int32_t n = k1 - k0;
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  int32_t i = 0;
+  for (; i + 3 < n; i += 4, q += 4 * kTileRows) {
+    s0 += q[0];
+    s1 += q[kTileRows];
+    s2 += q[2 * kTileRows];
+    s3 += q[3 * kTileRows];
+  }
+  if (i < n) s0 += q[0];
+  if (i + 1 < n) s1 += q[kTileRows];
+  if (i + 2 < n) s2 += q[2 * kTileRows];
+  return (s0 + s1) + (s2 + s3);
+}
+
 // Combines the partial sums of every row (fixed chunk order: deterministic
 // and independent of the number of GPUs) and applies the update
 //   new = est - mixw * lambda eps ln(s)   (averaging of PAPER.md:293-315).
@@ -271,8 +292,7 @@ __global__ void __launch_bounds__(kTileRows) softmin_finalize(const __grid_const
   if (P.row_sum) {  // batched group: the row partials were reduced per batch
     s = P.row_sum[r];
   } else {
-    const int32_t k0 = P.tile_ibase[t], k1 = P.tile_ibase[t + 1];
-    for (int32_t k = k0; k < k1; ++k) s += G.part[static_cast<int64_t>(k) * kTileRows + lr];
+    s = sum_items(G.part + lr, P.tile_ibase[t], P.tile_ibase[t + 1], 0);
   }
   if (P.row_add) s += P.row_add[r];  // column side of an evaluate-once self problem
   const float est = P.row_est ? P.row_est[r] : 0.f;
@@ -287,7 +307,7 @@ __global__ void __launch_bounds__(kTileRows) softmin_finalize(const __grid_const
 }
 
 // Row partials of one colpart batch (solver.cu: Plan::Batch): the rows of
-// the batch's tiles sum their items' partials in item order — the same float
+// the batch's tiles sum their items' partials (sum_items) — the same float
 // additions softmin_finalize makes unbatched — into P.row_sum.  G.part holds
 // the batch's items only (item k at k - i0); G.t0 / tile_prefix describe the
 // batch's tiles.
@@ -301,10 +321,7 @@ __global__ void __launch_bounds__(kTileRows) softmin_rowsum(const __grid_constan
   const int lr = threadIdx.x;
   const int r = P.tile_start[t] + lr;
   if (r >= P.tile_start[t + 1]) return;
-  const int32_t k0 = P.tile_ibase[t], k1 = P.tile_ibase[t + 1];
-  float s = 0.f;
-  for (int32_t k = k0; k < k1; ++k) s += G.part[static_cast<int64_t>(k - i0) * kTileRows + lr];
-  P.row_sum[r] = s;
+  P.row_sum[r] = sum_items(G.part + lr, P.tile_ibase[t], P.tile_ibase[t + 1], i0);
 }
 
 // Exact online-max LSE for the rows the fixed-reference path rejected: one

@@ -1,13 +1,15 @@
-"""One C2 solve (100k vs 100k mixtures, seeds 3/4, bench parameters) after two
-warm-ups, for launch lists: python tools/c2_once.py"""
+"""One C2 solve (100k vs 100k mixtures, seeds 3/4, bench.py's parameters)
+after two warm-ups, for launch lists: python tools/c2_once.py [n]"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import bench
 from paper_2107_02010_b200.solver import Context
-w = dict(bench.WORKLOAD, n=100000, m=100000)
-x, y = bench.mixture(100000, 3), bench.mixture(100000, 4)
-a = np.full(100000, 1e-5)
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 100000
+x, y = bench.mixture(n, 3), bench.mixture(n, 4)
+a = np.full(n, 1.0 / n)
+w = dict(bench.WORKLOAD, n=n, m=n)
 ctx = Context(0)
 for _ in range(3):
     loss, _, st = ctx.sinkhorn(bench.params(w), x, a, y, a, potentials=False)

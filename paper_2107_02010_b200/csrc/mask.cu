@@ -178,7 +178,7 @@ __device__ __forceinline__ float2 bounds_regs(float4 X, float rI, float F, float
                                               float rJ, float G, float4 HJ, int d, bool g,
                                               bool box = false, float4 LI = float4{},
                                               float4 UI = float4{}, float4 LJ = float4{},
-                                              float4 UJ = float4{}, double thr = -INFINITY) {
+                                              float4 UJ = float4{}, float thr = -INFINITY) {
   const float dx = X.x - Y.x, dy = d > 1 ? X.y - Y.y : 0.f, dz = d > 2 ? X.z - Y.z : 0.f;
   const float s = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
   const float rr = rI + rJ;
@@ -194,7 +194,7 @@ __device__ __forceinline__ float2 bounds_regs(float4 X, float rI, float F, float
     const float vb = ((GI.w + HJ.w) + marg) - 0.5f * s;
     v = fminf(v, vb);
     mag += fabsf(GI.w) + fabsf(HJ.w) + marg;
-    if (box && static_cast<double>(v + 1e-5f * mag) >= thr) {
+    if (box && v + 1e-5f * mag >= thr) {
       float q = box_quad_f(a0, b0, LI.x, UI.x, LJ.x, UJ.x);
       if (d > 1) q += box_quad_f(a1, b1, LI.y, UI.y, LJ.y, UJ.y);
       if (d > 2) q += box_quad_f(a2, b2, LI.z, UI.z, LJ.z, UJ.z);
@@ -281,6 +281,9 @@ mask_rows_kernel(MaskIn m, const float4* blk, const float* blkg, double thr, int
   const bool bx = m.box();
   const float4 LI = bx ? m.lx[I] : zero, UI = bx ? m.ux[I] : zero;
   uint32_t* row = mask + static_cast<int64_t>(I) * m.words;
+  // for a float v, double(v) >= thr  <=>  v >= thrf (the least float >= thr):
+  // the float screens compare without conversions
+  const float thrf = __double2float_ru(thr);
   bool any = false;
   // pass 1 (upper: a self mask's words from the diagonal word on; the words
   // below, the transpose of other rows' words, are zeroed here and filled by
@@ -292,20 +295,20 @@ mask_rows_kernel(MaskIn m, const float4* blk, const float* blkg, double thr, int
     bool need = false;
     if (wl < m.words && wl >= wmin) {
       const float4 B = blk[wl];
-      const double u = static_cast<double>(ub_regs(X, rI, F, B, B.w, blkg[wl], m.d));
-      need = u >= thr || (self && (I >> 5) == wl);
+      const float u = ub_regs(X, rI, F, B, B.w, blkg[wl], m.d);
+      need = u >= thrf || (self && (I >> 5) == wl);
       if (!need) row[wl] = 0u;
     }
     uint32_t todo = __ballot_sync(0xffffffffu, need);
     // two words per step: both words' column loads are in flight together
     auto keep_of = [&](int32_t J, float4 Y, float rJ, float G, float4 HJ) {
       bool keep = self && I == J;  // diagonal of a self mask
-      if (static_cast<double>(ub_regs(X, rI, F, Y, rJ, G, m.d)) >= thr) {
+      if (ub_regs(X, rI, F, Y, rJ, G, m.d) >= thrf) {
         const float4 LJ = bx ? m.ly[J] : zero, UJ = bx ? m.uy[J] : zero;
-        const float2 vm = bounds_regs(X, rI, F, GI, Y, rJ, G, HJ, m.d, g, bx, LI, UI, LJ, UJ, thr);
-        if (static_cast<double>(vm.x - vm.y) >= thr)
+        const float2 vm = bounds_regs(X, rI, F, GI, Y, rJ, G, HJ, m.d, g, bx, LI, UI, LJ, UJ, thrf);
+        if (vm.x - vm.y >= thrf)
           keep = true;  // float32 lower bound settles it
-        else if (static_cast<double>(vm.x + vm.y) >= thr)  // in between: float64
+        else if (vm.x + vm.y >= thrf)  // in between: float64
           keep = keep || pair_slack(X, rI, F, GI, Y, rJ, G, HJ, m.d, g, bx, LI, UI, LJ, UJ, thr) >= thr;
       }
       return keep;

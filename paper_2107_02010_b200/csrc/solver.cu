@@ -732,7 +732,10 @@ void shard_tiles(const std::vector<double>& work, int world, std::vector<int64_t
 void build_plan(msot_ctx* c, const std::string& tag, Plan& P, int waves = 32, int dim = 3) {
   cudaStream_t st = c->st;
   // per-problem shard of row tiles, weighted by evaluated pairs
-  int64_t tot_tiles = 0, tot_cols = 0;
+  // tot_cols_all: the group's columns over every rank's tiles — item and
+  // batch sizing depend on it, not on this rank's share, so the items (and
+  // the row sums' additions) are the same for any number of GPUs
+  int64_t tot_tiles = 0, tot_cols = 0, tot_cols_all = 0;
   P.pairs_all = P.pairs_local = P.terms_all = 0.0;
   for (int p = 0; p < P.np; ++p) {
     const RangeSet& R = *P.ps[p].rs;
@@ -749,6 +752,7 @@ void build_plan(msot_ctx* c, const std::string& tag, Plan& P, int waves = 32, in
     std::vector<int64_t> tb;
     shard_tiles(work, c->world, tb);
     if (p == 0 && P.skip_p0) tb.assign(c->world + 1, 0);
+    for (int64_t t = tb[0]; t < tb[c->world]; ++t) tot_cols_all += R.tile_cols_h[t];
     P.t0[p] = tb[c->rank];
     P.t1[p] = tb[c->rank + 1];
     P.row_bounds[p].resize(c->world + 1);
@@ -765,16 +769,14 @@ void build_plan(msot_ctx* c, const std::string& tag, Plan& P, int waves = 32, in
   // against ~2 waves (8: 321, 16: 315, 64: 315 ms); the high-D kernel keeps 2
   // (its CTAs walk block ranges; 32 cost config 4 ~1.5%)
   const int64_t target = static_cast<int64_t>(c->n_sm) * 12 * waves;
-  int64_t chunk = std::max<int64_t>(2 * kColTile, (tot_cols + target - 1) / std::max<int64_t>(target, 1));
+  int64_t chunk = std::max<int64_t>(2 * kColTile, (tot_cols_all + target - 1) / std::max<int64_t>(target, 1));
   chunk = (chunk + kColTile - 1) / kColTile * kColTile;
+  (void)tot_cols;
   if (P.ps[0].sym) {
     // colpart batches: consecutive (problem, tile) runs of at most `budget`
     // slots; each batch is cut into ~`waves` waves of items of its own
-    int64_t rows_cols = 0, slots_all = 0;
-    for (int p = 0; p < P.np; ++p) {
-      rows_cols += P.ps[p].n_rows + P.ps[p].n_cols;
-      for (int64_t t = P.t0[p]; t < P.t1[p]; ++t) slots_all += P.ps[p].rs->tile_cols_h[t];
-    }
+    int64_t rows_cols = 0, slots_all = tot_cols_all;  // every rank's slots
+    for (int p = 0; p < P.np; ++p) rows_cols += P.ps[p].n_rows + P.ps[p].n_cols;
     // automatic budget: per atom of the group or of the whole solve, whichever
     // is larger (coarse-level groups are quadratic in the cluster count, far
     // below N + M: they keep one batch)

@@ -2,8 +2,10 @@
 (msot_create_dist_host): two processes, each a rank with its own context on
 cuda:0, exchanging column sums (all-reduce) and row shards (broadcast) over
 gloo instead of NCCL.  The sharded result must match the single-rank solve:
-bitwise for the row-wise (dense) path, to float rounding (1e-3 eps) for the
-evaluate-once path (its column sums are added across ranks)."""
+bitwise for row-wise pair sets (dense solves, pair_eval 0: every row reduced
+by one rank in an item order that does not depend on the rank count), to
+float rounding (1e-3 eps) for the evaluate-once path (its column sums are
+added across ranks)."""
 import math
 import os
 import socket
@@ -32,11 +34,16 @@ CASES = {
     "dense": dict(blur=0.05),
     "multiscale": dict(blur=0.01, multiscale=True, retruncate=1, cluster_scale=0.04),
     "unbalanced": dict(blur=0.02, reach=0.3, multiscale=True, retruncate=1, cluster_scale=0.04),
+    # row-wise pair sets (pair_eval 0): every row reduced by its own rank in a
+    # fixed item order -> bitwise identical for any number of GPUs
+    "multiscale_rowwise": dict(blur=0.01, multiscale=True, retruncate=1, cluster_scale=0.04,
+                               pair_eval=0),
 }
+BITWISE = ("dense", "multiscale_rowwise", "bench_rowwise")
 
 
 def _inputs(case):
-    if case == "bench":  # bench.py's generator and parameters at 30k
+    if case.startswith("bench"):  # bench.py's generator and parameters at 30k
         import bench
         w = dict(bench.WORKLOAD, n=30000, m=30000)
         return bench.make_inputs(w)
@@ -53,9 +60,12 @@ def _inputs(case):
 
 def _params(case):
     from paper_2107_02010_b200.abi import make_params
-    if case == "bench":
+    if case.startswith("bench"):
         import bench
-        return bench.params(dict(bench.WORKLOAD, n=30000, m=30000))
+        prm = bench.params(dict(bench.WORKLOAD, n=30000, m=30000))
+        if case == "bench_rowwise":
+            prm.pair_eval = 0
+        return prm
     if case == "hd":
         return make_params(blur=0.05, reach=0.3)
     if case == "hd_ms":
@@ -124,40 +134,50 @@ def run_two_ranks(case, timeout=300, world=2, env=None):
     return out
 
 
-@pytest.mark.parametrize("case", ["dense", "multiscale", "unbalanced", "hd", "hd_ms"])
+def _check_ranks(case, l1, p1, out, world):
+    ref = [p1.a_xx, p1.b_yy, p1.a_xy, p1.b_yx]
+    eps = _params(case).blur ** 2
+    for rank in range(world):
+        lw, pw, w = out[rank]
+        assert w == world
+        for u, v in zip(pw, ref):
+            if case in BITWISE:
+                np.testing.assert_array_equal(u, v)
+            else:
+                # evaluate-once: float32 column sums added in another order
+                # (per-rank partials), compounded over the eps schedule
+                assert np.abs(u - v).max() <= 1e-3 * eps
+        if case in BITWISE:
+            assert lw == l1
+        else:
+            assert abs(lw - l1) <= 1e-6 * abs(l1) + 1e-12
+
+
+@pytest.mark.parametrize("case", ["dense", "multiscale", "unbalanced", "hd", "hd_ms",
+                                  "multiscale_rowwise"])
 def test_two_ranks_match_one(ctx, case):
     x, a, y, b = _inputs(case)
     l1, p1, _ = ctx.sinkhorn(_params(case), x, a, y, b)
-    out = run_two_ranks(case)
-    ref = [p1.a_xx, p1.b_yy, p1.a_xy, p1.b_yx]
-    eps = _params(case).blur ** 2
-    for rank in (0, 1):
-        l2, p2, world = out[rank]
-        assert world == 2
-        for u, v in zip(p2, ref):
-            if case == "dense":
-                np.testing.assert_array_equal(u, v)
-            else:
-                # float32 column sums added in another order (per-rank
-                # partials), compounded over the eps schedule; masks follow
-                assert np.abs(u - v).max() <= 1e-3 * eps
-        assert abs(l2 - l1) <= 1e-6 * abs(l1) + 1e-12
+    _check_ranks(case, l1, p1, run_two_ranks(case), 2)
 
 
-@pytest.mark.parametrize("case", ["multiscale", "hd_ms"])
+@pytest.mark.parametrize("case", ["multiscale", "hd_ms", "multiscale_rowwise"])
 def test_three_ranks_match_one(ctx, case):
     """Uneven shards: three ranks (row tiles, mask rows and broadcast blocks
     split 3 ways)."""
     x, a, y, b = _inputs(case)
     l1, p1, _ = ctx.sinkhorn(_params(case), x, a, y, b)
-    out = run_two_ranks(case, world=3)
-    eps = _params(case).blur ** 2
-    for rank in range(3):
-        l3, p3, world = out[rank]
-        assert world == 3
-        for u, v in zip(p3, [p1.a_xx, p1.b_yy, p1.a_xy, p1.b_yx]):
-            assert np.abs(u - v).max() <= 1e-3 * eps
-        assert abs(l3 - l1) <= 1e-6 * abs(l1) + 1e-12
+    _check_ranks(case, l1, p1, run_two_ranks(case, world=3), 3)
+
+
+def test_four_ranks_bench_parameters_rowwise_bitwise(ctx):
+    """bench.py's parameters at 30k with row-wise pair sets on four ranks and
+    forced small colpart batches: bitwise the one-rank solve (item cuts do
+    not depend on the rank count)."""
+    x, a, y, b = _inputs("bench_rowwise")
+    l1, p1, _ = ctx.sinkhorn(_params("bench_rowwise"), x, a, y, b)
+    out = run_two_ranks("bench_rowwise", world=4, env={"MSOT_COLPART_BUDGET": "200000"})
+    _check_ranks("bench_rowwise", l1, p1, out, 4)
 
 
 def test_four_ranks_bench_parameters_batched(ctx):

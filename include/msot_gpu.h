@@ -147,7 +147,10 @@ int msot_world_info(const msot_ctx* ctx, int* rank, int* world, int* comm_ranks)
  * the caller (e.g. torch.distributed gloo) in place of NCCL, so the
  * multi-rank logic runs with several processes on one GPU.  allreduce sums
  * `count` floats in place across ranks; broadcast copies root's `count`
- * floats to every rank.  Both return 0 on success. */
+ * 32-bit words to every rank bit for bit (the solver also moves its float64
+ * column totals through it, all-gather style).  Both return 0 on success.
+ * (The current solver exchanges everything through broadcast; allreduce is
+ * kept for the signature and must still be supplied.) */
 typedef int (*msot_host_allreduce_fn)(float* data, int64_t count, void* user);
 typedef int (*msot_host_broadcast_fn)(float* data, int64_t count, int root, void* user);
 int msot_create_dist_host(int device, int rank, int world, msot_host_allreduce_fn allreduce,

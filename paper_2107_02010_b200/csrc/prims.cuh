@@ -42,7 +42,7 @@ struct ColSum {
   const int32_t* etile;
   const int32_t* tile_start;
   const float* colpart;       // base such that colpart[eslot] is the slot (batch-shifted)
-  float* tot;
+  float* tot;                 // null: the float64 total stays in acc (multi-rank exchange)
   double* acc;                // running float64 totals across batches (nullable: one batch)
   int32_t n_cols, self, t0, t1;
   int32_t first, last;        // first / last batch of this problem
@@ -54,6 +54,7 @@ struct ColSumGroup {
 // uniform: every row weight equal and lambda = 1 (column sums need no row factor)
 cudaError_t launch_softmin_sym(const Group& g, int d, bool uniform, cudaStream_t st);
 cudaError_t launch_colsum(const ColSum* c, int n, cudaStream_t st);
+cudaError_t totals_f32(const double* acc, float* tot, int32_t n, cudaStream_t st);
 cudaError_t launch_colfinal(const Group& g, int p, cudaStream_t st);
 cudaError_t launch_fallback_dense(const Group& g, int d, int n_sm, cudaStream_t st);
 cudaError_t sym_ranges(const uint32_t* tbits, int32_t k, int64_t nt, const int32_t* co,

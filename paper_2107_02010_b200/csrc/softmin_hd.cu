@@ -541,8 +541,8 @@ __global__ void hd_colsum_kernel(const float* colpart, const int64_t* tslot, con
     s += static_cast<double>(v3);
   }
   for (; t < te; ++t) s += static_cast<double>(term(t));
-  if (last || !acc) tot[j] = static_cast<float>(s);
-  else acc[j] = s;
+  if ((last || !acc) && tot) tot[j] = static_cast<float>(s);
+  else acc[j] = s;  // (tot null: multi-rank float64 exchange, sym_colsum_kernel)
 }
 
 cudaError_t hd_colsum(const float* colpart, const int64_t* tslot, const int32_t* ts, int32_t t0,

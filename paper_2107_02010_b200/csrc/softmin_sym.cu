@@ -252,8 +252,23 @@ __global__ void sym_colsum_kernel(const __grid_constant__ ColSumGroup g) {
     if (a.self && a.tile_start[t + 1] > j) continue;
     s += static_cast<double>(a.colpart[a.eslot[e] + off]);
   }
-  if (a.last || !a.acc) a.tot[j] = static_cast<float>(s);
+  // (tot null: a multi-rank group keeps the float64 total for the exchange)
+  if ((a.last || !a.acc) && a.tot) a.tot[j] = static_cast<float>(s);
   else a.acc[j] = s;
+}
+
+// Column totals exchanged in float64 (multi-rank): tot = float(acc) after the
+// all-reduce, the one rounding a single-rank solve makes.
+__global__ void totals_f32_kernel(const double* acc, float* tot, int32_t n) {
+  const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) tot[j] = static_cast<float>(acc[j]);
+}
+
+cudaError_t totals_f32(const double* acc, float* tot, int32_t n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  ++g_launches;
+  totals_f32_kernel<<<(n + 255) / 256, 256, 0, st>>>(acc, tot, n);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_colsum(const ColSum* c, int n, cudaStream_t st) {

@@ -215,29 +215,38 @@ namespace {
 constexpr int64_t kColpartPerAtom = 6;
 
 // ------------------------------------------------------------- collectives
-// The two exchange steps of a sharded scale: an all-reduce of
+// The two exchange steps of a sharded scale: a float64 all-reduce of
 // the column sums and a broadcast of every rank's row shard.  NCCL over
 // NVLink in the product; host-staged caller callbacks in the test seam.
 // A communicator of one rank (msot_create_dist with world = 1) runs the NCCL
 // calls too: they are no-ops on the data, but the product's NCCL path is
 // exercised on a one-GPU box (tests/test_dist_gpu.py).
-void coll_allreduce(msot_ctx* c, float* const* bufs, const int64_t* counts, int nb) {
-  if (!c->comm && (c->world <= 1 || !c->host_ar)) return;
+// float64 sum over ranks.  NCCL: ncclDouble all-reduce.  Host seam: each
+// rank's vector travels through the broadcast callback as raw 32-bit words
+// (bit-preserving), and every rank adds them in rank order.
+void coll_allreduce64(msot_ctx* c, double* const* bufs, const int64_t* counts, int nb) {
+  if (!c->comm && (c->world <= 1 || !c->host_bc)) return;
   cudaStream_t st = c->st;
   if (!c->comm) {
     for (int b = 0; b < nb; ++b) {
-      std::vector<float> h(counts[b]);
-      CK(cudaMemcpyAsync(h.data(), bufs[b], counts[b] * sizeof(float), cudaMemcpyDeviceToHost, st));
+      const int64_t n = counts[b];
+      std::vector<double> mine(n), part(n), sum(n, 0.0);
+      CK(cudaMemcpyAsync(mine.data(), bufs[b], n * sizeof(double), cudaMemcpyDeviceToHost, st));
       CK(host_sync(__LINE__, st));
-      if (c->host_ar(h.data(), counts[b], c->host_user) != 0) raise(MSOT_ECUDA, "host all-reduce failed");
-      CK(cudaMemcpyAsync(bufs[b], h.data(), counts[b] * sizeof(float), cudaMemcpyHostToDevice, st));
+      for (int r = 0; r < c->world; ++r) {
+        if (r == c->rank) part = mine;
+        if (n > 0 && c->host_bc(reinterpret_cast<float*>(part.data()), 2 * n, r, c->host_user) != 0)
+          raise(MSOT_ECUDA, "host broadcast failed");
+        for (int64_t j = 0; j < n; ++j) sum[j] += part[j];
+      }
+      CK(cudaMemcpyAsync(bufs[b], sum.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
       CK(host_sync(__LINE__, st));
     }
     return;
   }
   NK(ncclGroupStart());
   for (int b = 0; b < nb; ++b)
-    NK(ncclAllReduce(bufs[b], bufs[b], counts[b], ncclFloat, ncclSum, c->comm, st));
+    NK(ncclAllReduce(bufs[b], bufs[b], counts[b], ncclDouble, ncclSum, c->comm, st));
   NK(ncclGroupEnd());
 }
 
@@ -1081,14 +1090,17 @@ void run_group_sym(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& s
   double* acc[3] = {nullptr, nullptr, nullptr};
   float* rsum[3] = {nullptr, nullptr, nullptr};
   const bool multi = nbt > 1;
+  // several ranks: the column totals are exchanged in float64 and rounded
+  // once afterwards, so they differ from a single rank's only where the
+  // float64 sums (in another association) straddle a float32 rounding point
+  const bool x64 = c->comm || (c->world > 1 && c->host_bc);
   // overlap consecutive batches on the two side streams; profiling keeps
   // every launch on the main stream so each softmin is timed alone
   const bool overlap = multi && !c->profiling;
-  if (multi)
-    for (int p = 0; p < 3; ++p) {
-      acc[p] = c->buf<double>("sym.acc" + std::to_string(p), P.ps[p].n_cols);
-      rsum[p] = c->buf<float>("sym.rsum" + std::to_string(p), P.ps[p].n_rows);
-    }
+  for (int p = 0; p < 3; ++p) {
+    if (multi || x64) acc[p] = c->buf<double>("sym.acc" + std::to_string(p), P.ps[p].n_cols);
+    if (multi) rsum[p] = c->buf<float>("sym.rsum" + std::to_string(p), P.ps[p].n_rows);
+  }
   if (overlap) {
     CK(cudaEventRecord(c->ev_fork, st));
     for (int k = 0; k < 2; ++k) CK(cudaStreamWaitEvent(c->side[k], c->ev_fork, 0));
@@ -1145,11 +1157,12 @@ void run_group_sym(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& s
       const int32_t t0 = has ? B.bt0[p] : 0, t1 = has ? B.bt1[p] : 0;
       if (S.dense) {  // dense pair sets (high-D path, coarse phase, dense solves)
         CK(hd_colsum(cp[p], S.tslot, S.R.tile_start, t0, t1, S.self,
-                     static_cast<int32_t>(P.ps[p].n_cols), X.tot[p], acc[p], first, last, bs));
+                     static_cast<int32_t>(P.ps[p].n_cols), x64 ? nullptr : X.tot[p], acc[p], first,
+                     last, bs));
       } else {
         cs[ncs++] = ColSum{X.labels[p], X.co[p], S.ebase, S.eslot, S.etile, S.R.tile_start, cp[p],
-                           X.tot[p], acc[p], static_cast<int32_t>(P.ps[p].n_cols), S.self, t0, t1,
-                           first, last};
+                           x64 ? nullptr : X.tot[p], acc[p],
+                           static_cast<int32_t>(P.ps[p].n_cols), S.self, t0, t1, first, last};
       }
     }
     if (ncs > 0) CK(launch_colsum(cs, ncs, bs));
@@ -1158,9 +1171,11 @@ void run_group_sym(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& s
   if (overlap) CK(cudaStreamWaitEvent(st, c->ev_cs[(nbt - 1) & 1], 0));
   if (multi)
     for (int p = 0; p < 3; ++p) G.P[p].row_sum = rsum[p];
-  {  // column sums of every rank's tiles (NCCL over NVLink)
+  if (x64) {  // column sums of every rank's tiles (NCCL over NVLink), float64
     const int64_t cnt[3] = {P.ps[0].n_cols, P.ps[1].n_cols, P.ps[2].n_cols};
-    coll_allreduce(c, X.tot, cnt, 3);
+    coll_allreduce64(c, acc, cnt, 3);
+    for (int p = 0; p < 3; ++p)
+      CK(totals_f32(acc[p], X.tot[p], static_cast<int32_t>(P.ps[p].n_cols), st));
   }
   CK(launch_finalize(G, st));
   CK(launch_colfinal(G, 3, st));

@@ -39,6 +39,13 @@ def lib():
         if not os.path.exists(LIB_PATH):
             raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() — "
                                "the solver has no CPU fallback")
+        # libmsot links libnccl.so.2: when torch is installed, load it first
+        # so its bundled (newer) NCCL is the process's libnccl — loading the
+        # system one first would leave torch's CUDA library unresolvable
+        try:
+            import torch  # noqa: F401
+        except ImportError:
+            pass
         L = C.CDLL(LIB_PATH)
         L.msot_last_error.restype = C.c_char_p
         L.msot_params_default.argtypes = [C.POINTER(Params)]

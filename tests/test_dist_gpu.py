@@ -3,9 +3,10 @@
 cuda:0, exchanging column sums (all-reduce) and row shards (broadcast) over
 gloo instead of NCCL.  The sharded result must match the single-rank solve:
 bitwise for row-wise pair sets (dense solves, pair_eval 0: every row reduced
-by one rank in an item order that does not depend on the rank count), to
-float rounding (1e-3 eps) for the evaluate-once path (its column sums are
-added across ranks)."""
+by one rank in an item order that does not depend on the rank count); for
+the evaluate-once path the per-rank float64 column partials are all-reduced
+and rounded once, which is bitwise in every case measured and bounded here
+at 1e-5 eps."""
 import math
 import os
 import socket
@@ -144,13 +145,16 @@ def _check_ranks(case, l1, p1, out, world):
             if case in BITWISE:
                 np.testing.assert_array_equal(u, v)
             else:
-                # evaluate-once: float32 column sums added in another order
-                # (per-rank partials), compounded over the eps schedule
-                assert np.abs(u - v).max() <= 1e-3 * eps
+                # evaluate-once: the per-rank float64 column partials are
+                # added in another association and rounded once to float32,
+                # so a column total can differ by one float32 ulp only where
+                # the float64 sums straddle a rounding point (bitwise in
+                # every case measured, tools/rank_diff.py)
+                assert np.abs(u - v).max() <= 1e-5 * eps
         if case in BITWISE:
             assert lw == l1
         else:
-            assert abs(lw - l1) <= 1e-6 * abs(l1) + 1e-12
+            assert abs(lw - l1) <= 1e-9 * abs(l1) + 1e-15
 
 
 @pytest.mark.parametrize("case", ["dense", "multiscale", "unbalanced", "hd", "hd_ms",
@@ -190,13 +194,7 @@ def test_four_ranks_bench_parameters_batched(ctx):
     l1, p1, s1 = ctx.sinkhorn(_params("bench"), x, a, y, b)
     assert s1["t_super"] > 0 or s1["t_switch"] > 0
     out = run_two_ranks("bench", world=4, env={"MSOT_COLPART_BUDGET": "200000"})
-    eps = 0.01 ** 2
-    for rank in range(4):
-        l4, p4, world = out[rank]
-        assert world == 4
-        for u, v in zip(p4, [p1.a_xx, p1.b_yy, p1.a_xy, p1.b_yx]):
-            assert np.abs(u - v).max() <= 1e-3 * eps
-        assert abs(l4 - l1) <= 1e-6 * abs(l1) + 1e-12
+    _check_ranks("bench", l1, p1, out, 4)
 
 
 @pytest.mark.parametrize("case", ["dense", "multiscale", "unbalanced", "hd_ms"])

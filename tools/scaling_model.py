@@ -3,7 +3,7 @@ per-kernel launch list (profiles/r2_launches_c3.txt, second table: one batch
 per update, whose total equals the timed step) and the NVLink references of
 the B200 profiling guide (8-rank all-reduce bus bandwidth 725 GB/s, peer copy
 770 GB/s per direction), with the per-solve exchange volumes of the sharded
-solver (solver.cu: coll_allreduce / coll_bcast_rows):
+solver (solver.cu: coll_allreduce64 / coll_bcast_rows):
 
     T(N) = replicated + sharded x (1 + imbalance) / N + comm(N) + host waits
 
@@ -47,8 +47,8 @@ def comm_ms(N):
     f = (N - 1) / N
     ar = lambda b: LAT + b * 2 * f / AR_BUS          # ring all-reduce
     bc = lambda b: LAT + b * f / P2P                 # grouped row-shard broadcast
-    t = fine_updates * (ar(4 * (n + 2 * m)) + bc(4 * (2 * n + m)))
-    t += coarse_scales * (ar(4 * (kx + 2 * ky)) + bc(4 * (2 * kx + ky)))
+    t = fine_updates * (ar(8 * (n + 2 * m)) + bc(4 * (2 * n + m)))  # float64 column totals
+    t += coarse_scales * (ar(8 * (kx + 2 * ky)) + bc(4 * (2 * kx + ky)))
     t += rebuilds * bc(mask_bytes)
     return 1e3 * t
 

@@ -30,18 +30,36 @@ __device__ __forceinline__ double km_dist2(const double* x, const double* c, int
 }
 
 // farthest-point step: mind_i = min(mind_i, |x_i - c|^2); per-block argmax
-// (largest, then lowest index)
-__global__ void fps_update_kernel(const double* x, int64_t n, int d, const double* c, double* mind,
-                                  int first, double* bval, int64_t* bidx) {
+// (largest, then lowest index).  asg_i = the centre that attains mind_i,
+// dnew[a] = |c_a - c|^2 (fps_ccdist_kernel): when |c_asg - c| >= 2 sqrt(mind_i)
+// the triangle inequality puts c no closer than the current minimum, so the
+// atom's row is not read at all (margin 1e-9 against the float64 rounding of
+// the three distances, ~1e-14 relative) — mind is exactly what the full scan
+// computes, and most atoms skip once the centres are dense.
+__global__ void fps_update_kernel(const double* x, int64_t n, int d, const double* c, int kc,
+                                  double* mind, int32_t* asg, const double* dnew, int first,
+                                  double* bval, int64_t* bidx) {
   __shared__ double sv[256];
   __shared__ int64_t si[256];
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   double m = -1.0;
   int64_t mi = INT64_MAX;
   if (i < n) {
-    const double dd = km_dist2(x + i * d, c, d);
-    m = first ? dd : fmin(mind[i], dd);
-    mind[i] = m;
+    if (first) {
+      m = km_dist2(x + i * d, c, d);
+      mind[i] = m;
+      asg[i] = kc;
+    } else {
+      m = mind[i];
+      if (!(dnew[asg[i]] >= 4.0 * m * (1.0 + 1e-9))) {
+        const double dd = km_dist2(x + i * d, c, d);
+        if (dd < m) {  // fmin(m, dd)
+          m = dd;
+          mind[i] = m;
+          asg[i] = kc;
+        }
+      }
+    }
     mi = i;
   }
   sv[threadIdx.x] = m;
@@ -92,6 +110,24 @@ __global__ void fps_select_kernel(const double* bval, const int64_t* bidx, int n
   }
   const int64_t w = si[0];
   for (int q = threadIdx.x; q < d; q += blockDim.x) centers[static_cast<int64_t>(k) * d + q] = x[w * d + q];
+}
+
+// distances of the earlier centres to the newest one, centre k
+// (fps_update_kernel's skip; a bound with a margin, so any summation order):
+// one warp per earlier centre, spread over the SMs
+__global__ void fps_ccdist_kernel(const double* centers, int d, int k, double* dnew) {
+  const int lane = threadIdx.x & 31;
+  const int a = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+  if (a >= k) return;
+  const double* ca = centers + static_cast<int64_t>(a) * d;
+  const double* ck = centers + static_cast<int64_t>(k) * d;
+  double s = 0.0;
+  for (int q = lane; q < d; q += 32) {
+    const double t = ca[q] - ck[q];
+    s = fma(t, t, s);
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) dnew[a] = s;
 }
 
 __global__ void copy_center_kernel(const double* x, int64_t i, int d, double* c) {
@@ -256,16 +292,24 @@ cudaError_t kmeans(const double* x, const double* w, int64_t n, int d, int K, ui
   uint32_t* keys = reinterpret_cast<uint32_t*>(p);
   p += n * sizeof(uint32_t);
   void* rtmp = p;
-  // farthest-point seeding
+  // farthest-point seeding (the atoms' nearest-centre index lives in `keys`,
+  // the new centre's distances to the earlier ones in `c2`, both free until
+  // Lloyd)
+  int32_t* asg = reinterpret_cast<int32_t*>(keys);
+  double* dnew = c2;
   ++g_launches;
   copy_center_kernel<<<1, 64, 0, st>>>(x, static_cast<int64_t>(seed % static_cast<uint64_t>(n)), d,
                                        centers);
   for (int k = 1; k < K; ++k) {
     ++g_launches;
-    fps_update_kernel<<<nb, 256, 0, st>>>(x, n, d, centers + static_cast<int64_t>(k - 1) * d, mind,
-                                          k == 1, bval, bidx);
+    fps_update_kernel<<<nb, 256, 0, st>>>(x, n, d, centers + static_cast<int64_t>(k - 1) * d, k - 1,
+                                          mind, asg, dnew, k == 1, bval, bidx);
     ++g_launches;
     fps_select_kernel<<<1, 256, 0, st>>>(bval, bidx, nb, x, d, centers, k);
+    if (k + 1 < K) {
+      ++g_launches;
+      fps_ccdist_kernel<<<(k + 7) / 8, 256, 0, st>>>(centers, d, k, dnew);
+    }
   }
   const int kb = static_cast<int>((static_cast<int64_t>(K) * d + 255) / 256);
   int it = 0;

@@ -136,17 +136,25 @@ __global__ void copy_center_kernel(const double* x, int64_t i, int d, double* c)
 
 // nearest centre of every atom (ties to the lowest centre); centres staged
 // through shared memory in chunks, the atom's coordinates in registers
+// list (nullable): scan only the atoms list[0 .. *count) (km_bounds_kernel).
+// ub / lb (nullable): the distance to the nearest centre and to the second
+// nearest (Hamerly bounds for the next iteration).
 template <int DM>
 __global__ void __launch_bounds__(128) km_assign_kernel(const double* x, int64_t n, int d,
                                                         const double* centers, int K,
-                                                        uint32_t* labels) {
+                                                        uint32_t* labels, const int32_t* list,
+                                                        const int32_t* count, double* ub,
+                                                        double* lb) {
   constexpr int kChunk = 32;
   __shared__ double cs[kChunk * DM];
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t slot = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t m = list ? *count : n;
+  if (static_cast<int64_t>(blockIdx.x) * blockDim.x >= m) return;  // whole block idle
+  const int64_t i = slot < m ? (list ? list[slot] : slot) : n;
   double xr[DM];
 #pragma unroll
   for (int k = 0; k < DM; ++k) xr[k] = (i < n && k < d) ? x[i * d + k] : 0.0;
-  double best = INFINITY;
+  double best = INFINITY, second = INFINITY;
   int bl = 0;
   for (int c0 = 0; c0 < K; c0 += kChunk) {
     const int nc = min(kChunk, K - c0);
@@ -172,11 +180,11 @@ __global__ void __launch_bounds__(128) km_assign_kernel(const double* x, int64_t
           s2 = __dadd_rn(s2, __dmul_rn(t2, t2));
           s3 = __dadd_rn(s3, __dmul_rn(t3, t3));
         }
-      // strict: ties keep the lowest centre
-      if (s0 < best) { best = s0; bl = c0 + c; }
-      if (s1 < best) { best = s1; bl = c0 + c + 1; }
-      if (s2 < best) { best = s2; bl = c0 + c + 2; }
-      if (s3 < best) { best = s3; bl = c0 + c + 3; }
+      // strict: ties keep the lowest centre (and make second == best)
+      if (s0 < best) { second = best; best = s0; bl = c0 + c; } else second = fmin(second, s0);
+      if (s1 < best) { second = best; best = s1; bl = c0 + c + 1; } else second = fmin(second, s1);
+      if (s2 < best) { second = best; best = s2; bl = c0 + c + 2; } else second = fmin(second, s2);
+      if (s3 < best) { second = best; best = s3; bl = c0 + c + 3; } else second = fmin(second, s3);
     }
     for (; c < nc; ++c) {
       const double* cc = cs + c * DM;
@@ -188,12 +196,85 @@ __global__ void __launch_bounds__(128) km_assign_kernel(const double* x, int64_t
           s = __dadd_rn(s, __dmul_rn(t, t));
         }
       if (s < best) {
+        second = best;
         best = s;
         bl = c0 + c;
+      } else {
+        second = fmin(second, s);
       }
     }
   }
-  if (i < n) labels[i] = static_cast<uint32_t>(bl);
+  if (i < n) {
+    labels[i] = static_cast<uint32_t>(bl);
+    if (ub) {
+      ub[i] = sqrt(best);
+      lb[i] = sqrt(second);
+    }
+  }
+}
+
+// Hamerly's test before an assignment (labels, ub, lb from the previous one;
+// the centres then moved by move[c], at most mmax): the nearest centre stays
+// the same when ub + move[a] < max(lb - mmax, half the distance from c_a to
+// its nearest other centre) — every other centre is then strictly farther,
+// so the full scan (ties to the lowest index) would keep a.  An atom that
+// fails is retried with its exact distance to c_a as the upper bound.  Margins
+// of 1e-9 relative cover the float64 rounding of the distances (~1e-14).
+// Atoms that still fail are listed for km_assign_kernel; the others keep
+// their label, with the moved bounds.
+__global__ void km_bounds_kernel(const double* x, int64_t n, int d, const double* centers,
+                                 const uint32_t* labels, const double* move, const double* mmax,
+                                 const double* half, double* ub, double* lb, int32_t* list,
+                                 int32_t* count) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t a = labels[i];
+  double u = (ub[i] + move[a]) * (1.0 + 1e-9);
+  const double l = (lb[i] - *mmax) * (1.0 - 1e-9);
+  const double bound = fmax(l, half[a] * (1.0 - 1e-9));
+  if (!(u < bound))  // tighten: the distance to the assigned centre itself
+    u = sqrt(km_dist2(x + i * d, centers + static_cast<int64_t>(a) * d, d)) * (1.0 + 1e-9);
+  if (u < bound) {
+    ub[i] = u;
+    lb[i] = l;
+  } else {
+    list[atomicAdd(count, 1)] = static_cast<int32_t>(i);
+  }
+}
+
+// per-centre move |c_new - c_old| and its maximum; half the distance from
+// each (new) centre to its nearest other centre.  One warp per centre.
+__global__ void km_centre_geom_kernel(const double* old_c, const double* new_c, int K, int d,
+                                      double* move, double* half, unsigned long long* mmax_bits) {
+  const int lane = threadIdx.x & 31;
+  const int c = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+  if (c >= K) return;
+  const double* cc = new_c + static_cast<int64_t>(c) * d;
+  double mv = 0.0;
+  for (int q = lane; q < d; q += 32) {
+    const double t = cc[q] - old_c[static_cast<int64_t>(c) * d + q];
+    mv = fma(t, t, mv);
+  }
+  for (int o = 16; o > 0; o >>= 1) mv += __shfl_xor_sync(0xffffffffu, mv, o);
+  double nn = INFINITY;
+  for (int e = 0; e < K; ++e) {
+    if (e == c) continue;
+    const double* ce = new_c + static_cast<int64_t>(e) * d;
+    double s = 0.0;
+    for (int q = lane; q < d; q += 32) {
+      const double t = cc[q] - ce[q];
+      s = fma(t, t, s);
+    }
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    nn = fmin(nn, s);
+  }
+  if (lane == 0) {
+    const double m = sqrt(mv);
+    move[c] = m;
+    half[c] = 0.5 * sqrt(nn);
+    // non-negative doubles order as their bit patterns
+    atomicMax(mmax_bits, static_cast<unsigned long long>(__double_as_longlong(m)));
+  }
 }
 
 // mass-weighted centroids: one thread per (cluster, coordinate), sequential
@@ -291,6 +372,25 @@ cudaError_t kmeans(const double* x, const double* w, int64_t n, int d, int K, ui
   p += 2 * sizeof(double);
   uint32_t* keys = reinterpret_cast<uint32_t*>(p);
   p += n * sizeof(uint32_t);
+  // Hamerly bounds: distance to the nearest / second-nearest centre, the
+  // centres' moves and half nearest-centre distances, the list of atoms to
+  // rescan and its length, the largest move (as ordered bits)
+  p += (16 - reinterpret_cast<uintptr_t>(p) % 16) % 16;
+  double* ub = reinterpret_cast<double*>(p);
+  p += n * sizeof(double);
+  double* lb = reinterpret_cast<double*>(p);
+  p += n * sizeof(double);
+  double* cmove = reinterpret_cast<double*>(p);
+  p += static_cast<size_t>(K) * sizeof(double);
+  double* chalf = reinterpret_cast<double*>(p);
+  p += static_cast<size_t>(K) * sizeof(double);
+  unsigned long long* mmax = reinterpret_cast<unsigned long long*>(p);
+  p += sizeof(unsigned long long);
+  int32_t* cnt = reinterpret_cast<int32_t*>(p);
+  p += 2 * sizeof(int32_t);
+  int32_t* list = reinterpret_cast<int32_t*>(p);
+  p += n * sizeof(int32_t);
+  p += (256 - reinterpret_cast<uintptr_t>(p) % 256) % 256;
   void* rtmp = p;
   // farthest-point seeding (the atoms' nearest-centre index lives in `keys`,
   // the new centre's distances to the earlier ones in `c2`, both free until
@@ -315,14 +415,26 @@ cudaError_t kmeans(const double* x, const double* w, int64_t n, int d, int K, ui
   int it = 0;
   const int key_bits = K <= 1 ? 1 : 32 - __builtin_clz(static_cast<unsigned>(K - 1));
   for (;;) {
-    // assignment to the current centres, then the clusters in index order
+    // assignment to the current centres (after the first: only the atoms
+    // Hamerly's test cannot keep), then the clusters in index order
+    const int32_t* sl = nullptr;
+    if (it > 0) {
+      cudaError_t e0 = cudaMemsetAsync(cnt, 0, sizeof(int32_t), st);
+      if (e0 != cudaSuccess) return e0;
+      ++g_launches;
+      km_bounds_kernel<<<nb, 256, 0, st>>>(x, n, d, centers, labels, cmove,
+                                           reinterpret_cast<const double*>(mmax), chalf, ub, lb,
+                                           list, cnt);
+      sl = list;
+    }
+    const unsigned ab = static_cast<unsigned>((n + 127) / 128);
     ++g_launches;
     if (d <= 16)
-      km_assign_kernel<16><<<static_cast<unsigned>((n + 127) / 128), 128, 0, st>>>(x, n, d, centers, K, labels);
+      km_assign_kernel<16><<<ab, 128, 0, st>>>(x, n, d, centers, K, labels, sl, cnt, ub, lb);
     else if (d <= 32)
-      km_assign_kernel<32><<<static_cast<unsigned>((n + 127) / 128), 128, 0, st>>>(x, n, d, centers, K, labels);
+      km_assign_kernel<32><<<ab, 128, 0, st>>>(x, n, d, centers, K, labels, sl, cnt, ub, lb);
     else
-      km_assign_kernel<64><<<static_cast<unsigned>((n + 127) / 128), 128, 0, st>>>(x, n, d, centers, K, labels);
+      km_assign_kernel<64><<<ab, 128, 0, st>>>(x, n, d, centers, K, labels, sl, cnt, ub, lb);
     cudaError_t e = cudaMemcpyAsync(keys, labels, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return e;
     ++g_launches;
@@ -337,6 +449,12 @@ cudaError_t kmeans(const double* x, const double* w, int64_t n, int d, int K, ui
     km_centroid_kernel<<<kb, 256, 0, st>>>(x, w, perm, off, K, d, centers, c2, cw);
     ++g_launches;
     km_move_kernel<<<1, 256, 0, st>>>(centers, c2, K, d, mv);
+    // the moves and centre spacing the next assignment's bounds need
+    e = cudaMemsetAsync(mmax, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+    ++g_launches;
+    km_centre_geom_kernel<<<static_cast<unsigned>((static_cast<int64_t>(K) * 32 + 255) / 256), 256, 0,
+                            st>>>(centers, c2, K, d, cmove, chalf, mmax);
     e = cudaMemcpyAsync(centers, c2, static_cast<size_t>(K) * d * sizeof(double),
                         cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return e;
@@ -423,7 +541,11 @@ size_t kmeans_ws_bytes(int64_t n, int d, int K) {
   const int64_t nb = (n + 255) / 256;
   return static_cast<size_t>(n) * sizeof(double) + nb * (sizeof(double) + sizeof(int64_t)) +
          static_cast<size_t>(K) * d * sizeof(double) + 2 * sizeof(double) +
-         static_cast<size_t>(n) * sizeof(uint32_t) + radix_temp_bytes(n) + 256;
+         static_cast<size_t>(n) * sizeof(uint32_t) +
+         // Hamerly bounds, moves, half spacings, max move, count, rescan list
+         2 * static_cast<size_t>(n) * sizeof(double) + 2 * static_cast<size_t>(K) * sizeof(double) +
+         sizeof(unsigned long long) + 2 * sizeof(int32_t) + static_cast<size_t>(n) * sizeof(int32_t) +
+         256 + radix_temp_bytes(n) + 256;
 }
 
 }  // namespace msot_dev

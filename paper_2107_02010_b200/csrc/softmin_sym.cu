@@ -246,10 +246,25 @@ __global__ void sym_colsum_kernel(const __grid_constant__ ColSumGroup g) {
     e = lo;
   }
   double s = (a.acc && !a.first) ? a.acc[j] : 0.0;
+  // entries are in ascending tile order, so both stopping rules end the
+  // walk: tile >= t1 (batch end), and for self problems the first tile that
+  // ends after j (so do all later ones).  Four entries' loads in flight per
+  // step, added in entry order (the bits of the one-at-a-time loop).
+  const int32_t tend = a.t1;
+  auto stop = [&](int32_t t) { return t >= tend || (a.self && a.tile_start[t + 1] > j); };
+  for (; e + 4 <= e1; e += 4) {
+    const int32_t t0 = a.etile[e], t1 = a.etile[e + 1], t2 = a.etile[e + 2], t3 = a.etile[e + 3];
+    if (stop(t3)) break;  // the last of the four decides for all (ascending)
+    const float v0 = a.colpart[a.eslot[e] + off], v1 = a.colpart[a.eslot[e + 1] + off];
+    const float v2 = a.colpart[a.eslot[e + 2] + off], v3 = a.colpart[a.eslot[e + 3] + off];
+    (void)t0; (void)t1; (void)t2;
+    s += static_cast<double>(v0);
+    s += static_cast<double>(v1);
+    s += static_cast<double>(v2);
+    s += static_cast<double>(v3);
+  }
   for (; e < e1; ++e) {
-    const int32_t t = a.etile[e];
-    if (t >= a.t1) break;
-    if (a.self && a.tile_start[t + 1] > j) continue;
+    if (stop(a.etile[e])) break;
     s += static_cast<double>(a.colpart[a.eslot[e] + off]);
   }
   // (tot null: a multi-rank group keeps the float64 total for the exchange)

@@ -744,7 +744,7 @@ void build_plan(msot_ctx* c, const std::string& tag, Plan& P, int waves = 32, in
   // tot_cols_all: the group's columns over every rank's tiles — item and
   // batch sizing depend on it, not on this rank's share, so the items (and
   // the row sums' additions) are the same for any number of GPUs
-  int64_t tot_tiles = 0, tot_cols = 0, tot_cols_all = 0;
+  int64_t tot_tiles = 0, tot_cols_all = 0;
   P.pairs_all = P.pairs_local = P.terms_all = 0.0;
   for (int p = 0; p < P.np; ++p) {
     const RangeSet& R = *P.ps[p].rs;
@@ -768,7 +768,6 @@ void build_plan(msot_ctx* c, const std::string& tag, Plan& P, int waves = 32, in
     for (int r = 0; r <= c->world; ++r) P.row_bounds[p][r] = R.tile_start_h[tb[r]];
     tot_tiles += P.t1[p] - P.t0[p];
     for (int64_t t = P.t0[p]; t < P.t1[p]; ++t) {
-      tot_cols += R.tile_cols_h[t];
       const int64_t rows = R.tile_start_h[t + 1] - R.tile_start_h[t];
       P.pairs_local += static_cast<double>(rows) * static_cast<double>(R.tile_cols_h[t]);
     }
@@ -780,7 +779,6 @@ void build_plan(msot_ctx* c, const std::string& tag, Plan& P, int waves = 32, in
   const int64_t target = static_cast<int64_t>(c->n_sm) * 12 * waves;
   int64_t chunk = std::max<int64_t>(2 * kColTile, (tot_cols_all + target - 1) / std::max<int64_t>(target, 1));
   chunk = (chunk + kColTile - 1) / kColTile * kColTile;
-  (void)tot_cols;
   if (P.ps[0].sym) {
     // colpart batches: consecutive (problem, tile) runs of at most `budget`
     // slots; each batch is cut into ~`waves` waves of items of its own

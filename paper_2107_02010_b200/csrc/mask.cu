@@ -975,12 +975,20 @@ __global__ void sym_entries_kernel(const uint32_t* tbits, int32_t words, int32_t
   const int64_t ncl = J < k ? co[J + 1] - co[J] : 0;
   int64_t e = kFill ? ebase[static_cast<int64_t>(J < k ? J : 0) * kEntryChunks + ch] : 0;
   int32_t c = 0;
+  // one tile ahead in flight (the walk is latency-bound)
+  int32_t I1n = (self && t0 < t1) ? rl[ts[t0 + 1] - 1] : -1;
+  uint32_t bn = t0 < t1 ? tbits[t0 * words + w] : 0u;
   for (int64_t t = t0; t < t1; ++t) {
-    const int32_t I1 = self ? rl[ts[t + 1] - 1] : -1;
+    const int32_t I1 = I1n;
     // self: I1 grows with t, and past this word neither list bits nor the
     // head entry remain
     if (self && I1 >= (w + 1) * 32) break;
-    const uint32_t b = list_bits(tbits[t * words + w], w, I1, self);
+    const uint32_t braw = bn;
+    if (t + 1 < t1) {
+      I1n = self ? rl[ts[t + 2] - 1] : -1;
+      bn = tbits[(t + 1) * words + w];
+    }
+    const uint32_t b = list_bits(braw, w, I1, self);
     const bool head = self && J == I1;
     const bool mine = J < k && (((b >> lane) & 1u) || head);
     if (!__any_sync(0xffffffffu, mine)) continue;

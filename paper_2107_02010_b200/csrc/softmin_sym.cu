@@ -169,7 +169,7 @@ softmin_sym_kernel(const __grid_constant__ Group G) {
     __syncthreads();
     if (tp + kSymCols < pos_end) fetch(tp + kSymCols);
     const float4* s4 = reinterpret_cast<const float4*>(smem[buf]);
-#pragma unroll 1
+#pragma unroll 2  // (1: +1% time; 4: 110 registers, +3%)
     for (int c0 = 0; c0 < kSymCols / 2; c0 += 8) {
       float v[16];
 #pragma unroll

@@ -99,6 +99,7 @@ softmin_kernel(const __grid_constant__ Group G) {
     __syncthreads();
     if (tp + kColTile < pos_end) fetch(tp + kColTile);
     const float4* s4 = reinterpret_cast<const float4*>(smem[buf]);
+#pragma unroll 2
     for (int c0 = 0; c0 < kColTile / 2; c0 += 8) {
 #pragma unroll
       for (int k = 0; k < 8; ++k) {

@@ -248,20 +248,18 @@ __global__ void sym_colsum_kernel(const __grid_constant__ ColSumGroup g) {
   double s = (a.acc && !a.first) ? a.acc[j] : 0.0;
   // entries are in ascending tile order, so both stopping rules end the
   // walk: tile >= t1 (batch end), and for self problems the first tile that
-  // ends after j (so do all later ones).  Four entries' loads in flight per
+  // ends after j (so do all later ones).  Eight entries' loads in flight per
   // step, added in entry order (the bits of the one-at-a-time loop).
   const int32_t tend = a.t1;
   auto stop = [&](int32_t t) { return t >= tend || (a.self && a.tile_start[t + 1] > j); };
-  for (; e + 4 <= e1; e += 4) {
-    const int32_t t0 = a.etile[e], t1 = a.etile[e + 1], t2 = a.etile[e + 2], t3 = a.etile[e + 3];
-    if (stop(t3)) break;  // the last of the four decides for all (ascending)
-    const float v0 = a.colpart[a.eslot[e] + off], v1 = a.colpart[a.eslot[e + 1] + off];
-    const float v2 = a.colpart[a.eslot[e + 2] + off], v3 = a.colpart[a.eslot[e + 3] + off];
-    (void)t0; (void)t1; (void)t2;
-    s += static_cast<double>(v0);
-    s += static_cast<double>(v1);
-    s += static_cast<double>(v2);
-    s += static_cast<double>(v3);
+  constexpr int kAhead = 8;
+  for (; e + kAhead <= e1; e += kAhead) {
+    if (stop(a.etile[e + kAhead - 1])) break;  // the last decides for all (ascending)
+    float v[kAhead];
+#pragma unroll
+    for (int u = 0; u < kAhead; ++u) v[u] = a.colpart[a.eslot[e + u] + off];
+#pragma unroll
+    for (int u = 0; u < kAhead; ++u) s += static_cast<double>(v[u]);
   }
   for (; e < e1; ++e) {
     if (stop(a.etile[e])) break;

@@ -527,18 +527,18 @@ __global__ void hd_colsum_kernel(const float* colpart, const int64_t* tslot, con
     }
     te = lo;
   }
-  // 4 independent loads per step, added in tile order (bitwise the plain loop)
+  // 8 independent loads per step, added in tile order (bitwise the plain loop)
   auto term = [&](int32_t t) {
     return __ldg(colpart + tslot[t] + (j - (self ? ts[t] : 0)));
   };
   double s = (acc && !first) ? acc[j] : 0.0;  // running total of earlier batches
   int32_t t = t0;
-  for (; t + 4 <= te; t += 4) {
-    const float v0 = term(t), v1 = term(t + 1), v2 = term(t + 2), v3 = term(t + 3);
-    s += static_cast<double>(v0);
-    s += static_cast<double>(v1);
-    s += static_cast<double>(v2);
-    s += static_cast<double>(v3);
+  for (; t + 8 <= te; t += 8) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = term(t + u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += static_cast<double>(v[u]);
   }
   for (; t < te; ++t) s += static_cast<double>(term(t));
   if ((last || !acc) && tot) tot[j] = static_cast<float>(s);

@@ -77,9 +77,20 @@ cudaError_t launch_softmin_hd(const Group& g, int d, int n_sm, bool sym, cudaStr
 // per-scale column constants of a high-D problem into `out` (hd_padded(n_cols));
 // out2 (nullable): column factor exponents of evaluate-once groups
 cudaError_t hd_colconst(const Problem& P, float* out, float* out2, cudaStream_t st);
-cudaError_t hd_colsum(const float* colpart, const int64_t* tslot, const int32_t* ts, int32_t t0,
-                      int32_t t1, int self, int32_t n_cols, float* tot, double* acc, int first,
-                      int last, cudaStream_t st);
+// the dense column sums of up to three problems in one launch
+struct DenseColSum {
+  const float* colpart;
+  const int64_t* tslot;
+  const int32_t* ts;
+  float* tot;                 // null: keep the float64 total in acc (multi-rank exchange)
+  double* acc;
+  int32_t t0, t1, self, n_cols, first, last;
+};
+struct DenseColSumGroup {
+  DenseColSum c[3];
+  int n;
+};
+cudaError_t hd_colsum_group(const DenseColSum* c, int n, cudaStream_t st);
 cudaError_t launch_fallback_hd(const Group& g, int d, int n_sm, cudaStream_t st);
 
 // label transfer (labels.cu, K9)

@@ -513,9 +513,16 @@ cudaError_t hd_colconst(const Problem& P, float* out, float* out2, cudaStream_t 
 // Column totals of a dense evaluate-once problem: column j sums the partial
 // of every row tile of [t0, t1) that owns it (self: tiles ending at or
 // before j), in tile order, float64.
-__global__ void hd_colsum_kernel(const float* colpart, const int64_t* tslot, const int32_t* ts,
-                                 int32_t t0, int32_t t1, int self, int32_t n_cols, float* tot,
-                                 double* acc, int first, int last) {
+// (blockIdx.y = the problem of a grouped launch)
+__global__ void hd_colsum_kernel(const __grid_constant__ DenseColSumGroup g) {
+  const DenseColSum& a = g.c[blockIdx.y];
+  const float* colpart = a.colpart;
+  const int64_t* tslot = a.tslot;
+  const int32_t* ts = a.ts;
+  const int32_t t0 = a.t0, t1 = a.t1, self = a.self, n_cols = a.n_cols;
+  float* tot = a.tot;
+  double* acc = a.acc;
+  const int first = a.first, last = a.last;
   const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n_cols) return;
   int32_t te = t1;  // self: tiles that end at or before j (ts ascending)
@@ -545,13 +552,17 @@ __global__ void hd_colsum_kernel(const float* colpart, const int64_t* tslot, con
   else acc[j] = s;  // (tot null: multi-rank float64 exchange, sym_colsum_kernel)
 }
 
-cudaError_t hd_colsum(const float* colpart, const int64_t* tslot, const int32_t* ts, int32_t t0,
-                      int32_t t1, int self, int32_t n_cols, float* tot, double* acc, int first,
-                      int last, cudaStream_t st) {
-  if (n_cols <= 0) return cudaSuccess;
+cudaError_t hd_colsum_group(const DenseColSum* c, int n, cudaStream_t st) {
+  DenseColSumGroup g{};
+  int32_t mx = 0;
+  for (int k = 0; k < n; ++k) {
+    g.c[k] = c[k];
+    mx = max(mx, c[k].n_cols);
+  }
+  g.n = n;
+  if (n <= 0 || mx <= 0) return cudaSuccess;
   ++g_launches;
-  hd_colsum_kernel<<<(n_cols + 255) / 256, 256, 0, st>>>(colpart, tslot, ts, t0, t1, self, n_cols,
-                                                         tot, acc, first, last);
+  hd_colsum_kernel<<<dim3((mx + 255) / 256, n), 256, 0, st>>>(g);
   return cudaGetLastError();
 }
 

@@ -1144,7 +1144,8 @@ void run_group_sym(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& s
       CK(launch_rowsum(Gr, B.i0, bs));
     }
     ColSum cs[3];
-    int ncs = 0;
+    DenseColSum ds[3];
+    int ncs = 0, nds = 0;
     // column sums accumulate batch after batch: wait for the previous batch's
     if (overlap && bi > 0) CK(cudaStreamWaitEvent(bs, c->ev_cs[(bi - 1) & 1], 0));
     for (int p = 0; p < 3; ++p) {
@@ -1154,9 +1155,9 @@ void run_group_sym(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& s
       const int first = bi == first_b[p], last = bi == last_b[p];
       const int32_t t0 = has ? B.bt0[p] : 0, t1 = has ? B.bt1[p] : 0;
       if (S.dense) {  // dense pair sets (high-D path, coarse phase, dense solves)
-        CK(hd_colsum(cp[p], S.tslot, S.R.tile_start, t0, t1, S.self,
-                     static_cast<int32_t>(P.ps[p].n_cols), x64 ? nullptr : X.tot[p], acc[p], first,
-                     last, bs));
+        ds[nds++] = DenseColSum{cp[p], S.tslot, S.R.tile_start, x64 ? nullptr : X.tot[p], acc[p],
+                                t0, t1, S.self, static_cast<int32_t>(P.ps[p].n_cols), first,
+                                last};
       } else {
         cs[ncs++] = ColSum{X.labels[p], X.co[p], S.ebase, S.eslot, S.etile, S.R.tile_start, cp[p],
                            x64 ? nullptr : X.tot[p], acc[p],
@@ -1164,6 +1165,7 @@ void run_group_sym(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& s
       }
     }
     if (ncs > 0) CK(launch_colsum(cs, ncs, bs));
+    if (nds > 0) CK(hd_colsum_group(ds, nds, bs));
     if (overlap) CK(cudaEventRecord(c->ev_cs[bi & 1], bs));
   }
   if (overlap) CK(cudaStreamWaitEvent(st, c->ev_cs[(nbt - 1) & 1], 0));

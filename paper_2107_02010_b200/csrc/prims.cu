@@ -95,6 +95,36 @@ __global__ void scan_apply(const TI* in, int64_t n, const TO* sums, TO* out, int
   }
 }
 
+// Small inputs (<= kScanSingleTiles tiles): one block walks the tiles in
+// order with a running carry — one launch instead of three (the pair-set
+// builds scan many short per-tile arrays).  Same integer sums.
+constexpr int64_t kScanSingleTiles = 16;
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(kScanThreads) scan_single(const TI* in, int64_t n, TO* out,
+                                                            int inclusive, TO* total) {
+  __shared__ TO sh[32];
+  TO carry = 0;
+  for (int64_t base = 0; base < n; base += kScanTile) {
+    TO v[kScanItems];
+    TO acc = 0;
+    for (int i = 0; i < kScanItems; ++i) {
+      const int64_t g = base + static_cast<int64_t>(threadIdx.x) * kScanItems + i;
+      v[i] = g < n ? static_cast<TO>(in[g]) : TO(0);
+      acc += v[i];
+    }
+    TO tot;
+    TO pre = block_exclusive_scan<TO>(acc, sh, &tot) + carry;
+    for (int i = 0; i < kScanItems; ++i) {
+      const int64_t g = base + static_cast<int64_t>(threadIdx.x) * kScanItems + i;
+      if (inclusive) pre += v[i];
+      if (g < n) out[g] = pre;
+      if (!inclusive) pre += v[i];
+    }
+    carry += tot;
+  }
+  if (threadIdx.x == 0 && total) *total = carry;
+}
+
 size_t scan_temp_elems(int64_t n) { return static_cast<size_t>((n + kScanTile - 1) / kScanTile) + 1; }
 
 template <typename TI, typename TO>
@@ -105,6 +135,11 @@ cudaError_t scan(const TI* in, TO* out, int64_t n, bool inclusive, TO* tmp, TO* 
     return cudaSuccess;
   }
   const int64_t nb = (n + kScanTile - 1) / kScanTile;
+  if (nb <= kScanSingleTiles) {
+    ++g_launches;
+    scan_single<TI, TO><<<1, kScanThreads, 0, st>>>(in, n, out, inclusive ? 1 : 0, total);
+    return cudaGetLastError();
+  }
   ++g_launches; scan_reduce<TI, TO><<<static_cast<unsigned>(nb), kScanThreads, 0, st>>>(in, n, tmp);
   ++g_launches; scan_sums<TO><<<1, 1024, 0, st>>>(tmp, nb, total);
   ++g_launches; scan_apply<TI, TO><<<static_cast<unsigned>(nb), kScanThreads, 0, st>>>(in, n, tmp, out,

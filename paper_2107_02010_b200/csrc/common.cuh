@@ -90,6 +90,9 @@ struct Group {
   int32_t force_fb;       // tests (MSOT_FORCE_FALLBACK): every row takes the exact path
   int32_t* bad_scale;     // first scale that produced a non-finite potential
   int32_t scale;          // index of this launch group's scale
+  int32_t colfinal_p;     // > 0: softmin_finalize also updates this problem's rows
+                          // from their column totals (evaluate-once, sym_colfinal_row);
+                          // 0 (the zero-initialised default): off
 };
 
 // Kernel launches issued by this thread (reported as stats.gpu_launches).
@@ -100,6 +103,27 @@ extern thread_local int64_t g_launches;
 __device__ __forceinline__ void store_potential(const Group& G, float* out, int32_t r, float v) {
   out[r] = v;
   if (!isfinite(v) && G.bad_scale) atomicMin(G.bad_scale, G.scale);
+}
+
+// The transposed cross problem of an evaluate-once group (problem p, no
+// tiles of its own): its row sum is the column total alone.  Out-of-window
+// rows are queued for the exact path.
+__device__ __forceinline__ void sym_colfinal_row(const Group& G, int p, int32_t r) {
+  const Problem& P = G.P[p];
+  if (r >= P.n_rows) return;
+  const float s = P.row_add[r];
+  const float est = P.row_est ? P.row_est[r] : 0.f;
+  if (P.row_lw2 && P.row_lw2[r] == -INFINITY) {  // zero-weight atom (padding): no update
+    store_potential(G, P.row_out, r, est);
+    return;
+  }
+  if (!(s >= 8.67361738e-19f && s <= 1.2676506e30f) || G.force_fb) {
+    const int slot = atomicAdd(G.fb_count, 1);
+    atomicAdd(G.fb_total, 1);
+    if (slot < G.fb_cap) G.fb_list[slot] = make_int4(p, r, -1, 0);
+    return;
+  }
+  store_potential(G, P.row_out, r, est - P.mixw * P.lam_eps * logf(s));
 }
 
 __device__ __forceinline__ float ex2_approx(float x) {

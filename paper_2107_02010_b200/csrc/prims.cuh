@@ -55,7 +55,6 @@ struct ColSumGroup {
 cudaError_t launch_softmin_sym(const Group& g, int d, bool uniform, cudaStream_t st);
 cudaError_t launch_colsum(const ColSum* c, int n, cudaStream_t st);
 cudaError_t totals_f32(const double* acc, float* tot, int32_t n, cudaStream_t st);
-cudaError_t launch_colfinal(const Group& g, int p, cudaStream_t st);
 cudaError_t launch_fallback_dense(const Group& g, int d, int n_sm, cudaStream_t st);
 cudaError_t sym_ranges(const uint32_t* tbits, int32_t k, int64_t nt, const int32_t* co,
                        const int32_t* ts, const int32_t* rl, int self, int64_t* n_ranges,

@@ -282,6 +282,11 @@ __device__ __forceinline__ float sum_items(const float* part, int32_t k0, int32_
 // One CTA per row tile of this rank's shard.
 __global__ void __launch_bounds__(kTileRows) softmin_finalize(const __grid_constant__ Group G) {
   const int b = blockIdx.x;
+  const int nt = G.tile_prefix[G.n_problems];
+  if (b >= nt) {  // the extra blocks: the transposed problem's rows (evaluate-once)
+    sym_colfinal_row(G, G.colfinal_p, (b - nt) * kTileRows + static_cast<int32_t>(threadIdx.x));
+    return;
+  }
   int p = 0;
   while (p + 1 < G.n_problems && b >= G.tile_prefix[p + 1]) ++p;
   const Problem& P = G.P[p];
@@ -420,8 +425,9 @@ cudaError_t launch_plan(const Group& g, int d, cudaStream_t st) {
 
 cudaError_t launch_finalize(const Group& g, cudaStream_t st) {
   const int tiles = g.tile_prefix[g.n_problems];
-  if (tiles <= 0) return cudaSuccess;
-  ++g_launches; softmin_finalize<<<tiles, kTileRows, 0, st>>>(g);
+  const int extra = g.colfinal_p > 0 ? (g.P[g.colfinal_p].n_rows + kTileRows - 1) / kTileRows : 0;
+  if (tiles + extra <= 0) return cudaSuccess;
+  ++g_launches; softmin_finalize<<<tiles + extra, kTileRows, 0, st>>>(g);
   return cudaGetLastError();
 }
 

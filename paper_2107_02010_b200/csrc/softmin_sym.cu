@@ -298,36 +298,6 @@ cudaError_t launch_colsum(const ColSum* c, int n, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-// The transposed cross problem (problem `p`, no tiles of its own): its sum
-// is the column total alone.  One thread per row; out-of-window rows are
-// queued for the exact path.
-__global__ void sym_colfinal_kernel(const __grid_constant__ Group G, int p) {
-  const Problem& P = G.P[p];
-  const int32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= P.n_rows) return;
-  const float s = P.row_add[r];
-  const float est = P.row_est ? P.row_est[r] : 0.f;
-  if (P.row_lw2 && P.row_lw2[r] == -INFINITY) {  // zero-weight atom (padding): no update
-    store_potential(G, P.row_out, r, est);
-    return;
-  }
-  if (!(s >= 8.67361738e-19f && s <= 1.2676506e30f) || G.force_fb) {
-    const int slot = atomicAdd(G.fb_count, 1);
-    atomicAdd(G.fb_total, 1);
-    if (slot < G.fb_cap) G.fb_list[slot] = make_int4(p, r, -1, 0);
-    return;
-  }
-  store_potential(G, P.row_out, r, est - P.mixw * P.lam_eps * logf(s));
-}
-
-cudaError_t launch_colfinal(const Group& g, int p, cudaStream_t st) {
-  const int32_t n = g.P[p].n_rows;
-  if (n <= 0) return cudaSuccess;
-  ++g_launches;
-  sym_colfinal_kernel<<<(n + 255) / 256, 256, 0, st>>>(g, p);
-  return cudaGetLastError();
-}
-
 // Exact online-max LSE for the rows the fixed-reference path rejected.  In
 // the fine phase (P.fb_mask set) a row sums the columns of the clusters its
 // own cluster keeps in the problem's mask (a subset of its pair set that

@@ -1177,8 +1177,8 @@ void run_group_sym(msot_ctx* c, const Plan& P, const ScaleArgs& a, SolveState& s
     for (int p = 0; p < 3; ++p)
       CK(totals_f32(acc[p], X.tot[p], static_cast<int32_t>(P.ps[p].n_cols), st));
   }
+  G.colfinal_p = 3;  // a_xy from the column totals, in the same launch
   CK(launch_finalize(G, st));
-  CK(launch_colfinal(G, 3, st));
   CK(hd ? launch_fallback_hd(G, ss.d, c->n_sm, st) : launch_fallback_dense(G, ss.d, c->n_sm, st));
   ss.S->softmin_launches += nbt;
   ss.S->colpart_batches = std::max(ss.S->colpart_batches, nbt);
